@@ -1,0 +1,249 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes binding of the plain-C FP64 oracle (oracle/ipr_oracle.c).
+
+Only tests/, ``__graft_entry__.smoke()`` and bench.py's ``cpu_baseline`` / ``--impl reference``
+legs may import this module.  The CUDA product path (``paper_1703_02283_b200``) never imports,
+links or executes anything under ``oracle/``; the two share no code.
+
+Every function cites the PAPER.md passage it follows (see ipr_oracle.h / ipr_oracle.c).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "ipr_oracle.c")
+_LIB = os.path.join(_HERE, "libipr_oracle.so")
+
+FP64, TF32, BF16, FP16 = 0, 1, 2, 3
+RNE, RTZ = 0, 1
+CONTINUE, CONVERGED, ITER_LIMIT, DIVERGED, NONFINITE, SWITCH = 0, 1, 2, 3, 4, 5
+OUTCOME_NAMES = {0: "running", 1: "converged", 2: "iter_limit", 3: "diverged", 4: "nonfinite",
+                 5: "switch"}
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (-ffp-contract=off: no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
+            os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "ipr_oracle.h"))):
+        cmd = ["gcc", "-O3", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+               "-shared", "-std=c11", "-Wall", "-o", _LIB + ".tmp", _SRC, "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(_LIB + ".tmp", _LIB)
+    return _LIB
+
+
+class Phase(C.Structure):
+    _fields_ = [("prec", C.c_int), ("mant_bits", C.c_int), ("round", C.c_int),
+                ("switch_tol", C.c_double), ("plateau_ratio", C.c_double),
+                ("plateau_arm", C.c_double), ("max_iters", C.c_int)]
+
+
+class Record(C.Structure):
+    _fields_ = [("k", C.c_int), ("phase", C.c_int), ("prec", C.c_int), ("mant_bits", C.c_int),
+                ("decision", C.c_int), ("rho", C.c_double), ("rho_hat", C.c_double),
+                ("delta", C.c_double), ("gamma", C.c_double)]
+
+
+class Ctrl(C.Structure):
+    _fields_ = [("phase", C.c_int), ("nphases", C.c_int), ("it_in_phase", C.c_int),
+                ("n", C.c_int64), ("rho_prev", C.c_double), ("rho_best", C.c_double),
+                ("rhohat_min", C.c_double), ("final_tol", C.c_double),
+                ("best_is_new", C.c_int)]
+
+
+_lib = None
+_dp = C.POINTER(C.c_double)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        L = _lib
+        L.orc_qm.restype = C.c_double
+        L.orc_qm.argtypes = [C.c_double, C.c_int, C.c_int, C.c_int]
+        L.orc_qm_array.argtypes = [C.c_int64, _dp, _dp, C.c_int, C.c_int, C.c_int]
+        L.orc_norms.argtypes = [C.c_int64, _dp, _dp]
+        L.orc_is_symmetric.argtypes = [C.c_int64, _dp]
+        L.orc_gemm.argtypes = [C.c_int64, _dp, _dp, _dp]
+        L.orc_matvec.argtypes = [C.c_int64, _dp, _dp, _dp]
+        L.orc_c0.argtypes = [C.c_int64, _dp, C.c_double, C.POINTER(Phase), _dp]
+        L.orc_step.restype = C.c_double
+        L.orc_step.argtypes = [C.c_int64, C.c_int, _dp, _dp, C.POINTER(Phase), _dp, _dp]
+        L.orc_solve.argtypes = [C.c_int64, C.c_int, _dp, C.POINTER(Phase), C.c_int, C.c_double,
+                                C.c_int, C.POINTER(Record), C.c_int, C.POINTER(C.c_int), _dp,
+                                _dp, C.c_int, C.c_double, _dp]
+        L.orc_jacobi.argtypes = [C.c_int64, _dp, _dp, _dp]
+        L.orc_inv_proot_eig.argtypes = [C.c_int64, _dp, _dp, C.c_int, _dp]
+        L.orc_spectral.argtypes = [C.c_int64, _dp, C.c_int, C.c_double, C.c_int, _dp]
+        L.orc_fp16_sigma.argtypes = [C.c_double]
+        L.orc_ctrl_init.argtypes = [C.POINTER(Ctrl), C.c_int64, C.c_int, C.c_double]
+        L.orc_ctrl_decide.argtypes = [C.POINTER(Ctrl), C.POINTER(Phase), C.c_double]
+        L.orc_ctrl_enter_next_phase.argtypes = [C.POINTER(Ctrl)]
+        L.orc_prec_format.argtypes = [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.orc_container_E.argtypes = [C.c_int]
+        L.orc_native_m.argtypes = [C.c_int]
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def phase(prec=FP64, mant_bits=-1, round=RNE, switch_tol=0.0, plateau_ratio=0.0,
+          plateau_arm=0.5, max_iters=0) -> Phase:
+    return Phase(prec, mant_bits, round, switch_tol, plateau_ratio, plateau_arm, max_iters)
+
+
+def qm(x, E: int, m: int, rtz: bool = False) -> np.ndarray:
+    """q_m of PAPER.md:191-194 (custom exponent/mantissa widths), elementwise."""
+    x = _f64(x)
+    y = np.empty_like(x)
+    lib().orc_qm_array(x.size, _p(x), _p(y), E, m, int(rtz))
+    return y
+
+
+def prec_format(prec: int):
+    E, M = C.c_int(), C.c_int()
+    lib().orc_prec_format(prec, C.byref(E), C.byref(M))
+    return E.value, M.value
+
+
+def container_E(prec: int) -> int:
+    return lib().orc_container_E(prec)
+
+
+def native_m(prec: int) -> int:
+    return lib().orc_native_m(prec)
+
+
+def fp16_sigma(maxabs: float) -> int:
+    return lib().orc_fp16_sigma(maxabs)
+
+
+def norms(A):
+    """(||A||_1, ||A||_inf, max diag) of Eq. (3)."""
+    A = _f64(A)
+    out = np.empty(3)
+    lib().orc_norms(A.shape[0], _p(A), _p(out))
+    return float(out[0]), float(out[1]), float(out[2])
+
+
+def is_symmetric(A) -> bool:
+    A = _f64(A)
+    return bool(lib().orc_is_symmetric(A.shape[0], _p(A)))
+
+
+def gemm(X, Y) -> np.ndarray:
+    X, Y = _f64(X), _f64(Y)
+    Z = np.empty_like(X)
+    lib().orc_gemm(X.shape[0], _p(X), _p(Y), _p(Z))
+    return Z
+
+
+def matvec(X, v) -> np.ndarray:
+    X, v = _f64(X), _f64(v)
+    y = np.empty(X.shape[0])
+    lib().orc_matvec(X.shape[0], _p(X), _p(v), _p(y))
+    return y
+
+
+def c0(A, s: float, ph0: Phase) -> np.ndarray:
+    A = _f64(A)
+    out = np.empty_like(A)
+    lib().orc_c0(A.shape[0], _p(A), s, C.byref(ph0), _p(out))
+    return out
+
+
+def step(A, Ck, p: int, ph: Phase, want_next: bool = True):
+    """One Eq. (1) iteration from C_k: returns (rho(C_k), C_{k+1}, delta)."""
+    A, Ck = _f64(A), _f64(Ck)
+    nxt = np.empty_like(Ck) if want_next else None
+    d = C.c_double(np.nan)
+    rho = lib().orc_step(A.shape[0], p, _p(A), _p(Ck), C.byref(ph),
+                         _p(nxt) if want_next else None, C.byref(d))
+    return rho, nxt, d.value
+
+
+class SolveResult:
+    def __init__(self, outcome, records, C_best, C_hist, s):
+        self.outcome = outcome
+        self.records = records
+        self.C_best = C_best
+        self.C_hist = C_hist
+        self.s = s
+
+    @property
+    def rho(self):
+        return np.array([r["rho"] for r in self.records])
+
+
+def solve(A, p: int, phases, final_tol: float = 1e-12, max_total: int = 200,
+          hist: int = 0, gamma_normA2: float = 0.0) -> SolveResult:
+    """Full controller-driven solve (init + iterations), reading R-5 of DESIGN.md."""
+    A = _f64(A)
+    n = A.shape[0]
+    arr = (Phase * len(phases))(*phases)
+    recs = (Record * max_total)()
+    nrec = C.c_int(0)
+    best = np.empty_like(A)
+    H = np.empty((hist, n, n)) if hist > 0 else None
+    s = C.c_double(0)
+    out = lib().orc_solve(n, p, _p(A), arr, len(phases), final_tol, max_total, recs, max_total,
+                          C.byref(nrec), _p(best), _p(H) if H is not None else None, hist,
+                          gamma_normA2, C.byref(s))
+    if out < 0:
+        raise ValueError({-1: "invalid argument", -2: "A is not exactly symmetric"}[out])
+    records = [dict(k=r.k, phase=r.phase, prec=r.prec, mant_bits=r.mant_bits,
+                    decision=r.decision, rho=r.rho, rho_hat=r.rho_hat, delta=r.delta,
+                    gamma=r.gamma) for r in recs[:min(nrec.value, max_total)]]
+    return SolveResult(out, records, best, H, s.value)
+
+
+def jacobi(A):
+    """Cyclic Jacobi eigen-decomposition (SPEC.md oracle module): (lambda asc, V)."""
+    A = _f64(A)
+    n = A.shape[0]
+    lam, V = np.empty(n), np.empty_like(A)
+    lib().orc_jacobi(n, _p(A), _p(lam), _p(V))
+    return lam, V
+
+
+def inv_proot_eig(lam, V, p: int) -> np.ndarray:
+    lam, V = _f64(lam), _f64(V)
+    X = np.empty_like(V)
+    lib().orc_inv_proot_eig(V.shape[0], _p(lam), _p(V), p, _p(X))
+    return X
+
+
+def spectral(lam, p: int, s: float, kmax: int) -> np.ndarray:
+    lam = _f64(lam)
+    out = np.empty(kmax)
+    lib().orc_spectral(lam.size, _p(lam), p, s, kmax, _p(out))
+    return out
+
+
+class Controller:
+    """Pure controller state machine of reading R-5 (for direct tests)."""
+
+    def __init__(self, n: int, nphases: int, final_tol: float):
+        self.c = Ctrl()
+        lib().orc_ctrl_init(C.byref(self.c), n, nphases, final_tol)
+
+    def decide(self, ph: Phase, rho: float) -> int:
+        return lib().orc_ctrl_decide(C.byref(self.c), C.byref(ph), rho)
+
+    def next_phase(self):
+        lib().orc_ctrl_enter_next_phase(C.byref(self.c))
+
+    @property
+    def best_is_new(self) -> bool:
+        return bool(self.c.best_is_new)

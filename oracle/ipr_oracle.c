@@ -1,0 +1,432 @@
+/*
+ * ipr_oracle.c -- TEST INFRASTRUCTURE ONLY (see ipr_oracle.h).
+ *
+ * Plain FP64 CPU oracle for the Bini inverse p-th root iteration of arXiv:1703.02283.
+ * Compiled with -ffp-contract=off (no FMA contraction) so every line below is the
+ * IEEE operation it reads as.  No BLAS, no bit tricks: rounding is written with
+ * frexp/ldexp/nearbyint, products are i-k-j triple loops with an FP64 accumulator.
+ * Nothing here is shared with, or loaded by, the CUDA path.
+ */
+#include "ipr_oracle.h"
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------------------------
+ * q_m -- approximate storage / arithmetic as custom-precision rounding.
+ * PAPER.md:191-194 [Sec. 4.2] "floating-point types with a custom number of bits in the
+ * exponent and mantissa"; PAPER.md:106-111 footnotes give the (exponent, stored mantissa)
+ * splits of half (5,10), single (8,23), double (11,52).
+ * Reading R-7: round-to-nearest-even by default, RTZ ("bit truncation")
+ * selectable.  Reading R-8: subnormals kept.  Overflow: RNE -> Inf, RTZ -> max finite.
+ * Definition: with e = max(floor(log2|x|), emin) the representable neighbours of x are
+ * the integer multiples of ulp = 2^(e-m); x/ulp and q*ulp are exact power-of-two
+ * scalings, nearbyint() rounds half-to-even in the default rounding mode.
+ * ------------------------------------------------------------------------------ */
+double orc_qm(double x, int E, int m, int rtz) {
+  if (isnan(x) || isinf(x) || x == 0.0) return x;
+  const int bias = (1 << (E - 1)) - 1;
+  const int emin = 1 - bias, emax = bias;
+  int ex;
+  frexp(fabs(x), &ex);            /* |x| = f 2^ex, f in [0.5, 1)  =>  floor(log2|x|) = ex-1 */
+  int e = ex - 1;
+  if (e < emin) e = emin;         /* subnormal range: fixed spacing 2^(emin-m) */
+  const double ulp = ldexp(1.0, e - m);
+  const double r = x / ulp;
+  const double q = rtz ? trunc(r) : nearbyint(r);
+  double y = q * ulp;
+  const double maxf = ldexp(2.0 - ldexp(1.0, -m), emax);
+  if (fabs(y) > maxf) y = rtz ? copysign(maxf, x) : copysign(INFINITY, x);
+  return y;
+}
+
+void orc_qm_array(int64_t len, const double *x, double *y, int E, int m, int rtz) {
+  for (int64_t i = 0; i < len; ++i) y[i] = orc_qm(x[i], E, m, rtz);
+}
+
+/* Operand formats (R-9, R-10): BF16 = e8m7, FP16 = e5m10 (PAPER.md:106-107 footnote),
+ * TF32 = e8m10, FP64 = e11m52 (PAPER.md:110-111 footnote). */
+void orc_prec_format(int prec, int *E, int *M) {
+  switch (prec) {
+    case ORC_TF32: *E = 8;  *M = 10; break;
+    case ORC_BF16: *E = 8;  *M = 7;  break;
+    case ORC_FP16: *E = 5;  *M = 10; break;
+    default:       *E = 11; *M = 52; break;
+  }
+}
+/* Reading R-8: container of a phase = its accumulate format: e8 (FP32) for the
+ * BF16/FP16/TF32 phases, e11 (FP64) for FP64 phases. */
+int orc_container_E(int prec) { return prec == ORC_FP64 ? 11 : 8; }
+int orc_native_m(int prec) { int E, M; orc_prec_format(prec, &E, &M); return M; }
+
+static int phase_m(const orc_phase *ph) {
+  return ph->mant_bits < 0 ? orc_native_m(ph->prec) : ph->mant_bits;
+}
+/* stored value of a phase: q_m in the container (approximate storage) */
+static double store_q(const orc_phase *ph, double x) {
+  return orc_qm(x, orc_container_E(ph->prec), phase_m(ph), ph->round == ORC_RTZ);
+}
+
+int orc_fp16_sigma(double maxabs) {
+  if (!(maxabs > 0.0) || !isfinite(maxabs)) return 0;
+  int ex;
+  frexp(maxabs, &ex);
+  return 14 - (ex - 1);        /* scaled max in [2^14, 2^15), below FP16 max 65504 */
+}
+
+static double maxabs_of(int64_t len, const double *x) {
+  double m = 0.0;
+  for (int64_t i = 0; i < len; ++i) { double a = fabs(x[i]); if (a > m || isnan(a)) m = a; }
+  return m;
+}
+
+/* Operand quantisation qin (hardware round-to-nearest-even conversion, R-9).
+ * FP16 phase (reading R-20): operand = q16(2^sigma X), sigma from max|X|; returns sigma. */
+static int qin_matrix(int prec, int64_t len, const double *x, double *y) {
+  int E, M;
+  orc_prec_format(prec, &E, &M);
+  if (prec == ORC_FP64) { if (y != x) memcpy(y, x, (size_t)len * sizeof(double)); return 0; }
+  int sigma = 0;
+  if (prec == ORC_FP16) sigma = orc_fp16_sigma(maxabs_of(len, x));
+  for (int64_t i = 0; i < len; ++i) y[i] = orc_qm(ldexp(x[i], sigma), E, M, 0);
+  return sigma;
+}
+
+/* ---------------------------------------------------------------------------------
+ * Norms of Eq. (3): ||A||_1 = max_j sum_i |a_ij|, ||A||_inf =
+ * max_i sum_j |a_ij|; sums sequential in ascending index.  Plus max diagonal (the
+ * sufficient condition of reading R-12).
+ * ------------------------------------------------------------------------------ */
+void orc_norms(int64_t n, const double *A, double *out3) {
+  double n1 = 0.0, ninf = 0.0, md = -INFINITY;
+  for (int64_t j = 0; j < n; ++j) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n; ++i) s += fabs(A[i * n + j]);
+    if (s > n1 || isnan(s)) n1 = s;
+  }
+  for (int64_t i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int64_t j = 0; j < n; ++j) s += fabs(A[i * n + j]);
+    if (s > ninf || isnan(s)) ninf = s;
+    if (A[i * n + i] > md) md = A[i * n + i];
+  }
+  out3[0] = n1; out3[1] = ninf; out3[2] = md;
+}
+
+int orc_is_symmetric(int64_t n, const double *A) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = i + 1; j < n; ++j)
+      if (memcmp(&A[i * n + j], &A[j * n + i], sizeof(double)) != 0) return 0;
+  return 1;
+}
+
+/* Z = X Y: the matrix product of Eq. (1), written as the textbook triple loop. */
+void orc_gemm(int64_t n, const double *X, const double *Y, double *Z) {
+  #pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    double *z = Z + i * n;
+    for (int64_t j = 0; j < n; ++j) z[j] = 0.0;
+    for (int64_t k = 0; k < n; ++k) {
+      const double x = X[i * n + k];
+      const double *y = Y + k * n;
+      for (int64_t j = 0; j < n; ++j) z[j] += x * y[j];
+    }
+  }
+}
+
+void orc_matvec(int64_t n, const double *X, const double *v, double *y) {
+  #pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int64_t k = 0; k < n; ++k) s += X[i * n + k] * v[k];
+    y[i] = s;
+  }
+}
+
+/* ---------------------------------------------------------------------------------
+ * Initial guess, Eq. (3): C_0 = (||A||_1 ||A||_inf)^{-1} A^T, then the
+ * phase-0 storage rounding ("as well as the input data itself").
+ * ------------------------------------------------------------------------------ */
+void orc_c0(int64_t n, const double *A, double s, const orc_phase *ph0, double *C0) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) C0[i * n + j] = store_q(ph0, A[j * n + i] / s);
+}
+
+/* ---------------------------------------------------------------------------------
+ * Controller, reading R-5 ("Increasing the precision in later
+ * iterations ... the necessity of increased precision can be detected at runtime";
+ * divergence rule from SPEC.md solver: residual > 10x running minimum and > 1).
+ * ------------------------------------------------------------------------------ */
+void orc_ctrl_init(orc_ctrl *c, int64_t n, int nphases, double final_tol) {
+  c->phase = 0; c->nphases = nphases; c->it_in_phase = 0; c->n = n;
+  c->rho_prev = NAN; c->rho_best = INFINITY; c->rhohat_min = INFINITY;
+  c->final_tol = final_tol; c->best_is_new = 0;
+}
+
+int orc_ctrl_decide(orc_ctrl *c, const orc_phase *ph, double rho) {
+  const int last = (c->phase == c->nphases - 1);
+  const double rhohat = rho / sqrt((double)c->n);
+  const int fin = isfinite(rho);
+  int d;
+  c->best_is_new = 0;
+  if (fin && rho < c->rho_best) { c->rho_best = rho; c->best_is_new = 1; }
+  if (!fin)
+    d = last ? ORC_NONFINITE : ORC_SWITCH;
+  else if (last && rho <= c->final_tol)
+    d = ORC_CONVERGED;
+  else if (rhohat > 10.0 * c->rhohat_min && rhohat > 1.0)
+    d = last ? ORC_DIVERGED : ORC_SWITCH;
+  else if (!last && ph->switch_tol > 0.0 && rho <= ph->switch_tol)
+    d = ORC_SWITCH;
+  else if (!last && ph->plateau_ratio > 0.0 && rhohat < ph->plateau_arm &&
+           isfinite(c->rho_prev) && rho > ph->plateau_ratio * c->rho_prev)
+    d = ORC_SWITCH;
+  else if (ph->max_iters > 0 && c->it_in_phase + 1 >= ph->max_iters)
+    d = last ? ORC_ITER_LIMIT : ORC_SWITCH;
+  else
+    d = ORC_CONTINUE;
+  if (fin && rhohat < c->rhohat_min) c->rhohat_min = rhohat;
+  c->rho_prev = rho;
+  c->it_in_phase += 1;
+  return d;
+}
+
+void orc_ctrl_enter_next_phase(orc_ctrl *c) {
+  c->phase += 1; c->it_in_phase = 0; c->rho_prev = NAN;
+}
+
+/* ---------------------------------------------------------------------------------
+ * One iteration of Eq. (1), in the reading of DESIGN.md:
+ *  R-1 right-to-left chain  T_1 = Chat Ahat,  T_j = Chat qin(T_{j-1}),  P = Chat qin(T_p)
+ *  R-9 Ahat = qin(q_m(A)) and Chat = qin(C); intermediates take the operand format
+ *  R-2 C_next = q_m( ((p+1) C - P) / p )  -- three FP64 operations, one rounding
+ *  residual rho = ||I - T_p||_F from the unrounded T_p (T_p = C^p A).
+ * ------------------------------------------------------------------------------ */
+typedef struct {
+  int64_t n;
+  double *Chat, *X, *T;
+  int sigC, sigX;
+} chain_ws;
+
+static double chain(int64_t n, int p, const double *A, const double *C, const orc_phase *ph,
+                    chain_ws *w) {
+  const int64_t nn = n * n;
+  /* Ahat = qin(q_m(A)) */
+  for (int64_t i = 0; i < nn; ++i) w->T[i] = store_q(ph, A[i]);
+  w->sigX = qin_matrix(ph->prec, nn, w->T, w->X);
+  w->sigC = qin_matrix(ph->prec, nn, C, w->Chat);
+  double rho = 0.0;
+  for (int j = 1; j <= p; ++j) {
+    orc_gemm(n, w->Chat, w->X, w->T);                      /* T_j = Chat X */
+    if (w->sigC + w->sigX != 0)
+      for (int64_t i = 0; i < nn; ++i) w->T[i] = ldexp(w->T[i], -(w->sigC + w->sigX));
+    if (j == p) {                                           /* rho = ||I - T_p||_F */
+      double s2 = 0.0;
+      for (int64_t r = 0; r < n; ++r)
+        for (int64_t c = 0; c < n; ++c) {
+          const double d = (r == c ? 1.0 : 0.0) - w->T[r * n + c];
+          s2 += d * d;
+        }
+      rho = sqrt(s2);
+    }
+    w->sigX = qin_matrix(ph->prec, nn, w->T, w->X);        /* X = qin(T_j) */
+  }
+  return rho;
+}
+
+static double update(int64_t n, int p, const double *C, const orc_phase *ph, chain_ws *w,
+                     double *C_next) {
+  const int64_t nn = n * n;
+  orc_gemm(n, w->Chat, w->X, w->T);                        /* P = Chat qin(T_p) */
+  if (w->sigC + w->sigX != 0)
+    for (int64_t i = 0; i < nn; ++i) w->T[i] = ldexp(w->T[i], -(w->sigC + w->sigX));
+  const double pp1 = (double)(p + 1), pd = (double)p;
+  double s2 = 0.0;
+  for (int64_t i = 0; i < nn; ++i) {
+    const double a = pp1 * C[i];
+    const double d = a - w->T[i];
+    const double e = d / pd;
+    const double c1 = store_q(ph, e);
+    const double dd = c1 - C[i];
+    s2 += dd * dd;
+    C_next[i] = c1;
+  }
+  return sqrt(s2);
+}
+
+static int ws_alloc(chain_ws *w, int64_t n) {
+  const size_t b = (size_t)(n * n) * sizeof(double);
+  w->n = n;
+  w->Chat = (double *)malloc(b); w->X = (double *)malloc(b); w->T = (double *)malloc(b);
+  return w->Chat && w->X && w->T;
+}
+static void ws_free(chain_ws *w) { free(w->Chat); free(w->X); free(w->T); }
+
+double orc_step(int64_t n, int p, const double *A, const double *C, const orc_phase *ph,
+                double *C_next, double *delta) {
+  chain_ws w;
+  if (!ws_alloc(&w, n)) { ws_free(&w); return NAN; }
+  const double rho = chain(n, p, A, C, ph, &w);
+  if (C_next) { const double d = update(n, p, C, ph, &w, C_next); if (delta) *delta = d; }
+  ws_free(&w);
+  return rho;
+}
+
+static double gamma_of(int64_t n, const double *C, const double *A, double normA2,
+                       double *t1, double *t2) {
+  orc_gemm(n, C, A, t1);
+  orc_gemm(n, A, C, t2);
+  double s = 0.0, c = 0.0;
+  for (int64_t i = 0; i < n * n; ++i) {
+    const double d = t1[i] - t2[i];
+    s += d * d; c += C[i] * C[i];
+  }
+  return sqrt(s) / (sqrt(c) * normA2);
+}
+
+/* Re-container an FP64 copy of an iterate into phase ph's storage format (reading R-5:
+ * the next phase restarts from the best iterate). */
+static void recontainer(int64_t nn, const double *src, const orc_phase *ph, double *dst) {
+  for (int64_t i = 0; i < nn; ++i) dst[i] = store_q(ph, src[i]);
+}
+
+int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int nphases,
+              double final_tol, int max_total, orc_record *rec, int cap_rec, int *nrec,
+              double *C_best, double *C_hist, int hist_cap, double gamma_normA2,
+              double *s_out) {
+  *nrec = 0;
+  if (n <= 0 || p < 1 || nphases < 1) return -1;
+  if (!orc_is_symmetric(n, A)) return -2;
+  const int64_t nn = n * n;
+  double nrm[3];
+  orc_norms(n, A, nrm);
+  const double s = nrm[0] * nrm[1];
+  if (s_out) *s_out = s;
+  double *C = (double *)malloc((size_t)nn * sizeof(double));
+  double *Cn = (double *)malloc((size_t)nn * sizeof(double));
+  double *g1 = NULL, *g2 = NULL;
+  if (gamma_normA2 > 0) {
+    g1 = (double *)malloc((size_t)nn * sizeof(double));
+    g2 = (double *)malloc((size_t)nn * sizeof(double));
+  }
+  chain_ws w;
+  ws_alloc(&w, n);
+  orc_c0(n, A, s, &phases[0], C);
+  memcpy(C_best, C, (size_t)nn * sizeof(double));
+  orc_ctrl ctl;
+  orc_ctrl_init(&ctl, n, nphases, final_tol);
+  int outcome = ORC_CONTINUE;
+  for (int k = 0; k < max_total; ++k) {
+    const orc_phase *ph = &phases[ctl.phase];
+    if (C_hist && k < hist_cap) memcpy(C_hist + (int64_t)k * nn, C, (size_t)nn * sizeof(double));
+    const double rho = chain(n, p, A, C, ph, &w);
+    const int phase_now = ctl.phase;
+    const int d = orc_ctrl_decide(&ctl, ph, rho);
+    if (ctl.best_is_new) memcpy(C_best, C, (size_t)nn * sizeof(double));
+    orc_record r;
+    r.k = k; r.phase = phase_now; r.prec = ph->prec; r.mant_bits = phase_m(ph);
+    r.decision = d; r.rho = rho; r.rho_hat = rho / sqrt((double)n); r.delta = NAN;
+    r.gamma = (gamma_normA2 > 0) ? gamma_of(n, C, A, gamma_normA2, g1, g2) : NAN;
+    if (d == ORC_CONTINUE) {
+      r.delta = update(n, p, C, ph, &w, Cn);
+      double *t = C; C = Cn; Cn = t;
+    } else if (d == ORC_SWITCH) {
+      orc_ctrl_enter_next_phase(&ctl);
+      recontainer(nn, C_best, &phases[ctl.phase], C);
+    }
+    if (*nrec < cap_rec) rec[*nrec] = r;
+    *nrec += 1;
+    if (d != ORC_CONTINUE && d != ORC_SWITCH) { outcome = d; break; }
+  }
+  ws_free(&w);
+  free(C); free(Cn); free(g1); free(g2);
+  return outcome;
+}
+
+/* ---------------------------------------------------------------------------------
+ * Brute-force limit for small n (SPEC.md oracle module; the paper's "solution that was
+ * precomputed using double-precision"): cyclic Jacobi rotations
+ * (Golub & Van Loan, Alg. 8.5.3) and X = V diag(lambda^{-1/p}) V^T.
+ * ------------------------------------------------------------------------------ */
+int orc_jacobi(int64_t n, const double *A0, double *lambda, double *V) {
+  double *A = (double *)malloc((size_t)(n * n) * sizeof(double));
+  memcpy(A, A0, (size_t)(n * n) * sizeof(double));
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) V[i * n + j] = (i == j) ? 1.0 : 0.0;
+  double fro = 0.0;
+  for (int64_t i = 0; i < n * n; ++i) fro += A[i] * A[i];
+  fro = sqrt(fro);
+  int sweep;
+  for (sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = 0; j < n; ++j)
+        if (i != j) off += A[i * n + j] * A[i * n + j];
+    if (sqrt(off) <= 1e-15 * fro) break;
+    for (int64_t pi = 0; pi < n - 1; ++pi)
+      for (int64_t qi = pi + 1; qi < n; ++qi) {
+        const double apq = A[pi * n + qi];
+        if (apq == 0.0) continue;
+        const double theta = (A[qi * n + qi] - A[pi * n + pi]) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(1.0 + theta * theta));
+        const double c = 1.0 / sqrt(1.0 + t * t), sn = t * c;
+        for (int64_t k = 0; k < n; ++k) {           /* A <- A J (columns p, q) */
+          const double akp = A[k * n + pi], akq = A[k * n + qi];
+          A[k * n + pi] = c * akp - sn * akq;
+          A[k * n + qi] = sn * akp + c * akq;
+        }
+        for (int64_t k = 0; k < n; ++k) {           /* A <- J^T A (rows p, q) */
+          const double apk = A[pi * n + k], aqk = A[qi * n + k];
+          A[pi * n + k] = c * apk - sn * aqk;
+          A[qi * n + k] = sn * apk + c * aqk;
+        }
+        for (int64_t k = 0; k < n; ++k) {           /* V <- V J */
+          const double vkp = V[k * n + pi], vkq = V[k * n + qi];
+          V[k * n + pi] = c * vkp - sn * vkq;
+          V[k * n + qi] = sn * vkp + c * vkq;
+        }
+      }
+  }
+  for (int64_t i = 0; i < n; ++i) lambda[i] = A[i * n + i];
+  /* selection sort ascending, permuting V's columns with lambda */
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t m = i;
+    for (int64_t j = i + 1; j < n; ++j) if (lambda[j] < lambda[m]) m = j;
+    if (m != i) {
+      double t = lambda[i]; lambda[i] = lambda[m]; lambda[m] = t;
+      for (int64_t k = 0; k < n; ++k) {
+        double u = V[k * n + i]; V[k * n + i] = V[k * n + m]; V[k * n + m] = u;
+      }
+    }
+  }
+  free(A);
+  return sweep;
+}
+
+void orc_inv_proot_eig(int64_t n, const double *lambda, const double *V, int p, double *X) {
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      double s = 0.0;
+      for (int64_t k = 0; k < n; ++k)
+        s += V[i * n + k] * pow(lambda[k], -1.0 / (double)p) * V[j * n + k];
+      X[i * n + j] = s;
+    }
+}
+
+/* ---------------------------------------------------------------------------------
+ * Spectral predictor (exact arithmetic).  C_0 = A/s is a polynomial in A, hence so is
+ * every C_k (Eq. 1); in A's eigenbasis c_{k+1} = c_k ((p+1) - c_k^p lambda)/p.  With
+ * t = c^p lambda:  t_0 = lambda^{p+1}/s^p,  t_{k+1} = t_k ((p+1 - t_k)/p)^p,  and
+ * ||I - C_k^p A||_F^2 = sum_i (1 - t_i)^2.
+ * ------------------------------------------------------------------------------ */
+void orc_spectral(int64_t n, const double *lambda, int p, double s, int kmax, double *rho_hat) {
+  double *t = (double *)malloc((size_t)n * sizeof(double));
+  for (int64_t i = 0; i < n; ++i) t[i] = pow(lambda[i], (double)(p + 1)) / pow(s, (double)p);
+  for (int k = 0; k < kmax; ++k) {
+    double s2 = 0.0;
+    for (int64_t i = 0; i < n; ++i) s2 += (1.0 - t[i]) * (1.0 - t[i]);
+    rho_hat[k] = sqrt(s2 / (double)n);
+    for (int64_t i = 0; i < n; ++i) t[i] = t[i] * pow(((double)(p + 1) - t[i]) / (double)p, (double)p);
+  }
+  free(t);
+}

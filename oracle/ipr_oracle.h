@@ -1,0 +1,122 @@
+/*
+ * ipr_oracle.h -- TEST INFRASTRUCTURE ONLY.
+ *
+ * Plain, slow, obviously-correct CPU oracle for the Bini et al. inverse p-th root
+ * iteration studied in arXiv:1703.02283 ("approximate computing for inverse matrix
+ * p-th roots").  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this.  It shares NO code, header, table or constant
+ * generator with the CUDA path under paper_1703_02283_b200/ (which must never load it).
+ *
+ * Citations are PAPER.md line numbers (section / equation in brackets):
+ *   Eq. (1)  PAPER.md:71-73  [Sec. 2]   C_{k+1} = ((p+1) C_k - C_k^{p+1} A) / p
+ *   Eq. (2)  PAPER.md:76-78  [Sec. 2]   ||I - C_0^p A||_2 < 1  => convergence
+ *   Eq. (3)  PAPER.md:84-86  [Sec. 2]   C_0 = (||A||_1 ||A||_inf)^{-1} A^T
+ *   approximate arithmetic / storage: PAPER.md:101-145 [Sec. 3], :149-155 [Sec. 4]
+ *   dynamic precision scaling: PAPER.md:256-261 [Sec. 4.3.1]
+ * Readings of silent/ambiguous passages (R-1 ... R-21) are listed in DESIGN.md.
+ *
+ * Parity status: every function below is pinned by tests in tests/test_oracle_*.py
+ * against closed forms, library routines or hand values, EXCEPT the paper's own
+ * curves (Figs. 2-5 are missing from PAPER.md): "parity unpinned" for those (R-21).
+ */
+#ifndef IPR_ORACLE_H
+#define IPR_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Operand (GEMM input) formats.  Values are independent of include/ipr.h on purpose. */
+enum { ORC_FP64 = 0, ORC_TF32 = 1, ORC_BF16 = 2, ORC_FP16 = 3 };
+enum { ORC_RNE = 0, ORC_RTZ = 1 };
+enum { ORC_CONTINUE = 0, ORC_CONVERGED = 1, ORC_ITER_LIMIT = 2, ORC_DIVERGED = 3,
+       ORC_NONFINITE = 4, ORC_SWITCH = 5 };
+
+/* q_m: round x to a binary format with E exponent bits and m stored mantissa bits,
+ * subnormals kept, overflow -> +-Inf (RNE) or +-max finite (RTZ), NaN -> NaN,
+ * -0 kept.  Definition written out with frexp/ldexp (no bit tricks). */
+double orc_qm(double x, int E, int m, int rtz);
+void   orc_qm_array(int64_t len, const double *x, double *y, int E, int m, int rtz);
+
+/* Operand format of a precision: (E, M).  Container exponent bits of a phase. */
+void orc_prec_format(int prec, int *E, int *M);
+int  orc_container_E(int prec);
+int  orc_native_m(int prec);
+
+/* Norms of Eq. (3): out[0] = ||A||_1 (max column abs-sum), out[1] = ||A||_inf (max row
+ * abs-sum), out[2] = max diagonal.  Sums sequential in ascending index. */
+void orc_norms(int64_t n, const double *A, double *out3);
+
+/* 1 if A == A^T bit for bit, else 0. */
+int orc_is_symmetric(int64_t n, const double *A);
+
+/* Z = X * Y (all n x n row-major), i-k-j loops, FP64 accumulator, no FMA. */
+void orc_gemm(int64_t n, const double *X, const double *Y, double *Z);
+/* y = X v (row-major), sequential sums. */
+void orc_matvec(int64_t n, const double *X, const double *v, double *y);
+
+typedef struct {
+  int    prec;          /* ORC_FP64 / TF32 / BF16 / FP16                              */
+  int    mant_bits;     /* m stored bits of C (and A) in this phase; -1 = native      */
+  int    round;         /* ORC_RNE / ORC_RTZ for stored C (and A)                     */
+  double switch_tol;    /* leave phase when rho <= switch_tol; 0 = off                */
+  double plateau_ratio; /* armed plateau: rho_k > ratio * rho_{k-1}; 0 = off          */
+  double plateau_arm;   /* armed when rho_hat_k < plateau_arm                          */
+  int    max_iters;     /* per-phase cap on chains; 0 = unlimited                     */
+} orc_phase;
+
+typedef struct {
+  int k, phase, prec, mant_bits, decision;
+  double rho, rho_hat, delta, gamma;
+} orc_record;
+
+/* Controller (reading R-5 of DESIGN.md).  Pure state machine, no matrices. */
+typedef struct {
+  int phase, nphases, it_in_phase;
+  int64_t n;
+  double rho_prev, rho_best, rhohat_min, final_tol;
+  int best_is_new;                     /* out: 1 if this rho became the new best */
+} orc_ctrl;
+void orc_ctrl_init(orc_ctrl *c, int64_t n, int nphases, double final_tol);
+int  orc_ctrl_decide(orc_ctrl *c, const orc_phase *ph, double rho);
+void orc_ctrl_enter_next_phase(orc_ctrl *c);
+
+/* Scalars of the phase-0 initial guess: C0 = q_m0(A^T / s), s = ||A||_1 ||A||_inf. */
+void orc_c0(int64_t n, const double *A, double s, const orc_phase *ph0, double *C0);
+
+/* One full Bini iteration from C_k at phase ph (R-1 right-to-left chain):
+ *   Chat = qin(C), Ahat = qin(q_m(A)), T_1 = Chat Ahat, T_j = Chat qin(T_{j-1}),
+ *   rho = ||I - T_p||_F (unrounded T_p), P = Chat qin(T_p),
+ *   C_next = q_m(((p+1) C - P) / p)  (three FP64 ops, one rounding; R-2).
+ * C_next may be NULL (chain + residual only).  Returns rho; *delta = ||C_next - C||_F. */
+double orc_step(int64_t n, int p, const double *A, const double *C, const orc_phase *ph,
+                double *C_next, double *delta);
+
+/* Full solve: init (norms, C0) + controller-driven iterations.
+ *   rec[cap_rec] trace; C_best (n*n) answer; C_hist (hist_cap * n*n, may be NULL) keeps
+ *   the iterate evaluated by each record (C_k of record k);
+ *   gamma_normA2 > 0 => record gamma_k = ||C A - A C||_F / (||C||_F gamma_normA2).
+ * Returns outcome (ORC_CONVERGED, ...); *nrec = records written. */
+int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int nphases,
+              double final_tol, int max_total, orc_record *rec, int cap_rec, int *nrec,
+              double *C_best, double *C_hist, int hist_cap, double gamma_normA2,
+              double *s_out);
+
+/* Cyclic Jacobi eigen-decomposition of a symmetric matrix (n small).
+ * lambda ascending, V columns = eigenvectors (row-major n x n).  Returns sweeps used. */
+int orc_jacobi(int64_t n, const double *A, double *lambda, double *V);
+/* X = V diag(lambda^{-1/p}) V^T. */
+void orc_inv_proot_eig(int64_t n, const double *lambda, const double *V, int p, double *X);
+
+/* Spectral predictor: rho_hat_k (k = 0..kmax-1) of the exact-arithmetic iteration from
+ * the eigenvalues lambda of A and s: t_0 = lambda^{p+1}/s^p, t <- t ((p+1-t)/p)^p. */
+void orc_spectral(int64_t n, const double *lambda, int p, double s, int kmax, double *rho_hat);
+
+/* FP16 phase operand scale exponent: sigma = 14 - floor(log2(max|X|)) (0 if max is 0
+ * or non-finite).  Stored FP16 operand = q16(2^sigma X). */
+int orc_fp16_sigma(double maxabs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
