@@ -1,0 +1,155 @@
+/*
+ * ipr.h -- C-ABI of the B200-native (sm_100a) inverse matrix p-th root library.
+ *
+ * The library computes A^{-1/p} for a symmetric positive definite A with the iteration of
+ * Bini et al. studied in arXiv:1703.02283:
+ *
+ *   Eq. (1)  PAPER.md:71-73  [Sec. 2]   C_{k+1} = ((p+1) C_k - C_k^{p+1} A) / p
+ *   Eq. (3)  PAPER.md:84-86  [Sec. 2]   C_0 = (||A||_1 ||A||_inf)^{-1} A^T
+ *   Eq. (2)  PAPER.md:76-79  [Sec. 2]   ||I - C_0^p A||_2 < 1  =>  C_k -> A^{-1/p}
+ *
+ * running "approximate" (reduced precision) phases first -- approximate arithmetic
+ * (Sec. 3.1) and approximate storage / data exchange (PAPER.md:129-141,
+ * Sec. 3.2) -- and switching to higher precision at runtime (dynamic precision scaling,
+ * PAPER.md:256-261, Sec. 4.3.1), ending with FP64 refinement.
+ *
+ * Readings of passages the paper leaves open (product order, update form, rounding,
+ * controller rules, ...) are numbered R-1 ... R-21 in DESIGN.md and cited below.
+ *
+ * General conventions
+ *  - Every function returns ipr_status (IPR_OK == 0).  No function aborts the process and
+ *    there is NO CPU fallback: anything the GPU path cannot do returns IPR_E_UNSUPPORTED.
+ *  - Numerical failure is NOT an error: it is reported as an ipr_outcome (IPR_DIVERGED,
+ *    IPR_NONFINITE) with status IPR_OK.  Misuse (bad arguments, wrong call order,
+ *    non-symmetric A) is an error status.
+ *  - Matrices at the boundary are FP64, row-major, on the device, with a leading dimension
+ *    (elements) >= n.  The caller owns them.  The library owns every internal buffer.
+ *  - One context per host thread; contexts are independent.  All device work is enqueued
+ *    on the caller's stream; ipr_iterate/ipr_residual/ipr_finalize synchronise it.
+ *  - ipr_last_error(NULL) returns the message of the last failed call on this thread.
+ */
+#ifndef IPR_H
+#define IPR_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ipr_ctx ipr_ctx;
+
+typedef enum {
+  IPR_OK = 0,
+  IPR_E_INVALID_ARG = 1,   /* null pointer, n <= 0, lda < n, bad p / schedule ...            */
+  IPR_E_NOT_SYMMETRIC = 2, /* A != A^T bit for bit (reading R-13)                            */
+  IPR_E_STATE = 3,         /* wrong call order (e.g. iterate before set_schedule)            */
+  IPR_E_UNSUPPORTED = 4,   /* combination the GPU path does not implement (never CPU)       */
+  IPR_E_OOM = 5,           /* device allocation failed                                       */
+  IPR_E_CUDA = 6,          /* CUDA runtime / driver error (message in ipr_last_error)        */
+  IPR_E_NCCL = 7           /* NCCL error or NCCL library not loadable                        */
+} ipr_status;
+
+/* GEMM input (operand) format of a phase.  Accumulation is FP32 for BF16/FP16/TF32
+ * (tcgen05 tensor cores, kind::f16 / kind::tf32) and FP64 for FP64 (DMMA). */
+typedef enum { IPR_FP64 = 0, IPR_TF32 = 1, IPR_BF16 = 2, IPR_FP16 = 3 } ipr_prec;
+
+/* Rounding of the stored iterate (reading R-7: RNE default; RTZ = "bit truncation",
+ * PAPER.md:26).  Operand conversions are always round-to-nearest-even (hardware cvt.rn). */
+typedef enum { IPR_RNE = 0, IPR_RTZ = 1 } ipr_round;
+
+typedef enum {
+  IPR_RUNNING = 0,    /* ipr_iterate's max_iters budget ran out; call again to continue     */
+  IPR_CONVERGED = 1,  /* rho <= final_tol in the last phase                                  */
+  IPR_ITER_LIMIT = 2, /* last phase hit its max_iters                                        */
+  IPR_DIVERGED = 3,   /* rho_hat > 10 * min rho_hat and rho_hat > 1 in the last phase (R-5)  */
+  IPR_NONFINITE = 4   /* rho not finite in the last phase                                    */
+} ipr_outcome;
+
+/* Controller decisions recorded in the trace (reading R-5). */
+typedef enum { IPR_DEC_CONTINUE = 0, IPR_DEC_CONVERGED = 1, IPR_DEC_ITER_LIMIT = 2,
+               IPR_DEC_DIVERGED = 3, IPR_DEC_NONFINITE = 4, IPR_DEC_SWITCH = 5 } ipr_decision;
+
+/* One precision phase ("imprecise arithmetic for the majority of iterations and
+ * then refining ... using precise arithmetic").  rho = ||I - C_k^p A||_F (absolute), rho_hat =
+ * rho / sqrt(n).  A phase is left (reading R-5) when rho <= switch_tol, or when armed
+ * (rho_hat < plateau_arm) and rho_k > plateau_ratio * rho_{k-1}, or on divergence /
+ * non-finite rho, or after max_iters chains; the next phase restarts from the best iterate. */
+typedef struct {
+  ipr_prec  prec;          /* operand format of the p+1 GEMMs                                */
+  int       mant_bits;     /* m: stored mantissa bits of C and A (R-8 container: e8 for      */
+                           /* BF16/FP16/TF32 phases, m <= 23; e11 for FP64, m <= 52); -1 =   */
+                           /* the operand format's own (7 BF16, 10 FP16/TF32, 52 FP64)       */
+  ipr_round round;         /* rounding of stored C and A                                     */
+  double    switch_tol;    /* 0 = off                                                         */
+  double    plateau_ratio; /* 0 = off (typ. 0.7)                                              */
+  double    plateau_arm;   /* typ. 0.5                                                        */
+  int       max_iters;     /* per-phase cap on chains; 0 = unlimited                          */
+} ipr_phase;
+
+/* Trace record: one per evaluated iterate C_k (one chain of p GEMMs). */
+typedef struct {
+  int    k;          /* record index (0-based)                                               */
+  int    phase;      /* schedule index of the phase that evaluated C_k                       */
+  int    prec;       /* ipr_prec of that phase                                               */
+  int    mant_bits;  /* effective m of that phase                                            */
+  int    decision;   /* ipr_decision taken after this residual                               */
+  double rho;        /* in-chain ||I - C_k^p A||_F (reading R-4)                             */
+  double rho_hat;    /* rho / sqrt(n)                                                        */
+  double delta;      /* ||C_{k+1} - C_k||_F of the update that followed (NaN if none)        */
+  double gemm_ms;    /* device time of this record's GEMMs (chain + update), CUDA events     */
+} ipr_record;
+
+/* Create a context for an n x n SPD matrix A (FP64, row-major, device, leading dimension
+ * lda >= n), borrowed read-only until ipr_finalize.  Checks exact symmetry (IPR_E_NOT_
+ * SYMMETRIC otherwise), computes ||A||_1, ||A||_inf and max diagonal on the GPU (Eq. 3) and
+ * records a warning (ipr_last_error) if the sufficient condition of reading R-12 for Eq. (2)
+ * fails; that never fails init.
+ * Multi-GPU: world > 1 ranks, one process per GPU, each passing the FULL A;
+ * nccl_unique_id = 128 bytes from ipr_nccl_unique_id on rank 0 broadcast by the caller.
+ * grid_rows x grid_cols must be 1 x world (column panels); other grids -> IPR_E_UNSUPPORTED.
+ * world == 1: nccl_unique_id may be NULL, grid 1 x 1.  cuda_stream: cudaStream_t (NULL ok). */
+ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda,
+                    void *cuda_stream, int world, int rank, const void *nccl_unique_id,
+                    int grid_rows, int grid_cols);
+
+/* Root order p >= 1 and 1..16 phases; the precision (operand mantissa bits,
+ * then m) must be non-decreasing along the schedule.  final_tol >= 0: stop when rho <=
+ * final_tol in the last phase.  May be called again only before the first ipr_iterate. */
+ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int nphases,
+                            double final_tol);
+
+/* Run at most max_iters (> 0) chains.  *iters_done = chains evaluated by this call,
+ * *outcome = IPR_RUNNING if the budget ran out, else the terminal outcome.  Resumable. */
+ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *outcome);
+
+/* certify == 0: the in-chain residual of the latest evaluated iterate (reading R-4).
+ * certify == 1: ||I - C_best^p A||_F recomputed with FP64 DMMA GEMMs from the best iterate
+ * (the one ipr_finalize returns), reading R-3. */
+ipr_status ipr_residual(ipr_ctx *c, int certify, double *rho);
+
+/* Copy up to cap trace records; *count = total records so far (may exceed cap). */
+ipr_status ipr_get_trace(ipr_ctx *c, ipr_record *buf, int cap, int *count);
+
+/* Copy an iterate (FP64) to a caller device buffer: which = 0 the current C_k (the iterate
+ * the next chain evaluates), which = 1 the best iterate (minimum rho, reading R-17). */
+ipr_status ipr_get_iterate(ipr_ctx *c, int which, double *C_dev_out, int64_t ldc);
+
+/* s = ||A||_1 * ||A||_inf and the norms: out4 = {||A||_1, ||A||_inf, max diag, s}. */
+ipr_status ipr_get_norms(ipr_ctx *c, double *out4);
+
+/* Write the best iterate (FP64, full matrix on every rank) to C_dev_out (ldc >= n; may be
+ * NULL to discard) and free the context (also on error). */
+ipr_status ipr_finalize(ipr_ctx *c, double *C_dev_out, int64_t ldc);
+
+/* Message of the last failure (or init warning) of c; c == NULL: this thread's last. */
+const char *ipr_last_error(const ipr_ctx *c);
+
+/* Rank-0 bootstrap helper: 128-byte NCCL unique id (NCCL loaded with dlopen). */
+ipr_status ipr_nccl_unique_id(void *out128);
+
+/* Library version string. */
+const char *ipr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,42 @@
+/*
+ * ipr_testing.h -- kernel-level entry points of libipr used by the parity tests.
+ *
+ * Same conventions as ipr.h (status codes, device pointers, no CPU fallback).  Each call
+ * enqueues on `stream` (cudaStream_t, NULL = legacy default) and synchronises it before
+ * returning, so the caller may read the outputs immediately.
+ */
+#ifndef IPR_TESTING_H
+#define IPR_TESTING_H
+#include <stdint.h>
+#include "ipr.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Device quantisers (approximate storage / operand formats, PAPER.md:191-194 and the format
+ * footnotes PAPER.md:106-111; readings R-7, R-8, R-9, R-20):
+ *   mode 0: FP64 in  -> FP32 out : q_m with e8 container (stored C/A of BF16/FP16/TF32 phases)
+ *   mode 1: FP64 in  -> FP64 out : q_m with e11 container (stored C/A of FP64 phases)
+ *   mode 2: FP32 in  -> BF16 out (uint16 bit patterns), round-to-nearest-even
+ *   mode 3: FP32 in  -> FP32 out rounded to the TF32 grid (e8m10), round-to-nearest-even
+ *   mode 4: FP32 in  -> FP16 out (uint16 bit patterns) of 2^sigma * x, RNE (R-20 scaling)
+ * m: stored mantissa bits (modes 0/1), round: ipr_round (modes 0/1).  len >= 0. */
+ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_t len, int m,
+                             int round, int sigma, void *stream);
+
+/* One GEMM of the hot path with a plain FP64 store epilogue:  Z = X Y  (n x n).
+ *   X  : row-major operand (element (i,k) at X[i*n + k])
+ *   Yt : K-major operand   (element (k,j) of Y at Yt[j*n + k])
+ *   Z  : FP64 row-major, the accumulator converted exactly (FP32 -> FP64 for tensor-core
+ *        kinds).  Formats: prec = IPR_FP64 (double), IPR_TF32 (float on the TF32 grid),
+ *        IPR_BF16 / IPR_FP16 (uint16 bit patterns).  n >= 1 (any n; ragged tiles handled). */
+ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_dev,
+                         double *Z_dev, void *stream);
+
+/* Number of this process's kernel launches since load (all libipr kernels). */
+int64_t ipr_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,265 @@
+"""B200-native (sm_100a) inverse matrix p-th roots -- the Bini iteration of arXiv:1703.02283.
+
+Thin Python binding of libipr.so (include/ipr.h): argument marshalling only.  Every step of
+the hot path (norms, C_0, the p+1 GEMMs, the fused residual/update epilogues, reductions,
+conversions, all-gathers) runs in the library's CUDA kernels.  There is no CPU fallback:
+importing this package without the built library raises, and every call that the GPU path
+cannot serve returns an error status.
+
+PyTorch is used only for device memory and streams (pass tensors or raw device pointers).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libipr.so")
+
+IPR_OK, IPR_E_INVALID_ARG, IPR_E_NOT_SYMMETRIC, IPR_E_STATE = 0, 1, 2, 3
+IPR_E_UNSUPPORTED, IPR_E_OOM, IPR_E_CUDA, IPR_E_NCCL = 4, 5, 6, 7
+IPR_FP64, IPR_TF32, IPR_BF16, IPR_FP16 = 0, 1, 2, 3
+IPR_RNE, IPR_RTZ = 0, 1
+IPR_RUNNING, IPR_CONVERGED, IPR_ITER_LIMIT, IPR_DIVERGED, IPR_NONFINITE = 0, 1, 2, 3, 4
+IPR_DEC_CONTINUE, IPR_DEC_SWITCH = 0, 5
+PREC_NAMES = {IPR_FP64: "fp64", IPR_TF32: "tf32", IPR_BF16: "bf16", IPR_FP16: "fp16"}
+PREC_BY_NAME = {v: k for k, v in PREC_NAMES.items()}
+OUTCOME_NAMES = {0: "running", 1: "converged", 2: "iter_limit", 3: "diverged", 4: "nonfinite"}
+
+# Every symbol include/ipr.h and include/ipr_testing.h declare.
+EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_get_trace",
+            "ipr_get_iterate", "ipr_get_norms", "ipr_finalize", "ipr_last_error",
+            "ipr_nccl_unique_id", "ipr_version", "ipr_test_quantize", "ipr_test_gemm",
+            "ipr_launch_count"]
+
+
+class IprError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"ipr status {status}: {msg}")
+        self.status = status
+
+
+class ipr_phase(C.Structure):
+    _fields_ = [("prec", C.c_int), ("mant_bits", C.c_int), ("round", C.c_int),
+                ("switch_tol", C.c_double), ("plateau_ratio", C.c_double),
+                ("plateau_arm", C.c_double), ("max_iters", C.c_int)]
+
+
+class ipr_record(C.Structure):
+    _fields_ = [("k", C.c_int), ("phase", C.c_int), ("prec", C.c_int), ("mant_bits", C.c_int),
+                ("decision", C.c_int), ("rho", C.c_double), ("rho_hat", C.c_double),
+                ("delta", C.c_double), ("gemm_ms", C.c_double)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; "
+                          "g.build()'` (no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+    vp, i64, dp = C.c_void_p, C.c_int64, C.POINTER(C.c_double)
+    L.ipr_init.argtypes = [C.POINTER(vp), i64, vp, i64, vp, C.c_int, C.c_int, vp, C.c_int, C.c_int]
+    L.ipr_set_schedule.argtypes = [vp, C.c_int, C.POINTER(ipr_phase), C.c_int, C.c_double]
+    L.ipr_iterate.argtypes = [vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.ipr_residual.argtypes = [vp, C.c_int, dp]
+    L.ipr_get_trace.argtypes = [vp, C.POINTER(ipr_record), C.c_int, C.POINTER(C.c_int)]
+    L.ipr_get_iterate.argtypes = [vp, C.c_int, vp, i64]
+    L.ipr_get_norms.argtypes = [vp, dp]
+    L.ipr_finalize.argtypes = [vp, vp, i64]
+    L.ipr_last_error.argtypes = [vp]
+    L.ipr_last_error.restype = C.c_char_p
+    L.ipr_nccl_unique_id.argtypes = [vp]
+    L.ipr_version.restype = C.c_char_p
+    L.ipr_test_quantize.argtypes = [C.c_int, vp, vp, i64, C.c_int, C.c_int, C.c_int, vp]
+    L.ipr_test_gemm.argtypes = [C.c_int, i64, vp, vp, vp, vp]
+    L.ipr_launch_count.restype = C.c_int64
+    for f in EXPORTED:
+        if f not in ("ipr_last_error", "ipr_version", "ipr_launch_count"):
+            getattr(L, f).restype = C.c_int
+    return L
+
+
+_lib = _load()
+
+
+def lib():
+    return _lib
+
+
+def _ptr(x) -> int:
+    """Device pointer of a torch tensor (or an int/None passed through)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def _stream(s) -> int:
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+def _check(st: int, ctx=None):
+    if st != IPR_OK:
+        msg = _lib.ipr_last_error(ctx)
+        raise IprError(st, msg.decode() if msg else "")
+
+
+# ---- the C-ABI, same names ------------------------------------------------------------------
+def ipr_version() -> str:
+    return _lib.ipr_version().decode()
+
+
+def ipr_last_error(ctx=None) -> str:
+    m = _lib.ipr_last_error(ctx)
+    return m.decode() if m else ""
+
+
+def ipr_nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(_lib.ipr_nccl_unique_id(buf))
+    return buf.raw
+
+
+def ipr_init(n: int, A, lda: int | None = None, stream=None, world: int = 1, rank: int = 0,
+             nccl_unique_id: bytes | None = None, grid_rows: int = 1, grid_cols: int | None = None):
+    ctx = C.c_void_p()
+    uid = C.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id is not None else None
+    _check(_lib.ipr_init(C.byref(ctx), n, _ptr(A), lda if lda is not None else n, _stream(stream),
+                         world, rank, uid, grid_rows, grid_cols if grid_cols is not None else world))
+    return ctx
+
+
+def make_phase(prec="fp64", mant_bits=-1, round="rne", switch_tol=0.0, plateau_ratio=0.0,
+               plateau_arm=0.5, max_iters=0) -> ipr_phase:
+    pr = PREC_BY_NAME[prec] if isinstance(prec, str) else int(prec)
+    rd = {"rne": IPR_RNE, "rtz": IPR_RTZ}[round] if isinstance(round, str) else int(round)
+    return ipr_phase(pr, mant_bits, rd, switch_tol, plateau_ratio, plateau_arm, max_iters)
+
+
+def ipr_set_schedule(ctx, p: int, phases, final_tol: float):
+    arr = (ipr_phase * len(phases))(*phases)
+    _check(_lib.ipr_set_schedule(ctx, p, arr, len(phases), final_tol), ctx)
+
+
+def ipr_iterate(ctx, max_iters: int):
+    done, out = C.c_int(0), C.c_int(0)
+    _check(_lib.ipr_iterate(ctx, max_iters, C.byref(done), C.byref(out)), ctx)
+    return done.value, out.value
+
+
+def ipr_residual(ctx, certify: bool = False) -> float:
+    r = C.c_double(0)
+    _check(_lib.ipr_residual(ctx, int(certify), C.byref(r)), ctx)
+    return r.value
+
+
+def ipr_get_trace(ctx):
+    cnt = C.c_int(0)
+    _check(_lib.ipr_get_trace(ctx, None, 0, C.byref(cnt)), ctx)
+    buf = (ipr_record * max(cnt.value, 1))()
+    _check(_lib.ipr_get_trace(ctx, buf, cnt.value, C.byref(cnt)), ctx)
+    return [dict(k=r.k, phase=r.phase, prec=PREC_NAMES[r.prec], mant_bits=r.mant_bits,
+                 decision=r.decision, rho=r.rho, rho_hat=r.rho_hat, delta=r.delta, gemm_ms=r.gemm_ms)
+            for r in buf[:cnt.value]]
+
+
+def ipr_get_iterate(ctx, which: int, C_out, ldc: int | None = None):
+    _check(_lib.ipr_get_iterate(ctx, which, _ptr(C_out), ldc if ldc is not None else C_out.shape[1]), ctx)
+
+
+def ipr_get_norms(ctx):
+    out = (C.c_double * 4)()
+    _check(_lib.ipr_get_norms(ctx, out), ctx)
+    return tuple(out)
+
+
+def ipr_finalize(ctx, C_out=None, ldc: int | None = None):
+    st = _lib.ipr_finalize(ctx, _ptr(C_out), ldc if ldc is not None else (C_out.shape[1] if C_out is not None else 0))
+    _check(st)
+
+
+def ipr_test_quantize(mode: int, x_in, x_out, m: int = 0, round: int = IPR_RNE, sigma: int = 0, stream=None):
+    _check(_lib.ipr_test_quantize(mode, _ptr(x_in), _ptr(x_out), x_in.numel(), m, round, sigma, _stream(stream)))
+
+
+def ipr_test_gemm(prec: int, n: int, X, Yt, Z, stream=None):
+    _check(_lib.ipr_test_gemm(prec, n, _ptr(X), _ptr(Yt), _ptr(Z), _stream(stream)))
+
+
+def ipr_launch_count() -> int:
+    return _lib.ipr_launch_count()
+
+
+# ---- convenience wrapper (still marshalling only) -------------------------------------------
+class Solver:
+    """Owns one ipr_ctx.  A: FP64 CUDA tensor (n x n, symmetric), kept alive by the Solver."""
+
+    def __init__(self, A, p: int, phases, final_tol: float = 1e-12, stream=None, world: int = 1,
+                 rank: int = 0, nccl_unique_id: bytes | None = None):
+        self.A = A
+        self.n = A.shape[0]
+        self.ctx = ipr_init(self.n, A, A.stride(0), stream, world, rank, nccl_unique_id)
+        try:
+            ipr_set_schedule(self.ctx, p, [ph if isinstance(ph, ipr_phase) else make_phase(**ph)
+                                           for ph in phases], final_tol)
+        except Exception:
+            ipr_finalize(self.ctx)
+            self.ctx = None
+            raise
+        self.outcome = IPR_RUNNING
+        self.iters = 0
+
+    def iterate(self, max_iters: int = 1000) -> int:
+        done, out = ipr_iterate(self.ctx, max_iters)
+        self.iters += done
+        self.outcome = out
+        return out
+
+    def trace(self):
+        return ipr_get_trace(self.ctx)
+
+    def residual(self, certify: bool = False) -> float:
+        return ipr_residual(self.ctx, certify)
+
+    def norms(self):
+        return ipr_get_norms(self.ctx)
+
+    def iterate_copy(self, which: int = 0, out=None):
+        import torch
+        if out is None:
+            out = torch.empty((self.n, self.n), dtype=torch.float64, device=self.A.device)
+        ipr_get_iterate(self.ctx, which, out, out.stride(0))
+        return out
+
+    def finalize(self, out=None):
+        import torch
+        if out is None:
+            out = torch.empty((self.n, self.n), dtype=torch.float64, device=self.A.device)
+        ctx, self.ctx = self.ctx, None
+        ipr_finalize(ctx, out, out.stride(0))
+        return out
+
+    def close(self):
+        if self.ctx is not None:
+            ctx, self.ctx = self.ctx, None
+            ipr_finalize(ctx)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve(A, p: int, phases, final_tol: float = 1e-12, max_iters: int = 1000, stream=None):
+    """Run a full solve; returns (C_best, outcome name, trace)."""
+    s = Solver(A, p, phases, final_tol, stream)
+    s.iterate(max_iters)
+    tr = s.trace()
+    out = OUTCOME_NAMES[s.outcome]
+    return s.finalize(), out, tr

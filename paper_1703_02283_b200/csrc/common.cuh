@@ -1,0 +1,171 @@
+// common.cuh -- shared device helpers of libipr (CUDA path only; shares no code with the oracle).
+//
+// Quantisers written at the bit level (the oracle uses an independent frexp/ldexp
+// definition).  Citations: PAPER.md:191-194 [Sec. 4.2] custom exponent/mantissa widths;
+// PAPER.md:106-111 format footnotes; readings R-7 (RNE default, RTZ option), R-8 (container
+// e8 for BF16/FP16/TF32 phases, e11 for FP64 phases, subnormals kept), R-9 (operands take the
+// MMA input format), R-20 (FP16 operands scaled by 2^sigma) -- see DESIGN.md.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+namespace ipr {
+
+enum Prec { P_FP64 = 0, P_TF32 = 1, P_BF16 = 2, P_FP16 = 3 };
+
+// Epilogue modes of the GEMM kernels (bit flags).
+enum EpiMode : int {
+  EPI_STORE_T = 1,    // write qin(scale*D) transposed (K-major operand for the next GEMM)
+  EPI_RESID = 2,      // per-tile partial of sum (delta_ij - scale*D_ij)^2  (fused residual)
+  EPI_UPDATE = 4,     // C_next = q_m(((p+1) C - scale*D) / p), Chat_next, delta partials
+  EPI_F64 = 8,        // test hook: FP64 row-major store of scale*D
+  EPI_TSCRATCH = 16,  // FP16 phase: FP32 store of scale*D transposed + per-tile max|.|
+};
+
+struct GemmArgs {
+  int64_t M, N, K;      // padded sizes (multiples of 128); N = local panel width
+  int64_t n;            // true matrix order (residual masking)
+  int64_t col0;         // global column of local column 0
+  // A operand (Chat): element (i,k) at A + (k / a_kp) * a_pstride + i * a_kp + k % a_kp
+  const void *A; int64_t a_kp, a_pstride;
+  // B operand, K-major: element (k,j) at B + j * ldb + k
+  const void *B; int64_t ldb;
+  int prec, mode;
+  const int *sigA, *sigB; // FP16 phase: device scale exponents of the A / B operands; else NULL
+  // EPI_STORE_T / EPI_TSCRATCH: T(i,j) -> tout[j * ldt + i]
+  void *tout; int64_t ldt;
+  // partial sums: part[tile_n_global * tiles_m + tile_m]
+  double *part; int64_t tiles_m;
+  float *pmax;          // per-tile max |.| (EPI_TSCRATCH, EPI_UPDATE in FP16 phase)
+  // EPI_UPDATE: container C(i,j) at cold/cnew[i * ldc + j]; operand Chat_next at chat_new[i*ldh+j]
+  const void *cold; void *cnew; int64_t ldc;
+  void *chat_new; int64_t ldh;
+  int p, m, rtz, cont64;
+  // EPI_F64
+  double *zout; int64_t ldz;
+};
+
+// ------------------------------------------------------------------------------------
+// Bit-level quantisers
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ double bits2d(uint64_t b) { return __longlong_as_double((long long)b); }
+__device__ __forceinline__ uint64_t d2bits(double x) { return (uint64_t)__double_as_longlong(x); }
+
+// Round the magnitude bits `mag` of an IEEE encoding to keep `s` fewer low bits.
+__device__ __forceinline__ uint64_t round_mag64(uint64_t mag, int s, int rtz) {
+  if (s <= 0) return mag;
+  const uint64_t mask = ~((1ull << s) - 1ull);
+  if (rtz) return mag & mask;
+  const uint64_t half = (1ull << (s - 1)) - 1ull;
+  const uint64_t lsb = (mag >> s) & 1ull;
+  return (mag + half + lsb) & mask;
+}
+
+// FP64 value -> m stored bits in an e11 (FP64) container.  Works for subnormal doubles (the
+// encoding is fixed point there) and carries into Inf on RNE overflow.
+__device__ __forceinline__ double q_e11(double x, int m, int rtz) {
+  const uint64_t b = d2bits(x);
+  const uint64_t sign = b & 0x8000000000000000ull, mag = b ^ sign;
+  if (mag >= 0x7ff0000000000000ull) return x;            // Inf / NaN
+  uint64_t r = round_mag64(mag, 52 - m, rtz);
+  if (rtz && r >= 0x7ff0000000000000ull) r = 0x7fefffffffffffffull;  // unreachable, kept safe
+  return bits2d(r | sign);
+}
+
+// FP64 value -> m stored bits in an e8 (FP32) container, single rounding from FP64.
+__device__ __forceinline__ float q_e8(double x, int m, int rtz) {
+  const uint64_t b = d2bits(x);
+  const uint64_t sign = b & 0x8000000000000000ull, mag = b ^ sign;
+  if (mag >= 0x7ff0000000000000ull) return (float)x;     // Inf / NaN
+  const uint64_t E128 = (uint64_t)(1023 + 128) << 52;    // 2^128: beyond e8
+  const uint64_t E126 = (uint64_t)(1023 - 126) << 52;    // 2^-126: e8 normal minimum
+  // max finite of e8 with m bits: (2 - 2^-m) 2^127
+  const double maxf = bits2d(((uint64_t)(1023 + 127) << 52) | (((1ull << m) - 1ull) << (52 - m)));
+  if (mag >= E128) return rtz ? (float)copysign(maxf, x) : (float)copysign(__longlong_as_double(0x7ff0000000000000ll), x);
+  if (mag >= E126) {
+    const uint64_t r = round_mag64(mag, 52 - m, rtz);
+    if (r >= E128) return (float)copysign(__longlong_as_double(0x7ff0000000000000ll), x);
+    return (float)bits2d(r | sign);                      // exact: <= m+1 significant bits
+  }
+  // e8 subnormal range: multiples of 2^(-126-m)
+  const double up = bits2d((uint64_t)(1023 + 126 + m) << 52);
+  const double dn = bits2d((uint64_t)(1023 - 126 - m) << 52);
+  const double y = __dmul_rn(x, up);
+  const double q = rtz ? trunc(y) : rint(y);
+  return (float)__dmul_rn(q, dn);
+}
+
+// FP32 -> TF32 grid (e8m10), round-to-nearest-even, Inf/NaN kept (operand conversion).
+__device__ __forceinline__ float to_tf32(float x) {
+  const uint32_t b = __float_as_uint(x);
+  const uint32_t sign = b & 0x80000000u, mag = b ^ sign;
+  if (mag >= 0x7f800000u) return x;
+  const uint32_t r = (mag + 0xfffu + ((mag >> 13) & 1u)) & ~0x1fffu;
+  return __uint_as_float(r | sign);
+}
+
+// FP16 phase scale exponent (reading R-20): sigma = 14 - floor(log2 max), 0 if max <= 0 / NaN / Inf.
+__device__ __forceinline__ int fp16_sigma(double mx) {
+  if (!(mx > 0.0) || isinf(mx)) return 0;
+  return 14 - ilogb(mx);
+}
+
+// exact 2^e as double (|e| <= 1000)
+__device__ __forceinline__ double pow2(int e) { return bits2d((uint64_t)(1023 + e) << 52); }
+
+// Operand store of an FP32/FP64 value in phase precision (RNE), FP16 scaled by 2^sig.
+__device__ __forceinline__ void store_operand(void *base, int64_t idx, int prec, double v, int sig) {
+  switch (prec) {
+    case P_FP64: ((double *)base)[idx] = v; break;
+    case P_TF32: ((float *)base)[idx] = to_tf32((float)v); break;
+    case P_BF16: ((__nv_bfloat16 *)base)[idx] = __float2bfloat16_rn((float)v); break;
+    case P_FP16: ((__half *)base)[idx] = __float2half_rn((float)__dmul_rn(v, pow2(sig))); break;
+  }
+}
+
+__host__ __device__ inline int elt_size(int prec) {
+  return prec == P_FP64 ? 8 : (prec == P_BF16 || prec == P_FP16) ? 2 : 4;
+}
+
+// Deterministic block-wide sum of one double per thread (fixed shuffle tree + warp order).
+template <int NT>
+__device__ __forceinline__ double block_sum_det(double v, double *red) {
+  #pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NT / 32; ++i) s += red[i];
+  }
+  return s;  // valid in thread 0
+}
+
+template <int NT>
+__device__ __forceinline__ float block_max(float v, float *red) {
+  #pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float s = 0.f;
+  if (threadIdx.x == 0) for (int i = 0; i < NT / 32; ++i) s = fmaxf(s, red[i]);
+  return s;
+}
+
+}  // namespace ipr
+
+// Host-side launch declarations (implemented in kernels.cu / gemm_dmma.cu / gemm_tc.cu).
+namespace ipr {
+extern int64_t g_launches;
+cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s);
+cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s);  // BF16 / FP16 / TF32
+bool tc_supported(int prec);
+int gemm_tile_n(int prec);   // BN of the kernel used for a precision (partial layout)
+int gemm_tile_m(int prec);
+}  // namespace ipr

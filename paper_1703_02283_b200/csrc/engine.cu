@@ -1,0 +1,680 @@
+// engine.cu -- the C-ABI (include/ipr.h), iteration engine and host precision-switch
+// controller of libipr.
+//
+// Per iteration k in phase phi:
+//   p GEMMs  T_1 = Chat Ahat, T_j = Chat qin(T_{j-1})     (R-1, Eq. (1))
+//            the p-th with the fused residual partials      (R-4)
+//   deterministic reduction -> rho; ONE 16-byte D2H + stream sync (the only host round trip)
+//   controller (R-5) -> continue / switch / stop
+//   GEMM p+1 with the fused FP64 update C_{k+1} = q_m(((p+1)C_k - P)/p)   (R-2)
+//   world > 1: NCCL all-gather of Chat_{k+1} panels in the operand format
+//
+// Multi-GPU layout ("1 x G" column panels): rank g owns columns
+// S_g = [g*kp, (g+1)*kp) of A, T_j and C_{k+1}; Chat is replicated in a panel-major buffer
+// [G][npad][kp] so one in-place ncclAllGather assembles it; every per-tile partial has a
+// global slot so rho / delta are reduced in the same fixed order for any G.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <dlfcn.h>
+#include <string>
+#include <vector>
+
+#include "../../include/ipr.h"
+#include "../../include/ipr_testing.h"
+#include "common.cuh"
+#include "kernels.h"
+#include "nccl_dl.h"
+
+using namespace ipr;
+
+namespace {
+
+thread_local std::string t_err;
+
+struct PhaseC {
+  int prec, m, rtz, cont64;
+  double switch_tol, plateau_ratio, plateau_arm;
+  int max_iters;
+};
+
+}  // namespace
+
+struct ipr_ctx {
+  int64_t n = 0, lda = 0, npad = 0, kp = 0, col0 = 0;
+  int world = 1, rank = 0;
+  cudaStream_t st = nullptr;
+  const double *A = nullptr;
+  double norms[4] = {0, 0, 0, 0};
+  std::string err;
+  NcclComm comm;
+  // schedule
+  int p = 0;
+  std::vector<PhaseC> ph;
+  double final_tol = 0.0;
+  bool scheduled = false, started = false, done = false;
+  int outcome = IPR_RUNNING;
+  // controller state (reading R-5)
+  int phase = 0, it_in_phase = 0;
+  double rho_prev = NAN, rho_best = INFINITY, rhohat_min = INFINITY, last_rho = NAN;
+  // device buffers
+  void *chat[2] = {nullptr, nullptr};   // operand Chat, panel-major [G][npad][kp], 8 B slots
+  void *cont[2] = {nullptr, nullptr};   // container local panel [npad][kp]
+  double *best = nullptr;                // FP64 local panel
+  void *T[2] = {nullptr, nullptr};      // chain intermediates, K-major [kp][npad]
+  void *Aop = nullptr;                  // stage-A operand of the current phase [kp][npad]
+  float *tscr = nullptr;                // FP16 phase T scratch (FP32)
+  double *full64 = nullptr;             // FP64 npad x npad scratch (copy-out / certify)
+  void *Acert = nullptr;                // FP64 Ahat for certify
+  double *part = nullptr; float *pmax = nullptr; int64_t npart = 0;
+  double *dscal = nullptr; double *hscal = nullptr;   // [0] rho^2 [1] delta^2 [2] max
+  int *dsig = nullptr;                  // [0] sigma_A(phase) [1,2] sigma_C ping-pong [3,4] sigma_T
+  double *colsum = nullptr; int *dflag = nullptr;
+  int cur = 0;
+  int best_loc = -1;                    // 0/1: cont[best_loc] holds the best; 2: `best`; -1 none
+  int best_cont64 = 1;
+  int64_t pending_delta = -1;           // trace record whose delta is in flight
+  std::vector<ipr_record> trace;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  bool upd_timed = false;
+};
+
+namespace {
+
+ipr_status fail(ipr_ctx *c, ipr_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  t_err = buf;
+  if (c) c->err = buf;
+  return s;
+}
+
+#define CK(expr)                                                                              \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess)                                                                    \
+      return fail(c, IPR_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+  } while (0)
+#define CKS(expr)                                                                             \
+  do {                                                                                        \
+    ipr_status _s = (expr);                                                                   \
+    if (_s != IPR_OK) return _s;                                                              \
+  } while (0)
+
+int native_m(int prec) { return prec == IPR_FP64 ? 52 : prec == IPR_BF16 ? 7 : 10; }
+int operand_bits(int prec) { return native_m(prec); }
+
+template <typename T>
+ipr_status dalloc(ipr_ctx *c, T **p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc((void **)p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, IPR_E_OOM, "cudaMalloc(%zu bytes) failed: %s", bytes, cudaGetErrorString(e));
+  }
+  return IPR_OK;
+}
+
+inline size_t slot_bytes(const ipr_ctx *c) { return (size_t)(c->npad * c->kp) * 8; }
+
+// container of iterate buffer i in the current phase (FP64 phases alias the operand slot)
+void *cont_ptr(ipr_ctx *c, int i, const PhaseC &P) {
+  if (P.prec == IPR_FP64) return (char *)c->chat[i] + (size_t)c->rank * slot_bytes(c);
+  return c->cont[i];
+}
+void *chat_slot(ipr_ctx *c, int i, int prec) {
+  return (char *)c->chat[i] + (size_t)c->rank * (size_t)(c->npad * c->kp) * elt_size(prec);
+}
+
+ipr_status gather_chat(ipr_ctx *c, int i, int prec) {
+  if (c->world == 1) return IPR_OK;
+  // packed panel-major layout for this precision: rank r's slot at r * npad * kp * esz
+  const size_t bytes = (size_t)(c->npad * c->kp) * elt_size(prec);
+  char *base = (char *)c->chat[i];
+  if (!c->comm.allgather(base + c->rank * bytes, base, bytes, c->st))
+    return fail(c, IPR_E_NCCL, "ncclAllGather(Chat) failed: %s", c->comm.last_error());
+  return IPR_OK;
+}
+
+// A-operand view of Chat for the GEMMs: element (i,k) at (k/kp)*pstride + i*kp + k%kp
+void chat_view(ipr_ctx *c, int i, int prec, const void **A, int64_t *akp, int64_t *pstride) {
+  *A = c->chat[i];
+  *akp = c->kp;
+  *pstride = (c->world == 1) ? c->npad * c->kp : c->npad * c->kp;
+  (void)prec;
+}
+
+ipr_status gather_partials(ipr_ctx *c, double *part, int64_t per_rank) {
+  if (c->world == 1) return IPR_OK;
+  if (!c->comm.allgather(part + c->rank * per_rank, part, (size_t)per_rank * 8, c->st))
+    return fail(c, IPR_E_NCCL, "ncclAllGather(partials) failed: %s", c->comm.last_error());
+  return IPR_OK;
+}
+ipr_status gather_pmax(ipr_ctx *c, float *pm, int64_t per_rank) {
+  if (c->world == 1) return IPR_OK;
+  if (!c->comm.allgather(pm + c->rank * per_rank, pm, (size_t)per_rank * 4, c->st))
+    return fail(c, IPR_E_NCCL, "ncclAllGather(max partials) failed: %s", c->comm.last_error());
+  return IPR_OK;
+}
+
+int64_t tiles_m(const ipr_ctx *c, int prec) { return c->npad / gemm_tile_m(prec); }
+int64_t tiles_n_total(const ipr_ctx *c, int prec) { return c->npad / gemm_tile_n(prec); }
+
+cudaError_t run_gemm(ipr_ctx *c, GemmArgs &g) {
+  return g.prec == IPR_FP64 ? launch_gemm_dmma(g, c->st) : launch_gemm_tc(g, c->st);
+}
+
+GemmArgs base_args(ipr_ctx *c, int prec, const void *Bop) {
+  GemmArgs g;
+  memset(&g, 0, sizeof g);
+  g.M = c->npad; g.N = c->kp; g.K = c->npad; g.n = c->n; g.col0 = c->col0;
+  g.B = Bop; g.ldb = c->npad; g.prec = prec;
+  g.tiles_m = tiles_m(c, prec);
+  g.p = c->p;
+  return g;
+}
+
+// ---- stage A for a phase (a1) ----
+ipr_status stage_a(ipr_ctx *c, const PhaseC &P, void *dst, int *sig_dst) {
+  const int *sig = nullptr;
+  if (P.prec == IPR_FP16) {
+    const int nparts = 1024;
+    CK(launch_maxabs_qA(c->A, c->lda, c->n, P.cont64, P.m, P.rtz, c->pmax, nparts, c->st));
+    CK(launch_reduce_max(c->pmax, nparts, nullptr, sig_dst, c->st));
+    sig = sig_dst;
+  }
+  CK(launch_stage_a(c->A, c->lda, c->n, c->npad, c->col0, c->kp, P.prec, P.cont64, P.m, P.rtz, sig, dst, c->st));
+  return IPR_OK;
+}
+
+// container cont(i) -> operand Chat(i) (+ FP16 sigma), then all-gather (a8 / a9)
+ipr_status make_operand(ipr_ctx *c, int i, const PhaseC &P) {
+  const int64_t cnt = c->npad * c->kp;
+  if (P.prec != IPR_FP64) {
+    const int *sig = nullptr;
+    if (P.prec == IPR_FP16) {
+      const int nparts = 256;
+      CK(launch_maxabs_cont(c->cont[i], P.cont64, cnt, c->pmax + c->rank * nparts, nparts, c->st));
+      CKS(gather_pmax(c, c->pmax, nparts));
+      CK(launch_reduce_max(c->pmax, (int64_t)nparts * c->world, nullptr, c->dsig + 1 + i, c->st));
+      sig = c->dsig + 1 + i;
+    }
+    CK(launch_make_operand(cont_ptr(c, i, P), P.cont64, cnt, P.prec, sig, chat_slot(c, i, P.prec), c->st));
+  }
+  return gather_chat(c, i, P.prec);
+}
+
+// materialise the best iterate into c->best (FP64 local panel)
+ipr_status save_best(ipr_ctx *c) {
+  if (c->best_loc == 0 || c->best_loc == 1) {
+    const PhaseC &P = c->ph[c->phase];
+    (void)P;
+    const int64_t cnt = c->npad * c->kp;
+    const void *src = c->best_cont64 ? (const void *)((char *)c->chat[c->best_loc] + (size_t)c->rank * slot_bytes(c))
+                                     : c->cont[c->best_loc];
+    // FP64 phases keep the iterate in the operand slot; low phases in cont[]
+    CK(launch_cont_to_f64(src, c->best_cont64, cnt, c->best, c->st));
+    c->best_loc = 2;
+  }
+  return IPR_OK;
+}
+
+ipr_status begin_phase(ipr_ctx *c, bool first) {
+  const PhaseC &P = c->ph[c->phase];
+  CKS(stage_a(c, P, c->Aop, c->dsig + 0));
+  if (first) {
+    CK(launch_c0(c->A, c->lda, c->n, c->npad, c->col0, c->kp, c->norms[3], P.cont64, P.m, P.rtz,
+                 cont_ptr(c, c->cur, P), c->st));
+  } else {
+    CKS(save_best(c));
+    if (c->best_loc == 2) {
+      CK(launch_f64_to_cont(c->best, c->npad * c->kp, P.cont64, P.m, P.rtz, cont_ptr(c, c->cur, P), c->st));
+    }
+  }
+  return make_operand(c, c->cur, P);
+}
+
+// ---- one chain: p GEMMs + fused residual; returns rho (host sync) ----
+ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
+  const PhaseC &P = c->ph[c->phase];
+  const int prec = P.prec;
+  const void *X = c->Aop;
+  const int *sigX = (prec == IPR_FP16) ? c->dsig + 0 : nullptr;
+  const int64_t tm = tiles_m(c, prec), tn_loc = c->kp / gemm_tile_n(prec);
+  double *part = c->part + (c->world > 1 ? 0 : 0);
+  CK(cudaEventRecord(c->ev[0], c->st));
+  for (int j = 1; j <= c->p; ++j) {
+    GemmArgs g = base_args(c, prec, X);
+    chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
+    if (prec == IPR_FP16) { g.sigA = c->dsig + 1 + c->cur; g.sigB = sigX; }
+    g.mode = (prec == IPR_FP16 ? EPI_TSCRATCH : EPI_STORE_T) | (j == c->p ? EPI_RESID : 0);
+    g.tout = (prec == IPR_FP16) ? (void *)c->tscr : c->T[j & 1];
+    g.ldt = c->npad;
+    g.part = part;
+    if (prec == IPR_FP16) g.pmax = c->pmax;
+    CK(run_gemm(c, g));
+    if (prec == IPR_FP16) {
+      CKS(gather_pmax(c, c->pmax, tn_loc * tm));
+      CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 3 + (j & 1), c->st));
+      CK(launch_scale_fp16(c->tscr, c->kp * c->npad, c->dsig + 3 + (j & 1), c->T[j & 1], c->st));
+      sigX = c->dsig + 3 + (j & 1);
+    }
+    X = c->T[j & 1];
+  }
+  CK(cudaEventRecord(c->ev[1], c->st));
+  CKS(gather_partials(c, part, tn_loc * tm));
+  CK(launch_reduce_sum(part, tiles_n_total(c, prec) * tm, c->dscal + 0, c->st));
+  CK(cudaMemcpyAsync(c->hscal, c->dscal, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  float t = 0.f, tu = 0.f;
+  CK(cudaEventElapsedTime(&t, c->ev[0], c->ev[1]));
+  if (c->upd_timed) { CK(cudaEventElapsedTime(&tu, c->ev[2], c->ev[3])); c->upd_timed = false; }
+  if (c->pending_delta >= 0) {
+    c->trace[c->pending_delta].delta = std::sqrt(c->hscal[1]);
+    c->trace[c->pending_delta].gemm_ms += tu;
+    c->pending_delta = -1;
+  }
+  *rho_out = std::sqrt(c->hscal[0]);
+  *ms = t;
+  return IPR_OK;
+}
+
+// ---- GEMM p+1 with the fused update (a6) ----
+ipr_status update(ipr_ctx *c) {
+  const PhaseC &P = c->ph[c->phase];
+  const int prec = P.prec, nx = 1 - c->cur;
+  // the update overwrites buffer nx: keep the best iterate if it lives there
+  if (c->best_loc == nx) CKS(save_best(c));
+  const int64_t tm = tiles_m(c, prec), tn_loc = c->kp / gemm_tile_n(prec);
+  GemmArgs g = base_args(c, prec, c->T[c->p & 1]);
+  chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
+  if (prec == IPR_FP16) { g.sigA = c->dsig + 1 + c->cur; g.sigB = c->dsig + 3 + (c->p & 1); g.pmax = c->pmax; }
+  g.mode = EPI_UPDATE;
+  g.cold = cont_ptr(c, c->cur, P);
+  g.cnew = cont_ptr(c, nx, P);
+  g.ldc = c->kp;
+  g.chat_new = (prec == IPR_FP64) ? nullptr : chat_slot(c, nx, prec);
+  g.ldh = c->kp;
+  g.m = P.m; g.rtz = P.rtz; g.cont64 = P.cont64;
+  g.part = c->part;
+  CK(cudaEventRecord(c->ev[2], c->st));
+  CK(run_gemm(c, g));
+  CK(cudaEventRecord(c->ev[3], c->st));
+  c->upd_timed = true;
+  CKS(gather_partials(c, c->part, tn_loc * tm));
+  CK(launch_reduce_sum(c->part, tiles_n_total(c, prec) * tm, c->dscal + 1, c->st));
+  if (prec == IPR_FP16) {
+    CKS(gather_pmax(c, c->pmax, tn_loc * tm));
+    CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 1 + nx, c->st));
+    CK(launch_make_operand(c->cont[nx], 0, c->npad * c->kp, IPR_FP16, c->dsig + 1 + nx, chat_slot(c, nx, prec), c->st));
+  }
+  CKS(gather_chat(c, nx, prec));
+  c->cur = nx;
+  return IPR_OK;
+}
+
+// Controller, reading R-5 (independent implementation of the rules in DESIGN.md).
+int decide(ipr_ctx *c, double rho, bool *best_new) {
+  const PhaseC &P = c->ph[c->phase];
+  const bool last = c->phase == (int)c->ph.size() - 1;
+  const double rhohat = rho / std::sqrt((double)c->n);
+  const bool fin = std::isfinite(rho);
+  *best_new = fin && rho < c->rho_best;
+  if (*best_new) c->rho_best = rho;
+  int d;
+  if (!fin) d = last ? IPR_DEC_NONFINITE : IPR_DEC_SWITCH;
+  else if (last && rho <= c->final_tol) d = IPR_DEC_CONVERGED;
+  else if (rhohat > 10.0 * c->rhohat_min && rhohat > 1.0) d = last ? IPR_DEC_DIVERGED : IPR_DEC_SWITCH;
+  else if (!last && P.switch_tol > 0.0 && rho <= P.switch_tol) d = IPR_DEC_SWITCH;
+  else if (!last && P.plateau_ratio > 0.0 && rhohat < P.plateau_arm && std::isfinite(c->rho_prev) &&
+           rho > P.plateau_ratio * c->rho_prev)
+    d = IPR_DEC_SWITCH;
+  else if (P.max_iters > 0 && c->it_in_phase + 1 >= P.max_iters) d = last ? IPR_DEC_ITER_LIMIT : IPR_DEC_SWITCH;
+  else d = IPR_DEC_CONTINUE;
+  if (fin && rhohat < c->rhohat_min) c->rhohat_min = rhohat;
+  c->rho_prev = rho;
+  c->it_in_phase += 1;
+  return d;
+}
+
+void free_ctx(ipr_ctx *c) {
+  if (!c) return;
+  cudaFree(c->chat[0]); cudaFree(c->chat[1]); cudaFree(c->cont[0]); cudaFree(c->cont[1]);
+  cudaFree(c->best); cudaFree(c->T[0]); cudaFree(c->T[1]); cudaFree(c->Aop); cudaFree(c->tscr);
+  cudaFree(c->full64); cudaFree(c->Acert); cudaFree(c->part); cudaFree(c->pmax); cudaFree(c->dscal);
+  cudaFree(c->dsig); cudaFree(c->colsum); cudaFree(c->dflag);
+  if (c->hscal) cudaFreeHost(c->hscal);
+  for (auto &e : c->ev) if (e) cudaEventDestroy(e);
+  c->comm.destroy();
+  delete c;
+}
+
+// FP64 full matrix (panel-major [G][npad][kp]) of a local FP64 panel -> full64
+ipr_status gather_f64(ipr_ctx *c, const double *local) {
+  if (!c->full64) CKS(dalloc(c, &c->full64, (size_t)(c->npad * c->npad) * 8));
+  double *slot = c->full64 + (size_t)c->rank * c->npad * c->kp;
+  if (local != slot) CK(cudaMemcpyAsync(slot, local, (size_t)(c->npad * c->kp) * 8, cudaMemcpyDeviceToDevice, c->st));
+  if (c->world > 1 && !c->comm.allgather(slot, c->full64, (size_t)(c->npad * c->kp) * 8, c->st))
+    return fail(c, IPR_E_NCCL, "ncclAllGather(C) failed: %s", c->comm.last_error());
+  return IPR_OK;
+}
+
+}  // namespace
+
+// =========================================================================================
+// C-ABI
+// =========================================================================================
+extern "C" {
+
+const char *ipr_version(void) { return "ipr 0.1.0 (sm_100a: tcgen05 BF16/FP16/TF32, DMMA FP64)"; }
+
+const char *ipr_last_error(const ipr_ctx *c) { return c ? c->err.c_str() : t_err.c_str(); }
+
+ipr_status ipr_nccl_unique_id(void *out128) {
+  ipr_ctx *c = nullptr;
+  if (!out128) return fail(c, IPR_E_INVALID_ARG, "ipr_nccl_unique_id: null output");
+  std::string e;
+  if (!NcclComm::unique_id(out128, &e)) return fail(c, IPR_E_NCCL, "%s", e.c_str());
+  return IPR_OK;
+}
+
+ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, void *cuda_stream, int world,
+                    int rank, const void *nccl_unique_id, int grid_rows, int grid_cols) {
+  ipr_ctx *c = nullptr;
+  if (!out || !A_dev) return fail(c, IPR_E_INVALID_ARG, "ipr_init: null pointer");
+  *out = nullptr;
+  if (n <= 0 || lda < n) return fail(c, IPR_E_INVALID_ARG, "ipr_init: need n > 0 and lda >= n (n=%lld lda=%lld)",
+                                     (long long)n, (long long)lda);
+  if (n > 65535) return fail(c, IPR_E_UNSUPPORTED, "ipr_init: n > 65535 not supported");
+  if (world < 1 || rank < 0 || rank >= world) return fail(c, IPR_E_INVALID_ARG, "ipr_init: bad world/rank");
+  if (grid_rows != 1 || grid_cols != world)
+    return fail(c, IPR_E_UNSUPPORTED, "ipr_init: only 1 x world column-panel grids are implemented");
+  if (world > 1 && !nccl_unique_id) return fail(c, IPR_E_INVALID_ARG, "ipr_init: world > 1 needs an NCCL id");
+  c = new ipr_ctx();
+  c->n = n; c->lda = lda; c->A = A_dev; c->world = world; c->rank = rank;
+  c->st = (cudaStream_t)cuda_stream;
+  const int64_t unit = 128 * (int64_t)world;
+  c->npad = (n + unit - 1) / unit * unit;
+  c->kp = c->npad / world;
+  c->col0 = (int64_t)rank * c->kp;
+  ipr_status s;
+#define TRY(x) do { s = (x); if (s != IPR_OK) { std::string m = c->err; free_ctx(c); t_err = m; return s; } } while (0)
+#define TRYC(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { TRY(fail(c, IPR_E_CUDA, "%s: %s", #x, cudaGetErrorString(_e))); } } while (0)
+  // validate the stream / device early
+  {
+    cudaError_t q = cudaStreamQuery(c->st);
+    if (q != cudaSuccess && q != cudaErrorNotReady) TRYC(q);
+  }
+  TRY(dalloc(c, &c->dflag, 16));
+  TRY(dalloc(c, &c->colsum, (size_t)n * 8));
+  TRY(dalloc(c, &c->dscal, 8 * 8));
+  TRY(dalloc(c, &c->dsig, 8 * 4));
+  TRYC(cudaMallocHost((void **)&c->hscal, 8 * 8));
+  for (auto &e : c->ev) TRYC(cudaEventCreate(&e));
+  TRYC(cudaMemsetAsync(c->dflag, 0, 16, c->st));
+  TRYC(cudaMemsetAsync(c->dsig, 0, 32, c->st));
+  TRYC(launch_symcheck(A_dev, lda, n, c->dflag, c->st));
+  TRYC(launch_norms(A_dev, lda, n, c->colsum, c->dscal, c->st));
+  int flag = 0;
+  TRYC(cudaMemcpyAsync(&flag, c->dflag, 4, cudaMemcpyDeviceToHost, c->st));
+  TRYC(cudaMemcpyAsync(c->norms, c->dscal, 3 * 8, cudaMemcpyDeviceToHost, c->st));
+  TRYC(cudaStreamSynchronize(c->st));
+  if (flag) TRY(fail(c, IPR_E_NOT_SYMMETRIC, "ipr_init: A is not exactly symmetric (A[i][j] != A[j][i] bitwise)"));
+  c->norms[3] = c->norms[0] * c->norms[1];   // s of Eq. (3)
+  if (!(c->norms[3] > 0.0) || !std::isfinite(c->norms[3]))
+    TRY(fail(c, IPR_E_INVALID_ARG, "ipr_init: ||A||_1 ||A||_inf = %g (zero or non-finite A)", c->norms[3]));
+  // buffers sized for the widest (FP64) phase
+  const size_t full = (size_t)(c->npad * c->npad) * 8, panel = (size_t)(c->npad * c->kp) * 8;
+  TRY(dalloc(c, &c->chat[0], full));
+  TRY(dalloc(c, &c->chat[1], full));
+  TRY(dalloc(c, &c->cont[0], panel / 2));
+  TRY(dalloc(c, &c->cont[1], panel / 2));
+  TRY(dalloc(c, &c->best, panel));
+  TRY(dalloc(c, &c->T[0], panel));
+  TRY(dalloc(c, &c->T[1], panel));
+  TRY(dalloc(c, &c->Aop, panel));
+  c->npart = (c->npad / 128) * (c->npad / 128) + 1024;
+  TRY(dalloc(c, &c->part, (size_t)c->npart * 8));
+  TRY(dalloc(c, &c->pmax, (size_t)c->npart * 4));
+  TRYC(cudaMemsetAsync(c->chat[0], 0, full, c->st));
+  TRYC(cudaMemsetAsync(c->chat[1], 0, full, c->st));
+  if (world > 1) {
+    std::string e;
+    if (!c->comm.init(world, rank, nccl_unique_id, &e)) TRY(fail(c, IPR_E_NCCL, "%s", e.c_str()));
+  }
+  TRYC(cudaStreamSynchronize(c->st));
+#undef TRY
+#undef TRYC
+  *out = c;
+  return IPR_OK;
+}
+
+ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int nphases, double final_tol) {
+  if (!c) return fail(c, IPR_E_INVALID_ARG, "ipr_set_schedule: null context");
+  if (c->started) return fail(c, IPR_E_STATE, "ipr_set_schedule: iteration already started");
+  if (p < 1 || p > 64) return fail(c, IPR_E_INVALID_ARG, "ipr_set_schedule: p must be in [1, 64] (got %d)", p);
+  if (!phases || nphases < 1 || nphases > 16) return fail(c, IPR_E_INVALID_ARG, "ipr_set_schedule: 1..16 phases");
+  if (!(final_tol >= 0.0)) return fail(c, IPR_E_INVALID_ARG, "ipr_set_schedule: final_tol must be >= 0");
+  std::vector<PhaseC> v;
+  int prev_ob = -1, prev_m = -1;
+  for (int i = 0; i < nphases; ++i) {
+    const ipr_phase &q = phases[i];
+    if (q.prec < IPR_FP64 || q.prec > IPR_FP16) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad prec", i);
+    PhaseC P;
+    P.prec = q.prec;
+    P.cont64 = q.prec == IPR_FP64;
+    const int mmax = P.cont64 ? 52 : 23;
+    P.m = q.mant_bits < 0 ? native_m(q.prec) : q.mant_bits;
+    if (P.m > mmax) return fail(c, IPR_E_INVALID_ARG, "phase %d: mant_bits %d > %d for this container", i, P.m, mmax);
+    if (q.round != IPR_RNE && q.round != IPR_RTZ) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad round", i);
+    P.rtz = q.round == IPR_RTZ;
+    if (!(q.switch_tol >= 0) || !(q.plateau_ratio >= 0) || q.max_iters < 0)
+      return fail(c, IPR_E_INVALID_ARG, "phase %d: negative tolerance / cap", i);
+    if (q.plateau_ratio > 0 && !(q.plateau_arm > 0))
+      return fail(c, IPR_E_INVALID_ARG, "phase %d: plateau_ratio needs plateau_arm > 0", i);
+    P.switch_tol = q.switch_tol; P.plateau_ratio = q.plateau_ratio; P.plateau_arm = q.plateau_arm;
+    P.max_iters = q.max_iters;
+    const int ob = operand_bits(q.prec);
+    if (ob < prev_ob || (ob == prev_ob && P.m < prev_m))
+      return fail(c, IPR_E_INVALID_ARG, "phase %d: precision must be non-decreasing along the schedule", i);
+    prev_ob = ob; prev_m = P.m;
+    if (P.prec != IPR_FP64 && !tc_supported(P.prec))
+      return fail(c, IPR_E_UNSUPPORTED, "phase %d: tcgen05 path for this precision is not built", i);
+    v.push_back(P);
+  }
+  c->p = p; c->ph = v; c->final_tol = final_tol; c->scheduled = true;
+  c->err.clear();
+  if (p >= 2 && !(c->norms[2] > std::pow(2.0, -1.0 / (p - 1)))) {
+    c->err = "warning: max diagonal <= 2^(-1/(p-1)): the sufficient condition for Eq. (2) (reading R-12) fails";
+  }
+  for (auto &P : c->ph)
+    if (P.prec == IPR_FP16 && !c->tscr) CKS(dalloc(c, &c->tscr, (size_t)(c->npad * c->kp) * 4));
+  return IPR_OK;
+}
+
+ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *outcome) {
+  if (!c || !iters_done || !outcome) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: null pointer");
+  if (!c->scheduled) return fail(c, IPR_E_STATE, "ipr_iterate: call ipr_set_schedule first");
+  if (max_iters <= 0) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: max_iters must be > 0");
+  *iters_done = 0;
+  if (c->done) { *outcome = (ipr_outcome)c->outcome; return IPR_OK; }
+  if (!c->started) {
+    c->phase = 0; c->it_in_phase = 0; c->cur = 0;
+    CKS(begin_phase(c, true));
+    c->started = true;
+  }
+  for (int it = 0; it < max_iters; ++it) {
+    double rho = NAN;
+    float ms = 0.f;
+    CKS(chain(c, &rho, &ms));
+    c->last_rho = rho;
+    const int phase_now = c->phase;
+    bool best_new = false;
+    const int d = decide(c, rho, &best_new);
+    if (best_new) { c->best_loc = c->cur; c->best_cont64 = c->ph[c->phase].prec == IPR_FP64; }
+    ipr_record r;
+    r.k = (int)c->trace.size(); r.phase = phase_now; r.prec = c->ph[phase_now].prec; r.mant_bits = c->ph[phase_now].m;
+    r.decision = d; r.rho = rho; r.rho_hat = rho / std::sqrt((double)c->n); r.delta = NAN; r.gemm_ms = ms;
+    c->trace.push_back(r);
+    *iters_done += 1;
+    if (d == IPR_DEC_CONTINUE) {
+      CKS(update(c));
+      c->pending_delta = (int64_t)c->trace.size() - 1;
+    } else if (d == IPR_DEC_SWITCH) {
+      if (c->best_loc < 0) { c->best_loc = c->cur; c->best_cont64 = c->ph[c->phase].prec == IPR_FP64; }
+      CKS(save_best(c));
+      c->phase += 1; c->it_in_phase = 0; c->rho_prev = NAN;
+      c->cur = 0;
+      CKS(begin_phase(c, false));
+    } else {
+      c->done = true;
+      c->outcome = d;   // IPR_DEC_* terminal values equal the ipr_outcome values
+      break;
+    }
+  }
+  *outcome = c->done ? (ipr_outcome)c->outcome : IPR_RUNNING;
+  return IPR_OK;
+}
+
+ipr_status ipr_get_trace(ipr_ctx *c, ipr_record *buf, int cap, int *count) {
+  if (!c || !count) return fail(c, IPR_E_INVALID_ARG, "ipr_get_trace: null pointer");
+  if (c->pending_delta >= 0) {
+    CK(cudaMemcpyAsync(c->hscal + 1, c->dscal + 1, 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    float tu = 0.f;
+    if (c->upd_timed) { CK(cudaEventElapsedTime(&tu, c->ev[2], c->ev[3])); c->upd_timed = false; }
+    c->trace[c->pending_delta].delta = std::sqrt(c->hscal[1]);
+    c->trace[c->pending_delta].gemm_ms += tu;
+    c->pending_delta = -1;
+  }
+  *count = (int)c->trace.size();
+  if (buf && cap > 0) {
+    const int k = cap < *count ? cap : *count;
+    memcpy(buf, c->trace.data(), sizeof(ipr_record) * (size_t)k);
+  }
+  return IPR_OK;
+}
+
+ipr_status ipr_get_norms(ipr_ctx *c, double *out4) {
+  if (!c || !out4) return fail(c, IPR_E_INVALID_ARG, "ipr_get_norms: null pointer");
+  memcpy(out4, c->norms, sizeof c->norms);
+  return IPR_OK;
+}
+
+static ipr_status copy_iterate(ipr_ctx *c, int which, double *dst, int64_t ldc) {
+  const int64_t cnt = c->npad * c->kp;
+  if (!c->full64) CKS(dalloc(c, &c->full64, (size_t)(c->npad * c->npad) * 8));
+  double *slot = c->full64 + (size_t)c->rank * cnt;
+  if (which == 0) {
+    const PhaseC &P = c->ph[c->phase];
+    CK(launch_cont_to_f64(cont_ptr(c, c->cur, P), P.cont64, cnt, slot, c->st));
+  } else {
+    if (c->best_loc < 0) return fail(c, IPR_E_STATE, "no iterate evaluated yet");
+    CKS(save_best(c));
+    CK(cudaMemcpyAsync(slot, c->best, (size_t)cnt * 8, cudaMemcpyDeviceToDevice, c->st));
+  }
+  CKS(gather_f64(c, slot));
+  if (dst) CK(launch_copy_out(c->full64, c->npad, c->kp, c->n, dst, ldc, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return IPR_OK;
+}
+
+ipr_status ipr_get_iterate(ipr_ctx *c, int which, double *C_dev_out, int64_t ldc) {
+  if (!c || !C_dev_out) return fail(c, IPR_E_INVALID_ARG, "ipr_get_iterate: null pointer");
+  if (ldc < c->n) return fail(c, IPR_E_INVALID_ARG, "ipr_get_iterate: ldc < n");
+  if (which != 0 && which != 1) return fail(c, IPR_E_INVALID_ARG, "ipr_get_iterate: which must be 0 or 1");
+  if (!c->started) return fail(c, IPR_E_STATE, "ipr_get_iterate: no iterate yet (call ipr_iterate)");
+  return copy_iterate(c, which, C_dev_out, ldc);
+}
+
+ipr_status ipr_residual(ipr_ctx *c, int certify, double *rho) {
+  if (!c || !rho) return fail(c, IPR_E_INVALID_ARG, "ipr_residual: null pointer");
+  if (!c->started || c->trace.empty()) return fail(c, IPR_E_STATE, "ipr_residual: no iterate evaluated yet");
+  if (!certify) { *rho = c->last_rho; return IPR_OK; }
+  // reading R-3: ||I - C_best^p A||_F with FP64 DMMA GEMMs
+  CKS(copy_iterate(c, 1, nullptr, 0));              // full64 = best (FP64, panel-major)
+  if (!c->Acert) CKS(dalloc(c, &c->Acert, (size_t)(c->npad * c->kp) * 8));
+  PhaseC P64{IPR_FP64, 52, 0, 1, 0, 0, 0, 0};
+  CKS(stage_a(c, P64, c->Acert, c->dsig + 0));
+  const void *X = c->Acert;
+  for (int j = 1; j <= c->p; ++j) {
+    GemmArgs g = base_args(c, IPR_FP64, X);
+    g.A = c->full64; g.a_kp = c->kp; g.a_pstride = c->npad * c->kp;
+    g.mode = EPI_STORE_T | (j == c->p ? EPI_RESID : 0);
+    g.tout = c->T[j & 1]; g.ldt = c->npad; g.part = c->part;
+    CK(run_gemm(c, g));
+    X = c->T[j & 1];
+  }
+  const int64_t tm = tiles_m(c, IPR_FP64), tn_loc = c->kp / gemm_tile_n(IPR_FP64);
+  CKS(gather_partials(c, c->part, tn_loc * tm));
+  CK(launch_reduce_sum(c->part, tiles_n_total(c, IPR_FP64) * tm, c->dscal + 2, c->st));
+  CK(cudaMemcpyAsync(c->hscal + 2, c->dscal + 2, 8, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  *rho = std::sqrt(c->hscal[2]);
+  return IPR_OK;
+}
+
+ipr_status ipr_finalize(ipr_ctx *c, double *C_dev_out, int64_t ldc) {
+  if (!c) return fail(c, IPR_E_INVALID_ARG, "ipr_finalize: null context");
+  ipr_status s = IPR_OK;
+  if (C_dev_out) {
+    if (ldc < c->n) s = fail(c, IPR_E_INVALID_ARG, "ipr_finalize: ldc < n");
+    else if (!c->started || c->best_loc < 0) s = fail(c, IPR_E_STATE, "ipr_finalize: no iterate evaluated");
+    else s = copy_iterate(c, 1, C_dev_out, ldc);
+  }
+  if (s != IPR_OK) t_err = c->err;
+  free_ctx(c);
+  return s;
+}
+
+// ---- test hooks (include/ipr_testing.h) ----
+int64_t ipr_launch_count(void) { return g_launches; }
+
+ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_t len, int m, int round, int sigma,
+                             void *stream) {
+  ipr_ctx *c = nullptr;
+  if (mode < 0 || mode > 4 || len < 0 || (len > 0 && (!in_dev || !out_dev)))
+    return fail(c, IPR_E_INVALID_ARG, "ipr_test_quantize: bad arguments");
+  if ((mode == 0 && (m < 0 || m > 23)) || (mode == 1 && (m < 0 || m > 52)))
+    return fail(c, IPR_E_INVALID_ARG, "ipr_test_quantize: bad m");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(launch_test_quant(mode, in_dev, out_dev, len, m, round == IPR_RTZ, sigma, s));
+  CK(cudaStreamSynchronize(s));
+  return IPR_OK;
+}
+
+ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_dev, double *Z_dev, void *stream) {
+  ipr_ctx *c = nullptr;
+  if (n <= 0 || !X_dev || !Yt_dev || !Z_dev || prec < 0 || prec > 3)
+    return fail(c, IPR_E_INVALID_ARG, "ipr_test_gemm: bad arguments");
+  if (prec != IPR_FP64 && !tc_supported(prec))
+    return fail(c, IPR_E_UNSUPPORTED, "ipr_test_gemm: tcgen05 path for this precision is not built");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t np = (n + 127) / 128 * 128;
+  const int esz = elt_size(prec);
+  void *X = nullptr, *Y = nullptr;
+  double *Z = nullptr;
+  CK(cudaMalloc(&X, (size_t)(np * np) * esz));
+  CK(cudaMalloc(&Y, (size_t)(np * np) * esz));
+  CK(cudaMalloc(&Z, (size_t)(np * np) * 8));
+  CK(launch_pad_copy(X_dev, n, np, esz, X, s));
+  CK(launch_pad_copy(Yt_dev, n, np, esz, Y, s));
+  GemmArgs g;
+  memset(&g, 0, sizeof g);
+  g.M = np; g.N = np; g.K = np; g.n = n; g.col0 = 0;
+  g.A = X; g.a_kp = np; g.a_pstride = np * np;
+  g.B = Y; g.ldb = np; g.prec = prec; g.mode = EPI_F64;
+  g.zout = Z; g.ldz = np; g.tiles_m = np / gemm_tile_m(prec);
+  cudaError_t e = prec == IPR_FP64 ? launch_gemm_dmma(g, s) : launch_gemm_tc(g, s);
+  if (e == cudaSuccess) e = launch_unpad_f64(Z, n, np, Z_dev, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(X); cudaFree(Y); cudaFree(Z);
+  if (e != cudaSuccess) return fail(c, IPR_E_CUDA, "ipr_test_gemm: %s", cudaGetErrorString(e));
+  return IPR_OK;
+}
+
+}  // extern "C"

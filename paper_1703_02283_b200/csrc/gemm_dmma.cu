@@ -1,0 +1,157 @@
+// gemm_dmma.cu -- FP64 GEMM of the hot path on the FP64 tensor pipe (SASS DMMA.8x8x4).
+//
+// tcgen05.mma has no f64 kind on sm_100a (ptxas 12.9), so FP64 phases use the
+// warp-level mma.sync.aligned.m8n8k4.row.col.f64 (DMMA), fed by a 4-stage cp.async
+// (LDGSTS) shared-memory pipeline.  On B200 the DMMA issue peak measured 37.1 TFLOP/s
+// (profiles/r01_calibration.md).
+//
+// Tile 128 x 128 x 16 per CTA, 8 warps (2 x 4) with 64 x 32 warp tiles = 8 x 4 DMMA tiles,
+// 64 FP64 accumulators per thread.  K inside a 16-block is visited in pairs so every thread
+// fetches its two A (and B) fragment values with ONE 16-byte ld.shared; the pairing is the
+// same for A and B, so each DMMA still contracts matching k.  Shared layout: 128 rows x 128 B,
+// 16-byte chunks XOR-swizzled by (row & 1) << 2 -> conflict-free quarter-warp LDS.128.
+// All problem sizes are padded to multiples of 128 by the engine (zero padding), so the
+// main loop carries no bounds checks.  Each output element is produced by exactly one CTA
+// with a fixed K order -> bit-reproducible and independent of the column-panel sharding.
+#include "common.cuh"
+#include "epilogue.cuh"
+
+namespace ipr {
+
+constexpr int DM_BM = 128, DM_BN = 128, DM_BK = 16, DM_ST = 4, DM_NT = 256;
+constexpr int DM_STAGE_DBL = DM_BM * DM_BK + DM_BN * DM_BK;     // doubles per stage
+constexpr int DM_SMEM = DM_ST * DM_STAGE_DBL * 8;               // 131072 bytes
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ int swz(int row, int chunk) { return chunk ^ ((row & 1) << 2); }
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(DM_NT, 1) k_gemm_dmma(const GemmArgs g) {
+  extern __shared__ __align__(128) double smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;              // 2 x 4 warps
+  const int64_t m0 = (int64_t)blockIdx.y * DM_BM, n0 = (int64_t)blockIdx.x * DM_BN;
+  const double *A = (const double *)g.A, *B = (const double *)g.B;
+  const int nkb = (int)(g.K / DM_BK);
+
+  auto sA = [&](int s) { return smem + s * DM_STAGE_DBL; };
+  auto sB = [&](int s) { return smem + s * DM_STAGE_DBL + DM_BM * DM_BK; };
+
+  auto load_stage = [&](int s, int kb) {
+    const int64_t k0 = (int64_t)kb * DM_BK;
+    const double *Ap = A + (k0 / g.a_kp) * g.a_pstride + (k0 % g.a_kp);
+    double *a = sA(s), *b = sB(s);
+    #pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + i * DM_NT, r = idx >> 3, c = idx & 7;
+      cp_async16(a + r * DM_BK + swz(r, c) * 2, Ap + (m0 + r) * g.a_kp + c * 2);
+    }
+    #pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + i * DM_NT, r = idx >> 3, c = idx & 7;
+      cp_async16(b + r * DM_BK + swz(r, c) * 2, B + (n0 + r) * g.ldb + k0 + c * 2);
+    }
+  };
+
+  double acc[8][4][2];
+  #pragma unroll
+  for (int i = 0; i < 8; ++i)
+    #pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  #pragma unroll
+  for (int s = 0; s < DM_ST - 1; ++s) {
+    if (s < nkb) load_stage(s, s);
+    cp_async_commit();
+  }
+
+  const int fr = lane >> 2, fk = lane & 3;
+  for (int kb = 0; kb < nkb; ++kb) {
+    cp_async_wait<DM_ST - 2>();
+    __syncthreads();
+    {
+      const int nk = kb + DM_ST - 1;
+      if (nk < nkb) load_stage(nk % DM_ST, nk);
+      cp_async_commit();
+    }
+    const double *a = sA(kb % DM_ST), *b = sB(kb % DM_ST);
+    #pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const int chunk = kk * 4 + fk;
+      double2 af[8], bf[4];
+      #pragma unroll
+      for (int mi = 0; mi < 8; ++mi) {
+        const int r = wm * 64 + mi * 8 + fr;
+        af[mi] = *(const double2 *)(a + r * DM_BK + swz(r, chunk) * 2);
+      }
+      #pragma unroll
+      for (int ni = 0; ni < 4; ++ni) {
+        const int r = wn * 32 + ni * 8 + fr;
+        bf[ni] = *(const double2 *)(b + r * DM_BK + swz(r, chunk) * 2);
+      }
+      #pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+        #pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], af[mi].x, bf[ni].x);
+      #pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+        #pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], af[mi].y, bf[ni].y);
+    }
+  }
+  cp_async_wait<0>();
+
+  // ---- fused epilogue ----
+  double scale = 1.0;
+  if (g.sigA) scale = pow2(-(*g.sigA + *g.sigB));
+  EpiAcc ea{0.0, 0.0, 0.0f};
+  #pragma unroll
+  for (int mi = 0; mi < 8; ++mi)
+    #pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+      #pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t row = m0 + wm * 64 + mi * 8 + fr;
+        const int64_t col = n0 + wn * 32 + ni * 8 + fk * 2 + e;
+        epi_element(g, row, col, __dmul_rn(acc[mi][ni][e], scale), ea);
+      }
+  __shared__ double red[DM_NT / 32];
+  __shared__ float redf[DM_NT / 32];
+  const int64_t tile = ((g.col0 + n0) / DM_BN) * g.tiles_m + blockIdx.y;
+  if (g.mode & (EPI_RESID | EPI_UPDATE)) {
+    const double s = block_sum_det<DM_NT>((g.mode & EPI_RESID) ? ea.r2 : ea.d2, red);
+    if (tid == 0) g.part[tile] = s;
+  }
+  if (g.pmax) {
+    const float s = block_max<DM_NT>(ea.mx, redf);
+    if (tid == 0) g.pmax[tile] = s;
+  }
+}
+
+cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, DM_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (a.M % DM_BM || a.N % DM_BN || a.K % DM_BK) return cudaErrorInvalidValue;
+  dim3 grid((unsigned)(a.N / DM_BN), (unsigned)(a.M / DM_BM));
+  k_gemm_dmma<<<grid, DM_NT, DM_SMEM, s>>>(a);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace ipr

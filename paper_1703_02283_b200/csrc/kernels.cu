@@ -1,0 +1,319 @@
+// kernels.cu -- HBM-bound kernels of the hot path:
+// symmetry check, the norms of Eq. (3), stage-A conversion of A to a phase's formats, the
+// initial guess C_0, operand / container conversions at phase switches, deterministic
+// reductions of per-tile partials, and copy-out of the answer.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ipr {
+
+int64_t g_launches = 0;
+
+#define LAUNCH_CHECK() do { ++g_launches; return cudaGetLastError(); } while (0)
+
+// ---------------------------------------------------------------------------------------
+// a1: exact symmetry (reading R-13): flag = 1 if any A[i][j] != A[j][i] bit for bit.
+// 32x32 tiles above the diagonal compare against their transpose via shared memory.
+// ---------------------------------------------------------------------------------------
+__global__ void k_symcheck(const double *A, int64_t lda, int64_t n, int *flag) {
+  __shared__ unsigned long long t[32][33];
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;
+  if (bj < bi) return;
+  const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = bj * 32 + r, j = bi * 32 + tx;   // transposed tile
+    t[r][tx] = (i < n && j < n) ? (unsigned long long)__double_as_longlong(A[i * lda + j]) : 0ull;
+  }
+  __syncthreads();
+  int bad = 0;
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = bi * 32 + r, j = bj * 32 + tx;
+    if (i < n && j < n) bad |= ((unsigned long long)__double_as_longlong(A[i * lda + j]) != t[tx][r]);
+  }
+  if (__syncthreads_or(bad) && tx == 0 && ty == 0) atomicOr(flag, 1);
+}
+
+// ---------------------------------------------------------------------------------------
+// a2: norms of Eq. (3).  One thread per column j sums |a_ij| strictly in
+// ascending i (coalesced across the warp).  For an exactly symmetric A the column sum j is
+// the same sequence of terms as the row sum j, so ||A||_inf == ||A||_1 bit for bit.
+// ---------------------------------------------------------------------------------------
+__global__ void k_colsum(const double *A, int64_t lda, int64_t n, double *colsum) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double *p = A + j;
+  double s = 0.0;
+  int64_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    double v[8];
+    #pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(p + (i + u) * lda);
+    #pragma unroll
+    for (int u = 0; u < 8; ++u) s = __dadd_rn(s, fabs(v[u]));
+  }
+  for (; i < n; ++i) s = __dadd_rn(s, fabs(__ldg(p + i * lda)));
+  colsum[j] = s;
+}
+
+// out[0] = max colsum (||A||_1), out[1] = ||A||_inf (= out[0] by exact symmetry), out[2] = max diag
+__global__ void k_norm_final(const double *A, int64_t lda, int64_t n, const double *colsum, double *out) {
+  __shared__ double r1[32], r2[32];
+  double m = 0.0, d = -INFINITY;
+  bool nan = false;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const double c = colsum[j];
+    nan |= isnan(c);
+    m = fmax(m, c);
+    d = fmax(d, A[j * lda + j]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    d = fmax(d, __shfl_xor_sync(0xffffffffu, d, o));
+  }
+  nan = __syncthreads_or(nan);
+  if ((threadIdx.x & 31) == 0) { r1[threadIdx.x >> 5] = m; r2[threadIdx.x >> 5] = d; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { m = fmax(m, r1[w]); d = fmax(d, r2[w]); }
+    m = fmax(m, r1[0]); d = fmax(d, r2[0]);
+    if (nan) m = __longlong_as_double(0x7ff8000000000000ll);
+    out[0] = m; out[1] = m; out[2] = d;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// a1: stage A for a phase (reading R-9): Aop[jj][k] = qin(q_m(A[col0+jj][k])) -- the local
+// column panel A[:, S_g] read as rows of A (exact symmetry), stored K-major for the B operand;
+// zero outside n.  FP16: sigma from max|q_m(A)| over the whole A (same on every rank).
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ double store_q(double x, int cont64, int m, int rtz) {
+  return cont64 ? q_e11(x, m, rtz) : (double)q_e8(x, m, rtz);
+}
+
+__global__ void k_maxabs_qA(const double *A, int64_t lda, int64_t n, int cont64, int m, int rtz, float *pmax) {
+  __shared__ float red[32];
+  float mx = 0.f;
+  const int64_t total = n * n;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / n, j = t % n;
+    mx = fmaxf(mx, fabsf((float)store_q(A[i * lda + j], cont64, m, rtz)));
+  }
+  const float b = block_max<256>(mx, red);
+  if (threadIdx.x == 0) pmax[blockIdx.x] = b;
+}
+
+__global__ void k_stage_a(const double *A, int64_t lda, int64_t n, int64_t npad, int64_t col0, int64_t kp,
+                          int prec, int cont64, int m, int rtz, const int *sig, void *Aop) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t jj = blockIdx.y;
+  if (k >= npad) return;
+  const int64_t j = col0 + jj;
+  double v = 0.0;
+  if (j < n && k < n) v = store_q(A[j * lda + k], cont64, m, rtz);
+  store_operand(Aop, jj * npad + k, prec, v, sig ? sig[0] : 0);
+}
+
+// ---------------------------------------------------------------------------------------
+// a3: initial guess, Eq. (3): C_0(i,j) = q_m0(A(j,i) / s) for the local panel,
+// row-major [npad][kp], A(j,i) == A(i,j) bitwise (checked symmetry) -> coalesced reads.
+// ---------------------------------------------------------------------------------------
+__global__ void k_c0(const double *A, int64_t lda, int64_t n, int64_t col0, int64_t kp, double s,
+                     int cont64, int m, int rtz, void *cont) {
+  const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = blockIdx.y;
+  if (jj >= kp) return;
+  const int64_t j = col0 + jj;
+  double v = 0.0;
+  if (i < n && j < n) v = __ddiv_rn(A[i * lda + j], s);
+  const int64_t o = i * kp + jj;
+  if (cont64) ((double *)cont)[o] = q_e11(v, m, rtz);
+  else ((float *)cont)[o] = q_e8(v, m, rtz);
+}
+
+// container (FP32 or FP64) local panel -> operand (phase prec), same [npad][kp] layout
+__global__ void k_make_operand(const void *cont, int cont64, int64_t count, int prec, const int *sig, void *op) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const double c = cont64 ? ((const double *)cont)[t] : (double)((const float *)cont)[t];
+  store_operand(op, t, prec, c, sig ? sig[0] : 0);
+}
+
+// FP16 T scratch (FP32, [kp][npad]) -> scaled FP16 operand
+__global__ void k_scale_fp16(const float *src, int64_t count, const int *sig, __half *dst) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  dst[t] = __float2half_rn((float)__dmul_rn((double)src[t], pow2(sig[0])));
+}
+
+__global__ void k_maxabs_cont(const void *cont, int cont64, int64_t count, float *pmax) {
+  __shared__ float red[32];
+  float mx = 0.f;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
+    const double c = cont64 ? ((const double *)cont)[t] : (double)((const float *)cont)[t];
+    mx = fmaxf(mx, fabsf((float)c));
+  }
+  const float b = block_max<256>(mx, red);
+  if (threadIdx.x == 0) pmax[blockIdx.x] = b;
+}
+
+// container -> FP64 copy (best iterate), and FP64 -> container of a new phase (a8)
+__global__ void k_cont_to_f64(const void *cont, int cont64, int64_t count, double *dst) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  dst[t] = cont64 ? ((const double *)cont)[t] : (double)((const float *)cont)[t];
+}
+__global__ void k_f64_to_cont(const double *src, int64_t count, int cont64, int m, int rtz, void *cont) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  if (cont64) ((double *)cont)[t] = q_e11(src[t], m, rtz);
+  else ((float *)cont)[t] = q_e8(src[t], m, rtz);
+}
+
+// ---------------------------------------------------------------------------------------
+// Deterministic reductions of per-tile partials (fixed order for a fixed count).
+// ---------------------------------------------------------------------------------------
+__global__ void k_reduce_sum(const double *part, int64_t count, double *out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t t = threadIdx.x; t < count; t += blockDim.x) s = __dadd_rn(s, part[t]);
+  const double b = block_sum_det<512>(s, red);
+  if (threadIdx.x == 0) *out = b;
+}
+// max over float partials -> double out + sigma (FP16 scale) of it
+__global__ void k_reduce_max(const float *part, int64_t count, double *out, int *sig_out) {
+  __shared__ float red[32];
+  float s = 0.f;
+  bool nan = false;
+  for (int64_t t = threadIdx.x; t < count; t += blockDim.x) { s = fmaxf(s, part[t]); nan |= isnan(part[t]); }
+  nan = __syncthreads_or(nan);
+  const float b = block_max<512>(s, red);
+  if (threadIdx.x == 0) {
+    const double mx = nan ? (double)__int_as_float(0x7fc00000) : (double)b;
+    if (out) *out = mx;
+    if (sig_out) *sig_out = fp16_sigma(mx);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// a10: copy out.  src panel-major [G][npad][kp] FP64 (G = 1: row-major npad x npad).
+// ---------------------------------------------------------------------------------------
+__global__ void k_copy_out(const double *src, int64_t npad, int64_t kp, int64_t n, double *dst, int64_t ldc) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = blockIdx.y;
+  if (j >= n) return;
+  dst[i * ldc + j] = src[(j / kp) * npad * kp + i * kp + (j % kp)];
+}
+// copy a caller matrix into a padded row-major buffer (test hook helper)
+__global__ void k_pad_copy(const void *src, int64_t n, int64_t npad, int esz, void *dst) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = blockIdx.y;
+  if (j >= npad) return;
+  char *d = (char *)dst + (i * npad + j) * esz;
+  if (i < n && j < n) { const char *s = (const char *)src + (i * n + j) * esz; for (int b = 0; b < esz; ++b) d[b] = s[b]; }
+  else for (int b = 0; b < esz; ++b) d[b] = 0;
+}
+__global__ void k_unpad_f64(const double *src, int64_t n, int64_t npad, double *dst) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = blockIdx.y;
+  if (j < n) dst[i * n + j] = src[i * npad + j];
+}
+
+// test hook: quantisers
+__global__ void k_test_quant(int mode, const void *in, void *out, int64_t len, int m, int rtz, int sigma) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= len) return;
+  switch (mode) {
+    case 0: ((float *)out)[t] = q_e8(((const double *)in)[t], m, rtz); break;
+    case 1: ((double *)out)[t] = q_e11(((const double *)in)[t], m, rtz); break;
+    case 2: { __nv_bfloat16 h = __float2bfloat16_rn(((const float *)in)[t]); ((uint16_t *)out)[t] = *(uint16_t *)&h; } break;
+    case 3: ((float *)out)[t] = to_tf32(((const float *)in)[t]); break;
+    case 4: { __half h = __float2half_rn((float)__dmul_rn((double)((const float *)in)[t], pow2(sigma))); ((uint16_t *)out)[t] = *(uint16_t *)&h; } break;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------------------
+static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+cudaError_t launch_symcheck(const double *A, int64_t lda, int64_t n, int *flag, cudaStream_t s) {
+  dim3 g(nblk(n, 32), nblk(n, 32)), b(32, 8);
+  k_symcheck<<<g, b, 0, s>>>(A, lda, n, flag);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_norms(const double *A, int64_t lda, int64_t n, double *colsum, double *out3, cudaStream_t s) {
+  k_colsum<<<nblk(n, 128), 128, 0, s>>>(A, lda, n, colsum);
+  ++g_launches;
+  k_norm_final<<<1, 1024, 0, s>>>(A, lda, n, colsum, out3);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_maxabs_qA(const double *A, int64_t lda, int64_t n, int cont64, int m, int rtz, float *pmax,
+                             int nparts, cudaStream_t s) {
+  k_maxabs_qA<<<nparts, 256, 0, s>>>(A, lda, n, cont64, m, rtz, pmax);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_stage_a(const double *A, int64_t lda, int64_t n, int64_t npad, int64_t col0, int64_t kp, int prec,
+                           int cont64, int m, int rtz, const int *sig, void *Aop, cudaStream_t s) {
+  dim3 g(nblk(npad, 256), (unsigned)kp);
+  k_stage_a<<<g, 256, 0, s>>>(A, lda, n, npad, col0, kp, prec, cont64, m, rtz, sig, Aop);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_c0(const double *A, int64_t lda, int64_t n, int64_t npad, int64_t col0, int64_t kp, double sv,
+                      int cont64, int m, int rtz, void *cont, cudaStream_t s) {
+  dim3 g(nblk(kp, 256), (unsigned)npad);
+  k_c0<<<g, 256, 0, s>>>(A, lda, n, col0, kp, sv, cont64, m, rtz, cont);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_make_operand(const void *cont, int cont64, int64_t count, int prec, const int *sig, void *op,
+                                cudaStream_t s) {
+  k_make_operand<<<nblk(count, 256), 256, 0, s>>>(cont, cont64, count, prec, sig, op);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_scale_fp16(const float *src, int64_t count, const int *sig, void *dst, cudaStream_t s) {
+  k_scale_fp16<<<nblk(count, 256), 256, 0, s>>>(src, count, sig, (__half *)dst);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_maxabs_cont(const void *cont, int cont64, int64_t count, float *pmax, int nparts, cudaStream_t s) {
+  k_maxabs_cont<<<nparts, 256, 0, s>>>(cont, cont64, count, pmax);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_cont_to_f64(const void *cont, int cont64, int64_t count, double *dst, cudaStream_t s) {
+  k_cont_to_f64<<<nblk(count, 256), 256, 0, s>>>(cont, cont64, count, dst);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_f64_to_cont(const double *src, int64_t count, int cont64, int m, int rtz, void *cont, cudaStream_t s) {
+  k_f64_to_cont<<<nblk(count, 256), 256, 0, s>>>(src, count, cont64, m, rtz, cont);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_reduce_sum(const double *part, int64_t count, double *out, cudaStream_t s) {
+  k_reduce_sum<<<1, 512, 0, s>>>(part, count, out);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_reduce_max(const float *part, int64_t count, double *out, int *sig, cudaStream_t s) {
+  k_reduce_max<<<1, 512, 0, s>>>(part, count, out, sig);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_copy_out(const double *src, int64_t npad, int64_t kp, int64_t n, double *dst, int64_t ldc,
+                            cudaStream_t s) {
+  dim3 g(nblk(n, 256), (unsigned)n);
+  k_copy_out<<<g, 256, 0, s>>>(src, npad, kp, n, dst, ldc);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_pad_copy(const void *src, int64_t n, int64_t npad, int esz, void *dst, cudaStream_t s) {
+  dim3 g(nblk(npad, 256), (unsigned)npad);
+  k_pad_copy<<<g, 256, 0, s>>>(src, n, npad, esz, dst);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_unpad_f64(const double *src, int64_t n, int64_t npad, double *dst, cudaStream_t s) {
+  dim3 g(nblk(n, 256), (unsigned)n);
+  k_unpad_f64<<<g, 256, 0, s>>>(src, n, npad, dst);
+  LAUNCH_CHECK();
+}
+cudaError_t launch_test_quant(int mode, const void *in, void *out, int64_t len, int m, int rtz, int sigma,
+                              cudaStream_t s) {
+  if (len <= 0) return cudaSuccess;
+  k_test_quant<<<nblk(len, 256), 256, 0, s>>>(mode, in, out, len, m, rtz, sigma);
+  LAUNCH_CHECK();
+}
+
+}  // namespace ipr

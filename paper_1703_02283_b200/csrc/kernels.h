@@ -1,0 +1,30 @@
+// kernels.h -- host launchers of the HBM-bound kernels (kernels.cu).  Internal to libipr.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ipr {
+cudaError_t launch_symcheck(const double *A, int64_t lda, int64_t n, int *flag, cudaStream_t s);
+cudaError_t launch_norms(const double *A, int64_t lda, int64_t n, double *colsum, double *out3, cudaStream_t s);
+cudaError_t launch_maxabs_qA(const double *A, int64_t lda, int64_t n, int cont64, int m, int rtz, float *pmax,
+                             int nparts, cudaStream_t s);
+cudaError_t launch_stage_a(const double *A, int64_t lda, int64_t n, int64_t npad, int64_t col0, int64_t kp, int prec,
+                           int cont64, int m, int rtz, const int *sig, void *Aop, cudaStream_t s);
+cudaError_t launch_c0(const double *A, int64_t lda, int64_t n, int64_t npad, int64_t col0, int64_t kp, double sv,
+                      int cont64, int m, int rtz, void *cont, cudaStream_t s);
+cudaError_t launch_make_operand(const void *cont, int cont64, int64_t count, int prec, const int *sig, void *op,
+                                cudaStream_t s);
+cudaError_t launch_scale_fp16(const float *src, int64_t count, const int *sig, void *dst, cudaStream_t s);
+cudaError_t launch_maxabs_cont(const void *cont, int cont64, int64_t count, float *pmax, int nparts, cudaStream_t s);
+cudaError_t launch_cont_to_f64(const void *cont, int cont64, int64_t count, double *dst, cudaStream_t s);
+cudaError_t launch_f64_to_cont(const double *src, int64_t count, int cont64, int m, int rtz, void *cont,
+                               cudaStream_t s);
+cudaError_t launch_reduce_sum(const double *part, int64_t count, double *out, cudaStream_t s);
+cudaError_t launch_reduce_max(const float *part, int64_t count, double *out, int *sig, cudaStream_t s);
+cudaError_t launch_copy_out(const double *src, int64_t npad, int64_t kp, int64_t n, double *dst, int64_t ldc,
+                            cudaStream_t s);
+cudaError_t launch_pad_copy(const void *src, int64_t n, int64_t npad, int esz, void *dst, cudaStream_t s);
+cudaError_t launch_unpad_f64(const double *src, int64_t n, int64_t npad, double *dst, cudaStream_t s);
+cudaError_t launch_test_quant(int mode, const void *in, void *out, int64_t len, int m, int rtz, int sigma,
+                              cudaStream_t s);
+}  // namespace ipr
