@@ -166,6 +166,7 @@ extern int64_t g_launches;
 cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s);
 cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s);  // BF16 / FP16 / TF32
 bool tc_supported(int prec);
+const char *tc_last_error();
 int gemm_tile_n(int prec);   // BN of the kernel used for a precision (partial layout)
 int gemm_tile_m(int prec);
 }  // namespace ipr

@@ -97,7 +97,7 @@ ipr_status fail(ipr_ctx *c, ipr_status s, const char *fmt, ...) {
   do {                                                                                        \
     cudaError_t _e = (expr);                                                                  \
     if (_e != cudaSuccess)                                                                    \
-      return fail(c, IPR_E_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+      return fail(c, IPR_E_CUDA, "%s:%d %s: %s %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e), tc_last_error()); \
   } while (0)
 #define CKS(expr)                                                                             \
   do {                                                                                        \
@@ -397,7 +397,8 @@ ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, 
   c = new ipr_ctx();
   c->n = n; c->lda = lda; c->A = A_dev; c->world = world; c->rank = rank;
   c->st = (cudaStream_t)cuda_stream;
-  const int64_t unit = 128 * (int64_t)world;
+  // padded order: whole 256-wide tiles per rank (tcgen05 tile N), zero padding
+  const int64_t unit = 256 * (int64_t)world;
   c->npad = (n + unit - 1) / unit * unit;
   c->kp = c->npad / world;
   c->col0 = (int64_t)rank * c->kp;
@@ -654,7 +655,8 @@ ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_
   if (prec != IPR_FP64 && !tc_supported(prec))
     return fail(c, IPR_E_UNSUPPORTED, "ipr_test_gemm: tcgen05 path for this precision is not built");
   cudaStream_t s = (cudaStream_t)stream;
-  const int64_t np = (n + 127) / 128 * 128;
+  const int64_t unit = prec == IPR_FP64 ? 128 : 256;
+  const int64_t np = (n + unit - 1) / unit * unit;
   const int esz = elt_size(prec);
   void *X = nullptr, *Y = nullptr;
   double *Z = nullptr;
@@ -673,7 +675,7 @@ ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_
   if (e == cudaSuccess) e = launch_unpad_f64(Z, n, np, Z_dev, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   cudaFree(X); cudaFree(Y); cudaFree(Z);
-  if (e != cudaSuccess) return fail(c, IPR_E_CUDA, "ipr_test_gemm: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) return fail(c, IPR_E_CUDA, "ipr_test_gemm: %s %s", cudaGetErrorString(e), tc_last_error());
   return IPR_OK;
 }
 

@@ -1,9 +1,374 @@
-// gemm_tc.cu -- tcgen05 (TMEM/TMA) GEMM for BF16 / FP16 / TF32 phases.  (placeholder until the
-// tcgen05 kernel lands: every low-precision phase returns IPR_E_UNSUPPORTED, never a CPU path)
+// gemm_tc.cu -- tcgen05 GEMM of the hot path for the reduced-precision phases (BF16, FP16 and
+// TF32 operands, FP32 accumulation in TMEM).  D = Chat * X, one of:
+// T_j = Chat T_{j-1} (stored transposed in the operand format), the fused residual, or the
+// fused FP64 update C_{k+1} = q_m(((p+1) C_k - P) / p)  (epilogue.cuh, readings R-1/R-2/R-4).
+//
+// Design (sm_100a): persistent kernel, one CTA per SM, 192 threads = 6 warps:
+//   warp 0     TMA producer  -- cp.async.bulk.tensor (SWIZZLE_128B) of A (128 x 128 B) and
+//                               B (256 x 128 B) per K-block into a 4-stage smem ring
+//   warp 1     MMA issuer    -- one thread issues tcgen05.mma.cta_group::1 (M=128, N=256,
+//                               K = 32 B per instruction), commits to mbarriers
+//   warps 2-5  epilogue      -- tcgen05.ld 32x32b.x32 (thread = accumulator row) -> FP64
+//                               epilogue -> global; 4 warps cover the 4 TMEM lane quarters
+// The 512 TMEM columns hold two 128 x 256 FP32 accumulators, so the epilogue of tile i
+// overlaps the MMAs of tile i+1.  Tiles are visited in groups of 16 M-tiles so one wave's
+// A and B working set (~70 MB at n = 8192) stays in the 126 MB L2.
+// Each output element is produced by one CTA with a fixed K order (deterministic; identical
+// for any column-panel sharding).
+#include <cuda.h>
+#include <cstdio>
+
 #include "common.cuh"
+#include "epilogue.cuh"
+
 namespace ipr {
-bool tc_supported(int) { return false; }
-int gemm_tile_n(int prec) { return 128; }
+
+constexpr int TC_BM = 128, TC_BN = 256, TC_BKB = 128;  // BK in bytes (one 128-B swizzle row)
+constexpr int TC_ST = 4, TC_NT = 192;
+constexpr int TC_A_BYTES = TC_BM * TC_BKB, TC_B_BYTES = TC_BN * TC_BKB;
+constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
+constexpr int TC_SMEM = TC_ST * TC_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int TC_GROUP_M = 16;
+
+bool tc_supported(int prec) { return prec == P_BF16 || prec == P_FP16 || prec == P_TF32; }
+int gemm_tile_n(int prec) { return prec == P_FP64 ? 128 : TC_BN; }
 int gemm_tile_m(int prec) { return 128; }
-cudaError_t launch_gemm_tc(const GemmArgs &, cudaStream_t) { return cudaErrorNotSupported; }
+
+// ---------------------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(
+          su32(dst)),
+      "l"((uint64_t)map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
+          su32(dst)),
+      "l"((uint64_t)map), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
+               : "memory");
+}
+
+template <int KIND>  // 0: kind::f16 (bf16/fp16), 1: kind::tf32
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  if (KIND == 0)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, 8-row core-matrix groups 1024 B apart.
+__device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3fff);          // start address
+  d |= (uint64_t)1 << 16;                          // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                // stride byte offset
+  d |= (uint64_t)1 << 46;                          // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: FP32 accumulate, K-major A and B, M = 128, N = 256.
+__host__ __device__ constexpr uint32_t make_idesc(int prec) {
+  const uint32_t fmt = prec == P_BF16 ? 1u : prec == P_FP16 ? 0u : 2u;   // bf16 / f16 / tf32
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+}
+
+struct TileSched {
+  int tiles_m, tiles_n;
+  __device__ void get(int t, int &tm, int &tn) const {
+    const int per_group = TC_GROUP_M * tiles_n;
+    const int gidx = t / per_group, first_m = gidx * TC_GROUP_M;
+    const int gm = min(tiles_m - first_m, TC_GROUP_M);
+    const int r = t - gidx * per_group;
+    tm = first_m + r % gm;
+    tn = r / gm;
+  }
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(TC_NT, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const GemmArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = (uint64_t *)(smem + TC_ST * TC_STAGE_BYTES);
+  uint64_t *empty = full + TC_ST;
+  uint64_t *tfull = empty + TC_ST;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
+  __shared__ double red[2][4];
+  __shared__ float redm[2][4];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TileSched sch{(int)(g.M / TC_BM), (int)(g.N / TC_BN)};
+  const int ntiles = sch.tiles_m * sch.tiles_n;
+  const int esz = elt_size(g.prec);
+  const int nkb = (int)(g.K * esz / TC_BKB);
+  const int bke = TC_BKB / esz;                       // K elements per block
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 128); }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        int tm, tn;
+        sch.get(t, tm, tn);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t *sa = smem + stage * TC_STAGE_BYTES, *sb = sa + TC_A_BYTES;
+          mbar_expect_tx(&full[stage], TC_STAGE_BYTES);
+          const int64_t k0 = (int64_t)kb * bke;
+          tma_load_3d(sa, &mapA, &full[stage], (int)(k0 % g.a_kp), tm * TC_BM, (int)(k0 / g.a_kp));
+          tma_load_2d(sb, &mapB, &full[stage], (int)k0, tn * TC_BN);
+          if (++stage == TC_ST) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (single thread) =====
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc(g.prec);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int buf = it & 1;
+        const uint32_t tph = (it >> 1) & 1;
+        mbar_wait(&tempty[buf], tph ^ 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem + buf * TC_BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = su32(smem + stage * TC_STAGE_BYTES), sb = sa + TC_A_BYTES;
+          #pragma unroll
+          for (int k = 0; k < TC_BKB / 32; ++k) {
+            tc_mma<KIND>(dcol, smem_desc_sw128(sa + k * 32), smem_desc_sw128(sb + k * 32), idesc, (kb | k) != 0);
+          }
+          tc_commit(&empty[stage]);
+          if (++stage == TC_ST) { stage = 0; phase ^= 1; }
+        }
+        tc_commit(&tfull[buf]);
+      }
+    }
+  } else {
+    // ===== epilogue warps 2..5: TMEM lane quarter q = warp % 4 =====
+    const int q = warp & 3;
+    const int et = threadIdx.x - 64;    // 0..127
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      int tm, tn;
+      sch.get(t, tm, tn);
+      const int buf = it & 1;
+      mbar_wait(&tfull[buf], (it >> 1) & 1);
+      tc_fence_after();
+      double scale = 1.0;
+      if (g.sigA) scale = pow2(-(*g.sigA + *g.sigB));
+      const int64_t row = (int64_t)tm * TC_BM + q * 32 + lane;
+      const int64_t colb = (int64_t)tn * TC_BN;
+      EpiAcc ea{0.0, 0.0, 0.0f};
+      #pragma unroll 1
+      for (int ch = 0; ch < TC_BN / 32; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * TC_BN + ch * 32, r);
+        #pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const double v = __dmul_rn((double)__uint_as_float(r[j]), scale);
+          epi_element(g, row, colb + ch * 32 + j, v, ea);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[buf]);
+      // per-tile partials: deterministic (fixed shuffle tree, warps summed in order 0..3)
+      if (g.mode & (EPI_RESID | EPI_UPDATE) || g.pmax) {
+        double s = (g.mode & EPI_RESID) ? ea.r2 : ea.d2;
+        float mx = ea.mx;
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          s += __shfl_xor_sync(0xffffffffu, s, o);
+          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) { red[it & 1][q] = s; redm[it & 1][q] = mx; }
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (et == 0) {
+          const int64_t tile = ((g.col0 + colb) / TC_BN) * g.tiles_m + tm;
+          if (g.mode & (EPI_RESID | EPI_UPDATE))
+            g.part[tile] = ((red[it & 1][0] + red[it & 1][1]) + red[it & 1][2]) + red[it & 1][3];
+          if (g.pmax)
+            g.pmax[tile] = fmaxf(fmaxf(redm[it & 1][0], redm[it & 1][1]), fmaxf(redm[it & 1][2], redm[it & 1][3]));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// host side: tensor maps through the driver entry point (no -lcuda link dependency)
+// ---------------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+char g_tc_err[256] = "";
+const char *tc_last_error() { return g_tc_err; }
+
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
+  if (!tc_supported(a.prec)) return cudaErrorNotSupported;
+  if (a.M % TC_BM || a.N % TC_BN || a.K % 128 || a.a_kp % 128) {
+    snprintf(g_tc_err, sizeof g_tc_err, "tcgen05 GEMM: sizes M=%lld N=%lld K=%lld kp=%lld not tile multiples",
+             (long long)a.M, (long long)a.N, (long long)a.K, (long long)a.a_kp);
+    return cudaErrorInvalidValue;
+  }
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return cudaErrorNotSupported;
+  const int esz = elt_size(a.prec);
+  const CUtensorMapDataType dt = a.prec == P_BF16   ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                 : a.prec == P_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                    : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  const cuuint32_t bke = TC_BKB / esz;
+  CUtensorMap ma, mb;
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)a.a_kp, (cuuint64_t)a.M, (cuuint64_t)(a.K / a.a_kp)};
+    const cuuint64_t strides[2] = {(cuuint64_t)(a.a_kp * esz), (cuuint64_t)(a.a_pstride * esz)};
+    const cuuint32_t box[3] = {bke, (cuuint32_t)TC_BM, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&ma, dt, 3, (void *)a.A, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      snprintf(g_tc_err, sizeof g_tc_err, "cuTensorMapEncodeTiled(A) failed");
+      return cudaErrorInvalidValue;
+    }
+  }
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a.N};
+    const cuuint64_t strides[1] = {(cuuint64_t)(a.ldb * esz)};
+    const cuuint32_t box[2] = {bke, (cuuint32_t)TC_BN};
+    const cuuint32_t es[2] = {1, 1};
+    if (enc(&mb, dt, 2, (void *)a.B, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      snprintf(g_tc_err, sizeof g_tc_err, "cuTensorMapEncodeTiled(B) failed");
+      return cudaErrorInvalidValue;
+    }
+  }
+  const int ntiles = (int)((a.M / TC_BM) * (a.N / TC_BN));
+  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  cudaError_t e;
+  if (a.prec == P_TF32) {
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(k_gemm_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    k_gemm_tc<1><<<grid, TC_NT, TC_SMEM, s>>>(ma, mb, a);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(k_gemm_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    k_gemm_tc<0><<<grid, TC_NT, TC_SMEM, s>>>(ma, mb, a);
+  }
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 }  // namespace ipr
