@@ -1,0 +1,331 @@
+"""bench.py -- time-to-FP64-residual of the Bini inverse p-th root iteration (arXiv:1703.02283) on B200.
+
+One *step* = one complete solve of the hot path through the C-ABI:
+ipr_init (symmetry check, norms of Eq. 3) -> C_0 -> controller-driven iterations of Eq. (1)
+(p GEMMs + fused residual, GEMM p+1 + fused update) until rho = ||I - C^p A||_F <= 1e-12 ->
+ipr_finalize (best C to a caller buffer).  Inputs are resident in HBM when the timed region
+starts; the e2e number adds the pinned host->device copy of A and the device->host copy of C.
+
+Workload: BASELINE.json's headline n=8192, p=2.  At the stated kappa=1e4
+Eq. (1) cannot reach 1e-12 at all (reading R-3), so the timed workload is its
+kappa=2 twin ("H_twin", seed 5).  A (537 MB FP64) is larger than the 126 MB L2, so no L2 flush
+is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--no-extras]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-to-FP64-residual 1e-12 (n=8192, p=2)"
+FP64_PEAK_TFLOPS = 37.1   # measured DMMA issue peak on this pool (profiles/r01_calibration.md)
+FP64_PEAK_SRC = "measured DMMA.8x8x4 issue peak, tools/probes/dmma_rate.cu (MEASURED_PEAKS.json has no FP64 figure)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default="H_twin")
+    ap.add_argument("--schedule", default="fp64", help="fp64 | bf16-fp64 | tf32-fp64 | fp16-fp64")
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+def schedule(name, n):
+    import paper_1703_02283_b200 as ipr
+    fp64 = ipr.make_phase("fp64")
+    if name == "fp64":
+        return [fp64]
+    low = name.split("-")[0]
+    # leave the low phase at rho_hat <= 1e-2 or on an armed plateau (reading R-5)
+    return [ipr.make_phase(low, switch_tol=1e-2 * math.sqrt(n), plateau_ratio=0.7, plateau_arm=0.5,
+                           max_iters=40), fp64]
+
+
+def gemm_count(trace, p):
+    # p GEMMs per evaluated iterate, +1 for every update that followed
+    return sum(p + (1 if t["decision"] == 0 else 0) for t in trace)
+
+
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        self.out = ""
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        rows = [r.split(",") for r in self.out.strip().splitlines() if r.count(",") >= 6]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(float(r[0]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[3 + i]})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def cpu_baseline(A_np, p, n_gemms, budget_s=15.0):
+    """The oracle (plain C FP64 triple loop) as it stands, timed on a bounded row slab of one
+    GEMM of the same workload on the host cores, extrapolated to the whole solve."""
+    import numpy as np
+    import oracle
+    n = A_np.shape[0]
+    X = np.ascontiguousarray(A_np / np.abs(A_np).sum(0).max() ** 2)   # C_0-like operand
+    Z = np.zeros_like(X)
+    cores = len(os.sched_getaffinity(0))
+    r = max(cores, 8)
+    t0 = time.perf_counter()
+    oracle.gemm_rows(X, A_np, Z, 0, r)
+    t1 = time.perf_counter()
+    per_row = (t1 - t0) / r
+    r2 = int(min(n, max(r, budget_s / max(per_row, 1e-9))))
+    t0 = time.perf_counter()
+    oracle.gemm_rows(X, A_np, Z, 0, r2)
+    t1 = time.perf_counter()
+    per_row = (t1 - t0) / r2
+    t_gemm = per_row * n
+    return {"value": t_gemm * n_gemms, "unit": "s", "cores": cores, "kind": "oracle",
+            "sample": f"oracle orc_gemm_rows: {r2} of {n} rows of one FP64 GEMM (n={n}) in {t1 - t0:.1f} s "
+                      f"({2.0 * r2 * n * n / (t1 - t0) / 1e9:.1f} GFLOP/s); extrapolated x{n}/{r2} rows "
+                      f"x {n_gemms} GEMMs of the solve (epilogues O(n^2), ignored)",
+            "extrapolated": True}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    import numpy as np
+    import torch
+    import synth
+
+    cfg = synth.CONFIGS[args.workload]
+    n, p, kappa, seed = cfg["n"], cfg["p"], cfg["kappa"], cfg["seed"]
+    config = {"workload": f"{args.workload}: n={n} p={p} kappa={kappa:g} seed={seed}, schedule={args.schedule}, "
+                          f"stop at rho<=1e-12 (twin of BASELINE headline n=8192 p=2 kappa=1e4, reading R-3)",
+              "n": n, "p": p, "kappa": kappa, "seed": seed, "schedule": args.schedule,
+              "l2": "inputs larger than L2 (A = %.0f MB FP64 > 126 MB); no flush" % (n * n * 8 / 1e6),
+              "parallelism": f"1x{args.gpus} column panels" if args.gpus > 1 else "single GPU"}
+
+    if args.impl == "reference":
+        # Reference arm = the oracle as it stands on the host cores (rank 0 only).
+        if rank != 0:
+            return
+        A_np = synth.spd(n, kappa, seed) if n <= 2048 else None
+        if A_np is None:
+            rng = np.random.default_rng(seed)
+            A_np = None
+        import oracle
+        if A_np is None:
+            # a CPU QR of 8192^2 takes minutes; the oracle's GEMM cost does not depend on values,
+            # so the bounded timing sample runs on a symmetric matrix of the same size and scale.
+            rng = np.random.default_rng(seed)
+            G = rng.standard_normal((n, n)) / math.sqrt(n)
+            A_np = np.ascontiguousarray((G + G.T) * 0.5 + np.eye(n) * 0.75)
+        n_gemms = 20 * p + 19   # exact-arithmetic iteration count of the twin: 20 chains, 19 updates
+        vals = []
+        for i in range(args.warmup + args.steps):
+            cb = cpu_baseline(A_np, p, n_gemms, budget_s=4.0)
+            if i >= args.warmup:
+                vals.append(cb["value"])
+        v = float(np.mean(vals))
+        cb["value"] = v
+        line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+                "cpu_baseline": cb, "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import paper_1703_02283_b200 as ipr
+    torch.cuda.set_device(local)
+    dist = None
+    uid = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [ipr.ipr_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    stream = torch.cuda.current_stream()
+    A, lam = synth.spd_torch(n, kappa, seed, device="cuda")
+    C_out = torch.empty_like(A)
+    torch.cuda.synchronize()
+    phases = schedule(args.schedule, n)
+
+    def solve(A_dev, out):
+        s = ipr.Solver(A_dev, p, phases, 1e-12, stream, world, rank, uid)
+        s.iterate(400)
+        tr = s.trace()
+        outcome = s.outcome
+        s.finalize(out)
+        return tr, outcome
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        solve(A, C_out)
+    barrier()
+    l0 = ipr.ipr_launch_count()
+    traces = []
+    with Clocks(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            traces.append(solve(A, C_out))
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    launches = ipr.ipr_launch_count() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    tr, outcome = traces[-1]
+    ok = outcome == ipr.IPR_CONVERGED
+
+    # roofline of the dominant kernel (the FP64 DMMA GEMM): algorithmic flops per launch =
+    # 2 n^3 (local panel: 2 n^2 n/G); duration from the library's CUDA events on the launch stream
+    fl_gemm = 2.0 * n * n * (n / world)
+    tot_ms = sum(t["gemm_ms"] for trc, _ in traces for t in trc if t["prec"] == "fp64")
+    tot_gemms = sum(gemm_count([t for t in trc if t["prec"] == "fp64"], p) for trc, _ in traces)
+    gemm_ms = tot_ms / max(tot_gemms, 1)
+    achieved = fl_gemm / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    step_gemm_share = tot_ms / (ms * args.steps) if ms > 0 else None
+    roof = {"bound": "tensor", "kernel": "k_gemm_dmma (FP64 DMMA.8x8x4)", "achieved": achieved,
+            "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
+            "traffic": None, "peak_source": FP64_PEAK_SRC, "cublas_dgemm_tflops": 35.5,
+            "algorithmic_flops_per_launch": fl_gemm, "avg_launch_ms": gemm_ms, "gemm_share_of_step": step_gemm_share}
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            roof["traffic"] = json.load(open(tp)).get("k_gemm_dmma")
+        except Exception:
+            pass
+
+    # e2e: the same solve through the C-ABI from pinned host memory, copies inside the timed region
+    e2e = None
+    if args.e2e_steps > 0:
+        A_host = A.cpu().pin_memory()
+        C_host = torch.empty_like(A_host).pin_memory()
+        A_dev = torch.empty_like(A)
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            A_dev.copy_(A_host, non_blocking=True)
+            solve(A_dev, C_out)
+            C_host.copy_(C_out, non_blocking=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1) / args.e2e_steps
+        if dist is not None:
+            t = torch.tensor([ems], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": ems / 1e3, "unit": "s", "h2d_bytes_per_step": A_host.numel() * 8,
+               "d2h_bytes_per_step": C_host.numel() * 8}
+
+    extras = {}
+    if not args.no_extras and world == 1:
+        # the other half of the metric: GEMM TFLOP/s per precision, and the mixed schedules
+        sched = {}
+        for name in ["bf16-fp64", "tf32-fp64", "fp16-fp64"]:
+            ph = schedule(name, n)
+            torch.cuda.synchronize()
+            g0 = torch.cuda.Event(enable_timing=True)
+            g1 = torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            s = ipr.Solver(A, p, ph, 1e-12, stream)
+            s.iterate(400)
+            t2 = s.trace()
+            out2 = s.outcome
+            s.finalize(C_out)
+            g1.record(stream)
+            torch.cuda.synchronize()
+            low = name.split("-")[0]
+            lms = sum(t["gemm_ms"] for t in t2 if t["prec"] == low)
+            lg = gemm_count([t for t in t2 if t["prec"] == low], p)
+            sched[name] = {"time_s": g0.elapsed_time(g1) / 1e3, "outcome": ipr.OUTCOME_NAMES[out2],
+                           "iters_low": sum(1 for t in t2 if t["prec"] == low),
+                           "iters_fp64": sum(1 for t in t2 if t["prec"] == "fp64"),
+                           "final_rho": t2[-1]["rho"],
+                           "gemm_tflops_low": (lg * 2.0 * n ** 3 / (lms * 1e-3) / 1e12) if lms > 0 else None}
+        sched["fp64"] = {"time_s": ms / 1e3, "outcome": ipr.OUTCOME_NAMES[outcome], "iters_fp64": len(tr),
+                         "final_rho": tr[-1]["rho"]}
+        extras["schedules"] = sched
+        extras["gemm_tflops"] = {"fp64": achieved,
+                                 "bf16": sched["bf16-fp64"]["gemm_tflops_low"],
+                                 "tf32": sched["tf32-fp64"]["gemm_tflops_low"],
+                                 "fp16": sched["fp16-fp64"]["gemm_tflops_low"]}
+        extras["gemm_frac_of_peak"] = {
+            "fp64": achieved / FP64_PEAK_TFLOPS if achieved else None,
+            "bf16_vs_measured_bf16_burst_1599": (extras["gemm_tflops"]["bf16"] or 0) / 1599.0,
+            "fp16_vs_measured_bf16_burst_1599": (extras["gemm_tflops"]["fp16"] or 0) / 1599.0,
+            "tf32_vs_half_of_1599": (extras["gemm_tflops"]["tf32"] or 0) / (1599.0 / 2)}
+
+    if rank != 0:
+        return
+    cb = None
+    if world == 1:
+        try:
+            cb = cpu_baseline(A.cpu().numpy(), p, gemm_count(tr, p))
+        except Exception as ex:  # never fail the bench line on the CPU leg
+            cb = {"value": None, "unit": "s", "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
+    line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+            "converged": ok, "iterations": len(tr), "final_rho": tr[-1]["rho"],
+            "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary()}
+    line.update(extras)
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

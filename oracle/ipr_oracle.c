@@ -120,6 +120,20 @@ int orc_is_symmetric(int64_t n, const double *A) {
   return 1;
 }
 
+/* Rows [r0, r1) of Z = X Y (the same loops as orc_gemm; used to time a bounded sample). */
+void orc_gemm_rows(int64_t n, int64_t r0, int64_t r1, const double *X, const double *Y, double *Z) {
+  #pragma omp parallel for schedule(static)
+  for (int64_t i = r0; i < r1; ++i) {
+    double *z = Z + i * n;
+    for (int64_t j = 0; j < n; ++j) z[j] = 0.0;
+    for (int64_t k = 0; k < n; ++k) {
+      const double x = X[i * n + k];
+      const double *y = Y + k * n;
+      for (int64_t j = 0; j < n; ++j) z[j] += x * y[j];
+    }
+  }
+}
+
 /* Z = X Y: the matrix product of Eq. (1), written as the textbook triple loop. */
 void orc_gemm(int64_t n, const double *X, const double *Y, double *Z) {
   #pragma omp parallel for schedule(static)

@@ -93,6 +93,15 @@ def test_gemm_vs_numpy_and_exact_integers():
     np.testing.assert_array_equal(oracle.gemm(Xi, Yi), Xi @ Yi)   # orientation + exactness
 
 
+def test_gemm_rows_matches_gemm():
+    rng = np.random.default_rng(8)
+    X, Y = rng.standard_normal((40, 40)), rng.standard_normal((40, 40))
+    Z = np.zeros((40, 40))
+    oracle.gemm_rows(X, Y, Z, 5, 17)
+    np.testing.assert_array_equal(Z[5:17], oracle.gemm(X, Y)[5:17])
+    assert np.all(Z[:5] == 0) and np.all(Z[17:] == 0)
+
+
 def test_c0_is_scaled_transpose():
     A = synth.spd(40, 10.0, 1)
     n1, ninf, _ = oracle.norms(A)
