@@ -3,16 +3,19 @@
 // T_j = Chat T_{j-1} (stored transposed in the operand format), the fused residual, or the
 // fused FP64 update C_{k+1} = q_m(((p+1) C_k - P) / p)  (epilogue.cuh, readings R-1/R-2/R-4).
 //
-// Design (sm_100a): persistent kernel, one CTA per SM, 192 threads = 6 warps:
-//   warp 0     TMA producer  -- cp.async.bulk.tensor (SWIZZLE_128B) of A (128 x 128 B) and
-//                               B (256 x 128 B) per K-block into a 4-stage smem ring
-//   warp 1     MMA issuer    -- one thread issues tcgen05.mma.cta_group::1 (M=128, N=256,
-//                               K = 32 B per instruction), commits to mbarriers
-//   warps 2-5  epilogue      -- tcgen05.ld 32x32b.x32 (thread = accumulator row) -> FP64
-//                               epilogue -> global; 4 warps cover the 4 TMEM lane quarters
-// The 512 TMEM columns hold two 128 x 256 FP32 accumulators, so the epilogue of tile i
-// overlaps the MMAs of tile i+1.  Tiles are visited in groups of 16 M-tiles so one wave's
-// A and B working set (~70 MB at n = 8192) stays in the 126 MB L2.
+// Design (sm_100a): persistent kernel, clusters of 2 CTAs (a CTA pair on one TPC) computing
+// 256 x 256 output tiles with tcgen05.mma.cta_group::2 (M = 256, N = 256):
+//   warp 0     TMA producer (both CTAs): each CTA loads its 128 rows of A and its 128 rows of
+//              B per 128-byte K-block (SWIZZLE_128B) into a 6-stage ring; completion bytes of
+//              both CTAs land on the leader CTA's mbarrier
+//   warp 1     MMA issuer (leader CTA, one thread): 4 x tcgen05.mma per K-block, commits
+//              multicast to both CTAs' "stage empty" / "accumulator full" mbarriers
+//   warps 2-5  epilogue (both CTAs): tcgen05.ld 32x32b.x32 (thread = accumulator row) ->
+//              FP64 epilogue -> global; the 4 warps cover the 4 TMEM lane quarters
+// Each CTA keeps two 128 x 256 FP32 accumulators (all 512 TMEM columns), so the epilogue of
+// tile i overlaps the MMAs of tile i+1.  Per SM and K-block the operands are 32 KB for 128 x 256
+// outputs (a 1-CTA 128 x 256 tile needs 48 KB), which keeps the L2 -> SM traffic under the
+// L2 bandwidth.  Pair tiles are visited in groups of 8 along M for L2 reuse.
 // Each output element is produced by one CTA with a fixed K order (deterministic; identical
 // for any column-panel sharding).
 #include <cuda.h>
@@ -23,12 +26,15 @@
 
 namespace ipr {
 
-constexpr int TC_BM = 128, TC_BN = 256, TC_BKB = 128;  // BK in bytes (one 128-B swizzle row)
-constexpr int TC_ST = 4, TC_NT = 192;
-constexpr int TC_A_BYTES = TC_BM * TC_BKB, TC_B_BYTES = TC_BN * TC_BKB;
+constexpr int TC_BM = 128;            // rows per CTA (256 per pair)
+constexpr int TC_BN = 256;            // columns per pair tile
+constexpr int TC_BKB = 128;           // K-block in bytes (one 128-B swizzle row)
+constexpr int TC_ST = 6, TC_NT = 192;
+constexpr int TC_A_BYTES = TC_BM * TC_BKB;          // 16 KB
+constexpr int TC_B_BYTES = (TC_BN / 2) * TC_BKB;    // 16 KB (this CTA's half of N)
 constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
 constexpr int TC_SMEM = TC_ST * TC_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int TC_GROUP_M = 16;
+constexpr int TC_GROUP_M = 8;         // pair-rows per scheduling group
 
 bool tc_supported(int prec) { return prec == P_BF16 || prec == P_FP16 || prec == P_TF32; }
 int gemm_tile_n(int prec) { return prec == P_FP64 ? 128 : TC_BN; }
@@ -38,15 +44,27 @@ int gemm_tile_m(int prec) { return 128; }
 // PTX wrappers
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t su32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
 __device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t cnt) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(cnt));
 }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t *b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+// arrive on the mbarrier at the same smem offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t *b, uint32_t rank) {
+  asm volatile(
+      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(su32(b)),
+      "r"(rank)
+      : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
   asm volatile(
@@ -61,39 +79,60 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1, int c2) {
+// cluster-scope acquire wait (barrier arrived from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *b, uint32_t parity) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];\n" ::"r"(
-          su32(dst)),
-      "l"((uint64_t)map), "r"(su32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(su32(b)),
+      "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+// 2-CTA TMA: the transaction bytes complete on the LEADER CTA's barrier (peer bit cleared)
+__device__ __forceinline__ void tma_load_3d_pair(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                                 int c2) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];\n" ::"r"(
-          su32(dst)),
-      "l"((uint64_t)map), "r"(su32(bar)), "r"(c0), "r"(c1)
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5}], [%2];\n" ::"r"(su32(dst)),
+      "l"((uint64_t)map), "r"(su32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4}], [%2];\n" ::"r"(su32(dst)),
+      "l"((uint64_t)map), "r"(su32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
       : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
-__device__ __forceinline__ void tc_commit(uint64_t *bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(su32(bar))
-               : "memory");
+// commit all prior MMAs of this thread; arrive on the barrier at this offset in both CTAs
+__device__ __forceinline__ void tc_commit_pair(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          su32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
 }
 
 template <int KIND>  // 0: kind::f16 (bf16/fp16), 1: kind::tf32
-__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t acc) {
   if (KIND == 0)
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
   else
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
 
@@ -120,13 +159,13 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor: FP32 accumulate, K-major A and B, M = 128, N = 256.
+// Instruction descriptor: FP32 accumulate, K-major A and B, M = 256 (pair), N = 256.
 __host__ __device__ constexpr uint32_t make_idesc(int prec) {
   const uint32_t fmt = prec == P_BF16 ? 1u : prec == P_FP16 ? 0u : 2u;   // bf16 / f16 / tf32
-  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)(TC_BM >> 4) << 24);
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)((2 * TC_BM) >> 4) << 24);
 }
 
-struct TileSched {
+struct TileSched {      // pair tiles: tiles_m pair-rows (256 rows) x tiles_n (256 columns)
   int tiles_m, tiles_n;
   __device__ void get(int t, int &tm, int &tn) const {
     const int per_group = TC_GROUP_M * tiles_n;
@@ -138,8 +177,81 @@ struct TileSched {
   }
 };
 
+// One 32-column chunk of one accumulator row: the fused epilogue with vectorised row access.
+__device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_t col, const uint32_t (&r)[32],
+                                          double scale, EpiAcc &ea) {
+  const int mode = g.mode;
+  if (mode & (EPI_STORE_T | EPI_TSCRATCH | EPI_RESID | EPI_F64)) {
+    #pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double v = __dmul_rn((double)__uint_as_float(r[j]), scale);
+      const int64_t c = col + j;
+      if (mode & EPI_STORE_T) store_operand(g.tout, c * g.ldt + row, g.prec, v, 0);
+      if (mode & EPI_TSCRATCH) {
+        ((float *)g.tout)[c * g.ldt + row] = (float)v;
+        ea.mx = fmaxf(ea.mx, fabsf((float)v));
+      }
+      if (mode & EPI_RESID) {
+        const int64_t gc = g.col0 + c;
+        if (row < g.n && gc < g.n) {
+          const double d = __dsub_rn(row == gc ? 1.0 : 0.0, v);
+          ea.r2 = __fma_rn(d, d, ea.r2);
+        }
+      }
+      if (mode & EPI_F64) g.zout[row * g.ldz + c] = v;
+    }
+  }
+  if (mode & EPI_UPDATE) {
+    // container row segment [row][col .. col+31]: 128 B (FP32) per thread, 16-byte accesses
+    const double pp1 = (double)(g.p + 1), pd = (double)g.p;
+    const float4 *src = (const float4 *)((const float *)g.cold + row * g.ldc + col);
+    float4 *dst = (float4 *)((float *)g.cnew + row * g.ldc + col);
+    float cn[32];
+    #pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 c4 = src[q];
+      const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+      #pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = q * 4 + u;
+        const double v = __dmul_rn((double)__uint_as_float(r[j]), scale);
+        const double c = (double)cc[u];
+        const double a = __dmul_rn(pp1, c);
+        const double d = __dsub_rn(a, v);
+        const double e = __ddiv_rn(d, pd);
+        const float f = q_e8(e, g.m, g.rtz);
+        cn[j] = f;
+        const double dd = __dsub_rn((double)f, c);
+        ea.d2 = __fma_rn(dd, dd, ea.d2);
+        ea.mx = fmaxf(ea.mx, fabsf(f));
+      }
+      dst[q] = make_float4(cn[q * 4], cn[q * 4 + 1], cn[q * 4 + 2], cn[q * 4 + 3]);
+    }
+    if (g.chat_new && g.prec != P_FP16) {
+      if (g.prec == P_TF32) {
+        float4 *h = (float4 *)((float *)g.chat_new + row * g.ldh + col);
+        #pragma unroll
+        for (int q = 0; q < 8; ++q)
+          h[q] = make_float4(to_tf32(cn[q * 4]), to_tf32(cn[q * 4 + 1]), to_tf32(cn[q * 4 + 2]), to_tf32(cn[q * 4 + 3]));
+      } else {
+        uint4 *h = (uint4 *)((__nv_bfloat16 *)g.chat_new + row * g.ldh + col);
+        #pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t w[4];
+          #pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(cn[q * 8 + 2 * u], cn[q * 8 + 2 * u + 1]);
+            w[u] = *(uint32_t *)&b2;
+          }
+          h[q] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+    }
+  }
+}
+
 template <int KIND>
-__global__ void __launch_bounds__(TC_NT, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const GemmArgs g) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -152,7 +264,10 @@ __global__ void __launch_bounds__(TC_NT, 1)
   __shared__ float redm[2][4];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const TileSched sch{(int)(g.M / TC_BM), (int)(g.N / TC_BN)};
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN)};
   const int ntiles = sch.tiles_m * sch.tiles_n;
   const int esz = elt_size(g.prec);
   const int nkb = (int)(g.K * esz / TC_BKB);
@@ -160,49 +275,49 @@ __global__ void __launch_bounds__(TC_NT, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 128); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(tmem_slot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(su32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ===== TMA producer =====
+    // ===== TMA producer (both CTAs) =====
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      for (int t = pair; t < ntiles; t += npairs) {
         int tm, tn;
         sch.get(t, tm, tn);
+        const int arow = tm * 2 * TC_BM + (int)rank * TC_BM;
+        const int brow = tn * TC_BN + (int)rank * (TC_BN / 2);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t *sa = smem + stage * TC_STAGE_BYTES, *sb = sa + TC_A_BYTES;
-          mbar_expect_tx(&full[stage], TC_STAGE_BYTES);
+          if (leader) mbar_expect_tx(&full[stage], 2 * TC_STAGE_BYTES);
           const int64_t k0 = (int64_t)kb * bke;
-          tma_load_3d(sa, &mapA, &full[stage], (int)(k0 % g.a_kp), tm * TC_BM, (int)(k0 / g.a_kp));
-          tma_load_2d(sb, &mapB, &full[stage], (int)k0, tn * TC_BN);
+          tma_load_3d_pair(sa, &mapA, &full[stage], (int)(k0 % g.a_kp), arow, (int)(k0 / g.a_kp));
+          tma_load_2d_pair(sb, &mapB, &full[stage], (int)k0, brow);
           if (++stage == TC_ST) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ===== MMA issuer (single thread) =====
-    if (lane == 0) {
+    // ===== MMA issuer (leader CTA, single thread) =====
+    if (leader && lane == 0) {
       const uint32_t idesc = make_idesc(g.prec);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+      for (int t = pair; t < ntiles; t += npairs, ++it) {
         const int buf = it & 1;
-        const uint32_t tph = (it >> 1) & 1;
-        mbar_wait(&tempty[buf], tph ^ 1);
+        mbar_wait_cluster(&tempty[buf], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t dcol = tmem + buf * TC_BN;
         for (int kb = 0; kb < nkb; ++kb) {
@@ -210,45 +325,42 @@ __global__ void __launch_bounds__(TC_NT, 1)
           tc_fence_after();
           const uint32_t sa = su32(smem + stage * TC_STAGE_BYTES), sb = sa + TC_A_BYTES;
           #pragma unroll
-          for (int k = 0; k < TC_BKB / 32; ++k) {
-            tc_mma<KIND>(dcol, smem_desc_sw128(sa + k * 32), smem_desc_sw128(sb + k * 32), idesc, (kb | k) != 0);
-          }
-          tc_commit(&empty[stage]);
+          for (int k = 0; k < TC_BKB / 32; ++k)
+            tc_mma_pair<KIND>(dcol, smem_desc_sw128(sa + k * 32), smem_desc_sw128(sb + k * 32), idesc, (kb | k) != 0);
+          tc_commit_pair(&empty[stage]);
           if (++stage == TC_ST) { stage = 0; phase ^= 1; }
         }
-        tc_commit(&tfull[buf]);
+        tc_commit_pair(&tfull[buf]);
       }
     }
   } else {
-    // ===== epilogue warps 2..5: TMEM lane quarter q = warp % 4 =====
+    // ===== epilogue warps 2..5 (both CTAs): TMEM lane quarter q = warp % 4 =====
     const int q = warp & 3;
     const int et = threadIdx.x - 64;    // 0..127
+    double scale = 1.0;
+    if (g.sigA) scale = pow2(-(*g.sigA + *g.sigB));
     int it = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+    for (int t = pair; t < ntiles; t += npairs, ++it) {
       int tm, tn;
       sch.get(t, tm, tn);
       const int buf = it & 1;
       mbar_wait(&tfull[buf], (it >> 1) & 1);
       tc_fence_after();
-      double scale = 1.0;
-      if (g.sigA) scale = pow2(-(*g.sigA + *g.sigB));
-      const int64_t row = (int64_t)tm * TC_BM + q * 32 + lane;
+      const int tile_m = tm * 2 + (int)rank;             // 128-row tile index
+      const int64_t row = (int64_t)tile_m * TC_BM + q * 32 + lane;
       const int64_t colb = (int64_t)tn * TC_BN;
       EpiAcc ea{0.0, 0.0, 0.0f};
       #pragma unroll 1
       for (int ch = 0; ch < TC_BN / 32; ++ch) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * TC_BN + ch * 32, r);
-        #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const double v = __dmul_rn((double)__uint_as_float(r[j]), scale);
-          epi_element(g, row, colb + ch * 32 + j, v, ea);
-        }
+        epi_chunk(g, row, colb + ch * 32, r, scale, ea);
       }
       tc_fence_before();
-      mbar_arrive(&tempty[buf]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
       // per-tile partials: deterministic (fixed shuffle tree, warps summed in order 0..3)
-      if (g.mode & (EPI_RESID | EPI_UPDATE) || g.pmax) {
+      if ((g.mode & (EPI_RESID | EPI_UPDATE)) || g.pmax) {
         double s = (g.mode & EPI_RESID) ? ea.r2 : ea.d2;
         float mx = ea.mx;
         #pragma unroll
@@ -259,7 +371,7 @@ __global__ void __launch_bounds__(TC_NT, 1)
         if (lane == 0) { red[it & 1][q] = s; redm[it & 1][q] = mx; }
         asm volatile("bar.sync 1, 128;\n" ::: "memory");
         if (et == 0) {
-          const int64_t tile = ((g.col0 + colb) / TC_BN) * g.tiles_m + tm;
+          const int64_t tile = ((g.col0 + colb) / TC_BN) * g.tiles_m + tile_m;
           if (g.mode & (EPI_RESID | EPI_UPDATE))
             g.part[tile] = ((red[it & 1][0] + red[it & 1][1]) + red[it & 1][2]) + red[it & 1][3];
           if (g.pmax)
@@ -269,10 +381,10 @@ __global__ void __launch_bounds__(TC_NT, 1)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
   }
 }
 
@@ -310,13 +422,16 @@ static int num_sms() {
 
 cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
   if (!tc_supported(a.prec)) return cudaErrorNotSupported;
-  if (a.M % TC_BM || a.N % TC_BN || a.K % 128 || a.a_kp % 128) {
+  if (a.M % (2 * TC_BM) || a.N % TC_BN || a.K % 128 || a.a_kp % 128) {
     snprintf(g_tc_err, sizeof g_tc_err, "tcgen05 GEMM: sizes M=%lld N=%lld K=%lld kp=%lld not tile multiples",
              (long long)a.M, (long long)a.N, (long long)a.K, (long long)a.a_kp);
     return cudaErrorInvalidValue;
   }
   EncodeTiledFn enc = encode_fn();
-  if (!enc) return cudaErrorNotSupported;
+  if (!enc) {
+    snprintf(g_tc_err, sizeof g_tc_err, "cuTensorMapEncodeTiled entry point unavailable");
+    return cudaErrorNotSupported;
+  }
   const int esz = elt_size(a.prec);
   const CUtensorMapDataType dt = a.prec == P_BF16   ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                  : a.prec == P_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
@@ -338,7 +453,7 @@ cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
   {
     const cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a.N};
     const cuuint64_t strides[1] = {(cuuint64_t)(a.ldb * esz)};
-    const cuuint32_t box[2] = {bke, (cuuint32_t)TC_BN};
+    const cuuint32_t box[2] = {bke, (cuuint32_t)(TC_BN / 2)};
     const cuuint32_t es[2] = {1, 1};
     if (enc(&mb, dt, 2, (void *)a.B, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -347,8 +462,9 @@ cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
       return cudaErrorInvalidValue;
     }
   }
-  const int ntiles = (int)((a.M / TC_BM) * (a.N / TC_BN));
-  const int grid = ntiles < num_sms() ? ntiles : num_sms();
+  const int ntiles = (int)((a.M / (2 * TC_BM)) * (a.N / TC_BN));
+  const int maxpairs = num_sms() / 2;
+  const int grid = 2 * (ntiles < maxpairs ? ntiles : maxpairs);
   cudaError_t e;
   if (a.prec == P_TF32) {
     static bool attr = false;
