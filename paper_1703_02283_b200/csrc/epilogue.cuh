@@ -49,7 +49,8 @@ __device__ __forceinline__ void epi_element(const GemmArgs &g, int64_t row, int6
     const double c = g.cont64 ? ((const double *)g.cold)[ci] : (double)((const float *)g.cold)[ci];
     const double a = __dmul_rn((double)(g.p + 1), c);
     const double d = __dsub_rn(a, v);
-    const double e = __ddiv_rn(d, (double)g.p);
+    // d / p; for p = 2^k the product with the exact reciprocal is the same IEEE result
+    const double e = ((g.p & (g.p - 1)) == 0) ? __dmul_rn(d, 1.0 / (double)g.p) : __ddiv_rn(d, (double)g.p);
     double cn;
     if (g.cont64) {
       cn = q_e11(e, g.m, g.rtz);

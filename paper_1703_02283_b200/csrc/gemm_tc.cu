@@ -10,8 +10,9 @@
 //              both CTAs land on the leader CTA's mbarrier
 //   warp 1     MMA issuer (leader CTA, one thread): 4 x tcgen05.mma per K-block, commits
 //              multicast to both CTAs' "stage empty" / "accumulator full" mbarriers
-//   warps 2-5  epilogue (both CTAs): tcgen05.ld 32x32b.x32 (thread = accumulator row) ->
-//              FP64 epilogue -> global; the 4 warps cover the 4 TMEM lane quarters
+//   warps 2-9  epilogue (both CTAs): tcgen05.ld 32x32b.x32 (thread = accumulator row) ->
+//              FP64 epilogue -> global; warp w reads TMEM lane quarter w % 4 and column
+//              half (w - 2) / 4, so two warps share each quarter
 // Each CTA keeps two 128 x 256 FP32 accumulators (all 512 TMEM columns), so the epilogue of
 // tile i overlaps the MMAs of tile i+1.  Per SM and K-block the operands are 32 KB for 128 x 256
 // outputs (a 1-CTA 128 x 256 tile needs 48 KB), which keeps the L2 -> SM traffic under the
@@ -29,7 +30,7 @@ namespace ipr {
 constexpr int TC_BM = 128;            // rows per CTA (256 per pair)
 constexpr int TC_BN = 256;            // columns per pair tile
 constexpr int TC_BKB = 128;           // K-block in bytes (one 128-B swizzle row)
-constexpr int TC_ST = 6, TC_NT = 192;
+constexpr int TC_ST = 6, TC_NT = 320;   // 2 control warps + 8 epilogue warps
 constexpr int TC_A_BYTES = TC_BM * TC_BKB;          // 16 KB
 constexpr int TC_B_BYTES = (TC_BN / 2) * TC_BKB;    // 16 KB (this CTA's half of N)
 constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
@@ -203,7 +204,8 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
   }
   if (mode & EPI_UPDATE) {
     // container row segment [row][col .. col+31]: 128 B (FP32) per thread, 16-byte accesses
-    const double pp1 = (double)(g.p + 1), pd = (double)g.p;
+    const double pp1 = (double)(g.p + 1), pd = (double)g.p, invp = 1.0 / (double)g.p;
+    const bool p2 = (g.p & (g.p - 1)) == 0;   // d/p == d*(1/p) exactly for p = 2^k
     const float4 *src = (const float4 *)((const float *)g.cold + row * g.ldc + col);
     float4 *dst = (float4 *)((float *)g.cnew + row * g.ldc + col);
     float cn[32];
@@ -218,7 +220,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
         const double c = (double)cc[u];
         const double a = __dmul_rn(pp1, c);
         const double d = __dsub_rn(a, v);
-        const double e = __ddiv_rn(d, pd);
+        const double e = p2 ? __dmul_rn(d, invp) : __ddiv_rn(d, pd);
         const float f = q_e8(e, g.m, g.rtz);
         cn[j] = f;
         const double dd = __dsub_rn((double)f, c);
@@ -260,8 +262,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
   uint64_t *tfull = empty + TC_ST;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = (uint32_t *)(tempty + 2);
-  __shared__ double red[2][4];
-  __shared__ float redm[2][4];
+  __shared__ double red[2][8];
+  __shared__ float redm[2][8];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
@@ -275,7 +277,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_ST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 8); }
+    for (int b = 0; b < 2; ++b) { mbar_init(&tfull[b], 1); mbar_init(&tempty[b], 16); }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -335,8 +337,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
     }
   } else {
     // ===== epilogue warps 2..5 (both CTAs): TMEM lane quarter q = warp % 4 =====
-    const int q = warp & 3;
-    const int et = threadIdx.x - 64;    // 0..127
+    const int q = warp & 3;             // TMEM lane quarter
+    const int hh = (warp - 2) >> 2;     // column half: chunks [4 hh, 4 hh + 4)
+    const int et = threadIdx.x - 64;    // 0..255
     double scale = 1.0;
     if (g.sigA) scale = pow2(-(*g.sigA + *g.sigB));
     int it = 0;
@@ -351,7 +354,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       const int64_t colb = (int64_t)tn * TC_BN;
       EpiAcc ea{0.0, 0.0, 0.0f};
       #pragma unroll 1
-      for (int ch = 0; ch < TC_BN / 32; ++ch) {
+      for (int ch = hh * 4; ch < hh * 4 + 4; ++ch) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * TC_BN + ch * 32, r);
         epi_chunk(g, row, colb + ch * 32, r, scale, ea);
@@ -368,14 +371,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
           s += __shfl_xor_sync(0xffffffffu, s, o);
           mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         }
-        if (lane == 0) { red[it & 1][q] = s; redm[it & 1][q] = mx; }
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (lane == 0) { red[it & 1][hh * 4 + q] = s; redm[it & 1][hh * 4 + q] = mx; }
+        asm volatile("bar.sync 1, 256;\n" ::: "memory");
         if (et == 0) {
           const int64_t tile = ((g.col0 + colb) / TC_BN) * g.tiles_m + tile_m;
           if (g.mode & (EPI_RESID | EPI_UPDATE))
-            g.part[tile] = ((red[it & 1][0] + red[it & 1][1]) + red[it & 1][2]) + red[it & 1][3];
+          {
+            const double *rr = red[it & 1];
+            double acc = 0.0;
+            #pragma unroll
+            for (int w = 0; w < 8; ++w) acc += rr[w];
+            g.part[tile] = acc;
+          }
           if (g.pmax)
-            g.pmax[tile] = fmaxf(fmaxf(redm[it & 1][0], redm[it & 1][1]), fmaxf(redm[it & 1][2], redm[it & 1][3]));
+          {
+            float m8 = 0.f;
+            #pragma unroll
+            for (int w = 0; w < 8; ++w) m8 = fmaxf(m8, redm[it & 1][w]);
+            g.pmax[tile] = m8;
+          }
         }
       }
     }
