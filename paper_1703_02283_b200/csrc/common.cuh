@@ -168,5 +168,6 @@ cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s);  // BF16 / FP16 /
 bool tc_supported(int prec);
 const char *tc_last_error();
 int gemm_tile_n(int prec);   // BN of the kernel used for a precision (partial layout)
+int dmma_tile_n();
 int gemm_tile_m(int prec);
 }  // namespace ipr

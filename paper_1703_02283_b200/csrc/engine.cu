@@ -438,7 +438,7 @@ ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, 
   TRY(dalloc(c, &c->T[0], panel));
   TRY(dalloc(c, &c->T[1], panel));
   TRY(dalloc(c, &c->Aop, panel));
-  c->npart = (c->npad / 128) * (c->npad / 128) + 1024;
+  c->npart = (c->npad / 128) * (c->npad / 64) + 1024;   // one slot per 128 x 64 output tile
   TRY(dalloc(c, &c->part, (size_t)c->npart * 8));
   TRY(dalloc(c, &c->pmax, (size_t)c->npart * 4));
   TRYC(cudaMemsetAsync(c->chat[0], 0, full, c->st));

@@ -5,22 +5,24 @@
 // (LDGSTS) shared-memory pipeline.  On B200 the DMMA issue peak measured 37.1 TFLOP/s
 // (profiles/r01_calibration.md).
 //
-// Tile 128 x 128 x 16 per CTA, 8 warps (2 x 4) with 64 x 32 warp tiles = 8 x 4 DMMA tiles,
-// 64 FP64 accumulators per thread.  K inside a 16-block is visited in pairs so every thread
-// fetches its two A (and B) fragment values with ONE 16-byte ld.shared; the pairing is the
-// same for A and B, so each DMMA still contracts matching k.  Shared layout: 128 rows x 128 B,
-// 16-byte chunks XOR-swizzled by (row & 1) << 2 -> conflict-free quarter-warp LDS.128.
-// All problem sizes are padded to multiples of 128 by the engine (zero padding), so the
-// main loop carries no bounds checks.  Each output element is produced by exactly one CTA
-// with a fixed K order -> bit-reproducible and independent of the column-panel sharding.
+// Tile 128 x 64 x 16 per CTA, 4 warps (2 x 2) with 64 x 32 warp tiles = 8 x 4 DMMA tiles and
+// 64 FP64 accumulators per thread; two CTAs per SM (8 warps/SM) so one CTA's barrier / refill
+// bubble is covered by the other -- the tiling sweep in tools/probes/dmma_variants.cu measured
+// 34.3 TFLOP/s for this shape vs 31.6 for one 128 x 128 CTA per SM.  K inside a 16-block is
+// visited in pairs so every thread fetches its two A (and B) fragment values with ONE 16-byte
+// ld.shared; the pairing is the same for A and B, so each DMMA contracts matching k.  Shared
+// rows are 128 B with 16-byte chunks XOR-swizzled by (row & 1) << 2 -> conflict-free LDS.128.
+// All sizes are padded to multiples of 128 by the engine (zero padding), so the main loop has
+// no bounds checks.  Each output element is produced by exactly one CTA with a fixed K order
+// -> bit-reproducible and independent of the column-panel sharding.
 #include "common.cuh"
 #include "epilogue.cuh"
 
 namespace ipr {
 
-constexpr int DM_BM = 128, DM_BN = 128, DM_BK = 16, DM_ST = 4, DM_NT = 256;
+constexpr int DM_BM = 128, DM_BN = 64, DM_BK = 16, DM_ST = 4, DM_NT = 128;
 constexpr int DM_STAGE_DBL = DM_BM * DM_BK + DM_BN * DM_BK;     // doubles per stage
-constexpr int DM_SMEM = DM_ST * DM_STAGE_DBL * 8;               // 131072 bytes
+constexpr int DM_SMEM = DM_ST * DM_STAGE_DBL * 8;               // 98304 bytes
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
@@ -38,30 +40,32 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(DM_NT, 1) k_gemm_dmma(const GemmArgs g) {
+__global__ void __launch_bounds__(DM_NT, 2) k_gemm_dmma(const GemmArgs g) {
   extern __shared__ __align__(128) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 2, wn = warp & 3;              // 2 x 4 warps
+  const int wm = warp >> 1, wn = warp & 1;              // 2 x 2 warps
   const int64_t m0 = (int64_t)blockIdx.y * DM_BM, n0 = (int64_t)blockIdx.x * DM_BN;
   const double *A = (const double *)g.A, *B = (const double *)g.B;
   const int nkb = (int)(g.K / DM_BK);
+  const int kb_per_panel = (int)(g.a_kp / DM_BK);
 
   auto sA = [&](int s) { return smem + s * DM_STAGE_DBL; };
   auto sB = [&](int s) { return smem + s * DM_STAGE_DBL + DM_BM * DM_BK; };
 
   auto load_stage = [&](int s, int kb) {
-    const int64_t k0 = (int64_t)kb * DM_BK;
-    const double *Ap = A + (k0 / g.a_kp) * g.a_pstride + (k0 % g.a_kp);
+    const int panel = kb / kb_per_panel, kin = (kb - panel * kb_per_panel) * DM_BK;
+    const double *Ap = A + (int64_t)panel * g.a_pstride + kin + m0 * g.a_kp;
+    const double *Bp = B + n0 * g.ldb + (int64_t)kb * DM_BK;
     double *a = sA(s), *b = sB(s);
     #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 8; ++i) {            // A: 128 rows x 8 chunks
       const int idx = tid + i * DM_NT, r = idx >> 3, c = idx & 7;
-      cp_async16(a + r * DM_BK + swz(r, c) * 2, Ap + (m0 + r) * g.a_kp + c * 2);
+      cp_async16(a + r * DM_BK + swz(r, c) * 2, Ap + r * g.a_kp + c * 2);
     }
     #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < 4; ++i) {            // B: 64 rows x 8 chunks
       const int idx = tid + i * DM_NT, r = idx >> 3, c = idx & 7;
-      cp_async16(b + r * DM_BK + swz(r, c) * 2, B + (n0 + r) * g.ldb + k0 + c * 2);
+      cp_async16(b + r * DM_BK + swz(r, c) * 2, Bp + r * g.ldb + c * 2);
     }
   };
 
@@ -113,7 +117,7 @@ __global__ void __launch_bounds__(DM_NT, 1) k_gemm_dmma(const GemmArgs g) {
   }
   cp_async_wait<0>();
 
-  // ---- fused epilogue ----
+  // ---- fused epilogue (per element, fixed order) ----
   double scale = 1.0;
   if (g.sigA) scale = pow2(-(*g.sigA + *g.sigB));
   EpiAcc ea{0.0, 0.0, 0.0f};
@@ -147,11 +151,13 @@ cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (a.M % DM_BM || a.N % DM_BN || a.K % DM_BK) return cudaErrorInvalidValue;
+  if (a.M % DM_BM || a.N % DM_BN || a.K % DM_BK || a.a_kp % DM_BK) return cudaErrorInvalidValue;
   dim3 grid((unsigned)(a.N / DM_BN), (unsigned)(a.M / DM_BM));
   k_gemm_dmma<<<grid, DM_NT, DM_SMEM, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
 }
+
+int dmma_tile_n() { return DM_BN; }
 
 }  // namespace ipr

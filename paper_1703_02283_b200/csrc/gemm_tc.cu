@@ -38,7 +38,7 @@ constexpr int TC_SMEM = TC_ST * TC_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers
 constexpr int TC_GROUP_M = 8;         // pair-rows per scheduling group
 
 bool tc_supported(int prec) { return prec == P_BF16 || prec == P_FP16 || prec == P_TF32; }
-int gemm_tile_n(int prec) { return prec == P_FP64 ? 128 : TC_BN; }
+int gemm_tile_n(int prec) { return prec == P_FP64 ? dmma_tile_n() : TC_BN; }
 int gemm_tile_m(int prec) { return 128; }
 
 // ---------------------------------------------------------------------------------------
