@@ -33,6 +33,14 @@ ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_
 ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_dev,
                          double *Z_dev, void *stream);
 
+/* Host-side plan of the 1 x world column-panel decomposition; needs no GPU.
+ * out8 = {npad (padded order), kp (columns per rank), col0 (first global column of `rank`),
+ *         tile_m, tile_n (output tile of the GEMM kernel used for prec), tiles_m,
+ *         tiles_n_total, first global partial slot of this rank = (col0 / tile_n) * tiles_m}.
+ * Partial slot of output tile (tm, tn_global) = tn_global * tiles_m + tm, identical for
+ * every world size, so per-tile partials reduce in the same order for any G. */
+ipr_status ipr_plan(int64_t n, int world, int rank, int prec, int64_t *out8);
+
 /* Number of this process's kernel launches since load (all libipr kernels). */
 int64_t ipr_launch_count(void);
 

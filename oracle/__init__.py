@@ -72,6 +72,7 @@ def lib():
         L.orc_gemm.argtypes = [C.c_int64, _dp, _dp, _dp]
         L.orc_matvec.argtypes = [C.c_int64, _dp, _dp, _dp]
         L.orc_gemm_rows.argtypes = [C.c_int64, C.c_int64, C.c_int64, _dp, _dp, _dp]
+        L.orc_gemm_cols.argtypes = [C.c_int64, C.c_int64, C.c_int64, _dp, _dp, _dp]
         L.orc_c0.argtypes = [C.c_int64, _dp, C.c_double, C.POINTER(Phase), _dp]
         L.orc_step.restype = C.c_double
         L.orc_step.argtypes = [C.c_int64, C.c_int, _dp, _dp, C.POINTER(Phase), _dp, _dp]
@@ -153,6 +154,11 @@ def gemm(X, Y) -> np.ndarray:
 def gemm_rows(X, Y, Z, r0: int, r1: int) -> None:
     """Rows [r0, r1) of Z = X Y in place (bounded timing sample; same loops as gemm)."""
     lib().orc_gemm_rows(X.shape[0], r0, r1, _p(X), _p(Y), _p(Z))
+
+
+def gemm_cols(X, Y, Z, c0: int, c1: int) -> None:
+    """Columns [c0, c1) of Z = X Y in place (same per-element k order as gemm)."""
+    lib().orc_gemm_cols(X.shape[0], c0, c1, _p(X), _p(Y), _p(Z))
 
 
 def matvec(X, v) -> np.ndarray:

@@ -134,6 +134,20 @@ void orc_gemm_rows(int64_t n, int64_t r0, int64_t r1, const double *X, const dou
   }
 }
 
+/* Columns [c0, c1) of Z = X Y (same per-element k order as orc_gemm; column-panel tests). */
+void orc_gemm_cols(int64_t n, int64_t c0, int64_t c1, const double *X, const double *Y, double *Z) {
+  #pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i) {
+    double *z = Z + i * n;
+    for (int64_t j = c0; j < c1; ++j) z[j] = 0.0;
+    for (int64_t k = 0; k < n; ++k) {
+      const double x = X[i * n + k];
+      const double *y = Y + k * n;
+      for (int64_t j = c0; j < c1; ++j) z[j] += x * y[j];
+    }
+  }
+}
+
 /* Z = X Y: the matrix product of Eq. (1), written as the textbook triple loop. */
 void orc_gemm(int64_t n, const double *X, const double *Y, double *Z) {
   #pragma omp parallel for schedule(static)

@@ -52,6 +52,8 @@ int orc_is_symmetric(int64_t n, const double *A);
 
 /* Z = X * Y (all n x n row-major), i-k-j loops, FP64 accumulator, no FMA. */
 void orc_gemm(int64_t n, const double *X, const double *Y, double *Z);
+/* Columns [c0, c1) of Z = X Y, same per-element k order (column-panel decomposition tests). */
+void orc_gemm_cols(int64_t n, int64_t c0, int64_t c1, const double *X, const double *Y, double *Z);
 /* Rows [r0, r1) of Z = X Y, same loops (bounded timing sample for the CPU baseline). */
 void orc_gemm_rows(int64_t n, int64_t r0, int64_t r1, const double *X, const double *Y, double *Z);
 /* y = X v (row-major), sequential sums. */

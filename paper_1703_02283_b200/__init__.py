@@ -31,7 +31,7 @@ OUTCOME_NAMES = {0: "running", 1: "converged", 2: "iter_limit", 3: "diverged", 4
 EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_get_trace",
             "ipr_get_iterate", "ipr_get_norms", "ipr_finalize", "ipr_last_error",
             "ipr_nccl_unique_id", "ipr_version", "ipr_test_quantize", "ipr_test_gemm",
-            "ipr_launch_count"]
+            "ipr_launch_count", "ipr_plan"]
 
 
 class IprError(RuntimeError):
@@ -73,6 +73,7 @@ def _load():
     L.ipr_test_quantize.argtypes = [C.c_int, vp, vp, i64, C.c_int, C.c_int, C.c_int, vp]
     L.ipr_test_gemm.argtypes = [C.c_int, i64, vp, vp, vp, vp]
     L.ipr_launch_count.restype = C.c_int64
+    L.ipr_plan.argtypes = [i64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)]
     for f in EXPORTED:
         if f not in ("ipr_last_error", "ipr_version", "ipr_launch_count"):
             getattr(L, f).restype = C.c_int
@@ -193,6 +194,14 @@ def ipr_test_gemm(prec: int, n: int, X, Yt, Z, stream=None):
 
 def ipr_launch_count() -> int:
     return _lib.ipr_launch_count()
+
+
+def ipr_plan(n: int, world: int, rank: int, prec: int = IPR_FP64) -> dict:
+    """Host-side layout plan of the 1 x world column-panel decomposition (no GPU needed)."""
+    out = (C.c_int64 * 8)()
+    _check(_lib.ipr_plan(n, world, rank, prec, out))
+    keys = ["npad", "kp", "col0", "tile_m", "tile_n", "tiles_m", "tiles_n_total", "part0"]
+    return dict(zip(keys, list(out)))
 
 
 # ---- convenience wrapper (still marshalling only) -------------------------------------------

@@ -106,6 +106,12 @@ ipr_status fail(ipr_ctx *c, ipr_status s, const char *fmt, ...) {
   } while (0)
 
 int native_m(int prec) { return prec == IPR_FP64 ? 52 : prec == IPR_BF16 ? 7 : 10; }
+
+// padded order: whole 256-wide tiles per rank (tcgen05 tile N), zero padding
+int64_t padded_order(int64_t n, int world) {
+  const int64_t unit = 256 * (int64_t)world;
+  return (n + unit - 1) / unit * unit;
+}
 int operand_bits(int prec) { return native_m(prec); }
 
 template <typename T>
@@ -397,9 +403,7 @@ ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, 
   c = new ipr_ctx();
   c->n = n; c->lda = lda; c->A = A_dev; c->world = world; c->rank = rank;
   c->st = (cudaStream_t)cuda_stream;
-  // padded order: whole 256-wide tiles per rank (tcgen05 tile N), zero padding
-  const int64_t unit = 256 * (int64_t)world;
-  c->npad = (n + unit - 1) / unit * unit;
+  c->npad = padded_order(n, world);
   c->kp = c->npad / world;
   c->col0 = (int64_t)rank * c->kp;
   ipr_status s;
@@ -634,6 +638,17 @@ ipr_status ipr_finalize(ipr_ctx *c, double *C_dev_out, int64_t ldc) {
 
 // ---- test hooks (include/ipr_testing.h) ----
 int64_t ipr_launch_count(void) { return g_launches; }
+
+ipr_status ipr_plan(int64_t n, int world, int rank, int prec, int64_t *out8) {
+  ipr_ctx *c = nullptr;
+  if (n <= 0 || world < 1 || rank < 0 || rank >= world || prec < 0 || prec > 3 || !out8)
+    return fail(c, IPR_E_INVALID_ARG, "ipr_plan: bad arguments");
+  const int64_t npad = padded_order(n, world), kp = npad / world, col0 = (int64_t)rank * kp;
+  const int64_t tm = gemm_tile_m(prec), tn = gemm_tile_n(prec);
+  out8[0] = npad; out8[1] = kp; out8[2] = col0; out8[3] = tm; out8[4] = tn;
+  out8[5] = npad / tm; out8[6] = npad / tn; out8[7] = (col0 / tn) * (npad / tm);
+  return IPR_OK;
+}
 
 ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_t len, int m, int round, int sigma,
                              void *stream) {

@@ -1,0 +1,162 @@
+"""World-size-2 CPU test (gloo) of the multi-GPU decomposition.
+
+The CUDA engine shards every GEMM of the chain by output columns (rank g owns S_g), keeps Chat
+replicated through an all-gather of per-rank panels, and reduces per-tile residual / delta
+partials from GLOBAL slots.  This test drives that exact data flow on the CPU: the layout plan
+comes from libipr's own host code (ipr_plan, no GPU needed), products are the oracle's column-
+panel GEMM (same per-element k order as the full product), panels and partials travel through
+torch.distributed all_gather over gloo.  It checks that
+  * the ranks' plans tile the padded columns and the partial slots exactly once,
+  * every iterate assembled from the 2 ranks' panels is bit-identical to the single-process
+    oracle trajectory (Eq. 1), and
+  * rho reduced in slot order is bit-identical for world = 1 and world = 2.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def emulate(A, p, iters, world, rank, m=52, gather=None):
+    """Column-panel iteration in the library's layout; returns ([C_k], [rho_k])."""
+    import paper_1703_02283_b200 as ipr
+    n = A.shape[0]
+    plan = ipr.ipr_plan(n, world, rank, ipr.IPR_FP64)
+    npad, kp, col0 = plan["npad"], plan["kp"], plan["col0"]
+    tm, tn, tiles_m, tiles_n = plan["tile_m"], plan["tile_n"], plan["tiles_m"], plan["tiles_n_total"]
+    Ap = np.zeros((npad, npad)); Ap[:n, :n] = A
+    n1, ninf, _ = oracle.norms(A)
+    s = n1 * ninf
+    ph = oracle.phase(oracle.FP64, mant_bits=m)
+    cols = slice(col0, col0 + kp)
+
+    def allgather_panels(panel):          # [npad][kp] local panel -> full row-major Chat
+        if gather is None:
+            return panel.copy()
+        parts = gather(panel)
+        return np.concatenate(parts, axis=1)
+
+    def allgather_partials(local):        # local slots -> global slot array
+        if gather is None:
+            return local
+        return np.concatenate(gather(local))
+
+    C_panel = oracle.c0(Ap, s, ph)[:, cols]        # C_0 of the padded matrix, local panel
+    hist, rhos = [], []
+    for k in range(iters):
+        C = allgather_panels(C_panel)              # replicated Chat (FP64 phase: = container)
+        hist.append(C[:n, :n].copy())
+        X = Ap
+        T = np.zeros((npad, npad))
+        for j in range(p):
+            T = np.zeros((npad, npad))
+            oracle.gemm_cols(C, X, T, col0, col0 + kp)
+            X = T
+        # per-tile residual partials in global slots [tn_global][tm]
+        I = np.eye(npad)[:, cols]
+        D = (I - T[:, cols])
+        D[n:, :] = 0.0
+        if col0 + kp > n:
+            D[:, max(0, n - col0):] = 0.0
+        local = np.zeros((kp // tn) * tiles_m)
+        for a in range(kp // tn):
+            for b in range(tiles_m):
+                blk = D[b * tm:(b + 1) * tm, a * tn:(a + 1) * tn]
+                local[a * tiles_m + b] = np.sum(blk * blk)
+        part = allgather_partials(local)
+        assert part.size == tiles_m * tiles_n
+        rho = 0.0
+        for v in part:
+            rho += v
+        rhos.append(np.sqrt(rho))
+        P = np.zeros((npad, npad))
+        oracle.gemm_cols(C, T, P, col0, col0 + kp)
+        a_ = float(p + 1) * C_panel
+        d_ = a_ - P[:, cols]
+        e_ = d_ / float(p)
+        C_panel = oracle.qm(e_, 11, m)
+    return hist, rhos
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1703_02283_b200 as ipr
+        A = synth.spd(300, 2.0, 21)
+
+        def gather(arr):
+            t = torch.from_numpy(np.ascontiguousarray(arr))
+            out = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(out, t)
+            return [o.numpy() for o in out]
+
+        plans = [None] * world
+        dist.all_gather_object(plans, ipr.ipr_plan(300, world, rank, ipr.IPR_FP64))
+        hist, rhos = emulate(A, 2, 6, world, rank, gather=gather)
+        if rank == 0:
+            q.put(("ok", plans, hist, rhos))
+    except Exception as e:  # surface the failure to the parent
+        if rank == 0:
+            q.put(("err", repr(e), None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_plan_covers_columns_and_slots():
+    import paper_1703_02283_b200 as ipr
+    for n in [64, 300, 1024, 8192, 32768]:
+        for world in [1, 2, 4, 8]:
+            for prec in [ipr.IPR_FP64, ipr.IPR_BF16]:
+                plans = [ipr.ipr_plan(n, world, r, prec) for r in range(world)]
+                npad = plans[0]["npad"]
+                assert npad >= n and npad % (256 * world) == 0
+                cols = np.zeros(npad, int)
+                for pl in plans:
+                    assert pl["npad"] == npad and pl["kp"] * world == npad
+                    cols[pl["col0"]:pl["col0"] + pl["kp"]] += 1
+                    assert pl["kp"] % pl["tile_n"] == 0
+                assert np.all(cols == 1)
+                slots = [pl["part0"] for pl in plans] + [pl["tiles_m"] * pl["tiles_n_total"] for pl in plans[:1]]
+                per = plans[0]["kp"] // plans[0]["tile_n"] * plans[0]["tiles_m"]
+                assert all(slots[r] == r * per for r in range(world))
+    assert ipr.ipr_plan(32768, 8, 7, ipr.IPR_BF16)["kp"] == 4096
+
+
+def test_world2_gloo_matches_single_rank_and_oracle():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    status, plans, hist2, rhos2 = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=300)
+    assert status == "ok", plans
+    assert all(pr.exitcode == 0 for pr in procs)
+    assert plans[0]["col0"] == 0 and plans[1]["col0"] == plans[0]["kp"]
+    A = synth.spd(300, 2.0, 21)
+    hist1, rhos1 = emulate(A, 2, 6, 1, 0)
+    r = oracle.solve(A, 2, [oracle.phase()], 0.0, 6, hist=6)
+    for k in range(6):
+        np.testing.assert_array_equal(hist2[k], hist1[k])
+        np.testing.assert_array_equal(hist2[k], r.C_hist[k])
+    assert rhos2 == rhos1                     # bit-identical slot-ordered reduction
+    np.testing.assert_allclose(rhos1, r.rho, rtol=1e-13)

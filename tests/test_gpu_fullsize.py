@@ -1,0 +1,143 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+The oracle cannot run whole trajectories at n = 8192 in test time, so (Level 1):
+  * Freivalds-style one-step probe: for random +-1 vectors v, the GPU's step
+    C_k -> C_{k+1} must satisfy  |C_{k+1} v - ((p+1) C_k v - Chat^{p+1} Ahat v)/p|  <=
+    2^-m |C_{k+1}||v| + ((p+1)/p)(n u_acc + (p+1) u_in) |Chat|^{p+1}|Ahat||v|  elementwise,
+    evaluated right-to-left with the oracle's matvec (O(n^2) per vector);
+  * sampled outputs: whole rows of C_{k+1} recomputed one by one by the oracle from C_k
+    (row_i(Chat) Chat ... Ahat with vector-matrix products), within the same bound;
+  * the headline twin reaches rho <= 1e-12 (certified in FP64) and the answer satisfies the
+    defining property C^p A = I in the Freivalds sense.
+Plus config C2 (n=1024, kappa=1e3, p=1) as a Level-3 trajectory case."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+ipr = pytest.importorskip("paper_1703_02283_b200")
+
+OPR = {"fp64": oracle.FP64, "tf32": oracle.TF32, "bf16": oracle.BF16, "fp16": oracle.FP16}
+
+
+@pytest.fixture(scope="module")
+def twin():
+    c = synth.CONFIGS["H_twin"]
+    A, _ = synth.spd_torch(c["n"], c["kappa"], c["seed"], device="cuda")
+    return A, A.cpu().numpy()
+
+
+def _qin(X, prec):
+    if prec == "fp64":
+        return X
+    E, M = oracle.prec_format(OPR[prec])
+    if prec == "fp16":
+        sig = oracle.fp16_sigma(float(np.max(np.abs(X))))
+        return oracle.qm(X * 2.0 ** sig, E, M) / 2.0 ** sig
+    return oracle.qm(X, E, M)
+
+
+def _step_bound_check(A, Ck, Ck1, p, prec, m, nvec=2):
+    n = A.shape[0]
+    Ec = 11 if prec == "fp64" else 8
+    Ahat = _qin(oracle.qm(A, Ec, m), prec)
+    Chat = _qin(Ck, prec)
+    aC, aA = np.abs(Chat), np.abs(Ahat)
+    aC1 = np.abs(Ck1)
+    u_acc = 2.0 ** -53 if prec == "fp64" else 2.0 ** -24
+    u_in = 0.0 if prec == "fp64" else 2.0 ** -(oracle.prec_format(OPR[prec])[1] + 1)
+    worst = 0.0
+    for v in synth.probe_vectors(n, nvec, 3):
+        w = oracle.matvec(Ahat, v)
+        aw = oracle.matvec(aA, np.abs(v))
+        for _ in range(p + 1):
+            w = oracle.matvec(Chat, w)
+            aw = oracle.matvec(aC, aw)
+        ref = ((p + 1) * oracle.matvec(Ck, v) - w) / p
+        got = oracle.matvec(Ck1, v)
+        b = 2.0 ** -m * oracle.matvec(aC1, np.abs(v)) + (p + 1) / p * (n * u_acc + (p + 1) * u_in) * aw
+        r = np.abs(got - ref) / (b + 1e-300)
+        worst = max(worst, float(np.max(r)))
+        assert np.all(np.abs(got - ref) <= b), float(np.max(r))
+    return worst
+
+
+def _sampled_rows(A, Ck, Ck1, p, prec, m, rows):
+    Ec = 11 if prec == "fp64" else 8
+    Ahat = _qin(oracle.qm(A, Ec, m), prec)
+    Chat = _qin(Ck, prec)
+    ChatT, AhatT = np.ascontiguousarray(Chat.T), np.ascontiguousarray(Ahat.T)
+    aCT, aAT = np.abs(ChatT), np.abs(AhatT)
+    n = A.shape[0]
+    u_acc = 2.0 ** -53 if prec == "fp64" else 2.0 ** -24
+    u_in = 0.0 if prec == "fp64" else 2.0 ** -(oracle.prec_format(OPR[prec])[1] + 1)
+    for i in rows:
+        r = Chat[i].copy()                 # row i of P = Chat^{p+1} Ahat, one vector-matrix at a time
+        ar = np.abs(r)
+        for _ in range(p):
+            r = oracle.matvec(ChatT, r)
+            ar = oracle.matvec(aCT, ar)
+        r = oracle.matvec(AhatT, r)
+        ar = oracle.matvec(aAT, ar)
+        ref = ((p + 1) * Ck[i] - r) / p
+        b = 2.0 ** -m * np.abs(Ck1[i]) + (p + 1) / p * (n * u_acc + (p + 1) * u_in) * ar
+        assert np.all(np.abs(Ck1[i] - ref) <= b), i
+
+
+@pytest.mark.parametrize("prec", ["fp64", "bf16", "tf32", "fp16"])
+def test_headline_one_step_parity(twin, prec):
+    A, A_np = twin
+    p, k = 2, 3
+    m = {"fp64": 52, "bf16": 7, "tf32": 10, "fp16": 10}[prec]
+    phases = [ipr.make_phase(prec, max_iters=50)] + ([ipr.make_phase("fp64")] if prec != "fp64" else [])
+    s = ipr.Solver(A, p, phases, 1e-12)
+    assert s.iterate(k) == ipr.IPR_RUNNING
+    Ck = s.iterate_copy(0).cpu().numpy()
+    assert s.iterate(1) == ipr.IPR_RUNNING
+    Ck1 = s.iterate_copy(0).cpu().numpy()
+    s.close()
+    _step_bound_check(A_np, Ck, Ck1, p, prec, m)
+    _sampled_rows(A_np, Ck, Ck1, p, prec, m, rows=[0, 4097, 8191])
+
+
+def test_headline_twin_converges_and_certifies(twin):
+    A, A_np = twin
+    s = ipr.Solver(A, 2, [ipr.make_phase("fp64")], 1e-12)
+    assert s.iterate(100) == ipr.IPR_CONVERGED
+    tr = s.trace()
+    assert tr[-1]["rho"] <= 1e-12 and 15 <= len(tr) <= 30
+    rc = s.residual(True)
+    assert rc <= 2e-12
+    C = s.finalize().cpu().numpy()
+    # defining property: C^2 A v = v for probe vectors
+    for v in synth.probe_vectors(A_np.shape[0], 2, 4):
+        w = oracle.matvec(C, oracle.matvec(C, oracle.matvec(A_np, v)))
+        assert np.linalg.norm(w - v) / np.linalg.norm(v) < 1e-12
+
+
+def test_config_c2_level3():
+    # n=1024, kappa=1e3, p=1 (Newton-Schulz form of Eq. 1), FP64 and TF32 -> FP64: the literal
+    # iteration is unstable at this kappa: compare envelopes after gamma onset.
+    c = synth.CONFIGS["C2"]
+    A, lam, _ = synth.spd(c["n"], c["kappa"], c["seed"], return_eig=True)
+    for pg, po in [([ipr.make_phase("fp64", max_iters=60)], [oracle.phase(max_iters=60)]),
+                   ([ipr.make_phase("tf32", switch_tol=1e-3, plateau_ratio=0.7, plateau_arm=0.5, max_iters=40),
+                     ipr.make_phase("fp64", max_iters=60)],
+                    [oracle.phase(oracle.TF32, switch_tol=1e-3, plateau_ratio=0.7, plateau_arm=0.5, max_iters=40),
+                     oracle.phase(max_iters=60)])]:
+        r = oracle.solve(A, 1, po, 1e-12, 120, gamma_normA2=float(lam.max()))
+        s = ipr.Solver(torch.from_numpy(A).cuda(), 1, pg, 1e-12)
+        s.iterate(120)
+        tr = s.trace()
+        out = s.outcome
+        s.close()
+        rg = np.array([t["rho"] for t in tr])
+        ro = r.rho
+        fin_g, fin_o = rg[np.isfinite(rg)], ro[np.isfinite(ro)]
+        assert abs(int(np.nanargmin(rg)) - int(np.nanargmin(ro))) <= 1
+        assert fin_o.min() / 4 <= fin_g.min() <= 4 * fin_o.min()
+        assert {out, r.outcome} <= {ipr.IPR_DIVERGED, ipr.IPR_NONFINITE, ipr.IPR_ITER_LIMIT, ipr.IPR_CONVERGED}
+        assert (out == ipr.IPR_CONVERGED) == (r.outcome == oracle.CONVERGED)
