@@ -21,6 +21,7 @@
 namespace ipr {
 
 constexpr int DM_BM = 128, DM_BN = 64, DM_BK = 16, DM_ST = 4, DM_NT = 128;
+constexpr int DM_GROUP_M = 16;
 constexpr int DM_STAGE_DBL = DM_BM * DM_BK + DM_BN * DM_BK;     // doubles per stage
 constexpr int DM_SMEM = DM_ST * DM_STAGE_DBL * 8;               // 98304 bytes
 
@@ -44,7 +45,19 @@ __global__ void __launch_bounds__(DM_NT, 2) k_gemm_dmma(const GemmArgs g) {
   extern __shared__ __align__(128) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;              // 2 x 2 warps
-  const int64_t m0 = (int64_t)blockIdx.y * DM_BM, n0 = (int64_t)blockIdx.x * DM_BN;
+  // grouped raster: consecutive CTAs sweep DM_GROUP_M tile-rows x all tile-columns, so the A and B
+  // K-slices a wave touches are shared across many CTAs through L2 (DRAM re-reads / 3 vs row-major)
+  int tm, tn;
+  {
+    const int tiles_m = (int)(g.M / DM_BM), tiles_n = (int)(g.N / DM_BN);
+    const int per_group = DM_GROUP_M * tiles_n, bid = blockIdx.x;
+    const int gidx = bid / per_group, first_m = gidx * DM_GROUP_M;
+    const int gm = min(tiles_m - first_m, DM_GROUP_M);
+    const int r = bid - gidx * per_group;
+    tm = first_m + r % gm;
+    tn = r / gm;
+  }
+  const int64_t m0 = (int64_t)tm * DM_BM, n0 = (int64_t)tn * DM_BN;
   const double *A = (const double *)g.A, *B = (const double *)g.B;
   const int nkb = (int)(g.K / DM_BK);
   const int kb_per_panel = (int)(g.a_kp / DM_BK);
@@ -133,7 +146,7 @@ __global__ void __launch_bounds__(DM_NT, 2) k_gemm_dmma(const GemmArgs g) {
       }
   __shared__ double red[DM_NT / 32];
   __shared__ float redf[DM_NT / 32];
-  const int64_t tile = ((g.col0 + n0) / DM_BN) * g.tiles_m + blockIdx.y;
+  const int64_t tile = ((g.col0 + n0) / DM_BN) * g.tiles_m + tm;
   if (g.mode & (EPI_RESID | EPI_UPDATE)) {
     const double s = block_sum_det<DM_NT>((g.mode & EPI_RESID) ? ea.r2 : ea.d2, red);
     if (tid == 0) g.part[tile] = s;
@@ -152,7 +165,7 @@ cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s) {
     attr = true;
   }
   if (a.M % DM_BM || a.N % DM_BN || a.K % DM_BK || a.a_kp % DM_BK) return cudaErrorInvalidValue;
-  dim3 grid((unsigned)(a.N / DM_BN), (unsigned)(a.M / DM_BM));
+  dim3 grid((unsigned)((a.N / DM_BN) * (a.M / DM_BM)));
   k_gemm_dmma<<<grid, DM_NT, DM_SMEM, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
