@@ -79,6 +79,11 @@ def lib():
         L.orc_solve.argtypes = [C.c_int64, C.c_int, _dp, C.POINTER(Phase), C.c_int, C.c_double,
                                 C.c_int, C.POINTER(Record), C.c_int, C.POINTER(C.c_int), _dp,
                                 _dp, C.c_int, C.c_double, _dp]
+        L.orc_solve_form.argtypes = [C.c_int64, C.c_int, C.c_int, _dp, C.POINTER(Phase), C.c_int,
+                                     C.c_double, C.c_int, C.POINTER(Record), C.c_int,
+                                     C.POINTER(C.c_int), _dp, _dp, C.c_int, C.c_double, _dp]
+        L.orc_step_ns.restype = C.c_double
+        L.orc_step_ns.argtypes = [C.c_int64, _dp, _dp, C.POINTER(Phase), _dp, _dp]
         L.orc_jacobi.argtypes = [C.c_int64, _dp, _dp, _dp]
         L.orc_inv_proot_eig.argtypes = [C.c_int64, _dp, _dp, C.c_int, _dp]
         L.orc_spectral.argtypes = [C.c_int64, _dp, C.c_int, C.c_double, C.c_int, _dp]
@@ -198,9 +203,23 @@ class SolveResult:
         return np.array([r["rho"] for r in self.records])
 
 
+def step_ns(A, Xk, ph: Phase, want_next: bool = True):
+    """One Newton-Schulz step X (2I - A X) (NEXT-1): returns (rho(X_k), X_{k+1}, delta)."""
+    A, Xk = _f64(A), _f64(Xk)
+    nxt = np.empty_like(Xk) if want_next else None
+    d = C.c_double(np.nan)
+    rho = lib().orc_step_ns(A.shape[0], _p(A), _p(Xk), C.byref(ph),
+                            _p(nxt) if want_next else None, C.byref(d))
+    return rho, nxt, d.value
+
+
+FORM_LITERAL, FORM_NEWTON_SCHULZ = 0, 1
+
+
 def solve(A, p: int, phases, final_tol: float = 1e-12, max_total: int = 200,
-          hist: int = 0, gamma_normA2: float = 0.0) -> SolveResult:
-    """Full controller-driven solve (init + iterations), reading R-5 of DESIGN.md."""
+          hist: int = 0, gamma_normA2: float = 0.0, form: int = FORM_LITERAL) -> SolveResult:
+    """Full controller-driven solve (init + iterations), reading R-5 of DESIGN.md.
+    form = FORM_LITERAL (Eq. 1 as printed) or FORM_NEWTON_SCHULZ (p = 1, X(2I - AX))."""
     A = _f64(A)
     n = A.shape[0]
     arr = (Phase * len(phases))(*phases)
@@ -209,9 +228,9 @@ def solve(A, p: int, phases, final_tol: float = 1e-12, max_total: int = 200,
     best = np.empty_like(A)
     H = np.empty((hist, n, n)) if hist > 0 else None
     s = C.c_double(0)
-    out = lib().orc_solve(n, p, _p(A), arr, len(phases), final_tol, max_total, recs, max_total,
-                          C.byref(nrec), _p(best), _p(H) if H is not None else None, hist,
-                          gamma_normA2, C.byref(s))
+    out = lib().orc_solve_form(n, p, form, _p(A), arr, len(phases), final_tol, max_total, recs,
+                               max_total, C.byref(nrec), _p(best),
+                               _p(H) if H is not None else None, hist, gamma_normA2, C.byref(s))
     if out < 0:
         raise ValueError({-1: "invalid argument", -2: "A is not exactly symmetric"}[out])
     records = [dict(k=r.k, phase=r.phase, prec=r.prec, mant_bits=r.mant_bits,

@@ -282,6 +282,49 @@ static double update(int64_t n, int p, const double *C, const orc_phase *ph, cha
   return sqrt(s2);
 }
 
+/* ---------------------------------------------------------------------------------
+ * NEXT-1: the Newton-Schulz ordering of the p = 1 iteration.
+ * [Sec. 2]: "For p=1 the algorithm corresponds to the well-known Newton-Schulz method"; the
+ * textbook Newton-Schulz step is X_{k+1} = X_k (2I - A X_k):
+ *   Xhat = qin(X), Ahat = qin(q_m(A)), T = Ahat Xhat (FP64 accumulator),
+ *   rho = ||I - T||_F (unrounded T), What = qin(2I - T) (one FP64 subtraction per element),
+ *   X_{k+1} = q_m(Xhat What)  (FP64 accumulator, one rounding to m bits).
+ * ------------------------------------------------------------------------------ */
+static double chain_ns(int64_t n, const double *A, const double *X, const orc_phase *ph, chain_ws *w) {
+  const int64_t nn = n * n;
+  for (int64_t i = 0; i < nn; ++i) w->T[i] = store_q(ph, A[i]);
+  const int sigA = qin_matrix(ph->prec, nn, w->T, w->X);   /* w->X = Ahat (scratch) */
+  w->sigC = qin_matrix(ph->prec, nn, X, w->Chat);           /* w->Chat = Xhat        */
+  orc_gemm(n, w->X, w->Chat, w->T);                         /* T = Ahat Xhat         */
+  if (sigA + w->sigC != 0)
+    for (int64_t i = 0; i < nn; ++i) w->T[i] = ldexp(w->T[i], -(sigA + w->sigC));
+  double s2 = 0.0;
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t c = 0; c < n; ++c) {
+      const double d = (r == c ? 1.0 : 0.0) - w->T[r * n + c];
+      s2 += d * d;
+    }
+  for (int64_t r = 0; r < n; ++r)                           /* W = 2I - T            */
+    for (int64_t c = 0; c < n; ++c) w->T[r * n + c] = (r == c ? 2.0 : 0.0) - w->T[r * n + c];
+  w->sigX = qin_matrix(ph->prec, nn, w->T, w->X);           /* w->X = What           */
+  return sqrt(s2);
+}
+
+static double update_ns(int64_t n, const double *X, const orc_phase *ph, chain_ws *w, double *X_next) {
+  const int64_t nn = n * n;
+  orc_gemm(n, w->Chat, w->X, w->T);                         /* Xhat What             */
+  if (w->sigC + w->sigX != 0)
+    for (int64_t i = 0; i < nn; ++i) w->T[i] = ldexp(w->T[i], -(w->sigC + w->sigX));
+  double s2 = 0.0;
+  for (int64_t i = 0; i < nn; ++i) {
+    const double x1 = store_q(ph, w->T[i]);
+    const double dd = x1 - X[i];
+    s2 += dd * dd;
+    X_next[i] = x1;
+  }
+  return sqrt(s2);
+}
+
 static int ws_alloc(chain_ws *w, int64_t n) {
   const size_t b = (size_t)(n * n) * sizeof(double);
   w->n = n;
@@ -318,12 +361,31 @@ static void recontainer(int64_t nn, const double *src, const orc_phase *ph, doub
   for (int64_t i = 0; i < nn; ++i) dst[i] = store_q(ph, src[i]);
 }
 
+double orc_step_ns(int64_t n, const double *A, const double *X, const orc_phase *ph,
+                   double *X_next, double *delta) {
+  chain_ws w;
+  if (!ws_alloc(&w, n)) { ws_free(&w); return NAN; }
+  const double rho = chain_ns(n, A, X, ph, &w);
+  if (X_next) { const double d = update_ns(n, X, ph, &w, X_next); if (delta) *delta = d; }
+  ws_free(&w);
+  return rho;
+}
+
 int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int nphases,
               double final_tol, int max_total, orc_record *rec, int cap_rec, int *nrec,
               double *C_best, double *C_hist, int hist_cap, double gamma_normA2,
               double *s_out) {
+  return orc_solve_form(n, p, ORC_FORM_LITERAL, A, phases, nphases, final_tol, max_total, rec,
+                        cap_rec, nrec, C_best, C_hist, hist_cap, gamma_normA2, s_out);
+}
+
+int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase *phases,
+                   int nphases, double final_tol, int max_total, orc_record *rec, int cap_rec,
+                   int *nrec, double *C_best, double *C_hist, int hist_cap, double gamma_normA2,
+                   double *s_out) {
   *nrec = 0;
   if (n <= 0 || p < 1 || nphases < 1) return -1;
+  if (form == ORC_FORM_NEWTON_SCHULZ && p != 1) return -1;
   if (!orc_is_symmetric(n, A)) return -2;
   const int64_t nn = n * n;
   double nrm[3];
@@ -347,7 +409,7 @@ int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int np
   for (int k = 0; k < max_total; ++k) {
     const orc_phase *ph = &phases[ctl.phase];
     if (C_hist && k < hist_cap) memcpy(C_hist + (int64_t)k * nn, C, (size_t)nn * sizeof(double));
-    const double rho = chain(n, p, A, C, ph, &w);
+    const double rho = form == ORC_FORM_NEWTON_SCHULZ ? chain_ns(n, A, C, ph, &w) : chain(n, p, A, C, ph, &w);
     const int phase_now = ctl.phase;
     const int d = orc_ctrl_decide(&ctl, ph, rho);
     if (ctl.best_is_new) memcpy(C_best, C, (size_t)nn * sizeof(double));
@@ -356,7 +418,7 @@ int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int np
     r.decision = d; r.rho = rho; r.rho_hat = rho / sqrt((double)n); r.delta = NAN;
     r.gamma = (gamma_normA2 > 0) ? gamma_of(n, C, A, gamma_normA2, g1, g2) : NAN;
     if (d == ORC_CONTINUE) {
-      r.delta = update(n, p, C, ph, &w, Cn);
+      r.delta = form == ORC_FORM_NEWTON_SCHULZ ? update_ns(n, C, ph, &w, Cn) : update(n, p, C, ph, &w, Cn);
       double *t = C; C = Cn; Cn = t;
     } else if (d == ORC_SWITCH) {
       orc_ctrl_enter_next_phase(&ctl);

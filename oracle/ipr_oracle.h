@@ -106,6 +106,17 @@ int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int np
               double *C_best, double *C_hist, int hist_cap, double gamma_normA2,
               double *s_out);
 
+/* Iteration forms: ORC_FORM_LITERAL = Eq. (1) as printed (right-to-left chain, reading R-1);
+ * ORC_FORM_NEWTON_SCHULZ = p = 1 only, X_{k+1} = X_k (2I - A X_k) (NEXT-1). */
+enum { ORC_FORM_LITERAL = 0, ORC_FORM_NEWTON_SCHULZ = 1 };
+int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase *phases,
+                   int nphases, double final_tol, int max_total, orc_record *rec, int cap_rec,
+                   int *nrec, double *C_best, double *C_hist, int hist_cap, double gamma_normA2,
+                   double *s_out);
+/* One Newton-Schulz step from X: returns rho(X) = ||I - Ahat Xhat||_F; X_next may be NULL. */
+double orc_step_ns(int64_t n, const double *A, const double *X, const orc_phase *ph,
+                   double *X_next, double *delta);
+
 /* Cyclic Jacobi eigen-decomposition of a symmetric matrix (n small).
  * lambda ascending, V columns = eigenvectors (row-major n x n).  Returns sweeps used. */
 int orc_jacobi(int64_t n, const double *A, double *lambda, double *V);

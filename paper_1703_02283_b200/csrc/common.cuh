@@ -22,6 +22,8 @@ enum EpiMode : int {
   EPI_UPDATE = 4,     // C_next = q_m(((p+1) C - scale*D) / p), Chat_next, delta partials
   EPI_F64 = 8,        // test hook: FP64 row-major store of scale*D
   EPI_TSCRATCH = 16,  // FP16 phase: FP32 store of scale*D transposed + per-tile max|.|
+  EPI_TWO_I_MINUS = 32,  // modifier of STORE_T/TSCRATCH: store 2*delta_ij - D (Newton-Schulz W)
+  EPI_NSUPDATE = 64,  // Newton-Schulz: X_{k+1} = q_m(D) -> container, operand, delta partials
 };
 
 struct GemmArgs {

@@ -26,16 +26,43 @@ struct EpiAcc {
 
 // v: accumulator value converted to FP64 (exact) and scaled (exact power of two).
 // row: global row; col: local column (global = col0 + col).
+// MODE >= 0: the epilogue mode is a compile-time constant (specialised kernels); -1: g.mode.
+template <int MODE = -1>
 __device__ __forceinline__ void epi_element(const GemmArgs &g, int64_t row, int64_t col,
                                             double v, EpiAcc &acc) {
-  const int mode = g.mode;
-  if (mode & EPI_STORE_T) {
-    const int sig = 0;  // FP16 T operands go through EPI_TSCRATCH + a scale kernel
-    store_operand(g.tout, col * g.ldt + row, g.prec, v, sig);
+  const int mode = MODE >= 0 ? MODE : g.mode;
+  if (mode & (EPI_STORE_T | EPI_TSCRATCH)) {
+    double w = v;
+    if (mode & EPI_TWO_I_MINUS) {     // Newton-Schulz W = 2I - A X (one FP64 subtraction)
+      const int64_t gc = g.col0 + col;
+      w = __dsub_rn((row == gc && row < g.n) ? 2.0 : 0.0, v);
+    }
+    if (mode & EPI_STORE_T) {
+      // FP16 T operands go through EPI_TSCRATCH + a scale kernel (sigma 0 here)
+      store_operand(g.tout, col * g.ldt + row, g.prec, w, 0);
+    } else {
+      ((float *)g.tout)[col * g.ldt + row] = (float)w;
+      acc.mx = fmaxf(acc.mx, fabsf((float)w));
+    }
   }
-  if (mode & EPI_TSCRATCH) {
-    ((float *)g.tout)[col * g.ldt + row] = (float)v;
-    acc.mx = fmaxf(acc.mx, fabsf((float)v));
+  if (mode & EPI_NSUPDATE) {          // X_{k+1} = q_m(Xhat What): one rounding to m bits
+    const int64_t ci = row * g.ldc + col;
+    const double c = g.cont64 ? ((const double *)g.cold)[ci] : (double)((const float *)g.cold)[ci];
+    double cn;
+    if (g.cont64) {
+      cn = q_e11(v, g.m, g.rtz);
+      ((double *)g.cnew)[ci] = cn;
+    } else {
+      const float f = q_e8(v, g.m, g.rtz);
+      ((float *)g.cnew)[ci] = f;
+      cn = (double)f;
+    }
+    if (g.chat_new) {
+      if (g.prec == P_FP16) acc.mx = fmaxf(acc.mx, fabsf((float)cn));
+      else store_operand(g.chat_new, row * g.ldh + col, g.prec, cn, 0);
+    }
+    const double dd = __dsub_rn(cn, c);
+    acc.d2 = __fma_rn(dd, dd, acc.d2);
   }
   if (mode & EPI_RESID) {
     const int64_t gc = g.col0 + col;

@@ -41,6 +41,7 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(DM_NT, 2) k_gemm_dmma(const GemmArgs g) {
   extern __shared__ __align__(128) double smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -142,13 +143,14 @@ __global__ void __launch_bounds__(DM_NT, 2) k_gemm_dmma(const GemmArgs g) {
       for (int e = 0; e < 2; ++e) {
         const int64_t row = m0 + wm * 64 + mi * 8 + fr;
         const int64_t col = n0 + wn * 32 + ni * 8 + fk * 2 + e;
-        epi_element(g, row, col, __dmul_rn(acc[mi][ni][e], scale), ea);
+        epi_element<MODE>(g, row, col, __dmul_rn(acc[mi][ni][e], scale), ea);
       }
   __shared__ double red[DM_NT / 32];
   __shared__ float redf[DM_NT / 32];
+  const int mode = MODE >= 0 ? MODE : g.mode;
   const int64_t tile = ((g.col0 + n0) / DM_BN) * g.tiles_m + tm;
-  if (g.mode & (EPI_RESID | EPI_UPDATE)) {
-    const double s = block_sum_det<DM_NT>((g.mode & EPI_RESID) ? ea.r2 : ea.d2, red);
+  if (mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE)) {
+    const double s = block_sum_det<DM_NT>((mode & EPI_RESID) ? ea.r2 : ea.d2, red);
     if (tid == 0) g.part[tile] = s;
   }
   if (g.pmax) {
@@ -157,18 +159,29 @@ __global__ void __launch_bounds__(DM_NT, 2) k_gemm_dmma(const GemmArgs g) {
   }
 }
 
-cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s) {
+template <int MODE>
+static cudaError_t launch_mode(const GemmArgs &a, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, DM_SMEM);
+    cudaError_t e = cudaFuncSetAttribute(k_gemm_dmma<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, DM_SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  if (a.M % DM_BM || a.N % DM_BN || a.K % DM_BK || a.a_kp % DM_BK) return cudaErrorInvalidValue;
   dim3 grid((unsigned)((a.N / DM_BN) * (a.M / DM_BM)));
-  k_gemm_dmma<<<grid, DM_NT, DM_SMEM, s>>>(a);
+  k_gemm_dmma<MODE><<<grid, DM_NT, DM_SMEM, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s) {
+  if (a.M % DM_BM || a.N % DM_BN || a.K % DM_BK || a.a_kp % DM_BK) return cudaErrorInvalidValue;
+  // the hot-path modes get specialised kernels; anything else uses the runtime-mode build
+  if (!a.pmax && a.prec == P_FP64) {
+    if (a.mode == EPI_STORE_T) return launch_mode<EPI_STORE_T>(a, s);
+    if (a.mode == (EPI_STORE_T | EPI_RESID)) return launch_mode<EPI_STORE_T | EPI_RESID>(a, s);
+    if (a.mode == EPI_UPDATE && a.cont64 && !a.chat_new) return launch_mode<EPI_UPDATE>(a, s);
+  }
+  return launch_mode<-1>(a, s);
 }
 
 int dmma_tile_n() { return DM_BN; }

@@ -187,10 +187,15 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
     for (int j = 0; j < 32; ++j) {
       const double v = __dmul_rn((double)__uint_as_float(r[j]), scale);
       const int64_t c = col + j;
-      if (mode & EPI_STORE_T) store_operand(g.tout, c * g.ldt + row, g.prec, v, 0);
+      double w = v;
+      if (mode & EPI_TWO_I_MINUS) {   // Newton-Schulz W = 2I - A X (one FP64 subtraction)
+        const int64_t gc = g.col0 + c;
+        w = __dsub_rn((row == gc && row < g.n) ? 2.0 : 0.0, v);
+      }
+      if (mode & EPI_STORE_T) store_operand(g.tout, c * g.ldt + row, g.prec, w, 0);
       if (mode & EPI_TSCRATCH) {
-        ((float *)g.tout)[c * g.ldt + row] = (float)v;
-        ea.mx = fmaxf(ea.mx, fabsf((float)v));
+        ((float *)g.tout)[c * g.ldt + row] = (float)w;
+        ea.mx = fmaxf(ea.mx, fabsf((float)w));
       }
       if (mode & EPI_RESID) {
         const int64_t gc = g.col0 + c;
@@ -202,8 +207,9 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
       if (mode & EPI_F64) g.zout[row * g.ldz + c] = v;
     }
   }
-  if (mode & EPI_UPDATE) {
+  if (mode & (EPI_UPDATE | EPI_NSUPDATE)) {
     // container row segment [row][col .. col+31]: 128 B (FP32) per thread, 16-byte accesses
+    const bool ns = (mode & EPI_NSUPDATE) != 0;   // Newton-Schulz: X_{k+1} = q_m(D)
     const double pp1 = (double)(g.p + 1), pd = (double)g.p, invp = 1.0 / (double)g.p;
     const bool p2 = (g.p & (g.p - 1)) == 0;   // d/p == d*(1/p) exactly for p = 2^k
     const float4 *src = (const float4 *)((const float *)g.cold + row * g.ldc + col);
@@ -218,9 +224,12 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
         const int j = q * 4 + u;
         const double v = __dmul_rn((double)__uint_as_float(r[j]), scale);
         const double c = (double)cc[u];
-        const double a = __dmul_rn(pp1, c);
-        const double d = __dsub_rn(a, v);
-        const double e = p2 ? __dmul_rn(d, invp) : __ddiv_rn(d, pd);
+        double e = v;
+        if (!ns) {
+          const double a = __dmul_rn(pp1, c);
+          const double d = __dsub_rn(a, v);
+          e = p2 ? __dmul_rn(d, invp) : __ddiv_rn(d, pd);
+        }
         const float f = q_e8(e, g.m, g.rtz);
         cn[j] = f;
         const double dd = __dsub_rn((double)f, c);
@@ -363,7 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
       // per-tile partials: deterministic (fixed shuffle tree, warps summed in order 0..3)
-      if ((g.mode & (EPI_RESID | EPI_UPDATE)) || g.pmax) {
+      if ((g.mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE)) || g.pmax) {
         double s = (g.mode & EPI_RESID) ? ea.r2 : ea.d2;
         float mx = ea.mx;
         #pragma unroll
@@ -375,7 +384,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
         asm volatile("bar.sync 1, 256;\n" ::: "memory");
         if (et == 0) {
           const int64_t tile = ((g.col0 + colb) / TC_BN) * g.tiles_m + tile_m;
-          if (g.mode & (EPI_RESID | EPI_UPDATE))
+          if (g.mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE))
           {
             const double *rr = red[it & 1];
             double acc = 0.0;

@@ -1,0 +1,104 @@
+"""Run every BASELINE.json config (C1-C5) and its kappa = 2 twin through the C-ABI on one GPU and
+report what the method does: outcome, iterations per phase, min rho, time, GEMM
+TFLOP/s per phase.  Usage: python tools/configs_report.py [--only C1,C2] [--out file.json]"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch
+
+import paper_1703_02283_b200 as ipr
+import synth
+
+
+def low_then_fp64(low, n, m=-1, fp64_cap=0, switch_rho_hat=1e-2):
+    return [ipr.make_phase(low, mant_bits=m, switch_tol=switch_rho_hat * math.sqrt(n), plateau_ratio=0.7,
+                           plateau_arm=0.5, max_iters=60),
+            ipr.make_phase("fp64", max_iters=fp64_cap)]
+
+
+def run(A, p, phases, label, max_iters=400):
+    n = A.shape[0]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s = ipr.Solver(A, p, phases, 1e-12)
+    s.iterate(max_iters)
+    tr = s.trace()
+    out = ipr.OUTCOME_NAMES[s.outcome]
+    certified = s.residual(True) if tr else float("nan")
+    s.close()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    rho = [t["rho"] for t in tr]
+    fin = [(r, k) for k, r in enumerate(rho) if math.isfinite(r)]
+    rmin, kmin = min(fin) if fin else (float("nan"), -1)
+    per = {}
+    for t in tr:
+        native = {"fp64": 52, "bf16": 7, "tf32": 10, "fp16": 10}[t["prec"]]
+        d = per.setdefault(t["prec"] + ("" if t["mant_bits"] == native else f"/m{t['mant_bits']}"),
+                           {"iters": 0, "ms": 0.0, "gemms": 0})
+        d["iters"] += 1
+        d["ms"] += t["gemm_ms"]
+        d["gemms"] += p + (1 if t["decision"] == 0 else 0)
+    for d in per.values():
+        d["tflops"] = d["gemms"] * 2.0 * n ** 3 / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else None
+    rec = {"label": label, "n": n, "p": p, "outcome": out, "iterations": len(tr), "min_rho": rmin,
+           "argmin": kmin, "final_rho": rho[-1] if rho else None, "certified_rho_best": certified,
+           "time_s": dt, "phases": per}
+    print(json.dumps(rec), flush=True)
+    return rec
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="")
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    only = set(a.only.split(",")) if a.only else None
+    recs = []
+
+    def want(c):
+        return only is None or c in only
+
+    for name in ["C1", "C2", "C3", "C4", "C5"]:
+        if not want(name):
+            continue
+        c = synth.CONFIGS[name]
+        n, p, kap, seed = c["n"], c["p"], c["kappa"], c["seed"]
+        for kappa, tag in [(kap, "stated"), (2.0, "twin")]:
+            A, _ = synth.spd_torch(n, kappa, seed) if n >= 4096 else (torch.from_numpy(synth.spd(n, kappa, seed)).cuda(), None)
+            lab = f"{name} n={n} p={p} kappa={kappa:g} ({tag})"
+            if name == "C1":
+                recs.append(run(A, p, [ipr.make_phase("fp64", max_iters=200)], lab + " fp64"))
+            elif name == "C2":
+                recs.append(run(A, p, [ipr.make_phase("fp64", max_iters=200)], lab + " fp64"))
+                recs.append(run(A, p, low_then_fp64("tf32", n, fp64_cap=200), lab + " tf32->fp64"))
+            elif name == "C3":
+                recs.append(run(A, p, [ipr.make_phase("fp64", max_iters=120)], lab + " fp64"))
+                recs.append(run(A, p, low_then_fp64("bf16", n, fp64_cap=120), lab + " bf16->fp64"))
+            elif name == "C4":
+                recs.append(run(A, p, [ipr.make_phase("fp64", max_iters=120)], lab + " fp64"))
+                for m in [7, 10, 16, 23]:
+                    recs.append(run(A, p, [ipr.make_phase("fp64", mant_bits=m, switch_tol=1e-2 * math.sqrt(n),
+                                                          plateau_ratio=0.7, plateau_arm=0.5, max_iters=60),
+                                           ipr.make_phase("fp64", max_iters=120)], lab + f" fp64-storage m={m}->fp64"))
+                recs.append(run(A, p, low_then_fp64("bf16", n, fp64_cap=120), lab + " bf16(m=7)->fp64 (paired)"))
+                recs.append(run(A, p, low_then_fp64("tf32", n, fp64_cap=120), lab + " tf32(m=10)->fp64 (paired)"))
+            elif name == "C5":
+                cap = 30 if tag == "twin" else 8
+                if tag == "twin":
+                    recs.append(run(A, p, [ipr.make_phase("fp64", max_iters=cap)], lab + " fp64"))
+                recs.append(run(A, p, low_then_fp64("bf16", n, fp64_cap=cap), lab + f" bf16->fp64 (fp64 cap {cap})"))
+            del A
+            torch.cuda.empty_cache()
+    if a.out:
+        json.dump(recs, open(a.out, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
