@@ -117,6 +117,16 @@ ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda,
 ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int nphases,
                             double final_tol);
 
+/* Iteration form.  IPR_FORM_LITERAL (default): Eq. (1) as printed, evaluated as
+ * the right-to-left chain of reading R-1.  IPR_FORM_NEWTON_SCHULZ: p = 1 only, the textbook
+ * Newton-Schulz ordering X_{k+1} = X_k (2I - A X_k) that PAPER.md:79-81 names (SURVEY 8(f)
+ * NEXT-1): two GEMMs per iteration, T = Ahat Xhat with the fused residual ||I - T||_F and
+ * What = qin(2I - T), then X_{k+1} = q_m(Xhat What).  Its error is quadratic in the deviation
+ * (no linear term), so low-precision noise is removed by the FP64 phase.  Call before the
+ * first ipr_iterate; a p != 1 schedule with this form fails at ipr_iterate (INVALID_ARG). */
+typedef enum { IPR_FORM_LITERAL = 0, IPR_FORM_NEWTON_SCHULZ = 1 } ipr_form;
+ipr_status ipr_set_form(ipr_ctx *c, int form);
+
 /* Run at most max_iters (> 0) chains.  *iters_done = chains evaluated by this call,
  * *outcome = IPR_RUNNING if the budget ran out, else the terminal outcome.  Resumable. */
 ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *outcome);

@@ -31,7 +31,9 @@ OUTCOME_NAMES = {0: "running", 1: "converged", 2: "iter_limit", 3: "diverged", 4
 EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_get_trace",
             "ipr_get_iterate", "ipr_get_norms", "ipr_finalize", "ipr_last_error",
             "ipr_nccl_unique_id", "ipr_version", "ipr_test_quantize", "ipr_test_gemm",
-            "ipr_launch_count", "ipr_plan"]
+            "ipr_launch_count", "ipr_plan", "ipr_set_form"]
+IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ = 0, 1
+FORM_BY_NAME = {"literal": IPR_FORM_LITERAL, "newton_schulz": IPR_FORM_NEWTON_SCHULZ, "ns": IPR_FORM_NEWTON_SCHULZ}
 
 
 class IprError(RuntimeError):
@@ -74,6 +76,7 @@ def _load():
     L.ipr_test_gemm.argtypes = [C.c_int, i64, vp, vp, vp, vp]
     L.ipr_launch_count.restype = C.c_int64
     L.ipr_plan.argtypes = [i64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)]
+    L.ipr_set_form.argtypes = [vp, C.c_int]
     for f in EXPORTED:
         if f not in ("ipr_last_error", "ipr_version", "ipr_launch_count"):
             getattr(L, f).restype = C.c_int
@@ -147,6 +150,11 @@ def ipr_set_schedule(ctx, p: int, phases, final_tol: float):
     _check(_lib.ipr_set_schedule(ctx, p, arr, len(phases), final_tol), ctx)
 
 
+def ipr_set_form(ctx, form):
+    f = FORM_BY_NAME[form] if isinstance(form, str) else int(form)
+    _check(_lib.ipr_set_form(ctx, f), ctx)
+
+
 def ipr_iterate(ctx, max_iters: int):
     done, out = C.c_int(0), C.c_int(0)
     _check(_lib.ipr_iterate(ctx, max_iters, C.byref(done), C.byref(out)), ctx)
@@ -209,13 +217,14 @@ class Solver:
     """Owns one ipr_ctx.  A: FP64 CUDA tensor (n x n, symmetric), kept alive by the Solver."""
 
     def __init__(self, A, p: int, phases, final_tol: float = 1e-12, stream=None, world: int = 1,
-                 rank: int = 0, nccl_unique_id: bytes | None = None):
+                 rank: int = 0, nccl_unique_id: bytes | None = None, form="literal"):
         self.A = A
         self.n = A.shape[0]
         self.ctx = ipr_init(self.n, A, A.stride(0), stream, world, rank, nccl_unique_id)
         try:
             ipr_set_schedule(self.ctx, p, [ph if isinstance(ph, ipr_phase) else make_phase(**ph)
                                            for ph in phases], final_tol)
+            ipr_set_form(self.ctx, form)
         except Exception:
             ipr_finalize(self.ctx)
             self.ctx = None
@@ -265,9 +274,10 @@ class Solver:
             pass
 
 
-def solve(A, p: int, phases, final_tol: float = 1e-12, max_iters: int = 1000, stream=None):
+def solve(A, p: int, phases, final_tol: float = 1e-12, max_iters: int = 1000, stream=None,
+          form="literal"):
     """Run a full solve; returns (C_best, outcome name, trace)."""
-    s = Solver(A, p, phases, final_tol, stream)
+    s = Solver(A, p, phases, final_tol, stream, form=form)
     s.iterate(max_iters)
     tr = s.trace()
     out = OUTCOME_NAMES[s.outcome]

@@ -64,6 +64,8 @@ struct ipr_ctx {
   double *best = nullptr;                // FP64 local panel
   void *T[2] = {nullptr, nullptr};      // chain intermediates, K-major [kp][npad]
   void *Aop = nullptr;                  // stage-A operand of the current phase [kp][npad]
+  void *Afull = nullptr;                // Newton-Schulz, world > 1: full row-major Ahat (A operand)
+  int form = IPR_FORM_LITERAL;          // iteration form (ipr_set_form)
   float *tscr = nullptr;                // FP16 phase T scratch (FP32)
   double *full64 = nullptr;             // FP64 npad x npad scratch (copy-out / certify)
   void *Acert = nullptr;                // FP64 Ahat for certify
@@ -229,9 +231,15 @@ ipr_status save_best(ipr_ctx *c) {
   return IPR_OK;
 }
 
+ipr_status make_xt(ipr_ctx *c, int i, const PhaseC &P);
+
 ipr_status begin_phase(ipr_ctx *c, bool first) {
   const PhaseC &P = c->ph[c->phase];
   CKS(stage_a(c, P, c->Aop, c->dsig + 0));
+  if (c->form == IPR_FORM_NEWTON_SCHULZ && c->world > 1) {   // full row-major Ahat (A operand)
+    CK(launch_stage_a(c->A, c->lda, c->n, c->npad, 0, c->npad, P.prec, P.cont64, P.m, P.rtz,
+                      P.prec == IPR_FP16 ? c->dsig + 0 : nullptr, c->Afull, c->st));
+  }
   if (first) {
     CK(launch_c0(c->A, c->lda, c->n, c->npad, c->col0, c->kp, c->norms[3], P.cont64, P.m, P.rtz,
                  cont_ptr(c, c->cur, P), c->st));
@@ -241,7 +249,16 @@ ipr_status begin_phase(ipr_ctx *c, bool first) {
       CK(launch_f64_to_cont(c->best, c->npad * c->kp, P.cont64, P.m, P.rtz, cont_ptr(c, c->cur, P), c->st));
     }
   }
-  return make_operand(c, c->cur, P);
+  CKS(make_operand(c, c->cur, P));
+  if (c->form == IPR_FORM_NEWTON_SCHULZ) CKS(make_xt(c, c->cur, P));
+  return IPR_OK;
+}
+
+// Newton-Schulz form (NEXT-1): the transposed operand X^T of the local column panel (the B operand
+// of T = Ahat Xhat) from the row-major local slot of Chat(i).
+ipr_status make_xt(ipr_ctx *c, int i, const PhaseC &P) {
+  CK(launch_transpose(chat_slot(c, i, P.prec), c->npad, c->kp, elt_size(P.prec), c->T[0], c->st));
+  return IPR_OK;
 }
 
 // ---- one chain: p GEMMs + fused residual; returns rho (host sync) ----
@@ -251,9 +268,27 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
   const void *X = c->Aop;
   const int *sigX = (prec == IPR_FP16) ? c->dsig + 0 : nullptr;
   const int64_t tm = tiles_m(c, prec), tn_loc = c->kp / gemm_tile_n(prec);
-  double *part = c->part + (c->world > 1 ? 0 : 0);
+  double *part = c->part;
   CK(cudaEventRecord(c->ev[0], c->st));
-  for (int j = 1; j <= c->p; ++j) {
+  if (c->form == IPR_FORM_NEWTON_SCHULZ) {
+    // T = Ahat Xhat (A operand: full row-major Ahat; B: X^T panel), epilogue: residual partials
+    // and What = qin(2I - T) stored K-major for the update GEMM
+    GemmArgs g = base_args(c, prec, c->T[0]);
+    g.A = c->world == 1 ? c->Aop : c->Afull;
+    g.a_kp = c->npad; g.a_pstride = c->npad * c->npad;
+    if (prec == IPR_FP16) { g.sigA = c->dsig + 0; g.sigB = c->dsig + 1 + c->cur; g.pmax = c->pmax; }
+    g.mode = (prec == IPR_FP16 ? EPI_TSCRATCH : EPI_STORE_T) | EPI_TWO_I_MINUS | EPI_RESID;
+    g.tout = (prec == IPR_FP16) ? (void *)c->tscr : c->T[1];
+    g.ldt = c->npad;
+    g.part = part;
+    CK(run_gemm(c, g));
+    if (prec == IPR_FP16) {
+      CKS(gather_pmax(c, c->pmax, tn_loc * tm));
+      CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 4, c->st));
+      CK(launch_scale_fp16(c->tscr, c->kp * c->npad, c->dsig + 4, c->T[1], c->st));
+    }
+  }
+  for (int j = 1; c->form == IPR_FORM_LITERAL && j <= c->p; ++j) {
     GemmArgs g = base_args(c, prec, X);
     chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
     if (prec == IPR_FP16) { g.sigA = c->dsig + 1 + c->cur; g.sigB = sigX; }
@@ -296,10 +331,13 @@ ipr_status update(ipr_ctx *c) {
   // the update overwrites buffer nx: keep the best iterate if it lives there
   if (c->best_loc == nx) CKS(save_best(c));
   const int64_t tm = tiles_m(c, prec), tn_loc = c->kp / gemm_tile_n(prec);
-  GemmArgs g = base_args(c, prec, c->T[c->p & 1]);
+  const bool ns = c->form == IPR_FORM_NEWTON_SCHULZ;
+  // literal: P = Chat qin(T_p); Newton-Schulz: X_{k+1} = Xhat What (What in T[1])
+  const int tb = ns ? 1 : (c->p & 1);
+  GemmArgs g = base_args(c, prec, c->T[tb]);
   chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
-  if (prec == IPR_FP16) { g.sigA = c->dsig + 1 + c->cur; g.sigB = c->dsig + 3 + (c->p & 1); g.pmax = c->pmax; }
-  g.mode = EPI_UPDATE;
+  if (prec == IPR_FP16) { g.sigA = c->dsig + 1 + c->cur; g.sigB = c->dsig + 3 + tb; g.pmax = c->pmax; }
+  g.mode = ns ? EPI_NSUPDATE : EPI_UPDATE;
   g.cold = cont_ptr(c, c->cur, P);
   g.cnew = cont_ptr(c, nx, P);
   g.ldc = c->kp;
@@ -319,6 +357,7 @@ ipr_status update(ipr_ctx *c) {
     CK(launch_make_operand(c->cont[nx], 0, c->npad * c->kp, IPR_FP16, c->dsig + 1 + nx, chat_slot(c, nx, prec), c->st));
   }
   CKS(gather_chat(c, nx, prec));
+  if (ns) CKS(make_xt(c, nx, P));
   c->cur = nx;
   return IPR_OK;
 }
@@ -351,6 +390,7 @@ void free_ctx(ipr_ctx *c) {
   if (!c) return;
   cudaFree(c->chat[0]); cudaFree(c->chat[1]); cudaFree(c->cont[0]); cudaFree(c->cont[1]);
   cudaFree(c->best); cudaFree(c->T[0]); cudaFree(c->T[1]); cudaFree(c->Aop); cudaFree(c->tscr);
+  cudaFree(c->Afull);
   cudaFree(c->full64); cudaFree(c->Acert); cudaFree(c->part); cudaFree(c->pmax); cudaFree(c->dscal);
   cudaFree(c->dsig); cudaFree(c->colsum); cudaFree(c->dflag);
   if (c->hscal) cudaFreeHost(c->hscal);
@@ -501,6 +541,15 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
   return IPR_OK;
 }
 
+ipr_status ipr_set_form(ipr_ctx *c, int form) {
+  if (!c) return fail(c, IPR_E_INVALID_ARG, "ipr_set_form: null context");
+  if (c->started) return fail(c, IPR_E_STATE, "ipr_set_form: iteration already started");
+  if (form != IPR_FORM_LITERAL && form != IPR_FORM_NEWTON_SCHULZ)
+    return fail(c, IPR_E_INVALID_ARG, "ipr_set_form: unknown form %d", form);
+  c->form = form;
+  return IPR_OK;
+}
+
 ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *outcome) {
   if (!c || !iters_done || !outcome) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: null pointer");
   if (!c->scheduled) return fail(c, IPR_E_STATE, "ipr_iterate: call ipr_set_schedule first");
@@ -508,6 +557,10 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
   *iters_done = 0;
   if (c->done) { *outcome = (ipr_outcome)c->outcome; return IPR_OK; }
   if (!c->started) {
+    if (c->form == IPR_FORM_NEWTON_SCHULZ) {
+      if (c->p != 1) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: the Newton-Schulz form needs p = 1");
+      if (c->world > 1 && !c->Afull) CKS(dalloc(c, &c->Afull, (size_t)(c->npad * c->npad) * 8));
+    }
     c->phase = 0; c->it_in_phase = 0; c->cur = 0;
     CKS(begin_phase(c, true));
     c->started = true;

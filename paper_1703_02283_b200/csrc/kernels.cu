@@ -218,6 +218,23 @@ __global__ void k_unpad_f64(const double *src, int64_t n, int64_t npad, double *
   if (j < n) dst[i * n + j] = src[i * npad + j];
 }
 
+// Newton-Schulz form: dst[j][i] = src[i][j] for a rows x cols operand panel (element size esz),
+// 32 x 32 tiles through shared memory (coalesced on both sides)
+template <typename T>
+__global__ void k_transpose(const T *src, int64_t rows, int64_t cols, T *dst) {
+  __shared__ T t[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int64_t r = r0 + k, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) t[k][threadIdx.x] = src[r * cols + c];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int64_t c = c0 + k, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) dst[c * rows + r] = t[threadIdx.x][k];
+  }
+}
+
 // test hook: quantisers
 __global__ void k_test_quant(int mode, const void *in, void *out, int64_t len, int m, int rtz, int sigma) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -309,6 +326,14 @@ cudaError_t launch_unpad_f64(const double *src, int64_t n, int64_t npad, double 
   k_unpad_f64<<<g, 256, 0, s>>>(src, n, npad, dst);
   LAUNCH_CHECK();
 }
+cudaError_t launch_transpose(const void *src, int64_t rows, int64_t cols, int esz, void *dst, cudaStream_t s) {
+  dim3 g(nblk(cols, 32), nblk(rows, 32)), b(32, 8);
+  if (esz == 8) k_transpose<double><<<g, b, 0, s>>>((const double *)src, rows, cols, (double *)dst);
+  else if (esz == 4) k_transpose<float><<<g, b, 0, s>>>((const float *)src, rows, cols, (float *)dst);
+  else k_transpose<uint16_t><<<g, b, 0, s>>>((const uint16_t *)src, rows, cols, (uint16_t *)dst);
+  LAUNCH_CHECK();
+}
+
 cudaError_t launch_test_quant(int mode, const void *in, void *out, int64_t len, int m, int rtz, int sigma,
                               cudaStream_t s) {
   if (len <= 0) return cudaSuccess;
