@@ -22,11 +22,11 @@ def low_then_fp64(low, n, m=-1, fp64_cap=0, switch_rho_hat=1e-2):
             ipr.make_phase("fp64", max_iters=fp64_cap)]
 
 
-def run(A, p, phases, label, max_iters=400):
+def run(A, p, phases, label, max_iters=400, form="literal", tol=1e-12):
     n = A.shape[0]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    s = ipr.Solver(A, p, phases, 1e-12)
+    s = ipr.Solver(A, p, phases, tol, form=form)
     s.iterate(max_iters)
     tr = s.trace()
     out = ipr.OUTCOME_NAMES[s.outcome]
@@ -94,6 +94,21 @@ def main():
                 if tag == "twin":
                     recs.append(run(A, p, [ipr.make_phase("fp64", max_iters=cap)], lab + " fp64"))
                 recs.append(run(A, p, low_then_fp64("bf16", n, fp64_cap=cap), lab + f" bf16->fp64 (fp64 cap {cap})"))
+            del A
+            torch.cuda.empty_cache()
+    # NEXT-1: Newton-Schulz ordering (p = 1) -- where mixed precision beats all-FP64
+    for name, n in [("NS-C2", 1024), ("NS-C2@8192", 8192)]:
+        if not want(name):
+            continue
+        c = synth.CONFIGS["C2"]
+        for kappa, tol in [(c["kappa"], 1e-9), (2.0, 1e-12)]:
+            A, _ = synth.spd_torch(n, kappa, c["seed"])
+            lab = f"{name} n={n} p=1 kappa={kappa:g} Newton-Schulz X(2I-AX), tol={tol:g}"
+            recs.append(run(A, 1, [ipr.make_phase("fp64", max_iters=200)], lab + " fp64", form="ns", tol=tol))
+            for low in ["bf16", "tf32", "fp16"]:
+                ph = [ipr.make_phase(low, switch_tol=1e-2 * math.sqrt(n), plateau_ratio=0.7, plateau_arm=0.1,
+                                     max_iters=80), ipr.make_phase("fp64", max_iters=200)]
+                recs.append(run(A, 1, ph, lab + f" {low}->fp64", form="ns", tol=tol))
             del A
             torch.cuda.empty_cache()
     if a.out:
