@@ -39,13 +39,13 @@ def build(force: bool = False) -> str:
 class Phase(C.Structure):
     _fields_ = [("prec", C.c_int), ("mant_bits", C.c_int), ("round", C.c_int),
                 ("switch_tol", C.c_double), ("plateau_ratio", C.c_double),
-                ("plateau_arm", C.c_double), ("max_iters", C.c_int)]
+                ("plateau_arm", C.c_double), ("max_iters", C.c_int), ("corr_prec", C.c_int)]
 
 
 class Record(C.Structure):
     _fields_ = [("k", C.c_int), ("phase", C.c_int), ("prec", C.c_int), ("mant_bits", C.c_int),
                 ("decision", C.c_int), ("rho", C.c_double), ("rho_hat", C.c_double),
-                ("delta", C.c_double), ("gamma", C.c_double)]
+                ("delta", C.c_double), ("gamma", C.c_double), ("rho_cert", C.c_double)]
 
 
 class Ctrl(C.Structure):
@@ -82,6 +82,8 @@ def lib():
         L.orc_solve_form.argtypes = [C.c_int64, C.c_int, C.c_int, _dp, C.POINTER(Phase), C.c_int,
                                      C.c_double, C.c_int, C.POINTER(Record), C.c_int,
                                      C.POINTER(C.c_int), _dp, _dp, C.c_int, C.c_double, _dp]
+        L.orc_step_sym.restype = C.c_double
+        L.orc_step_sym.argtypes = [C.c_int64, C.c_int, _dp, _dp, C.POINTER(Phase), _dp, _dp]
         L.orc_step_ns.restype = C.c_double
         L.orc_step_ns.argtypes = [C.c_int64, _dp, _dp, C.POINTER(Phase), _dp, _dp]
         L.orc_jacobi.argtypes = [C.c_int64, _dp, _dp, _dp]
@@ -106,8 +108,10 @@ def _f64(a) -> np.ndarray:
 
 
 def phase(prec=FP64, mant_bits=-1, round=RNE, switch_tol=0.0, plateau_ratio=0.0,
-          plateau_arm=0.5, max_iters=0) -> Phase:
-    return Phase(prec, mant_bits, round, switch_tol, plateau_ratio, plateau_arm, max_iters)
+          plateau_arm=0.5, max_iters=0, corr_prec=-1) -> Phase:
+    """corr_prec: operand format of the correction GEMM of FORM_SYMMETRIC (-1 = prec)."""
+    return Phase(prec, mant_bits, round, switch_tol, plateau_ratio, plateau_arm, max_iters,
+                 corr_prec)
 
 
 def qm(x, E: int, m: int, rtz: bool = False) -> np.ndarray:
@@ -213,13 +217,25 @@ def step_ns(A, Xk, ph: Phase, want_next: bool = True):
     return rho, nxt, d.value
 
 
-FORM_LITERAL, FORM_NEWTON_SCHULZ = 0, 1
+def step_sym(A, Ck, p: int, ph: Phase, want_next: bool = True):
+    """One symmetrised-correction step (NEXT-2, p >= 2): C + (W + W^T)/(2p), W = qc(C) qc(I - Z_p),
+    Z_p = C^{p-1} A C.  Returns (rho_s(C_k) = ||I - Z_p||_F, C_{k+1}, delta)."""
+    A, Ck = _f64(A), _f64(Ck)
+    nxt = np.empty_like(Ck) if want_next else None
+    d = C.c_double(np.nan)
+    rho = lib().orc_step_sym(A.shape[0], p, _p(A), _p(Ck), C.byref(ph),
+                             _p(nxt) if want_next else None, C.byref(d))
+    return rho, nxt, d.value
+
+
+FORM_LITERAL, FORM_NEWTON_SCHULZ, FORM_SYMMETRIC = 0, 1, 2
 
 
 def solve(A, p: int, phases, final_tol: float = 1e-12, max_total: int = 200,
           hist: int = 0, gamma_normA2: float = 0.0, form: int = FORM_LITERAL) -> SolveResult:
     """Full controller-driven solve (init + iterations), reading R-5 of DESIGN.md.
-    form = FORM_LITERAL (Eq. 1 as printed) or FORM_NEWTON_SCHULZ (p = 1, X(2I - AX))."""
+    form = FORM_LITERAL (Eq. 1 as printed), FORM_NEWTON_SCHULZ (p = 1, X(2I - AX)) or
+    FORM_SYMMETRIC (p >= 2, C + (W + W^T)/(2p); convergence certified on ||I - C^p A||_F)."""
     A = _f64(A)
     n = A.shape[0]
     arr = (Phase * len(phases))(*phases)
@@ -235,7 +251,7 @@ def solve(A, p: int, phases, final_tol: float = 1e-12, max_total: int = 200,
         raise ValueError({-1: "invalid argument", -2: "A is not exactly symmetric"}[out])
     records = [dict(k=r.k, phase=r.phase, prec=r.prec, mant_bits=r.mant_bits,
                     decision=r.decision, rho=r.rho, rho_hat=r.rho_hat, delta=r.delta,
-                    gamma=r.gamma) for r in recs[:min(nrec.value, max_total)]]
+                    gamma=r.gamma, rho_cert=r.rho_cert) for r in recs[:min(nrec.value, max_total)]]
     return SolveResult(out, records, best, H, s.value)
 
 

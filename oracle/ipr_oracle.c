@@ -325,6 +325,61 @@ static double update_ns(int64_t n, const double *X, const orc_phase *ph, chain_w
   return sqrt(s2);
 }
 
+/* ---------------------------------------------------------------------------------
+ * NEXT-2: the symmetrised-correction form for p >= 2.  Not printed in the
+ * paper: it is the Newton correction of Eq. (1) (PAPER.md:71-73 reads C_{k+1} = C_k +
+ * C_k (I - C_k^p A) / p) with the residual taken as R = I - C^{p-1} A C and the correction
+ * symmetrised, so that noise which does not commute with A is damped (R-22):
+ *   Chat = qin(C), Ahat = qin(q_m(A)),  Z_1 = Ahat Chat,  Z_j = Chat qin(Z_{j-1}) (j = 2..p)
+ *   rho_s = ||I - Z_p||_F (unrounded Z_p),  Rhat = qc(I - Z_p)   (one FP64 subtraction)
+ *   W = qc(C) Rhat  (FP64 accumulator),   C_{k+1}[i][j] = q_m(C_ij + (W_ij + W_ji) / (2p))
+ * where qc is the operand format of the correction GEMM (corr_prec; = prec by default).
+ * C_{k+1} is exactly symmetric whenever C_k is (W_ij + W_ji is commutative in IEEE).
+ * FP16 phases are not defined for this form (no operand scaling here).
+ * ------------------------------------------------------------------------------ */
+static int corr_of(const orc_phase *ph) { return ph->corr_prec < 0 ? ph->prec : ph->corr_prec; }
+
+static double chain_sym(int64_t n, int p, const double *A, const double *C, const orc_phase *ph,
+                        chain_ws *w) {
+  const int64_t nn = n * n;
+  for (int64_t i = 0; i < nn; ++i) w->T[i] = store_q(ph, A[i]);
+  qin_matrix(ph->prec, nn, w->T, w->X);                     /* w->X = Ahat            */
+  qin_matrix(ph->prec, nn, C, w->Chat);                     /* w->Chat = Chat         */
+  orc_gemm(n, w->X, w->Chat, w->T);                         /* Z_1 = Ahat Chat        */
+  for (int j = 2; j <= p; ++j) {
+    qin_matrix(ph->prec, nn, w->T, w->X);                   /* qin(Z_{j-1})           */
+    orc_gemm(n, w->Chat, w->X, w->T);                       /* Z_j = Chat qin(Z_{j-1}) */
+  }
+  double s2 = 0.0;
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t c = 0; c < n; ++c) {
+      const double d = (r == c ? 1.0 : 0.0) - w->T[r * n + c];   /* R = I - Z_p        */
+      s2 += d * d;
+      w->T[r * n + c] = d;
+    }
+  qin_matrix(corr_of(ph), nn, w->T, w->X);                  /* w->X = Rhat            */
+  return sqrt(s2);
+}
+
+static double update_sym(int64_t n, int p, const double *C, const orc_phase *ph, chain_ws *w,
+                         double *C_next) {
+  const int64_t nn = n * n;
+  qin_matrix(corr_of(ph), nn, C, w->Chat);                  /* qc(C)                  */
+  orc_gemm(n, w->Chat, w->X, w->T);                         /* W = qc(C) Rhat         */
+  const double tp = (double)(2 * p);
+  double s2 = 0.0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      const double sw = w->T[i * n + j] + w->T[j * n + i];
+      const double e = sw / tp;
+      const double c1 = store_q(ph, C[i * n + j] + e);
+      const double dd = c1 - C[i * n + j];
+      s2 += dd * dd;
+      C_next[i * n + j] = c1;
+    }
+  return sqrt(s2);
+}
+
 static int ws_alloc(chain_ws *w, int64_t n) {
   const size_t b = (size_t)(n * n) * sizeof(double);
   w->n = n;
@@ -371,6 +426,17 @@ double orc_step_ns(int64_t n, const double *A, const double *X, const orc_phase 
   return rho;
 }
 
+double orc_step_sym(int64_t n, int p, const double *A, const double *C, const orc_phase *ph,
+                    double *C_next, double *delta) {
+  if (p < 2 || ph->prec == ORC_FP16 || corr_of(ph) == ORC_FP16) return NAN;
+  chain_ws w;
+  if (!ws_alloc(&w, n)) { ws_free(&w); return NAN; }
+  const double rho = chain_sym(n, p, A, C, ph, &w);
+  if (C_next) { const double d = update_sym(n, p, C, ph, &w, C_next); if (delta) *delta = d; }
+  ws_free(&w);
+  return rho;
+}
+
 int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int nphases,
               double final_tol, int max_total, orc_record *rec, int cap_rec, int *nrec,
               double *C_best, double *C_hist, int hist_cap, double gamma_normA2,
@@ -386,6 +452,12 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
   *nrec = 0;
   if (n <= 0 || p < 1 || nphases < 1) return -1;
   if (form == ORC_FORM_NEWTON_SCHULZ && p != 1) return -1;
+  if (form == ORC_FORM_SYMMETRIC) {
+    if (p < 2) return -1;
+    for (int i = 0; i < nphases; ++i)
+      if (phases[i].prec == ORC_FP16 || corr_of(&phases[i]) == ORC_FP16) return -1;
+  }
+  if (form < ORC_FORM_LITERAL || form > ORC_FORM_SYMMETRIC) return -1;
   if (!orc_is_symmetric(n, A)) return -2;
   const int64_t nn = n * n;
   double nrm[3];
@@ -409,16 +481,33 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
   for (int k = 0; k < max_total; ++k) {
     const orc_phase *ph = &phases[ctl.phase];
     if (C_hist && k < hist_cap) memcpy(C_hist + (int64_t)k * nn, C, (size_t)nn * sizeof(double));
-    const double rho = form == ORC_FORM_NEWTON_SCHULZ ? chain_ns(n, A, C, ph, &w) : chain(n, p, A, C, ph, &w);
+    const double rho = form == ORC_FORM_NEWTON_SCHULZ ? chain_ns(n, A, C, ph, &w)
+                       : form == ORC_FORM_SYMMETRIC    ? chain_sym(n, p, A, C, ph, &w)
+                                                       : chain(n, p, A, C, ph, &w);
     const int phase_now = ctl.phase;
-    const int d = orc_ctrl_decide(&ctl, ph, rho);
+    int d = orc_ctrl_decide(&ctl, ph, rho);
     if (ctl.best_is_new) memcpy(C_best, C, (size_t)nn * sizeof(double));
     orc_record r;
     r.k = k; r.phase = phase_now; r.prec = ph->prec; r.mant_bits = phase_m(ph);
     r.decision = d; r.rho = rho; r.rho_hat = rho / sqrt((double)n); r.delta = NAN;
     r.gamma = (gamma_normA2 > 0) ? gamma_of(n, C, A, gamma_normA2, g1, g2) : NAN;
-    if (d == ORC_CONTINUE) {
-      r.delta = form == ORC_FORM_NEWTON_SCHULZ ? update_ns(n, C, ph, &w, Cn) : update(n, p, C, ph, &w, Cn);
+    r.rho_cert = NAN;
+    if (d == ORC_CONVERGED && form == ORC_FORM_SYMMETRIC) {
+      /* rho_s = ||I - C^{p-1} A C||_F is not the north-star residual: certify
+       * ||I - C^p A||_F with the FP64 literal chain (reading R-3); if it misses final_tol the
+       * iteration continues from the update computed first (as the GPU engine does). */
+      r.delta = update_sym(n, p, C, ph, &w, Cn);
+      const orc_phase ph64 = {ORC_FP64, -1, ORC_RNE, 0.0, 0.0, 0.0, 0, -1};
+      r.rho_cert = chain(n, p, A, C, &ph64, &w);
+      if (!(r.rho_cert <= final_tol)) {
+        d = ORC_CONTINUE;
+        r.decision = d;
+        double *t = C; C = Cn; Cn = t;
+      }
+    } else if (d == ORC_CONTINUE) {
+      r.delta = form == ORC_FORM_NEWTON_SCHULZ ? update_ns(n, C, ph, &w, Cn)
+                : form == ORC_FORM_SYMMETRIC    ? update_sym(n, p, C, ph, &w, Cn)
+                                                : update(n, p, C, ph, &w, Cn);
       double *t = C; C = Cn; Cn = t;
     } else if (d == ORC_SWITCH) {
       orc_ctrl_enter_next_phase(&ctl);

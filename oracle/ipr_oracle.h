@@ -67,11 +67,15 @@ typedef struct {
   double plateau_ratio; /* armed plateau: rho_k > ratio * rho_{k-1}; 0 = off          */
   double plateau_arm;   /* armed when rho_hat_k < plateau_arm                          */
   int    max_iters;     /* per-phase cap on chains; 0 = unlimited                     */
+  int    corr_prec;     /* ORC_FORM_SYMMETRIC: operand format of the correction GEMM  */
+                        /* W = qc(C) Rhat; -1 = prec.  Ignored by the other forms.    */
 } orc_phase;
 
 typedef struct {
   int k, phase, prec, mant_bits, decision;
   double rho, rho_hat, delta, gamma;
+  double rho_cert;     /* ORC_FORM_SYMMETRIC: certified ||I - C^p A||_F (FP64) when the */
+                       /* in-chain rho_s met final_tol; NaN otherwise                   */
 } orc_record;
 
 /* Controller (reading R-5 of DESIGN.md).  Pure state machine, no matrices. */
@@ -108,7 +112,7 @@ int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int np
 
 /* Iteration forms: ORC_FORM_LITERAL = Eq. (1) as printed (right-to-left chain, reading R-1);
  * ORC_FORM_NEWTON_SCHULZ = p = 1 only, X_{k+1} = X_k (2I - A X_k) (NEXT-1). */
-enum { ORC_FORM_LITERAL = 0, ORC_FORM_NEWTON_SCHULZ = 1 };
+enum { ORC_FORM_LITERAL = 0, ORC_FORM_NEWTON_SCHULZ = 1, ORC_FORM_SYMMETRIC = 2 };
 int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase *phases,
                    int nphases, double final_tol, int max_total, orc_record *rec, int cap_rec,
                    int *nrec, double *C_best, double *C_hist, int hist_cap, double gamma_normA2,
@@ -116,6 +120,12 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
 /* One Newton-Schulz step from X: returns rho(X) = ||I - Ahat Xhat||_F; X_next may be NULL. */
 double orc_step_ns(int64_t n, const double *A, const double *X, const orc_phase *ph,
                    double *X_next, double *delta);
+
+/* One symmetrised-correction step (NEXT-2, p >= 2, no FP16): returns rho_s(C) =
+ * ||I - C^{p-1} A C||_F (in-chain); C_next = q_m(C + (W + W^T)/(2p)), W = qc(C) qc(I - Z_p).
+ * Returns NaN for p < 2 or an FP16 phase. */
+double orc_step_sym(int64_t n, int p, const double *A, const double *C, const orc_phase *ph,
+                    double *C_next, double *delta);
 
 /* Cyclic Jacobi eigen-decomposition of a symmetric matrix (n small).
  * lambda ascending, V columns = eigenvectors (row-major n x n).  Returns sweeps used. */

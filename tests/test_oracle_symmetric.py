@@ -1,0 +1,162 @@
+"""Pins of the oracle's NEXT-2 form: the symmetrised correction
+
+    Z_p = C^{p-1} A C,  R = I - Z_p,  W = C R,  C_{k+1} = q_m(C + (W + W^T) / (2p)),   p >= 2
+
+(Eq. (1), is C + C (I - C^p A) / p; this form takes the residual as
+C^{p-1} A C and symmetrises the correction -- DESIGN.md reading R-22).  Pinned against: exact
+rational arithmetic of the definition on a non-commuting 2 x 2, the closed-form linearisation
+at the fixed point (derived by hand below, independent of the code), closed-form limits, the
+eigen-decomposition limit, exact symmetry, and the spectral predictor of the exact iteration.
+"""
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import scipy.linalg
+
+import oracle
+import synth
+
+SYM = oracle.FORM_SYMMETRIC
+
+
+def _fr(M):
+    return [[Fraction(x) for x in row] for row in M]
+
+
+def _mm(X, Y):
+    n = len(X)
+    return [[sum(X[i][k] * Y[k][j] for k in range(n)) for j in range(n)] for i in range(n)]
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_one_step_matches_exact_rational_arithmetic(p):
+    # A and C symmetric but NOT commuting, so every transposition / product order matters.
+    A = np.array([[2.0, 1.0], [1.0, 3.0]])
+    Ck = np.array([[0.5, 0.125], [0.125, 0.375]])
+    assert not np.allclose(A @ Ck, Ck @ A)
+    Af, Cf = _fr(A), _fr(Ck)
+    Z = _mm(Af, Cf)                         # Z_1 = A C
+    for _ in range(2, p + 1):
+        Z = _mm(Cf, Z)                      # Z_j = C Z_{j-1}
+    R = [[(1 if i == j else 0) - Z[i][j] for j in range(2)] for i in range(2)]
+    W = _mm(Cf, R)
+    exact = [[Cf[i][j] + (W[i][j] + W[j][i]) / (2 * p) for j in range(2)] for i in range(2)]
+    rho_exact = sum(float(R[i][j]) ** 2 for i in range(2) for j in range(2)) ** 0.5
+    rho, nxt, _ = oracle.step_sym(A, Ck, p, oracle.phase())
+    np.testing.assert_allclose(nxt, np.array(exact, dtype=float), rtol=2e-16, atol=1e-17)
+    assert rho == pytest.approx(rho_exact, rel=1e-14)
+    assert nxt[0, 1] == nxt[1, 0]           # exactly symmetric
+
+
+def _mu_pred(p, li, lj):
+    """Hand linearisation of G(C) = C + (W + W^T)/(2p) at X = A^{-1/p} (X^p A = I, XA = AX).
+    In A's eigenbasis with x = lambda^{-1/p} and a symmetric perturbation E:
+      d(C^{p-1} A C)_ij = E_ij g_ij,  g_ij = sum_{l=0}^{p-2} x_i^l x_j^{p-1-l} lambda_j + x_i^{p-1} lambda_i
+      dW_ij = -x_i g_ij E_ij  (R(X) = 0),  so  mu_ij = 1 - (x_i g_ij + x_j g_ji) / (2p)."""
+    xi, xj = li ** (-1.0 / p), lj ** (-1.0 / p)
+
+    def g(xa, xb, la, lb):
+        return sum(xa ** l * xb ** (p - 1 - l) * lb for l in range(p - 1)) + xa ** (p - 1) * la
+    return 1.0 - (xi * g(xi, xj, li, lj) + xj * g(xj, xi, lj, li)) / (2 * p)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_linearisation_at_fixed_point_matches_derivation(p):
+    n = 24
+    A, lam, Q = synth.spd(n, 10.0, 7, return_eig=True)
+    X = (Q * lam[None, :] ** (-1.0 / p)) @ Q.T
+    X = (X + X.T) / 2
+    _, X1, _ = oracle.step_sym(A, X, p, oracle.phase())
+    eps = 1e-7
+    for (i, j) in [(0, 1), (0, 5), (3, 9), (4, 4)]:
+        E = np.outer(Q[:, i], Q[:, j])
+        E = eps * (E + E.T)
+        C = X + E
+        C = (C + C.T) / 2
+        _, C1, _ = oracle.step_sym(A, C, p, oracle.phase())
+        mu = np.sum((C1 - X1) * E) / np.sum(E * E)
+        assert mu == pytest.approx(_mu_pred(p, lam[i], lam[j]), abs=2e-5), (p, i, j)
+
+
+def test_linearisation_predicts_stability_threshold():
+    # the derived multiplier leaves the unit disc at kappa ~ 34 for p = 2 (SURVEY A12 measured
+    # stable at 30, growing at 40)
+    r = np.geomspace(1 / 30, 30, 2001)
+    assert max(abs(_mu_pred(2, 1.0, x)) for x in r) < 1
+    r = np.geomspace(1 / 40, 40, 2001)
+    assert max(abs(_mu_pred(2, 1.0, x)) for x in r) > 1
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_diagonal_limit_closed_form(p):
+    a = np.array([0.3, 0.55, 0.8, 1.0, 0.9])
+    r = oracle.solve(np.diag(a), p, [oracle.phase()], 1e-14, 200, form=SYM)
+    assert r.outcome == oracle.CONVERGED
+    np.testing.assert_allclose(np.diag(r.C_best), a ** (-1.0 / p), rtol=8 * 2.0 ** -52)
+    assert np.count_nonzero(r.C_best - np.diag(np.diag(r.C_best))) == 0
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_twin_limit_is_eigen_root(p):
+    A = synth.spd(64, 2.0, 0)
+    r = oracle.solve(A, p, [oracle.phase()], 1e-12, 100, form=SYM)
+    assert r.outcome == oracle.CONVERGED
+    ref = np.real(scipy.linalg.fractional_matrix_power(A, -1.0 / p))
+    assert np.linalg.norm(r.C_best - ref) / np.linalg.norm(ref) < 1e-12
+    last = r.records[-1]
+    assert last["rho_cert"] <= 1e-12          # certified ||I - C^p A||_F (reading R-3)
+
+
+def test_iterates_exactly_symmetric_and_match_spectral_predictor():
+    n, p = 48, 2
+    A, lam, _ = synth.spd(n, 5.0, 2, return_eig=True)
+    r = oracle.solve(A, p, [oracle.phase()], 0.0, 14, hist=14, form=SYM)
+    for k in range(14):
+        Ck = r.C_hist[k]
+        assert np.array_equal(Ck, Ck.T), k
+    # exact-arithmetic iterates are polynomials in A: rho_s(C_k) = ||I - C^p A||_F, so the
+    # O(n) spectral recurrence of Eq. (1) predicts rho_hat until rounding matters
+    pred = oracle.spectral(lam, p, r.s, 14)
+    got = np.array([x["rho_hat"] for x in r.records[:14]])
+    ok = pred > 1e-6
+    np.testing.assert_allclose(got[ok], pred[ok], rtol=1e-8)
+
+
+def test_mixed_precision_refinement_is_fast_where_literal_is_not():
+    # literal Eq. (1) needs ~60 FP64 iterations after a BF16 phase (kappa = 2);
+    # the symmetrised correction removes the non-commuting noise at rate max|mu| ~ 0.03.
+    A = synth.spd(128, 2.0, 5)
+    low = oracle.phase(oracle.BF16, plateau_ratio=0.7, plateau_arm=0.5, max_iters=60)
+    lit = oracle.solve(A, 2, [low, oracle.phase()], 1e-12, 300)
+    sym = oracle.solve(A, 2, [low, oracle.phase()], 1e-12, 300, form=SYM)
+    sym_c = oracle.solve(A, 2, [low, oracle.phase(corr_prec=oracle.BF16)], 1e-12, 300, form=SYM)
+    fp64 = oracle.solve(A, 2, [oracle.phase()], 1e-12, 300, form=SYM)
+    n64 = lambda r: sum(1 for x in r.records if x["phase"] == 1)
+    assert all(r.outcome == oracle.CONVERGED for r in (lit, sym, sym_c, fp64))
+    assert n64(sym) <= 10 and n64(sym_c) <= 10 and n64(lit) >= 3 * n64(sym)
+    assert n64(sym) < len(fp64.records)
+
+
+def test_bf16_correction_in_fp64_phase_still_reaches_fp64_accuracy():
+    A = synth.spd(96, 2.0, 1)
+    r = oracle.solve(A, 2, [oracle.phase(corr_prec=oracle.BF16)], 1e-12, 100, form=SYM)
+    ref = np.real(scipy.linalg.fractional_matrix_power(A, -0.5))
+    assert r.outcome == oracle.CONVERGED
+    assert np.linalg.norm(r.C_best - ref) / np.linalg.norm(ref) < 1e-12
+
+
+def test_stable_at_kappa_10_where_literal_diverges():
+    A = synth.spd(96, 10.0, 3)
+    lit = oracle.solve(A, 2, [oracle.phase()], 1e-12, 120)
+    sym = oracle.solve(A, 2, [oracle.phase()], 1e-12, 120, form=SYM)
+    assert lit.outcome != oracle.CONVERGED
+    assert sym.outcome == oracle.CONVERGED
+
+
+def test_rejects_p1_and_fp16():
+    with pytest.raises(ValueError):
+        oracle.solve(np.eye(4), 1, [oracle.phase()], form=SYM)
+    with pytest.raises(ValueError):
+        oracle.solve(np.eye(4), 2, [oracle.phase(oracle.FP16), oracle.phase()], form=SYM)
+    assert np.isnan(oracle.step_sym(np.eye(2), np.eye(2), 1, oracle.phase())[0])
