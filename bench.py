@@ -28,6 +28,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "time-to-FP64-residual 1e-12 (n=8192, p=2)"
+# headline schedule: BF16 tensor-core phase, then FP64 refinement with a BF16 correction GEMM,
+# in the symmetrised-correction form (NEXT-2, R-22)
+DEFAULT_SCHEDULE = "sym:bf16>fp64/cbf16"
+EXTRA_SCHEDULES = ["fp64", "bf16>fp64", "tf32>fp64", "fp16>fp64", "sym:fp64", "sym:fp64/cbf16",
+                   "sym:bf16>fp64", "sym:tf32>fp64/cbf16", "sym:bf16>tf32>fp64/cbf16"]
 FP64_PEAK_TFLOPS = 37.1   # measured DMMA issue peak on this pool (profiles/r01_calibration.md)
 FP64_PEAK_SRC = "measured DMMA.8x8x4 issue peak, tools/probes/dmma_rate.cu (MEASURED_PEAKS.json has no FP64 figure)"
 
@@ -39,21 +44,43 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", default="H_twin")
-    ap.add_argument("--schedule", default="fp64", help="fp64 | bf16-fp64 | tf32-fp64 | fp16-fp64")
+    ap.add_argument("--schedule", default=DEFAULT_SCHEDULE,
+                    help="[sym:|ns:]phase>phase..., phase = prec[/c<corr prec>], e.g. fp64, bf16>fp64, "
+                         "sym:bf16>fp64/cbf16 (sym: = IPR_FORM_SYMMETRIC, NEXT-2)")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     return ap.parse_args()
 
 
+def parse_schedule(name):
+    """'sym:bf16>fp64/cbf16' -> ("symmetric", [("bf16", -1), ("fp64", "bf16")])."""
+    form = "literal"
+    if ":" in name:
+        f, name = name.split(":", 1)
+        form = {"sym": "symmetric", "ns": "newton_schulz", "lit": "literal"}[f]
+    parts = []
+    for ph in name.replace("-", ">").split(">"):
+        prec, _, corr = ph.partition("/c")
+        parts.append((prec, corr or -1))
+    return form, parts
+
+
 def schedule(name, n):
+    """Phases of a named schedule.  Every phase but the last is left on an armed plateau (and,
+    in the literal form, at rho_hat <= 1e-2) -- reading R-5; the last runs to final_tol."""
     import paper_1703_02283_b200 as ipr
-    fp64 = ipr.make_phase("fp64")
-    if name == "fp64":
-        return [fp64]
-    low = name.split("-")[0]
-    # leave the low phase at rho_hat <= 1e-2 or on an armed plateau (reading R-5)
-    return [ipr.make_phase(low, switch_tol=1e-2 * math.sqrt(n), plateau_ratio=0.7, plateau_arm=0.5,
-                           max_iters=40), fp64]
+    form, parts = parse_schedule(name)
+    out = []
+    for i, (prec, corr) in enumerate(parts):
+        if i == len(parts) - 1:
+            out.append(ipr.make_phase(prec, corr_prec=corr))
+        else:
+            # the symmetric form damps low-precision noise in the next phase, so a low phase runs
+            # to its plateau; the literal form leaves at rho_hat <= 1e-2 as well
+            sw = 0.0 if form == "symmetric" else 1e-2 * math.sqrt(n)
+            out.append(ipr.make_phase(prec, switch_tol=sw, plateau_ratio=0.7, plateau_arm=0.5,
+                                      max_iters=40, corr_prec=corr))
+    return form, out
 
 
 def gemm_count(trace, p):
@@ -188,10 +215,10 @@ def main():
     A, lam = synth.spd_torch(n, kappa, seed, device="cuda")
     C_out = torch.empty_like(A)
     torch.cuda.synchronize()
-    phases = schedule(args.schedule, n)
+    form, phases = schedule(args.schedule, n)
 
     def solve(A_dev, out):
-        s = ipr.Solver(A_dev, p, phases, 1e-12, stream, world, rank, uid)
+        s = ipr.Solver(A_dev, p, phases, 1e-12, stream, world, rank, uid, form=form)
         s.iterate(400)
         tr = s.trace()
         outcome = s.outcome
@@ -225,19 +252,25 @@ def main():
         ms = float(t.item())
     tr, outcome = traces[-1]
     ok = outcome == ipr.IPR_CONVERGED
+    cert = [t["rho_cert"] for t in tr if t["rho_cert"] == t["rho_cert"]]
+    final_rho = cert[-1] if cert else tr[-1]["rho"]
 
     # roofline of the dominant kernel (the FP64 DMMA GEMM): algorithmic flops per launch =
     # 2 n^3 (local panel: 2 n^2 n/G); duration from the library's CUDA events on the launch stream
     fl_gemm = 2.0 * n * n * (n / world)
-    tot_ms = sum(t["gemm_ms"] for trc, _ in traces for t in trc if t["prec"] == "fp64")
-    tot_gemms = sum(gemm_count([t for t in trc if t["prec"] == "fp64"], p) for trc, _ in traces)
+    # the p chain GEMMs of every FP64 record (gemm_ms - upd_ms: the update may be a BF16
+    # correction GEMM + k_sym_update in the symmetric form)
+    tot_ms = sum(t["gemm_ms"] - t["upd_ms"] for trc, _ in traces for t in trc if t["prec"] == "fp64")
+    tot_gemms = sum(p * sum(1 for t in trc if t["prec"] == "fp64") for trc, _ in traces)
     gemm_ms = tot_ms / max(tot_gemms, 1)
     achieved = fl_gemm / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    all_ms = sum(t["gemm_ms"] for trc, _ in traces for t in trc)
     step_gemm_share = tot_ms / (ms * args.steps) if ms > 0 else None
     roof = {"bound": "tensor", "kernel": "k_gemm_dmma (FP64 DMMA.8x8x4)", "achieved": achieved,
             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
             "traffic": None, "peak_source": FP64_PEAK_SRC, "cublas_dgemm_tflops": 35.5,
-            "algorithmic_flops_per_launch": fl_gemm, "avg_launch_ms": gemm_ms, "gemm_share_of_step": step_gemm_share}
+            "algorithmic_flops_per_launch": fl_gemm, "avg_launch_ms": gemm_ms, "gemm_share_of_step": step_gemm_share,
+            "all_gemm_share_of_step": all_ms / (ms * args.steps) if ms > 0 else None}
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
@@ -273,34 +306,33 @@ def main():
     if not args.no_extras and world == 1:
         # the other half of the metric: GEMM TFLOP/s per precision, and the mixed schedules
         sched = {}
-        for name in ["bf16-fp64", "tf32-fp64", "fp16-fp64"]:
-            ph = schedule(name, n)
+        for name in EXTRA_SCHEDULES:
+            f2, ph = schedule(name, n)
             torch.cuda.synchronize()
             g0 = torch.cuda.Event(enable_timing=True)
             g1 = torch.cuda.Event(enable_timing=True)
             g0.record(stream)
-            s = ipr.Solver(A, p, ph, 1e-12, stream)
+            s = ipr.Solver(A, p, ph, 1e-12, stream, form=f2)
             s.iterate(400)
             t2 = s.trace()
             out2 = s.outcome
             s.finalize(C_out)
             g1.record(stream)
             torch.cuda.synchronize()
-            low = name.split("-")[0]
-            lms = sum(t["gemm_ms"] for t in t2 if t["prec"] == low)
-            lg = gemm_count([t for t in t2 if t["prec"] == low], p)
+            precs = [ipr.PREC_NAMES[q.prec] for q in ph]
+            low = precs[0] if len(precs) > 1 else None
+            lms = sum(t["gemm_ms"] for t in t2 if t["prec"] == low) if low else 0.0
+            lg = gemm_count([t for t in t2 if t["prec"] == low], p) if low else 0
+            c2 = [t["rho_cert"] for t in t2 if t["rho_cert"] == t["rho_cert"]]
             sched[name] = {"time_s": g0.elapsed_time(g1) / 1e3, "outcome": ipr.OUTCOME_NAMES[out2],
-                           "iters_low": sum(1 for t in t2 if t["prec"] == low),
-                           "iters_fp64": sum(1 for t in t2 if t["prec"] == "fp64"),
-                           "final_rho": t2[-1]["rho"],
+                           "iters_per_phase": [sum(1 for t in t2 if t["phase"] == i) for i in range(len(ph))],
+                           "final_rho": c2[-1] if c2 else t2[-1]["rho"],
                            "gemm_tflops_low": (lg * 2.0 * n ** 3 / (lms * 1e-3) / 1e12) if lms > 0 else None}
-        sched["fp64"] = {"time_s": ms / 1e3, "outcome": ipr.OUTCOME_NAMES[outcome], "iters_fp64": len(tr),
-                         "final_rho": tr[-1]["rho"]}
         extras["schedules"] = sched
         extras["gemm_tflops"] = {"fp64": achieved,
-                                 "bf16": sched["bf16-fp64"]["gemm_tflops_low"],
-                                 "tf32": sched["tf32-fp64"]["gemm_tflops_low"],
-                                 "fp16": sched["fp16-fp64"]["gemm_tflops_low"]}
+                                 "bf16": sched["bf16>fp64"]["gemm_tflops_low"],
+                                 "tf32": sched["tf32>fp64"]["gemm_tflops_low"],
+                                 "fp16": sched["fp16>fp64"]["gemm_tflops_low"]}
         extras["gemm_frac_of_peak"] = {
             "fp64": achieved / FP64_PEAK_TFLOPS if achieved else None,
             "bf16_vs_measured_bf16_burst_1599": (extras["gemm_tflops"]["bf16"] or 0) / 1599.0,
@@ -318,7 +350,8 @@ def main():
     line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
-            "converged": ok, "iterations": len(tr), "final_rho": tr[-1]["rho"],
+            "converged": ok, "iterations": len(tr), "final_rho": final_rho,
+            "iters_per_phase": [sum(1 for t in tr if t["phase"] == i) for i in range(len(phases))],
             "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary()}
     line.update(extras)

@@ -83,6 +83,11 @@ typedef struct {
   double    plateau_ratio; /* 0 = off (typ. 0.7)                                              */
   double    plateau_arm;   /* typ. 0.5                                                        */
   int       max_iters;     /* per-phase cap on chains; 0 = unlimited                          */
+  int       corr_prec;     /* IPR_FORM_SYMMETRIC only: ipr_prec of the correction GEMM        */
+                           /* W = qc(C) qc(I - C^{p-1}AC); -1 = prec.  FP16 unsupported; FP64 */
+                           /* only in FP64 phases.  A BF16/TF32 correction in an FP64 phase   */
+                           /* is mixed-precision refinement: R is small, so W needs only      */
+                           /* relative accuracy (R-22).  Ignored by other forms.    */
 } ipr_phase;
 
 /* Trace record: one per evaluated iterate C_k (one chain of p GEMMs). */
@@ -96,6 +101,11 @@ typedef struct {
   double rho_hat;    /* rho / sqrt(n)                                                        */
   double delta;      /* ||C_{k+1} - C_k||_F of the update that followed (NaN if none)        */
   double gemm_ms;    /* device time of this record's GEMMs (chain + update), CUDA events     */
+  double upd_ms;     /* the part of gemm_ms spent in the update (GEMM p+1 + its epilogue /    */
+                     /* k_sym_update); gemm_ms - upd_ms = the chain's p GEMMs                  */
+  double rho_cert;   /* IPR_FORM_SYMMETRIC: ||I - C^p A||_F recomputed in FP64 when the      */
+                     /* in-chain rho met final_tol (converged iff rho_cert <= final_tol);    */
+                     /* NaN otherwise                                                         */
 } ipr_record;
 
 /* Create a context for an n x n SPD matrix A (FP64, row-major, device, leading dimension
@@ -123,8 +133,20 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
  * NEXT-1): two GEMMs per iteration, T = Ahat Xhat with the fused residual ||I - T||_F and
  * What = qin(2I - T), then X_{k+1} = q_m(Xhat What).  Its error is quadratic in the deviation
  * (no linear term), so low-precision noise is removed by the FP64 phase.  Call before the
- * first ipr_iterate; a p != 1 schedule with this form fails at ipr_iterate (INVALID_ARG). */
-typedef enum { IPR_FORM_LITERAL = 0, IPR_FORM_NEWTON_SCHULZ = 1 } ipr_form;
+ * first ipr_iterate; a p != 1 schedule with this form fails at ipr_iterate (INVALID_ARG).
+ *
+ * IPR_FORM_SYMMETRIC (p >= 2; BF16/TF32/FP64 phases): the Newton correction
+ * of Eq. (1) (C_{k+1} = C_k + C_k (I - C_k^p A) / p) with the residual taken as
+ * R = I - C^{p-1} A C and the correction symmetrised (reading R-22):
+ *   Z_1 = Ahat Chat, Z_j = Chat qin(Z_{j-1}) (j = 2..p), rho_s = ||I - Z_p||_F (fused),
+ *   Rhat = qc(I - Z_p);  W = qc(C) Rhat;  C_{k+1} = q_m(C + (W + W^T) / (2p)).
+ * C_k stays exactly symmetric; at the fixed point the error multiplier is
+ * mu_ij = 1 - (x_i g_ij + x_j g_ji)/(2p) (|mu| <= 0.03 at kappa = 2, < 1 up to kappa ~ 34 for
+ * p = 2), so low-precision noise is damped in the FP64 phase instead of persisting.
+ * The trace's rho is rho_s; when it meets final_tol in the last phase the engine computes
+ * C_{k+1}, then certifies ||I - C_k^p A||_F with FP64 DMMA GEMMs: converged if that is <=
+ * final_tol (record.rho_cert), else the iteration continues from C_{k+1}. */
+typedef enum { IPR_FORM_LITERAL = 0, IPR_FORM_NEWTON_SCHULZ = 1, IPR_FORM_SYMMETRIC = 2 } ipr_form;
 ipr_status ipr_set_form(ipr_ctx *c, int form);
 
 /* Run at most max_iters (> 0) chains.  *iters_done = chains evaluated by this call,

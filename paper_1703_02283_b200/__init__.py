@@ -32,8 +32,9 @@ EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_
             "ipr_get_iterate", "ipr_get_norms", "ipr_finalize", "ipr_last_error",
             "ipr_nccl_unique_id", "ipr_version", "ipr_test_quantize", "ipr_test_gemm",
             "ipr_launch_count", "ipr_plan", "ipr_set_form"]
-IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ = 0, 1
-FORM_BY_NAME = {"literal": IPR_FORM_LITERAL, "newton_schulz": IPR_FORM_NEWTON_SCHULZ, "ns": IPR_FORM_NEWTON_SCHULZ}
+IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ, IPR_FORM_SYMMETRIC = 0, 1, 2
+FORM_BY_NAME = {"literal": IPR_FORM_LITERAL, "newton_schulz": IPR_FORM_NEWTON_SCHULZ, "ns": IPR_FORM_NEWTON_SCHULZ,
+                "symmetric": IPR_FORM_SYMMETRIC, "sym": IPR_FORM_SYMMETRIC}
 
 
 class IprError(RuntimeError):
@@ -45,13 +46,14 @@ class IprError(RuntimeError):
 class ipr_phase(C.Structure):
     _fields_ = [("prec", C.c_int), ("mant_bits", C.c_int), ("round", C.c_int),
                 ("switch_tol", C.c_double), ("plateau_ratio", C.c_double),
-                ("plateau_arm", C.c_double), ("max_iters", C.c_int)]
+                ("plateau_arm", C.c_double), ("max_iters", C.c_int), ("corr_prec", C.c_int)]
 
 
 class ipr_record(C.Structure):
     _fields_ = [("k", C.c_int), ("phase", C.c_int), ("prec", C.c_int), ("mant_bits", C.c_int),
                 ("decision", C.c_int), ("rho", C.c_double), ("rho_hat", C.c_double),
-                ("delta", C.c_double), ("gemm_ms", C.c_double)]
+                ("delta", C.c_double), ("gemm_ms", C.c_double), ("upd_ms", C.c_double),
+                ("rho_cert", C.c_double)]
 
 
 def _load():
@@ -139,10 +141,11 @@ def ipr_init(n: int, A, lda: int | None = None, stream=None, world: int = 1, ran
 
 
 def make_phase(prec="fp64", mant_bits=-1, round="rne", switch_tol=0.0, plateau_ratio=0.0,
-               plateau_arm=0.5, max_iters=0) -> ipr_phase:
+               plateau_arm=0.5, max_iters=0, corr_prec=-1) -> ipr_phase:
     pr = PREC_BY_NAME[prec] if isinstance(prec, str) else int(prec)
     rd = {"rne": IPR_RNE, "rtz": IPR_RTZ}[round] if isinstance(round, str) else int(round)
-    return ipr_phase(pr, mant_bits, rd, switch_tol, plateau_ratio, plateau_arm, max_iters)
+    cp = PREC_BY_NAME[corr_prec] if isinstance(corr_prec, str) else int(corr_prec)
+    return ipr_phase(pr, mant_bits, rd, switch_tol, plateau_ratio, plateau_arm, max_iters, cp)
 
 
 def ipr_set_schedule(ctx, p: int, phases, final_tol: float):
@@ -173,7 +176,8 @@ def ipr_get_trace(ctx):
     buf = (ipr_record * max(cnt.value, 1))()
     _check(_lib.ipr_get_trace(ctx, buf, cnt.value, C.byref(cnt)), ctx)
     return [dict(k=r.k, phase=r.phase, prec=PREC_NAMES[r.prec], mant_bits=r.mant_bits,
-                 decision=r.decision, rho=r.rho, rho_hat=r.rho_hat, delta=r.delta, gemm_ms=r.gemm_ms)
+                 decision=r.decision, rho=r.rho, rho_hat=r.rho_hat, delta=r.delta, gemm_ms=r.gemm_ms,
+                 upd_ms=r.upd_ms, rho_cert=r.rho_cert)
             for r in buf[:cnt.value]]
 
 

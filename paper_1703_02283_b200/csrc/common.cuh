@@ -22,8 +22,10 @@ enum EpiMode : int {
   EPI_UPDATE = 4,     // C_next = q_m(((p+1) C - scale*D) / p), Chat_next, delta partials
   EPI_F64 = 8,        // test hook: FP64 row-major store of scale*D
   EPI_TSCRATCH = 16,  // FP16 phase: FP32 store of scale*D transposed + per-tile max|.|
-  EPI_TWO_I_MINUS = 32,  // modifier of STORE_T/TSCRATCH: store 2*delta_ij - D (Newton-Schulz W)
+  EPI_DIAG_MINUS = 32,  // modifier of STORE_T/TSCRATCH: store diag*delta_ij - D (Newton-Schulz
+                        // What = 2I - T with diag = 2; symmetric form R = I - Z_p with diag = 1)
   EPI_NSUPDATE = 64,  // Newton-Schulz: X_{k+1} = q_m(D) -> container, operand, delta partials
+  EPI_WSTORE = 128,   // symmetric form: W = D row-major to wout[i * ldw + j] (FP32, or FP64 if w64)
 };
 
 struct GemmArgs {
@@ -35,6 +37,9 @@ struct GemmArgs {
   // B operand, K-major: element (k,j) at B + j * ldb + k
   const void *B; int64_t ldb;
   int prec, mode;
+  int tprec;            // operand format of the EPI_STORE_T output (= prec except the symmetric
+                        // form's Rhat, stored in the correction format)
+  double diag;          // EPI_DIAG_MINUS coefficient
   const int *sigA, *sigB; // FP16 phase: device scale exponents of the A / B operands; else NULL
   // EPI_STORE_T / EPI_TSCRATCH: T(i,j) -> tout[j * ldt + i]
   void *tout; int64_t ldt;
@@ -47,6 +52,8 @@ struct GemmArgs {
   int p, m, rtz, cont64;
   // EPI_F64
   double *zout; int64_t ldz;
+  // EPI_WSTORE
+  void *wout; int64_t ldw; int w64;
 };
 
 // ------------------------------------------------------------------------------------

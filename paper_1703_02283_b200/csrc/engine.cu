@@ -35,6 +35,7 @@ thread_local std::string t_err;
 
 struct PhaseC {
   int prec, m, rtz, cont64;
+  int corr;                    // symmetric form: operand format of the correction GEMM
   double switch_tol, plateau_ratio, plateau_arm;
   int max_iters;
 };
@@ -64,7 +65,10 @@ struct ipr_ctx {
   double *best = nullptr;                // FP64 local panel
   void *T[2] = {nullptr, nullptr};      // chain intermediates, K-major [kp][npad]
   void *Aop = nullptr;                  // stage-A operand of the current phase [kp][npad]
-  void *Afull = nullptr;                // Newton-Schulz, world > 1: full row-major Ahat (A operand)
+  void *Afull = nullptr;                // NS / symmetric, world > 1: full row-major Ahat (A operand)
+  void *chatc[2] = {nullptr, nullptr};  // symmetric form: Chat in the correction format (panel-major)
+  void *wbuf = nullptr;                 // symmetric form: W = qc(C) Rhat, full panel-major
+  int wbytes = 4;                       // allocated element size of wbuf (8 if any FP64 correction)
   int form = IPR_FORM_LITERAL;          // iteration form (ipr_set_form)
   float *tscr = nullptr;                // FP16 phase T scratch (FP32)
   double *full64 = nullptr;             // FP64 npad x npad scratch (copy-out / certify)
@@ -78,6 +82,7 @@ struct ipr_ctx {
   int best_cont64 = 1;
   int64_t pending_delta = -1;           // trace record whose delta is in flight
   std::vector<ipr_record> trace;
+  void *arena = nullptr;                // every O(n^2) buffer: ONE cudaMalloc at the first ipr_iterate
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   bool upd_timed = false;
 };
@@ -180,7 +185,7 @@ GemmArgs base_args(ipr_ctx *c, int prec, const void *Bop) {
   GemmArgs g;
   memset(&g, 0, sizeof g);
   g.M = c->npad; g.N = c->kp; g.K = c->npad; g.n = c->n; g.col0 = c->col0;
-  g.B = Bop; g.ldb = c->npad; g.prec = prec;
+  g.B = Bop; g.ldb = c->npad; g.prec = prec; g.tprec = prec;
   g.tiles_m = tiles_m(c, prec);
   g.p = c->p;
   return g;
@@ -232,11 +237,27 @@ ipr_status save_best(ipr_ctx *c) {
 }
 
 ipr_status make_xt(ipr_ctx *c, int i, const PhaseC &P);
+void *chatc_slot(ipr_ctx *c, int i, int prec) {
+  return (char *)c->chatc[i] + (size_t)c->rank * (size_t)(c->npad * c->kp) * elt_size(prec);
+}
+ipr_status gather_bytes(ipr_ctx *c, void *base, size_t per_rank, const char *what) {
+  if (c->world == 1) return IPR_OK;
+  if (!c->comm.allgather((char *)base + c->rank * per_rank, base, per_rank, c->st))
+    return fail(c, IPR_E_NCCL, "ncclAllGather(%s) failed: %s", what, c->comm.last_error());
+  return IPR_OK;
+}
+// symmetric form: Chat of iterate buffer i in the correction format (if it differs from prec)
+ipr_status make_corr_operand(ipr_ctx *c, int i, const PhaseC &P) {
+  if (P.corr == P.prec) return IPR_OK;
+  const int64_t cnt = c->npad * c->kp;
+  CK(launch_make_operand(cont_ptr(c, i, P), P.cont64, cnt, P.corr, nullptr, chatc_slot(c, i, P.corr), c->st));
+  return gather_bytes(c, c->chatc[i], (size_t)cnt * elt_size(P.corr), "Chat corr");
+}
 
 ipr_status begin_phase(ipr_ctx *c, bool first) {
   const PhaseC &P = c->ph[c->phase];
   CKS(stage_a(c, P, c->Aop, c->dsig + 0));
-  if (c->form == IPR_FORM_NEWTON_SCHULZ && c->world > 1) {   // full row-major Ahat (A operand)
+  if (c->form != IPR_FORM_LITERAL && c->world > 1) {   // full row-major Ahat (A operand)
     CK(launch_stage_a(c->A, c->lda, c->n, c->npad, 0, c->npad, P.prec, P.cont64, P.m, P.rtz,
                       P.prec == IPR_FP16 ? c->dsig + 0 : nullptr, c->Afull, c->st));
   }
@@ -251,6 +272,10 @@ ipr_status begin_phase(ipr_ctx *c, bool first) {
   }
   CKS(make_operand(c, c->cur, P));
   if (c->form == IPR_FORM_NEWTON_SCHULZ) CKS(make_xt(c, c->cur, P));
+  if (c->form == IPR_FORM_SYMMETRIC) {
+    CKS(make_corr_operand(c, c->cur, P));
+    if (c->world > 1) CKS(make_xt(c, c->cur, P));
+  }
   return IPR_OK;
 }
 
@@ -277,7 +302,8 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
     g.A = c->world == 1 ? c->Aop : c->Afull;
     g.a_kp = c->npad; g.a_pstride = c->npad * c->npad;
     if (prec == IPR_FP16) { g.sigA = c->dsig + 0; g.sigB = c->dsig + 1 + c->cur; g.pmax = c->pmax; }
-    g.mode = (prec == IPR_FP16 ? EPI_TSCRATCH : EPI_STORE_T) | EPI_TWO_I_MINUS | EPI_RESID;
+    g.mode = (prec == IPR_FP16 ? EPI_TSCRATCH : EPI_STORE_T) | EPI_DIAG_MINUS | EPI_RESID;
+    g.diag = 2.0;
     g.tout = (prec == IPR_FP16) ? (void *)c->tscr : c->T[1];
     g.ldt = c->npad;
     g.part = part;
@@ -286,6 +312,26 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
       CKS(gather_pmax(c, c->pmax, tn_loc * tm));
       CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 4, c->st));
       CK(launch_scale_fp16(c->tscr, c->kp * c->npad, c->dsig + 4, c->T[1], c->st));
+    }
+  }
+  if (c->form == IPR_FORM_SYMMETRIC) {
+    // Z_1 = Ahat Chat (A operand: Ahat row-major; B: Chat itself for G = 1 -- exactly symmetric --
+    // else the transposed local panel), Z_j = Chat qin(Z_{j-1}); GEMM p: R = I - Z_p in the
+    // correction format (K-major for the W GEMM) + residual partials.  Z_j -> T[j & 1].
+    for (int j = 1; j <= c->p; ++j) {
+      GemmArgs g = base_args(c, prec, j == 1 ? (c->world == 1 ? c->chat[c->cur] : c->T[0]) : c->T[(j - 1) & 1]);
+      if (j == 1) {
+        g.A = c->world == 1 ? c->Aop : c->Afull;
+        g.a_kp = c->npad; g.a_pstride = c->npad * c->npad;
+      } else {
+        chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
+      }
+      g.mode = EPI_STORE_T;
+      if (j == c->p) { g.mode |= EPI_DIAG_MINUS | EPI_RESID; g.diag = 1.0; g.tprec = P.corr; }
+      g.tout = c->T[j & 1];
+      g.ldt = c->npad;
+      g.part = part;
+      CK(run_gemm(c, g));
     }
   }
   for (int j = 1; c->form == IPR_FORM_LITERAL && j <= c->p; ++j) {
@@ -317,6 +363,7 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
   if (c->pending_delta >= 0) {
     c->trace[c->pending_delta].delta = std::sqrt(c->hscal[1]);
     c->trace[c->pending_delta].gemm_ms += tu;
+    c->trace[c->pending_delta].upd_ms = tu;
     c->pending_delta = -1;
   }
   *rho_out = std::sqrt(c->hscal[0]);
@@ -362,6 +409,41 @@ ipr_status update(ipr_ctx *c) {
   return IPR_OK;
 }
 
+// ---- symmetric form (NEXT-2): W = qc(C) Rhat, then C_{k+1} = q_m(C + (W + W^T)/(2p)) ----
+ipr_status update_sym(ipr_ctx *c) {
+  const PhaseC &P = c->ph[c->phase];
+  const int nx = 1 - c->cur;
+  if (c->best_loc == nx) CKS(save_best(c));
+  GemmArgs g = base_args(c, P.corr, c->T[c->p & 1]);
+  if (P.corr == P.prec) chat_view(c, c->cur, P.prec, &g.A, &g.a_kp, &g.a_pstride);
+  else { g.A = c->chatc[c->cur]; g.a_kp = c->kp; g.a_pstride = c->npad * c->kp; }
+  // W holds the exact accumulator values: FP64 for an FP64 (DMMA) correction, else FP32
+  const int wb = P.corr == IPR_FP64 ? 8 : 4;
+  g.mode = EPI_WSTORE;
+  g.w64 = wb == 8;
+  g.wout = (char *)c->wbuf + (size_t)c->rank * (size_t)(c->npad * c->kp) * wb;
+  g.ldw = c->kp;
+  CK(cudaEventRecord(c->ev[2], c->st));
+  CK(run_gemm(c, g));
+  CKS(gather_bytes(c, c->wbuf, (size_t)(c->npad * c->kp) * wb, "W"));
+  CK(launch_sym_update(cont_ptr(c, c->cur, P), P.cont64, cont_ptr(c, nx, P), c->wbuf, wb == 8, c->npad,
+                       c->kp, c->col0, c->p, P.m, P.rtz, P.prec,
+                       P.prec == IPR_FP64 ? nullptr : chat_slot(c, nx, P.prec), P.corr,
+                       P.corr == P.prec ? nullptr : chatc_slot(c, nx, P.corr), c->part, c->st));
+  CK(cudaEventRecord(c->ev[3], c->st));
+  c->upd_timed = true;
+  const int64_t t64 = c->npad / 64;
+  CKS(gather_partials(c, c->part, (c->kp / 64) * t64));
+  CK(launch_reduce_sum(c->part, t64 * t64, c->dscal + 1, c->st));
+  CKS(gather_chat(c, nx, P.prec));
+  if (P.corr != P.prec) CKS(gather_bytes(c, c->chatc[nx], (size_t)(c->npad * c->kp) * elt_size(P.corr), "Chat corr"));
+  if (c->world > 1) CKS(make_xt(c, nx, P));
+  c->cur = nx;
+  return IPR_OK;
+}
+
+ipr_status step_update(ipr_ctx *c) { return c->form == IPR_FORM_SYMMETRIC ? update_sym(c) : update(c); }
+
 // Controller, reading R-5 (independent implementation of the rules in DESIGN.md).
 int decide(ipr_ctx *c, double rho, bool *best_new) {
   const PhaseC &P = c->ph[c->phase];
@@ -388,10 +470,7 @@ int decide(ipr_ctx *c, double rho, bool *best_new) {
 
 void free_ctx(ipr_ctx *c) {
   if (!c) return;
-  cudaFree(c->chat[0]); cudaFree(c->chat[1]); cudaFree(c->cont[0]); cudaFree(c->cont[1]);
-  cudaFree(c->best); cudaFree(c->T[0]); cudaFree(c->T[1]); cudaFree(c->Aop); cudaFree(c->tscr);
-  cudaFree(c->Afull);
-  cudaFree(c->full64); cudaFree(c->Acert); cudaFree(c->part); cudaFree(c->pmax); cudaFree(c->dscal);
+  cudaFree(c->arena); cudaFree(c->dscal);
   cudaFree(c->dsig); cudaFree(c->colsum); cudaFree(c->dflag);
   if (c->hscal) cudaFreeHost(c->hscal);
   for (auto &e : c->ev) if (e) cudaEventDestroy(e);
@@ -399,9 +478,39 @@ void free_ctx(ipr_ctx *c) {
   delete c;
 }
 
+// All O(n^2) buffers in one arena, sized once the schedule and the form are known (first
+// ipr_iterate): one cudaMalloc / cudaFree per solve, and an OOM is reported before any work.
+ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
+  const size_t full = (size_t)(c->npad * c->npad), panel = (size_t)(c->npad * c->kp);
+  bool fp16 = false;
+  for (auto &P : c->ph) fp16 |= P.prec == IPR_FP16;
+  struct Slot { void **p; size_t bytes; };
+  const Slot slots[] = {
+      {&c->chat[0], full * 8}, {&c->chat[1], full * 8}, {&c->cont[0], panel * 4}, {&c->cont[1], panel * 4},
+      {(void **)&c->best, panel * 8}, {&c->T[0], panel * 8}, {&c->T[1], panel * 8}, {&c->Aop, panel * 8},
+      {(void **)&c->part, (size_t)c->npart * 8}, {(void **)&c->pmax, (size_t)c->npart * 4},
+      {(void **)&c->tscr, fp16 ? panel * 4 : 0},
+      {&c->Afull, (c->world > 1 && c->form != IPR_FORM_LITERAL) ? full * 8 : 0},
+      {&c->chatc[0], need_corr ? full * 4 : 0}, {&c->chatc[1], need_corr ? full * 4 : 0},
+      {&c->wbuf, c->form == IPR_FORM_SYMMETRIC ? full * c->wbytes : 0},
+      {(void **)&c->full64, full * 8}, {&c->Acert, panel * 8}};
+  size_t total = 0;
+  for (const Slot &q : slots) total += (q.bytes + 255) / 256 * 256;
+  char *base = nullptr;
+  CKS(dalloc(c, &base, total));
+  c->arena = base;
+  size_t off = 0;
+  for (const Slot &q : slots) {
+    *q.p = q.bytes ? base + off : nullptr;
+    off += (q.bytes + 255) / 256 * 256;
+  }
+  CK(cudaMemsetAsync(c->chat[0], 0, full * 8, c->st));
+  CK(cudaMemsetAsync(c->chat[1], 0, full * 8, c->st));
+  return IPR_OK;
+}
+
 // FP64 full matrix (panel-major [G][npad][kp]) of a local FP64 panel -> full64
 ipr_status gather_f64(ipr_ctx *c, const double *local) {
-  if (!c->full64) CKS(dalloc(c, &c->full64, (size_t)(c->npad * c->npad) * 8));
   double *slot = c->full64 + (size_t)c->rank * c->npad * c->kp;
   if (local != slot) CK(cudaMemcpyAsync(slot, local, (size_t)(c->npad * c->kp) * 8, cudaMemcpyDeviceToDevice, c->st));
   if (c->world > 1 && !c->comm.allgather(slot, c->full64, (size_t)(c->npad * c->kp) * 8, c->st))
@@ -415,6 +524,8 @@ ipr_status gather_f64(ipr_ctx *c, const double *local) {
 // C-ABI
 // =========================================================================================
 extern "C" {
+
+static ipr_status certify_best(ipr_ctx *c, double *rho);
 
 const char *ipr_version(void) { return "ipr 0.1.0 (sm_100a: tcgen05 BF16/FP16/TF32, DMMA FP64)"; }
 
@@ -472,21 +583,8 @@ ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, 
   c->norms[3] = c->norms[0] * c->norms[1];   // s of Eq. (3)
   if (!(c->norms[3] > 0.0) || !std::isfinite(c->norms[3]))
     TRY(fail(c, IPR_E_INVALID_ARG, "ipr_init: ||A||_1 ||A||_inf = %g (zero or non-finite A)", c->norms[3]));
-  // buffers sized for the widest (FP64) phase
-  const size_t full = (size_t)(c->npad * c->npad) * 8, panel = (size_t)(c->npad * c->kp) * 8;
-  TRY(dalloc(c, &c->chat[0], full));
-  TRY(dalloc(c, &c->chat[1], full));
-  TRY(dalloc(c, &c->cont[0], panel / 2));
-  TRY(dalloc(c, &c->cont[1], panel / 2));
-  TRY(dalloc(c, &c->best, panel));
-  TRY(dalloc(c, &c->T[0], panel));
-  TRY(dalloc(c, &c->T[1], panel));
-  TRY(dalloc(c, &c->Aop, panel));
-  c->npart = (c->npad / 128) * (c->npad / 64) + 1024;   // one slot per 128 x 64 output tile
-  TRY(dalloc(c, &c->part, (size_t)c->npart * 8));
-  TRY(dalloc(c, &c->pmax, (size_t)c->npart * 4));
-  TRYC(cudaMemsetAsync(c->chat[0], 0, full, c->st));
-  TRYC(cudaMemsetAsync(c->chat[1], 0, full, c->st));
+  // O(n^2) buffers (sized for the widest, FP64, phase): one arena at the first ipr_iterate
+  c->npart = (c->npad / 64) * (c->npad / 64) + 1024;    // one slot per 64 x 64 tile (k_sym_update)
   if (world > 1) {
     std::string e;
     if (!c->comm.init(world, rank, nccl_unique_id, &e)) TRY(fail(c, IPR_E_NCCL, "%s", e.c_str()));
@@ -523,6 +621,10 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
       return fail(c, IPR_E_INVALID_ARG, "phase %d: plateau_ratio needs plateau_arm > 0", i);
     P.switch_tol = q.switch_tol; P.plateau_ratio = q.plateau_ratio; P.plateau_arm = q.plateau_arm;
     P.max_iters = q.max_iters;
+    P.corr = q.corr_prec < 0 ? q.prec : q.corr_prec;
+    if (P.corr < IPR_FP64 || P.corr > IPR_FP16) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad corr_prec", i);
+    if (P.corr == IPR_FP64 && P.prec != IPR_FP64)
+      return fail(c, IPR_E_INVALID_ARG, "phase %d: an FP64 correction needs an FP64 phase", i);
     const int ob = operand_bits(q.prec);
     if (ob < prev_ob || (ob == prev_ob && P.m < prev_m))
       return fail(c, IPR_E_INVALID_ARG, "phase %d: precision must be non-decreasing along the schedule", i);
@@ -536,15 +638,13 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
   if (p >= 2 && !(c->norms[2] > std::pow(2.0, -1.0 / (p - 1)))) {
     c->err = "warning: max diagonal <= 2^(-1/(p-1)): the sufficient condition for Eq. (2) (reading R-12) fails";
   }
-  for (auto &P : c->ph)
-    if (P.prec == IPR_FP16 && !c->tscr) CKS(dalloc(c, &c->tscr, (size_t)(c->npad * c->kp) * 4));
   return IPR_OK;
 }
 
 ipr_status ipr_set_form(ipr_ctx *c, int form) {
   if (!c) return fail(c, IPR_E_INVALID_ARG, "ipr_set_form: null context");
   if (c->started) return fail(c, IPR_E_STATE, "ipr_set_form: iteration already started");
-  if (form != IPR_FORM_LITERAL && form != IPR_FORM_NEWTON_SCHULZ)
+  if (form != IPR_FORM_LITERAL && form != IPR_FORM_NEWTON_SCHULZ && form != IPR_FORM_SYMMETRIC)
     return fail(c, IPR_E_INVALID_ARG, "ipr_set_form: unknown form %d", form);
   c->form = form;
   return IPR_OK;
@@ -559,8 +659,21 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
   if (!c->started) {
     if (c->form == IPR_FORM_NEWTON_SCHULZ) {
       if (c->p != 1) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: the Newton-Schulz form needs p = 1");
-      if (c->world > 1 && !c->Afull) CKS(dalloc(c, &c->Afull, (size_t)(c->npad * c->npad) * 8));
     }
+    bool need_c = false;
+    if (c->form == IPR_FORM_SYMMETRIC) {
+      if (c->p < 2) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: the symmetric form needs p >= 2 (p = 1: Newton-Schulz)");
+      c->wbytes = 4;
+      for (auto &P : c->ph) {
+        if (P.prec == IPR_FP16 || P.corr == IPR_FP16)
+          return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: FP16 phases are not implemented for the symmetric form");
+        if (P.corr != IPR_FP64 && !tc_supported(P.corr))
+          return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: tcgen05 path for the correction precision is not built");
+        need_c |= P.corr != P.prec;
+        if (P.corr == IPR_FP64) c->wbytes = 8;
+      }
+    }
+    if (!c->arena) CKS(alloc_arena(c, need_c));
     c->phase = 0; c->it_in_phase = 0; c->cur = 0;
     CKS(begin_phase(c, true));
     c->started = true;
@@ -577,10 +690,28 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     ipr_record r;
     r.k = (int)c->trace.size(); r.phase = phase_now; r.prec = c->ph[phase_now].prec; r.mant_bits = c->ph[phase_now].m;
     r.decision = d; r.rho = rho; r.rho_hat = rho / std::sqrt((double)c->n); r.delta = NAN; r.gemm_ms = ms;
+    r.rho_cert = NAN; r.upd_ms = 0.0;
     c->trace.push_back(r);
     *iters_done += 1;
+    if (d == IPR_DEC_CONVERGED && c->form == IPR_FORM_SYMMETRIC) {
+      // rho_s = ||I - C^{p-1}AC||_F met final_tol: compute C_{k+1} (the T buffers are consumed),
+      // then certify ||I - C_k^p A||_F in FP64 (R-3); continue from C_{k+1} if it misses.
+      CKS(update_sym(c));
+      c->pending_delta = (int64_t)c->trace.size() - 1;
+      double rc = NAN;
+      CKS(certify_best(c, &rc));
+      c->trace.back().rho_cert = rc;
+      if (!(rc <= c->final_tol)) {
+        c->trace.back().decision = IPR_DEC_CONTINUE;
+        if (c->world > 1) CKS(make_xt(c, c->cur, c->ph[c->phase]));
+        continue;
+      }
+      c->done = true;
+      c->outcome = d;
+      break;
+    }
     if (d == IPR_DEC_CONTINUE) {
-      CKS(update(c));
+      CKS(step_update(c));
       c->pending_delta = (int64_t)c->trace.size() - 1;
     } else if (d == IPR_DEC_SWITCH) {
       if (c->best_loc < 0) { c->best_loc = c->cur; c->best_cont64 = c->ph[c->phase].prec == IPR_FP64; }
@@ -607,6 +738,7 @@ ipr_status ipr_get_trace(ipr_ctx *c, ipr_record *buf, int cap, int *count) {
     if (c->upd_timed) { CK(cudaEventElapsedTime(&tu, c->ev[2], c->ev[3])); c->upd_timed = false; }
     c->trace[c->pending_delta].delta = std::sqrt(c->hscal[1]);
     c->trace[c->pending_delta].gemm_ms += tu;
+    c->trace[c->pending_delta].upd_ms = tu;
     c->pending_delta = -1;
   }
   *count = (int)c->trace.size();
@@ -625,7 +757,6 @@ ipr_status ipr_get_norms(ipr_ctx *c, double *out4) {
 
 static ipr_status copy_iterate(ipr_ctx *c, int which, double *dst, int64_t ldc) {
   const int64_t cnt = c->npad * c->kp;
-  if (!c->full64) CKS(dalloc(c, &c->full64, (size_t)(c->npad * c->npad) * 8));
   double *slot = c->full64 + (size_t)c->rank * cnt;
   if (which == 0) {
     const PhaseC &P = c->ph[c->phase];
@@ -649,13 +780,9 @@ ipr_status ipr_get_iterate(ipr_ctx *c, int which, double *C_dev_out, int64_t ldc
   return copy_iterate(c, which, C_dev_out, ldc);
 }
 
-ipr_status ipr_residual(ipr_ctx *c, int certify, double *rho) {
-  if (!c || !rho) return fail(c, IPR_E_INVALID_ARG, "ipr_residual: null pointer");
-  if (!c->started || c->trace.empty()) return fail(c, IPR_E_STATE, "ipr_residual: no iterate evaluated yet");
-  if (!certify) { *rho = c->last_rho; return IPR_OK; }
+static ipr_status certify_best(ipr_ctx *c, double *rho) {
   // reading R-3: ||I - C_best^p A||_F with FP64 DMMA GEMMs
   CKS(copy_iterate(c, 1, nullptr, 0));              // full64 = best (FP64, panel-major)
-  if (!c->Acert) CKS(dalloc(c, &c->Acert, (size_t)(c->npad * c->kp) * 8));
   PhaseC P64{IPR_FP64, 52, 0, 1, 0, 0, 0, 0};
   CKS(stage_a(c, P64, c->Acert, c->dsig + 0));
   const void *X = c->Acert;
@@ -673,6 +800,16 @@ ipr_status ipr_residual(ipr_ctx *c, int certify, double *rho) {
   CK(cudaMemcpyAsync(c->hscal + 2, c->dscal + 2, 8, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   *rho = std::sqrt(c->hscal[2]);
+  return IPR_OK;
+}
+
+ipr_status ipr_residual(ipr_ctx *c, int certify, double *rho) {
+  if (!c || !rho) return fail(c, IPR_E_INVALID_ARG, "ipr_residual: null pointer");
+  if (!c->started || c->trace.empty()) return fail(c, IPR_E_STATE, "ipr_residual: no iterate evaluated yet");
+  if (!certify) { *rho = c->last_rho; return IPR_OK; }
+  CKS(certify_best(c, rho));
+  // the certification chain reuses the T buffers: restore the transposed operand it clobbered
+  if (c->world > 1 && c->form != IPR_FORM_LITERAL && !c->done) CKS(make_xt(c, c->cur, c->ph[c->phase]));
   return IPR_OK;
 }
 

@@ -5,6 +5,8 @@
 //                GEMM, reading R-1: right-to-left chain T_j = Chat T_{j-1})
 //  EPI_RESID   : partial of rho^2 = sum (delta_ij - T_p,ij)^2 from the unrounded accumulator
 //                (the in-chain residual of reading R-4)
+//  EPI_WSTORE  : W = D row-major (symmetric form, NEXT-2); the update C + (W + W^T)/(2p)
+//                needs W^T, so it runs in k_sym_update (kernels.cu) after the GEMM
 //  EPI_UPDATE  : C_{k+1} = q_m(((p+1) C_k - P) / p)  with P = D: three separately rounded FP64
 //                operations and ONE rounding to m bits (reading R-2, Eq. (1) PAPER.md:71-73;
 //                approximate storage PAPER.md:133-136), plus Chat_{k+1} = qin(C_{k+1}) and the
@@ -33,13 +35,13 @@ __device__ __forceinline__ void epi_element(const GemmArgs &g, int64_t row, int6
   const int mode = MODE >= 0 ? MODE : g.mode;
   if (mode & (EPI_STORE_T | EPI_TSCRATCH)) {
     double w = v;
-    if (mode & EPI_TWO_I_MINUS) {     // Newton-Schulz W = 2I - A X (one FP64 subtraction)
+    if (mode & EPI_DIAG_MINUS) {      // diag*I - D: NS What = 2I - A X, symmetric R = I - Z_p
       const int64_t gc = g.col0 + col;
-      w = __dsub_rn((row == gc && row < g.n) ? 2.0 : 0.0, v);
+      w = __dsub_rn((row == gc && row < g.n) ? g.diag : 0.0, v);
     }
     if (mode & EPI_STORE_T) {
       // FP16 T operands go through EPI_TSCRATCH + a scale kernel (sigma 0 here)
-      store_operand(g.tout, col * g.ldt + row, g.prec, w, 0);
+      store_operand(g.tout, col * g.ldt + row, g.tprec, w, 0);
     } else {
       ((float *)g.tout)[col * g.ldt + row] = (float)w;
       acc.mx = fmaxf(acc.mx, fabsf((float)w));
@@ -100,6 +102,10 @@ __device__ __forceinline__ void epi_element(const GemmArgs &g, int64_t row, int6
     acc.d2 = __fma_rn(dd, dd, acc.d2);
   }
   if (mode & EPI_F64) g.zout[row * g.ldz + col] = v;
+  if (mode & EPI_WSTORE) {            // symmetric form: W = qc(C) Rhat, exact accumulator value
+    if (g.w64) ((double *)g.wout)[row * g.ldw + col] = v;
+    else ((float *)g.wout)[row * g.ldw + col] = (float)v;
+  }
 }
 
 }  // namespace ipr

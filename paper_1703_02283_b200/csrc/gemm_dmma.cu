@@ -179,6 +179,9 @@ cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s) {
   if (!a.pmax && a.prec == P_FP64) {
     if (a.mode == EPI_STORE_T) return launch_mode<EPI_STORE_T>(a, s);
     if (a.mode == (EPI_STORE_T | EPI_RESID)) return launch_mode<EPI_STORE_T | EPI_RESID>(a, s);
+    if (a.mode == (EPI_STORE_T | EPI_DIAG_MINUS | EPI_RESID))
+      return launch_mode<EPI_STORE_T | EPI_DIAG_MINUS | EPI_RESID>(a, s);
+    if (a.mode == EPI_WSTORE) return launch_mode<EPI_WSTORE>(a, s);
     if (a.mode == EPI_UPDATE && a.cont64 && !a.chat_new) return launch_mode<EPI_UPDATE>(a, s);
   }
   return launch_mode<-1>(a, s);

@@ -188,11 +188,11 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
       const double v = __dmul_rn((double)__uint_as_float(r[j]), scale);
       const int64_t c = col + j;
       double w = v;
-      if (mode & EPI_TWO_I_MINUS) {   // Newton-Schulz W = 2I - A X (one FP64 subtraction)
+      if (mode & EPI_DIAG_MINUS) {    // diag*I - D: NS What = 2I - A X, symmetric R = I - Z_p
         const int64_t gc = g.col0 + c;
-        w = __dsub_rn((row == gc && row < g.n) ? 2.0 : 0.0, v);
+        w = __dsub_rn((row == gc && row < g.n) ? g.diag : 0.0, v);
       }
-      if (mode & EPI_STORE_T) store_operand(g.tout, c * g.ldt + row, g.prec, w, 0);
+      if (mode & EPI_STORE_T) store_operand(g.tout, c * g.ldt + row, g.tprec, w, 0);
       if (mode & EPI_TSCRATCH) {
         ((float *)g.tout)[c * g.ldt + row] = (float)w;
         ea.mx = fmaxf(ea.mx, fabsf((float)w));
@@ -206,6 +206,15 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
       }
       if (mode & EPI_F64) g.zout[row * g.ldz + c] = v;
     }
+  }
+  if (mode & EPI_WSTORE) {
+    // symmetric form: W row segment [row][col .. col+31] as the exact FP32 accumulator values
+    // (scale is 1: no FP16 operands in this form), 16-byte stores
+    float4 *dst = (float4 *)((float *)g.wout + row * g.ldw + col);
+    #pragma unroll
+    for (int q = 0; q < 8; ++q)
+      dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
+                           __uint_as_float(r[4 * q + 3]));
   }
   if (mode & (EPI_UPDATE | EPI_NSUPDATE)) {
     // container row segment [row][col .. col+31]: 128 B (FP32) per thread, 16-byte accesses

@@ -235,6 +235,63 @@ __global__ void k_transpose(const T *src, int64_t rows, int64_t cols, T *dst) {
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// a6 of the symmetric form (R-22):
+//   C_{k+1}(i,j) = q_m(C(i,j) + (W(i,j) + W(j,i)) / (2p))
+// for the local column panel j in [col0, col0 + kp).  W is the FULL correction product in the
+// panel-major layout [G][npad][kp] (all-gathered for G > 1): W(r,c) at
+// (c / kp) * npad * kp + r * kp + c % kp.  64 x 64 tiles: W(j,i) of the mirrored tile is staged
+// through shared memory so both reads are coalesced.  W(i,j) + W(j,i) is commutative in IEEE,
+// so C_{k+1} is bitwise symmetric when C_k is.  Also writes the next operands (phase format
+// and correction format) and the per-tile partial of delta^2 = sum (C_{k+1} - C_k)^2 at the
+// GLOBAL tile index (col tile * npad/64 + row tile): the same reduction order for any G.
+// ---------------------------------------------------------------------------------------
+template <typename CT, typename WT>
+__global__ void __launch_bounds__(256) k_sym_update(const CT *__restrict__ cold, CT *__restrict__ cnew,
+                                                    const WT *__restrict__ W, int64_t npad, int64_t kp, int64_t col0,
+                                                    int p, int m, int rtz, int prec, void *chat_new, int corr,
+                                                    void *chat_corr_new, double *part) {
+  __shared__ WT t[64][65];
+  __shared__ double red[8];
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4 (1-D block: block_sum_det)
+  const int64_t jb = (int64_t)blockIdx.x * 64;             // local column tile
+  const int64_t ib = (int64_t)blockIdx.y * 64;             // row tile
+  const int64_t slot = npad * kp;
+  // mirrored tile: t[r][c] = W(col0 + jb + r, ib + c)
+  {
+    const int64_t gi = ib + tx;
+    const WT *src = W + (gi / kp) * slot + gi % kp;
+    for (int r = ty; r < 64; r += 4) t[r][tx] = src[(col0 + jb + r) * kp];
+  }
+  __syncthreads();
+  const bool pow2p = (p & (p - 1)) == 0;
+  const double tp = (double)(2 * p), itp = 1.0 / tp;
+  const WT *wl = W + (col0 / kp) * slot;                  // this rank's slot
+  double d2 = 0.0;
+  for (int r = ty; r < 64; r += 4) {
+    const int64_t i = ib + r, jl = jb + tx, ci = i * kp + jl;
+    const double sw = __dadd_rn((double)wl[ci], (double)t[tx][r]);
+    const double e = pow2p ? __dmul_rn(sw, itp) : __ddiv_rn(sw, tp);   // d/(2p); exact recip. for 2^k
+    const double c = (double)cold[ci];
+    const double x = __dadd_rn(c, e);
+    double cn;
+    if (sizeof(CT) == 8) {
+      cn = q_e11(x, m, rtz);
+      ((double *)cnew)[ci] = cn;
+    } else {
+      const float f = q_e8(x, m, rtz);
+      ((float *)cnew)[ci] = f;
+      cn = (double)f;
+    }
+    if (chat_new) store_operand(chat_new, ci, prec, cn, 0);
+    if (chat_corr_new) store_operand(chat_corr_new, ci, corr, cn, 0);
+    const double dd = __dsub_rn(cn, c);
+    d2 = __fma_rn(dd, dd, d2);
+  }
+  const double b = block_sum_det<256>(d2, red);
+  if (threadIdx.x == 0) part[((col0 + jb) / 64) * (npad / 64) + blockIdx.y] = b;
+}
+
 // test hook: quantisers
 __global__ void k_test_quant(int mode, const void *in, void *out, int64_t len, int m, int rtz, int sigma) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -331,6 +388,21 @@ cudaError_t launch_transpose(const void *src, int64_t rows, int64_t cols, int es
   if (esz == 8) k_transpose<double><<<g, b, 0, s>>>((const double *)src, rows, cols, (double *)dst);
   else if (esz == 4) k_transpose<float><<<g, b, 0, s>>>((const float *)src, rows, cols, (float *)dst);
   else k_transpose<uint16_t><<<g, b, 0, s>>>((const uint16_t *)src, rows, cols, (uint16_t *)dst);
+  LAUNCH_CHECK();
+}
+
+cudaError_t launch_sym_update(const void *cold, int cont64, void *cnew, const void *W, int w64, int64_t npad,
+                              int64_t kp, int64_t col0, int p, int m, int rtz, int prec, void *chat_new, int corr,
+                              void *chat_corr_new, double *part, cudaStream_t s) {
+  if (kp % 64 || npad % 64) return cudaErrorInvalidValue;
+  dim3 g((unsigned)(kp / 64), (unsigned)(npad / 64)), b(256);
+#define SYMU(CT, WT) k_sym_update<CT, WT><<<g, b, 0, s>>>((const CT *)cold, (CT *)cnew, (const WT *)W, npad, kp, col0, \
+                                                          p, m, rtz, prec, chat_new, corr, chat_corr_new, part)
+  if (cont64 && w64) SYMU(double, double);
+  else if (cont64) SYMU(double, float);
+  else if (w64) SYMU(float, double);
+  else SYMU(float, float);
+#undef SYMU
   LAUNCH_CHECK();
 }
 

@@ -7,14 +7,14 @@ def torch_cuda(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
-def run_gpu_trajectory(A_np, p, phases, final_tol, max_iters, keep=True):
+def run_gpu_trajectory(A_np, p, phases, final_tol, max_iters, keep=True, form="literal"):
     """Iterate one chain at a time through the C-ABI.  Returns (outcome, trace, hist, C_best)
     with hist[k] = the iterate evaluated by trace record k, for k >= 1 (same indexing as the
     oracle's C_hist)."""
     import torch
     import paper_1703_02283_b200 as ipr
     A = torch_cuda(A_np)
-    s = ipr.Solver(A, p, phases, final_tol)
+    s = ipr.Solver(A, p, phases, final_tol, form=form)
     hist = {}
     out = ipr.IPR_RUNNING
     for k in range(max_iters):

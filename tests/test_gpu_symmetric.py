@@ -1,0 +1,137 @@
+"""GPU parity of NEXT-2, the symmetrised-correction form (reading R-22)
+
+    Z_1 = Ahat Chat, Z_j = Chat qin(Z_{j-1}), Rhat = qc(I - Z_p), W = qc(C) Rhat,
+    C_{k+1} = q_m(C + (W + W^T)/(2p)),
+
+through the C-ABI (ipr_set_form(IPR_FORM_SYMMETRIC), ipr_phase.corr_prec) against the oracle's
+FORM_SYMMETRIC.  Parity levels as for the literal form: diagonal A bit-exact
+(every dot product has one non-zero term), kappa = 2 twins within the north-star tolerances,
+bitwise symmetry and run-to-run determinism of the GPU iterates."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.gpu_util import rel_fro, run_gpu_trajectory, torch_cuda
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+ipr = pytest.importorskip("paper_1703_02283_b200")
+
+OPR = {"fp64": oracle.FP64, "tf32": oracle.TF32, "bf16": oracle.BF16}
+LOW = dict(switch_tol=0.0, plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
+
+
+def schedules(name):
+    """(gpu phases, oracle phases) of a named schedule; 'x/cy' = phase x with correction y."""
+    pg, po = [], []
+    parts = name.split(">")
+    for i, part in enumerate(parts):
+        prec, _, corr = part.partition("/c")
+        kw = {} if i == len(parts) - 1 else LOW
+        pg.append(ipr.make_phase(prec, corr_prec=corr or -1, **kw))
+        po.append(oracle.phase(OPR[prec], corr_prec=OPR[corr] if corr else -1, **kw))
+    return pg, po
+
+
+def run_sym(A, p, name, tol, iters):
+    pg, po = schedules(name)
+    r = oracle.solve(A, p, po, tol, iters, hist=iters, form=oracle.FORM_SYMMETRIC)
+    g = run_gpu_trajectory(A, p, pg, tol, iters, form="symmetric")
+    return r, g
+
+
+@pytest.mark.parametrize("p,name", [(2, "fp64"), (3, "fp64"), (2, "fp64/cbf16"), (2, "bf16>fp64"),
+                                    (2, "tf32>fp64/cbf16"), (3, "bf16>fp64/ctf32"), (2, "bf16/ctf32>fp64")])
+def test_diagonal_bit_exact(p, name):
+    A = synth.diag_spd(200, 1e3, 9)
+    r, (out, tr, hist, best) = run_sym(A, p, name, 1e-13, 120)
+    assert r.outcome == oracle.CONVERGED and out == ipr.IPR_CONVERGED
+    assert [t["decision"] for t in tr] == [x["decision"] for x in r.records]
+    for k, Ck in hist.items():
+        if k < len(r.records):
+            np.testing.assert_array_equal(Ck, r.C_hist[k], err_msg=f"iterate {k}")
+    np.testing.assert_array_equal(best, r.C_best)
+    for t, x in zip(tr, r.records):
+        assert t["rho"] == pytest.approx(x["rho"], rel=1e-12, abs=1e-300)
+    assert tr[-1]["rho_cert"] <= 1e-13
+
+
+@pytest.mark.parametrize("n,p", [(300, 2), (300, 3), (520, 2)])
+def test_fp64_twin_trajectory(n, p):
+    A = synth.spd(n, 2.0, 12)
+    r, (out, tr, hist, best) = run_sym(A, p, "fp64", 1e-12, 60)
+    assert out == ipr.IPR_CONVERGED and r.outcome == oracle.CONVERGED
+    assert abs(len(tr) - len(r.records)) <= 1
+    for k, Ck in hist.items():
+        assert np.array_equal(Ck, Ck.T), f"GPU iterate {k} not bitwise symmetric"
+        if k < len(r.records):
+            assert rel_fro(Ck, r.C_hist[k]) <= 1e-10, k
+    assert rel_fro(best, r.C_best) <= 1e-10
+    assert tr[-1]["rho_cert"] <= 1e-12
+
+
+@pytest.mark.parametrize("name,m", [("bf16>fp64/cbf16", 7), ("tf32>fp64/cbf16", 10), ("bf16>fp64", 7),
+                                    ("bf16>tf32>fp64/cbf16", 7)])
+def test_mixed_level2(name, m):
+    # Level 2: low-phase iterates within 4 * 2^-m of the oracle, the same switch
+    # iteration (R-6: +-1 only at a tie), final C within 1e-10, certified rho <= 1e-12; and the
+    # refinement claim: the FP64 phase needs far fewer iterations than the literal form (F4).
+    n, p = 384, 2
+    A = synth.spd(n, 2.0, 4)
+    r, (out, tr, hist, best) = run_sym(A, p, name, 1e-12, 120)
+    assert out == ipr.IPR_CONVERGED and r.outcome == oracle.CONVERGED
+    sw_g = [t["k"] for t in tr if t["decision"] == ipr.IPR_DEC_SWITCH]
+    sw_o = [x["k"] for x in r.records if x["decision"] == oracle.SWITCH]
+    assert len(sw_g) == len(sw_o) and all(abs(a - b) <= 1 for a, b in zip(sw_g, sw_o)), (sw_g, sw_o)
+    for k, Ck in hist.items():
+        if k <= sw_o[0]:
+            assert rel_fro(Ck, r.C_hist[k]) <= 4 * 2.0 ** -m, k
+    assert rel_fro(best, r.C_best) <= 1e-10
+    assert tr[-1]["rho_cert"] <= 1e-12
+    n64 = sum(1 for t in tr if t["phase"] == len(sw_g))
+    assert n64 <= 12, n64
+
+
+def test_run_to_run_deterministic_and_symmetric():
+    A = synth.spd(640, 2.0, 3)
+    pg, _ = schedules("bf16>fp64/cbf16")
+    res = []
+    for _ in range(2):
+        out, tr, hist, best = run_gpu_trajectory(A, 2, pg, 1e-12, 60, form="symmetric")
+        res.append((tr, best))
+        assert np.array_equal(best, best.T)
+    (t1, b1), (t2, b2) = res
+    for key in ("rho", "delta", "decision", "rho_cert"):
+        assert np.array_equal([a[key] for a in t1], [a[key] for a in t2], equal_nan=True), key
+    assert all(np.isfinite(a["delta"]) for a in t1 if a["decision"] != ipr.IPR_DEC_SWITCH)
+    np.testing.assert_array_equal(b1, b2)
+
+
+def test_config_c3_family_level3_envelope():
+    # BASELINE config C3's family (kappa = 1e4, p = 2) at n = 1024: the form is unstable there
+    # (kappa > 34, reading R-22), so Level 3: same outcome class and min rho within 4x.
+    A = synth.spd(1024, 1e4, 2)
+    pg, po = schedules("bf16>fp64/cbf16")
+    r = oracle.solve(A, 2, po, 1e-12, 80, form=oracle.FORM_SYMMETRIC)
+    out, tr, _, _ = run_gpu_trajectory(A, 2, pg, 1e-12, 80, keep=False, form="symmetric")
+    mg, mo = min(t["rho"] for t in tr), min(x["rho"] for x in r.records)
+    assert mg <= 4 * mo and mo <= 4 * mg
+    assert (out == ipr.IPR_CONVERGED) == (r.outcome == oracle.CONVERGED)
+
+
+def test_errors():
+    A = torch_cuda(synth.spd(64, 2.0, 0))
+    s = ipr.Solver(A, 1, [ipr.make_phase("fp64")], 1e-12, form="symmetric")
+    with pytest.raises(ipr.IprError) as e:
+        s.iterate(1)
+    assert e.value.status == ipr.IPR_E_INVALID_ARG
+    s.close()
+    s = ipr.Solver(A, 2, [ipr.make_phase("fp16", max_iters=3), ipr.make_phase("fp64")], 1e-12, form="symmetric")
+    with pytest.raises(ipr.IprError) as e:
+        s.iterate(1)
+    assert e.value.status == ipr.IPR_E_UNSUPPORTED
+    s.close()
+    with pytest.raises(ipr.IprError) as e:
+        ipr.Solver(A, 2, [ipr.make_phase("bf16", corr_prec="fp64")], 1e-12, form="symmetric")
+    assert e.value.status == ipr.IPR_E_INVALID_ARG
