@@ -29,9 +29,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "time-to-FP64-residual 1e-12 (n=8192, p=2)"
 # headline schedule: BF16 tensor-core phase, then FP64 refinement with a BF16 correction GEMM,
-# in the symmetrised-correction form (NEXT-2, R-22)
-DEFAULT_SCHEDULE = "sym:bf16>fp64/cbf16"
-EXTRA_SCHEDULES = ["fp64", "bf16>fp64", "tf32>fp64", "fp16>fp64", "sym:fp64", "sym:fp64/cbf16",
+# in the symmetrised-correction form with the upper-triangle GEMM 2 (NEXT-2 (i)+(iii), R-22)
+DEFAULT_SCHEDULE = "symtri:bf16>fp64/cbf16"
+EXTRA_SCHEDULES = ["fp64", "bf16>fp64", "tf32>fp64", "fp16>fp64", "sym:fp64", "sym:fp64/cbf16", "symtri:fp64/cbf16",
+                   "symtri:bf16>fp64/cbf16", "symtri:bf16>tf32>fp64/cbf16",
                    "sym:bf16>fp64", "sym:tf32>fp64/cbf16", "sym:bf16>tf32>fp64/cbf16"]
 FP64_PEAK_TFLOPS = 37.1   # measured DMMA issue peak on this pool (profiles/r01_calibration.md)
 FP64_PEAK_SRC = "measured DMMA.8x8x4 issue peak, tools/probes/dmma_rate.cu (MEASURED_PEAKS.json has no FP64 figure)"
@@ -57,7 +58,7 @@ def parse_schedule(name):
     form = "literal"
     if ":" in name:
         f, name = name.split(":", 1)
-        form = {"sym": "symmetric", "ns": "newton_schulz", "lit": "literal"}[f]
+        form = {"sym": "symmetric", "symtri": "symmetric_tri", "ns": "newton_schulz", "lit": "literal"}[f]
     parts = []
     for ph in name.replace("-", ">").split(">"):
         prec, _, corr = ph.partition("/c")
@@ -77,7 +78,7 @@ def schedule(name, n):
         else:
             # the symmetric form damps low-precision noise in the next phase, so a low phase runs
             # to its plateau; the literal form leaves at rho_hat <= 1e-2 as well
-            sw = 0.0 if form == "symmetric" else 1e-2 * math.sqrt(n)
+            sw = 0.0 if form.startswith("symmetric") else 1e-2 * math.sqrt(n)
             out.append(ipr.make_phase(prec, switch_tol=sw, plateau_ratio=0.7, plateau_arm=0.5,
                                       max_iters=40, corr_prec=corr))
     return form, out

@@ -145,8 +145,14 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
  * p = 2), so low-precision noise is damped in the FP64 phase instead of persisting.
  * The trace's rho is rho_s; when it meets final_tol in the last phase the engine computes
  * C_{k+1}, then certifies ||I - C_k^p A||_F with FP64 DMMA GEMMs: converged if that is <=
- * final_tol (record.rho_cert), else the iteration continues from C_{k+1}. */
-typedef enum { IPR_FORM_LITERAL = 0, IPR_FORM_NEWTON_SCHULZ = 1, IPR_FORM_SYMMETRIC = 2 } ipr_form;
+ * final_tol (record.rho_cert), else the iteration continues from C_{k+1}.
+ *
+ * IPR_FORM_SYMMETRIC_TRI (p = 2, world = 1): as IPR_FORM_SYMMETRIC, but
+ * Z_2 = C A C -- symmetric in exact arithmetic -- is computed on the upper triangle only (tiles
+ * wholly below the diagonal are skipped: ~1/2 of GEMM 2) and R_ij = delta_ij - Z_2[min(i,j)][max(i,j)]
+ * is exactly symmetric; rho_s sums the off-diagonal terms twice. */
+typedef enum { IPR_FORM_LITERAL = 0, IPR_FORM_NEWTON_SCHULZ = 1, IPR_FORM_SYMMETRIC = 2,
+               IPR_FORM_SYMMETRIC_TRI = 3 } ipr_form;
 ipr_status ipr_set_form(ipr_ctx *c, int form);
 
 /* Run at most max_iters (> 0) chains.  *iters_done = chains evaluated by this call,

@@ -339,8 +339,8 @@ static double update_ns(int64_t n, const double *X, const orc_phase *ph, chain_w
  * ------------------------------------------------------------------------------ */
 static int corr_of(const orc_phase *ph) { return ph->corr_prec < 0 ? ph->prec : ph->corr_prec; }
 
-static double chain_sym(int64_t n, int p, const double *A, const double *C, const orc_phase *ph,
-                        chain_ws *w) {
+static double chain_sym(int64_t n, int p, int tri, const double *A, const double *C,
+                        const orc_phase *ph, chain_ws *w) {
   const int64_t nn = n * n;
   for (int64_t i = 0; i < nn; ++i) w->T[i] = store_q(ph, A[i]);
   qin_matrix(ph->prec, nn, w->T, w->X);                     /* w->X = Ahat            */
@@ -350,6 +350,9 @@ static double chain_sym(int64_t n, int p, const double *A, const double *C, cons
     qin_matrix(ph->prec, nn, w->T, w->X);                   /* qin(Z_{j-1})           */
     orc_gemm(n, w->Chat, w->X, w->T);                       /* Z_j = Chat qin(Z_{j-1}) */
   }
+  if (tri)                     /* ORC_FORM_SYMMETRIC_TRI: Z_2 = C A C from its upper triangle */
+    for (int64_t r = 0; r < n; ++r)
+      for (int64_t c = 0; c < r; ++c) w->T[r * n + c] = w->T[c * n + r];
   double s2 = 0.0;
   for (int64_t r = 0; r < n; ++r)
     for (int64_t c = 0; c < n; ++c) {
@@ -431,7 +434,7 @@ double orc_step_sym(int64_t n, int p, const double *A, const double *C, const or
   if (p < 2 || ph->prec == ORC_FP16 || corr_of(ph) == ORC_FP16) return NAN;
   chain_ws w;
   if (!ws_alloc(&w, n)) { ws_free(&w); return NAN; }
-  const double rho = chain_sym(n, p, A, C, ph, &w);
+  const double rho = chain_sym(n, p, 0, A, C, ph, &w);
   if (C_next) { const double d = update_sym(n, p, C, ph, &w, C_next); if (delta) *delta = d; }
   ws_free(&w);
   return rho;
@@ -452,12 +455,13 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
   *nrec = 0;
   if (n <= 0 || p < 1 || nphases < 1) return -1;
   if (form == ORC_FORM_NEWTON_SCHULZ && p != 1) return -1;
-  if (form == ORC_FORM_SYMMETRIC) {
-    if (p < 2) return -1;
+  const int sym = form == ORC_FORM_SYMMETRIC || form == ORC_FORM_SYMMETRIC_TRI;
+  if (sym) {
+    if (p < 2 || (form == ORC_FORM_SYMMETRIC_TRI && p != 2)) return -1;
     for (int i = 0; i < nphases; ++i)
       if (phases[i].prec == ORC_FP16 || corr_of(&phases[i]) == ORC_FP16) return -1;
   }
-  if (form < ORC_FORM_LITERAL || form > ORC_FORM_SYMMETRIC) return -1;
+  if (form < ORC_FORM_LITERAL || form > ORC_FORM_SYMMETRIC_TRI) return -1;
   if (!orc_is_symmetric(n, A)) return -2;
   const int64_t nn = n * n;
   double nrm[3];
@@ -482,7 +486,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
     const orc_phase *ph = &phases[ctl.phase];
     if (C_hist && k < hist_cap) memcpy(C_hist + (int64_t)k * nn, C, (size_t)nn * sizeof(double));
     const double rho = form == ORC_FORM_NEWTON_SCHULZ ? chain_ns(n, A, C, ph, &w)
-                       : form == ORC_FORM_SYMMETRIC    ? chain_sym(n, p, A, C, ph, &w)
+                       : sym ? chain_sym(n, p, form == ORC_FORM_SYMMETRIC_TRI, A, C, ph, &w)
                                                        : chain(n, p, A, C, ph, &w);
     const int phase_now = ctl.phase;
     int d = orc_ctrl_decide(&ctl, ph, rho);
@@ -492,7 +496,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
     r.decision = d; r.rho = rho; r.rho_hat = rho / sqrt((double)n); r.delta = NAN;
     r.gamma = (gamma_normA2 > 0) ? gamma_of(n, C, A, gamma_normA2, g1, g2) : NAN;
     r.rho_cert = NAN;
-    if (d == ORC_CONVERGED && form == ORC_FORM_SYMMETRIC) {
+    if (d == ORC_CONVERGED && sym) {
       /* rho_s = ||I - C^{p-1} A C||_F is not the north-star residual: certify
        * ||I - C^p A||_F with the FP64 literal chain (reading R-3); if it misses final_tol the
        * iteration continues from the update computed first (as the GPU engine does). */
@@ -506,7 +510,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
       }
     } else if (d == ORC_CONTINUE) {
       r.delta = form == ORC_FORM_NEWTON_SCHULZ ? update_ns(n, C, ph, &w, Cn)
-                : form == ORC_FORM_SYMMETRIC    ? update_sym(n, p, C, ph, &w, Cn)
+                : sym                           ? update_sym(n, p, C, ph, &w, Cn)
                                                 : update(n, p, C, ph, &w, Cn);
       double *t = C; C = Cn; Cn = t;
     } else if (d == ORC_SWITCH) {

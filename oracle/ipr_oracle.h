@@ -112,7 +112,10 @@ int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int np
 
 /* Iteration forms: ORC_FORM_LITERAL = Eq. (1) as printed (right-to-left chain, reading R-1);
  * ORC_FORM_NEWTON_SCHULZ = p = 1 only, X_{k+1} = X_k (2I - A X_k) (NEXT-1). */
-enum { ORC_FORM_LITERAL = 0, ORC_FORM_NEWTON_SCHULZ = 1, ORC_FORM_SYMMETRIC = 2 };
+/* ORC_FORM_SYMMETRIC_TRI (p = 2): as ORC_FORM_SYMMETRIC with Z_2 = C A C replaced by the mirror
+ * of its upper triangle (Z_2[i][j] := Z_2[min(i,j)][max(i,j)]), so R is exactly symmetric. */
+enum { ORC_FORM_LITERAL = 0, ORC_FORM_NEWTON_SCHULZ = 1, ORC_FORM_SYMMETRIC = 2,
+       ORC_FORM_SYMMETRIC_TRI = 3 };
 int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase *phases,
                    int nphases, double final_tol, int max_total, orc_record *rec, int cap_rec,
                    int *nrec, double *C_best, double *C_hist, int hist_cap, double gamma_normA2,

@@ -26,6 +26,8 @@ enum EpiMode : int {
                         // What = 2I - T with diag = 2; symmetric form R = I - Z_p with diag = 1)
   EPI_NSUPDATE = 64,  // Newton-Schulz: X_{k+1} = q_m(D) -> container, operand, delta partials
   EPI_WSTORE = 128,   // symmetric form: W = D row-major to wout[i * ldw + j] (FP32, or FP64 if w64)
+  EPI_STORE_N = 256,  // also store qin(D) row-major (nout[i * ldn + j]): symmetric form, FP64,
+                      // G = 1 -- D = A C row-major is the B operand of C (C A) for certification
 };
 
 struct GemmArgs {
@@ -40,6 +42,9 @@ struct GemmArgs {
   int tprec;            // operand format of the EPI_STORE_T output (= prec except the symmetric
                         // form's Rhat, stored in the correction format)
   double diag;          // EPI_DIAG_MINUS coefficient
+  int tri;              // symmetric-tri form (G = 1): D is symmetric in exact arithmetic; only
+                        // elements with row <= col are computed, each stored at (i,j) AND (j,i),
+                        // residual weight 2 off the diagonal; tiles wholly below are skipped
   const int *sigA, *sigB; // FP16 phase: device scale exponents of the A / B operands; else NULL
   // EPI_STORE_T / EPI_TSCRATCH: T(i,j) -> tout[j * ldt + i]
   void *tout; int64_t ldt;
@@ -54,6 +59,8 @@ struct GemmArgs {
   double *zout; int64_t ldz;
   // EPI_WSTORE
   void *wout; int64_t ldw; int w64;
+  // EPI_STORE_N
+  void *nout; int64_t ldn;
 };
 
 // ------------------------------------------------------------------------------------

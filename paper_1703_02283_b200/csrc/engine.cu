@@ -18,6 +18,7 @@
 #include <cstdio>
 #include <cstring>
 #include <dlfcn.h>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -69,6 +70,8 @@ struct ipr_ctx {
   void *chatc[2] = {nullptr, nullptr};  // symmetric form: Chat in the correction format (panel-major)
   void *wbuf = nullptr;                 // symmetric form: W = qc(C) Rhat, full panel-major
   int wbytes = 4;                       // allocated element size of wbuf (8 if any FP64 correction)
+  void *Zr = nullptr;                   // symmetric form, G = 1: Z_1 = A C row-major (FP64 phases)
+  int zr_for = -1;                      // iterate buffer whose chain wrote Zr (-1: none)
   int form = IPR_FORM_LITERAL;          // iteration form (ipr_set_form)
   float *tscr = nullptr;                // FP16 phase T scratch (FP32)
   double *full64 = nullptr;             // FP64 npad x npad scratch (copy-out / certify)
@@ -82,12 +85,60 @@ struct ipr_ctx {
   int best_cont64 = 1;
   int64_t pending_delta = -1;           // trace record whose delta is in flight
   std::vector<ipr_record> trace;
-  void *arena = nullptr;                // every O(n^2) buffer: ONE cudaMalloc at the first ipr_iterate
+  void *arena = nullptr;                // every O(n^2) buffer: ONE pool allocation at the first ipr_iterate
+  void *aux = nullptr;                  // the small device buffers (flag, scalars, sigmas, colsum)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   bool upd_timed = false;
 };
 
 namespace {
+
+// Process-wide pinned slab for the per-context 8-double D2H scalars (cudaMallocHost /
+// cudaFreeHost synchronise the device and can stall for 100+ ms: never on the solve path).
+constexpr int kPinnedSlots = 1024;
+std::mutex g_pin_mu;
+double *g_pin_base = nullptr;
+bool g_pin_used[kPinnedSlots] = {};
+double *pinned_acquire() {
+  std::lock_guard<std::mutex> lock(g_pin_mu);
+  if (!g_pin_base && cudaMallocHost((void **)&g_pin_base, (size_t)kPinnedSlots * 64) != cudaSuccess) {
+    cudaGetLastError();
+    g_pin_base = nullptr;
+    return nullptr;
+  }
+  for (int i = 0; i < kPinnedSlots; ++i)
+    if (!g_pin_used[i]) { g_pin_used[i] = true; return g_pin_base + 8 * i; }
+  return nullptr;
+}
+void pinned_release(double *p) {
+  std::lock_guard<std::mutex> lock(g_pin_mu);
+  const int64_t i = (p - g_pin_base) / 8;
+  if (g_pin_base && i >= 0 && i < kPinnedSlots) g_pin_used[i] = false;
+}
+
+// One retained stream-ordered memory pool per device (release threshold = unlimited): the
+// arenas of back-to-back solves are recycled without driver (un)mapping.
+cudaMemPool_t arena_pool() {
+  static cudaMemPool_t pools[64] = {};
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!pools[dev]) {
+    cudaMemPoolProps props;
+    memset(&props, 0, sizeof props);
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+    pools[dev] = p;
+  }
+  return pools[dev];
+}
 
 ipr_status fail(ipr_ctx *c, ipr_status s, const char *fmt, ...) {
   char buf[512];
@@ -237,6 +288,7 @@ ipr_status save_best(ipr_ctx *c) {
 }
 
 ipr_status make_xt(ipr_ctx *c, int i, const PhaseC &P);
+inline bool is_sym(const ipr_ctx *c) { return c->form == IPR_FORM_SYMMETRIC || c->form == IPR_FORM_SYMMETRIC_TRI; }
 void *chatc_slot(ipr_ctx *c, int i, int prec) {
   return (char *)c->chatc[i] + (size_t)c->rank * (size_t)(c->npad * c->kp) * elt_size(prec);
 }
@@ -272,7 +324,7 @@ ipr_status begin_phase(ipr_ctx *c, bool first) {
   }
   CKS(make_operand(c, c->cur, P));
   if (c->form == IPR_FORM_NEWTON_SCHULZ) CKS(make_xt(c, c->cur, P));
-  if (c->form == IPR_FORM_SYMMETRIC) {
+  if (is_sym(c)) {
     CKS(make_corr_operand(c, c->cur, P));
     if (c->world > 1) CKS(make_xt(c, c->cur, P));
   }
@@ -314,7 +366,7 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
       CK(launch_scale_fp16(c->tscr, c->kp * c->npad, c->dsig + 4, c->T[1], c->st));
     }
   }
-  if (c->form == IPR_FORM_SYMMETRIC) {
+  if (is_sym(c)) {
     // Z_1 = Ahat Chat (A operand: Ahat row-major; B: Chat itself for G = 1 -- exactly symmetric --
     // else the transposed local panel), Z_j = Chat qin(Z_{j-1}); GEMM p: R = I - Z_p in the
     // correction format (K-major for the W GEMM) + residual partials.  Z_j -> T[j & 1].
@@ -327,7 +379,18 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
         chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
       }
       g.mode = EPI_STORE_T;
-      if (j == c->p) { g.mode |= EPI_DIAG_MINUS | EPI_RESID; g.diag = 1.0; g.tprec = P.corr; }
+      if (j == 1) {
+        // FP64 last phase (G = 1): also keep Z_1 = A C row-major -- the B operand of C (C A), so
+        // certifying ||I - C^p A||_F costs p - 1 GEMMs instead of p
+        c->zr_for = -1;
+        if (c->Zr && prec == IPR_FP64 && P.m == 52 && c->phase == (int)c->ph.size() - 1) {
+          g.mode |= EPI_STORE_N; g.nout = c->Zr; g.ldn = c->npad; c->zr_for = c->cur;
+        }
+      }
+      if (j == c->p) {
+        g.mode |= EPI_DIAG_MINUS | EPI_RESID; g.diag = 1.0; g.tprec = P.corr;
+        g.tri = c->form == IPR_FORM_SYMMETRIC_TRI;   // Z_2 = C A C: upper triangle + mirror
+      }
       g.tout = c->T[j & 1];
       g.ldt = c->npad;
       g.part = part;
@@ -442,7 +505,7 @@ ipr_status update_sym(ipr_ctx *c) {
   return IPR_OK;
 }
 
-ipr_status step_update(ipr_ctx *c) { return c->form == IPR_FORM_SYMMETRIC ? update_sym(c) : update(c); }
+ipr_status step_update(ipr_ctx *c) { return is_sym(c) ? update_sym(c) : update(c); }
 
 // Controller, reading R-5 (independent implementation of the rules in DESIGN.md).
 int decide(ipr_ctx *c, double rho, bool *best_new) {
@@ -470,9 +533,9 @@ int decide(ipr_ctx *c, double rho, bool *best_new) {
 
 void free_ctx(ipr_ctx *c) {
   if (!c) return;
-  cudaFree(c->arena); cudaFree(c->dscal);
-  cudaFree(c->dsig); cudaFree(c->colsum); cudaFree(c->dflag);
-  if (c->hscal) cudaFreeHost(c->hscal);
+  if (c->arena) cudaFreeAsync(c->arena, c->st);   // back to the library's retained pool
+  if (c->aux) cudaFreeAsync(c->aux, c->st);
+  if (c->hscal) pinned_release(c->hscal);
   for (auto &e : c->ev) if (e) cudaEventDestroy(e);
   c->comm.destroy();
   delete c;
@@ -492,12 +555,21 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       {(void **)&c->tscr, fp16 ? panel * 4 : 0},
       {&c->Afull, (c->world > 1 && c->form != IPR_FORM_LITERAL) ? full * 8 : 0},
       {&c->chatc[0], need_corr ? full * 4 : 0}, {&c->chatc[1], need_corr ? full * 4 : 0},
-      {&c->wbuf, c->form == IPR_FORM_SYMMETRIC ? full * c->wbytes : 0},
+      {&c->wbuf, is_sym(c) ? full * c->wbytes : 0},
+      {&c->Zr, (is_sym(c) && c->world == 1) ? panel * 8 : 0},
       {(void **)&c->full64, full * 8}, {&c->Acert, panel * 8}};
   size_t total = 0;
   for (const Slot &q : slots) total += (q.bytes + 255) / 256 * 256;
+  // stream-ordered allocation from a library-owned pool that retains its memory, so back-to-back
+  // solves reuse the arena without driver (un)mapping: one context = one cudaMallocFromPoolAsync
+  cudaMemPool_t pool = arena_pool();
+  if (!pool) return fail(c, IPR_E_CUDA, "cudaMemPoolCreate failed");
   char *base = nullptr;
-  CKS(dalloc(c, &base, total));
+  cudaError_t e = cudaMallocFromPoolAsync((void **)&base, total, pool, c->st);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, IPR_E_OOM, "arena of %zu bytes: %s", total, cudaGetErrorString(e));
+  }
   c->arena = base;
   size_t off = 0;
   for (const Slot &q : slots) {
@@ -526,6 +598,7 @@ ipr_status gather_f64(ipr_ctx *c, const double *local) {
 extern "C" {
 
 static ipr_status certify_best(ipr_ctx *c, double *rho);
+static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho);
 
 const char *ipr_version(void) { return "ipr 0.1.0 (sm_100a: tcgen05 BF16/FP16/TF32, DMMA FP64)"; }
 
@@ -565,11 +638,20 @@ ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, 
     cudaError_t q = cudaStreamQuery(c->st);
     if (q != cudaSuccess && q != cudaErrorNotReady) TRYC(q);
   }
-  TRY(dalloc(c, &c->dflag, 16));
-  TRY(dalloc(c, &c->colsum, (size_t)n * 8));
-  TRY(dalloc(c, &c->dscal, 8 * 8));
-  TRY(dalloc(c, &c->dsig, 8 * 4));
-  TRYC(cudaMallocHost((void **)&c->hscal, 8 * 8));
+  // small device buffers: one stream-ordered block from the retained pool (no synchronous
+  // cudaMalloc / cudaFree on the solve path); 8 pinned doubles from a process-wide slab
+  {
+    cudaMemPool_t pool = arena_pool();
+    if (!pool) TRY(fail(c, IPR_E_CUDA, "cudaMemPoolCreate failed"));
+    const size_t cs = ((size_t)n * 8 + 255) / 256 * 256;
+    char *b = nullptr;
+    TRYC(cudaMallocFromPoolAsync((void **)&b, 256 * 3 + cs, pool, c->st));
+    c->aux = b;
+    c->dflag = (int *)b; c->dscal = (double *)(b + 256); c->dsig = (int *)(b + 512);
+    c->colsum = (double *)(b + 768);
+    c->hscal = pinned_acquire();
+    if (!c->hscal) TRY(fail(c, IPR_E_OOM, "pinned host slab exhausted (too many live contexts)"));
+  }
   for (auto &e : c->ev) TRYC(cudaEventCreate(&e));
   TRYC(cudaMemsetAsync(c->dflag, 0, 16, c->st));
   TRYC(cudaMemsetAsync(c->dsig, 0, 32, c->st));
@@ -644,7 +726,7 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
 ipr_status ipr_set_form(ipr_ctx *c, int form) {
   if (!c) return fail(c, IPR_E_INVALID_ARG, "ipr_set_form: null context");
   if (c->started) return fail(c, IPR_E_STATE, "ipr_set_form: iteration already started");
-  if (form != IPR_FORM_LITERAL && form != IPR_FORM_NEWTON_SCHULZ && form != IPR_FORM_SYMMETRIC)
+  if (form < IPR_FORM_LITERAL || form > IPR_FORM_SYMMETRIC_TRI)
     return fail(c, IPR_E_INVALID_ARG, "ipr_set_form: unknown form %d", form);
   c->form = form;
   return IPR_OK;
@@ -661,8 +743,12 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       if (c->p != 1) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: the Newton-Schulz form needs p = 1");
     }
     bool need_c = false;
-    if (c->form == IPR_FORM_SYMMETRIC) {
+    if (is_sym(c)) {
       if (c->p < 2) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: the symmetric form needs p >= 2 (p = 1: Newton-Schulz)");
+      if (c->form == IPR_FORM_SYMMETRIC_TRI && c->p != 2)
+        return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: the symmetric-tri form needs p = 2 (Z_2 = C A C symmetric)");
+      if (c->form == IPR_FORM_SYMMETRIC_TRI && c->world != 1)
+        return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: the symmetric-tri form is single-GPU (mirror writes cross panels)");
       c->wbytes = 4;
       for (auto &P : c->ph) {
         if (P.prec == IPR_FP16 || P.corr == IPR_FP16)
@@ -693,13 +779,16 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     r.rho_cert = NAN; r.upd_ms = 0.0;
     c->trace.push_back(r);
     *iters_done += 1;
-    if (d == IPR_DEC_CONVERGED && c->form == IPR_FORM_SYMMETRIC) {
+    if (d == IPR_DEC_CONVERGED && is_sym(c)) {
       // rho_s = ||I - C^{p-1}AC||_F met final_tol: compute C_{k+1} (the T buffers are consumed),
       // then certify ||I - C_k^p A||_F in FP64 (R-3); continue from C_{k+1} if it misses.
+      const int ck = c->cur;
+      const bool fast = c->zr_for == ck && c->best_loc == ck;
       CKS(update_sym(c));
       c->pending_delta = (int64_t)c->trace.size() - 1;
       double rc = NAN;
-      CKS(certify_best(c, &rc));
+      if (fast) CKS(certify_from_zr(c, ck, &rc));
+      else CKS(certify_best(c, &rc));
       c->trace.back().rho_cert = rc;
       if (!(rc <= c->final_tol)) {
         c->trace.back().decision = IPR_DEC_CONTINUE;
@@ -778,6 +867,26 @@ ipr_status ipr_get_iterate(ipr_ctx *c, int which, double *C_dev_out, int64_t ldc
   if (which != 0 && which != 1) return fail(c, IPR_E_INVALID_ARG, "ipr_get_iterate: which must be 0 or 1");
   if (!c->started) return fail(c, IPR_E_STATE, "ipr_get_iterate: no iterate yet (call ipr_iterate)");
   return copy_iterate(c, which, C_dev_out, ldc);
+}
+
+// ||I - C^p A||_F of the iterate in buffer i (FP64, exact operand) from the Zr = A C kept by its
+// chain: X_1 = C (C A) [B = Zr row-major], X_j = C X_{j-1}; p - 1 DMMA GEMMs, the last with the
+// residual partials (reading R-3; same arithmetic class as certify_best).
+static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho) {
+  const void *X = c->Zr;
+  for (int j = 2; j <= c->p; ++j) {
+    GemmArgs g = base_args(c, IPR_FP64, X);
+    chat_view(c, i, IPR_FP64, &g.A, &g.a_kp, &g.a_pstride);
+    g.mode = EPI_STORE_T | (j == c->p ? EPI_RESID : 0);
+    g.tout = c->T[j & 1]; g.ldt = c->npad; g.part = c->part;
+    CK(run_gemm(c, g));
+    X = c->T[j & 1];
+  }
+  CK(launch_reduce_sum(c->part, tiles_n_total(c, IPR_FP64) * tiles_m(c, IPR_FP64), c->dscal + 2, c->st));
+  CK(cudaMemcpyAsync(c->hscal + 2, c->dscal + 2, 8, cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  *rho = std::sqrt(c->hscal[2]);
+  return IPR_OK;
 }
 
 static ipr_status certify_best(ipr_ctx *c, double *rho) {

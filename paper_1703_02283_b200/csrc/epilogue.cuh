@@ -33,6 +33,9 @@ template <int MODE = -1>
 __device__ __forceinline__ void epi_element(const GemmArgs &g, int64_t row, int64_t col,
                                             double v, EpiAcc &acc) {
   const int mode = MODE >= 0 ? MODE : g.mode;
+  if (mode & EPI_STORE_N) store_operand(g.nout, row * g.ldn + col, g.prec, v, 0);
+  const bool mirror = g.tri && row != g.col0 + col;   // tri: (i,j), i < j, also stands for (j,i)
+  if (g.tri && row > g.col0 + col) return;             // tri: lower triangle comes from the mirror
   if (mode & (EPI_STORE_T | EPI_TSCRATCH)) {
     double w = v;
     if (mode & EPI_DIAG_MINUS) {      // diag*I - D: NS What = 2I - A X, symmetric R = I - Z_p
@@ -42,6 +45,7 @@ __device__ __forceinline__ void epi_element(const GemmArgs &g, int64_t row, int6
     if (mode & EPI_STORE_T) {
       // FP16 T operands go through EPI_TSCRATCH + a scale kernel (sigma 0 here)
       store_operand(g.tout, col * g.ldt + row, g.tprec, w, 0);
+      if (mirror) store_operand(g.tout, row * g.ldt + col, g.tprec, w, 0);
     } else {
       ((float *)g.tout)[col * g.ldt + row] = (float)w;
       acc.mx = fmaxf(acc.mx, fabsf((float)w));
@@ -70,7 +74,7 @@ __device__ __forceinline__ void epi_element(const GemmArgs &g, int64_t row, int6
     const int64_t gc = g.col0 + col;
     if (row < g.n && gc < g.n) {
       const double d = __dsub_rn(row == gc ? 1.0 : 0.0, v);
-      acc.r2 = __fma_rn(d, d, acc.r2);
+      acc.r2 = __fma_rn(mirror ? 2.0 * d : d, d, acc.r2);
     }
   }
   if (mode & EPI_UPDATE) {

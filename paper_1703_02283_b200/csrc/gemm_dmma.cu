@@ -59,6 +59,10 @@ __global__ void __launch_bounds__(DM_NT, 2) k_gemm_dmma(const GemmArgs g) {
     tn = r / gm;
   }
   const int64_t m0 = (int64_t)tm * DM_BM, n0 = (int64_t)tn * DM_BN;
+  if (g.tri && m0 > g.col0 + n0 + DM_BN - 1) {          // wholly below the diagonal (tri form)
+    if (tid == 0 && (g.mode & EPI_RESID)) g.part[((g.col0 + n0) / DM_BN) * g.tiles_m + tm] = 0.0;
+    return;
+  }
   const double *A = (const double *)g.A, *B = (const double *)g.B;
   const int nkb = (int)(g.K / DM_BK);
   const int kb_per_panel = (int)(g.a_kp / DM_BK);
@@ -178,6 +182,7 @@ cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s) {
   // the hot-path modes get specialised kernels; anything else uses the runtime-mode build
   if (!a.pmax && a.prec == P_FP64) {
     if (a.mode == EPI_STORE_T) return launch_mode<EPI_STORE_T>(a, s);
+    if (a.mode == (EPI_STORE_T | EPI_STORE_N)) return launch_mode<EPI_STORE_T | EPI_STORE_N>(a, s);
     if (a.mode == (EPI_STORE_T | EPI_RESID)) return launch_mode<EPI_STORE_T | EPI_RESID>(a, s);
     if (a.mode == (EPI_STORE_T | EPI_DIAG_MINUS | EPI_RESID))
       return launch_mode<EPI_STORE_T | EPI_DIAG_MINUS | EPI_RESID>(a, s);

@@ -187,12 +187,17 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
     for (int j = 0; j < 32; ++j) {
       const double v = __dmul_rn((double)__uint_as_float(r[j]), scale);
       const int64_t c = col + j;
+      if (g.tri && row > g.col0 + c) continue;         // tri: lower triangle comes from the mirror
+      const bool mirror = g.tri && row != g.col0 + c;
       double w = v;
       if (mode & EPI_DIAG_MINUS) {    // diag*I - D: NS What = 2I - A X, symmetric R = I - Z_p
         const int64_t gc = g.col0 + c;
         w = __dsub_rn((row == gc && row < g.n) ? g.diag : 0.0, v);
       }
-      if (mode & EPI_STORE_T) store_operand(g.tout, c * g.ldt + row, g.tprec, w, 0);
+      if (mode & EPI_STORE_T) {
+        store_operand(g.tout, c * g.ldt + row, g.tprec, w, 0);
+        if (mirror) store_operand(g.tout, row * g.ldt + c, g.tprec, w, 0);
+      }
       if (mode & EPI_TSCRATCH) {
         ((float *)g.tout)[c * g.ldt + row] = (float)w;
         ea.mx = fmaxf(ea.mx, fabsf((float)w));
@@ -201,7 +206,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
         const int64_t gc = g.col0 + c;
         if (row < g.n && gc < g.n) {
           const double d = __dsub_rn(row == gc ? 1.0 : 0.0, v);
-          ea.r2 = __fma_rn(d, d, ea.r2);
+          ea.r2 = __fma_rn(mirror ? 2.0 * d : d, d, ea.r2);
         }
       }
       if (mode & EPI_F64) g.zout[row * g.ldz + c] = v;
@@ -315,6 +320,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       for (int t = pair; t < ntiles; t += npairs) {
         int tm, tn;
         sch.get(t, tm, tn);
+        if (g.tri && tm > tn) continue;                // pair tile wholly below the diagonal
         const int arow = tm * 2 * TC_BM + (int)rank * TC_BM;
         const int brow = tn * TC_BN + (int)rank * (TC_BN / 2);
         for (int kb = 0; kb < nkb; ++kb) {
@@ -335,7 +341,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = pair; t < ntiles; t += npairs, ++it) {
+      for (int t = pair; t < ntiles; t += npairs) {
+        {
+          int tm, tn;
+          sch.get(t, tm, tn);
+          if (g.tri && tm > tn) continue;
+        }
         const int buf = it & 1;
         mbar_wait_cluster(&tempty[buf], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -351,6 +362,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
           if (++stage == TC_ST) { stage = 0; phase ^= 1; }
         }
         tc_commit_pair(&tfull[buf]);
+        ++it;
       }
     }
   } else {
@@ -361,9 +373,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
     double scale = 1.0;
     if (g.sigA) scale = pow2(-(*g.sigA + *g.sigB));
     int it = 0;
-    for (int t = pair; t < ntiles; t += npairs, ++it) {
+    for (int t = pair; t < ntiles; t += npairs) {
       int tm, tn;
       sch.get(t, tm, tn);
+      if (g.tri && tm > tn) {   // skipped pair tile: its residual partials are zero
+        if (et == 0 && (g.mode & EPI_RESID))
+          g.part[((g.col0 + (int64_t)tn * TC_BN) / TC_BN) * g.tiles_m + tm * 2 + (int)rank] = 0.0;
+        continue;
+      }
       const int buf = it & 1;
       mbar_wait(&tfull[buf], (it >> 1) & 1);
       tc_fence_after();
@@ -410,6 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
           }
         }
       }
+      ++it;
     }
   }
   tc_fence_before();

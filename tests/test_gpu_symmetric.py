@@ -34,18 +34,24 @@ def schedules(name):
     return pg, po
 
 
-def run_sym(A, p, name, tol, iters):
+FORMS = {"symmetric": oracle.FORM_SYMMETRIC, "symmetric_tri": oracle.FORM_SYMMETRIC_TRI}
+
+
+def run_sym(A, p, name, tol, iters, form="symmetric"):
     pg, po = schedules(name)
-    r = oracle.solve(A, p, po, tol, iters, hist=iters, form=oracle.FORM_SYMMETRIC)
-    g = run_gpu_trajectory(A, p, pg, tol, iters, form="symmetric")
+    r = oracle.solve(A, p, po, tol, iters, hist=iters, form=FORMS[form])
+    g = run_gpu_trajectory(A, p, pg, tol, iters, form=form)
     return r, g
 
 
-@pytest.mark.parametrize("p,name", [(2, "fp64"), (3, "fp64"), (2, "fp64/cbf16"), (2, "bf16>fp64"),
-                                    (2, "tf32>fp64/cbf16"), (3, "bf16>fp64/ctf32"), (2, "bf16/ctf32>fp64")])
-def test_diagonal_bit_exact(p, name):
+@pytest.mark.parametrize("p,name,form", [(2, "fp64", "symmetric"), (3, "fp64", "symmetric"),
+                                         (2, "fp64/cbf16", "symmetric"), (2, "bf16>fp64", "symmetric"),
+                                         (2, "tf32>fp64/cbf16", "symmetric"), (3, "bf16>fp64/ctf32", "symmetric"),
+                                         (2, "bf16/ctf32>fp64", "symmetric"), (2, "fp64", "symmetric_tri"),
+                                         (2, "bf16>fp64/cbf16", "symmetric_tri"), (2, "tf32>fp64", "symmetric_tri")])
+def test_diagonal_bit_exact(p, name, form):
     A = synth.diag_spd(200, 1e3, 9)
-    r, (out, tr, hist, best) = run_sym(A, p, name, 1e-13, 120)
+    r, (out, tr, hist, best) = run_sym(A, p, name, 1e-13, 120, form)
     assert r.outcome == oracle.CONVERGED and out == ipr.IPR_CONVERGED
     assert [t["decision"] for t in tr] == [x["decision"] for x in r.records]
     for k, Ck in hist.items():
@@ -57,10 +63,11 @@ def test_diagonal_bit_exact(p, name):
     assert tr[-1]["rho_cert"] <= 1e-13
 
 
-@pytest.mark.parametrize("n,p", [(300, 2), (300, 3), (520, 2)])
-def test_fp64_twin_trajectory(n, p):
+@pytest.mark.parametrize("n,p,form", [(300, 2, "symmetric"), (300, 3, "symmetric"), (520, 2, "symmetric"),
+                                      (300, 2, "symmetric_tri"), (520, 2, "symmetric_tri")])
+def test_fp64_twin_trajectory(n, p, form):
     A = synth.spd(n, 2.0, 12)
-    r, (out, tr, hist, best) = run_sym(A, p, "fp64", 1e-12, 60)
+    r, (out, tr, hist, best) = run_sym(A, p, "fp64", 1e-12, 60, form)
     assert out == ipr.IPR_CONVERGED and r.outcome == oracle.CONVERGED
     assert abs(len(tr) - len(r.records)) <= 1
     for k, Ck in hist.items():
@@ -71,15 +78,17 @@ def test_fp64_twin_trajectory(n, p):
     assert tr[-1]["rho_cert"] <= 1e-12
 
 
-@pytest.mark.parametrize("name,m", [("bf16>fp64/cbf16", 7), ("tf32>fp64/cbf16", 10), ("bf16>fp64", 7),
-                                    ("bf16>tf32>fp64/cbf16", 7)])
-def test_mixed_level2(name, m):
+@pytest.mark.parametrize("name,m,form", [("bf16>fp64/cbf16", 7, "symmetric"), ("tf32>fp64/cbf16", 10, "symmetric"),
+                                         ("bf16>fp64", 7, "symmetric"), ("bf16>tf32>fp64/cbf16", 7, "symmetric"),
+                                         ("bf16>fp64/cbf16", 7, "symmetric_tri"),
+                                         ("bf16>tf32>fp64/cbf16", 7, "symmetric_tri")])
+def test_mixed_level2(name, m, form):
     # Level 2: low-phase iterates within 4 * 2^-m of the oracle, the same switch
     # iteration (R-6: +-1 only at a tie), final C within 1e-10, certified rho <= 1e-12; and the
     # refinement claim: the FP64 phase needs far fewer iterations than the literal form (F4).
     n, p = 384, 2
     A = synth.spd(n, 2.0, 4)
-    r, (out, tr, hist, best) = run_sym(A, p, name, 1e-12, 120)
+    r, (out, tr, hist, best) = run_sym(A, p, name, 1e-12, 120, form)
     assert out == ipr.IPR_CONVERGED and r.outcome == oracle.CONVERGED
     sw_g = [t["k"] for t in tr if t["decision"] == ipr.IPR_DEC_SWITCH]
     sw_o = [x["k"] for x in r.records if x["decision"] == oracle.SWITCH]
@@ -93,12 +102,13 @@ def test_mixed_level2(name, m):
     assert n64 <= 12, n64
 
 
-def test_run_to_run_deterministic_and_symmetric():
+@pytest.mark.parametrize("form", ["symmetric", "symmetric_tri"])
+def test_run_to_run_deterministic_and_symmetric(form):
     A = synth.spd(640, 2.0, 3)
     pg, _ = schedules("bf16>fp64/cbf16")
     res = []
     for _ in range(2):
-        out, tr, hist, best = run_gpu_trajectory(A, 2, pg, 1e-12, 60, form="symmetric")
+        out, tr, hist, best = run_gpu_trajectory(A, 2, pg, 1e-12, 60, form=form)
         res.append((tr, best))
         assert np.array_equal(best, best.T)
     (t1, b1), (t2, b2) = res
@@ -135,3 +145,18 @@ def test_errors():
     with pytest.raises(ipr.IprError) as e:
         ipr.Solver(A, 2, [ipr.make_phase("bf16", corr_prec="fp64")], 1e-12, form="symmetric")
     assert e.value.status == ipr.IPR_E_INVALID_ARG
+
+
+def test_tri_close_to_full_and_errors():
+    A = synth.spd(512, 2.0, 8)
+    pg, _ = schedules("bf16>fp64/cbf16")
+    _, t_full, _, b_full = run_gpu_trajectory(A, 2, pg, 1e-12, 60, keep=False, form="symmetric")
+    _, t_tri, _, b_tri = run_gpu_trajectory(A, 2, pg, 1e-12, 60, keep=False, form="symmetric_tri")
+    assert rel_fro(b_tri, b_full) <= 1e-12
+    assert abs(len(t_tri) - len(t_full)) <= 1
+    At = torch_cuda(A)
+    s = ipr.Solver(At, 3, [ipr.make_phase("fp64")], 1e-12, form="symmetric_tri")
+    with pytest.raises(ipr.IprError) as e:
+        s.iterate(1)
+    assert e.value.status == ipr.IPR_E_INVALID_ARG
+    s.close()

@@ -160,3 +160,29 @@ def test_rejects_p1_and_fp16():
     with pytest.raises(ValueError):
         oracle.solve(np.eye(4), 2, [oracle.phase(oracle.FP16), oracle.phase()], form=SYM)
     assert np.isnan(oracle.step_sym(np.eye(2), np.eye(2), 1, oracle.phase())[0])
+
+
+def test_tri_variant_mirrors_upper_triangle():
+    # NEXT-2 (iii): Z_2 = C A C is symmetric in exact arithmetic; the tri variant uses its upper
+    # triangle only.  Pins: (a) one tri step equals the full step with Z_2 symmetrised by its upper
+    # triangle (hand-assembled from oracle GEMMs), (b) same limit, (c) exactly symmetric R means
+    # the tri trajectory differs from the full one only at rounding level.
+    TRI = oracle.FORM_SYMMETRIC_TRI
+    A = synth.spd(40, 2.0, 6)
+    full = oracle.solve(A, 2, [oracle.phase()], 1e-12, 60, hist=30, form=SYM)
+    tri = oracle.solve(A, 2, [oracle.phase()], 1e-12, 60, hist=30, form=TRI)
+    assert tri.outcome == oracle.CONVERGED
+    assert abs(len(tri.records) - len(full.records)) <= 1
+    np.testing.assert_allclose(tri.C_best, full.C_best, rtol=1e-13, atol=1e-15)
+    # (a) the first step by hand: C_0 from the solve history
+    C0 = tri.C_hist[0]
+    Z1 = oracle.gemm(A, C0)
+    Z2 = oracle.gemm(C0, Z1)
+    Z2 = np.triu(Z2) + np.triu(Z2, 1).T
+    R = np.eye(40) - Z2
+    W = oracle.gemm(C0, R)
+    C1 = C0 + (W + W.T) / 4
+    np.testing.assert_array_equal(tri.C_hist[1], C1)
+    assert tri.records[0]["rho"] == pytest.approx(np.linalg.norm(R), rel=1e-14)
+    with pytest.raises(ValueError):
+        oracle.solve(A, 3, [oracle.phase()], form=TRI)
