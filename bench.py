@@ -217,6 +217,10 @@ def main():
     C_out = torch.empty_like(A)
     torch.cuda.synchronize()
     form, phases = schedule(args.schedule, n)
+    if world > 1 and form == "symmetric_tri":
+        # the tri form's mirrored stores cross column panels: single-GPU only (include/ipr.h)
+        form = "symmetric"
+        config["form_note"] = "symmetric_tri is single-GPU; N > 1 runs the full symmetric form"
 
     def solve(A_dev, out):
         s = ipr.Solver(A_dev, p, phases, 1e-12, stream, world, rank, uid, form=form)
@@ -260,17 +264,22 @@ def main():
     # 2 n^3 (local panel: 2 n^2 n/G); duration from the library's CUDA events on the launch stream
     fl_gemm = 2.0 * n * n * (n / world)
     # the p chain GEMMs of every FP64 record (gemm_ms - upd_ms: the update may be a BF16
-    # correction GEMM + k_sym_update in the symmetric form)
+    # correction GEMM + k_sym_update in the symmetric form).  Algorithmic flops of a chain:
+    # p * 2 n^3 / G, except the tri form, whose GEMM 2 (C A C) needs only the upper triangle:
+    # 2 n^3 + n^2 (n + 1) (its extra work on the diagonal tiles is overhead, not credit).
+    fl_chain = (2.0 * n ** 3 + n * n * (n + 1.0)) if form == "symmetric_tri" else p * fl_gemm
     tot_ms = sum(t["gemm_ms"] - t["upd_ms"] for trc, _ in traces for t in trc if t["prec"] == "fp64")
-    tot_gemms = sum(p * sum(1 for t in trc if t["prec"] == "fp64") for trc, _ in traces)
+    n_chains = sum(sum(1 for t in trc if t["prec"] == "fp64") for trc, _ in traces)
+    tot_gemms = p * n_chains
     gemm_ms = tot_ms / max(tot_gemms, 1)
-    achieved = fl_gemm / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+    achieved = (n_chains * fl_chain) / (tot_ms * 1e-3) / 1e12 if tot_ms > 0 else None
     all_ms = sum(t["gemm_ms"] for trc, _ in traces for t in trc)
     step_gemm_share = tot_ms / (ms * args.steps) if ms > 0 else None
     roof = {"bound": "tensor", "kernel": "k_gemm_dmma (FP64 DMMA.8x8x4)", "achieved": achieved,
             "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
             "traffic": None, "peak_source": FP64_PEAK_SRC, "cublas_dgemm_tflops": 35.5,
-            "algorithmic_flops_per_launch": fl_gemm, "avg_launch_ms": gemm_ms, "gemm_share_of_step": step_gemm_share,
+            "algorithmic_flops_per_launch": fl_chain / p, "avg_launch_ms": gemm_ms,
+            "algorithmic_flops_per_chain": fl_chain, "launches_per_chain": p, "gemm_share_of_step": step_gemm_share,
             "all_gemm_share_of_step": all_ms / (ms * args.steps) if ms > 0 else None}
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):

@@ -261,6 +261,7 @@ __global__ void __launch_bounds__(256) k_sym_update(const CT *__restrict__ cold,
   {
     const int64_t gi = ib + tx;
     const WT *src = W + (gi / kp) * slot + gi % kp;
+    #pragma unroll
     for (int r = ty; r < 64; r += 4) t[r][tx] = src[(col0 + jb + r) * kp];
   }
   __syncthreads();
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(256) k_sym_update(const CT *__restrict__ cold,
   const double tp = (double)(2 * p), itp = 1.0 / tp;
   const WT *wl = W + (col0 / kp) * slot;                  // this rank's slot
   double d2 = 0.0;
+  #pragma unroll 16
   for (int r = ty; r < 64; r += 4) {
     const int64_t i = ib + r, jl = jb + tx, ci = i * kp + jl;
     const double sw = __dadd_rn((double)wl[ci], (double)t[tx][r]);
