@@ -48,9 +48,17 @@ typedef enum {
   IPR_E_NCCL = 7           /* NCCL error or NCCL library not loadable                        */
 } ipr_status;
 
-/* GEMM input (operand) format of a phase.  Accumulation is FP32 for BF16/FP16/TF32
- * (tcgen05 tensor cores, kind::f16 / kind::tf32) and FP64 for FP64 (DMMA). */
-typedef enum { IPR_FP64 = 0, IPR_TF32 = 1, IPR_BF16 = 2, IPR_FP16 = 3 } ipr_prec;
+/* GEMM input (operand) format of a phase.  Accumulation is FP32 for BF16/FP16/TF32/FP8
+ * (tcgen05 tensor cores, kind::f16 / kind::tf32 / kind::f8f6f4), exact INT32 for INT8
+ * (kind::i8) and FP64 for FP64 (DMMA).
+ * Scaled formats carry a per-tensor power-of-two scale 2^sigma chosen from max|X| (reading R-20;
+ * every product is unscaled exactly in FP64):
+ *   IPR_FP16  e5m10,  scaled max in [2^14, 2^15)
+ *   IPR_FP8   E4M3 (PAPER.md:263-267 finds 2 stored mantissa bits still
+ *             converge in storage-only mode), scaled max in [2^6, 2^7), one RNE rounding
+ *   IPR_INT8  8-bit fixed point q = sat_127(rint(2^sigma x)), scaled max in [2^6, 2^7) -- the
+ *             tensor-core analogue of the paper's fixed-point storage. */
+typedef enum { IPR_FP64 = 0, IPR_TF32 = 1, IPR_BF16 = 2, IPR_FP16 = 3, IPR_FP8 = 4, IPR_INT8 = 5 } ipr_prec;
 
 /* Rounding of the stored iterate (reading R-7: RNE default; RTZ = "bit truncation",
  * PAPER.md:26).  Operand conversions are always round-to-nearest-even (hardware cvt.rn). */
@@ -77,14 +85,16 @@ typedef struct {
   ipr_prec  prec;          /* operand format of the p+1 GEMMs                                */
   int       mant_bits;     /* m: stored mantissa bits of C and A (R-8 container: e8 for      */
                            /* BF16/FP16/TF32 phases, m <= 23; e11 for FP64, m <= 52); -1 =   */
-                           /* the operand format's own (7 BF16, 10 FP16/TF32, 52 FP64)       */
+                           /* the operand format's own (3 FP8, 7 BF16/INT8, 10 FP16/TF32,    */
+                           /* 52 FP64)                                                        */
   ipr_round round;         /* rounding of stored C and A                                     */
   double    switch_tol;    /* 0 = off                                                         */
   double    plateau_ratio; /* 0 = off (typ. 0.7)                                              */
   double    plateau_arm;   /* typ. 0.5                                                        */
   int       max_iters;     /* per-phase cap on chains; 0 = unlimited                          */
   int       corr_prec;     /* IPR_FORM_SYMMETRIC only: ipr_prec of the correction GEMM        */
-                           /* W = qc(C) qc(I - C^{p-1}AC); -1 = prec.  FP16 unsupported; FP64 */
+                           /* W = qc(C) qc(I - C^{p-1}AC); -1 = prec (BF16 for the scaled     */
+                           /* FP16/FP8/INT8 phases).  Must be BF16, TF32 or FP64; FP64     */
                            /* only in FP64 phases.  A BF16/TF32 correction in an FP64 phase   */
                            /* is mixed-precision refinement: R is small, so W needs only      */
                            /* relative accuracy (R-22).  Ignored by other forms.    */

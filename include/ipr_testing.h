@@ -20,6 +20,8 @@ extern "C" {
  *   mode 2: FP32 in  -> BF16 out (uint16 bit patterns), round-to-nearest-even
  *   mode 3: FP32 in  -> FP32 out rounded to the TF32 grid (e8m10), round-to-nearest-even
  *   mode 4: FP32 in  -> FP16 out (uint16 bit patterns) of 2^sigma * x, RNE (R-20 scaling)
+ *   mode 5: FP64 in  -> FP8 E4M3 out (uint8 bit patterns) of 2^sigma * x, one RNE rounding (NEXT-3)
+ *   mode 6: FP64 in  -> INT8 out of sat_127(rint(2^sigma * x)) (fixed point, NEXT-3)
  * m: stored mantissa bits (modes 0/1), round: ipr_round (modes 0/1).  len >= 0. */
 ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_t len, int m,
                              int round, int sigma, void *stream);
@@ -29,7 +31,9 @@ ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_
  *   Yt : K-major operand   (element (k,j) of Y at Yt[j*n + k])
  *   Z  : FP64 row-major, the accumulator converted exactly (FP32 -> FP64 for tensor-core
  *        kinds).  Formats: prec = IPR_FP64 (double), IPR_TF32 (float on the TF32 grid),
- *        IPR_BF16 / IPR_FP16 (uint16 bit patterns).  n >= 1 (any n; ragged tiles handled). */
+ *        IPR_BF16 / IPR_FP16 (uint16 bit patterns), IPR_FP8 (E4M3 bytes, FP32 accumulate),
+ *        IPR_INT8 (int8, exact INT32 accumulate).  Operands unscaled (sigma 0).
+ *        n >= 1 (any n; ragged tiles handled). */
 ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_dev,
                          double *Z_dev, void *stream);
 

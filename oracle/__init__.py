@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ipr_oracle.c")
 _LIB = os.path.join(_HERE, "libipr_oracle.so")
 
-FP64, TF32, BF16, FP16 = 0, 1, 2, 3
+FP64, TF32, BF16, FP16, FP8, INT8 = 0, 1, 2, 3, 4, 5
 RNE, RTZ = 0, 1
 CONTINUE, CONVERGED, ITER_LIMIT, DIVERGED, NONFINITE, SWITCH = 0, 1, 2, 3, 4, 5
 OUTCOME_NAMES = {0: "running", 1: "converged", 2: "iter_limit", 3: "diverged", 4: "nonfinite",
@@ -90,6 +90,9 @@ def lib():
         L.orc_inv_proot_eig.argtypes = [C.c_int64, _dp, _dp, C.c_int, _dp]
         L.orc_spectral.argtypes = [C.c_int64, _dp, C.c_int, C.c_double, C.c_int, _dp]
         L.orc_fp16_sigma.argtypes = [C.c_double]
+        L.orc_sigma.argtypes = [C.c_int, C.c_double]
+        L.orc_q_int8.restype = C.c_double
+        L.orc_q_int8.argtypes = [C.c_double]
         L.orc_ctrl_init.argtypes = [C.POINTER(Ctrl), C.c_int64, C.c_int, C.c_double]
         L.orc_ctrl_decide.argtypes = [C.POINTER(Ctrl), C.POINTER(Phase), C.c_double]
         L.orc_ctrl_enter_next_phase.argtypes = [C.POINTER(Ctrl)]
@@ -138,6 +141,16 @@ def native_m(prec: int) -> int:
 
 def fp16_sigma(maxabs: float) -> int:
     return lib().orc_fp16_sigma(maxabs)
+
+
+def sigma(prec: int, maxabs: float) -> int:
+    """Scale exponent of the scaled operand formats (FP16 / FP8 / INT8), 0 otherwise."""
+    return lib().orc_sigma(prec, maxabs)
+
+
+def q_int8(x: float) -> float:
+    """INT8 fixed-point quantiser: nearest-even integer saturated to [-127, 127]."""
+    return lib().orc_q_int8(x)
 
 
 def norms(A):

@@ -45,12 +45,17 @@ void orc_qm_array(int64_t len, const double *x, double *y, int E, int m, int rtz
 }
 
 /* Operand formats (R-9, R-10): BF16 = e8m7, FP16 = e5m10 (PAPER.md:106-107 footnote),
+ * FP8 = e4m3 (NEXT-3; scaled so |values| < 2^7: the IEEE-like e4m3 grid and the hardware's
+ * E4M3 "fn" grid coincide there), INT8 = 8-bit two's-complement fixed point (NEXT-3, the
+ * fixed-point analogue of PAPER.md:268-281; M = 7 magnitude bits, no exponent field),
  * TF32 = e8m10, FP64 = e11m52 (PAPER.md:110-111 footnote). */
 void orc_prec_format(int prec, int *E, int *M) {
   switch (prec) {
     case ORC_TF32: *E = 8;  *M = 10; break;
     case ORC_BF16: *E = 8;  *M = 7;  break;
     case ORC_FP16: *E = 5;  *M = 10; break;
+    case ORC_FP8:  *E = 4;  *M = 3;  break;
+    case ORC_INT8: *E = 0;  *M = 7;  break;
     default:       *E = 11; *M = 52; break;
   }
 }
@@ -74,6 +79,26 @@ int orc_fp16_sigma(double maxabs) {
   return 14 - (ex - 1);        /* scaled max in [2^14, 2^15), below FP16 max 65504 */
 }
 
+/* Scale exponent of a scaled operand format: FP16 as above; FP8 and INT8: scaled max in
+ * [2^6, 2^7) (below the E4M3 max 448 and inside the int8 range).  0 for unscaled formats. */
+int orc_sigma(int prec, double maxabs) {
+  if (prec == ORC_FP16) return orc_fp16_sigma(maxabs);
+  if (prec != ORC_FP8 && prec != ORC_INT8) return 0;
+  if (!(maxabs > 0.0) || !isfinite(maxabs)) return 0;
+  int ex;
+  frexp(maxabs, &ex);
+  return 6 - (ex - 1);
+}
+
+/* INT8 fixed point: nearest integer (ties to even), saturated to [-127, 127]. */
+double orc_q_int8(double x) {
+  if (isnan(x)) return x;
+  double q = nearbyint(x);
+  if (q > 127.0) q = 127.0;
+  if (q < -127.0) q = -127.0;
+  return q;
+}
+
 static double maxabs_of(int64_t len, const double *x) {
   double m = 0.0;
   for (int64_t i = 0; i < len; ++i) { double a = fabs(x[i]); if (a > m || isnan(a)) m = a; }
@@ -86,8 +111,11 @@ static int qin_matrix(int prec, int64_t len, const double *x, double *y) {
   int E, M;
   orc_prec_format(prec, &E, &M);
   if (prec == ORC_FP64) { if (y != x) memcpy(y, x, (size_t)len * sizeof(double)); return 0; }
-  int sigma = 0;
-  if (prec == ORC_FP16) sigma = orc_fp16_sigma(maxabs_of(len, x));
+  const int sigma = orc_sigma(prec, maxabs_of(len, x));
+  if (prec == ORC_INT8) {
+    for (int64_t i = 0; i < len; ++i) y[i] = orc_q_int8(ldexp(x[i], sigma));
+    return sigma;
+  }
   for (int64_t i = 0; i < len; ++i) y[i] = orc_qm(ldexp(x[i], sigma), E, M, 0);
   return sigma;
 }
@@ -335,20 +363,29 @@ static double update_ns(int64_t n, const double *X, const orc_phase *ph, chain_w
  *   W = qc(C) Rhat  (FP64 accumulator),   C_{k+1}[i][j] = q_m(C_ij + (W_ij + W_ji) / (2p))
  * where qc is the operand format of the correction GEMM (corr_prec; = prec by default).
  * C_{k+1} is exactly symmetric whenever C_k is (W_ij + W_ji is commutative in IEEE).
- * FP16 phases are not defined for this form (no operand scaling here).
+ * Scaled formats (FP16/FP8/INT8) scale Chat, Ahat and qin(Z_j) by powers of two (reading R-20)
+ * and unscale every product exactly; the correction format must be BF16, TF32 or FP64.
  * ------------------------------------------------------------------------------ */
-static int corr_of(const orc_phase *ph) { return ph->corr_prec < 0 ? ph->prec : ph->corr_prec; }
+static int is_scaled(int prec) { return prec == ORC_FP16 || prec == ORC_FP8 || prec == ORC_INT8; }
+/* default correction format: the phase's own, BF16 for the scaled formats */
+static int corr_of(const orc_phase *ph) {
+  if (ph->corr_prec >= 0) return ph->corr_prec;
+  return is_scaled(ph->prec) ? ORC_BF16 : ph->prec;
+}
 
 static double chain_sym(int64_t n, int p, int tri, const double *A, const double *C,
                         const orc_phase *ph, chain_ws *w) {
   const int64_t nn = n * n;
   for (int64_t i = 0; i < nn; ++i) w->T[i] = store_q(ph, A[i]);
-  qin_matrix(ph->prec, nn, w->T, w->X);                     /* w->X = Ahat            */
-  qin_matrix(ph->prec, nn, C, w->Chat);                     /* w->Chat = Chat         */
+  const int sigA = qin_matrix(ph->prec, nn, w->T, w->X);    /* w->X = Ahat            */
+  w->sigC = qin_matrix(ph->prec, nn, C, w->Chat);           /* w->Chat = Chat         */
   orc_gemm(n, w->X, w->Chat, w->T);                         /* Z_1 = Ahat Chat        */
-  for (int j = 2; j <= p; ++j) {
-    qin_matrix(ph->prec, nn, w->T, w->X);                   /* qin(Z_{j-1})           */
-    orc_gemm(n, w->Chat, w->X, w->T);                       /* Z_j = Chat qin(Z_{j-1}) */
+  int sigX = sigA;                                           /* scaled formats: unscale */
+  for (int j = 1; j <= p; ++j) {
+    if (j > 1) orc_gemm(n, w->Chat, w->X, w->T);            /* Z_j = Chat qin(Z_{j-1}) */
+    if (sigX + w->sigC != 0)
+      for (int64_t i = 0; i < nn; ++i) w->T[i] = ldexp(w->T[i], -(sigX + w->sigC));
+    if (j < p) sigX = qin_matrix(ph->prec, nn, w->T, w->X); /* qin(Z_j)               */
   }
   if (tri)                     /* ORC_FORM_SYMMETRIC_TRI: Z_2 = C A C from its upper triangle */
     for (int64_t r = 0; r < n; ++r)
@@ -431,7 +468,7 @@ double orc_step_ns(int64_t n, const double *A, const double *X, const orc_phase 
 
 double orc_step_sym(int64_t n, int p, const double *A, const double *C, const orc_phase *ph,
                     double *C_next, double *delta) {
-  if (p < 2 || ph->prec == ORC_FP16 || corr_of(ph) == ORC_FP16) return NAN;
+  if (p < 2 || is_scaled(corr_of(ph))) return NAN;
   chain_ws w;
   if (!ws_alloc(&w, n)) { ws_free(&w); return NAN; }
   const double rho = chain_sym(n, p, 0, A, C, ph, &w);
@@ -459,7 +496,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
   if (sym) {
     if (p < 2 || (form == ORC_FORM_SYMMETRIC_TRI && p != 2)) return -1;
     for (int i = 0; i < nphases; ++i)
-      if (phases[i].prec == ORC_FP16 || corr_of(&phases[i]) == ORC_FP16) return -1;
+      if (is_scaled(corr_of(&phases[i]))) return -1;
   }
   if (form < ORC_FORM_LITERAL || form > ORC_FORM_SYMMETRIC_TRI) return -1;
   if (!orc_is_symmetric(n, A)) return -2;

@@ -27,7 +27,7 @@ extern "C" {
 #endif
 
 /* Operand (GEMM input) formats.  Values are independent of include/ipr.h on purpose. */
-enum { ORC_FP64 = 0, ORC_TF32 = 1, ORC_BF16 = 2, ORC_FP16 = 3 };
+enum { ORC_FP64 = 0, ORC_TF32 = 1, ORC_BF16 = 2, ORC_FP16 = 3, ORC_FP8 = 4, ORC_INT8 = 5 };
 enum { ORC_RNE = 0, ORC_RTZ = 1 };
 enum { ORC_CONTINUE = 0, ORC_CONVERGED = 1, ORC_ITER_LIMIT = 2, ORC_DIVERGED = 3,
        ORC_NONFINITE = 4, ORC_SWITCH = 5 };
@@ -143,6 +143,10 @@ void orc_spectral(int64_t n, const double *lambda, int p, double s, int kmax, do
 /* FP16 phase operand scale exponent: sigma = 14 - floor(log2(max|X|)) (0 if max is 0
  * or non-finite).  Stored FP16 operand = q16(2^sigma X). */
 int orc_fp16_sigma(double maxabs);
+/* Scale exponent of the scaled operand formats: FP16 (as above), FP8 E4M3 and INT8 (scaled max
+ * in [2^6, 2^7)); 0 otherwise.  INT8 quantiser: nearest-even integer saturated to +-127. */
+int orc_sigma(int prec, double maxabs);
+double orc_q_int8(double x);
 
 #ifdef __cplusplus
 }

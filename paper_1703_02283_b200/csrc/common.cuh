@@ -10,10 +10,14 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 
 namespace ipr {
 
-enum Prec { P_FP64 = 0, P_TF32 = 1, P_BF16 = 2, P_FP16 = 3 };
+enum Prec { P_FP64 = 0, P_TF32 = 1, P_BF16 = 2, P_FP16 = 3, P_FP8 = 4, P_INT8 = 5 };
+
+// Operand formats that carry a per-tensor power-of-two scale 2^sigma (reading R-20; NEXT-3).
+__host__ __device__ inline bool is_scaled(int prec) { return prec == P_FP16 || prec == P_FP8 || prec == P_INT8; }
 
 // Epilogue modes of the GEMM kernels (bit flags).
 enum EpiMode : int {
@@ -122,27 +126,48 @@ __device__ __forceinline__ float to_tf32(float x) {
   return __uint_as_float(r | sign);
 }
 
-// FP16 phase scale exponent (reading R-20): sigma = 14 - floor(log2 max), 0 if max <= 0 / NaN / Inf.
-__device__ __forceinline__ int fp16_sigma(double mx) {
+// Scale exponent of a scaled operand (reading R-20): FP16 sigma = 14 - floor(log2 max) (scaled max
+// in [2^14, 2^15)); FP8 E4M3 and INT8 sigma = 6 - floor(log2 max) (scaled max in [64, 128)).
+// 0 if max <= 0 / NaN / Inf.
+__device__ __forceinline__ int op_sigma(int prec, double mx) {
   if (!(mx > 0.0) || isinf(mx)) return 0;
-  return 14 - ilogb(mx);
+  return (prec == P_FP16 ? 14 : 6) - ilogb(mx);
 }
 
 // exact 2^e as double (|e| <= 1000)
 __device__ __forceinline__ double pow2(int e) { return bits2d((uint64_t)(1023 + e) << 52); }
 
-// Operand store of an FP32/FP64 value in phase precision (RNE), FP16 scaled by 2^sig.
+// E4M3 grid (NEXT-3) of an FP64 value with |x| < 448: RNE to 3 mantissa bits for |x| >= 2^-6,
+// multiples of 2^-9 below (subnormals) -- one rounding from FP64; the result is exactly
+// representable, so the final cvt is exact.
+__device__ __forceinline__ uint8_t to_e4m3(double x) {
+  const double a = fabs(x);
+  double q;
+  if (a >= 0.015625) q = q_e11(x, 3, 0);
+  else q = __dmul_rn(rint(__dmul_rn(x, 512.0)), 1.0 / 512.0);
+  return (uint8_t)__nv_cvt_double_to_fp8(q, __NV_SATFINITE, __NV_E4M3);
+}
+// INT8 fixed point (NEXT-3): nearest-even integer, saturated to [-127, 127]
+__device__ __forceinline__ int8_t to_int8(double x) {
+  double q = rint(x);
+  q = fmin(fmax(q, -127.0), 127.0);
+  return (int8_t)(int)q;
+}
+
+// Operand store of an FP32/FP64 value in phase precision (RNE); scaled formats get 2^sig first.
 __device__ __forceinline__ void store_operand(void *base, int64_t idx, int prec, double v, int sig) {
   switch (prec) {
     case P_FP64: ((double *)base)[idx] = v; break;
     case P_TF32: ((float *)base)[idx] = to_tf32((float)v); break;
     case P_BF16: ((__nv_bfloat16 *)base)[idx] = __float2bfloat16_rn((float)v); break;
     case P_FP16: ((__half *)base)[idx] = __float2half_rn((float)__dmul_rn(v, pow2(sig))); break;
+    case P_FP8: ((uint8_t *)base)[idx] = to_e4m3(__dmul_rn(v, pow2(sig))); break;
+    case P_INT8: ((int8_t *)base)[idx] = to_int8(__dmul_rn(v, pow2(sig))); break;
   }
 }
 
 __host__ __device__ inline int elt_size(int prec) {
-  return prec == P_FP64 ? 8 : (prec == P_BF16 || prec == P_FP16) ? 2 : 4;
+  return prec == P_FP64 ? 8 : (prec == P_BF16 || prec == P_FP16) ? 2 : (prec == P_FP8 || prec == P_INT8) ? 1 : 4;
 }
 
 // Deterministic block-wide sum of one double per thread (fixed shuffle tree + warp order).
@@ -180,7 +205,7 @@ __device__ __forceinline__ float block_max(float v, float *red) {
 namespace ipr {
 extern int64_t g_launches;
 cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s);
-cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s);  // BF16 / FP16 / TF32
+cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s);  // BF16 / FP16 / TF32 / FP8 / INT8
 bool tc_supported(int prec);
 const char *tc_last_error();
 int gemm_tile_n(int prec);   // BN of the kernel used for a precision (partial layout)

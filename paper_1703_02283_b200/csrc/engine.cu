@@ -163,7 +163,9 @@ ipr_status fail(ipr_ctx *c, ipr_status s, const char *fmt, ...) {
     if (_s != IPR_OK) return _s;                                                              \
   } while (0)
 
-int native_m(int prec) { return prec == IPR_FP64 ? 52 : prec == IPR_BF16 ? 7 : 10; }
+int native_m(int prec) {
+  return prec == IPR_FP64 ? 52 : (prec == IPR_BF16 || prec == IPR_INT8) ? 7 : prec == IPR_FP8 ? 3 : 10;
+}
 
 // padded order: whole 256-wide tiles per rank (tcgen05 tile N), zero padding
 int64_t padded_order(int64_t n, int world) {
@@ -245,10 +247,10 @@ GemmArgs base_args(ipr_ctx *c, int prec, const void *Bop) {
 // ---- stage A for a phase (a1) ----
 ipr_status stage_a(ipr_ctx *c, const PhaseC &P, void *dst, int *sig_dst) {
   const int *sig = nullptr;
-  if (P.prec == IPR_FP16) {
+  if (is_scaled(P.prec)) {
     const int nparts = 1024;
     CK(launch_maxabs_qA(c->A, c->lda, c->n, P.cont64, P.m, P.rtz, c->pmax, nparts, c->st));
-    CK(launch_reduce_max(c->pmax, nparts, nullptr, sig_dst, c->st));
+    CK(launch_reduce_max(c->pmax, nparts, nullptr, sig_dst, P.prec, c->st));
     sig = sig_dst;
   }
   CK(launch_stage_a(c->A, c->lda, c->n, c->npad, c->col0, c->kp, P.prec, P.cont64, P.m, P.rtz, sig, dst, c->st));
@@ -260,11 +262,11 @@ ipr_status make_operand(ipr_ctx *c, int i, const PhaseC &P) {
   const int64_t cnt = c->npad * c->kp;
   if (P.prec != IPR_FP64) {
     const int *sig = nullptr;
-    if (P.prec == IPR_FP16) {
+    if (is_scaled(P.prec)) {
       const int nparts = 256;
       CK(launch_maxabs_cont(c->cont[i], P.cont64, cnt, c->pmax + c->rank * nparts, nparts, c->st));
       CKS(gather_pmax(c, c->pmax, nparts));
-      CK(launch_reduce_max(c->pmax, (int64_t)nparts * c->world, nullptr, c->dsig + 1 + i, c->st));
+      CK(launch_reduce_max(c->pmax, (int64_t)nparts * c->world, nullptr, c->dsig + 1 + i, P.prec, c->st));
       sig = c->dsig + 1 + i;
     }
     CK(launch_make_operand(cont_ptr(c, i, P), P.cont64, cnt, P.prec, sig, chat_slot(c, i, P.prec), c->st));
@@ -311,7 +313,7 @@ ipr_status begin_phase(ipr_ctx *c, bool first) {
   CKS(stage_a(c, P, c->Aop, c->dsig + 0));
   if (c->form != IPR_FORM_LITERAL && c->world > 1) {   // full row-major Ahat (A operand)
     CK(launch_stage_a(c->A, c->lda, c->n, c->npad, 0, c->npad, P.prec, P.cont64, P.m, P.rtz,
-                      P.prec == IPR_FP16 ? c->dsig + 0 : nullptr, c->Afull, c->st));
+                      is_scaled(P.prec) ? c->dsig + 0 : nullptr, c->Afull, c->st));
   }
   if (first) {
     CK(launch_c0(c->A, c->lda, c->n, c->npad, c->col0, c->kp, c->norms[3], P.cont64, P.m, P.rtz,
@@ -343,7 +345,8 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
   const PhaseC &P = c->ph[c->phase];
   const int prec = P.prec;
   const void *X = c->Aop;
-  const int *sigX = (prec == IPR_FP16) ? c->dsig + 0 : nullptr;
+  const bool scaled = is_scaled(prec);
+  const int *sigX = scaled ? c->dsig + 0 : nullptr;
   const int64_t tm = tiles_m(c, prec), tn_loc = c->kp / gemm_tile_n(prec);
   double *part = c->part;
   CK(cudaEventRecord(c->ev[0], c->st));
@@ -353,17 +356,17 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
     GemmArgs g = base_args(c, prec, c->T[0]);
     g.A = c->world == 1 ? c->Aop : c->Afull;
     g.a_kp = c->npad; g.a_pstride = c->npad * c->npad;
-    if (prec == IPR_FP16) { g.sigA = c->dsig + 0; g.sigB = c->dsig + 1 + c->cur; g.pmax = c->pmax; }
-    g.mode = (prec == IPR_FP16 ? EPI_TSCRATCH : EPI_STORE_T) | EPI_DIAG_MINUS | EPI_RESID;
+    if (scaled) { g.sigA = c->dsig + 0; g.sigB = c->dsig + 1 + c->cur; g.pmax = c->pmax; }
+    g.mode = (scaled ? EPI_TSCRATCH : EPI_STORE_T) | EPI_DIAG_MINUS | EPI_RESID;
     g.diag = 2.0;
-    g.tout = (prec == IPR_FP16) ? (void *)c->tscr : c->T[1];
+    g.tout = scaled ? (void *)c->tscr : c->T[1];
     g.ldt = c->npad;
     g.part = part;
     CK(run_gemm(c, g));
-    if (prec == IPR_FP16) {
+    if (scaled) {
       CKS(gather_pmax(c, c->pmax, tn_loc * tm));
-      CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 4, c->st));
-      CK(launch_scale_fp16(c->tscr, c->kp * c->npad, c->dsig + 4, c->T[1], c->st));
+      CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 4, prec, c->st));
+      CK(launch_scale_op(c->tscr, c->kp * c->npad, c->dsig + 4, prec, c->T[1], c->st));
     }
   }
   if (is_sym(c)) {
@@ -378,7 +381,11 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
       } else {
         chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
       }
-      g.mode = EPI_STORE_T;
+      // scaled formats (FP16/FP8/INT8): unscale by 2^-(sigma_X + sigma_C); Z_j (j < p) goes through
+      // the FP32 scratch + per-tile max so its own sigma is known before it becomes an operand
+      if (scaled) { g.sigA = c->dsig + 1 + c->cur; g.sigB = sigX; }
+      g.mode = (scaled && j < c->p) ? EPI_TSCRATCH : EPI_STORE_T;
+      if (scaled && j < c->p) { g.pmax = c->pmax; }
       if (j == 1) {
         // FP64 last phase (G = 1): also keep Z_1 = A C row-major -- the B operand of C (C A), so
         // certifying ||I - C^p A||_F costs p - 1 GEMMs instead of p
@@ -391,26 +398,32 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
         g.mode |= EPI_DIAG_MINUS | EPI_RESID; g.diag = 1.0; g.tprec = P.corr;
         g.tri = c->form == IPR_FORM_SYMMETRIC_TRI;   // Z_2 = C A C: upper triangle + mirror
       }
-      g.tout = c->T[j & 1];
+      g.tout = (scaled && j < c->p) ? (void *)c->tscr : c->T[j & 1];
       g.ldt = c->npad;
       g.part = part;
       CK(run_gemm(c, g));
+      if (scaled && j < c->p) {
+        CKS(gather_pmax(c, c->pmax, tn_loc * tm));
+        CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 3 + (j & 1), prec, c->st));
+        CK(launch_scale_op(c->tscr, c->kp * c->npad, c->dsig + 3 + (j & 1), prec, c->T[j & 1], c->st));
+        sigX = c->dsig + 3 + (j & 1);
+      }
     }
   }
   for (int j = 1; c->form == IPR_FORM_LITERAL && j <= c->p; ++j) {
     GemmArgs g = base_args(c, prec, X);
     chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
-    if (prec == IPR_FP16) { g.sigA = c->dsig + 1 + c->cur; g.sigB = sigX; }
-    g.mode = (prec == IPR_FP16 ? EPI_TSCRATCH : EPI_STORE_T) | (j == c->p ? EPI_RESID : 0);
-    g.tout = (prec == IPR_FP16) ? (void *)c->tscr : c->T[j & 1];
+    if (scaled) { g.sigA = c->dsig + 1 + c->cur; g.sigB = sigX; }
+    g.mode = (scaled ? EPI_TSCRATCH : EPI_STORE_T) | (j == c->p ? EPI_RESID : 0);
+    g.tout = scaled ? (void *)c->tscr : c->T[j & 1];
     g.ldt = c->npad;
     g.part = part;
-    if (prec == IPR_FP16) g.pmax = c->pmax;
+    if (scaled) g.pmax = c->pmax;
     CK(run_gemm(c, g));
-    if (prec == IPR_FP16) {
+    if (scaled) {
       CKS(gather_pmax(c, c->pmax, tn_loc * tm));
-      CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 3 + (j & 1), c->st));
-      CK(launch_scale_fp16(c->tscr, c->kp * c->npad, c->dsig + 3 + (j & 1), c->T[j & 1], c->st));
+      CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 3 + (j & 1), prec, c->st));
+      CK(launch_scale_op(c->tscr, c->kp * c->npad, c->dsig + 3 + (j & 1), prec, c->T[j & 1], c->st));
       sigX = c->dsig + 3 + (j & 1);
     }
     X = c->T[j & 1];
@@ -446,7 +459,7 @@ ipr_status update(ipr_ctx *c) {
   const int tb = ns ? 1 : (c->p & 1);
   GemmArgs g = base_args(c, prec, c->T[tb]);
   chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
-  if (prec == IPR_FP16) { g.sigA = c->dsig + 1 + c->cur; g.sigB = c->dsig + 3 + tb; g.pmax = c->pmax; }
+  if (is_scaled(prec)) { g.sigA = c->dsig + 1 + c->cur; g.sigB = c->dsig + 3 + tb; g.pmax = c->pmax; }
   g.mode = ns ? EPI_NSUPDATE : EPI_UPDATE;
   g.cold = cont_ptr(c, c->cur, P);
   g.cnew = cont_ptr(c, nx, P);
@@ -461,10 +474,10 @@ ipr_status update(ipr_ctx *c) {
   c->upd_timed = true;
   CKS(gather_partials(c, c->part, tn_loc * tm));
   CK(launch_reduce_sum(c->part, tiles_n_total(c, prec) * tm, c->dscal + 1, c->st));
-  if (prec == IPR_FP16) {
+  if (is_scaled(prec)) {
     CKS(gather_pmax(c, c->pmax, tn_loc * tm));
-    CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 1 + nx, c->st));
-    CK(launch_make_operand(c->cont[nx], 0, c->npad * c->kp, IPR_FP16, c->dsig + 1 + nx, chat_slot(c, nx, prec), c->st));
+    CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 1 + nx, prec, c->st));
+    CK(launch_make_operand(c->cont[nx], 0, c->npad * c->kp, prec, c->dsig + 1 + nx, chat_slot(c, nx, prec), c->st));
   }
   CKS(gather_chat(c, nx, prec));
   if (ns) CKS(make_xt(c, nx, P));
@@ -491,14 +504,15 @@ ipr_status update_sym(ipr_ctx *c) {
   CKS(gather_bytes(c, c->wbuf, (size_t)(c->npad * c->kp) * wb, "W"));
   CK(launch_sym_update(cont_ptr(c, c->cur, P), P.cont64, cont_ptr(c, nx, P), c->wbuf, wb == 8, c->npad,
                        c->kp, c->col0, c->p, P.m, P.rtz, P.prec,
-                       P.prec == IPR_FP64 ? nullptr : chat_slot(c, nx, P.prec), P.corr,
+                       (P.prec == IPR_FP64 || is_scaled(P.prec)) ? nullptr : chat_slot(c, nx, P.prec), P.corr,
                        P.corr == P.prec ? nullptr : chatc_slot(c, nx, P.corr), c->part, c->st));
   CK(cudaEventRecord(c->ev[3], c->st));
   c->upd_timed = true;
   const int64_t t64 = c->npad / 64;
   CKS(gather_partials(c, c->part, (c->kp / 64) * t64));
   CK(launch_reduce_sum(c->part, t64 * t64, c->dscal + 1, c->st));
-  CKS(gather_chat(c, nx, P.prec));
+  if (is_scaled(P.prec)) CKS(make_operand(c, nx, P));   // sigma from max|C_{k+1}|, then all-gather
+  else CKS(gather_chat(c, nx, P.prec));
   if (P.corr != P.prec) CKS(gather_bytes(c, c->chatc[nx], (size_t)(c->npad * c->kp) * elt_size(P.corr), "Chat corr"));
   if (c->world > 1) CKS(make_xt(c, nx, P));
   c->cur = nx;
@@ -545,8 +559,8 @@ void free_ctx(ipr_ctx *c) {
 // ipr_iterate): one cudaMalloc / cudaFree per solve, and an OOM is reported before any work.
 ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
   const size_t full = (size_t)(c->npad * c->npad), panel = (size_t)(c->npad * c->kp);
-  bool fp16 = false;
-  for (auto &P : c->ph) fp16 |= P.prec == IPR_FP16;
+  bool fp16 = false;                    // any scaled-format phase: FP32 T scratch
+  for (auto &P : c->ph) fp16 |= is_scaled(P.prec);
   struct Slot { void **p; size_t bytes; };
   const Slot slots[] = {
       {&c->chat[0], full * 8}, {&c->chat[1], full * 8}, {&c->cont[0], panel * 4}, {&c->cont[1], panel * 4},
@@ -600,7 +614,7 @@ extern "C" {
 static ipr_status certify_best(ipr_ctx *c, double *rho);
 static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho);
 
-const char *ipr_version(void) { return "ipr 0.1.0 (sm_100a: tcgen05 BF16/FP16/TF32, DMMA FP64)"; }
+const char *ipr_version(void) { return "ipr 0.2.0 (sm_100a: tcgen05 BF16/FP16/TF32/FP8/INT8, DMMA FP64)"; }
 
 const char *ipr_last_error(const ipr_ctx *c) { return c ? c->err.c_str() : t_err.c_str(); }
 
@@ -688,7 +702,7 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
   int prev_ob = -1, prev_m = -1;
   for (int i = 0; i < nphases; ++i) {
     const ipr_phase &q = phases[i];
-    if (q.prec < IPR_FP64 || q.prec > IPR_FP16) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad prec", i);
+    if (q.prec < IPR_FP64 || q.prec > IPR_INT8) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad prec", i);
     PhaseC P;
     P.prec = q.prec;
     P.cont64 = q.prec == IPR_FP64;
@@ -703,8 +717,8 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
       return fail(c, IPR_E_INVALID_ARG, "phase %d: plateau_ratio needs plateau_arm > 0", i);
     P.switch_tol = q.switch_tol; P.plateau_ratio = q.plateau_ratio; P.plateau_arm = q.plateau_arm;
     P.max_iters = q.max_iters;
-    P.corr = q.corr_prec < 0 ? q.prec : q.corr_prec;
-    if (P.corr < IPR_FP64 || P.corr > IPR_FP16) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad corr_prec", i);
+    P.corr = q.corr_prec >= 0 ? q.corr_prec : is_scaled(q.prec) ? IPR_BF16 : q.prec;
+    if (P.corr < IPR_FP64 || P.corr > IPR_INT8) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad corr_prec", i);
     if (P.corr == IPR_FP64 && P.prec != IPR_FP64)
       return fail(c, IPR_E_INVALID_ARG, "phase %d: an FP64 correction needs an FP64 phase", i);
     const int ob = operand_bits(q.prec);
@@ -751,8 +765,8 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
         return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: the symmetric-tri form is single-GPU (mirror writes cross panels)");
       c->wbytes = 4;
       for (auto &P : c->ph) {
-        if (P.prec == IPR_FP16 || P.corr == IPR_FP16)
-          return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: FP16 phases are not implemented for the symmetric form");
+        if (is_scaled(P.corr))
+          return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: the symmetric form's correction must be BF16, TF32 or FP64");
         if (P.corr != IPR_FP64 && !tc_supported(P.corr))
           return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: tcgen05 path for the correction precision is not built");
         need_c |= P.corr != P.prec;
@@ -940,7 +954,7 @@ int64_t ipr_launch_count(void) { return g_launches; }
 
 ipr_status ipr_plan(int64_t n, int world, int rank, int prec, int64_t *out8) {
   ipr_ctx *c = nullptr;
-  if (n <= 0 || world < 1 || rank < 0 || rank >= world || prec < 0 || prec > 3 || !out8)
+  if (n <= 0 || world < 1 || rank < 0 || rank >= world || prec < 0 || prec > IPR_INT8 || !out8)
     return fail(c, IPR_E_INVALID_ARG, "ipr_plan: bad arguments");
   const int64_t npad = padded_order(n, world), kp = npad / world, col0 = (int64_t)rank * kp;
   const int64_t tm = gemm_tile_m(prec), tn = gemm_tile_n(prec);
@@ -952,7 +966,7 @@ ipr_status ipr_plan(int64_t n, int world, int rank, int prec, int64_t *out8) {
 ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_t len, int m, int round, int sigma,
                              void *stream) {
   ipr_ctx *c = nullptr;
-  if (mode < 0 || mode > 4 || len < 0 || (len > 0 && (!in_dev || !out_dev)))
+  if (mode < 0 || mode > 6 || len < 0 || (len > 0 && (!in_dev || !out_dev)))
     return fail(c, IPR_E_INVALID_ARG, "ipr_test_quantize: bad arguments");
   if ((mode == 0 && (m < 0 || m > 23)) || (mode == 1 && (m < 0 || m > 52)))
     return fail(c, IPR_E_INVALID_ARG, "ipr_test_quantize: bad m");
@@ -964,7 +978,7 @@ ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_
 
 ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_dev, double *Z_dev, void *stream) {
   ipr_ctx *c = nullptr;
-  if (n <= 0 || !X_dev || !Yt_dev || !Z_dev || prec < 0 || prec > 3)
+  if (n <= 0 || !X_dev || !Yt_dev || !Z_dev || prec < 0 || prec > IPR_INT8)
     return fail(c, IPR_E_INVALID_ARG, "ipr_test_gemm: bad arguments");
   if (prec != IPR_FP64 && !tc_supported(prec))
     return fail(c, IPR_E_UNSUPPORTED, "ipr_test_gemm: tcgen05 path for this precision is not built");

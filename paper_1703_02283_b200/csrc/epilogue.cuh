@@ -64,7 +64,7 @@ __device__ __forceinline__ void epi_element(const GemmArgs &g, int64_t row, int6
       cn = (double)f;
     }
     if (g.chat_new) {
-      if (g.prec == P_FP16) acc.mx = fmaxf(acc.mx, fabsf((float)cn));
+      if (is_scaled(g.prec)) acc.mx = fmaxf(acc.mx, fabsf((float)cn));
       else store_operand(g.chat_new, row * g.ldh + col, g.prec, cn, 0);
     }
     const double dd = __dsub_rn(cn, c);
@@ -95,8 +95,8 @@ __device__ __forceinline__ void epi_element(const GemmArgs &g, int64_t row, int6
     }
     if (g.chat_new) {
       const int64_t hi = row * g.ldh + col;
-      if (g.prec == P_FP16) {
-        // FP16 Chat is produced by a separate scale kernel once max|C_{k+1}| is known
+      if (is_scaled(g.prec)) {
+        // a scaled Chat is produced by a separate kernel once max|C_{k+1}| is known
         acc.mx = fmaxf(acc.mx, fabsf((float)cn));
       } else {
         store_operand(g.chat_new, hi, g.prec, cn, 0);

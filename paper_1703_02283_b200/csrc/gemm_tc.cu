@@ -37,7 +37,14 @@ constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
 constexpr int TC_SMEM = TC_ST * TC_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int TC_GROUP_M = 8;         // pair-rows per scheduling group
 
-bool tc_supported(int prec) { return prec == P_BF16 || prec == P_FP16 || prec == P_TF32; }
+bool tc_supported(int prec) {
+  return prec == P_BF16 || prec == P_FP16 || prec == P_TF32 || prec == P_FP8 || prec == P_INT8;
+}
+// tcgen05.mma kind of an operand format: 0 kind::f16 (BF16/FP16), 1 kind::tf32, 2 kind::f8f6f4
+// (E4M3), 3 kind::i8 (signed).  Every kind consumes 32 bytes of K per instruction.
+__host__ __device__ constexpr int tc_kind(int prec) {
+  return prec == P_TF32 ? 1 : prec == P_FP8 ? 2 : prec == P_INT8 ? 3 : 0;
+}
 int gemm_tile_n(int prec) { return prec == P_FP64 ? dmma_tile_n() : TC_BN; }
 int gemm_tile_m(int prec) { return 128; }
 
@@ -122,7 +129,7 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t *bar) {
       : "memory");
 }
 
-template <int KIND>  // 0: kind::f16 (bf16/fp16), 1: kind::tf32
+template <int KIND>  // 0: kind::f16 (bf16/fp16), 1: kind::tf32, 2: kind::f8f6f4, 3: kind::i8
 __device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                             uint32_t acc) {
   if (KIND == 0)
@@ -130,10 +137,20 @@ __device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uin
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
-  else
+  else if (KIND == 1)
     asm volatile(
         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
         "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+  else if (KIND == 2)
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+  else
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
 }
 
@@ -160,10 +177,18 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
   return d;
 }
 
-// Instruction descriptor: FP32 accumulate, K-major A and B, M = 256 (pair), N = 256.
+// Instruction descriptor: K-major A and B, M = 256 (pair), N = 256.  D format (bits 4-5): F32 = 1,
+// S32 = 2 (kind::i8).  A/B formats (bits 7-9 / 10-12): kind::f16 F16 = 0, BF16 = 1; kind::tf32
+// TF32 = 2; kind::f8f6f4 E4M3 = 0; kind::i8 signed = 1.
 __host__ __device__ constexpr uint32_t make_idesc(int prec) {
-  const uint32_t fmt = prec == P_BF16 ? 1u : prec == P_FP16 ? 0u : 2u;   // bf16 / f16 / tf32
-  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)((2 * TC_BM) >> 4) << 24);
+  const uint32_t fmt = prec == P_BF16 ? 1u : prec == P_FP16 ? 0u : prec == P_TF32 ? 2u : prec == P_FP8 ? 0u : 1u;
+  const uint32_t dfmt = prec == P_INT8 ? 2u : 1u;
+  return (dfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)((2 * TC_BM) >> 4) << 24);
+}
+// accumulator word -> FP64 (exact): FP32 bits, or INT32 for kind::i8
+template <int KIND>
+__device__ __forceinline__ double acc_to_f64(uint32_t w) {
+  return KIND == 3 ? (double)(int32_t)w : (double)__uint_as_float(w);
 }
 
 struct TileSched {      // pair tiles: tiles_m pair-rows (256 rows) x tiles_n (256 columns)
@@ -179,13 +204,14 @@ struct TileSched {      // pair tiles: tiles_m pair-rows (256 rows) x tiles_n (2
 };
 
 // One 32-column chunk of one accumulator row: the fused epilogue with vectorised row access.
+template <int KIND>
 __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_t col, const uint32_t (&r)[32],
                                           double scale, EpiAcc &ea) {
   const int mode = g.mode;
   if (mode & (EPI_STORE_T | EPI_TSCRATCH | EPI_RESID | EPI_F64)) {
     #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      const double v = __dmul_rn((double)__uint_as_float(r[j]), scale);
+      const double v = __dmul_rn(acc_to_f64<KIND>(r[j]), scale);
       const int64_t c = col + j;
       if (g.tri && row > g.col0 + c) continue;         // tri: lower triangle comes from the mirror
       const bool mirror = g.tri && row != g.col0 + c;
@@ -218,8 +244,10 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
     float4 *dst = (float4 *)((float *)g.wout + row * g.ldw + col);
     #pragma unroll
     for (int q = 0; q < 8; ++q)
-      dst[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]), __uint_as_float(r[4 * q + 2]),
-                           __uint_as_float(r[4 * q + 3]));
+      dst[q] = make_float4((float)__dmul_rn(acc_to_f64<KIND>(r[4 * q]), scale),
+                           (float)__dmul_rn(acc_to_f64<KIND>(r[4 * q + 1]), scale),
+                           (float)__dmul_rn(acc_to_f64<KIND>(r[4 * q + 2]), scale),
+                           (float)__dmul_rn(acc_to_f64<KIND>(r[4 * q + 3]), scale));
   }
   if (mode & (EPI_UPDATE | EPI_NSUPDATE)) {
     // container row segment [row][col .. col+31]: 128 B (FP32) per thread, 16-byte accesses
@@ -236,7 +264,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
       #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int j = q * 4 + u;
-        const double v = __dmul_rn((double)__uint_as_float(r[j]), scale);
+        const double v = __dmul_rn(acc_to_f64<KIND>(r[j]), scale);
         const double c = (double)cc[u];
         double e = v;
         if (!ns) {
@@ -252,7 +280,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
       }
       dst[q] = make_float4(cn[q * 4], cn[q * 4 + 1], cn[q * 4 + 2], cn[q * 4 + 3]);
     }
-    if (g.chat_new && g.prec != P_FP16) {
+    if (g.chat_new && !is_scaled(g.prec)) {
       if (g.prec == P_TF32) {
         float4 *h = (float4 *)((float *)g.chat_new + row * g.ldh + col);
         #pragma unroll
@@ -392,7 +420,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       for (int ch = hh * 4; ch < hh * 4 + 4; ++ch) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * TC_BN + ch * 32, r);
-        epi_chunk(g, row, colb + ch * 32, r, scale, ea);
+        epi_chunk<KIND>(g, row, colb + ch * 32, r, scale, ea);
       }
       tc_fence_before();
       __syncwarp();
@@ -485,6 +513,7 @@ cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
   const int esz = elt_size(a.prec);
   const CUtensorMapDataType dt = a.prec == P_BF16   ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                  : a.prec == P_FP16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                 : (a.prec == P_FP8 || a.prec == P_INT8) ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                                     : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   const cuuint32_t bke = TC_BKB / esz;
   CUtensorMap ma, mb;
@@ -515,23 +544,23 @@ cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
   const int ntiles = (int)((a.M / (2 * TC_BM)) * (a.N / TC_BN));
   const int maxpairs = num_sms() / 2;
   const int grid = 2 * (ntiles < maxpairs ? ntiles : maxpairs);
-  cudaError_t e;
-  if (a.prec == P_TF32) {
-    static bool attr = false;
-    if (!attr) {
-      e = cudaFuncSetAttribute(k_gemm_tc<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    k_gemm_tc<1><<<grid, TC_NT, TC_SMEM, s>>>(ma, mb, a);
-  } else {
-    static bool attr = false;
-    if (!attr) {
-      e = cudaFuncSetAttribute(k_gemm_tc<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);
-      if (e != cudaSuccess) return e;
-      attr = true;
-    }
-    k_gemm_tc<0><<<grid, TC_NT, TC_SMEM, s>>>(ma, mb, a);
+  cudaError_t e = cudaSuccess;
+  switch (tc_kind(a.prec)) {
+#define TC_LAUNCH(K)                                                                                     \
+    case K: {                                                                                            \
+      static bool attr = false;                                                                          \
+      if (!attr) {                                                                                       \
+        e = cudaFuncSetAttribute(k_gemm_tc<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);     \
+        if (e != cudaSuccess) return e;                                                                  \
+        attr = true;                                                                                     \
+      }                                                                                                  \
+      k_gemm_tc<K><<<grid, TC_NT, TC_SMEM, s>>>(ma, mb, a);                                              \
+    } break;
+    TC_LAUNCH(0)
+    TC_LAUNCH(1)
+    TC_LAUNCH(2)
+    TC_LAUNCH(3)
+#undef TC_LAUNCH
   }
   ++g_launches;
   return cudaGetLastError();

@@ -138,11 +138,11 @@ __global__ void k_make_operand(const void *cont, int cont64, int64_t count, int 
   store_operand(op, t, prec, c, sig ? sig[0] : 0);
 }
 
-// FP16 T scratch (FP32, [kp][npad]) -> scaled FP16 operand
-__global__ void k_scale_fp16(const float *src, int64_t count, const int *sig, __half *dst) {
+// T scratch (FP32, [kp][npad]) -> scaled operand (FP16 / FP8 / INT8) with the exponent sig[0]
+__global__ void k_scale_op(const float *src, int64_t count, const int *sig, int prec, void *dst) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count) return;
-  dst[t] = __float2half_rn((float)__dmul_rn((double)src[t], pow2(sig[0])));
+  store_operand(dst, t, prec, (double)src[t], sig[0]);
 }
 
 __global__ void k_maxabs_cont(const void *cont, int cont64, int64_t count, float *pmax) {
@@ -180,7 +180,7 @@ __global__ void k_reduce_sum(const double *part, int64_t count, double *out) {
   if (threadIdx.x == 0) *out = b;
 }
 // max over float partials -> double out + sigma (FP16 scale) of it
-__global__ void k_reduce_max(const float *part, int64_t count, double *out, int *sig_out) {
+__global__ void k_reduce_max(const float *part, int64_t count, double *out, int *sig_out, int prec) {
   __shared__ float red[32];
   float s = 0.f;
   bool nan = false;
@@ -190,7 +190,7 @@ __global__ void k_reduce_max(const float *part, int64_t count, double *out, int 
   if (threadIdx.x == 0) {
     const double mx = nan ? (double)__int_as_float(0x7fc00000) : (double)b;
     if (out) *out = mx;
-    if (sig_out) *sig_out = fp16_sigma(mx);
+    if (sig_out) *sig_out = op_sigma(prec, mx);
   }
 }
 
@@ -304,6 +304,8 @@ __global__ void k_test_quant(int mode, const void *in, void *out, int64_t len, i
     case 2: { __nv_bfloat16 h = __float2bfloat16_rn(((const float *)in)[t]); ((uint16_t *)out)[t] = *(uint16_t *)&h; } break;
     case 3: ((float *)out)[t] = to_tf32(((const float *)in)[t]); break;
     case 4: { __half h = __float2half_rn((float)__dmul_rn((double)((const float *)in)[t], pow2(sigma))); ((uint16_t *)out)[t] = *(uint16_t *)&h; } break;
+    case 5: ((uint8_t *)out)[t] = to_e4m3(__dmul_rn(((const double *)in)[t], pow2(sigma))); break;   // FP8 E4M3
+    case 6: ((int8_t *)out)[t] = to_int8(__dmul_rn(((const double *)in)[t], pow2(sigma))); break;    // INT8
   }
 }
 
@@ -345,8 +347,8 @@ cudaError_t launch_make_operand(const void *cont, int cont64, int64_t count, int
   k_make_operand<<<nblk(count, 256), 256, 0, s>>>(cont, cont64, count, prec, sig, op);
   LAUNCH_CHECK();
 }
-cudaError_t launch_scale_fp16(const float *src, int64_t count, const int *sig, void *dst, cudaStream_t s) {
-  k_scale_fp16<<<nblk(count, 256), 256, 0, s>>>(src, count, sig, (__half *)dst);
+cudaError_t launch_scale_op(const float *src, int64_t count, const int *sig, int prec, void *dst, cudaStream_t s) {
+  k_scale_op<<<nblk(count, 256), 256, 0, s>>>(src, count, sig, prec, dst);
   LAUNCH_CHECK();
 }
 cudaError_t launch_maxabs_cont(const void *cont, int cont64, int64_t count, float *pmax, int nparts, cudaStream_t s) {
@@ -365,8 +367,8 @@ cudaError_t launch_reduce_sum(const double *part, int64_t count, double *out, cu
   k_reduce_sum<<<1, 512, 0, s>>>(part, count, out);
   LAUNCH_CHECK();
 }
-cudaError_t launch_reduce_max(const float *part, int64_t count, double *out, int *sig, cudaStream_t s) {
-  k_reduce_max<<<1, 512, 0, s>>>(part, count, out, sig);
+cudaError_t launch_reduce_max(const float *part, int64_t count, double *out, int *sig, int prec, cudaStream_t s) {
+  k_reduce_max<<<1, 512, 0, s>>>(part, count, out, sig, prec);
   LAUNCH_CHECK();
 }
 cudaError_t launch_copy_out(const double *src, int64_t npad, int64_t kp, int64_t n, double *dst, int64_t ldc,
@@ -389,7 +391,8 @@ cudaError_t launch_transpose(const void *src, int64_t rows, int64_t cols, int es
   dim3 g(nblk(cols, 32), nblk(rows, 32)), b(32, 8);
   if (esz == 8) k_transpose<double><<<g, b, 0, s>>>((const double *)src, rows, cols, (double *)dst);
   else if (esz == 4) k_transpose<float><<<g, b, 0, s>>>((const float *)src, rows, cols, (float *)dst);
-  else k_transpose<uint16_t><<<g, b, 0, s>>>((const uint16_t *)src, rows, cols, (uint16_t *)dst);
+  else if (esz == 2) k_transpose<uint16_t><<<g, b, 0, s>>>((const uint16_t *)src, rows, cols, (uint16_t *)dst);
+  else k_transpose<uint8_t><<<g, b, 0, s>>>((const uint8_t *)src, rows, cols, (uint8_t *)dst);
   LAUNCH_CHECK();
 }
 

@@ -14,13 +14,13 @@ cudaError_t launch_c0(const double *A, int64_t lda, int64_t n, int64_t npad, int
                       int cont64, int m, int rtz, void *cont, cudaStream_t s);
 cudaError_t launch_make_operand(const void *cont, int cont64, int64_t count, int prec, const int *sig, void *op,
                                 cudaStream_t s);
-cudaError_t launch_scale_fp16(const float *src, int64_t count, const int *sig, void *dst, cudaStream_t s);
+cudaError_t launch_scale_op(const float *src, int64_t count, const int *sig, int prec, void *dst, cudaStream_t s);
 cudaError_t launch_maxabs_cont(const void *cont, int cont64, int64_t count, float *pmax, int nparts, cudaStream_t s);
 cudaError_t launch_cont_to_f64(const void *cont, int cont64, int64_t count, double *dst, cudaStream_t s);
 cudaError_t launch_f64_to_cont(const double *src, int64_t count, int cont64, int m, int rtz, void *cont,
                                cudaStream_t s);
 cudaError_t launch_reduce_sum(const double *part, int64_t count, double *out, cudaStream_t s);
-cudaError_t launch_reduce_max(const float *part, int64_t count, double *out, int *sig, cudaStream_t s);
+cudaError_t launch_reduce_max(const float *part, int64_t count, double *out, int *sig, int prec, cudaStream_t s);
 cudaError_t launch_copy_out(const double *src, int64_t npad, int64_t kp, int64_t n, double *dst, int64_t ldc,
                             cudaStream_t s);
 cudaError_t launch_pad_copy(const void *src, int64_t n, int64_t npad, int esz, void *dst, cudaStream_t s);

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 ipr = pytest.importorskip("paper_1703_02283_b200")
 
-OPR = {"fp64": oracle.FP64, "tf32": oracle.TF32, "bf16": oracle.BF16}
+OPR = {"fp64": oracle.FP64, "tf32": oracle.TF32, "bf16": oracle.BF16, "fp16": oracle.FP16}
 LOW = dict(switch_tol=0.0, plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
 
 
@@ -48,7 +48,8 @@ def run_sym(A, p, name, tol, iters, form="symmetric"):
                                          (2, "fp64/cbf16", "symmetric"), (2, "bf16>fp64", "symmetric"),
                                          (2, "tf32>fp64/cbf16", "symmetric"), (3, "bf16>fp64/ctf32", "symmetric"),
                                          (2, "bf16/ctf32>fp64", "symmetric"), (2, "fp64", "symmetric_tri"),
-                                         (2, "bf16>fp64/cbf16", "symmetric_tri"), (2, "tf32>fp64", "symmetric_tri")])
+                                         (2, "bf16>fp64/cbf16", "symmetric_tri"), (2, "tf32>fp64", "symmetric_tri"),
+                                         (2, "fp16>fp64/cbf16", "symmetric_tri"), (3, "fp16/ctf32>fp64", "symmetric")])
 def test_diagonal_bit_exact(p, name, form):
     A = synth.diag_spd(200, 1e3, 9)
     r, (out, tr, hist, best) = run_sym(A, p, name, 1e-13, 120, form)
@@ -80,7 +81,7 @@ def test_fp64_twin_trajectory(n, p, form):
 
 @pytest.mark.parametrize("name,m,form", [("bf16>fp64/cbf16", 7, "symmetric"), ("tf32>fp64/cbf16", 10, "symmetric"),
                                          ("bf16>fp64", 7, "symmetric"), ("bf16>tf32>fp64/cbf16", 7, "symmetric"),
-                                         ("bf16>fp64/cbf16", 7, "symmetric_tri"),
+                                         ("bf16>fp64/cbf16", 7, "symmetric_tri"), ("fp16>fp64/cbf16", 10, "symmetric_tri"),
                                          ("bf16>tf32>fp64/cbf16", 7, "symmetric_tri")])
 def test_mixed_level2(name, m, form):
     # Level 2: low-phase iterates within 4 * 2^-m of the oracle, the same switch
@@ -137,8 +138,9 @@ def test_errors():
         s.iterate(1)
     assert e.value.status == ipr.IPR_E_INVALID_ARG
     s.close()
-    s = ipr.Solver(A, 2, [ipr.make_phase("fp16", max_iters=3), ipr.make_phase("fp64")], 1e-12, form="symmetric")
-    with pytest.raises(ipr.IprError) as e:
+    s = ipr.Solver(A, 2, [ipr.make_phase("fp16", max_iters=3, corr_prec="fp8"), ipr.make_phase("fp64")], 1e-12,
+                   form="symmetric")
+    with pytest.raises(ipr.IprError) as e:   # a scaled correction format is not defined
         s.iterate(1)
     assert e.value.status == ipr.IPR_E_UNSUPPORTED
     s.close()

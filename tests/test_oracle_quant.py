@@ -131,3 +131,46 @@ def test_fp16_sigma():
     for mx in [1e-9, 3e-5, 0.7, 123.0, 4e7]:
         s = oracle.fp16_sigma(mx)
         assert 2.0 ** 14 <= mx * 2.0 ** s < 2.0 ** 15
+
+
+# ---- NEXT-3: FP8 (E4M3) and INT8 fixed-point operand formats ---------------------------------
+def test_fp8_e4m3_grid_matches_torch_float8():
+    torch = pytest.importorskip("torch")
+    # every finite E4M3fn value below 2^7 is a fixed point of q_m(E=4, m=3) (the scaled operand range)
+    allv = torch.arange(256, dtype=torch.uint8).view(torch.float8_e4m3fn).to(torch.float64).numpy()
+    fin = allv[np.isfinite(allv) & (np.abs(allv) < 128)]
+    assert fin.size > 200
+    np.testing.assert_array_equal(oracle.qm(fin, 4, 3), fin)
+    # RNE from float32 inputs (exact in float64, so torch's float -> fp8 path is one rounding)
+    rng = np.random.default_rng(0)
+    x = (rng.standard_normal(200_000) * np.exp(rng.uniform(-12, 4, 200_000))).astype(np.float32)
+    x = x[np.abs(x) < 127]
+    ref = torch.from_numpy(x).to(torch.float8_e4m3fn).to(torch.float64).numpy()
+    np.testing.assert_array_equal(oracle.qm(x.astype(np.float64), 4, 3), ref)
+
+
+def test_scaled_format_sigmas():
+    for prec in (oracle.FP8, oracle.INT8):
+        for mx in (1e-5, 0.3, 1.0, 1.999, 77.0):
+            s = oracle.sigma(prec, mx)
+            assert 64 <= mx * 2.0 ** s < 128
+    assert oracle.sigma(oracle.BF16, 3.0) == 0 and oracle.sigma(oracle.FP8, 0.0) == 0
+
+
+def test_int8_fixed_point_quantiser():
+    assert [oracle.q_int8(v) for v in (2.5, 3.5, -2.5, 0.49, 126.6, 127.5, 300.0, -500.0)] == \
+        [2.0, 4.0, -2.0, 0.0, 127.0, 127.0, 127.0, -127.0]
+
+
+@pytest.mark.parametrize("prec", [oracle.FP8, oracle.INT8])
+def test_scaled_step_close_to_fp64(prec):
+    import synth
+    A = synth.spd(64, 2.0, 0)
+    C0 = oracle.c0(A, np.prod(oracle.norms(A)[:2]), oracle.phase())
+    _, c64, _ = oracle.step(A, C0, 2, oracle.phase())
+    _, c8, _ = oracle.step(A, C0, 2, oracle.phase(prec))
+    # operand rounding 2^-4 (FP8) / fixed point with 7 bits below the max (INT8), stored m bits
+    assert np.linalg.norm(c8 - c64) / np.linalg.norm(c64) < 0.2
+    _, s8, _ = oracle.step_sym(A, C0, 2, oracle.phase(prec))
+    _, s64, _ = oracle.step_sym(A, C0, 2, oracle.phase())
+    assert np.linalg.norm(s8 - s64) / np.linalg.norm(s64) < 0.2

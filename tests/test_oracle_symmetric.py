@@ -154,12 +154,17 @@ def test_stable_at_kappa_10_where_literal_diverges():
     assert sym.outcome == oracle.CONVERGED
 
 
-def test_rejects_p1_and_fp16():
+def test_rejects_p1_and_scaled_correction():
     with pytest.raises(ValueError):
         oracle.solve(np.eye(4), 1, [oracle.phase()], form=SYM)
-    with pytest.raises(ValueError):
-        oracle.solve(np.eye(4), 2, [oracle.phase(oracle.FP16), oracle.phase()], form=SYM)
+    with pytest.raises(ValueError):   # the correction format must be BF16 / TF32 / FP64
+        oracle.solve(np.eye(4), 2, [oracle.phase(oracle.FP16, corr_prec=oracle.FP16), oracle.phase()], form=SYM)
     assert np.isnan(oracle.step_sym(np.eye(2), np.eye(2), 1, oracle.phase())[0])
+    # scaled phases default to a BF16 correction and converge (FP16 -> FP64)
+    A = synth.spd(64, 2.0, 0)
+    r = oracle.solve(A, 2, [oracle.phase(oracle.FP16, plateau_ratio=0.7, plateau_arm=0.5, max_iters=40),
+                            oracle.phase()], 1e-12, 100, form=SYM)
+    assert r.outcome == oracle.CONVERGED
 
 
 def test_tri_variant_mirrors_upper_triangle():
