@@ -32,7 +32,8 @@ METRIC = "time-to-FP64-residual 1e-12 (n=8192, p=2)"
 # in the symmetrised-correction form with the upper-triangle GEMM 2 (NEXT-2 (i)+(iii), R-22)
 DEFAULT_SCHEDULE = "symtri:bf16>fp64/cbf16"
 EXTRA_SCHEDULES = ["fp64", "bf16>fp64", "tf32>fp64", "fp16>fp64", "sym:fp64", "sym:fp64/cbf16", "symtri:fp64/cbf16",
-                   "symtri:bf16>fp64/cbf16", "symtri:bf16>tf32>fp64/cbf16",
+                   "symtri:bf16>fp64/cbf16", "symtri:bf16>tf32>fp64/cbf16", "symtri:fp8>bf16>fp64/cbf16",
+                   "symtri:int8>bf16>fp64/cbf16", "symtri:fp16>fp64/cbf16",
                    "sym:bf16>fp64", "sym:tf32>fp64/cbf16", "sym:bf16>tf32>fp64/cbf16"]
 FP64_PEAK_TFLOPS = 37.1   # measured DMMA issue peak on this pool (profiles/r01_calibration.md)
 FP64_PEAK_SRC = "measured DMMA.8x8x4 issue peak, tools/probes/dmma_rate.cu (MEASURED_PEAKS.json has no FP64 figure)"
@@ -82,6 +83,24 @@ def schedule(name, n):
             out.append(ipr.make_phase(prec, switch_tol=sw, plateau_ratio=0.7, plateau_arm=0.5,
                                       max_iters=40, corr_prec=corr))
     return form, out
+
+
+def gemm_peaks():
+    """Dense tensor peak per operand format: MEASURED_PEAKS.json's bf16 burst (driver-written),
+    other formats by the guide's nominal ratios (tf32 = 1/2, fp8 = int8 = 2 x bf16); FP64 = the
+    measured DMMA issue peak."""
+    bf16 = 1599.0
+    src = "fallback 1599 (no MEASURED_PEAKS.json)"
+    mp = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(mp):
+        try:
+            bf16 = float(json.load(open(mp))["bf16_tflops"])
+            src = "MEASURED_PEAKS.json bf16_tflops (burst)"
+        except Exception:
+            pass
+    return {"fp64": (FP64_PEAK_TFLOPS, FP64_PEAK_SRC), "bf16": (bf16, src), "fp16": (bf16, src + " (fp16 = bf16 rate)"),
+            "tf32": (bf16 / 2, src + " x 1/2 (nominal tf32:bf16)"), "fp8": (bf16 * 2, src + " x 2 (nominal fp8:bf16)"),
+            "int8": (bf16 * 2, src + " x 2 (nominal int8:bf16)")}
 
 
 def gemm_count(trace, p):
@@ -339,15 +358,18 @@ def main():
                            "final_rho": c2[-1] if c2 else t2[-1]["rho"],
                            "gemm_tflops_low": (lg * 2.0 * n ** 3 / (lms * 1e-3) / 1e12) if lms > 0 else None}
         extras["schedules"] = sched
-        extras["gemm_tflops"] = {"fp64": achieved,
-                                 "bf16": sched["bf16>fp64"]["gemm_tflops_low"],
-                                 "tf32": sched["tf32>fp64"]["gemm_tflops_low"],
-                                 "fp16": sched["fp16>fp64"]["gemm_tflops_low"]}
-        extras["gemm_frac_of_peak"] = {
-            "fp64": achieved / FP64_PEAK_TFLOPS if achieved else None,
-            "bf16_vs_measured_bf16_burst_1599": (extras["gemm_tflops"]["bf16"] or 0) / 1599.0,
-            "fp16_vs_measured_bf16_burst_1599": (extras["gemm_tflops"]["fp16"] or 0) / 1599.0,
-            "tf32_vs_half_of_1599": (extras["gemm_tflops"]["tf32"] or 0) / (1599.0 / 2)}
+        # the other half of the metric: the hot-path GEMM kernel of every format, timed alone
+        # (ipr_bench_gemm: CUDA events, EPI_STORE_T epilogue, 2 n^3 flop per launch), against the
+        # peak of its own dtype (burst figure: a kernel timed alone)
+        peaks = gemm_peaks()
+        rates, fracs = {}, {}
+        for prec in ["fp64", "tf32", "bf16", "fp16", "fp8", "int8"]:
+            gms = ipr.ipr_bench_gemm(prec, n, 2, 5, stream)
+            rates[prec] = 2.0 * n ** 3 / (gms * 1e-3) / 1e12
+            fracs[prec] = rates[prec] / peaks[prec][0]
+        extras["gemm_tflops"] = rates
+        extras["gemm_frac_of_peak"] = fracs
+        extras["gemm_peaks"] = {k: {"tflops": v[0], "source": v[1]} for k, v in peaks.items()}
 
     if rank != 0:
         return

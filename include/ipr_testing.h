@@ -37,6 +37,14 @@ ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_
 ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_dev,
                          double *Z_dev, void *stream);
 
+/* Throughput probe of the hot-path GEMM kernel of a format (measurement): allocates
+ * two n x n operands (n rounded up to the tile: 256 tcgen05 / 128 DMMA) filled with pseudo-random
+ * values on the format's grid, runs `warmup` untimed then `iters` timed launches of the chain GEMM
+ * (epilogue EPI_STORE_T: qin(D) stored K-major, exactly as in the hot path) on `stream`, and
+ * writes the average device time per launch (CUDA events on `stream`) to *ms.  2 n^3 flop per
+ * launch.  Frees everything before returning. */
+ipr_status ipr_bench_gemm(int prec, int64_t n, int warmup, int iters, void *stream, double *ms);
+
 /* Host-side plan of the 1 x world column-panel decomposition; needs no GPU.
  * out8 = {npad (padded order), kp (columns per rank), col0 (first global column of `rank`),
  *         tile_m, tile_n (output tile of the GEMM kernel used for prec), tiles_m,

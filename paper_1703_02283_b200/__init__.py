@@ -32,7 +32,7 @@ OUTCOME_NAMES = {0: "running", 1: "converged", 2: "iter_limit", 3: "diverged", 4
 EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_get_trace",
             "ipr_get_iterate", "ipr_get_norms", "ipr_finalize", "ipr_last_error",
             "ipr_nccl_unique_id", "ipr_version", "ipr_test_quantize", "ipr_test_gemm",
-            "ipr_launch_count", "ipr_plan", "ipr_set_form"]
+            "ipr_launch_count", "ipr_plan", "ipr_set_form", "ipr_bench_gemm"]
 IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ, IPR_FORM_SYMMETRIC, IPR_FORM_SYMMETRIC_TRI = 0, 1, 2, 3
 FORM_BY_NAME = {"literal": IPR_FORM_LITERAL, "newton_schulz": IPR_FORM_NEWTON_SCHULZ, "ns": IPR_FORM_NEWTON_SCHULZ,
                 "symmetric": IPR_FORM_SYMMETRIC, "sym": IPR_FORM_SYMMETRIC,
@@ -81,6 +81,7 @@ def _load():
     L.ipr_launch_count.restype = C.c_int64
     L.ipr_plan.argtypes = [i64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)]
     L.ipr_set_form.argtypes = [vp, C.c_int]
+    L.ipr_bench_gemm.argtypes = [C.c_int, i64, C.c_int, C.c_int, vp, dp]
     for f in EXPORTED:
         if f not in ("ipr_last_error", "ipr_version", "ipr_launch_count"):
             getattr(L, f).restype = C.c_int
@@ -204,6 +205,14 @@ def ipr_test_quantize(mode: int, x_in, x_out, m: int = 0, round: int = IPR_RNE, 
 
 def ipr_test_gemm(prec: int, n: int, X, Yt, Z, stream=None):
     _check(_lib.ipr_test_gemm(prec, n, _ptr(X), _ptr(Yt), _ptr(Z), _stream(stream)))
+
+
+def ipr_bench_gemm(prec, n: int, warmup: int = 2, iters: int = 5, stream=None) -> float:
+    """Average device ms of the hot-path GEMM kernel of a format at order n (2 n^3 flop)."""
+    pr = PREC_BY_NAME[prec] if isinstance(prec, str) else int(prec)
+    ms = C.c_double(0)
+    _check(_lib.ipr_bench_gemm(pr, n, warmup, iters, _stream(stream), C.byref(ms)))
+    return ms.value
 
 
 def ipr_launch_count() -> int:

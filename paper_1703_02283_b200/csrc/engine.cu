@@ -1007,4 +1007,45 @@ ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_
   return IPR_OK;
 }
 
+ipr_status ipr_bench_gemm(int prec, int64_t n, int warmup, int iters, void *stream, double *ms) {
+  ipr_ctx *c = nullptr;
+  if (n <= 0 || prec < 0 || prec > IPR_INT8 || warmup < 0 || iters <= 0 || !ms)
+    return fail(c, IPR_E_INVALID_ARG, "ipr_bench_gemm: bad arguments");
+  if (prec != IPR_FP64 && !tc_supported(prec))
+    return fail(c, IPR_E_UNSUPPORTED, "ipr_bench_gemm: tcgen05 path for this precision is not built");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t unit = prec == IPR_FP64 ? 128 : 256;
+  const int64_t np = (n + unit - 1) / unit * unit;
+  const size_t bytes = (size_t)(np * np) * elt_size(prec);
+  void *X = nullptr, *Y = nullptr, *T = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  cudaError_t e = cudaMalloc(&X, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&Y, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&T, bytes);
+  if (e == cudaSuccess) e = cudaEventCreate(&e0);
+  if (e == cudaSuccess) e = cudaEventCreate(&e1);
+  if (e == cudaSuccess) e = launch_fill_operand(X, np * np, prec, 0x1234u, s);
+  if (e == cudaSuccess) e = launch_fill_operand(Y, np * np, prec, 0x9876u, s);
+  GemmArgs g;
+  memset(&g, 0, sizeof g);
+  g.M = np; g.N = np; g.K = np; g.n = n; g.col0 = 0;
+  g.A = X; g.a_kp = np; g.a_pstride = np * np;
+  g.B = Y; g.ldb = np; g.prec = prec; g.tprec = prec; g.mode = EPI_STORE_T;
+  g.tout = T; g.ldt = np; g.tiles_m = np / gemm_tile_m(prec);
+  auto run = [&]() { return prec == IPR_FP64 ? launch_gemm_dmma(g, s) : launch_gemm_tc(g, s); };
+  for (int i = 0; i < warmup && e == cudaSuccess; ++i) e = run();
+  if (e == cudaSuccess) e = cudaEventRecord(e0, s);
+  for (int i = 0; i < iters && e == cudaSuccess; ++i) e = run();
+  if (e == cudaSuccess) e = cudaEventRecord(e1, s);
+  if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+  float t = 0.f;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&t, e0, e1);
+  if (e == cudaSuccess) *ms = (double)t / iters;
+  cudaFree(X); cudaFree(Y); cudaFree(T);
+  if (e0) cudaEventDestroy(e0);
+  if (e1) cudaEventDestroy(e1);
+  if (e != cudaSuccess) return fail(c, IPR_E_CUDA, "ipr_bench_gemm: %s %s", cudaGetErrorString(e), tc_last_error());
+  return IPR_OK;
+}
+
 }  // extern "C"

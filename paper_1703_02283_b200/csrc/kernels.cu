@@ -294,6 +294,17 @@ __global__ void __launch_bounds__(256) k_sym_update(const CT *__restrict__ cold,
   if (threadIdx.x == 0) part[((col0 + jb) / 64) * (npad / 64) + blockIdx.y] = b;
 }
 
+// measurement hook: operand filled with pseudo-random values on the format's grid (|v| < 1;
+// INT8 integers in [-100, 100])
+__global__ void k_fill_operand(void *dst, int64_t count, int prec, uint32_t seed) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  uint32_t h = (uint32_t)t * 2654435761u ^ seed;
+  h ^= h >> 15; h *= 2246822519u; h ^= h >> 13; h *= 3266489917u; h ^= h >> 16;
+  const double v = (double)(h & 0xffff) / 32768.0 - 1.0;
+  store_operand(dst, t, prec, prec == P_INT8 ? v * 100.0 : v, 0);
+}
+
 // test hook: quantisers
 __global__ void k_test_quant(int mode, const void *in, void *out, int64_t len, int m, int rtz, int sigma) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -411,6 +422,10 @@ cudaError_t launch_sym_update(const void *cold, int cont64, void *cnew, const vo
   LAUNCH_CHECK();
 }
 
+cudaError_t launch_fill_operand(void *dst, int64_t count, int prec, uint32_t seed, cudaStream_t s) {
+  k_fill_operand<<<nblk(count, 256), 256, 0, s>>>(dst, count, prec, seed);
+  LAUNCH_CHECK();
+}
 cudaError_t launch_test_quant(int mode, const void *in, void *out, int64_t len, int m, int rtz, int sigma,
                               cudaStream_t s) {
   if (len <= 0) return cudaSuccess;
