@@ -40,7 +40,8 @@ ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_
 /* Throughput probe of the hot-path GEMM kernel of a format (measurement): allocates
  * two n x n operands (n rounded up to the tile: 256 tcgen05 / 128 DMMA) filled with pseudo-random
  * values on the format's grid, runs `warmup` untimed then `iters` timed launches of the chain GEMM
- * (epilogue EPI_STORE_T: qin(D) stored K-major, exactly as in the hot path) on `stream`, and
+ * with the hot path's epilogue (qin(D) stored K-major; for the scaled FP16/FP8/INT8 formats the
+ * FP32 scratch + per-tile max that precedes the operand scaling) on `stream`, and
  * writes the average device time per launch (CUDA events on `stream`) to *ms.  2 n^3 flop per
  * launch.  Frees everything before returning. */
 ipr_status ipr_bench_gemm(int prec, int64_t n, int warmup, int iters, void *stream, double *ms);

@@ -1018,10 +1018,14 @@ ipr_status ipr_bench_gemm(int prec, int64_t n, int warmup, int iters, void *stre
   const int64_t np = (n + unit - 1) / unit * unit;
   const size_t bytes = (size_t)(np * np) * elt_size(prec);
   void *X = nullptr, *Y = nullptr, *T = nullptr;
+  float *pm = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
+  // scaled formats: the chain GEMM's epilogue is the FP32 scratch + per-tile max (EPI_TSCRATCH)
+  const bool scaled = is_scaled(prec);
   cudaError_t e = cudaMalloc(&X, bytes);
   if (e == cudaSuccess) e = cudaMalloc(&Y, bytes);
-  if (e == cudaSuccess) e = cudaMalloc(&T, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&T, scaled ? (size_t)(np * np) * 4 : bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&pm, (size_t)(np / 128) * (np / 64) * 4 + 4096);
   if (e == cudaSuccess) e = cudaEventCreate(&e0);
   if (e == cudaSuccess) e = cudaEventCreate(&e1);
   if (e == cudaSuccess) e = launch_fill_operand(X, np * np, prec, 0x1234u, s);
@@ -1030,8 +1034,9 @@ ipr_status ipr_bench_gemm(int prec, int64_t n, int warmup, int iters, void *stre
   memset(&g, 0, sizeof g);
   g.M = np; g.N = np; g.K = np; g.n = n; g.col0 = 0;
   g.A = X; g.a_kp = np; g.a_pstride = np * np;
-  g.B = Y; g.ldb = np; g.prec = prec; g.tprec = prec; g.mode = EPI_STORE_T;
+  g.B = Y; g.ldb = np; g.prec = prec; g.tprec = prec; g.mode = scaled ? EPI_TSCRATCH : EPI_STORE_T;
   g.tout = T; g.ldt = np; g.tiles_m = np / gemm_tile_m(prec);
+  if (scaled) g.pmax = pm;
   auto run = [&]() { return prec == IPR_FP64 ? launch_gemm_dmma(g, s) : launch_gemm_tc(g, s); };
   for (int i = 0; i < warmup && e == cudaSuccess; ++i) e = run();
   if (e == cudaSuccess) e = cudaEventRecord(e0, s);
@@ -1041,7 +1046,7 @@ ipr_status ipr_bench_gemm(int prec, int64_t n, int warmup, int iters, void *stre
   float t = 0.f;
   if (e == cudaSuccess) e = cudaEventElapsedTime(&t, e0, e1);
   if (e == cudaSuccess) *ms = (double)t / iters;
-  cudaFree(X); cudaFree(Y); cudaFree(T);
+  cudaFree(X); cudaFree(Y); cudaFree(T); cudaFree(pm);
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
   if (e != cudaSuccess) return fail(c, IPR_E_CUDA, "ipr_bench_gemm: %s %s", cudaGetErrorString(e), tc_last_error());
