@@ -45,6 +45,9 @@ ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_
  * writes the average device time per launch (CUDA events on `stream`) to *ms.  2 n^3 flop per
  * launch.  Frees everything before returning. */
 ipr_status ipr_bench_gemm(int prec, int64_t n, int warmup, int iters, void *stream, double *ms);
+/* Same with an explicit epilogue mode (diagnostics): epi = 0 the hot-path default above,
+ * 1 none (accumulators read from TMEM / registers and dropped), 2 EPI_STORE_T, 3 EPI_TSCRATCH. */
+ipr_status ipr_bench_gemm_epi(int prec, int64_t n, int warmup, int iters, int epi, void *stream, double *ms);
 
 /* Host-side plan of the 1 x world column-panel decomposition; needs no GPU.
  * out8 = {npad (padded order), kp (columns per rank), col0 (first global column of `rank`),

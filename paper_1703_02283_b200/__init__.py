@@ -32,7 +32,7 @@ OUTCOME_NAMES = {0: "running", 1: "converged", 2: "iter_limit", 3: "diverged", 4
 EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_get_trace",
             "ipr_get_iterate", "ipr_get_norms", "ipr_finalize", "ipr_last_error",
             "ipr_nccl_unique_id", "ipr_version", "ipr_test_quantize", "ipr_test_gemm",
-            "ipr_launch_count", "ipr_plan", "ipr_set_form", "ipr_bench_gemm"]
+            "ipr_launch_count", "ipr_plan", "ipr_set_form", "ipr_bench_gemm", "ipr_bench_gemm_epi"]
 IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ, IPR_FORM_SYMMETRIC, IPR_FORM_SYMMETRIC_TRI = 0, 1, 2, 3
 FORM_BY_NAME = {"literal": IPR_FORM_LITERAL, "newton_schulz": IPR_FORM_NEWTON_SCHULZ, "ns": IPR_FORM_NEWTON_SCHULZ,
                 "symmetric": IPR_FORM_SYMMETRIC, "sym": IPR_FORM_SYMMETRIC,
@@ -82,6 +82,7 @@ def _load():
     L.ipr_plan.argtypes = [i64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)]
     L.ipr_set_form.argtypes = [vp, C.c_int]
     L.ipr_bench_gemm.argtypes = [C.c_int, i64, C.c_int, C.c_int, vp, dp]
+    L.ipr_bench_gemm_epi.argtypes = [C.c_int, i64, C.c_int, C.c_int, C.c_int, vp, dp]
     for f in EXPORTED:
         if f not in ("ipr_last_error", "ipr_version", "ipr_launch_count"):
             getattr(L, f).restype = C.c_int
@@ -212,6 +213,14 @@ def ipr_bench_gemm(prec, n: int, warmup: int = 2, iters: int = 5, stream=None) -
     pr = PREC_BY_NAME[prec] if isinstance(prec, str) else int(prec)
     ms = C.c_double(0)
     _check(_lib.ipr_bench_gemm(pr, n, warmup, iters, _stream(stream), C.byref(ms)))
+    return ms.value
+
+
+def ipr_bench_gemm_epi(prec, n: int, warmup: int = 2, iters: int = 5, epi: int = 0, stream=None) -> float:
+    """ipr_bench_gemm with an explicit epilogue (0 default, 1 none, 2 STORE_T, 3 TSCRATCH)."""
+    pr = PREC_BY_NAME[prec] if isinstance(prec, str) else int(prec)
+    ms = C.c_double(0)
+    _check(_lib.ipr_bench_gemm_epi(pr, n, warmup, iters, epi, _stream(stream), C.byref(ms)))
     return ms.value
 
 

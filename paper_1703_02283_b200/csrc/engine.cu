@@ -1008,8 +1008,12 @@ ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_
 }
 
 ipr_status ipr_bench_gemm(int prec, int64_t n, int warmup, int iters, void *stream, double *ms) {
+  return ipr_bench_gemm_epi(prec, n, warmup, iters, 0, stream, ms);
+}
+
+ipr_status ipr_bench_gemm_epi(int prec, int64_t n, int warmup, int iters, int epi, void *stream, double *ms) {
   ipr_ctx *c = nullptr;
-  if (n <= 0 || prec < 0 || prec > IPR_INT8 || warmup < 0 || iters <= 0 || !ms)
+  if (n <= 0 || prec < 0 || prec > IPR_INT8 || warmup < 0 || iters <= 0 || !ms || epi < 0 || epi > 3)
     return fail(c, IPR_E_INVALID_ARG, "ipr_bench_gemm: bad arguments");
   if (prec != IPR_FP64 && !tc_supported(prec))
     return fail(c, IPR_E_UNSUPPORTED, "ipr_bench_gemm: tcgen05 path for this precision is not built");
@@ -1024,7 +1028,7 @@ ipr_status ipr_bench_gemm(int prec, int64_t n, int warmup, int iters, void *stre
   const bool scaled = is_scaled(prec);
   cudaError_t e = cudaMalloc(&X, bytes);
   if (e == cudaSuccess) e = cudaMalloc(&Y, bytes);
-  if (e == cudaSuccess) e = cudaMalloc(&T, scaled ? (size_t)(np * np) * 4 : bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&T, (size_t)(np * np) * 8);
   if (e == cudaSuccess) e = cudaMalloc(&pm, (size_t)(np / 128) * (np / 64) * 4 + 4096);
   if (e == cudaSuccess) e = cudaEventCreate(&e0);
   if (e == cudaSuccess) e = cudaEventCreate(&e1);
@@ -1034,9 +1038,10 @@ ipr_status ipr_bench_gemm(int prec, int64_t n, int warmup, int iters, void *stre
   memset(&g, 0, sizeof g);
   g.M = np; g.N = np; g.K = np; g.n = n; g.col0 = 0;
   g.A = X; g.a_kp = np; g.a_pstride = np * np;
-  g.B = Y; g.ldb = np; g.prec = prec; g.tprec = prec; g.mode = scaled ? EPI_TSCRATCH : EPI_STORE_T;
+  const int mode = epi == 1 ? 0 : epi == 2 ? EPI_STORE_T : epi == 3 ? EPI_TSCRATCH : scaled ? EPI_TSCRATCH : EPI_STORE_T;
+  g.B = Y; g.ldb = np; g.prec = prec; g.tprec = prec; g.mode = mode;
   g.tout = T; g.ldt = np; g.tiles_m = np / gemm_tile_m(prec);
-  if (scaled) g.pmax = pm;
+  if (mode == EPI_TSCRATCH) g.pmax = pm;
   auto run = [&]() { return prec == IPR_FP64 ? launch_gemm_dmma(g, s) : launch_gemm_tc(g, s); };
   for (int i = 0; i < warmup && e == cudaSuccess; ++i) e = run();
   if (e == cudaSuccess) e = cudaEventRecord(e0, s);

@@ -208,10 +208,40 @@ template <int KIND>
 __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_t col, const uint32_t (&r)[32],
                                           double scale, EpiAcc &ea) {
   const int mode = g.mode;
+  // ---- FP32 fast paths (no FP64 arithmetic; results identical to the general path below) ----
+  // (a) plain chain store: qin(D) of an unscaled accumulator -- BF16 / TF32 are one RNE rounding
+  //     of the FP32 value, exactly what the FP64 detour produced ((float)(double)f == f)
+  if (mode == EPI_STORE_T && scale == 1.0 && !g.tri && KIND <= 1 && (g.tprec == P_BF16 || g.tprec == P_TF32)) {
+    if (g.tprec == P_BF16) {
+      __nv_bfloat16 *t = (__nv_bfloat16 *)g.tout + col * g.ldt + row;
+      #pragma unroll
+      for (int j = 0; j < 32; ++j) t[j * g.ldt] = __float2bfloat16_rn(__uint_as_float(r[j]));
+    } else {
+      float *t = (float *)g.tout + col * g.ldt + row;
+      #pragma unroll
+      for (int j = 0; j < 32; ++j) t[j * g.ldt] = to_tf32(__uint_as_float(r[j]));
+    }
+    return;
+  }
+  // (b) FP32 scratch of a scaled format: the scale is an exact power of two, so one FP32
+  //     multiply gives the same float as (float)(acc * scale) in FP64 (one rounding for INT32)
+  if (mode == EPI_TSCRATCH) {
+    const float sf = (float)scale;
+    float *t = (float *)g.tout + col * g.ldt + row;
+    #pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float a = KIND == 3 ? (float)(int32_t)r[j] : __uint_as_float(r[j]);
+      const float w = __fmul_rn(a, sf);
+      t[j * g.ldt] = w;
+      ea.mx = fmaxf(ea.mx, fabsf(w));
+    }
+    return;
+  }
   if (mode & (EPI_STORE_T | EPI_TSCRATCH | EPI_RESID | EPI_F64)) {
     #pragma unroll
     for (int j = 0; j < 32; ++j) {
-      const double v = __dmul_rn(acc_to_f64<KIND>(r[j]), scale);
+      const double a = acc_to_f64<KIND>(r[j]);
+      const double v = scale == 1.0 ? a : __dmul_rn(a, scale);
       const int64_t c = col + j;
       if (g.tri && row > g.col0 + c) continue;         // tri: lower triangle comes from the mirror
       const bool mirror = g.tri && row != g.col0 + c;
@@ -241,13 +271,19 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
   if (mode & EPI_WSTORE) {
     // symmetric form: W row segment [row][col .. col+31] as the exact FP32 accumulator values
     // (scale is 1: no FP16 operands in this form), 16-byte stores
+    // (the correction format is unscaled BF16/TF32, so scale == 1: raw FP32 accumulators)
     float4 *dst = (float4 *)((float *)g.wout + row * g.ldw + col);
+    const float sf = (float)scale;
     #pragma unroll
-    for (int q = 0; q < 8; ++q)
-      dst[q] = make_float4((float)__dmul_rn(acc_to_f64<KIND>(r[4 * q]), scale),
-                           (float)__dmul_rn(acc_to_f64<KIND>(r[4 * q + 1]), scale),
-                           (float)__dmul_rn(acc_to_f64<KIND>(r[4 * q + 2]), scale),
-                           (float)__dmul_rn(acc_to_f64<KIND>(r[4 * q + 3]), scale));
+    for (int q = 0; q < 8; ++q) {
+      float w[4];
+      #pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float a = KIND == 3 ? (float)(int32_t)r[4 * q + u] : __uint_as_float(r[4 * q + u]);
+        w[u] = __fmul_rn(a, sf);
+      }
+      dst[q] = make_float4(w[0], w[1], w[2], w[3]);
+    }
   }
   if (mode & (EPI_UPDATE | EPI_NSUPDATE)) {
     // container row segment [row][col .. col+31]: 128 B (FP32) per thread, 16-byte accesses

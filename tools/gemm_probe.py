@@ -8,6 +8,8 @@ import paper_1703_02283_b200 as ipr
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
 precs = sys.argv[2].split(",") if len(sys.argv) > 2 else ["bf16", "fp16", "tf32", "fp8", "int8", "fp64"]
+epis = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [0]
 for prec in precs:
-    ms = ipr.ipr_bench_gemm(prec, n, 2, 10)
-    print(f"n={n} {prec}: {ms:.3f} ms  {2.0 * n ** 3 / ms / 1e9:.1f} TFLOP/s", flush=True)
+    for epi in epis:
+        ms = ipr.ipr_bench_gemm_epi(prec, n, 2, 10, epi)
+        print(f"n={n} {prec} epi={epi}: {ms:.3f} ms  {2.0 * n ** 3 / ms / 1e9:.1f} TFLOP/s", flush=True)
