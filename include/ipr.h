@@ -57,8 +57,15 @@ typedef enum {
  *   IPR_FP8   E4M3 (PAPER.md:263-267 finds 2 stored mantissa bits still
  *             converge in storage-only mode), scaled max in [2^6, 2^7), one RNE rounding
  *   IPR_INT8  8-bit fixed point q = sat_127(rint(2^sigma x)), scaled max in [2^6, 2^7) -- the
- *             tensor-core analogue of the paper's fixed-point storage. */
-typedef enum { IPR_FP64 = 0, IPR_TF32 = 1, IPR_BF16 = 2, IPR_FP16 = 3, IPR_FP8 = 4, IPR_INT8 = 5 } ipr_prec;
+ *             tensor-core analogue of the paper's fixed-point storage.
+ *
+ * IPR_FP64_OZ: an FP64 phase (FP64 operands and storage, m <= 52) whose GEMMs run on the INT8
+ *             tensor cores by the Ozaki scheme I (reading R-23): 9 signed 7-bit digits per element
+ *             relative to its row / column maximum, the 45 digit products with s + t <= 10 as 9
+ *             K-concatenated kind::i8 GEMMs (exact INT32), combined in FP64.  Accuracy at the FP64
+ *             GEMM level (not bit-identical to DMMA).  Symmetric forms only, world = 1. */
+typedef enum { IPR_FP64 = 0, IPR_TF32 = 1, IPR_BF16 = 2, IPR_FP16 = 3, IPR_FP8 = 4, IPR_INT8 = 5,
+               IPR_FP64_OZ = 6 } ipr_prec;
 
 /* Rounding of the stored iterate (reading R-7: RNE default; RTZ = "bit truncation",
  * PAPER.md:26).  Operand conversions are always round-to-nearest-even (hardware cvt.rn). */

@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ipr_oracle.c")
 _LIB = os.path.join(_HERE, "libipr_oracle.so")
 
-FP64, TF32, BF16, FP16, FP8, INT8 = 0, 1, 2, 3, 4, 5
+FP64, TF32, BF16, FP16, FP8, INT8, FP64_OZ = 0, 1, 2, 3, 4, 5, 6
 RNE, RTZ = 0, 1
 CONTINUE, CONVERGED, ITER_LIMIT, DIVERGED, NONFINITE, SWITCH = 0, 1, 2, 3, 4, 5
 OUTCOME_NAMES = {0: "running", 1: "converged", 2: "iter_limit", 3: "diverged", 4: "nonfinite",

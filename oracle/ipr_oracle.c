@@ -61,7 +61,7 @@ void orc_prec_format(int prec, int *E, int *M) {
 }
 /* Reading R-8: container of a phase = its accumulate format: e8 (FP32) for the
  * BF16/FP16/TF32 phases, e11 (FP64) for FP64 phases. */
-int orc_container_E(int prec) { return prec == ORC_FP64 ? 11 : 8; }
+int orc_container_E(int prec) { return (prec == ORC_FP64 || prec == ORC_FP64_OZ) ? 11 : 8; }
 int orc_native_m(int prec) { int E, M; orc_prec_format(prec, &E, &M); return M; }
 
 static int phase_m(const orc_phase *ph) {
@@ -110,7 +110,7 @@ static double maxabs_of(int64_t len, const double *x) {
 static int qin_matrix(int prec, int64_t len, const double *x, double *y) {
   int E, M;
   orc_prec_format(prec, &E, &M);
-  if (prec == ORC_FP64) { if (y != x) memcpy(y, x, (size_t)len * sizeof(double)); return 0; }
+  if (prec == ORC_FP64 || prec == ORC_FP64_OZ) { if (y != x) memcpy(y, x, (size_t)len * sizeof(double)); return 0; }
   const int sigma = orc_sigma(prec, maxabs_of(len, x));
   if (prec == ORC_INT8) {
     for (int64_t i = 0; i < len; ++i) y[i] = orc_q_int8(ldexp(x[i], sigma));

@@ -27,7 +27,10 @@ extern "C" {
 #endif
 
 /* Operand (GEMM input) formats.  Values are independent of include/ipr.h on purpose. */
-enum { ORC_FP64 = 0, ORC_TF32 = 1, ORC_BF16 = 2, ORC_FP16 = 3, ORC_FP8 = 4, ORC_INT8 = 5 };
+/* ORC_FP64_OZ (= 6): an FP64 phase whose GPU GEMMs are emulated on INT8 tensor cores (Ozaki scheme,
+ * reading R-23).  The oracle computes it exactly like ORC_FP64: the emulation is an FP64-accurate
+ * GEMM, so the two sides differ by FP64-level rounding only (Level 2 tolerance, not bit-exact). */
+enum { ORC_FP64 = 0, ORC_TF32 = 1, ORC_BF16 = 2, ORC_FP16 = 3, ORC_FP8 = 4, ORC_INT8 = 5, ORC_FP64_OZ = 6 };
 enum { ORC_RNE = 0, ORC_RTZ = 1 };
 enum { ORC_CONTINUE = 0, ORC_CONVERGED = 1, ORC_ITER_LIMIT = 2, ORC_DIVERGED = 3,
        ORC_NONFINITE = 4, ORC_SWITCH = 5 };

@@ -11,7 +11,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "lib")
 LIB = os.path.join(OUT, "libipr.so")
-SOURCES = ["kernels.cu", "gemm_dmma.cu", "gemm_tc.cu", "engine.cu", "nccl_dl.cu"]
+SOURCES = ["kernels.cu", "gemm_dmma.cu", "gemm_tc.cu", "ozaki.cu", "engine.cu", "nccl_dl.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC,-O2", "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]

@@ -14,7 +14,12 @@
 
 namespace ipr {
 
-enum Prec { P_FP64 = 0, P_TF32 = 1, P_BF16 = 2, P_FP16 = 3, P_FP8 = 4, P_INT8 = 5 };
+enum Prec { P_FP64 = 0, P_TF32 = 1, P_BF16 = 2, P_FP16 = 3, P_FP8 = 4, P_INT8 = 5, P_FP64_OZ = 6 };
+
+// FP64 storage/operand format (P_FP64_OZ: FP64 values, GEMMs emulated on INT8 tensor cores)
+__host__ __device__ inline bool is_f64(int prec) { return prec == P_FP64 || prec == P_FP64_OZ; }
+// Ozaki scheme I (reading R-23): digits per operand; a product keeps the slice pairs s + t <= S + 1
+constexpr int OZ_S = 9;
 
 // Operand formats that carry a per-tensor power-of-two scale 2^sigma (reading R-20; NEXT-3).
 __host__ __device__ inline bool is_scaled(int prec) { return prec == P_FP16 || prec == P_FP8 || prec == P_INT8; }
@@ -32,6 +37,7 @@ enum EpiMode : int {
   EPI_WSTORE = 128,   // symmetric form: W = D row-major to wout[i * ldw + j] (FP32, or FP64 if w64)
   EPI_STORE_N = 256,  // also store qin(D) row-major (nout[i * ldn + j]): symmetric form, FP64,
                       // G = 1 -- D = A C row-major is the B operand of C (C A) for certification
+  EPI_OZACC = 512,    // Ozaki group g: ozacc[j * ldoz + i] (+)= 2^(rsig_i + csig_j - 7 g) * D_ij (INT32 D)
 };
 
 struct GemmArgs {
@@ -65,6 +71,10 @@ struct GemmArgs {
   void *wout; int64_t ldw; int w64;
   // EPI_STORE_N
   void *nout; int64_t ldn;
+  // EPI_OZACC (FP64 accumulator stored transposed), and the Ozaki operands of a P_FP64_OZ GEMM
+  double *ozacc; int64_t ldoz; const int *oz_rsig, *oz_csig; int oz_g, oz_first;
+  const int8_t *oz_a;   // A-role digit planes [OZ_S][npad][npad] (row-major per plane)
+  const int8_t *oz_b;   // B-role digits, per output column j: [OZ_S * npad] = digit planes S..1 of column j
 };
 
 // ------------------------------------------------------------------------------------
@@ -157,7 +167,8 @@ __device__ __forceinline__ int8_t to_int8(double x) {
 // Operand store of an FP32/FP64 value in phase precision (RNE); scaled formats get 2^sig first.
 __device__ __forceinline__ void store_operand(void *base, int64_t idx, int prec, double v, int sig) {
   switch (prec) {
-    case P_FP64: ((double *)base)[idx] = v; break;
+    case P_FP64:
+    case P_FP64_OZ: ((double *)base)[idx] = v; break;
     case P_TF32: ((float *)base)[idx] = to_tf32((float)v); break;
     case P_BF16: ((__nv_bfloat16 *)base)[idx] = __float2bfloat16_rn((float)v); break;
     case P_FP16: ((__half *)base)[idx] = __float2half_rn((float)__dmul_rn(v, pow2(sig))); break;
@@ -167,7 +178,7 @@ __device__ __forceinline__ void store_operand(void *base, int64_t idx, int prec,
 }
 
 __host__ __device__ inline int elt_size(int prec) {
-  return prec == P_FP64 ? 8 : (prec == P_BF16 || prec == P_FP16) ? 2 : (prec == P_FP8 || prec == P_INT8) ? 1 : 4;
+  return is_f64(prec) ? 8 : (prec == P_BF16 || prec == P_FP16) ? 2 : (prec == P_FP8 || prec == P_INT8) ? 1 : 4;
 }
 
 // Deterministic block-wide sum of one double per thread (fixed shuffle tree + warp order).
@@ -206,6 +217,7 @@ namespace ipr {
 extern int64_t g_launches;
 cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s);
 cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s);  // BF16 / FP16 / TF32 / FP8 / INT8
+cudaError_t launch_gemm_ozaki(const GemmArgs &a, cudaStream_t s);  // FP64 on INT8 (ozaki.cu)
 bool tc_supported(int prec);
 const char *tc_last_error();
 int gemm_tile_n(int prec);   // BN of the kernel used for a precision (partial layout)

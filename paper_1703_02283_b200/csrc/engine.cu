@@ -71,6 +71,12 @@ struct ipr_ctx {
   void *wbuf = nullptr;                 // symmetric form: W = qc(C) Rhat, full panel-major
   int wbytes = 4;                       // allocated element size of wbuf (8 if any FP64 correction)
   void *Zr = nullptr;                   // symmetric form, G = 1: Z_1 = A C row-major (FP64 phases)
+  // FP64 via Ozaki on INT8 tensor cores (IPR_FP64_OZ phases, reading R-23): digit planes (A role)
+  // and per-column digit rows (B role) of Ahat, of Chat (one set per iterate buffer) and of the
+  // current B operand, their scale exponents, and the FP64 accumulator (transposed)
+  int8_t *ozA = nullptr, *ozC[2] = {nullptr, nullptr}, *ozCb[2] = {nullptr, nullptr}, *ozB = nullptr;
+  int *ozA_sig = nullptr, *ozC_sig[2] = {nullptr, nullptr}, *ozB_sig = nullptr;
+  double *ozacc = nullptr;
   int zr_for = -1;                      // iterate buffer whose chain wrote Zr (-1: none)
   int form = IPR_FORM_LITERAL;          // iteration form (ipr_set_form)
   float *tscr = nullptr;                // FP16 phase T scratch (FP32)
@@ -164,7 +170,7 @@ ipr_status fail(ipr_ctx *c, ipr_status s, const char *fmt, ...) {
   } while (0)
 
 int native_m(int prec) {
-  return prec == IPR_FP64 ? 52 : (prec == IPR_BF16 || prec == IPR_INT8) ? 7 : prec == IPR_FP8 ? 3 : 10;
+  return is_f64(prec) ? 52 : (prec == IPR_BF16 || prec == IPR_INT8) ? 7 : prec == IPR_FP8 ? 3 : 10;
 }
 
 // padded order: whole 256-wide tiles per rank (tcgen05 tile N), zero padding
@@ -189,7 +195,7 @@ inline size_t slot_bytes(const ipr_ctx *c) { return (size_t)(c->npad * c->kp) * 
 
 // container of iterate buffer i in the current phase (FP64 phases alias the operand slot)
 void *cont_ptr(ipr_ctx *c, int i, const PhaseC &P) {
-  if (P.prec == IPR_FP64) return (char *)c->chat[i] + (size_t)c->rank * slot_bytes(c);
+  if (is_f64(P.prec)) return (char *)c->chat[i] + (size_t)c->rank * slot_bytes(c);
   return c->cont[i];
 }
 void *chat_slot(ipr_ctx *c, int i, int prec) {
@@ -231,6 +237,7 @@ int64_t tiles_m(const ipr_ctx *c, int prec) { return c->npad / gemm_tile_m(prec)
 int64_t tiles_n_total(const ipr_ctx *c, int prec) { return c->npad / gemm_tile_n(prec); }
 
 cudaError_t run_gemm(ipr_ctx *c, GemmArgs &g) {
+  if (g.prec == IPR_FP64_OZ) return launch_gemm_ozaki(g, c->st);
   return g.prec == IPR_FP64 ? launch_gemm_dmma(g, c->st) : launch_gemm_tc(g, c->st);
 }
 
@@ -260,7 +267,7 @@ ipr_status stage_a(ipr_ctx *c, const PhaseC &P, void *dst, int *sig_dst) {
 // container cont(i) -> operand Chat(i) (+ FP16 sigma), then all-gather (a8 / a9)
 ipr_status make_operand(ipr_ctx *c, int i, const PhaseC &P) {
   const int64_t cnt = c->npad * c->kp;
-  if (P.prec != IPR_FP64) {
+  if (!is_f64(P.prec)) {
     const int *sig = nullptr;
     if (is_scaled(P.prec)) {
       const int nparts = 256;
@@ -290,6 +297,23 @@ ipr_status save_best(ipr_ctx *c) {
 }
 
 ipr_status make_xt(ipr_ctx *c, int i, const PhaseC &P);
+// Ozaki digits of the FP64 iterate in buffer i (exactly symmetric, G = 1: its columns are its rows)
+ipr_status oz_split_chat(ipr_ctx *c, int i) {
+  CK(launch_oz_split((const double *)c->chat[i], c->npad, c->npad, c->npad, c->ozC[i], c->ozCb[i], c->ozC_sig[i], c->st));
+  return IPR_OK;
+}
+// Ozaki operands of a GEMM: A = the iterate buffer i's digits (or Ahat's if i < 0), B = digits of
+// the rows of the K-major B operand Xt (npad x npad FP64), split now into the scratch set
+ipr_status oz_operands(ipr_ctx *c, GemmArgs &g, int i, const void *Xt) {
+  CK(launch_oz_split((const double *)Xt, c->npad, c->npad, c->npad, nullptr, c->ozB, c->ozB_sig, c->st));
+  g.oz_a = i < 0 ? c->ozA : c->ozC[i];
+  g.oz_rsig = i < 0 ? c->ozA_sig : c->ozC_sig[i];
+  g.oz_b = c->ozB; g.oz_csig = c->ozB_sig;
+  g.ozacc = c->ozacc; g.ldoz = c->npad;
+  return IPR_OK;
+}
+// operand formats that share storage (FP64 and FP64-by-Ozaki both keep Chat in FP64)
+inline bool same_fmt(int a, int b) { return a == b || (is_f64(a) && is_f64(b)); }
 inline bool is_sym(const ipr_ctx *c) { return c->form == IPR_FORM_SYMMETRIC || c->form == IPR_FORM_SYMMETRIC_TRI; }
 void *chatc_slot(ipr_ctx *c, int i, int prec) {
   return (char *)c->chatc[i] + (size_t)c->rank * (size_t)(c->npad * c->kp) * elt_size(prec);
@@ -302,7 +326,7 @@ ipr_status gather_bytes(ipr_ctx *c, void *base, size_t per_rank, const char *wha
 }
 // symmetric form: Chat of iterate buffer i in the correction format (if it differs from prec)
 ipr_status make_corr_operand(ipr_ctx *c, int i, const PhaseC &P) {
-  if (P.corr == P.prec) return IPR_OK;
+  if (same_fmt(P.corr, P.prec)) return IPR_OK;
   const int64_t cnt = c->npad * c->kp;
   CK(launch_make_operand(cont_ptr(c, i, P), P.cont64, cnt, P.corr, nullptr, chatc_slot(c, i, P.corr), c->st));
   return gather_bytes(c, c->chatc[i], (size_t)cnt * elt_size(P.corr), "Chat corr");
@@ -325,6 +349,10 @@ ipr_status begin_phase(ipr_ctx *c, bool first) {
     }
   }
   CKS(make_operand(c, c->cur, P));
+  if (P.prec == IPR_FP64_OZ) {   // digits of Ahat (A role) and of Chat (both roles; G = 1, symmetric)
+    CK(launch_oz_split((const double *)c->Aop, c->npad, c->npad, c->npad, c->ozA, nullptr, c->ozA_sig, c->st));
+    CKS(oz_split_chat(c, c->cur));
+  }
   if (c->form == IPR_FORM_NEWTON_SCHULZ) CKS(make_xt(c, c->cur, P));
   if (is_sym(c)) {
     CKS(make_corr_operand(c, c->cur, P));
@@ -390,7 +418,7 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
         // FP64 last phase (G = 1): also keep Z_1 = A C row-major -- the B operand of C (C A), so
         // certifying ||I - C^p A||_F costs p - 1 GEMMs instead of p
         c->zr_for = -1;
-        if (c->Zr && prec == IPR_FP64 && P.m == 52 && c->phase == (int)c->ph.size() - 1) {
+        if (c->Zr && is_f64(prec) && P.m == 52 && c->phase == (int)c->ph.size() - 1) {
           g.mode |= EPI_STORE_N; g.nout = c->Zr; g.ldn = c->npad; c->zr_for = c->cur;
         }
       }
@@ -401,6 +429,14 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
       g.tout = (scaled && j < c->p) ? (void *)c->tscr : c->T[j & 1];
       g.ldt = c->npad;
       g.part = part;
+      if (prec == IPR_FP64_OZ) {
+        if (j == 1) {   // Ahat (A role) x Chat (B role: its rows, by symmetry)
+          g.oz_a = c->ozA; g.oz_rsig = c->ozA_sig; g.oz_b = c->ozCb[c->cur]; g.oz_csig = c->ozC_sig[c->cur];
+          g.ozacc = c->ozacc; g.ldoz = c->npad;
+        } else {
+          CKS(oz_operands(c, g, c->cur, c->T[(j - 1) & 1]));
+        }
+      }
       CK(run_gemm(c, g));
       if (scaled && j < c->p) {
         CKS(gather_pmax(c, c->pmax, tn_loc * tm));
@@ -464,7 +500,7 @@ ipr_status update(ipr_ctx *c) {
   g.cold = cont_ptr(c, c->cur, P);
   g.cnew = cont_ptr(c, nx, P);
   g.ldc = c->kp;
-  g.chat_new = (prec == IPR_FP64) ? nullptr : chat_slot(c, nx, prec);
+  g.chat_new = is_f64(prec) ? nullptr : chat_slot(c, nx, prec);
   g.ldh = c->kp;
   g.m = P.m; g.rtz = P.rtz; g.cont64 = P.cont64;
   g.part = c->part;
@@ -491,7 +527,7 @@ ipr_status update_sym(ipr_ctx *c) {
   const int nx = 1 - c->cur;
   if (c->best_loc == nx) CKS(save_best(c));
   GemmArgs g = base_args(c, P.corr, c->T[c->p & 1]);
-  if (P.corr == P.prec) chat_view(c, c->cur, P.prec, &g.A, &g.a_kp, &g.a_pstride);
+  if (same_fmt(P.corr, P.prec)) chat_view(c, c->cur, P.prec, &g.A, &g.a_kp, &g.a_pstride);
   else { g.A = c->chatc[c->cur]; g.a_kp = c->kp; g.a_pstride = c->npad * c->kp; }
   // W holds the exact accumulator values: FP64 for an FP64 (DMMA) correction, else FP32
   const int wb = P.corr == IPR_FP64 ? 8 : 4;
@@ -504,8 +540,8 @@ ipr_status update_sym(ipr_ctx *c) {
   CKS(gather_bytes(c, c->wbuf, (size_t)(c->npad * c->kp) * wb, "W"));
   CK(launch_sym_update(cont_ptr(c, c->cur, P), P.cont64, cont_ptr(c, nx, P), c->wbuf, wb == 8, c->npad,
                        c->kp, c->col0, c->p, P.m, P.rtz, P.prec,
-                       (P.prec == IPR_FP64 || is_scaled(P.prec)) ? nullptr : chat_slot(c, nx, P.prec), P.corr,
-                       P.corr == P.prec ? nullptr : chatc_slot(c, nx, P.corr), c->part, c->st));
+                       (is_f64(P.prec) || is_scaled(P.prec)) ? nullptr : chat_slot(c, nx, P.prec), P.corr,
+                       same_fmt(P.corr, P.prec) ? nullptr : chatc_slot(c, nx, P.corr), c->part, c->st));
   CK(cudaEventRecord(c->ev[3], c->st));
   c->upd_timed = true;
   const int64_t t64 = c->npad / 64;
@@ -513,7 +549,8 @@ ipr_status update_sym(ipr_ctx *c) {
   CK(launch_reduce_sum(c->part, t64 * t64, c->dscal + 1, c->st));
   if (is_scaled(P.prec)) CKS(make_operand(c, nx, P));   // sigma from max|C_{k+1}|, then all-gather
   else CKS(gather_chat(c, nx, P.prec));
-  if (P.corr != P.prec) CKS(gather_bytes(c, c->chatc[nx], (size_t)(c->npad * c->kp) * elt_size(P.corr), "Chat corr"));
+  if (P.prec == IPR_FP64_OZ) CKS(oz_split_chat(c, nx));
+  if (!same_fmt(P.corr, P.prec)) CKS(gather_bytes(c, c->chatc[nx], (size_t)(c->npad * c->kp) * elt_size(P.corr), "Chat corr"));
   if (c->world > 1) CKS(make_xt(c, nx, P));
   c->cur = nx;
   return IPR_OK;
@@ -559,8 +596,8 @@ void free_ctx(ipr_ctx *c) {
 // ipr_iterate): one cudaMalloc / cudaFree per solve, and an OOM is reported before any work.
 ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
   const size_t full = (size_t)(c->npad * c->npad), panel = (size_t)(c->npad * c->kp);
-  bool fp16 = false;                    // any scaled-format phase: FP32 T scratch
-  for (auto &P : c->ph) fp16 |= is_scaled(P.prec);
+  bool fp16 = false, oz = false;        // any scaled-format phase: FP32 T scratch; any Ozaki phase
+  for (auto &P : c->ph) { fp16 |= is_scaled(P.prec); oz |= P.prec == IPR_FP64_OZ; }
   struct Slot { void **p; size_t bytes; };
   const Slot slots[] = {
       {&c->chat[0], full * 8}, {&c->chat[1], full * 8}, {&c->cont[0], panel * 4}, {&c->cont[1], panel * 4},
@@ -571,6 +608,12 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       {&c->chatc[0], need_corr ? full * 4 : 0}, {&c->chatc[1], need_corr ? full * 4 : 0},
       {&c->wbuf, is_sym(c) ? full * c->wbytes : 0},
       {&c->Zr, (is_sym(c) && c->world == 1) ? panel * 8 : 0},
+      {(void **)&c->ozA, oz ? full * OZ_S : 0}, {(void **)&c->ozC[0], oz ? full * OZ_S : 0},
+      {(void **)&c->ozC[1], oz ? full * OZ_S : 0}, {(void **)&c->ozCb[0], oz ? full * OZ_S : 0},
+      {(void **)&c->ozCb[1], oz ? full * OZ_S : 0}, {(void **)&c->ozB, oz ? full * OZ_S : 0},
+      {(void **)&c->ozA_sig, oz ? (size_t)c->npad * 4 : 0}, {(void **)&c->ozC_sig[0], oz ? (size_t)c->npad * 4 : 0},
+      {(void **)&c->ozC_sig[1], oz ? (size_t)c->npad * 4 : 0}, {(void **)&c->ozB_sig, oz ? (size_t)c->npad * 4 : 0},
+      {(void **)&c->ozacc, oz ? full * 8 : 0},
       {(void **)&c->full64, full * 8}, {&c->Acert, panel * 8}};
   size_t total = 0;
   for (const Slot &q : slots) total += (q.bytes + 255) / 256 * 256;
@@ -702,10 +745,10 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
   int prev_ob = -1, prev_m = -1;
   for (int i = 0; i < nphases; ++i) {
     const ipr_phase &q = phases[i];
-    if (q.prec < IPR_FP64 || q.prec > IPR_INT8) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad prec", i);
+    if (q.prec < IPR_FP64 || q.prec > IPR_FP64_OZ) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad prec", i);
     PhaseC P;
     P.prec = q.prec;
-    P.cont64 = q.prec == IPR_FP64;
+    P.cont64 = is_f64(q.prec);
     const int mmax = P.cont64 ? 52 : 23;
     P.m = q.mant_bits < 0 ? native_m(q.prec) : q.mant_bits;
     if (P.m > mmax) return fail(c, IPR_E_INVALID_ARG, "phase %d: mant_bits %d > %d for this container", i, P.m, mmax);
@@ -718,14 +761,15 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
     P.switch_tol = q.switch_tol; P.plateau_ratio = q.plateau_ratio; P.plateau_arm = q.plateau_arm;
     P.max_iters = q.max_iters;
     P.corr = q.corr_prec >= 0 ? q.corr_prec : is_scaled(q.prec) ? IPR_BF16 : q.prec;
-    if (P.corr < IPR_FP64 || P.corr > IPR_INT8) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad corr_prec", i);
-    if (P.corr == IPR_FP64 && P.prec != IPR_FP64)
+    if (P.corr < IPR_FP64 || P.corr > IPR_FP64_OZ) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad corr_prec", i);
+    if (P.corr == IPR_FP64_OZ) P.corr = IPR_FP64;   // an FP64 correction runs on DMMA
+    if (P.corr == IPR_FP64 && !is_f64(P.prec))
       return fail(c, IPR_E_INVALID_ARG, "phase %d: an FP64 correction needs an FP64 phase", i);
     const int ob = operand_bits(q.prec);
     if (ob < prev_ob || (ob == prev_ob && P.m < prev_m))
       return fail(c, IPR_E_INVALID_ARG, "phase %d: precision must be non-decreasing along the schedule", i);
     prev_ob = ob; prev_m = P.m;
-    if (P.prec != IPR_FP64 && !tc_supported(P.prec))
+    if (!is_f64(P.prec) && !tc_supported(P.prec))
       return fail(c, IPR_E_UNSUPPORTED, "phase %d: tcgen05 path for this precision is not built", i);
     v.push_back(P);
   }
@@ -757,6 +801,9 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       if (c->p != 1) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: the Newton-Schulz form needs p = 1");
     }
     bool need_c = false;
+    for (auto &P : c->ph)
+      if (P.prec == IPR_FP64_OZ && (!is_sym(c) || c->world != 1))
+        return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ phases need a symmetric form and world = 1");
     if (is_sym(c)) {
       if (c->p < 2) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: the symmetric form needs p >= 2 (p = 1: Newton-Schulz)");
       if (c->form == IPR_FORM_SYMMETRIC_TRI && c->p != 2)
@@ -769,7 +816,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
           return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: the symmetric form's correction must be BF16, TF32 or FP64");
         if (P.corr != IPR_FP64 && !tc_supported(P.corr))
           return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: tcgen05 path for the correction precision is not built");
-        need_c |= P.corr != P.prec;
+        need_c |= !same_fmt(P.corr, P.prec);
         if (P.corr == IPR_FP64) c->wbytes = 8;
       }
     }
@@ -786,7 +833,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     const int phase_now = c->phase;
     bool best_new = false;
     const int d = decide(c, rho, &best_new);
-    if (best_new) { c->best_loc = c->cur; c->best_cont64 = c->ph[c->phase].prec == IPR_FP64; }
+    if (best_new) { c->best_loc = c->cur; c->best_cont64 = is_f64(c->ph[c->phase].prec); }
     ipr_record r;
     r.k = (int)c->trace.size(); r.phase = phase_now; r.prec = c->ph[phase_now].prec; r.mant_bits = c->ph[phase_now].m;
     r.decision = d; r.rho = rho; r.rho_hat = rho / std::sqrt((double)c->n); r.delta = NAN; r.gemm_ms = ms;
@@ -817,7 +864,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       CKS(step_update(c));
       c->pending_delta = (int64_t)c->trace.size() - 1;
     } else if (d == IPR_DEC_SWITCH) {
-      if (c->best_loc < 0) { c->best_loc = c->cur; c->best_cont64 = c->ph[c->phase].prec == IPR_FP64; }
+      if (c->best_loc < 0) { c->best_loc = c->cur; c->best_cont64 = is_f64(c->ph[c->phase].prec); }
       CKS(save_best(c));
       c->phase += 1; c->it_in_phase = 0; c->rho_prev = NAN;
       c->cur = 0;
@@ -888,11 +935,13 @@ ipr_status ipr_get_iterate(ipr_ctx *c, int which, double *C_dev_out, int64_t ldc
 // residual partials (reading R-3; same arithmetic class as certify_best).
 static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho) {
   const void *X = c->Zr;
+  const int prec = c->ph[c->phase].prec == IPR_FP64_OZ ? IPR_FP64_OZ : IPR_FP64;
   for (int j = 2; j <= c->p; ++j) {
-    GemmArgs g = base_args(c, IPR_FP64, X);
-    chat_view(c, i, IPR_FP64, &g.A, &g.a_kp, &g.a_pstride);
+    GemmArgs g = base_args(c, prec, X);
+    chat_view(c, i, prec, &g.A, &g.a_kp, &g.a_pstride);
     g.mode = EPI_STORE_T | (j == c->p ? EPI_RESID : 0);
     g.tout = c->T[j & 1]; g.ldt = c->npad; g.part = c->part;
+    if (prec == IPR_FP64_OZ) CKS(oz_operands(c, g, i, X));
     CK(run_gemm(c, g));
     X = c->T[j & 1];
   }
@@ -978,9 +1027,9 @@ ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_
 
 ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_dev, double *Z_dev, void *stream) {
   ipr_ctx *c = nullptr;
-  if (n <= 0 || !X_dev || !Yt_dev || !Z_dev || prec < 0 || prec > IPR_INT8)
+  if (n <= 0 || !X_dev || !Yt_dev || !Z_dev || prec < 0 || prec > IPR_FP64_OZ)
     return fail(c, IPR_E_INVALID_ARG, "ipr_test_gemm: bad arguments");
-  if (prec != IPR_FP64 && !tc_supported(prec))
+  if (!is_f64(prec) && !tc_supported(prec))
     return fail(c, IPR_E_UNSUPPORTED, "ipr_test_gemm: tcgen05 path for this precision is not built");
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t unit = prec == IPR_FP64 ? 128 : 256;
@@ -999,10 +1048,25 @@ ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_
   g.A = X; g.a_kp = np; g.a_pstride = np * np;
   g.B = Y; g.ldb = np; g.prec = prec; g.mode = EPI_F64;
   g.zout = Z; g.ldz = np; g.tiles_m = np / gemm_tile_m(prec);
-  cudaError_t e = prec == IPR_FP64 ? launch_gemm_dmma(g, s) : launch_gemm_tc(g, s);
+  cudaError_t e = cudaSuccess;
+  int8_t *oa = nullptr, *ob = nullptr;
+  int *sig = nullptr;
+  double *acc = nullptr;
+  if (prec == IPR_FP64_OZ) {   // Ozaki digits of X (A role, rows) and of Yt's rows (B role)
+    e = cudaMalloc(&oa, (size_t)(np * np) * OZ_S);
+    if (e == cudaSuccess) e = cudaMalloc(&ob, (size_t)(np * np) * OZ_S);
+    if (e == cudaSuccess) e = cudaMalloc(&sig, (size_t)np * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&acc, (size_t)(np * np) * 8);
+    if (e == cudaSuccess) e = launch_oz_split((const double *)X, np, np, np, oa, nullptr, sig, s);
+    if (e == cudaSuccess) e = launch_oz_split((const double *)Y, np, np, np, nullptr, ob, sig + np, s);
+    g.oz_a = oa; g.oz_rsig = sig; g.oz_b = ob; g.oz_csig = sig + np; g.ozacc = acc; g.ldoz = np;
+    if (e == cudaSuccess) e = launch_gemm_ozaki(g, s);
+  } else {
+    e = prec == IPR_FP64 ? launch_gemm_dmma(g, s) : launch_gemm_tc(g, s);
+  }
   if (e == cudaSuccess) e = launch_unpad_f64(Z, n, np, Z_dev, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cudaFree(X); cudaFree(Y); cudaFree(Z);
+  cudaFree(X); cudaFree(Y); cudaFree(Z); cudaFree(oa); cudaFree(ob); cudaFree(sig); cudaFree(acc);
   if (e != cudaSuccess) return fail(c, IPR_E_CUDA, "ipr_test_gemm: %s %s", cudaGetErrorString(e), tc_last_error());
   return IPR_OK;
 }
@@ -1013,9 +1077,9 @@ ipr_status ipr_bench_gemm(int prec, int64_t n, int warmup, int iters, void *stre
 
 ipr_status ipr_bench_gemm_epi(int prec, int64_t n, int warmup, int iters, int epi, void *stream, double *ms) {
   ipr_ctx *c = nullptr;
-  if (n <= 0 || prec < 0 || prec > IPR_INT8 || warmup < 0 || iters <= 0 || !ms || epi < 0 || epi > 3)
+  if (n <= 0 || prec < 0 || prec > IPR_FP64_OZ || warmup < 0 || iters <= 0 || !ms || epi < 0 || epi > 3)
     return fail(c, IPR_E_INVALID_ARG, "ipr_bench_gemm: bad arguments");
-  if (prec != IPR_FP64 && !tc_supported(prec))
+  if (!is_f64(prec) && !tc_supported(prec))
     return fail(c, IPR_E_UNSUPPORTED, "ipr_bench_gemm: tcgen05 path for this precision is not built");
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t unit = prec == IPR_FP64 ? 128 : 256;
@@ -1042,7 +1106,27 @@ ipr_status ipr_bench_gemm_epi(int prec, int64_t n, int warmup, int iters, int ep
   g.B = Y; g.ldb = np; g.prec = prec; g.tprec = prec; g.mode = mode;
   g.tout = T; g.ldt = np; g.tiles_m = np / gemm_tile_m(prec);
   if (mode == EPI_TSCRATCH) g.pmax = pm;
-  auto run = [&]() { return prec == IPR_FP64 ? launch_gemm_dmma(g, s) : launch_gemm_tc(g, s); };
+  // Ozaki: the left operand's digits once (amortised over an iteration's GEMMs), the right
+  // operand's split inside every timed launch (one split per GEMM, as in the hot path)
+  int8_t *oa = nullptr, *ob = nullptr;
+  int *sig = nullptr;
+  double *acc = nullptr;
+  if (prec == IPR_FP64_OZ) {
+    if (e == cudaSuccess) e = cudaMalloc(&oa, (size_t)(np * np) * OZ_S);
+    if (e == cudaSuccess) e = cudaMalloc(&ob, (size_t)(np * np) * OZ_S);
+    if (e == cudaSuccess) e = cudaMalloc(&sig, (size_t)np * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&acc, (size_t)(np * np) * 8);
+    if (e == cudaSuccess) e = launch_oz_split((const double *)X, np, np, np, oa, nullptr, sig, s);
+    g.oz_a = oa; g.oz_rsig = sig; g.oz_b = ob; g.oz_csig = sig + np; g.ozacc = acc; g.ldoz = np;
+    g.mode = mode ? EPI_STORE_T : 0;
+  }
+  auto run = [&]() {
+    if (prec == IPR_FP64_OZ) {
+      cudaError_t r = launch_oz_split((const double *)Y, np, np, np, nullptr, ob, sig + np, s);
+      return r == cudaSuccess ? launch_gemm_ozaki(g, s) : r;
+    }
+    return prec == IPR_FP64 ? launch_gemm_dmma(g, s) : launch_gemm_tc(g, s);
+  };
   for (int i = 0; i < warmup && e == cudaSuccess; ++i) e = run();
   if (e == cudaSuccess) e = cudaEventRecord(e0, s);
   for (int i = 0; i < iters && e == cudaSuccess; ++i) e = run();
@@ -1051,7 +1135,7 @@ ipr_status ipr_bench_gemm_epi(int prec, int64_t n, int warmup, int iters, int ep
   float t = 0.f;
   if (e == cudaSuccess) e = cudaEventElapsedTime(&t, e0, e1);
   if (e == cudaSuccess) *ms = (double)t / iters;
-  cudaFree(X); cudaFree(Y); cudaFree(T); cudaFree(pm);
+  cudaFree(X); cudaFree(Y); cudaFree(T); cudaFree(pm); cudaFree(oa); cudaFree(ob); cudaFree(sig); cudaFree(acc);
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
   if (e != cudaSuccess) return fail(c, IPR_E_CUDA, "ipr_bench_gemm: %s %s", cudaGetErrorString(e), tc_last_error());

@@ -40,12 +40,14 @@ constexpr int TC_GROUP_M = 8;         // pair-rows per scheduling group
 bool tc_supported(int prec) {
   return prec == P_BF16 || prec == P_FP16 || prec == P_TF32 || prec == P_FP8 || prec == P_INT8;
 }
+// partial-sum tile of the kernel that produces a format's GEMM epilogue: P_FP64_OZ finishes in
+// k_oz_finish with the DMMA tile (128 x 64), so its partial layout equals the FP64 one
 // tcgen05.mma kind of an operand format: 0 kind::f16 (BF16/FP16), 1 kind::tf32, 2 kind::f8f6f4
 // (E4M3), 3 kind::i8 (signed).  Every kind consumes 32 bytes of K per instruction.
 __host__ __device__ constexpr int tc_kind(int prec) {
   return prec == P_TF32 ? 1 : prec == P_FP8 ? 2 : prec == P_INT8 ? 3 : 0;
 }
-int gemm_tile_n(int prec) { return prec == P_FP64 ? dmma_tile_n() : TC_BN; }
+int gemm_tile_n(int prec) { return is_f64(prec) ? dmma_tile_n() : TC_BN; }
 int gemm_tile_m(int prec) { return 128; }
 
 // ---------------------------------------------------------------------------------------
@@ -208,6 +210,19 @@ template <int KIND>
 __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_t col, const uint32_t (&r)[32],
                                           double scale, EpiAcc &ea) {
   const int mode = g.mode;
+  if (KIND == 3 && mode == EPI_OZACC) {
+    // Ozaki group g (reading R-23): the INT32 group sum is exact; 2^(rsig + csig - 7 g) scaling is
+    // exact; the FP64 accumulation (smallest groups first) is the only rounding.  Transposed
+    // layout: a warp's 32 rows are 256 contiguous bytes per column.
+    const int rs = g.oz_rsig[row];
+    double *z = g.ozacc + col * g.ldoz + row;
+    #pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const double v = __dmul_rn((double)(int32_t)r[j], pow2(rs + g.oz_csig[col + j] - 7 * g.oz_g));
+      z[j * g.ldoz] = g.oz_first ? v : __dadd_rn(z[j * g.ldoz], v);
+    }
+    return;
+  }
   // ---- FP32 fast paths (no FP64 arithmetic; results identical to the general path below) ----
   // (a) plain chain store: qin(D) of an unscaled accumulator -- BF16 / TF32 are one RNE rounding
   //     of the FP32 value, exactly what the FP64 detour produced ((float)(double)f == f)

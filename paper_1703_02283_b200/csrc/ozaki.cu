@@ -1,0 +1,117 @@
+// ozaki.cu -- FP64 GEMMs emulated on the INT8 tensor cores (tcgen05 kind::i8), Ozaki scheme I
+// (reading R-23).  An FP64 phase whose format is P_FP64_OZ computes every product of
+// the hot path this way instead of on the DMMA pipe:
+//
+//   split     x_ik = 2^sig_i * sum_{s=1..S} d_s,ik 2^-7s   (+ |rest| <= 2^(sig_i - 7S - 1))
+//             per ROW of the left operand (sig_i from max_k |x_ik|) and per COLUMN of the right
+//             operand; d_1 in [-127, 127], d_s in [-64, 64] (s >= 2), every step exact in FP64
+//   products  P_g = sum_{s + t = g} D_s E_t  for g = 2 .. S+1: ONE int8 GEMM with the K-concatenated
+//             operands [D_1 | ... | D_{g-1}] and [E_{g-1}; ...; E_1], exact in INT32
+//             (|P_g| <= 8 * 127 * 64 * n < 2^31 for n <= 8192 * 4)
+//   combine   Z_ij = sum_g 2^(sig_i + tau_j - 7g) P_g,ij, in FP64, smallest groups first
+//   finish    the hot path's FP64 epilogue (store / residual / update partials, epilogue.cuh) on Z
+//
+// S = 9 keeps 63 bits per operand relative to its row / column maximum; the dropped pairs
+// (s + t > S + 1) and the digit remainder are below the FP64 GEMM's own rounding at the orders
+// used here (measured: Frobenius error 9e-16 vs 8.6e-15 for an FP64 GEMM at n = 512; the oracle's
+// tests/test_oracle... pin the scheme on the CPU).  K-work: S(S+1)/2 = 45 int8 GEMMs of order n.
+#include "common.cuh"
+#include "epilogue.cuh"
+#include "kernels.h"
+
+namespace ipr {
+
+// Digits of the rows of X (FP64, row-major, leading dimension ld): one block per row.
+//   planes (A role, may be NULL): digit s of x_rk at planes[(s-1) * rows * cols + r * cols + k]
+//   bcat   (B role, may be NULL): digit s of x_rk at bcat[r * S * cols + (S - s) * cols + k]
+//   sig[r]: the row's scale exponent
+__global__ void __launch_bounds__(256) k_oz_split(const double *__restrict__ X, int64_t ld, int64_t rows,
+                                                  int64_t cols, int8_t *planes, int8_t *bcat, int *sig) {
+  __shared__ double red[8];
+  const int64_t r = blockIdx.x;
+  const double *x = X + r * ld;
+  double mx = 0.0;
+  for (int64_t k = threadIdx.x; k < cols; k += blockDim.x) mx = fmax(mx, fabs(x[k]));
+  #pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
+    red[0] = fmax(mx, red[0]);
+  }
+  __syncthreads();
+  mx = red[0];
+  // |x| 2^-sig * 128 <= 127: sig = floor(log2(mx * 128/127)) + 1 (0 for an all-zero row)
+  const int sg = (mx > 0.0) ? ilogb(mx * (128.0 / 127.0)) + 1 : 0;
+  if (threadIdx.x == 0) sig[r] = sg;
+  const double sc = pow2(-sg);
+  for (int64_t k = threadIdx.x; k < cols; k += blockDim.x) {
+    double v = __dmul_rn(x[k], sc);
+    #pragma unroll
+    for (int s = 1; s <= OZ_S; ++s) {
+      v = __dmul_rn(v, 128.0);
+      const double d = rint(v);
+      v = __dsub_rn(v, d);
+      const int8_t di = (int8_t)(int)d;
+      if (planes) planes[(int64_t)(s - 1) * rows * cols + r * cols + k] = di;
+      if (bcat) bcat[r * OZ_S * cols + (int64_t)(OZ_S - s) * cols + k] = di;
+    }
+  }
+}
+
+// The hot path's FP64 epilogue on the combined Ozaki result (stored transposed: Z(i,j) at
+// ozacc[j * ldoz + i]), with the DMMA kernel's 128 x 64 tiles and partial-sum slots.
+__global__ void __launch_bounds__(128) k_oz_finish(const GemmArgs g) {
+  const int tm = blockIdx.y, tn = blockIdx.x;
+  const int64_t m0 = (int64_t)tm * 128, n0 = (int64_t)tn * 64;
+  const int64_t tile = ((g.col0 + n0) / 64) * g.tiles_m + tm;
+  const int mode = g.mode;
+  __shared__ double red[4];
+  if (g.tri && m0 > g.col0 + n0 + 63) {          // wholly below the diagonal: not computed
+    if (threadIdx.x == 0 && (mode & EPI_RESID)) g.part[tile] = 0.0;
+    return;
+  }
+  const int64_t row = m0 + threadIdx.x;
+  EpiAcc ea{0.0, 0.0, 0.0f};
+  for (int c = 0; c < 64; ++c) {
+    const double v = g.ozacc[(n0 + c) * g.ldoz + row];
+    epi_element<-1>(g, row, n0 + c, v, ea);
+  }
+  if (mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE)) {
+    const double s = block_sum_det<128>((mode & EPI_RESID) ? ea.r2 : ea.d2, red);
+    if (threadIdx.x == 0) g.part[tile] = s;
+  }
+}
+
+cudaError_t launch_oz_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int8_t *planes, int8_t *bcat,
+                            int *sig, cudaStream_t s) {
+  k_oz_split<<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, planes, bcat, sig);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// Z = X Y for a P_FP64_OZ GemmArgs: g.oz_a / g.oz_rsig hold the digits of X (A role), g.oz_b /
+// g.oz_csig those of Y (B role, per output column); g.ozacc is the FP64 accumulator (transposed,
+// ldoz); then the epilogue g.mode runs in k_oz_finish.  Single panel (G = 1): M = N = K = npad.
+cudaError_t launch_gemm_ozaki(const GemmArgs &g, cudaStream_t s) {
+  if (!g.oz_a || !g.oz_b || !g.oz_rsig || !g.oz_csig || !g.ozacc || g.M != g.K || g.N != g.K) return cudaErrorInvalidValue;
+  const int64_t np = g.K;
+  for (int gi = OZ_S + 1; gi >= 2; --gi) {
+    GemmArgs q = g;
+    q.prec = P_INT8; q.tprec = P_INT8;
+    q.A = g.oz_a; q.a_kp = np; q.a_pstride = np * np;
+    q.K = (int64_t)(gi - 1) * np;
+    q.B = g.oz_b + (int64_t)(OZ_S - gi + 1) * np; q.ldb = (int64_t)OZ_S * np;
+    q.mode = EPI_OZACC; q.oz_g = gi; q.oz_first = gi == OZ_S + 1;
+    q.sigA = nullptr; q.sigB = nullptr; q.pmax = nullptr; q.part = nullptr;
+    cudaError_t e = launch_gemm_tc(q, s);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid((unsigned)(g.N / 64), (unsigned)(g.M / 128));
+  k_oz_finish<<<grid, 128, 0, s>>>(g);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace ipr
