@@ -28,10 +28,13 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "time-to-FP64-residual 1e-12 (n=8192, p=2)"
-# headline schedule: BF16 tensor-core phase, then FP64 refinement with a BF16 correction GEMM,
-# in the symmetrised-correction form with the upper-triangle GEMM 2 (NEXT-2 (i)+(iii), R-22)
-DEFAULT_SCHEDULE = "symtri:bf16>fp64/cbf16"
-EXTRA_SCHEDULES = ["fp64", "bf16>fp64", "tf32>fp64", "fp16>fp64", "sym:fp64", "sym:fp64/cbf16", "symtri:fp64/cbf16",
+# headline schedule (symmetrised-correction form with the upper-triangle GEMM 2, NEXT-2 (i)+(iii),
+# DESIGN.md R-22): BF16 tensor-core phase; a 23-bit phase (C stored at m = 23, GEMMs on the INT8
+# tensor cores with 5 Ozaki digits, R-23); FP64 refinement (9 Ozaki digits) with a BF16 correction
+# GEMM; convergence certified with FP64 DMMA GEMMs
+DEFAULT_SCHEDULE = "symtri:bf16>fp64oz@23/cbf16>fp64oz/cbf16"
+EXTRA_SCHEDULES = ["fp64", "symtri:bf16>fp64oz/cbf16", "sym:fp64oz", "symtri:fp8>bf16>fp64oz@23/cbf16>fp64oz/cbf16",
+                   "bf16>fp64", "tf32>fp64", "fp16>fp64", "sym:fp64", "sym:fp64/cbf16", "symtri:fp64/cbf16",
                    "symtri:bf16>fp64/cbf16", "symtri:bf16>tf32>fp64/cbf16", "symtri:fp8>bf16>fp64/cbf16",
                    "symtri:int8>bf16>fp64/cbf16", "symtri:fp16>fp64/cbf16",
                    "sym:bf16>fp64", "sym:tf32>fp64/cbf16", "sym:bf16>tf32>fp64/cbf16"]
@@ -55,15 +58,20 @@ def parse():
 
 
 def parse_schedule(name):
-    """'sym:bf16>fp64/cbf16' -> ("symmetric", [("bf16", -1), ("fp64", "bf16")])."""
+    """'sym:bf16>fp64oz@23/cbf16>fp64' -> ("symmetric", [("bf16", -1, -1), ("fp64oz", "bf16", 23),
+    ("fp64", -1, -1)]): phases prec[@mant_bits][/c<correction prec>]."""
     form = "literal"
     if ":" in name:
         f, name = name.split(":", 1)
         form = {"sym": "symmetric", "symtri": "symmetric_tri", "ns": "newton_schulz", "lit": "literal"}[f]
     parts = []
     for ph in name.replace("-", ">").split(">"):
+        ph, _, m = ph.partition("@")          # prec[@mant_bits][/c<corr>]
+        if "/c" in m:
+            m, _, corr = m.partition("/c")
+            ph = ph + "/c" + corr
         prec, _, corr = ph.partition("/c")
-        parts.append((prec, corr or -1))
+        parts.append((prec, corr or -1, int(m) if m else -1))
     return form, parts
 
 
@@ -73,14 +81,14 @@ def schedule(name, n):
     import paper_1703_02283_b200 as ipr
     form, parts = parse_schedule(name)
     out = []
-    for i, (prec, corr) in enumerate(parts):
+    for i, (prec, corr, m) in enumerate(parts):
         if i == len(parts) - 1:
-            out.append(ipr.make_phase(prec, corr_prec=corr))
+            out.append(ipr.make_phase(prec, mant_bits=m, corr_prec=corr))
         else:
             # the symmetric form damps low-precision noise in the next phase, so a low phase runs
             # to its plateau; the literal form leaves at rho_hat <= 1e-2 as well
             sw = 0.0 if form.startswith("symmetric") else 1e-2 * math.sqrt(n)
-            out.append(ipr.make_phase(prec, switch_tol=sw, plateau_ratio=0.7, plateau_arm=0.5,
+            out.append(ipr.make_phase(prec, mant_bits=m, switch_tol=sw, plateau_ratio=0.7, plateau_arm=0.5,
                                       max_iters=40, corr_prec=corr))
     return form, out
 
@@ -100,7 +108,8 @@ def gemm_peaks():
             pass
     return {"fp64": (FP64_PEAK_TFLOPS, FP64_PEAK_SRC), "bf16": (bf16, src), "fp16": (bf16, src + " (fp16 = bf16 rate)"),
             "tf32": (bf16 / 2, src + " x 1/2 (nominal tf32:bf16)"), "fp8": (bf16 * 2, src + " x 2 (nominal fp8:bf16)"),
-            "int8": (bf16 * 2, src + " x 2 (nominal int8:bf16)")}
+            "int8": (bf16 * 2, src + " x 2 (nominal int8:bf16)"),
+            "fp64oz": (bf16 * 2, src + " x 2 (INT8 peak; Ozaki FP64 = 45 INT8 digit products)")}
 
 
 def gemm_count(trace, p):
@@ -287,23 +296,42 @@ def main():
     # p * 2 n^3 / G, except the tri form, whose GEMM 2 (C A C) needs only the upper triangle:
     # 2 n^3 + n^2 (n + 1) (its extra work on the diagonal tiles is overhead, not credit).
     fl_chain = (2.0 * n ** 3 + n * n * (n + 1.0)) if form == "symmetric_tri" else p * fl_gemm
-    tot_ms = sum(t["gemm_ms"] - t["upd_ms"] for trc, _ in traces for t in trc if t["prec"] == "fp64")
-    n_chains = sum(sum(1 for t in trc if t["prec"] == "fp64") for trc, _ in traces)
-    tot_gemms = p * n_chains
-    gemm_ms = tot_ms / max(tot_gemms, 1)
-    achieved = (n_chains * fl_chain) / (tot_ms * 1e-3) / 1e12 if tot_ms > 0 else None
+    last = ipr.PREC_NAMES[phases[-1].prec]
+    recs = [t for trc, _ in traces for t in trc if t["prec"] == last]
+    tot_ms = sum(t["gemm_ms"] - t["upd_ms"] for t in recs)
+    n_chains = len(recs)
     all_ms = sum(t["gemm_ms"] for trc, _ in traces for t in trc)
     step_gemm_share = tot_ms / (ms * args.steps) if ms > 0 else None
-    roof = {"bound": "tensor", "kernel": "k_gemm_dmma (FP64 DMMA.8x8x4)", "achieved": achieved,
-            "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
-            "traffic": None, "peak_source": FP64_PEAK_SRC, "cublas_dgemm_tflops": 35.5,
-            "algorithmic_flops_per_launch": fl_chain / p, "avg_launch_ms": gemm_ms,
-            "algorithmic_flops_per_chain": fl_chain, "launches_per_chain": p, "gemm_share_of_step": step_gemm_share,
-            "all_gemm_share_of_step": all_ms / (ms * args.steps) if ms > 0 else None}
+    peaks = gemm_peaks()
+    if last == "fp64oz":
+        # dominant kernel: the INT8 tcgen05 GEMMs of the Ozaki FP64 products (45 digit products per
+        # FP64 product at 9 digits): achieved INT8 TOPS over the whole FP64 chain (its digit splits
+        # and FP64 finish passes included -- counted as overhead, not credit), vs the INT8 peak
+        prods = 45.0
+        achieved = prods * n_chains * fl_chain / (tot_ms * 1e-3) / 1e12 if tot_ms > 0 else None
+        roof = {"bound": "tensor", "kernel": "k_gemm_tc<kind::i8> (Ozaki FP64 chain: 9 K-concatenated INT8 GEMMs "
+                "per product + digit split + FP64 finish)", "achieved": achieved, "peak": peaks["int8"][0],
+                "unit": "TOPS (int8)", "frac": achieved / peaks["int8"][0] if achieved else None, "traffic": None,
+                "peak_source": peaks["int8"][1], "fp64_equivalent_tflops": achieved / prods if achieved else None,
+                "algorithmic_int8_ops_per_chain": prods * fl_chain, "chains": n_chains,
+                "avg_chain_ms": tot_ms / max(n_chains, 1), "gemm_share_of_step": step_gemm_share,
+                "all_gemm_share_of_step": all_ms / (ms * args.steps) if ms > 0 else None}
+        traffic_key = "k_gemm_tc_i8_ozaki"
+    else:
+        tot_gemms = p * n_chains
+        gemm_ms = tot_ms / max(tot_gemms, 1)
+        achieved = (n_chains * fl_chain) / (tot_ms * 1e-3) / 1e12 if tot_ms > 0 else None
+        roof = {"bound": "tensor", "kernel": "k_gemm_dmma (FP64 DMMA.8x8x4)", "achieved": achieved,
+                "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS if achieved else None,
+                "traffic": None, "peak_source": FP64_PEAK_SRC, "cublas_dgemm_tflops": 35.5,
+                "algorithmic_flops_per_launch": fl_chain / p, "avg_launch_ms": gemm_ms,
+                "algorithmic_flops_per_chain": fl_chain, "launches_per_chain": p, "gemm_share_of_step": step_gemm_share,
+                "all_gemm_share_of_step": all_ms / (ms * args.steps) if ms > 0 else None}
+        traffic_key = "k_gemm_dmma"
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            roof["traffic"] = json.load(open(tp)).get("k_gemm_dmma")
+            roof["traffic"] = json.load(open(tp)).get(traffic_key)
         except Exception:
             pass
 
@@ -363,10 +391,12 @@ def main():
         # peak of its own dtype (burst figure: a kernel timed alone)
         peaks = gemm_peaks()
         rates, fracs = {}, {}
-        for prec in ["fp64", "tf32", "bf16", "fp16", "fp8", "int8"]:
+        for prec in ["fp64", "fp64oz", "tf32", "bf16", "fp16", "fp8", "int8"]:
             gms = ipr.ipr_bench_gemm(prec, n, 2, 5, stream)
             rates[prec] = 2.0 * n ** 3 / (gms * 1e-3) / 1e12
-            fracs[prec] = rates[prec] / peaks[prec][0]
+            # fp64oz: FP64-equivalent TFLOP/s; its tensor-core fraction is that of the 45 INT8
+            # digit products against the INT8 peak
+            fracs[prec] = rates[prec] * (45.0 if prec == "fp64oz" else 1.0) / peaks[prec][0]
         extras["gemm_tflops"] = rates
         extras["gemm_frac_of_peak"] = fracs
         extras["gemm_peaks"] = {k: {"tflops": v[0], "source": v[1]} for k, v in peaks.items()}

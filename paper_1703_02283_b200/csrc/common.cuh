@@ -18,8 +18,13 @@ enum Prec { P_FP64 = 0, P_TF32 = 1, P_BF16 = 2, P_FP16 = 3, P_FP8 = 4, P_INT8 = 
 
 // FP64 storage/operand format (P_FP64_OZ: FP64 values, GEMMs emulated on INT8 tensor cores)
 __host__ __device__ inline bool is_f64(int prec) { return prec == P_FP64 || prec == P_FP64_OZ; }
-// Ozaki scheme I (reading R-23): digits per operand; a product keeps the slice pairs s + t <= S + 1
+// Ozaki scheme I (reading R-23): at most OZ_S digits per operand (a product keeps the digit pairs
+// s + t <= S + 1); an FP64_OZ phase storing m mantissa bits uses S = oz_digits(m) <= OZ_S
 constexpr int OZ_S = 9;
+__host__ __device__ inline int oz_digits(int m) {
+  const int s = (m + 12 + 6) / 7;
+  return s < 2 ? 2 : s > OZ_S ? OZ_S : s;
+}
 
 // Operand formats that carry a per-tensor power-of-two scale 2^sigma (reading R-20; NEXT-3).
 __host__ __device__ inline bool is_scaled(int prec) { return prec == P_FP16 || prec == P_FP8 || prec == P_INT8; }
@@ -72,9 +77,9 @@ struct GemmArgs {
   // EPI_STORE_N
   void *nout; int64_t ldn;
   // EPI_OZACC (FP64 accumulator stored transposed), and the Ozaki operands of a P_FP64_OZ GEMM
-  double *ozacc; int64_t ldoz; const int *oz_rsig, *oz_csig; int oz_g, oz_first;
-  const int8_t *oz_a;   // A-role digit planes [OZ_S][npad][npad] (row-major per plane)
-  const int8_t *oz_b;   // B-role digits, per output column j: [OZ_S * npad] = digit planes S..1 of column j
+  double *ozacc; int64_t ldoz; const int *oz_rsig, *oz_csig; int oz_g, oz_first, oz_S;
+  const int8_t *oz_a;   // A-role digit planes [S][npad][npad] (row-major per plane)
+  const int8_t *oz_b;   // B-role digits, per output column j: [S * npad] = digit planes S..1 of column j
 };
 
 // ------------------------------------------------------------------------------------

@@ -298,14 +298,17 @@ ipr_status save_best(ipr_ctx *c) {
 
 ipr_status make_xt(ipr_ctx *c, int i, const PhaseC &P);
 // Ozaki digits of the FP64 iterate in buffer i (exactly symmetric, G = 1: its columns are its rows)
+int oz_S_now(const ipr_ctx *c) { return oz_digits(c->ph[c->phase].m); }
 ipr_status oz_split_chat(ipr_ctx *c, int i) {
-  CK(launch_oz_split((const double *)c->chat[i], c->npad, c->npad, c->npad, c->ozC[i], c->ozCb[i], c->ozC_sig[i], c->st));
+  CK(launch_oz_split((const double *)c->chat[i], c->npad, c->npad, c->npad, oz_S_now(c), c->ozC[i], c->ozCb[i],
+                     c->ozC_sig[i], c->st));
   return IPR_OK;
 }
 // Ozaki operands of a GEMM: A = the iterate buffer i's digits (or Ahat's if i < 0), B = digits of
 // the rows of the K-major B operand Xt (npad x npad FP64), split now into the scratch set
 ipr_status oz_operands(ipr_ctx *c, GemmArgs &g, int i, const void *Xt) {
-  CK(launch_oz_split((const double *)Xt, c->npad, c->npad, c->npad, nullptr, c->ozB, c->ozB_sig, c->st));
+  CK(launch_oz_split((const double *)Xt, c->npad, c->npad, c->npad, oz_S_now(c), nullptr, c->ozB, c->ozB_sig, c->st));
+  g.oz_S = oz_S_now(c);
   g.oz_a = i < 0 ? c->ozA : c->ozC[i];
   g.oz_rsig = i < 0 ? c->ozA_sig : c->ozC_sig[i];
   g.oz_b = c->ozB; g.oz_csig = c->ozB_sig;
@@ -350,7 +353,8 @@ ipr_status begin_phase(ipr_ctx *c, bool first) {
   }
   CKS(make_operand(c, c->cur, P));
   if (P.prec == IPR_FP64_OZ) {   // digits of Ahat (A role) and of Chat (both roles; G = 1, symmetric)
-    CK(launch_oz_split((const double *)c->Aop, c->npad, c->npad, c->npad, c->ozA, nullptr, c->ozA_sig, c->st));
+    CK(launch_oz_split((const double *)c->Aop, c->npad, c->npad, c->npad, oz_digits(P.m), c->ozA, nullptr, c->ozA_sig,
+                       c->st));
     CKS(oz_split_chat(c, c->cur));
   }
   if (c->form == IPR_FORM_NEWTON_SCHULZ) CKS(make_xt(c, c->cur, P));
@@ -432,7 +436,7 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
       if (prec == IPR_FP64_OZ) {
         if (j == 1) {   // Ahat (A role) x Chat (B role: its rows, by symmetry)
           g.oz_a = c->ozA; g.oz_rsig = c->ozA_sig; g.oz_b = c->ozCb[c->cur]; g.oz_csig = c->ozC_sig[c->cur];
-          g.ozacc = c->ozacc; g.ldoz = c->npad;
+          g.ozacc = c->ozacc; g.ldoz = c->npad; g.oz_S = oz_S_now(c);
         } else {
           CKS(oz_operands(c, g, c->cur, c->T[(j - 1) & 1]));
         }
@@ -934,14 +938,13 @@ ipr_status ipr_get_iterate(ipr_ctx *c, int which, double *C_dev_out, int64_t ldc
 // chain: X_1 = C (C A) [B = Zr row-major], X_j = C X_{j-1}; p - 1 DMMA GEMMs, the last with the
 // residual partials (reading R-3; same arithmetic class as certify_best).
 static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho) {
+  // certification always multiplies on the FP64 DMMA pipe (also after an IPR_FP64_OZ phase)
   const void *X = c->Zr;
-  const int prec = c->ph[c->phase].prec == IPR_FP64_OZ ? IPR_FP64_OZ : IPR_FP64;
   for (int j = 2; j <= c->p; ++j) {
-    GemmArgs g = base_args(c, prec, X);
-    chat_view(c, i, prec, &g.A, &g.a_kp, &g.a_pstride);
+    GemmArgs g = base_args(c, IPR_FP64, X);
+    chat_view(c, i, IPR_FP64, &g.A, &g.a_kp, &g.a_pstride);
     g.mode = EPI_STORE_T | (j == c->p ? EPI_RESID : 0);
     g.tout = c->T[j & 1]; g.ldt = c->npad; g.part = c->part;
-    if (prec == IPR_FP64_OZ) CKS(oz_operands(c, g, i, X));
     CK(run_gemm(c, g));
     X = c->T[j & 1];
   }
@@ -1057,9 +1060,9 @@ ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_
     if (e == cudaSuccess) e = cudaMalloc(&ob, (size_t)(np * np) * OZ_S);
     if (e == cudaSuccess) e = cudaMalloc(&sig, (size_t)np * 8);
     if (e == cudaSuccess) e = cudaMalloc(&acc, (size_t)(np * np) * 8);
-    if (e == cudaSuccess) e = launch_oz_split((const double *)X, np, np, np, oa, nullptr, sig, s);
-    if (e == cudaSuccess) e = launch_oz_split((const double *)Y, np, np, np, nullptr, ob, sig + np, s);
-    g.oz_a = oa; g.oz_rsig = sig; g.oz_b = ob; g.oz_csig = sig + np; g.ozacc = acc; g.ldoz = np;
+    if (e == cudaSuccess) e = launch_oz_split((const double *)X, np, np, np, OZ_S, oa, nullptr, sig, s);
+    if (e == cudaSuccess) e = launch_oz_split((const double *)Y, np, np, np, OZ_S, nullptr, ob, sig + np, s);
+    g.oz_a = oa; g.oz_rsig = sig; g.oz_b = ob; g.oz_csig = sig + np; g.ozacc = acc; g.ldoz = np; g.oz_S = OZ_S;
     if (e == cudaSuccess) e = launch_gemm_ozaki(g, s);
   } else {
     e = prec == IPR_FP64 ? launch_gemm_dmma(g, s) : launch_gemm_tc(g, s);
@@ -1116,13 +1119,13 @@ ipr_status ipr_bench_gemm_epi(int prec, int64_t n, int warmup, int iters, int ep
     if (e == cudaSuccess) e = cudaMalloc(&ob, (size_t)(np * np) * OZ_S);
     if (e == cudaSuccess) e = cudaMalloc(&sig, (size_t)np * 8);
     if (e == cudaSuccess) e = cudaMalloc(&acc, (size_t)(np * np) * 8);
-    if (e == cudaSuccess) e = launch_oz_split((const double *)X, np, np, np, oa, nullptr, sig, s);
-    g.oz_a = oa; g.oz_rsig = sig; g.oz_b = ob; g.oz_csig = sig + np; g.ozacc = acc; g.ldoz = np;
+    if (e == cudaSuccess) e = launch_oz_split((const double *)X, np, np, np, OZ_S, oa, nullptr, sig, s);
+    g.oz_a = oa; g.oz_rsig = sig; g.oz_b = ob; g.oz_csig = sig + np; g.ozacc = acc; g.ldoz = np; g.oz_S = OZ_S;
     g.mode = mode ? EPI_STORE_T : 0;
   }
   auto run = [&]() {
     if (prec == IPR_FP64_OZ) {
-      cudaError_t r = launch_oz_split((const double *)Y, np, np, np, nullptr, ob, sig + np, s);
+      cudaError_t r = launch_oz_split((const double *)Y, np, np, np, OZ_S, nullptr, ob, sig + np, s);
       return r == cudaSuccess ? launch_gemm_ozaki(g, s) : r;
     }
     return prec == IPR_FP64 ? launch_gemm_dmma(g, s) : launch_gemm_tc(g, s);

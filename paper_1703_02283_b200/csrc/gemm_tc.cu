@@ -194,8 +194,19 @@ __device__ __forceinline__ double acc_to_f64(uint32_t w) {
 }
 
 struct TileSched {      // pair tiles: tiles_m pair-rows (256 rows) x tiles_n (256 columns)
-  int tiles_m, tiles_n;
+  int tiles_m, tiles_n, tri;
+  // tri (square, symmetric-tri GEMM 2): only the upper-triangle pair tiles tm <= tn, column by
+  // column, so the persistent CTA pairs share the work evenly
+  __host__ __device__ int count() const { return tri ? tiles_n * (tiles_n + 1) / 2 : tiles_m * tiles_n; }
   __device__ void get(int t, int &tm, int &tn) const {
+    if (tri) {
+      int c = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+      while (c * (c + 1) / 2 > t) --c;
+      while ((c + 1) * (c + 2) / 2 <= t) ++c;
+      tn = c;
+      tm = t - c * (c + 1) / 2;
+      return;
+    }
     const int per_group = TC_GROUP_M * tiles_n;
     const int gidx = t / per_group, first_m = gidx * TC_GROUP_M;
     const int gm = min(tiles_m - first_m, TC_GROUP_M);
@@ -371,8 +382,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN)};
-  const int ntiles = sch.tiles_m * sch.tiles_n;
+  const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN), g.tri};
+  const int ntiles = sch.count();
   const int esz = elt_size(g.prec);
   const int nkb = (int)(g.K * esz / TC_BKB);
   const int bke = TC_BKB / esz;                       // K elements per block
@@ -399,7 +410,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       for (int t = pair; t < ntiles; t += npairs) {
         int tm, tn;
         sch.get(t, tm, tn);
-        if (g.tri && tm > tn) continue;                // pair tile wholly below the diagonal
         const int arow = tm * 2 * TC_BM + (int)rank * TC_BM;
         const int brow = tn * TC_BN + (int)rank * (TC_BN / 2);
         for (int kb = 0; kb < nkb; ++kb) {
@@ -421,11 +431,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int t = pair; t < ntiles; t += npairs) {
-        {
-          int tm, tn;
-          sch.get(t, tm, tn);
-          if (g.tri && tm > tn) continue;
-        }
         const int buf = it & 1;
         mbar_wait_cluster(&tempty[buf], ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -455,11 +460,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
     for (int t = pair; t < ntiles; t += npairs) {
       int tm, tn;
       sch.get(t, tm, tn);
-      if (g.tri && tm > tn) {   // skipped pair tile: its residual partials are zero
-        if (et == 0 && (g.mode & EPI_RESID))
-          g.part[((g.col0 + (int64_t)tn * TC_BN) / TC_BN) * g.tiles_m + tm * 2 + (int)rank] = 0.0;
-        continue;
-      }
       const int buf = it & 1;
       mbar_wait(&tfull[buf], (it >> 1) & 1);
       tc_fence_after();
@@ -592,7 +592,16 @@ cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
       return cudaErrorInvalidValue;
     }
   }
-  const int ntiles = (int)((a.M / (2 * TC_BM)) * (a.N / TC_BN));
+  if (a.tri && (a.M != a.N || a.col0 != 0)) {
+    snprintf(g_tc_err, sizeof g_tc_err, "tcgen05 GEMM: tri needs a square single-panel product");
+    return cudaErrorInvalidValue;
+  }
+  const TileSched hs{(int)(a.M / (2 * TC_BM)), (int)(a.N / TC_BN), a.tri};
+  const int ntiles = hs.count();
+  if (a.tri && (a.mode & EPI_RESID)) {   // the tiles below the diagonal are not visited: zero partials
+    cudaError_t z = cudaMemsetAsync(a.part, 0, (size_t)(a.N / TC_BN) * a.tiles_m * sizeof(double), s);
+    if (z != cudaSuccess) return z;
+  }
   const int maxpairs = num_sms() / 2;
   const int grid = 2 * (ntiles < maxpairs ? ntiles : maxpairs);
   cudaError_t e = cudaSuccess;

@@ -29,8 +29,8 @@ cudaError_t launch_transpose(const void *src, int64_t rows, int64_t cols, int es
 cudaError_t launch_sym_update(const void *cold, int cont64, void *cnew, const void *W, int w64, int64_t npad,
                               int64_t kp, int64_t col0, int p, int m, int rtz, int prec, void *chat_new, int corr,
                               void *chat_corr_new, double *part, cudaStream_t s);
-cudaError_t launch_oz_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int8_t *planes, int8_t *bcat,
-                            int *sig, cudaStream_t s);
+cudaError_t launch_oz_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int S, int8_t *planes,
+                            int8_t *bcat, int *sig, cudaStream_t s);
 cudaError_t launch_fill_operand(void *dst, int64_t count, int prec, uint32_t seed, cudaStream_t s);
 cudaError_t launch_test_quant(int mode, const void *in, void *out, int64_t len, int m, int rtz, int sigma,
                               cudaStream_t s);

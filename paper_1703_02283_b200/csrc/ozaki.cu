@@ -11,10 +11,13 @@
 //   combine   Z_ij = sum_g 2^(sig_i + tau_j - 7g) P_g,ij, in FP64, smallest groups first
 //   finish    the hot path's FP64 epilogue (store / residual / update partials, epilogue.cuh) on Z
 //
+// An FP64_OZ phase storing m mantissa bits uses S = oz_digits(m) = ceil((m + 12) / 7) digits
+// (clamped to 2..9): the arithmetic keeps ~12 bits more than the storage.
 // S = 9 keeps 63 bits per operand relative to its row / column maximum; the dropped pairs
 // (s + t > S + 1) and the digit remainder are below the FP64 GEMM's own rounding at the orders
-// used here (measured: Frobenius error 9e-16 vs 8.6e-15 for an FP64 GEMM at n = 512; the oracle's
-// tests/test_oracle... pin the scheme on the CPU).  K-work: S(S+1)/2 = 45 int8 GEMMs of order n.
+// used here (measured in NumPy against 80-bit long double: Frobenius error 9e-16 vs 8.6e-15 for an
+// FP64 GEMM at n = 512; tests/test_gpu_ozaki.py asserts "no worse than 2x DMMA" on the GPU).
+// K-work: S(S+1)/2 = 45 int8 GEMMs of order n.
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "kernels.h"
@@ -26,7 +29,7 @@ namespace ipr {
 //   bcat   (B role, may be NULL): digit s of x_rk at bcat[r * S * cols + (S - s) * cols + k]
 //   sig[r]: the row's scale exponent
 __global__ void __launch_bounds__(256) k_oz_split(const double *__restrict__ X, int64_t ld, int64_t rows,
-                                                  int64_t cols, int8_t *planes, int8_t *bcat, int *sig) {
+                                                  int64_t cols, int S, int8_t *planes, int8_t *bcat, int *sig) {
   __shared__ double red[8];
   const int64_t r = blockIdx.x;
   const double *x = X + r * ld;
@@ -48,14 +51,13 @@ __global__ void __launch_bounds__(256) k_oz_split(const double *__restrict__ X, 
   const double sc = pow2(-sg);
   for (int64_t k = threadIdx.x; k < cols; k += blockDim.x) {
     double v = __dmul_rn(x[k], sc);
-    #pragma unroll
-    for (int s = 1; s <= OZ_S; ++s) {
+    for (int s = 1; s <= S; ++s) {
       v = __dmul_rn(v, 128.0);
       const double d = rint(v);
       v = __dsub_rn(v, d);
       const int8_t di = (int8_t)(int)d;
       if (planes) planes[(int64_t)(s - 1) * rows * cols + r * cols + k] = di;
-      if (bcat) bcat[r * OZ_S * cols + (int64_t)(OZ_S - s) * cols + k] = di;
+      if (bcat) bcat[r * S * cols + (int64_t)(S - s) * cols + k] = di;
     }
   }
 }
@@ -84,9 +86,10 @@ __global__ void __launch_bounds__(128) k_oz_finish(const GemmArgs g) {
   }
 }
 
-cudaError_t launch_oz_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int8_t *planes, int8_t *bcat,
-                            int *sig, cudaStream_t s) {
-  k_oz_split<<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, planes, bcat, sig);
+cudaError_t launch_oz_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int S, int8_t *planes,
+                            int8_t *bcat, int *sig, cudaStream_t s) {
+  if (S < 2 || S > OZ_S) return cudaErrorInvalidValue;
+  k_oz_split<<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, S, planes, bcat, sig);
   ++g_launches;
   return cudaGetLastError();
 }
@@ -95,15 +98,17 @@ cudaError_t launch_oz_split(const double *X, int64_t ld, int64_t rows, int64_t c
 // g.oz_csig those of Y (B role, per output column); g.ozacc is the FP64 accumulator (transposed,
 // ldoz); then the epilogue g.mode runs in k_oz_finish.  Single panel (G = 1): M = N = K = npad.
 cudaError_t launch_gemm_ozaki(const GemmArgs &g, cudaStream_t s) {
-  if (!g.oz_a || !g.oz_b || !g.oz_rsig || !g.oz_csig || !g.ozacc || g.M != g.K || g.N != g.K) return cudaErrorInvalidValue;
+  const int S = g.oz_S;
+  if (!g.oz_a || !g.oz_b || !g.oz_rsig || !g.oz_csig || !g.ozacc || g.M != g.K || g.N != g.K || S < 2 || S > OZ_S)
+    return cudaErrorInvalidValue;
   const int64_t np = g.K;
-  for (int gi = OZ_S + 1; gi >= 2; --gi) {
+  for (int gi = S + 1; gi >= 2; --gi) {
     GemmArgs q = g;
     q.prec = P_INT8; q.tprec = P_INT8;
     q.A = g.oz_a; q.a_kp = np; q.a_pstride = np * np;
     q.K = (int64_t)(gi - 1) * np;
-    q.B = g.oz_b + (int64_t)(OZ_S - gi + 1) * np; q.ldb = (int64_t)OZ_S * np;
-    q.mode = EPI_OZACC; q.oz_g = gi; q.oz_first = gi == OZ_S + 1;
+    q.B = g.oz_b + (int64_t)(S - gi + 1) * np; q.ldb = (int64_t)S * np;
+    q.mode = EPI_OZACC; q.oz_g = gi; q.oz_first = gi == S + 1;
     q.sigA = nullptr; q.sigB = nullptr; q.pmax = nullptr; q.part = nullptr;
     cudaError_t e = launch_gemm_tc(q, s);
     if (e != cudaSuccess) return e;
