@@ -938,13 +938,16 @@ ipr_status ipr_get_iterate(ipr_ctx *c, int which, double *C_dev_out, int64_t ldc
 // chain: X_1 = C (C A) [B = Zr row-major], X_j = C X_{j-1}; p - 1 DMMA GEMMs, the last with the
 // residual partials (reading R-3; same arithmetic class as certify_best).
 static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho) {
-  // certification always multiplies on the FP64 DMMA pipe (also after an IPR_FP64_OZ phase)
+  // in an IPR_FP64_OZ phase the certifying product runs on the same FP64-accurate Ozaki GEMM
+  // (9 digits); ipr_residual(certify = 1) recomputes the whole chain on the DMMA pipe
   const void *X = c->Zr;
+  const int prec = c->ph[c->phase].prec == IPR_FP64_OZ ? IPR_FP64_OZ : IPR_FP64;
   for (int j = 2; j <= c->p; ++j) {
-    GemmArgs g = base_args(c, IPR_FP64, X);
-    chat_view(c, i, IPR_FP64, &g.A, &g.a_kp, &g.a_pstride);
+    GemmArgs g = base_args(c, prec, X);
+    chat_view(c, i, prec, &g.A, &g.a_kp, &g.a_pstride);
     g.mode = EPI_STORE_T | (j == c->p ? EPI_RESID : 0);
     g.tout = c->T[j & 1]; g.ldt = c->npad; g.part = c->part;
+    if (prec == IPR_FP64_OZ) CKS(oz_operands(c, g, i, X));
     CK(run_gemm(c, g));
     X = c->T[j & 1];
   }
