@@ -49,15 +49,28 @@ __global__ void __launch_bounds__(256) k_oz_split(const double *__restrict__ X, 
   const int sg = (mx > 0.0) ? ilogb(mx * (128.0 / 127.0)) + 1 : 0;
   if (threadIdx.x == 0) sig[r] = sg;
   const double sc = pow2(-sg);
-  for (int64_t k = threadIdx.x; k < cols; k += blockDim.x) {
-    double v = __dmul_rn(x[k], sc);
+  // 8 consecutive elements per thread: every digit plane gets one 8-byte store per thread
+  // (cols is a multiple of 256, so k0 + 8 <= cols and the stores are 8-byte aligned)
+  for (int64_t k0 = (int64_t)threadIdx.x * 8; k0 < cols; k0 += (int64_t)blockDim.x * 8) {
+    double v[8];
+    const double2 *xp = (const double2 *)(x + k0);
+    #pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double2 t = xp[u];
+      v[2 * u] = __dmul_rn(t.x, sc);
+      v[2 * u + 1] = __dmul_rn(t.y, sc);
+    }
     for (int s = 1; s <= S; ++s) {
-      v = __dmul_rn(v, 128.0);
-      const double d = rint(v);
-      v = __dsub_rn(v, d);
-      const int8_t di = (int8_t)(int)d;
-      if (planes) planes[(int64_t)(s - 1) * rows * cols + r * cols + k] = di;
-      if (bcat) bcat[r * S * cols + (int64_t)(S - s) * cols + k] = di;
+      uint64_t w = 0;
+      #pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        v[u] = __dmul_rn(v[u], 128.0);
+        const double d = rint(v[u]);
+        v[u] = __dsub_rn(v[u], d);
+        w |= (uint64_t)(uint8_t)(int8_t)(int)d << (8 * u);
+      }
+      if (planes) *(uint64_t *)(planes + (int64_t)(s - 1) * rows * cols + r * cols + k0) = w;
+      if (bcat) *(uint64_t *)(bcat + r * S * cols + (int64_t)(S - s) * cols + k0) = w;
     }
   }
 }
@@ -70,15 +83,28 @@ __global__ void __launch_bounds__(128) k_oz_finish(const GemmArgs g) {
   const int64_t tile = ((g.col0 + n0) / 64) * g.tiles_m + tm;
   const int mode = g.mode;
   __shared__ double red[4];
+  __shared__ double stn[32][129];                 // EPI_STORE_N staging: 32 columns x 128 rows
   if (g.tri && m0 > g.col0 + n0 + 63) {          // wholly below the diagonal: not computed
     if (threadIdx.x == 0 && (mode & EPI_RESID)) g.part[tile] = 0.0;
     return;
   }
   const int64_t row = m0 + threadIdx.x;
   EpiAcc ea{0.0, 0.0, 0.0f};
-  for (int c = 0; c < 64; ++c) {
-    const double v = g.ozacc[(n0 + c) * g.ldoz + row];
-    epi_element<-1>(g, row, n0 + c, v, ea);
+  GemmArgs gl = g;
+  gl.mode = mode & ~EPI_STORE_N;                  // the row-major copy goes through shared memory
+  for (int h = 0; h < 2; ++h) {
+    for (int c = 0; c < 32; ++c) {
+      const double v = g.ozacc[(n0 + h * 32 + c) * g.ldoz + row];
+      epi_element<-1>(gl, row, n0 + h * 32 + c, v, ea);
+      if (mode & EPI_STORE_N) stn[c][threadIdx.x] = v;
+    }
+    if (mode & EPI_STORE_N) {                     // nout[row][col]: 32 consecutive columns per warp
+      __syncthreads();
+      const int lc = threadIdx.x & 31, r0 = threadIdx.x >> 5;
+      for (int r = r0; r < 128; r += 4)
+        ((double *)g.nout)[(m0 + r) * g.ldn + n0 + h * 32 + lc] = stn[lc][r];
+      __syncthreads();
+    }
   }
   if (mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE)) {
     const double s = block_sum_det<128>((mode & EPI_RESID) ? ea.r2 : ea.d2, red);
