@@ -33,7 +33,7 @@ METRIC = "time-to-FP64-residual 1e-12 (n=8192, p=2)"
 # tensor cores with 5 Ozaki digits, R-23); FP64 refinement (9 Ozaki digits) with a BF16 correction
 # GEMM; convergence certified with FP64 DMMA GEMMs
 DEFAULT_SCHEDULE = "symtri:bf16>fp64oz@23/cbf16>fp64oz/cbf16"
-EXTRA_SCHEDULES = ["fp64", "symtri:bf16>fp64oz/cbf16", "sym:fp64oz", "symtri:fp8>bf16>fp64oz@23/cbf16>fp64oz/cbf16",
+EXTRA_SCHEDULES = ["fp64", "symtri:bf16>fp64oz@a/cbf16", "symtri:bf16>fp64oz/cbf16", "sym:fp64oz", "symtri:fp8>bf16>fp64oz@23/cbf16>fp64oz/cbf16",
                    "bf16>fp64", "tf32>fp64", "fp16>fp64", "sym:fp64", "sym:fp64/cbf16", "symtri:fp64/cbf16",
                    "symtri:bf16>fp64/cbf16", "symtri:bf16>tf32>fp64/cbf16", "symtri:fp8>bf16>fp64/cbf16",
                    "symtri:int8>bf16>fp64/cbf16", "symtri:fp16>fp64/cbf16",
@@ -71,7 +71,7 @@ def parse_schedule(name):
             m, _, corr = m.partition("/c")
             ph = ph + "/c" + corr
         prec, _, corr = ph.partition("/c")
-        parts.append((prec, corr or -1, int(m) if m else -1))
+        parts.append((prec, corr or -1, (-2 if m == "a" else int(m)) if m else -1))   # @a: adaptive (R-26)
     return form, parts
 
 

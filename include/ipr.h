@@ -67,6 +67,15 @@ typedef enum {
 typedef enum { IPR_FP64 = 0, IPR_TF32 = 1, IPR_BF16 = 2, IPR_FP16 = 3, IPR_FP8 = 4, IPR_INT8 = 5,
                IPR_FP64_OZ = 6 } ipr_prec;
 
+/* ipr_phase.mant_bits = IPR_MANT_ADAPTIVE (IPR_FP64_OZ phases only): dynamic precision inside the
+ * phase (reading R-26, "the necessity of increased precision can be detected at
+ * runtime").  Before the chain of C_k the engine picks the Ozaki digits from the residual it
+ * expects for C_{k+1}: target = rho_hat_{k-1} q^2 (q = last in-phase contraction rho_{k-1} /
+ * rho_{k-2} clamped to [1e-3, 1], 0.03 without history), S = clamp(ceil((log2(30 sqrt n) -
+ * log2 target) / 7), 3, 9); C_{k+1} is stored with m = min(52, 7 S - 4) bits.  The first chain of a
+ * run uses S = 9; a phase entry stores C with the bits of the digits its first chain will use. */
+enum { IPR_MANT_ADAPTIVE = -2 };
+
 /* Rounding of the stored iterate (reading R-7: RNE default; RTZ = "bit truncation",
  * PAPER.md:26).  Operand conversions are always round-to-nearest-even (hardware cvt.rn). */
 typedef enum { IPR_RNE = 0, IPR_RTZ = 1 } ipr_round;

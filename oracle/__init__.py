@@ -19,6 +19,7 @@ _SRC = os.path.join(_HERE, "ipr_oracle.c")
 _LIB = os.path.join(_HERE, "libipr_oracle.so")
 
 FP64, TF32, BF16, FP16, FP8, INT8, FP64_OZ = 0, 1, 2, 3, 4, 5, 6
+MANT_ADAPTIVE = -2   # FP64_OZ phases: digits / stored bits chosen per iteration (reading R-26)
 RNE, RTZ = 0, 1
 CONTINUE, CONVERGED, ITER_LIMIT, DIVERGED, NONFINITE, SWITCH = 0, 1, 2, 3, 4, 5
 OUTCOME_NAMES = {0: "running", 1: "converged", 2: "iter_limit", 3: "diverged", 4: "nonfinite",
@@ -91,6 +92,8 @@ def lib():
         L.orc_spectral.argtypes = [C.c_int64, _dp, C.c_int, C.c_double, C.c_int, _dp]
         L.orc_fp16_sigma.argtypes = [C.c_double]
         L.orc_sigma.argtypes = [C.c_int, C.c_double]
+        L.orc_oz_digits.argtypes = [C.c_double, C.c_int64]
+        L.orc_oz_adaptive_m.argtypes = [C.c_int]
         L.orc_q_int8.restype = C.c_double
         L.orc_q_int8.argtypes = [C.c_double]
         L.orc_ctrl_init.argtypes = [C.POINTER(Ctrl), C.c_int64, C.c_int, C.c_double]
@@ -146,6 +149,14 @@ def fp16_sigma(maxabs: float) -> int:
 def sigma(prec: int, maxabs: float) -> int:
     """Scale exponent of the scaled operand formats (FP16 / FP8 / INT8), 0 otherwise."""
     return lib().orc_sigma(prec, maxabs)
+
+
+def oz_digits(rho_hat_target: float, n: int) -> int:
+    return lib().orc_oz_digits(rho_hat_target, n)
+
+
+def oz_adaptive_m(S: int) -> int:
+    return lib().orc_oz_adaptive_m(S)
 
 
 def q_int8(x: float) -> float:

@@ -67,6 +67,29 @@ int orc_native_m(int prec) { int E, M; orc_prec_format(prec, &E, &M); return M; 
 static int phase_m(const orc_phase *ph) {
   return ph->mant_bits < 0 ? orc_native_m(ph->prec) : ph->mant_bits;
 }
+
+/* ---------------------------------------------------------------------------------
+ * Dynamic precision inside an FP64_OZ phase (mant_bits = ORC_MANT_ADAPTIVE; reading R-26).
+ * PAPER.md:256-261 [Sec. 4.3.1]: "the necessity of increased precision can be detected at
+ * runtime".  Before the chain of C_k the GPU picks its Ozaki digit count S_k from the residual it
+ * expects for C_{k+1}, rho_hat_{k-1} q^2 (q = the last in-phase contraction ratio, clamped to
+ * [1e-3, 1], 0.03 without history): S = clamp(ceil((log2(30 sqrt n) - log2 target) / 7), 3, 9);
+ * C_{k+1} is then stored with m = min(52, 7 S - 4) bits.  The oracle's arithmetic stays FP64, so
+ * only that storage rule is mirrored here.
+ * ------------------------------------------------------------------------------ */
+int orc_oz_digits(double rho_hat_target, int64_t n) {
+  if (!(rho_hat_target > 0.0) || !isfinite(rho_hat_target)) return 9;
+  const double b = log2(30.0 * sqrt((double)n)) - log2(rho_hat_target);
+  int S = (int)ceil(b / 7.0);
+  if (S < 3) S = 3;
+  if (S > 9) S = 9;
+  return S;
+}
+int orc_oz_adaptive_m(int S) { return 7 * S - 4 < 52 ? 7 * S - 4 : 52; }
+static int is_adaptive(const orc_phase *ph) {
+  return ph->prec == ORC_FP64_OZ && ph->mant_bits == ORC_MANT_ADAPTIVE;
+}
+static double clampq(double q) { return q < 1e-3 ? 1e-3 : q > 1.0 ? 1.0 : q; }
 /* stored value of a phase: q_m in the container (approximate storage) */
 static double store_q(const orc_phase *ph, double x) {
   return orc_qm(x, orc_container_E(ph->prec), phase_m(ph), ph->round == ORC_RTZ);
@@ -519,8 +542,17 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
   orc_ctrl ctl;
   orc_ctrl_init(&ctl, n, nphases, final_tol);
   int outcome = ORC_CONTINUE;
+  /* R-26 state: last residual (any phase), the last two in-phase residuals, the stored m of C */
+  double last_rho_hat = NAN, ph_r1 = NAN, ph_r2 = NAN;
+  int m_of_C = is_adaptive(&phases[0]) ? 52 : phase_m(&phases[0]);
   for (int k = 0; k < max_total; ++k) {
     const orc_phase *ph = &phases[ctl.phase];
+    orc_phase ph_k = *ph;             /* the phase with this iteration's storage bits */
+    if (is_adaptive(ph)) {
+      const double q = (isfinite(ph_r1) && isfinite(ph_r2) && ph_r2 > 0.0) ? clampq(ph_r1 / ph_r2) : 0.03;
+      const int S = k == 0 ? 9 : orc_oz_digits(last_rho_hat * q * q, n);
+      ph_k.mant_bits = orc_oz_adaptive_m(S);
+    }
     if (C_hist && k < hist_cap) memcpy(C_hist + (int64_t)k * nn, C, (size_t)nn * sizeof(double));
     const double rho = form == ORC_FORM_NEWTON_SCHULZ ? chain_ns(n, A, C, ph, &w)
                        : sym ? chain_sym(n, p, form == ORC_FORM_SYMMETRIC_TRI, A, C, ph, &w)
@@ -529,7 +561,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
     int d = orc_ctrl_decide(&ctl, ph, rho);
     if (ctl.best_is_new) memcpy(C_best, C, (size_t)nn * sizeof(double));
     orc_record r;
-    r.k = k; r.phase = phase_now; r.prec = ph->prec; r.mant_bits = phase_m(ph);
+    r.k = k; r.phase = phase_now; r.prec = ph->prec; r.mant_bits = m_of_C;
     r.decision = d; r.rho = rho; r.rho_hat = rho / sqrt((double)n); r.delta = NAN;
     r.gamma = (gamma_normA2 > 0) ? gamma_of(n, C, A, gamma_normA2, g1, g2) : NAN;
     r.rho_cert = NAN;
@@ -537,23 +569,33 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
       /* rho_s = ||I - C^{p-1} A C||_F is not the north-star residual: certify
        * ||I - C^p A||_F with the FP64 literal chain (reading R-3); if it misses final_tol the
        * iteration continues from the update computed first (as the GPU engine does). */
-      r.delta = update_sym(n, p, C, ph, &w, Cn);
+      r.delta = update_sym(n, p, C, &ph_k, &w, Cn);
       const orc_phase ph64 = {ORC_FP64, -1, ORC_RNE, 0.0, 0.0, 0.0, 0, -1};
       r.rho_cert = chain(n, p, A, C, &ph64, &w);
       if (!(r.rho_cert <= final_tol)) {
         d = ORC_CONTINUE;
         r.decision = d;
         double *t = C; C = Cn; Cn = t;
+        m_of_C = phase_m(&ph_k);
       }
     } else if (d == ORC_CONTINUE) {
       r.delta = form == ORC_FORM_NEWTON_SCHULZ ? update_ns(n, C, ph, &w, Cn)
-                : sym                           ? update_sym(n, p, C, ph, &w, Cn)
+                : sym                           ? update_sym(n, p, C, &ph_k, &w, Cn)
                                                 : update(n, p, C, ph, &w, Cn);
       double *t = C; C = Cn; Cn = t;
+      m_of_C = phase_m(&ph_k);
     } else if (d == ORC_SWITCH) {
       orc_ctrl_enter_next_phase(&ctl);
-      recontainer(nn, C_best, &phases[ctl.phase], C);
+      orc_phase pe = phases[ctl.phase];
+      if (is_adaptive(&pe))   /* entry storage from the digits the entering chain will use */
+        pe.mant_bits = orc_oz_adaptive_m(orc_oz_digits(rho / sqrt((double)n) * 0.03 * 0.03, n));
+      recontainer(nn, C_best, &pe, C);
+      m_of_C = phase_m(&pe);
     }
+    /* R-26 bookkeeping */
+    last_rho_hat = rho / sqrt((double)n);
+    if (d == ORC_SWITCH) { ph_r1 = NAN; ph_r2 = NAN; }
+    else { ph_r2 = ph_r1; ph_r1 = rho; }
     if (*nrec < cap_rec) rec[*nrec] = r;
     *nrec += 1;
     if (d != ORC_CONTINUE && d != ORC_SWITCH) { outcome = d; break; }

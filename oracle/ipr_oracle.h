@@ -149,6 +149,13 @@ int orc_fp16_sigma(double maxabs);
 /* Scale exponent of the scaled operand formats: FP16 (as above), FP8 E4M3 and INT8 (scaled max
  * in [2^6, 2^7)); 0 otherwise.  INT8 quantiser: nearest-even integer saturated to +-127. */
 int orc_sigma(int prec, double maxabs);
+
+/* Dynamic precision inside an FP64_OZ phase (reading R-26): mant_bits = ORC_MANT_ADAPTIVE picks
+ * the Ozaki digit count per iteration from the expected residual and stores C with
+ * orc_oz_adaptive_m(S) = min(52, 7 S - 4) bits. */
+enum { ORC_MANT_ADAPTIVE = -2 };
+int orc_oz_digits(double rho_hat_target, int64_t n);
+int orc_oz_adaptive_m(int S);
 double orc_q_int8(double x);
 
 #ifdef __cplusplus

@@ -21,6 +21,7 @@ IPR_OK, IPR_E_INVALID_ARG, IPR_E_NOT_SYMMETRIC, IPR_E_STATE = 0, 1, 2, 3
 IPR_E_UNSUPPORTED, IPR_E_OOM, IPR_E_CUDA, IPR_E_NCCL = 4, 5, 6, 7
 IPR_FP64, IPR_TF32, IPR_BF16, IPR_FP16, IPR_FP8, IPR_INT8, IPR_FP64_OZ = 0, 1, 2, 3, 4, 5, 6
 IPR_RNE, IPR_RTZ = 0, 1
+IPR_MANT_ADAPTIVE = -2   # IPR_FP64_OZ phases: Ozaki digits / stored bits chosen per iteration (R-26)
 IPR_RUNNING, IPR_CONVERGED, IPR_ITER_LIMIT, IPR_DIVERGED, IPR_NONFINITE = 0, 1, 2, 3, 4
 IPR_DEC_CONTINUE, IPR_DEC_SWITCH = 0, 5
 PREC_NAMES = {IPR_FP64: "fp64", IPR_TF32: "tf32", IPR_BF16: "bf16", IPR_FP16: "fp16", IPR_FP8: "fp8",

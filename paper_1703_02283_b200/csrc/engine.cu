@@ -36,6 +36,7 @@ thread_local std::string t_err;
 
 struct PhaseC {
   int prec, m, rtz, cont64;
+  int adaptive;                // FP64_OZ with mant_bits = IPR_MANT_ADAPTIVE (reading R-26)
   int corr;                    // symmetric form: operand format of the correction GEMM
   double switch_tol, plateau_ratio, plateau_arm;
   int max_iters;
@@ -78,6 +79,10 @@ struct ipr_ctx {
   int *ozA_sig = nullptr, *ozC_sig[2] = {nullptr, nullptr}, *ozB_sig = nullptr;
   double *ozacc = nullptr;
   int zr_for = -1;                      // iterate buffer whose chain wrote Zr (-1: none)
+  // dynamic precision inside an FP64_OZ phase (R-26): digits of this chain, stored bits of the
+  // next iterate and of the current one, the last two in-phase residuals
+  int oz_S_cur = OZ_S, oz_m_next = 52, m_of_cur = 52;
+  double ph_r1 = NAN, ph_r2 = NAN;
   int form = IPR_FORM_LITERAL;          // iteration form (ipr_set_form)
   float *tscr = nullptr;                // FP16 phase T scratch (FP32)
   double *full64 = nullptr;             // FP64 npad x npad scratch (copy-out / certify)
@@ -298,16 +303,28 @@ ipr_status save_best(ipr_ctx *c) {
 
 ipr_status make_xt(ipr_ctx *c, int i, const PhaseC &P);
 // Ozaki digits of the FP64 iterate in buffer i (exactly symmetric, G = 1: its columns are its rows)
-int oz_S_now(const ipr_ctx *c) { return oz_digits(c->ph[c->phase].m); }
-ipr_status oz_split_chat(ipr_ctx *c, int i) {
-  CK(launch_oz_split((const double *)c->chat[i], c->npad, c->npad, c->npad, oz_S_now(c), c->ozC[i], c->ozCb[i],
+// R-26: digits for a target RMS residual, and the stored bits that go with them
+int oz_digits_for(double rho_hat_target, int64_t n) {
+  if (!(rho_hat_target > 0.0) || !std::isfinite(rho_hat_target)) return OZ_S;
+  const double b = std::log2(30.0 * std::sqrt((double)n)) - std::log2(rho_hat_target);
+  int S = (int)std::ceil(b / 7.0);
+  return S < 3 ? 3 : S > OZ_S ? OZ_S : S;
+}
+int oz_adaptive_m(int S) { return 7 * S - 4 < 52 ? 7 * S - 4 : 52; }
+// digits of the current chain's products: fixed per phase (m), or per iteration (R-26)
+int oz_S_now(const ipr_ctx *c) {
+  const PhaseC &P = c->ph[c->phase];
+  return P.adaptive ? c->oz_S_cur : oz_digits(P.m);
+}
+ipr_status oz_split_chat(ipr_ctx *c, int i) {   // always all OZ_S digits; a product uses the leading S
+  CK(launch_oz_split((const double *)c->chat[i], c->npad, c->npad, c->npad, OZ_S, c->ozC[i], c->ozCb[i],
                      c->ozC_sig[i], c->st));
   return IPR_OK;
 }
 // Ozaki operands of a GEMM: A = the iterate buffer i's digits (or Ahat's if i < 0), B = digits of
 // the rows of the K-major B operand Xt (npad x npad FP64), split now into the scratch set
 ipr_status oz_operands(ipr_ctx *c, GemmArgs &g, int i, const void *Xt) {
-  CK(launch_oz_split((const double *)Xt, c->npad, c->npad, c->npad, oz_S_now(c), nullptr, c->ozB, c->ozB_sig, c->st));
+  CK(launch_oz_split((const double *)Xt, c->npad, c->npad, c->npad, OZ_S, nullptr, c->ozB, c->ozB_sig, c->st));
   g.oz_S = oz_S_now(c);
   g.oz_a = i < 0 ? c->ozA : c->ozC[i];
   g.oz_rsig = i < 0 ? c->ozA_sig : c->ozC_sig[i];
@@ -342,19 +359,23 @@ ipr_status begin_phase(ipr_ctx *c, bool first) {
     CK(launch_stage_a(c->A, c->lda, c->n, c->npad, 0, c->npad, P.prec, P.cont64, P.m, P.rtz,
                       is_scaled(P.prec) ? c->dsig + 0 : nullptr, c->Afull, c->st));
   }
+  // stored bits of the entering iterate; R-26: those of the digits its first chain will use
+  int m_in = P.m;
+  if (P.adaptive && !first) m_in = oz_adaptive_m(oz_digits_for(c->last_rho / std::sqrt((double)c->n) * 0.03 * 0.03, c->n));
+  c->m_of_cur = m_in;
+  c->ph_r1 = NAN; c->ph_r2 = NAN;
   if (first) {
-    CK(launch_c0(c->A, c->lda, c->n, c->npad, c->col0, c->kp, c->norms[3], P.cont64, P.m, P.rtz,
+    CK(launch_c0(c->A, c->lda, c->n, c->npad, c->col0, c->kp, c->norms[3], P.cont64, m_in, P.rtz,
                  cont_ptr(c, c->cur, P), c->st));
   } else {
     CKS(save_best(c));
     if (c->best_loc == 2) {
-      CK(launch_f64_to_cont(c->best, c->npad * c->kp, P.cont64, P.m, P.rtz, cont_ptr(c, c->cur, P), c->st));
+      CK(launch_f64_to_cont(c->best, c->npad * c->kp, P.cont64, m_in, P.rtz, cont_ptr(c, c->cur, P), c->st));
     }
   }
   CKS(make_operand(c, c->cur, P));
   if (P.prec == IPR_FP64_OZ) {   // digits of Ahat (A role) and of Chat (both roles; G = 1, symmetric)
-    CK(launch_oz_split((const double *)c->Aop, c->npad, c->npad, c->npad, oz_digits(P.m), c->ozA, nullptr, c->ozA_sig,
-                       c->st));
+    CK(launch_oz_split((const double *)c->Aop, c->npad, c->npad, c->npad, OZ_S, c->ozA, nullptr, c->ozA_sig, c->st));
     CKS(oz_split_chat(c, c->cur));
   }
   if (c->form == IPR_FORM_NEWTON_SCHULZ) CKS(make_xt(c, c->cur, P));
@@ -401,6 +422,12 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
       CK(launch_scale_op(c->tscr, c->kp * c->npad, c->dsig + 4, prec, c->T[1], c->st));
     }
   }
+  if (is_sym(c) && P.adaptive) {   // R-26: this chain's digits and the next iterate's stored bits
+    const double q = (std::isfinite(c->ph_r1) && std::isfinite(c->ph_r2) && c->ph_r2 > 0.0)
+                         ? std::fmin(std::fmax(c->ph_r1 / c->ph_r2, 1e-3), 1.0) : 0.03;
+    c->oz_S_cur = c->trace.empty() ? OZ_S : oz_digits_for(c->last_rho / std::sqrt((double)c->n) * q * q, c->n);
+    c->oz_m_next = oz_adaptive_m(c->oz_S_cur);
+  }
   if (is_sym(c)) {
     // Z_1 = Ahat Chat (A operand: Ahat row-major; B: Chat itself for G = 1 -- exactly symmetric --
     // else the transposed local panel), Z_j = Chat qin(Z_{j-1}); GEMM p: R = I - Z_p in the
@@ -422,7 +449,8 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
         // FP64 last phase (G = 1): also keep Z_1 = A C row-major -- the B operand of C (C A), so
         // certifying ||I - C^p A||_F costs p - 1 GEMMs instead of p
         c->zr_for = -1;
-        if (c->Zr && is_f64(prec) && P.m == 52 && c->phase == (int)c->ph.size() - 1) {
+        const bool full = P.adaptive ? c->oz_S_cur == OZ_S : P.m == 52;
+        if (c->Zr && is_f64(prec) && full && c->phase == (int)c->ph.size() - 1) {
           g.mode |= EPI_STORE_N; g.nout = c->Zr; g.ldn = c->npad; c->zr_for = c->cur;
         }
       }
@@ -543,7 +571,7 @@ ipr_status update_sym(ipr_ctx *c) {
   CK(run_gemm(c, g));
   CKS(gather_bytes(c, c->wbuf, (size_t)(c->npad * c->kp) * wb, "W"));
   CK(launch_sym_update(cont_ptr(c, c->cur, P), P.cont64, cont_ptr(c, nx, P), c->wbuf, wb == 8, c->npad,
-                       c->kp, c->col0, c->p, P.m, P.rtz, P.prec,
+                       c->kp, c->col0, c->p, P.adaptive ? c->oz_m_next : P.m, P.rtz, P.prec,
                        (is_f64(P.prec) || is_scaled(P.prec)) ? nullptr : chat_slot(c, nx, P.prec), P.corr,
                        same_fmt(P.corr, P.prec) ? nullptr : chatc_slot(c, nx, P.corr), c->part, c->st));
   CK(cudaEventRecord(c->ev[3], c->st));
@@ -554,6 +582,7 @@ ipr_status update_sym(ipr_ctx *c) {
   if (is_scaled(P.prec)) CKS(make_operand(c, nx, P));   // sigma from max|C_{k+1}|, then all-gather
   else CKS(gather_chat(c, nx, P.prec));
   if (P.prec == IPR_FP64_OZ) CKS(oz_split_chat(c, nx));
+  c->m_of_cur = P.adaptive ? c->oz_m_next : P.m;
   if (!same_fmt(P.corr, P.prec)) CKS(gather_bytes(c, c->chatc[nx], (size_t)(c->npad * c->kp) * elt_size(P.corr), "Chat corr"));
   if (c->world > 1) CKS(make_xt(c, nx, P));
   c->cur = nx;
@@ -754,6 +783,9 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
     P.prec = q.prec;
     P.cont64 = is_f64(q.prec);
     const int mmax = P.cont64 ? 52 : 23;
+    P.adaptive = q.prec == IPR_FP64_OZ && q.mant_bits == IPR_MANT_ADAPTIVE;
+    if (q.mant_bits < -1 && !P.adaptive)
+      return fail(c, IPR_E_INVALID_ARG, "phase %d: mant_bits %d (IPR_MANT_ADAPTIVE needs IPR_FP64_OZ)", i, q.mant_bits);
     P.m = q.mant_bits < 0 ? native_m(q.prec) : q.mant_bits;
     if (P.m > mmax) return fail(c, IPR_E_INVALID_ARG, "phase %d: mant_bits %d > %d for this container", i, P.m, mmax);
     if (q.round != IPR_RNE && q.round != IPR_RTZ) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad round", i);
@@ -837,9 +869,10 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     const int phase_now = c->phase;
     bool best_new = false;
     const int d = decide(c, rho, &best_new);
+    c->ph_r2 = c->ph_r1; c->ph_r1 = rho;   // R-26 in-phase history (reset by begin_phase)
     if (best_new) { c->best_loc = c->cur; c->best_cont64 = is_f64(c->ph[c->phase].prec); }
     ipr_record r;
-    r.k = (int)c->trace.size(); r.phase = phase_now; r.prec = c->ph[phase_now].prec; r.mant_bits = c->ph[phase_now].m;
+    r.k = (int)c->trace.size(); r.phase = phase_now; r.prec = c->ph[phase_now].prec; r.mant_bits = c->m_of_cur;
     r.decision = d; r.rho = rho; r.rho_hat = rho / std::sqrt((double)c->n); r.delta = NAN; r.gemm_ms = ms;
     r.rho_cert = NAN; r.upd_ms = 0.0;
     c->trace.push_back(r);

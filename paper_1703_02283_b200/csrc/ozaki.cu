@@ -120,9 +120,11 @@ cudaError_t launch_oz_split(const double *X, int64_t ld, int64_t rows, int64_t c
   return cudaGetLastError();
 }
 
-// Z = X Y for a P_FP64_OZ GemmArgs: g.oz_a / g.oz_rsig hold the digits of X (A role), g.oz_b /
-// g.oz_csig those of Y (B role, per output column); g.ozacc is the FP64 accumulator (transposed,
-// ldoz); then the epilogue g.mode runs in k_oz_finish.  Single panel (G = 1): M = N = K = npad.
+// Z = X Y for a P_FP64_OZ GemmArgs: g.oz_a / g.oz_rsig hold the OZ_S digits of X (A role), g.oz_b /
+// g.oz_csig those of Y (B role, per output column, layout stride OZ_S); the product keeps the
+// digit pairs s + t <= g.oz_S + 1 (the leading g.oz_S digits of a 9-digit split ARE the g.oz_S-digit
+// split); g.ozacc is the FP64 accumulator (transposed, ldoz); then the epilogue g.mode runs in
+// k_oz_finish.  Single panel (G = 1): M = N = K = npad.
 cudaError_t launch_gemm_ozaki(const GemmArgs &g, cudaStream_t s) {
   const int S = g.oz_S;
   if (!g.oz_a || !g.oz_b || !g.oz_rsig || !g.oz_csig || !g.ozacc || g.M != g.K || g.N != g.K || S < 2 || S > OZ_S)
@@ -133,7 +135,7 @@ cudaError_t launch_gemm_ozaki(const GemmArgs &g, cudaStream_t s) {
     q.prec = P_INT8; q.tprec = P_INT8;
     q.A = g.oz_a; q.a_kp = np; q.a_pstride = np * np;
     q.K = (int64_t)(gi - 1) * np;
-    q.B = g.oz_b + (int64_t)(S - gi + 1) * np; q.ldb = (int64_t)S * np;
+    q.B = g.oz_b + (int64_t)(OZ_S - gi + 1) * np; q.ldb = (int64_t)OZ_S * np;
     q.mode = EPI_OZACC; q.oz_g = gi; q.oz_first = gi == S + 1;
     q.sigA = nullptr; q.sigB = nullptr; q.pmax = nullptr; q.part = nullptr;
     cudaError_t e = launch_gemm_tc(q, s);

@@ -83,3 +83,25 @@ def test_ozaki_unsupported_outside_symmetric_forms():
         s.iterate(1)
     assert e.value.status == ipr.IPR_E_UNSUPPORTED
     s.close()
+
+
+def test_adaptive_digits_level2_and_storage_rule():
+    # R-26: digits / stored bits chosen per iteration from the expected residual; the oracle
+    # mirrors the storage rule (its arithmetic stays FP64).  Same per-iteration stored bits (ties
+    # aside), final C within 1e-10 and certified rho <= 1e-12.
+    n, p = 520, 2
+    A = synth.spd(n, 2.0, 12)
+    low = dict(plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
+    pg = [ipr.make_phase("bf16", **low), ipr.make_phase("fp64oz", mant_bits=ipr.IPR_MANT_ADAPTIVE, corr_prec="bf16")]
+    po = [oracle.phase(oracle.BF16, **low), oracle.phase(oracle.FP64_OZ, mant_bits=oracle.MANT_ADAPTIVE,
+                                                         corr_prec=oracle.BF16)]
+    r = oracle.solve(A, p, po, 1e-12, 80, hist=80, form=oracle.FORM_SYMMETRIC_TRI)
+    out, tr, hist, best = run_gpu_trajectory(A, p, pg, 1e-12, 80, form="symmetric_tri")
+    assert out == ipr.IPR_CONVERGED and r.outcome == oracle.CONVERGED
+    mg = [t["mant_bits"] for t in tr if t["phase"] == 1]
+    mo = [x["mant_bits"] for x in r.records if x["phase"] == 1]
+    assert len(set(mg)) >= 3 and mg[-1] == 52                   # precision rises inside the phase
+    agree = sum(a == b for a, b in zip(mg, mo))
+    assert agree >= min(len(mg), len(mo)) - 1, (mg, mo)
+    assert rel_fro(best, r.C_best) <= 1e-10
+    assert tr[-1]["rho_cert"] <= 1e-12

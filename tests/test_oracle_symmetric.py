@@ -191,3 +191,20 @@ def test_tri_variant_mirrors_upper_triangle():
     assert tri.records[0]["rho"] == pytest.approx(np.linalg.norm(R), rel=1e-14)
     with pytest.raises(ValueError):
         oracle.solve(A, 3, [oracle.phase()], form=TRI)
+
+
+def test_adaptive_digits_rule_pins():
+    # R-26 storage rule written out: S = clamp(ceil((log2(30 sqrt n) - log2 t) / 7), 3, 9),
+    # m = min(52, 7 S - 4); the first chain uses S = 9; precision rises inside the phase and the
+    # solve still reaches the certified FP64 residual.
+    import math
+    for t, n in [(1e-4, 8192), (1e-16, 8192), (3e-3, 512), (1.0, 64)]:
+        S = min(9, max(3, math.ceil((math.log2(30 * math.sqrt(n)) - math.log2(t)) / 7)))
+        assert oracle.oz_digits(t, n) == S
+    assert [oracle.oz_adaptive_m(S) for S in (3, 5, 8, 9)] == [17, 31, 52, 52]
+    A = synth.spd(96, 2.0, 4)
+    low = oracle.phase(oracle.BF16, plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
+    r = oracle.solve(A, 2, [low, oracle.phase(oracle.FP64_OZ, mant_bits=oracle.MANT_ADAPTIVE)], 1e-12, 80,
+                     form=SYM)
+    ms = [x["mant_bits"] for x in r.records if x["phase"] == 1]
+    assert r.outcome == oracle.CONVERGED and ms == sorted(ms) and ms[0] < 52 and ms[-1] == 52
