@@ -29,11 +29,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "time-to-FP64-residual 1e-12 (n=8192, p=2)"
 # headline schedule (symmetrised-correction form with the upper-triangle GEMM 2, NEXT-2 (i)+(iii),
-# DESIGN.md R-22): BF16 tensor-core phase; a 23-bit phase (C stored at m = 23, GEMMs on the INT8
-# tensor cores with 5 Ozaki digits, R-23); FP64 refinement (9 Ozaki digits) with a BF16 correction
-# GEMM; convergence certified with FP64 DMMA GEMMs
-DEFAULT_SCHEDULE = "symtri:bf16>fp64oz@23/cbf16>fp64oz/cbf16"
-EXTRA_SCHEDULES = ["fp64", "symtri:bf16>fp64oz@a/cbf16", "symtri:bf16>fp64oz/cbf16", "sym:fp64oz", "symtri:fp8>bf16>fp64oz@23/cbf16>fp64oz/cbf16",
+# DESIGN.md R-22): a BF16 tensor-core phase, then an FP64-range phase whose GEMMs run on the INT8
+# tensor cores (Ozaki, R-23) with the digit count -- 3..9, i.e. ~17..63 bits -- and the stored bits
+# raised per iteration from the residual (dynamic precision scaling, R-26), a BF16 correction
+# GEMM, and convergence certified on ||I - C^2 A||_F at full FP64 accuracy
+DEFAULT_SCHEDULE = "symtri:bf16>fp64oz@a/cbf16"
+EXTRA_SCHEDULES = ["fp64", "symtri:bf16>fp64oz@23/cbf16>fp64oz/cbf16", "symtri:bf16>fp64oz/cbf16", "sym:fp64oz", "symtri:fp8>bf16>fp64oz@23/cbf16>fp64oz/cbf16",
                    "bf16>fp64", "tf32>fp64", "fp16>fp64", "sym:fp64", "sym:fp64/cbf16", "symtri:fp64/cbf16",
                    "symtri:bf16>fp64/cbf16", "symtri:bf16>tf32>fp64/cbf16", "symtri:fp8>bf16>fp64/cbf16",
                    "symtri:int8>bf16>fp64/cbf16", "symtri:fp16>fp64/cbf16",
