@@ -129,6 +129,8 @@ typedef struct {
   double gemm_ms;    /* device time of this record's GEMMs (chain + update), CUDA events     */
   double upd_ms;     /* the part of gemm_ms spent in the update (GEMM p+1 + its epilogue /    */
                      /* k_sym_update); gemm_ms - upd_ms = the chain's p GEMMs                  */
+  int    digits;     /* IPR_FP64_OZ: Ozaki digits S of this record's chain (S(S+1)/2 INT8      */
+                     /* digit products per FP64 product); 0 otherwise                         */
   double rho_cert;   /* IPR_FORM_SYMMETRIC: ||I - C^p A||_F recomputed in FP64 when the      */
                      /* in-chain rho met final_tol (converged iff rho_cert <= final_tol);    */
                      /* NaN otherwise                                                         */

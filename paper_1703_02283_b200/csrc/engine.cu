@@ -81,7 +81,7 @@ struct ipr_ctx {
   int zr_for = -1;                      // iterate buffer whose chain wrote Zr (-1: none)
   // dynamic precision inside an FP64_OZ phase (R-26): digits of this chain, stored bits of the
   // next iterate and of the current one, the last two in-phase residuals
-  int oz_S_cur = OZ_S, oz_m_next = 52, m_of_cur = 52;
+  int oz_S_cur = OZ_S, oz_m_next = 52, m_of_cur = 52, last_chain_S = 0;
   double ph_r1 = NAN, ph_r2 = NAN;
   int form = IPR_FORM_LITERAL;          // iteration form (ipr_set_form)
   float *tscr = nullptr;                // FP16 phase T scratch (FP32)
@@ -428,6 +428,7 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
     c->oz_S_cur = c->trace.empty() ? OZ_S : oz_digits_for(c->last_rho / std::sqrt((double)c->n) * q * q, c->n);
     c->oz_m_next = oz_adaptive_m(c->oz_S_cur);
   }
+  c->last_chain_S = prec == IPR_FP64_OZ ? oz_S_now(c) : 0;
   if (is_sym(c)) {
     // Z_1 = Ahat Chat (A operand: Ahat row-major; B: Chat itself for G = 1 -- exactly symmetric --
     // else the transposed local panel), Z_j = Chat qin(Z_{j-1}); GEMM p: R = I - Z_p in the
@@ -875,6 +876,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     r.k = (int)c->trace.size(); r.phase = phase_now; r.prec = c->ph[phase_now].prec; r.mant_bits = c->m_of_cur;
     r.decision = d; r.rho = rho; r.rho_hat = rho / std::sqrt((double)c->n); r.delta = NAN; r.gemm_ms = ms;
     r.rho_cert = NAN; r.upd_ms = 0.0;
+    r.digits = c->ph[phase_now].prec == IPR_FP64_OZ ? c->last_chain_S : 0;
     c->trace.push_back(r);
     *iters_done += 1;
     if (d == IPR_DEC_CONVERGED && is_sym(c)) {
