@@ -78,6 +78,9 @@ struct GemmArgs {
   void *nout; int64_t ldn;
   // EPI_OZACC (FP64 accumulator stored transposed), and the Ozaki operands of a P_FP64_OZ GEMM
   double *ozacc; int64_t ldoz; const int *oz_rsig, *oz_csig; int oz_g, oz_first, oz_S;
+  int oz_grouped;       // k_gemm_tc<kind::i8>: every group g = S+1..2 of a tile in one launch (K up to
+                        // OZ_S * npad, B offset (OZ_S - g + 1) * npad), the finish epilogue g.mode
+                        // fused into group 2; g.mode holds the FINISH mode
   const int8_t *oz_a;   // A-role digit planes [S][npad][npad] (row-major per plane)
   const int8_t *oz_b;   // B-role digits, per output column j: [S * npad] = digit planes S..1 of column j
 };

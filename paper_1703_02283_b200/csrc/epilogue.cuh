@@ -33,7 +33,7 @@ template <int MODE = -1>
 __device__ __forceinline__ void epi_element(const GemmArgs &g, int64_t row, int64_t col,
                                             double v, EpiAcc &acc) {
   const int mode = MODE >= 0 ? MODE : g.mode;
-  if (mode & EPI_STORE_N) store_operand(g.nout, row * g.ldn + col, g.prec, v, 0);
+  if (mode & EPI_STORE_N) store_operand(g.nout, row * g.ldn + col, g.tprec, v, 0);
   const bool mirror = g.tri && row != g.col0 + col;   // tri: (i,j), i < j, also stands for (j,i)
   if (g.tri && row > g.col0 + col) return;             // tri: lower triangle comes from the mirror
   if (mode & (EPI_STORE_T | EPI_TSCRATCH)) {

@@ -40,14 +40,14 @@ constexpr int TC_GROUP_M = 8;         // pair-rows per scheduling group
 bool tc_supported(int prec) {
   return prec == P_BF16 || prec == P_FP16 || prec == P_TF32 || prec == P_FP8 || prec == P_INT8;
 }
-// partial-sum tile of the kernel that produces a format's GEMM epilogue: P_FP64_OZ finishes in
-// k_oz_finish with the DMMA tile (128 x 64), so its partial layout equals the FP64 one
+// partial-sum tile of the kernel that produces a format's GEMM epilogue (P_FP64_OZ finishes inside
+// the grouped kind::i8 launch: the tcgen05 tile)
 // tcgen05.mma kind of an operand format: 0 kind::f16 (BF16/FP16), 1 kind::tf32, 2 kind::f8f6f4
 // (E4M3), 3 kind::i8 (signed).  Every kind consumes 32 bytes of K per instruction.
 __host__ __device__ constexpr int tc_kind(int prec) {
   return prec == P_TF32 ? 1 : prec == P_FP8 ? 2 : prec == P_INT8 ? 3 : 0;
 }
-int gemm_tile_n(int prec) { return is_f64(prec) ? dmma_tile_n() : TC_BN; }
+int gemm_tile_n(int prec) { return prec == P_FP64 ? dmma_tile_n() : TC_BN; }
 int gemm_tile_m(int prec) { return 128; }
 
 // ---------------------------------------------------------------------------------------
@@ -384,6 +384,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN), g.tri};
   const int ntiles = sch.count();
+  // Ozaki grouped launch: groups S+1 .. 2 per tile; otherwise one pass (g0 == g1)
+  // oz_grouped == 2: the single group g.oz_g (one launch per group keeps each group's digit planes
+  // L2-hot across all CTAs -- measured faster than all groups per tile in one launch)
+  const int g0 = g.oz_grouped == 1 ? g.oz_S + 1 : g.oz_grouped == 2 ? g.oz_g : 0;
+  const int g1 = g.oz_grouped == 1 ? 2 : g.oz_grouped == 2 ? g.oz_g : 0;
+  const int gfirst = g.oz_S + 1;                 // the group that initialises the FP64 accumulator
   const int esz = elt_size(g.prec);
   const int nkb = (int)(g.K * esz / TC_BKB);
   const int bke = TC_BKB / esz;                       // K elements per block
@@ -412,14 +418,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
         sch.get(t, tm, tn);
         const int arow = tm * 2 * TC_BM + (int)rank * TC_BM;
         const int brow = tn * TC_BN + (int)rank * (TC_BN / 2);
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t *sa = smem + stage * TC_STAGE_BYTES, *sb = sa + TC_A_BYTES;
-          if (leader) mbar_expect_tx(&full[stage], 2 * TC_STAGE_BYTES);
-          const int64_t k0 = (int64_t)kb * bke;
-          tma_load_3d_pair(sa, &mapA, &full[stage], (int)(k0 % g.a_kp), arow, (int)(k0 / g.a_kp));
-          tma_load_2d_pair(sb, &mapB, &full[stage], (int)k0, brow);
-          if (++stage == TC_ST) { stage = 0; phase ^= 1; }
+        for (int gi = g0; gi >= g1; --gi) {      // Ozaki groups (one pass otherwise)
+          const int nk = g.oz_grouped ? (int)((int64_t)(gi - 1) * g.a_kp * esz / TC_BKB) : nkb;
+          const int64_t boff = g.oz_grouped ? (int64_t)(OZ_S - gi + 1) * g.a_kp : 0;
+          for (int kb = 0; kb < nk; ++kb) {
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t *sa = smem + stage * TC_STAGE_BYTES, *sb = sa + TC_A_BYTES;
+            if (leader) mbar_expect_tx(&full[stage], 2 * TC_STAGE_BYTES);
+            const int64_t k0 = (int64_t)kb * bke;
+            tma_load_3d_pair(sa, &mapA, &full[stage], (int)(k0 % g.a_kp), arow, (int)(k0 / g.a_kp));
+            tma_load_2d_pair(sb, &mapB, &full[stage], (int)(boff + k0), brow);
+            if (++stage == TC_ST) { stage = 0; phase ^= 1; }
+          }
         }
       }
     }
@@ -431,22 +441,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       uint32_t phase = 0;
       int it = 0;
       for (int t = pair; t < ntiles; t += npairs) {
-        const int buf = it & 1;
-        mbar_wait_cluster(&tempty[buf], ((it >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t dcol = tmem + buf * TC_BN;
-        for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
+        for (int gi = g0; gi >= g1; --gi) {
+          const int nk = g.oz_grouped ? (int)((int64_t)(gi - 1) * g.a_kp * esz / TC_BKB) : nkb;
+          const int buf = it & 1;
+          mbar_wait_cluster(&tempty[buf], ((it >> 1) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t sa = su32(smem + stage * TC_STAGE_BYTES), sb = sa + TC_A_BYTES;
-          #pragma unroll
-          for (int k = 0; k < TC_BKB / 32; ++k)
-            tc_mma_pair<KIND>(dcol, smem_desc_sw128(sa + k * 32), smem_desc_sw128(sb + k * 32), idesc, (kb | k) != 0);
-          tc_commit_pair(&empty[stage]);
-          if (++stage == TC_ST) { stage = 0; phase ^= 1; }
+          const uint32_t dcol = tmem + buf * TC_BN;
+          for (int kb = 0; kb < nk; ++kb) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t sa = su32(smem + stage * TC_STAGE_BYTES), sb = sa + TC_A_BYTES;
+            #pragma unroll
+            for (int k = 0; k < TC_BKB / 32; ++k)
+              tc_mma_pair<KIND>(dcol, smem_desc_sw128(sa + k * 32), smem_desc_sw128(sb + k * 32), idesc, (kb | k) != 0);
+            tc_commit_pair(&empty[stage]);
+            if (++stage == TC_ST) { stage = 0; phase ^= 1; }
+          }
+          tc_commit_pair(&tfull[buf]);
+          ++it;
         }
-        tc_commit_pair(&tfull[buf]);
-        ++it;
       }
     }
   } else {
@@ -457,7 +470,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
     double scale = 1.0;
     if (g.sigA) scale = pow2(-(*g.sigA + *g.sigB));
     int it = 0;
-    for (int t = pair; t < ntiles; t += npairs) {
+    for (int t = pair; t < ntiles; t += npairs)
+    for (int gi = g0; gi >= g1; --gi) {
       int tm, tn;
       sch.get(t, tm, tn);
       const int buf = it & 1;
@@ -471,11 +485,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       for (int ch = hh * 4; ch < hh * 4 + 4; ++ch) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * TC_BN + ch * 32, r);
-        epi_chunk<KIND>(g, row, colb + ch * 32, r, scale, ea);
+        if (KIND == 3 && g.oz_grouped) {
+          if (gi > 2) {                                  // Ozaki group: FP64 accumulate (L2-resident tile)
+            const int rs = g.oz_rsig[row];
+            const int64_t c0 = colb + ch * 32;
+            double *z = g.ozacc + c0 * g.ldoz + row;
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const double v = __dmul_rn((double)(int32_t)r[j], pow2(rs + g.oz_csig[c0 + j] - 7 * gi));
+              z[j * g.ldoz] = gi == gfirst ? v : __dadd_rn(z[j * g.ldoz], v);
+            }
+          } else {                                       // group 2: complete Z, then the finish epilogue
+            const int rs = g.oz_rsig[row];
+            const int64_t c0 = colb + ch * 32;
+            const double *z = g.ozacc + c0 * g.ldoz + row;
+            for (int j = 0; j < 32; ++j) {
+              double v = __dmul_rn((double)(int32_t)r[j], pow2(rs + g.oz_csig[c0 + j] - 14));
+              if (gfirst > 2) v = __dadd_rn(z[j * g.ldoz], v);
+              epi_element<-1>(g, row, c0 + j, v, ea);
+            }
+          }
+        } else {
+          epi_chunk<KIND>(g, row, colb + ch * 32, r, scale, ea);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
+      if (KIND == 3 && g.oz_grouped && gi > 2) { ++it; continue; }   // partials after the finish only
       // per-tile partials: deterministic (fixed shuffle tree, warps summed in order 0..3)
       if ((g.mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE)) || g.pmax) {
         double s = (g.mode & EPI_RESID) ? ea.r2 : ea.d2;

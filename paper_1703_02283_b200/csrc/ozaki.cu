@@ -75,43 +75,6 @@ __global__ void __launch_bounds__(256) k_oz_split(const double *__restrict__ X, 
   }
 }
 
-// The hot path's FP64 epilogue on the combined Ozaki result (stored transposed: Z(i,j) at
-// ozacc[j * ldoz + i]), with the DMMA kernel's 128 x 64 tiles and partial-sum slots.
-__global__ void __launch_bounds__(128) k_oz_finish(const GemmArgs g) {
-  const int tm = blockIdx.y, tn = blockIdx.x;
-  const int64_t m0 = (int64_t)tm * 128, n0 = (int64_t)tn * 64;
-  const int64_t tile = ((g.col0 + n0) / 64) * g.tiles_m + tm;
-  const int mode = g.mode;
-  __shared__ double red[4];
-  __shared__ double stn[32][129];                 // EPI_STORE_N staging: 32 columns x 128 rows
-  if (g.tri && m0 > g.col0 + n0 + 63) {          // wholly below the diagonal: not computed
-    if (threadIdx.x == 0 && (mode & EPI_RESID)) g.part[tile] = 0.0;
-    return;
-  }
-  const int64_t row = m0 + threadIdx.x;
-  EpiAcc ea{0.0, 0.0, 0.0f};
-  GemmArgs gl = g;
-  gl.mode = mode & ~EPI_STORE_N;                  // the row-major copy goes through shared memory
-  for (int h = 0; h < 2; ++h) {
-    for (int c = 0; c < 32; ++c) {
-      const double v = g.ozacc[(n0 + h * 32 + c) * g.ldoz + row];
-      epi_element<-1>(gl, row, n0 + h * 32 + c, v, ea);
-      if (mode & EPI_STORE_N) stn[c][threadIdx.x] = v;
-    }
-    if (mode & EPI_STORE_N) {                     // nout[row][col]: 32 consecutive columns per warp
-      __syncthreads();
-      const int lc = threadIdx.x & 31, r0 = threadIdx.x >> 5;
-      for (int r = r0; r < 128; r += 4)
-        ((double *)g.nout)[(m0 + r) * g.ldn + n0 + h * 32 + lc] = stn[lc][r];
-      __syncthreads();
-    }
-  }
-  if (mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE)) {
-    const double s = block_sum_det<128>((mode & EPI_RESID) ? ea.r2 : ea.d2, red);
-    if (threadIdx.x == 0) g.part[tile] = s;
-  }
-}
-
 cudaError_t launch_oz_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int S, int8_t *planes,
                             int8_t *bcat, int *sig, cudaStream_t s) {
   if (S < 2 || S > OZ_S) return cudaErrorInvalidValue;
@@ -123,28 +86,31 @@ cudaError_t launch_oz_split(const double *X, int64_t ld, int64_t rows, int64_t c
 // Z = X Y for a P_FP64_OZ GemmArgs: g.oz_a / g.oz_rsig hold the OZ_S digits of X (A role), g.oz_b /
 // g.oz_csig those of Y (B role, per output column, layout stride OZ_S); the product keeps the
 // digit pairs s + t <= g.oz_S + 1 (the leading g.oz_S digits of a 9-digit split ARE the g.oz_S-digit
-// split); g.ozacc is the FP64 accumulator (transposed, ldoz); then the epilogue g.mode runs in
-// k_oz_finish.  Single panel (G = 1): M = N = K = npad.
+// split).  One persistent kind::i8 launch per group g = S+1 .. 2 (K' = (g-1) npad over digit planes
+// 1..g-1 and the B digits g-1..1), accumulating 2^(sig_i + tau_j - 7g) P_g in FP64 into g.ozacc
+// (transposed); the group-2 launch applies the hot path's epilogue g.mode (store / residual partials
+// / mirror) to the completed FP64 value (no separate finish pass).  Running all groups of a tile in
+// one launch (oz_grouped = 1) keeps the accumulator in L2 but spreads the CTAs over every digit
+// plane at once and measured slower (19.7 vs 16.6 ms at n = 8192).  G = 1: M = N = K = npad.
 cudaError_t launch_gemm_ozaki(const GemmArgs &g, cudaStream_t s) {
   const int S = g.oz_S;
   if (!g.oz_a || !g.oz_b || !g.oz_rsig || !g.oz_csig || !g.ozacc || g.M != g.K || g.N != g.K || S < 2 || S > OZ_S)
     return cudaErrorInvalidValue;
   const int64_t np = g.K;
+  GemmArgs q = g;
+  q.prec = P_INT8;
+  if (!is_f64(q.tprec) && q.tprec != P_BF16 && q.tprec != P_TF32) q.tprec = P_FP64;
+  q.A = g.oz_a; q.a_kp = np; q.a_pstride = np * np;
+  q.K = (int64_t)OZ_S * np;                      // map extents: all digit planes
+  q.B = g.oz_b; q.ldb = (int64_t)OZ_S * np;
+  q.oz_grouped = 2;                              // one launch per group, smallest contributions first
+  q.sigA = nullptr; q.sigB = nullptr; q.pmax = nullptr;
   for (int gi = S + 1; gi >= 2; --gi) {
-    GemmArgs q = g;
-    q.prec = P_INT8; q.tprec = P_INT8;
-    q.A = g.oz_a; q.a_kp = np; q.a_pstride = np * np;
-    q.K = (int64_t)(gi - 1) * np;
-    q.B = g.oz_b + (int64_t)(OZ_S - gi + 1) * np; q.ldb = (int64_t)OZ_S * np;
-    q.mode = EPI_OZACC; q.oz_g = gi; q.oz_first = gi == S + 1;
-    q.sigA = nullptr; q.sigB = nullptr; q.pmax = nullptr; q.part = nullptr;
+    q.oz_g = gi;
     cudaError_t e = launch_gemm_tc(q, s);
     if (e != cudaSuccess) return e;
   }
-  dim3 grid((unsigned)(g.N / 64), (unsigned)(g.M / 128));
-  k_oz_finish<<<grid, 128, 0, s>>>(g);
-  ++g_launches;
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 }  // namespace ipr
