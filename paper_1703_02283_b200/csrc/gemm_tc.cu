@@ -486,22 +486,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * TC_BN + ch * 32, r);
         if (KIND == 3 && g.oz_grouped) {
-          if (gi > 2) {                                  // Ozaki group: FP64 accumulate (L2-resident tile)
-            const int rs = g.oz_rsig[row];
-            const int64_t c0 = colb + ch * 32;
-            double *z = g.ozacc + c0 * g.ldoz + row;
+          // the 32 accumulator values of this row segment are loaded up front (independent loads in
+          // flight; a load-add-store chain per element serialised on memory latency)
+          const int rs = g.oz_rsig[row];
+          const int64_t c0 = colb + ch * 32;
+          double *z = g.ozacc + c0 * g.ldoz + row;
+          double zo[32];
+          if (gi != gfirst) {
+            #pragma unroll
+            for (int j = 0; j < 32; ++j) zo[j] = z[j * g.ldoz];
+          }
+          if (gi > 2) {                                  // Ozaki group: FP64 accumulate
             #pragma unroll
             for (int j = 0; j < 32; ++j) {
               const double v = __dmul_rn((double)(int32_t)r[j], pow2(rs + g.oz_csig[c0 + j] - 7 * gi));
-              z[j * g.ldoz] = gi == gfirst ? v : __dadd_rn(z[j * g.ldoz], v);
+              z[j * g.ldoz] = gi == gfirst ? v : __dadd_rn(zo[j], v);
             }
           } else {                                       // group 2: complete Z, then the finish epilogue
-            const int rs = g.oz_rsig[row];
-            const int64_t c0 = colb + ch * 32;
-            const double *z = g.ozacc + c0 * g.ldoz + row;
+            #pragma unroll
             for (int j = 0; j < 32; ++j) {
               double v = __dmul_rn((double)(int32_t)r[j], pow2(rs + g.oz_csig[c0 + j] - 14));
-              if (gfirst > 2) v = __dadd_rn(z[j * g.ldoz], v);
+              if (gfirst > 2) v = __dadd_rn(zo[j], v);
               epi_element<-1>(g, row, c0 + j, v, ea);
             }
           }
