@@ -160,3 +160,80 @@ def test_world2_gloo_matches_single_rank_and_oracle():
         np.testing.assert_array_equal(hist2[k], r.C_hist[k])
     assert rhos2 == rhos1                     # bit-identical slot-ordered reduction
     np.testing.assert_allclose(rhos1, r.rho, rtol=1e-13)
+
+
+def emulate_sym(A, iters, world, rank, gather=None):
+    """The symmetric form's (R-22, p = 2, FP64) column-panel data flow of the engine at G > 1:
+    Z_1[:, S_g] = A C[:, S_g] (A operand: the full Ahat), Z_2[:, S_g] = C Z_1[:, S_g], R = I - Z_2,
+    W[:, S_g] = C R[:, S_g]; W panels all-gathered (the W + W^T update needs W(j, i) from the
+    other ranks' panels), C_{k+1}[:, S_g] = C + (W + W^T)/4, C panels all-gathered."""
+    import paper_1703_02283_b200 as ipr
+    n = A.shape[0]
+    plan = ipr.ipr_plan(n, world, rank, ipr.IPR_FP64)
+    npad, kp, col0 = plan["npad"], plan["kp"], plan["col0"]
+    Ap = np.zeros((npad, npad)); Ap[:n, :n] = A
+    n1, ninf, _ = oracle.norms(A)
+    cols = slice(col0, col0 + kp)
+
+    def full(panel):
+        return panel.copy() if gather is None else np.concatenate(gather(panel), axis=1)
+
+    C_panel = oracle.c0(Ap, n1 * ninf, oracle.phase())[:, cols]
+    hist = []
+    for k in range(iters):
+        C = full(C_panel)
+        hist.append(C[:n, :n].copy())
+        Z1 = np.zeros((npad, npad)); oracle.gemm_cols(Ap, C, Z1, col0, col0 + kp)
+        Z2 = np.zeros((npad, npad)); oracle.gemm_cols(C, Z1, Z2, col0, col0 + kp)
+        R = np.zeros((npad, npad))
+        R[:, cols] = np.eye(npad)[:, cols] - Z2[:, cols]
+        R[n:, :] = 0.0
+        R[:, n:] = 0.0
+        W = np.zeros((npad, npad)); oracle.gemm_cols(C, R, W, col0, col0 + kp)
+        Wf = full(W[:, cols])
+        C_panel = C_panel + (Wf[:, cols] + Wf.T[:, cols]) / 4.0
+    return hist
+
+
+def _worker_sym(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = synth.spd(300, 2.0, 22)
+
+        def gather(arr):
+            t = torch.from_numpy(np.ascontiguousarray(arr))
+            out = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(out, t)
+            return [o.numpy() for o in out]
+
+        hist = emulate_sym(A, 5, world, rank, gather=gather)
+        if rank == 0:
+            q.put(("ok", hist))
+    except Exception as e:
+        if rank == 0:
+            q.put(("err", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_gloo_symmetric_form_matches_oracle():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_sym, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    status, hist2 = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=300)
+    assert status == "ok", hist2
+    assert all(pr.exitcode == 0 for pr in procs)
+    A = synth.spd(300, 2.0, 22)
+    hist1 = emulate_sym(A, 5, 1, 0)
+    r = oracle.solve(A, 2, [oracle.phase()], 0.0, 5, hist=5, form=oracle.FORM_SYMMETRIC)
+    for k in range(5):
+        np.testing.assert_array_equal(hist2[k], hist1[k])
+        np.testing.assert_array_equal(hist2[k], r.C_hist[k])     # bit-identical to the oracle
+        assert np.array_equal(hist2[k], hist2[k].T)
