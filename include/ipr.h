@@ -178,9 +178,17 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
  * IPR_FORM_SYMMETRIC_TRI (p = 2, world = 1): as IPR_FORM_SYMMETRIC, but
  * Z_2 = C A C -- symmetric in exact arithmetic -- is computed on the upper triangle only (tiles
  * wholly below the diagonal are skipped: ~1/2 of GEMM 2) and R_ij = delta_ij - Z_2[min(i,j)][max(i,j)]
- * is exactly symmetric; rho_s sums the off-diagonal terms twice. */
+ * is exactly symmetric; rho_s sums the off-diagonal terms twice.
+ *
+ * IPR_FORM_COUPLED (any p; FP64 / TF32 / BF16 phases): the M-carrying form
+ * of Eq. (1) (reading R-27): with M = X^p A and N = ((p+1) I - M) / p, X_{k+1} = X_k N_k
+ * and M_{k+1} = N_k^p M_k -- p + 1 GEMMs per iteration (X Nhat; Nhat Mhat; Nhat qin(T)...).  The last
+ * GEMM of each M chain stores Mhat = qin(q_m(M)) and Nhat = qin(((p+1)I - q_m(M))/p) and the
+ * residual rho = ||I - M||_F; every phase start re-anchors M = X^p A with the literal chain.
+ * Bounded after convergence for any kappa (it does not remove noise earlier phases left in X);
+ * convergence is certified on ||I - X^p A||_F like the symmetric forms. */
 typedef enum { IPR_FORM_LITERAL = 0, IPR_FORM_NEWTON_SCHULZ = 1, IPR_FORM_SYMMETRIC = 2,
-               IPR_FORM_SYMMETRIC_TRI = 3 } ipr_form;
+               IPR_FORM_SYMMETRIC_TRI = 3, IPR_FORM_COUPLED = 4 } ipr_form;
 ipr_status ipr_set_form(ipr_ctx *c, int form);
 
 /* Run at most max_iters (> 0) chains.  *iters_done = chains evaluated by this call,

@@ -252,7 +252,7 @@ def step_sym(A, Ck, p: int, ph: Phase, want_next: bool = True):
     return rho, nxt, d.value
 
 
-FORM_LITERAL, FORM_NEWTON_SCHULZ, FORM_SYMMETRIC, FORM_SYMMETRIC_TRI = 0, 1, 2, 3
+FORM_LITERAL, FORM_NEWTON_SCHULZ, FORM_SYMMETRIC, FORM_SYMMETRIC_TRI, FORM_COUPLED = 0, 1, 2, 3, 4
 
 
 def solve(A, p: int, phases, final_tol: float = 1e-12, max_total: int = 200,

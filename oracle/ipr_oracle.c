@@ -443,6 +443,72 @@ static double update_sym(int64_t n, int p, const double *C, const orc_phase *ph,
   return sqrt(s2);
 }
 
+/* ---------------------------------------------------------------------------------
+ * NEXT-2 (ii): the coupled (M-carrying) form of the same iteration.  With
+ * M_k = X_k^p A and N_k = ((p+1) I - M_k) / p, Eq. (1) reads X_{k+1} = X_k N_k and
+ * (in exact arithmetic) M_{k+1} = N_k^p M_k.  Carrying M keeps the error bounded after convergence
+ * for any kappa (SURVEY Table A3) but, unlike the symmetrised form, does not remove noise that
+ * earlier phases left in X.  In the order the GPU evaluates it (R-27):
+ *   anchor (first chain of a phase):  T_1 = qin(X) Ahat, T_j = qin(X) qin(T_{j-1}) (j = 2..p)
+ *   finish of a chain ending in T:    rho = ||I - T||_F (unrounded); w = q_m(T);
+ *                                     Mhat = qin(w); N = ((p+1) delta - w) / p (three FP64 ops,
+ *                                     the integers exact); Nhat = qin(N)
+ *   step:  X_{k+1} = q_m(qin(X_k) Nhat);  T_1 = Nhat Mhat, T_j = Nhat qin(T_{j-1});  finish(T_p)
+ * Scaled (FP16/FP8/INT8) formats are not defined for this form.
+ * ------------------------------------------------------------------------------ */
+static double coupled_finish(int64_t n, int p, const orc_phase *ph, const double *T, double *Mh, double *Nh) {
+  double s2 = 0.0;
+  const double pp1 = (double)(p + 1), pd = (double)p;
+  for (int64_t r = 0; r < n; ++r)
+    for (int64_t c = 0; c < n; ++c) {
+      const double v = T[r * n + c];
+      const double d = (r == c ? 1.0 : 0.0) - v;
+      s2 += d * d;
+      const double wv = store_q(ph, v);
+      Mh[r * n + c] = wv;
+      const double a = r == c ? pp1 : 0.0;
+      Nh[r * n + c] = (a - wv) / pd;
+    }
+  qin_matrix(ph->prec, n * n, Mh, Mh);
+  qin_matrix(ph->prec, n * n, Nh, Nh);
+  return sqrt(s2);
+}
+
+static double coupled_anchor(int64_t n, int p, const double *A, const double *X, const orc_phase *ph,
+                             chain_ws *w, double *Mh, double *Nh) {
+  const int64_t nn = n * n;
+  for (int64_t i = 0; i < nn; ++i) w->T[i] = store_q(ph, A[i]);
+  qin_matrix(ph->prec, nn, w->T, w->X);                     /* Ahat                   */
+  qin_matrix(ph->prec, nn, X, w->Chat);                     /* Xhat                   */
+  for (int j = 1; j <= p; ++j) {
+    orc_gemm(n, w->Chat, w->X, w->T);                       /* T_j = Xhat qin(T_{j-1}) */
+    if (j < p) qin_matrix(ph->prec, nn, w->T, w->X);
+  }
+  return coupled_finish(n, p, ph, w->T, Mh, Nh);
+}
+
+/* X_next = q_m(qin(X) Nhat); M chain; returns delta = ||X_next - X||_F, *rho_next from finish */
+static double coupled_step(int64_t n, int p, const double *X, const orc_phase *ph, chain_ws *w,
+                           double *Mh, double *Nh, double *X_next, double *rho_next) {
+  const int64_t nn = n * n;
+  qin_matrix(ph->prec, nn, X, w->Chat);
+  orc_gemm(n, w->Chat, Nh, w->T);                           /* X Nhat                 */
+  double s2 = 0.0;
+  for (int64_t i = 0; i < nn; ++i) {
+    const double x1 = store_q(ph, w->T[i]);
+    const double dd = x1 - X[i];
+    s2 += dd * dd;
+    X_next[i] = x1;
+  }
+  orc_gemm(n, Nh, Mh, w->T);                                /* T_1 = Nhat Mhat        */
+  for (int j = 2; j <= p; ++j) {
+    qin_matrix(ph->prec, nn, w->T, w->X);
+    orc_gemm(n, Nh, w->X, w->T);                            /* T_j = Nhat qin(T_{j-1}) */
+  }
+  *rho_next = coupled_finish(n, p, ph, w->T, Mh, Nh);
+  return sqrt(s2);
+}
+
 static int ws_alloc(chain_ws *w, int64_t n) {
   const size_t b = (size_t)(n * n) * sizeof(double);
   w->n = n;
@@ -515,13 +581,16 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
   *nrec = 0;
   if (n <= 0 || p < 1 || nphases < 1) return -1;
   if (form == ORC_FORM_NEWTON_SCHULZ && p != 1) return -1;
+  if (form == ORC_FORM_COUPLED)
+    for (int i = 0; i < nphases; ++i)
+      if (is_scaled(phases[i].prec)) return -1;
   const int sym = form == ORC_FORM_SYMMETRIC || form == ORC_FORM_SYMMETRIC_TRI;
   if (sym) {
     if (p < 2 || (form == ORC_FORM_SYMMETRIC_TRI && p != 2)) return -1;
     for (int i = 0; i < nphases; ++i)
       if (is_scaled(corr_of(&phases[i]))) return -1;
   }
-  if (form < ORC_FORM_LITERAL || form > ORC_FORM_SYMMETRIC_TRI) return -1;
+  if (form < ORC_FORM_LITERAL || form > ORC_FORM_COUPLED) return -1;
   if (!orc_is_symmetric(n, A)) return -2;
   const int64_t nn = n * n;
   double nrm[3];
@@ -537,6 +606,11 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
   }
   chain_ws w;
   ws_alloc(&w, n);
+  const int coupled = form == ORC_FORM_COUPLED;
+  double *Mh = coupled ? (double *)malloc((size_t)nn * sizeof(double)) : NULL;
+  double *Nh = coupled ? (double *)malloc((size_t)nn * sizeof(double)) : NULL;
+  int anchor = 1;
+  double rho_next = NAN;
   orc_c0(n, A, s, &phases[0], C);
   memcpy(C_best, C, (size_t)nn * sizeof(double));
   orc_ctrl ctl;
@@ -554,9 +628,15 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
       ph_k.mant_bits = orc_oz_adaptive_m(S);
     }
     if (C_hist && k < hist_cap) memcpy(C_hist + (int64_t)k * nn, C, (size_t)nn * sizeof(double));
-    const double rho = form == ORC_FORM_NEWTON_SCHULZ ? chain_ns(n, A, C, ph, &w)
-                       : sym ? chain_sym(n, p, form == ORC_FORM_SYMMETRIC_TRI, A, C, ph, &w)
-                                                       : chain(n, p, A, C, ph, &w);
+    double rho;
+    if (coupled) {
+      rho = anchor ? coupled_anchor(n, p, A, C, ph, &w, Mh, Nh) : rho_next;
+      anchor = 0;
+    } else {
+      rho = form == ORC_FORM_NEWTON_SCHULZ ? chain_ns(n, A, C, ph, &w)
+            : sym ? chain_sym(n, p, form == ORC_FORM_SYMMETRIC_TRI, A, C, ph, &w)
+                  : chain(n, p, A, C, ph, &w);
+    }
     const int phase_now = ctl.phase;
     int d = orc_ctrl_decide(&ctl, ph, rho);
     if (ctl.best_is_new) memcpy(C_best, C, (size_t)nn * sizeof(double));
@@ -565,7 +645,19 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
     r.decision = d; r.rho = rho; r.rho_hat = rho / sqrt((double)n); r.delta = NAN;
     r.gamma = (gamma_normA2 > 0) ? gamma_of(n, C, A, gamma_normA2, g1, g2) : NAN;
     r.rho_cert = NAN;
-    if (d == ORC_CONVERGED && sym) {
+    if (d == ORC_CONVERGED && coupled) {
+      /* rho = ||I - M_k||_F tracks ||I - X_k^p A||_F only up to drift: certify on X_k itself
+       * (the best iterate), continue with the step if it misses (as the GPU engine does) */
+      const orc_phase ph64 = {ORC_FP64, -1, ORC_RNE, 0.0, 0.0, 0.0, 0, -1};
+      r.rho_cert = chain(n, p, A, C, &ph64, &w);
+      if (!(r.rho_cert <= final_tol)) {
+        d = ORC_CONTINUE;
+        r.decision = d;
+        r.delta = coupled_step(n, p, C, ph, &w, Mh, Nh, Cn, &rho_next);
+        double *t = C; C = Cn; Cn = t;
+        m_of_C = phase_m(ph);
+      }
+    } else if (d == ORC_CONVERGED && sym) {
       /* rho_s = ||I - C^{p-1} A C||_F is not the north-star residual: certify
        * ||I - C^p A||_F with the FP64 literal chain (reading R-3); if it misses final_tol the
        * iteration continues from the update computed first (as the GPU engine does). */
@@ -578,6 +670,10 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
         double *t = C; C = Cn; Cn = t;
         m_of_C = phase_m(&ph_k);
       }
+    } else if (d == ORC_CONTINUE && coupled) {
+      r.delta = coupled_step(n, p, C, ph, &w, Mh, Nh, Cn, &rho_next);
+      double *t = C; C = Cn; Cn = t;
+      m_of_C = phase_m(ph);
     } else if (d == ORC_CONTINUE) {
       r.delta = form == ORC_FORM_NEWTON_SCHULZ ? update_ns(n, C, ph, &w, Cn)
                 : sym                           ? update_sym(n, p, C, &ph_k, &w, Cn)
@@ -591,6 +687,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
         pe.mant_bits = orc_oz_adaptive_m(orc_oz_digits(rho / sqrt((double)n) * 0.03 * 0.03, n));
       recontainer(nn, C_best, &pe, C);
       m_of_C = phase_m(&pe);
+      anchor = 1;                     /* coupled: re-anchor M = X^p A in the new phase */
     }
     /* R-26 bookkeeping */
     last_rho_hat = rho / sqrt((double)n);
@@ -601,7 +698,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
     if (d != ORC_CONTINUE && d != ORC_SWITCH) { outcome = d; break; }
   }
   ws_free(&w);
-  free(C); free(Cn); free(g1); free(g2);
+  free(C); free(Cn); free(g1); free(g2); free(Mh); free(Nh);
   return outcome;
 }
 

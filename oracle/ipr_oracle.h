@@ -117,8 +117,11 @@ int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int np
  * ORC_FORM_NEWTON_SCHULZ = p = 1 only, X_{k+1} = X_k (2I - A X_k) (NEXT-1). */
 /* ORC_FORM_SYMMETRIC_TRI (p = 2): as ORC_FORM_SYMMETRIC with Z_2 = C A C replaced by the mirror
  * of its upper triangle (Z_2[i][j] := Z_2[min(i,j)][max(i,j)]), so R is exactly symmetric. */
+/* ORC_FORM_COUPLED (NEXT-2 (ii)): X_{k+1} = X_k N_k, M_{k+1} = N_k^p M_k, N = ((p+1)I - M)/p, M
+ * re-anchored as X^p A at every phase start; rho = ||I - M_k||_F; convergence certified on
+ * ||I - X^p A||_F like the symmetric forms.  No scaled formats. */
 enum { ORC_FORM_LITERAL = 0, ORC_FORM_NEWTON_SCHULZ = 1, ORC_FORM_SYMMETRIC = 2,
-       ORC_FORM_SYMMETRIC_TRI = 3 };
+       ORC_FORM_SYMMETRIC_TRI = 3, ORC_FORM_COUPLED = 4 };
 int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase *phases,
                    int nphases, double final_tol, int max_total, orc_record *rec, int cap_rec,
                    int *nrec, double *C_best, double *C_hist, int hist_cap, double gamma_normA2,

@@ -43,6 +43,8 @@ enum EpiMode : int {
   EPI_STORE_N = 256,  // also store qin(D) row-major (nout[i * ldn + j]): symmetric form, FP64,
                       // G = 1 -- D = A C row-major is the B operand of C (C A) for certification
   EPI_OZACC = 512,    // Ozaki group g: ozacc[j * ldoz + i] (+)= 2^(rsig_i + csig_j - 7 g) * D_ij (INT32 D)
+  EPI_COUPLED = 1024, // coupled form: w = q_m(D); Mhat = qin(w) -> tout, Nhat = qin(((p+1)delta - w)/p)
+                      // -> nkout (both K-major at col * ldt + row); with EPI_RESID for rho
 };
 
 struct GemmArgs {
@@ -76,6 +78,8 @@ struct GemmArgs {
   void *wout; int64_t ldw; int w64;
   // EPI_STORE_N
   void *nout; int64_t ldn;
+  // EPI_COUPLED: the K-major Nhat output (same ldt as tout)
+  void *nkout;
   // EPI_OZACC (FP64 accumulator stored transposed), and the Ozaki operands of a P_FP64_OZ GEMM
   double *ozacc; int64_t ldoz; const int *oz_rsig, *oz_csig; int oz_g, oz_first, oz_S;
   int oz_grouped;       // k_gemm_tc<kind::i8>: every group g = S+1..2 of a tile in one launch (K up to

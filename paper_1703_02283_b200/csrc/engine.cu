@@ -78,6 +78,11 @@ struct ipr_ctx {
   int8_t *ozA = nullptr, *ozC[2] = {nullptr, nullptr}, *ozCb[2] = {nullptr, nullptr}, *ozB = nullptr;
   int *ozA_sig = nullptr, *ozC_sig[2] = {nullptr, nullptr}, *ozB_sig = nullptr;
   double *ozacc = nullptr;
+  // coupled form (R-27): Mhat and Nhat K-major local panels (ping-pong), Nhat as the replicated A
+  // operand (panel-major), which set is current, and whether the next chain must re-anchor M
+  void *cM[2] = {nullptr, nullptr}, *cNk[2] = {nullptr, nullptr}, *cNf = nullptr;
+  int cmi = 0;
+  bool c_anchor = true;
   int zr_for = -1;                      // iterate buffer whose chain wrote Zr (-1: none)
   // dynamic precision inside an FP64_OZ phase (R-26): digits of this chain, stored bits of the
   // next iterate and of the current one, the last two in-phase residuals
@@ -302,6 +307,7 @@ ipr_status save_best(ipr_ctx *c) {
 }
 
 ipr_status make_xt(ipr_ctx *c, int i, const PhaseC &P);
+ipr_status coupled_gather_n(ipr_ctx *c);
 // Ozaki digits of the FP64 iterate in buffer i (exactly symmetric, G = 1: its columns are its rows)
 // R-26: digits for a target RMS residual, and the stored bits that go with them
 int oz_digits_for(double rho_hat_target, int64_t n) {
@@ -374,6 +380,7 @@ ipr_status begin_phase(ipr_ctx *c, bool first) {
     }
   }
   CKS(make_operand(c, c->cur, P));
+  c->c_anchor = true;                // coupled form: re-anchor M = X^p A in this phase
   if (P.prec == IPR_FP64_OZ) {   // digits of Ahat (A role) and of Chat (both roles; G = 1, symmetric)
     CK(launch_oz_split((const double *)c->Aop, c->npad, c->npad, c->npad, OZ_S, c->ozA, nullptr, c->ozA_sig, c->st));
     CKS(oz_split_chat(c, c->cur));
@@ -479,6 +486,26 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
       }
     }
   }
+  const bool coupled_cached = c->form == IPR_FORM_COUPLED && !c->c_anchor;   // rho from the last step
+  if (c->form == IPR_FORM_COUPLED && c->c_anchor) {
+    // anchor: the literal chain T_j = Xhat qin(T_{j-1}) (T_0 = Ahat); the last GEMM stores
+    // Mhat = qin(q_m(T_p)) and Nhat = qin(((p+1)I - q_m(T_p))/p) K-major + residual partials
+    const void *Xb = c->Aop;
+    for (int j = 1; j <= c->p; ++j) {
+      GemmArgs g = base_args(c, prec, Xb);
+      chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
+      g.ldt = c->npad; g.part = part;
+      if (j < c->p) { g.mode = EPI_STORE_T; g.tout = c->T[j & 1]; }
+      else {
+        g.mode = EPI_COUPLED | EPI_RESID; g.tout = c->cM[c->cmi]; g.nkout = c->cNk[c->cmi];
+        g.m = P.m; g.rtz = P.rtz; g.cont64 = P.cont64;
+      }
+      CK(run_gemm(c, g));
+      Xb = c->T[j & 1];
+    }
+    CKS(coupled_gather_n(c));
+    c->c_anchor = false;
+  }
   for (int j = 1; c->form == IPR_FORM_LITERAL && j <= c->p; ++j) {
     GemmArgs g = base_args(c, prec, X);
     chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
@@ -498,8 +525,10 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
     X = c->T[j & 1];
   }
   CK(cudaEventRecord(c->ev[1], c->st));
-  CKS(gather_partials(c, part, tn_loc * tm));
-  CK(launch_reduce_sum(part, tiles_n_total(c, prec) * tm, c->dscal + 0, c->st));
+  if (!coupled_cached) {
+    CKS(gather_partials(c, part, tn_loc * tm));
+    CK(launch_reduce_sum(part, tiles_n_total(c, prec) * tm, c->dscal + 0, c->st));
+  }
   CK(cudaMemcpyAsync(c->hscal, c->dscal, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   float t = 0.f, tu = 0.f;
@@ -590,7 +619,62 @@ ipr_status update_sym(ipr_ctx *c) {
   return IPR_OK;
 }
 
-ipr_status step_update(ipr_ctx *c) { return is_sym(c) ? update_sym(c) : update(c); }
+// ---- coupled form (NEXT-2 (ii), R-27) ----
+// the current K-major Nhat panel -> row-major column panel (slot rank of cNf), all-gathered: the
+// replicated A operand of the M chain
+ipr_status coupled_gather_n(ipr_ctx *c) {
+  const PhaseC &P = c->ph[c->phase];
+  const size_t esz = elt_size(P.prec), slot = (size_t)(c->npad * c->kp) * esz;
+  CK(launch_transpose(c->cNk[c->cmi], c->kp, c->npad, (int)esz, (char *)c->cNf + c->rank * slot, c->st));
+  return gather_bytes(c, c->cNf, slot, "Nhat");
+}
+
+// X_{k+1} = q_m(Xhat Nhat) (+ Xhat_{k+1}, delta partials); T_1 = Nhat Mhat, T_j = Nhat qin(T_{j-1});
+// the last GEMM stores the next Mhat / Nhat and the residual partials of M_{k+1}
+ipr_status update_coupled(ipr_ctx *c) {
+  const PhaseC &P = c->ph[c->phase];
+  const int prec = P.prec, nx = 1 - c->cur;
+  if (c->best_loc == nx) CKS(save_best(c));
+  const int64_t tm = tiles_m(c, prec), tn_loc = c->kp / gemm_tile_n(prec);
+  CK(cudaEventRecord(c->ev[2], c->st));
+  GemmArgs g = base_args(c, prec, c->cNk[c->cmi]);
+  chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
+  g.mode = EPI_NSUPDATE;
+  g.cold = cont_ptr(c, c->cur, P); g.cnew = cont_ptr(c, nx, P); g.ldc = c->kp;
+  g.chat_new = is_f64(prec) ? nullptr : chat_slot(c, nx, prec); g.ldh = c->kp;
+  g.m = P.m; g.rtz = P.rtz; g.cont64 = P.cont64;
+  g.part = c->part;
+  CK(run_gemm(c, g));
+  CKS(gather_partials(c, c->part, tn_loc * tm));
+  CK(launch_reduce_sum(c->part, tiles_n_total(c, prec) * tm, c->dscal + 1, c->st));
+  const void *Xb = c->cM[c->cmi];
+  for (int j = 1; j <= c->p; ++j) {
+    GemmArgs q = base_args(c, prec, Xb);
+    q.A = c->cNf; q.a_kp = c->kp; q.a_pstride = c->npad * c->kp;
+    q.ldt = c->npad; q.part = c->part;
+    if (j < c->p) { q.mode = EPI_STORE_T; q.tout = c->T[j & 1]; }
+    else {
+      q.mode = EPI_COUPLED | EPI_RESID; q.tout = c->cM[1 - c->cmi]; q.nkout = c->cNk[1 - c->cmi];
+      q.m = P.m; q.rtz = P.rtz; q.cont64 = P.cont64;
+    }
+    CK(run_gemm(c, q));
+    Xb = c->T[j & 1];
+  }
+  CKS(gather_partials(c, c->part, tn_loc * tm));
+  CK(launch_reduce_sum(c->part, tiles_n_total(c, prec) * tm, c->dscal + 0, c->st));
+  c->cmi ^= 1;
+  CKS(gather_chat(c, nx, prec));
+  CKS(coupled_gather_n(c));
+  CK(cudaEventRecord(c->ev[3], c->st));
+  c->upd_timed = true;
+  c->m_of_cur = P.m;
+  c->cur = nx;
+  return IPR_OK;
+}
+
+ipr_status step_update(ipr_ctx *c) {
+  return is_sym(c) ? update_sym(c) : c->form == IPR_FORM_COUPLED ? update_coupled(c) : update(c);
+}
 
 // Controller, reading R-5 (independent implementation of the rules in DESIGN.md).
 int decide(ipr_ctx *c, double rho, bool *best_new) {
@@ -630,6 +714,7 @@ void free_ctx(ipr_ctx *c) {
 // ipr_iterate): one cudaMalloc / cudaFree per solve, and an OOM is reported before any work.
 ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
   const size_t full = (size_t)(c->npad * c->npad), panel = (size_t)(c->npad * c->kp);
+  const bool cpl = c->form == IPR_FORM_COUPLED;
   bool fp16 = false, oz = false;        // any scaled-format phase: FP32 T scratch; any Ozaki phase
   for (auto &P : c->ph) { fp16 |= is_scaled(P.prec); oz |= P.prec == IPR_FP64_OZ; }
   struct Slot { void **p; size_t bytes; };
@@ -648,6 +733,8 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       {(void **)&c->ozA_sig, oz ? (size_t)c->npad * 4 : 0}, {(void **)&c->ozC_sig[0], oz ? (size_t)c->npad * 4 : 0},
       {(void **)&c->ozC_sig[1], oz ? (size_t)c->npad * 4 : 0}, {(void **)&c->ozB_sig, oz ? (size_t)c->npad * 4 : 0},
       {(void **)&c->ozacc, oz ? full * 8 : 0},
+      {&c->cM[0], cpl ? panel * 8 : 0}, {&c->cM[1], cpl ? panel * 8 : 0}, {&c->cNk[0], cpl ? panel * 8 : 0},
+      {&c->cNk[1], cpl ? panel * 8 : 0}, {&c->cNf, cpl ? full * 8 : 0},
       {(void **)&c->full64, full * 8}, {&c->Acert, panel * 8}};
   size_t total = 0;
   for (const Slot &q : slots) total += (q.bytes + 255) / 256 * 256;
@@ -821,7 +908,7 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
 ipr_status ipr_set_form(ipr_ctx *c, int form) {
   if (!c) return fail(c, IPR_E_INVALID_ARG, "ipr_set_form: null context");
   if (c->started) return fail(c, IPR_E_STATE, "ipr_set_form: iteration already started");
-  if (form < IPR_FORM_LITERAL || form > IPR_FORM_SYMMETRIC_TRI)
+  if (form < IPR_FORM_LITERAL || form > IPR_FORM_COUPLED)
     return fail(c, IPR_E_INVALID_ARG, "ipr_set_form: unknown form %d", form);
   c->form = form;
   return IPR_OK;
@@ -838,6 +925,9 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       if (c->p != 1) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: the Newton-Schulz form needs p = 1");
     }
     bool need_c = false;
+    for (auto &P : c->ph)
+      if (c->form == IPR_FORM_COUPLED && (is_scaled(P.prec) || P.prec == IPR_FP64_OZ))
+        return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: the coupled form takes FP64 / TF32 / BF16 phases");
     for (auto &P : c->ph)
       if (P.prec == IPR_FP64_OZ && (!is_sym(c) || c->world != 1))
         return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ phases need a symmetric form and world = 1");
@@ -879,6 +969,22 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     r.digits = c->ph[phase_now].prec == IPR_FP64_OZ ? c->last_chain_S : 0;
     c->trace.push_back(r);
     *iters_done += 1;
+    if (d == IPR_DEC_CONVERGED && c->form == IPR_FORM_COUPLED) {
+      // rho = ||I - M_k||_F tracks ||I - X_k^p A||_F only up to drift: certify the best iterate
+      // in FP64 (R-3, R-27); if it misses, take the step and continue
+      double rc = NAN;
+      CKS(certify_best(c, &rc));
+      c->trace.back().rho_cert = rc;
+      if (!(rc <= c->final_tol)) {
+        c->trace.back().decision = IPR_DEC_CONTINUE;
+        CKS(update_coupled(c));
+        c->pending_delta = (int64_t)c->trace.size() - 1;
+        continue;
+      }
+      c->done = true;
+      c->outcome = d;
+      break;
+    }
     if (d == IPR_DEC_CONVERGED && is_sym(c)) {
       // rho_s = ||I - C^{p-1}AC||_F met final_tol: compute C_{k+1} (the T buffers are consumed),
       // then certify ||I - C_k^p A||_F in FP64 (R-3); continue from C_{k+1} if it misses.

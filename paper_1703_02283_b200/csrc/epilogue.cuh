@@ -70,6 +70,15 @@ __device__ __forceinline__ void epi_element(const GemmArgs &g, int64_t row, int6
     const double dd = __dsub_rn(cn, c);
     acc.d2 = __fma_rn(dd, dd, acc.d2);
   }
+  if (mode & EPI_COUPLED) {           // coupled form (R-27): M_{k+1} stored, N_{k+1} from it
+    const int64_t gc = g.col0 + col;
+    const double w = g.cont64 ? q_e11(v, g.m, g.rtz) : (double)q_e8(v, g.m, g.rtz);
+    store_operand(g.tout, col * g.ldt + row, g.prec, w, 0);
+    const double a = (row == gc && row < g.n) ? (double)(g.p + 1) : 0.0;
+    const double d = __dsub_rn(a, w);
+    const double e = ((g.p & (g.p - 1)) == 0) ? __dmul_rn(d, 1.0 / (double)g.p) : __ddiv_rn(d, (double)g.p);
+    store_operand(g.nkout, col * g.ldt + row, g.prec, e, 0);
+  }
   if (mode & EPI_RESID) {
     const int64_t gc = g.col0 + col;
     if (row < g.n && gc < g.n) {

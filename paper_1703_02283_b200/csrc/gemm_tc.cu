@@ -234,6 +234,11 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
     }
     return;
   }
+  if (mode & EPI_COUPLED) {           // coupled form: the generic per-element FP64 epilogue
+    #pragma unroll 1
+    for (int j = 0; j < 32; ++j) epi_element<-1>(g, row, col + j, __dmul_rn(acc_to_f64<KIND>(r[j]), scale), ea);
+    return;
+  }
   // ---- FP32 fast paths (no FP64 arithmetic; results identical to the general path below) ----
   // (a) plain chain store: qin(D) of an unscaled accumulator -- BF16 / TF32 are one RNE rounding
   //     of the FP32 value, exactly what the FP64 detour produced ((float)(double)f == f)
