@@ -38,7 +38,7 @@ EXTRA_SCHEDULES = ["fp64", "symtri:bf16>fp64oz@23/cbf16>fp64oz/cbf16", "symtri:b
                    "bf16>fp64", "tf32>fp64", "fp16>fp64", "sym:fp64", "sym:fp64/cbf16", "symtri:fp64/cbf16",
                    "symtri:bf16>fp64/cbf16", "symtri:bf16>tf32>fp64/cbf16", "symtri:fp8>bf16>fp64/cbf16",
                    "symtri:int8>bf16>fp64/cbf16", "symtri:fp16>fp64/cbf16",
-                   "sym:bf16>fp64", "sym:tf32>fp64/cbf16", "sym:bf16>tf32>fp64/cbf16"]
+                   "sym:bf16>fp64", "sym:tf32>fp64/cbf16", "sym:bf16>tf32>fp64/cbf16", "cpl:fp64"]
 FP64_PEAK_TFLOPS = 37.1   # measured DMMA issue peak on this pool (profiles/r01_calibration.md)
 FP64_PEAK_SRC = "measured DMMA.8x8x4 issue peak, tools/probes/dmma_rate.cu (MEASURED_PEAKS.json has no FP64 figure)"
 
@@ -64,7 +64,8 @@ def parse_schedule(name):
     form = "literal"
     if ":" in name:
         f, name = name.split(":", 1)
-        form = {"sym": "symmetric", "symtri": "symmetric_tri", "ns": "newton_schulz", "lit": "literal"}[f]
+        form = {"sym": "symmetric", "symtri": "symmetric_tri", "ns": "newton_schulz", "lit": "literal",
+                "cpl": "coupled"}[f]
     parts = []
     for ph in name.replace("-", ">").split(">"):
         ph, _, m = ph.partition("@")          # prec[@mant_bits][/c<corr>]
