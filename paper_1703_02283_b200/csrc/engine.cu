@@ -929,6 +929,9 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       if (c->form == IPR_FORM_COUPLED && (is_scaled(P.prec) || P.prec == IPR_FP64_OZ))
         return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: the coupled form takes FP64 / TF32 / BF16 phases");
     for (auto &P : c->ph)
+      if (P.prec == IPR_FP64_OZ && c->npad > 47800)   // INT32 digit-group sums (ozaki.cu)
+        return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ needs n <= 47800 (exact INT32 group sums)");
+    for (auto &P : c->ph)
       if (P.prec == IPR_FP64_OZ && (!is_sym(c) || c->world != 1))
         return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ phases need a symmetric form and world = 1");
     if (is_sym(c)) {

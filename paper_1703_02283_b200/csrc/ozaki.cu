@@ -6,8 +6,8 @@
 //             per ROW of the left operand (sig_i from max_k |x_ik|) and per COLUMN of the right
 //             operand; d_1 in [-127, 127], d_s in [-64, 64] (s >= 2), every step exact in FP64
 //   products  P_g = sum_{s + t = g} D_s E_t  for g = 2 .. S+1: ONE int8 GEMM with the K-concatenated
-//             operands [D_1 | ... | D_{g-1}] and [E_{g-1}; ...; E_1], exact in INT32
-//             (|P_g| <= 8 * 127 * 64 * n < 2^31 for n <= 8192 * 4)
+//             operands [D_1 | ... | D_{g-1}] and [E_{g-1}; ...; E_1], exact in INT32:
+//             |P_g| <= (2 * 127 * 64 + (S - 2) * 64 * 64) * n < 2^31 for n <= 47800 (S = 9)
 //   combine   Z_ij = sum_g 2^(sig_i + tau_j - 7g) P_g,ij, in FP64, smallest groups first
 //   finish    the hot path's FP64 epilogue (store / residual / update partials, epilogue.cuh) on Z
 //

@@ -39,7 +39,7 @@ def run(A, p, phases, label, max_iters=400, form="literal", tol=1e-12):
     rmin, kmin = min(fin) if fin else (float("nan"), -1)
     per = {}
     for t in tr:
-        native = {"fp64": 52, "bf16": 7, "tf32": 10, "fp16": 10}[t["prec"]]
+        native = {"fp64": 52, "fp64oz": 52, "bf16": 7, "tf32": 10, "fp16": 10, "fp8": 3, "int8": 7}[t["prec"]]
         d = per.setdefault(t["prec"] + ("" if t["mant_bits"] == native else f"/m{t['mant_bits']}"),
                            {"iters": 0, "ms": 0.0, "gemms": 0})
         d["iters"] += 1
@@ -109,6 +109,29 @@ def main():
                 ph = [ipr.make_phase(low, switch_tol=1e-2 * math.sqrt(n), plateau_ratio=0.7, plateau_arm=0.1,
                                      max_iters=80), ipr.make_phase("fp64", max_iters=200)]
                 recs.append(run(A, 1, ph, lab + f" {low}->fp64", form="ns", tol=tol))
+            del A
+            torch.cuda.empty_cache()
+    # NEXT-2: the symmetrised (R-22) / tri and coupled (R-27) forms, Ozaki FP64 with per-iteration
+    # digits (R-23, R-26) where it fits (n <= 8192); stated kappa and the kappa = 2 twin
+    import bench
+    for name in ["C1", "C3", "C4", "C5"]:
+        key = "N2-" + name
+        if not want(key):
+            continue
+        c = synth.CONFIGS[name]
+        n, p, kap, seed = c["n"], c["p"], c["kappa"], c["seed"]
+        sym = "symtri" if p == 2 else "sym"
+        for kappa, tag in [(kap, "stated"), (2.0, "twin")]:
+            A, _ = synth.spd_torch(n, kappa, seed) if n >= 4096 else (torch.from_numpy(synth.spd(n, kappa, seed)).cuda(), None)
+            lab = f"{name} n={n} p={p} kappa={kappa:g} ({tag})"
+            runs = [(f"{sym}:fp64/cbf16", 1e-12)]
+            runs.append((f"{sym}:bf16>fp64oz@a/cbf16" if (n <= 8192 and p == 2) else f"{sym}:bf16>fp64/cbf16", 1e-12))
+            if tag == "stated":
+                runs.append(("cpl:fp64", 1e-6))
+            for sched, tol in runs:
+                form, ph = bench.schedule(sched, n)
+                ph[-1].max_iters = 40 if n >= 32768 else 120
+                recs.append(run(A, p, ph, lab + " " + sched, form=form, tol=tol))
             del A
             torch.cuda.empty_cache()
     if a.out:
