@@ -253,42 +253,73 @@ __global__ void __launch_bounds__(256) k_sym_update(const CT *__restrict__ cold,
                                                     void *chat_corr_new, double *part) {
   __shared__ WT t[64][65];
   __shared__ double red[8];
-  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;  // 64 x 4 (1-D block: block_sum_det)
   const int64_t jb = (int64_t)blockIdx.x * 64;             // local column tile
   const int64_t ib = (int64_t)blockIdx.y * 64;             // row tile
   const int64_t slot = npad * kp;
   // mirrored tile: t[r][c] = W(col0 + jb + r, ib + c)
   {
+    const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
     const int64_t gi = ib + tx;
     const WT *src = W + (gi / kp) * slot + gi % kp;
     #pragma unroll
     for (int r = ty; r < 64; r += 4) t[r][tx] = src[(col0 + jb + r) * kp];
   }
   __syncthreads();
+  // 4 consecutive columns x 4 rows per thread: 16-byte (FP32) / 2 x 16-byte (FP64) accesses
+  const int c4 = (threadIdx.x & 15) * 4, ry = threadIdx.x >> 4;   // 16 x 16 threads
   const bool pow2p = (p & (p - 1)) == 0;
   const double tp = (double)(2 * p), itp = 1.0 / tp;
   const WT *wl = W + (col0 / kp) * slot;                  // this rank's slot
   double d2 = 0.0;
-  #pragma unroll 16
-  for (int r = ty; r < 64; r += 4) {
-    const int64_t i = ib + r, jl = jb + tx, ci = i * kp + jl;
-    const double sw = __dadd_rn((double)wl[ci], (double)t[tx][r]);
-    const double e = pow2p ? __dmul_rn(sw, itp) : __ddiv_rn(sw, tp);   // d/(2p); exact recip. for 2^k
-    const double c = (double)cold[ci];
-    const double x = __dadd_rn(c, e);
-    double cn;
-    if (sizeof(CT) == 8) {
-      cn = q_e11(x, m, rtz);
-      ((double *)cnew)[ci] = cn;
+  #pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int r = ry + 16 * u;
+    const int64_t ci = (ib + r) * kp + jb + c4;
+    double wv[4], cv[4], cn[4];
+    if (sizeof(WT) == 4) {
+      const float4 a = *(const float4 *)((const float *)wl + ci);
+      wv[0] = a.x; wv[1] = a.y; wv[2] = a.z; wv[3] = a.w;
     } else {
-      const float f = q_e8(x, m, rtz);
-      ((float *)cnew)[ci] = f;
-      cn = (double)f;
+      const double2 a = *(const double2 *)((const double *)wl + ci), b = *(const double2 *)((const double *)wl + ci + 2);
+      wv[0] = a.x; wv[1] = a.y; wv[2] = b.x; wv[3] = b.y;
     }
-    if (chat_new) store_operand(chat_new, ci, prec, cn, 0);
-    if (chat_corr_new) store_operand(chat_corr_new, ci, corr, cn, 0);
-    const double dd = __dsub_rn(cn, c);
-    d2 = __fma_rn(dd, dd, d2);
+    if (sizeof(CT) == 4) {
+      const float4 a = *(const float4 *)((const float *)cold + ci);
+      cv[0] = a.x; cv[1] = a.y; cv[2] = a.z; cv[3] = a.w;
+    } else {
+      const double2 a = *(const double2 *)((const double *)cold + ci), b = *(const double2 *)((const double *)cold + ci + 2);
+      cv[0] = a.x; cv[1] = a.y; cv[2] = b.x; cv[3] = b.y;
+    }
+    #pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const double sw = __dadd_rn(wv[v], (double)t[c4 + v][r]);
+      const double e = pow2p ? __dmul_rn(sw, itp) : __ddiv_rn(sw, tp);   // d/(2p); exact recip. for 2^k
+      const double x = __dadd_rn(cv[v], e);
+      cn[v] = sizeof(CT) == 8 ? q_e11(x, m, rtz) : (double)q_e8(x, m, rtz);
+      const double dd = __dsub_rn(cn[v], cv[v]);
+      d2 = __fma_rn(dd, dd, d2);
+    }
+    if (sizeof(CT) == 4) {
+      *(float4 *)((float *)cnew + ci) = make_float4((float)cn[0], (float)cn[1], (float)cn[2], (float)cn[3]);
+    } else {
+      *(double2 *)((double *)cnew + ci) = make_double2(cn[0], cn[1]);
+      *(double2 *)((double *)cnew + ci + 2) = make_double2(cn[2], cn[3]);
+    }
+    #pragma unroll
+    for (int o = 0; o < 2; ++o) {                  // the next operands (phase and correction format)
+      void *op = o == 0 ? chat_new : chat_corr_new;
+      const int pr = o == 0 ? prec : corr;
+      if (!op) continue;
+      if (pr == P_BF16) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn((float)cn[0], (float)cn[1]);
+        __nv_bfloat162 hi = __floats2bfloat162_rn((float)cn[2], (float)cn[3]);
+        uint2 w2; w2.x = *(uint32_t *)&lo; w2.y = *(uint32_t *)&hi;
+        *(uint2 *)((__nv_bfloat16 *)op + ci) = w2;
+      } else {
+        #pragma unroll
+        for (int v = 0; v < 4; ++v) store_operand(op, ci + v, pr, cn[v], 0);
+      }
+    }
   }
   const double b = block_sum_det<256>(d2, red);
   if (threadIdx.x == 0) part[((col0 + jb) / 64) * (npad / 64) + blockIdx.y] = b;
