@@ -370,6 +370,41 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
   }
 }
 
+// The hot path's FP64 epilogue on 32 completed FP64 values of one row (the group-2 finish of an
+// Ozaki product): STORE_T (+ mirror for tri), STORE_N, DIAG_MINUS, RESID, F64 -- the modes the
+// FP64_OZ GEMMs use, inline (the generic per-element epi_element spilled and was ~5x slower).
+__device__ __forceinline__ void epi_row_f64(const GemmArgs &g, int64_t row, int64_t col, const double (&v)[32],
+                                            EpiAcc &ea) {
+  const int mode = g.mode;
+  if (mode & EPI_STORE_N) {
+    double2 *dn = (double2 *)((double *)g.nout + row * g.ldn + col);
+    #pragma unroll
+    for (int j = 0; j < 16; ++j) dn[j] = make_double2(v[2 * j], v[2 * j + 1]);
+  }
+  if (mode & EPI_F64) {
+    double2 *dz = (double2 *)(g.zout + row * g.ldz + col);
+    #pragma unroll
+    for (int j = 0; j < 16; ++j) dz[j] = make_double2(v[2 * j], v[2 * j + 1]);
+  }
+  if (!(mode & (EPI_STORE_T | EPI_RESID))) return;
+  #pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int64_t c = col + j, gc = g.col0 + c;
+    if (g.tri && row > gc) continue;
+    const bool mirror = g.tri && row != gc;
+    double w = v[j];
+    if (mode & EPI_DIAG_MINUS) w = __dsub_rn((row == gc && row < g.n) ? g.diag : 0.0, v[j]);
+    if (mode & EPI_STORE_T) {
+      store_operand(g.tout, c * g.ldt + row, g.tprec, w, 0);
+      if (mirror) store_operand(g.tout, row * g.ldt + c, g.tprec, w, 0);
+    }
+    if ((mode & EPI_RESID) && row < g.n && gc < g.n) {
+      const double d = __dsub_rn(row == gc ? 1.0 : 0.0, v[j]);
+      ea.r2 = __fma_rn(mirror ? 2.0 * d : d, d, ea.r2);
+    }
+  }
+}
+
 template <int KIND>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const GemmArgs g) {
@@ -510,10 +545,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
           } else {                                       // group 2: complete Z, then the finish epilogue
             #pragma unroll
             for (int j = 0; j < 32; ++j) {
-              double v = __dmul_rn((double)(int32_t)r[j], pow2(rs + g.oz_csig[c0 + j] - 14));
-              if (gfirst > 2) v = __dadd_rn(zo[j], v);
-              epi_element<-1>(g, row, c0 + j, v, ea);
+              const double pv = __dmul_rn((double)(int32_t)r[j], pow2(rs + g.oz_csig[c0 + j] - 14));
+              zo[j] = gfirst > 2 ? __dadd_rn(zo[j], pv) : pv;
             }
+            epi_row_f64(g, row, c0, zo, ea);
           }
         } else {
           epi_chunk<KIND>(g, row, colb + ch * 32, r, scale, ea);
