@@ -372,7 +372,42 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
 
 // The hot path's FP64 epilogue on 32 completed FP64 values of one row (the group-2 finish of an
 // Ozaki product): STORE_T (+ mirror for tri), STORE_N, DIAG_MINUS, RESID, F64 -- the modes the
-// FP64_OZ GEMMs use, inline (the generic per-element epi_element spilled and was ~5x slower).
+// FP64_OZ GEMMs use.  The store format and the DIAG/RESID/tri path are template parameters: with
+// run-time switches per element the finish was instruction-bound (~1 ms per n = 8192 product).
+template <int TP>   // 0: FP64, 1: BF16, 2: TF32 (tprec of the STORE_T output)
+__device__ __forceinline__ void st_t(void *base, int64_t idx, double w) {
+  if (TP == 0) ((double *)base)[idx] = w;
+  else if (TP == 1) ((__nv_bfloat16 *)base)[idx] = __float2bfloat16_rn((float)w);
+  else ((float *)base)[idx] = to_tf32((float)w);
+}
+template <int TP, bool DR>
+__device__ __forceinline__ void epi_row_t(const GemmArgs &g, int64_t row, int64_t col, const double (&v)[32], EpiAcc &ea) {
+  const int mode = g.mode;
+  if (!DR) {                                    // plain STORE_T
+    if (mode & EPI_STORE_T) {
+      #pragma unroll
+      for (int j = 0; j < 32; ++j) st_t<TP>(g.tout, (col + j) * g.ldt + row, v[j]);
+    }
+    return;
+  }
+  const bool diag = (mode & EPI_DIAG_MINUS) != 0, st = (mode & EPI_STORE_T) != 0, rs = (mode & EPI_RESID) != 0;
+  #pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int64_t c = col + j, gc = g.col0 + c;
+    if (g.tri && row > gc) continue;
+    const bool mirror = g.tri && row != gc;
+    const double dv = (row == gc && row < g.n) ? 1.0 : 0.0;
+    const double w = diag ? __dsub_rn(dv * g.diag, v[j]) : v[j];
+    if (st) {
+      st_t<TP>(g.tout, c * g.ldt + row, w);
+      if (mirror) st_t<TP>(g.tout, row * g.ldt + c, w);
+    }
+    if (rs && row < g.n && gc < g.n) {
+      const double d = __dsub_rn(row == gc ? 1.0 : 0.0, v[j]);
+      ea.r2 = __fma_rn(mirror ? 2.0 * d : d, d, ea.r2);
+    }
+  }
+}
 __device__ __forceinline__ void epi_row_f64(const GemmArgs &g, int64_t row, int64_t col, const double (&v)[32],
                                             EpiAcc &ea) {
   const int mode = g.mode;
@@ -387,21 +422,16 @@ __device__ __forceinline__ void epi_row_f64(const GemmArgs &g, int64_t row, int6
     for (int j = 0; j < 16; ++j) dz[j] = make_double2(v[2 * j], v[2 * j + 1]);
   }
   if (!(mode & (EPI_STORE_T | EPI_RESID))) return;
-  #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int64_t c = col + j, gc = g.col0 + c;
-    if (g.tri && row > gc) continue;
-    const bool mirror = g.tri && row != gc;
-    double w = v[j];
-    if (mode & EPI_DIAG_MINUS) w = __dsub_rn((row == gc && row < g.n) ? g.diag : 0.0, v[j]);
-    if (mode & EPI_STORE_T) {
-      store_operand(g.tout, c * g.ldt + row, g.tprec, w, 0);
-      if (mirror) store_operand(g.tout, row * g.ldt + c, g.tprec, w, 0);
-    }
-    if ((mode & EPI_RESID) && row < g.n && gc < g.n) {
-      const double d = __dsub_rn(row == gc ? 1.0 : 0.0, v[j]);
-      ea.r2 = __fma_rn(mirror ? 2.0 * d : d, d, ea.r2);
-    }
+  const bool dr = (mode & (EPI_DIAG_MINUS | EPI_RESID)) || g.tri;
+  const int tp = is_f64(g.tprec) ? 0 : g.tprec == P_BF16 ? 1 : 2;
+  if (dr) {
+    if (tp == 0) epi_row_t<0, true>(g, row, col, v, ea);
+    else if (tp == 1) epi_row_t<1, true>(g, row, col, v, ea);
+    else epi_row_t<2, true>(g, row, col, v, ea);
+  } else {
+    if (tp == 0) epi_row_t<0, false>(g, row, col, v, ea);
+    else if (tp == 1) epi_row_t<1, false>(g, row, col, v, ea);
+    else epi_row_t<2, false>(g, row, col, v, ea);
   }
 }
 
