@@ -141,3 +141,29 @@ def test_config_c2_level3():
         assert fin_o.min() / 4 <= fin_g.min() <= 4 * fin_o.min()
         assert {out, r.outcome} <= {ipr.IPR_DIVERGED, ipr.IPR_NONFINITE, ipr.IPR_ITER_LIMIT, ipr.IPR_CONVERGED}
         assert (out == ipr.IPR_CONVERGED) == (r.outcome == oracle.CONVERGED)
+
+
+def test_headline_default_schedule_full_size(twin):
+    # bench.py's default (n = 8192, p = 2): BF16, then the Ozaki FP64 phase with per-iteration
+    # digits (R-23, R-26), symmetric-tri form (R-22).  Properties that hold at any size: converged
+    # and certified in-solve, re-certified by the literal chain on DMMA, exactly symmetric C,
+    # C^2 A v = v for probe vectors, and the same answer as the all-DMMA symmetric schedule.
+    import bench
+    A, A_np = twin
+    form, ph = bench.schedule(bench.DEFAULT_SCHEDULE, A.shape[0])
+    s = ipr.Solver(A, 2, ph, 1e-12, form=form)
+    assert s.iterate(200) == ipr.IPR_CONVERGED
+    tr = s.trace()
+    assert tr[-1]["rho_cert"] <= 1e-12
+    assert max(t["digits"] for t in tr) == 9 and min(t["digits"] for t in tr if t["digits"]) < 9
+    assert s.residual(True) <= 2e-12
+    C = s.finalize().cpu().numpy()
+    assert np.array_equal(C, C.T)
+    for v in synth.probe_vectors(A_np.shape[0], 2, 5):
+        w = oracle.matvec(C, oracle.matvec(C, oracle.matvec(A_np, v)))
+        assert np.linalg.norm(w - v) / np.linalg.norm(v) < 1e-12
+    form2, ph2 = bench.schedule("symtri:bf16>fp64/cbf16", A.shape[0])
+    s2 = ipr.Solver(A, 2, ph2, 1e-12, form=form2)
+    assert s2.iterate(200) == ipr.IPR_CONVERGED
+    C2 = s2.finalize().cpu().numpy()
+    assert np.linalg.norm(C - C2) / np.linalg.norm(C2) < 1e-11
