@@ -30,11 +30,12 @@ sys.path.insert(0, ROOT)
 METRIC = "time-to-FP64-residual 1e-12 (n=8192, p=2)"
 # headline schedule (symmetrised-correction form with the upper-triangle GEMM 2, NEXT-2 (i)+(iii),
 # DESIGN.md R-22): a BF16 tensor-core phase, then an FP64-range phase whose GEMMs run on the INT8
-# tensor cores (Ozaki, R-23) with the digit count -- 3..9, i.e. ~17..63 bits -- and the stored bits
-# raised per iteration from the residual (dynamic precision scaling, R-26), a BF16 correction
-# GEMM, and convergence certified on ||I - C^2 A||_F at full FP64 accuracy
-DEFAULT_SCHEDULE = "symtri:bf16>fp64oz@a/cbf16"
-EXTRA_SCHEDULES = ["fp64", "symtri:bf16>fp64oz@23/cbf16>fp64oz/cbf16", "symtri:bf16>fp64oz/cbf16", "sym:fp64oz", "symtri:fp8>bf16>fp64oz@23/cbf16>fp64oz/cbf16",
+# tensor cores by the Ozaki scheme II (CRT over 8-bit moduli, R-28) with the precision -- 3..9
+# digit-equivalents, i.e. 20..62 bits and 7..18 moduli -- and the stored bits raised per iteration
+# from the residual (dynamic precision scaling, R-26), a BF16 correction GEMM, and convergence
+# certified on ||I - C^2 A||_F at full FP64 accuracy
+DEFAULT_SCHEDULE = "symtri:bf16>fp64crt@a/cbf16"
+EXTRA_SCHEDULES = ["fp64", "symtri:bf16>fp64oz@a/cbf16", "sym:fp64crt", "symtri:bf16>fp64oz@23/cbf16>fp64oz/cbf16", "symtri:bf16>fp64oz/cbf16", "sym:fp64oz", "symtri:fp8>bf16>fp64oz@23/cbf16>fp64oz/cbf16",
                    "bf16>fp64", "tf32>fp64", "fp16>fp64", "sym:fp64", "sym:fp64/cbf16", "symtri:fp64/cbf16",
                    "symtri:bf16>fp64/cbf16", "symtri:bf16>tf32>fp64/cbf16", "symtri:fp8>bf16>fp64/cbf16",
                    "symtri:int8>bf16>fp64/cbf16", "symtri:fp16>fp64/cbf16",
@@ -111,7 +112,8 @@ def gemm_peaks():
     return {"fp64": (FP64_PEAK_TFLOPS, FP64_PEAK_SRC), "bf16": (bf16, src), "fp16": (bf16, src + " (fp16 = bf16 rate)"),
             "tf32": (bf16 / 2, src + " x 1/2 (nominal tf32:bf16)"), "fp8": (bf16 * 2, src + " x 2 (nominal fp8:bf16)"),
             "int8": (bf16 * 2, src + " x 2 (nominal int8:bf16)"),
-            "fp64oz": (bf16 * 2, src + " x 2 (INT8 peak; Ozaki FP64 = 45 INT8 digit products)")}
+            "fp64oz": (bf16 * 2, src + " x 2 (INT8 peak; Ozaki FP64 = 45 INT8 digit products)"),
+            "fp64crt": (bf16 * 2, src + " x 2 (INT8 peak; Ozaki-II FP64 = N INT8 modulus products)")}
 
 
 def gemm_count(trace, p):
@@ -333,6 +335,22 @@ def main():
                 "avg_chain_ms": tot_ms / max(n_chains, 1), "gemm_share_of_step": step_gemm_share,
                 "all_gemm_share_of_step": all_ms / (ms * args.steps) if ms > 0 else None}
         traffic_key = "k_gemm_tc_i8_ozaki"
+    elif last == "fp64crt":
+        # dominant kernel: the INT8 tcgen05 GEMMs of the Ozaki-II (CRT) FP64 products -- one n^3 INT8
+        # GEMM per modulus (each record's `moduli`): achieved INT8 TOPS over the whole chains (the
+        # residue splits and the CRT reconstruction / finish passes count as overhead, not credit)
+        mods_tot = sum(t["moduli"] for t in recs)
+        mods = mods_tot / max(n_chains, 1)
+        achieved = mods_tot * fl_chain / (tot_ms * 1e-3) / 1e12 if tot_ms > 0 else None
+        roof = {"bound": "tensor", "kernel": "k_gemm_tc<kind::i8> (Ozaki-II FP64 chain: one INT8 GEMM per CRT modulus "
+                "+ residue split + CRT reconstruction/finish)", "achieved": achieved, "peak": peaks["int8"][0],
+                "unit": "TOPS (int8)", "frac": achieved / peaks["int8"][0] if achieved else None, "traffic": None,
+                "peak_source": peaks["int8"][1], "fp64_equivalent_tflops": achieved / mods if achieved else None,
+                "algorithmic_int8_ops_per_chain_avg": mods * fl_chain, "moduli_per_chain_avg": mods,
+                "chains": n_chains,
+                "avg_chain_ms": tot_ms / max(n_chains, 1), "gemm_share_of_step": step_gemm_share,
+                "all_gemm_share_of_step": all_ms / (ms * args.steps) if ms > 0 else None}
+        traffic_key = "k_gemm_tc_i8_crt"
     else:
         tot_gemms = p * n_chains
         gemm_ms = tot_ms / max(tot_gemms, 1)
@@ -407,12 +425,14 @@ def main():
         # peak of its own dtype (burst figure: a kernel timed alone)
         peaks = gemm_peaks()
         rates, fracs = {}, {}
-        for prec in ["fp64", "fp64oz", "tf32", "bf16", "fp16", "fp8", "int8"]:
+        n_mod = ipr.ipr_test_crt_table(18, 62, n)["n_for"]       # CRT moduli at 9-digit-equivalent bits
+        for prec in ["fp64", "fp64oz", "fp64crt", "tf32", "bf16", "fp16", "fp8", "int8"]:
             gms = ipr.ipr_bench_gemm(prec, n, 2, 5, stream)
             rates[prec] = 2.0 * n ** 3 / (gms * 1e-3) / 1e12
-            # fp64oz: FP64-equivalent TFLOP/s; its tensor-core fraction is that of the 45 INT8
-            # digit products against the INT8 peak
-            fracs[prec] = rates[prec] * (45.0 if prec == "fp64oz" else 1.0) / peaks[prec][0]
+            # fp64oz / fp64crt: FP64-equivalent TFLOP/s; the tensor-core fraction is that of the 45 INT8
+            # digit products / the n_mod INT8 modulus products against the INT8 peak
+            mult = 45.0 if prec == "fp64oz" else float(n_mod) if prec == "fp64crt" else 1.0
+            fracs[prec] = rates[prec] * mult / peaks[prec][0]
         extras["gemm_tflops"] = rates
         extras["gemm_frac_of_peak"] = fracs
         extras["gemm_peaks"] = {k: {"tflops": v[0], "source": v[1]} for k, v in peaks.items()}

@@ -63,11 +63,19 @@ typedef enum {
  *             tensor cores by the Ozaki scheme I (reading R-23): 9 signed 7-bit digits per element
  *             relative to its row / column maximum, the 45 digit products with s + t <= 10 as 9
  *             K-concatenated kind::i8 GEMMs (exact INT32), combined in FP64.  Accuracy at the FP64
- *             GEMM level (not bit-identical to DMMA).  Symmetric forms only, world = 1. */
+ *             GEMM level (not bit-identical to DMMA).  Symmetric forms only, world = 1.
+ * IPR_FP64_CRT: the same FP64 phase with its GEMMs on the INT8 tensor cores by the Ozaki scheme II
+ *             (reading R-28): rows / columns quantised to b-bit integers relative to their maximum
+ *             (b = 7 S - 1 for the phase's digit count S -- the bits S Ozaki digits keep -- capped at 62
+ *             and at what 18 moduli allow at n), the integer product computed exactly modulo N pairwise
+ *             coprime moduli <= 256 (one kind::i8 GEMM each; N = 18 at b = 62, n = 8192) and rebuilt by
+ *             the Chinese remainder theorem in exact sliced FP64 arithmetic.  Error: the quantisation
+ *             only (2^-b relative to the row / column maximum).  Symmetric forms only, world = 1,
+ *             n <= 65535. */
 typedef enum { IPR_FP64 = 0, IPR_TF32 = 1, IPR_BF16 = 2, IPR_FP16 = 3, IPR_FP8 = 4, IPR_INT8 = 5,
-               IPR_FP64_OZ = 6 } ipr_prec;
+               IPR_FP64_OZ = 6, IPR_FP64_CRT = 7 } ipr_prec;
 
-/* ipr_phase.mant_bits = IPR_MANT_ADAPTIVE (IPR_FP64_OZ phases only): dynamic precision inside the
+/* ipr_phase.mant_bits = IPR_MANT_ADAPTIVE (IPR_FP64_OZ / IPR_FP64_CRT phases only): dynamic precision inside the
  * phase (reading R-26, "the necessity of increased precision can be detected at
  * runtime").  Before the chain of C_k the engine picks the Ozaki digits from the residual it
  * expects for C_{k+1}: target = rho_hat_{k-1} q^2 (q = last in-phase contraction rho_{k-1} /
@@ -129,11 +137,13 @@ typedef struct {
   double gemm_ms;    /* device time of this record's GEMMs (chain + update), CUDA events     */
   double upd_ms;     /* the part of gemm_ms spent in the update (GEMM p+1 + its epilogue /    */
                      /* k_sym_update); gemm_ms - upd_ms = the chain's p GEMMs                  */
-  int    digits;     /* IPR_FP64_OZ: Ozaki digits S of this record's chain (S(S+1)/2 INT8      */
-                     /* digit products per FP64 product); 0 otherwise                         */
+  int    digits;     /* IPR_FP64_OZ / _CRT: Ozaki digits S of this record's chain (OZ: S(S+1)/2 */
+                     /* INT8 digit products per FP64 product; CRT: b = 7 S - 1 bits); else 0     */
   double rho_cert;   /* IPR_FORM_SYMMETRIC: ||I - C^p A||_F recomputed in FP64 when the      */
                      /* in-chain rho met final_tol (converged iff rho_cert <= final_tol);    */
                      /* NaN otherwise                                                         */
+  int    moduli;     /* IPR_FP64_CRT: CRT moduli of this record's chain (INT8 GEMMs per FP64   */
+                     /* product); 0 otherwise                                                  */
 } ipr_record;
 
 /* Create a context for an n x n SPD matrix A (FP64, row-major, device, leading dimension

@@ -19,13 +19,13 @@ LIB_PATH = os.path.join(_HERE, "lib", "libipr.so")
 
 IPR_OK, IPR_E_INVALID_ARG, IPR_E_NOT_SYMMETRIC, IPR_E_STATE = 0, 1, 2, 3
 IPR_E_UNSUPPORTED, IPR_E_OOM, IPR_E_CUDA, IPR_E_NCCL = 4, 5, 6, 7
-IPR_FP64, IPR_TF32, IPR_BF16, IPR_FP16, IPR_FP8, IPR_INT8, IPR_FP64_OZ = 0, 1, 2, 3, 4, 5, 6
+IPR_FP64, IPR_TF32, IPR_BF16, IPR_FP16, IPR_FP8, IPR_INT8, IPR_FP64_OZ, IPR_FP64_CRT = 0, 1, 2, 3, 4, 5, 6, 7
 IPR_RNE, IPR_RTZ = 0, 1
-IPR_MANT_ADAPTIVE = -2   # IPR_FP64_OZ phases: Ozaki digits / stored bits chosen per iteration (R-26)
+IPR_MANT_ADAPTIVE = -2   # IPR_FP64_OZ / IPR_FP64_CRT phases: Ozaki digits / stored bits chosen per iteration (R-26)
 IPR_RUNNING, IPR_CONVERGED, IPR_ITER_LIMIT, IPR_DIVERGED, IPR_NONFINITE = 0, 1, 2, 3, 4
 IPR_DEC_CONTINUE, IPR_DEC_SWITCH = 0, 5
 PREC_NAMES = {IPR_FP64: "fp64", IPR_TF32: "tf32", IPR_BF16: "bf16", IPR_FP16: "fp16", IPR_FP8: "fp8",
-              IPR_INT8: "int8", IPR_FP64_OZ: "fp64oz"}
+              IPR_INT8: "int8", IPR_FP64_OZ: "fp64oz", IPR_FP64_CRT: "fp64crt"}
 PREC_BY_NAME = {v: k for k, v in PREC_NAMES.items()}
 OUTCOME_NAMES = {0: "running", 1: "converged", 2: "iter_limit", 3: "diverged", 4: "nonfinite"}
 
@@ -33,7 +33,8 @@ OUTCOME_NAMES = {0: "running", 1: "converged", 2: "iter_limit", 3: "diverged", 4
 EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_get_trace",
             "ipr_get_iterate", "ipr_get_norms", "ipr_finalize", "ipr_last_error",
             "ipr_nccl_unique_id", "ipr_version", "ipr_test_quantize", "ipr_test_gemm",
-            "ipr_launch_count", "ipr_plan", "ipr_set_form", "ipr_bench_gemm", "ipr_bench_gemm_epi"]
+            "ipr_launch_count", "ipr_plan", "ipr_set_form", "ipr_bench_gemm", "ipr_bench_gemm_epi",
+            "ipr_test_set_digits", "ipr_test_crt_table"]
 IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ, IPR_FORM_SYMMETRIC, IPR_FORM_SYMMETRIC_TRI, IPR_FORM_COUPLED = 0, 1, 2, 3, 4
 FORM_BY_NAME = {"literal": IPR_FORM_LITERAL, "newton_schulz": IPR_FORM_NEWTON_SCHULZ, "ns": IPR_FORM_NEWTON_SCHULZ,
                 "symmetric": IPR_FORM_SYMMETRIC, "sym": IPR_FORM_SYMMETRIC,
@@ -57,7 +58,7 @@ class ipr_record(C.Structure):
     _fields_ = [("k", C.c_int), ("phase", C.c_int), ("prec", C.c_int), ("mant_bits", C.c_int),
                 ("decision", C.c_int), ("rho", C.c_double), ("rho_hat", C.c_double),
                 ("delta", C.c_double), ("gemm_ms", C.c_double), ("upd_ms", C.c_double),
-                ("digits", C.c_int), ("rho_cert", C.c_double)]
+                ("digits", C.c_int), ("rho_cert", C.c_double), ("moduli", C.c_int)]
 
 
 def _load():
@@ -85,6 +86,8 @@ def _load():
     L.ipr_set_form.argtypes = [vp, C.c_int]
     L.ipr_bench_gemm.argtypes = [C.c_int, i64, C.c_int, C.c_int, vp, dp]
     L.ipr_bench_gemm_epi.argtypes = [C.c_int, i64, C.c_int, C.c_int, C.c_int, vp, dp]
+    L.ipr_test_set_digits.argtypes = [C.c_int]
+    L.ipr_test_crt_table.argtypes = [C.c_int, C.c_int, i64, C.POINTER(C.c_int), dp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
     for f in EXPORTED:
         if f not in ("ipr_last_error", "ipr_version", "ipr_launch_count"):
             getattr(L, f).restype = C.c_int
@@ -183,7 +186,7 @@ def ipr_get_trace(ctx):
     _check(_lib.ipr_get_trace(ctx, buf, cnt.value, C.byref(cnt)), ctx)
     return [dict(k=r.k, phase=r.phase, prec=PREC_NAMES[r.prec], mant_bits=r.mant_bits,
                  decision=r.decision, rho=r.rho, rho_hat=r.rho_hat, delta=r.delta, gemm_ms=r.gemm_ms,
-                 upd_ms=r.upd_ms, digits=r.digits, rho_cert=r.rho_cert)
+                 upd_ms=r.upd_ms, digits=r.digits, rho_cert=r.rho_cert, moduli=r.moduli)
             for r in buf[:cnt.value]]
 
 
@@ -208,6 +211,23 @@ def ipr_test_quantize(mode: int, x_in, x_out, m: int = 0, round: int = IPR_RNE, 
 
 def ipr_test_gemm(prec: int, n: int, X, Yt, Z, stream=None):
     _check(_lib.ipr_test_gemm(prec, n, _ptr(X), _ptr(Yt), _ptr(Z), _stream(stream)))
+
+
+def ipr_test_set_digits(digits: int):
+    """Ozaki digits S (OZ) / bits b = min(53, 7 S) (CRT) of ipr_test_gemm / ipr_bench_gemm products."""
+    _check(_lib.ipr_test_set_digits(digits))
+
+
+def ipr_test_crt_table(N: int, b: int = 53, n: int = 8192) -> dict:
+    """Host-side CRT constants of N moduli (no GPU): moduli, inverses, sliced weights; n_for = the
+    moduli a product with b bits at order n uses; b_for = the bits of S = b Ozaki-equivalent digits."""
+    iv = (C.c_int * 40)()
+    dv = (C.c_double * 64)()
+    nf, bf = C.c_int(0), C.c_int(0)
+    _check(_lib.ipr_test_crt_table(N, b, n, iv, dv, C.byref(nf), C.byref(bf)))
+    return dict(moduli=list(iv[:N]), inv=list(iv[20:20 + N]),
+                HLR=[tuple(dv[3 * l:3 * l + 3]) for l in range(N)], M_HLR=tuple(dv[54:57]),
+                p2s=(dv[57], dv[58]), n_for=nf.value, b_for=bf.value)
 
 
 def ipr_bench_gemm(prec, n: int, warmup: int = 2, iters: int = 5, stream=None) -> float:

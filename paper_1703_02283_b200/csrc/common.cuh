@@ -14,10 +14,12 @@
 
 namespace ipr {
 
-enum Prec { P_FP64 = 0, P_TF32 = 1, P_BF16 = 2, P_FP16 = 3, P_FP8 = 4, P_INT8 = 5, P_FP64_OZ = 6 };
+enum Prec { P_FP64 = 0, P_TF32 = 1, P_BF16 = 2, P_FP16 = 3, P_FP8 = 4, P_INT8 = 5, P_FP64_OZ = 6, P_FP64_CRT = 7 };
 
-// FP64 storage/operand format (P_FP64_OZ: FP64 values, GEMMs emulated on INT8 tensor cores)
-__host__ __device__ inline bool is_f64(int prec) { return prec == P_FP64 || prec == P_FP64_OZ; }
+// FP64 storage/operand format (P_FP64_OZ / P_FP64_CRT: FP64 values, GEMMs emulated on INT8 tensor
+// cores by the Ozaki scheme I (digits) / II (Chinese remainder theorem))
+__host__ __device__ inline bool is_f64(int prec) { return prec == P_FP64 || prec == P_FP64_OZ || prec == P_FP64_CRT; }
+__host__ __device__ inline bool is_emu(int prec) { return prec == P_FP64_OZ || prec == P_FP64_CRT; }
 // Ozaki scheme I (reading R-23): at most OZ_S digits per operand (a product keeps the digit pairs
 // s + t <= S + 1); an FP64_OZ phase storing m mantissa bits uses S = oz_digits(m) <= OZ_S
 constexpr int OZ_S = 9;
@@ -25,6 +27,31 @@ __host__ __device__ inline int oz_digits(int m) {
   const int s = (m + 12 + 6) / 7;
   return s < 2 ? 2 : s > OZ_S ? OZ_S : s;
 }
+
+// Ozaki scheme II (reading R-28): a product of operands quantised to b-bit integers relative to their
+// row / column maximum (b <= CRT_BMAX) is computed exactly modulo N pairwise coprime
+// moduli m_l <= 256 (one kind::i8 GEMM each, residues in [-128, 127]) and reconstructed by the CRT.
+// The table is per N (the modulus product M_N changes the CRT weights):
+//   X = sum_l v_l W_l, W_l = M_N / m_l, v_l = (u_l inv_l) mod m_l, u_l = (product mod m_l);
+//   W_l = H_l 2^s1 + L_l 2^s2 + R_l with H, L < 2^40 (those partial sums exact in FP64; R rounded
+//   to FP64 when s2 > 53, an absolute error far below the result's own rounding);
+//   P = X - q M_N, q = rint(X / M_N), with M_N = MH 2^s1 + ML 2^s2 + MR sliced the same way.
+constexpr int CRT_MAX = 18, CRT_BMAX = 62;
+struct CrtTab {
+  int m[CRT_MAX];                    // moduli (descending, pairwise coprime)
+  uint32_t mag[CRT_MAX];             // ceil(2^32 / m_l): x mod m_l by one multiply-high
+  int off[CRT_MAX];                  // m_l ceil(2^30 / m_l): makes an INT32 GEMM sum non-negative
+  double invm[CRT_MAX];              // 1 / m_l (RN)
+  float invmf[CRT_MAX];
+  int inv[CRT_MAX + 1][CRT_MAX];     // (M_N / m_l)^-1 mod m_l
+  double H[CRT_MAX + 1][CRT_MAX], L[CRT_MAX + 1][CRT_MAX], R[CRT_MAX + 1][CRT_MAX];
+  double MH[CRT_MAX + 1], ML[CRT_MAX + 1], MR[CRT_MAX + 1], invM[CRT_MAX + 1];
+  double p2s1[CRT_MAX + 1], p2s2[CRT_MAX + 1];
+  double log2M[CRT_MAX + 1];
+};
+const CrtTab &crt_table();                       // host copy (ozaki.cu)
+int crt_moduli(int b, int64_t n);                // smallest N with M_N > 4 n 2^(2b); -1 if none
+int crt_bits(int S, int64_t n);                  // digits S -> bits b = min(7 S - 1, 62, what 18 moduli allow at n)
 
 // Operand formats that carry a per-tensor power-of-two scale 2^sigma (reading R-20; NEXT-3).
 __host__ __device__ inline bool is_scaled(int prec) { return prec == P_FP16 || prec == P_FP8 || prec == P_INT8; }
@@ -87,6 +114,11 @@ struct GemmArgs {
                         // fused into group 2; g.mode holds the FINISH mode
   const int8_t *oz_a;   // A-role digit planes [S][npad][npad] (row-major per plane)
   const int8_t *oz_b;   // B-role digits, per output column j: [S * npad] = digit planes S..1 of column j
+                        // (oz_grouped == 3, CRT: residue planes [crt_n][npad][npad] of both operands)
+  int crt_n;            // oz_grouped == 3: number of moduli (one kind::i8 GEMM each)
+  int crt_l0, crt_l1;   // CRT: the moduli [crt_l0, crt_l1) of this launch (modulus-major)
+  uint8_t *crt_v;       // CRT: v_l of moduli 0..crt_n-1 at crt_v[(l * M + i) * ldv + j]
+  int64_t ldv;
 };
 
 // ------------------------------------------------------------------------------------
@@ -180,7 +212,8 @@ __device__ __forceinline__ int8_t to_int8(double x) {
 __device__ __forceinline__ void store_operand(void *base, int64_t idx, int prec, double v, int sig) {
   switch (prec) {
     case P_FP64:
-    case P_FP64_OZ: ((double *)base)[idx] = v; break;
+    case P_FP64_OZ:
+    case P_FP64_CRT: ((double *)base)[idx] = v; break;
     case P_TF32: ((float *)base)[idx] = to_tf32((float)v); break;
     case P_BF16: ((__nv_bfloat16 *)base)[idx] = __float2bfloat16_rn((float)v); break;
     case P_FP16: ((__half *)base)[idx] = __float2half_rn((float)__dmul_rn(v, pow2(sig))); break;
@@ -230,6 +263,9 @@ extern int64_t g_launches;
 cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s);
 cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s);  // BF16 / FP16 / TF32 / FP8 / INT8
 cudaError_t launch_gemm_ozaki(const GemmArgs &a, cudaStream_t s);  // FP64 on INT8 (ozaki.cu)
+cudaError_t launch_gemm_crt(const GemmArgs &a, cudaStream_t s);    // FP64 on INT8, CRT (ozaki.cu)
+cudaError_t tc_set_crt_table(const CrtTab &t);                      // upload (gemm_tc.cu)
+cudaError_t launch_crt_finish(const GemmArgs &a, cudaStream_t s);  // CRT reconstruction + epilogue
 bool tc_supported(int prec);
 const char *tc_last_error();
 int gemm_tile_n(int prec);   // BN of the kernel used for a precision (partial layout)

@@ -78,6 +78,14 @@ struct ipr_ctx {
   int8_t *ozA = nullptr, *ozC[2] = {nullptr, nullptr}, *ozCb[2] = {nullptr, nullptr}, *ozB = nullptr;
   int *ozA_sig = nullptr, *ozC_sig[2] = {nullptr, nullptr}, *ozB_sig = nullptr;
   double *ozacc = nullptr;
+  // FP64 via the Ozaki scheme II (IPR_FP64_CRT phases, reading R-28): residue planes [CRT_MAX][npad]
+  // [npad] of Ahat, of Chat (per iterate buffer; symmetric, so one set serves both roles) and of the
+  // current B operand, their exponents, the bits b each set was split with (-1: stale), and the
+  // byte scratch of the modulus products
+  int8_t *crA = nullptr, *crC[2] = {nullptr, nullptr}, *crB = nullptr;
+  int *crA_sig = nullptr, *crC_sig[2] = {nullptr, nullptr}, *crB_sig = nullptr;
+  int crA_b = -1, crC_b[2] = {-1, -1};
+  uint8_t *crV = nullptr;
   // coupled form (R-27): Mhat and Nhat K-major local panels (ping-pong), Nhat as the replicated A
   // operand (panel-major), which set is current, and whether the next chain must re-anchor M
   void *cM[2] = {nullptr, nullptr}, *cNk[2] = {nullptr, nullptr}, *cNf = nullptr;
@@ -248,6 +256,7 @@ int64_t tiles_n_total(const ipr_ctx *c, int prec) { return c->npad / gemm_tile_n
 
 cudaError_t run_gemm(ipr_ctx *c, GemmArgs &g) {
   if (g.prec == IPR_FP64_OZ) return launch_gemm_ozaki(g, c->st);
+  if (g.prec == IPR_FP64_CRT) return launch_gemm_crt(g, c->st);
   return g.prec == IPR_FP64 ? launch_gemm_dmma(g, c->st) : launch_gemm_tc(g, c->st);
 }
 
@@ -338,6 +347,39 @@ ipr_status oz_operands(ipr_ctx *c, GemmArgs &g, int i, const void *Xt) {
   g.ozacc = c->ozacc; g.ldoz = c->npad;
   return IPR_OK;
 }
+// Ozaki scheme II (R-28): residues of Ahat / Chat(i) with the bits of the current chain (split only
+// when stale), and of the K-major B operand Xt (split now)
+int crt_bits_now(const ipr_ctx *c) { return crt_bits(oz_S_now(c), c->n); }
+ipr_status crt_ensure_a(ipr_ctx *c, int b) {
+  if (c->crA_b == b) return IPR_OK;
+  CK(launch_crt_split((const double *)c->Aop, c->npad, c->npad, c->npad, b, crt_moduli(b, c->n), c->crA, c->crA_sig,
+                      c->st));
+  c->crA_b = b;
+  return IPR_OK;
+}
+ipr_status crt_ensure_c(ipr_ctx *c, int i, int b) {
+  if (c->crC_b[i] == b) return IPR_OK;
+  CK(launch_crt_split((const double *)c->chat[i], c->npad, c->npad, c->npad, b, crt_moduli(b, c->n), c->crC[i],
+                      c->crC_sig[i], c->st));
+  c->crC_b[i] = b;
+  return IPR_OK;
+}
+void crt_args(ipr_ctx *c, GemmArgs &g, int b) {
+  g.crt_n = crt_moduli(b, c->n);
+  g.crt_v = c->crV;
+}
+// A role: iterate buffer i (or Ahat if i < 0); B role: the rows of the K-major Xt
+ipr_status crt_operands(ipr_ctx *c, GemmArgs &g, int i, const void *Xt) {
+  const int b = crt_bits_now(c);
+  if (i < 0) CKS(crt_ensure_a(c, b));
+  else CKS(crt_ensure_c(c, i, b));
+  CK(launch_crt_split((const double *)Xt, c->npad, c->npad, c->npad, b, crt_moduli(b, c->n), c->crB, c->crB_sig, c->st));
+  g.oz_a = i < 0 ? c->crA : c->crC[i];
+  g.oz_rsig = i < 0 ? c->crA_sig : c->crC_sig[i];
+  g.oz_b = c->crB; g.oz_csig = c->crB_sig;
+  crt_args(c, g, b);
+  return IPR_OK;
+}
 // operand formats that share storage (FP64 and FP64-by-Ozaki both keep Chat in FP64)
 inline bool same_fmt(int a, int b) { return a == b || (is_f64(a) && is_f64(b)); }
 inline bool is_sym(const ipr_ctx *c) { return c->form == IPR_FORM_SYMMETRIC || c->form == IPR_FORM_SYMMETRIC_TRI; }
@@ -381,6 +423,7 @@ ipr_status begin_phase(ipr_ctx *c, bool first) {
   }
   CKS(make_operand(c, c->cur, P));
   c->c_anchor = true;                // coupled form: re-anchor M = X^p A in this phase
+  c->crA_b = -1; c->crC_b[0] = -1; c->crC_b[1] = -1;   // CRT residues: split lazily per chain
   if (P.prec == IPR_FP64_OZ) {   // digits of Ahat (A role) and of Chat (both roles; G = 1, symmetric)
     CK(launch_oz_split((const double *)c->Aop, c->npad, c->npad, c->npad, OZ_S, c->ozA, nullptr, c->ozA_sig, c->st));
     CKS(oz_split_chat(c, c->cur));
@@ -435,7 +478,7 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
     c->oz_S_cur = c->trace.empty() ? OZ_S : oz_digits_for(c->last_rho / std::sqrt((double)c->n) * q * q, c->n);
     c->oz_m_next = oz_adaptive_m(c->oz_S_cur);
   }
-  c->last_chain_S = prec == IPR_FP64_OZ ? oz_S_now(c) : 0;
+  c->last_chain_S = is_emu(prec) ? oz_S_now(c) : 0;
   if (is_sym(c)) {
     // Z_1 = Ahat Chat (A operand: Ahat row-major; B: Chat itself for G = 1 -- exactly symmetric --
     // else the transposed local panel), Z_j = Chat qin(Z_{j-1}); GEMM p: R = I - Z_p in the
@@ -475,6 +518,16 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
           g.ozacc = c->ozacc; g.ldoz = c->npad; g.oz_S = oz_S_now(c);
         } else {
           CKS(oz_operands(c, g, c->cur, c->T[(j - 1) & 1]));
+        }
+      } else if (prec == IPR_FP64_CRT) {
+        if (j == 1) {   // Ahat (A role) x Chat (B role: its rows, by symmetry)
+          const int b = crt_bits_now(c);
+          CKS(crt_ensure_a(c, b));
+          CKS(crt_ensure_c(c, c->cur, b));
+          g.oz_a = c->crA; g.oz_rsig = c->crA_sig; g.oz_b = c->crC[c->cur]; g.oz_csig = c->crC_sig[c->cur];
+          crt_args(c, g, b);
+        } else {
+          CKS(crt_operands(c, g, c->cur, c->T[(j - 1) & 1]));
         }
       }
       CK(run_gemm(c, g));
@@ -612,6 +665,7 @@ ipr_status update_sym(ipr_ctx *c) {
   if (is_scaled(P.prec)) CKS(make_operand(c, nx, P));   // sigma from max|C_{k+1}|, then all-gather
   else CKS(gather_chat(c, nx, P.prec));
   if (P.prec == IPR_FP64_OZ) CKS(oz_split_chat(c, nx));
+  c->crC_b[nx] = -1;
   c->m_of_cur = P.adaptive ? c->oz_m_next : P.m;
   if (!same_fmt(P.corr, P.prec)) CKS(gather_bytes(c, c->chatc[nx], (size_t)(c->npad * c->kp) * elt_size(P.corr), "Chat corr"));
   if (c->world > 1) CKS(make_xt(c, nx, P));
@@ -715,8 +769,9 @@ void free_ctx(ipr_ctx *c) {
 ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
   const size_t full = (size_t)(c->npad * c->npad), panel = (size_t)(c->npad * c->kp);
   const bool cpl = c->form == IPR_FORM_COUPLED;
-  bool fp16 = false, oz = false;        // any scaled-format phase: FP32 T scratch; any Ozaki phase
-  for (auto &P : c->ph) { fp16 |= is_scaled(P.prec); oz |= P.prec == IPR_FP64_OZ; }
+  bool fp16 = false, oz = false, cr = false;   // any scaled-format phase: FP32 T scratch; Ozaki I / II
+  for (auto &P : c->ph) { fp16 |= is_scaled(P.prec); oz |= P.prec == IPR_FP64_OZ; cr |= P.prec == IPR_FP64_CRT; }
+  const size_t crp = cr ? full * CRT_MAX : 0, crs = cr ? (size_t)c->npad * 4 : 0;
   struct Slot { void **p; size_t bytes; };
   const Slot slots[] = {
       {&c->chat[0], full * 8}, {&c->chat[1], full * 8}, {&c->cont[0], panel * 4}, {&c->cont[1], panel * 4},
@@ -733,6 +788,9 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       {(void **)&c->ozA_sig, oz ? (size_t)c->npad * 4 : 0}, {(void **)&c->ozC_sig[0], oz ? (size_t)c->npad * 4 : 0},
       {(void **)&c->ozC_sig[1], oz ? (size_t)c->npad * 4 : 0}, {(void **)&c->ozB_sig, oz ? (size_t)c->npad * 4 : 0},
       {(void **)&c->ozacc, oz ? full * 8 : 0},
+      {(void **)&c->crA, crp}, {(void **)&c->crC[0], crp}, {(void **)&c->crC[1], crp}, {(void **)&c->crB, crp},
+      {(void **)&c->crA_sig, crs}, {(void **)&c->crC_sig[0], crs}, {(void **)&c->crC_sig[1], crs},
+      {(void **)&c->crB_sig, crs}, {(void **)&c->crV, cr ? full * CRT_MAX : 0},
       {&c->cM[0], cpl ? panel * 8 : 0}, {&c->cM[1], cpl ? panel * 8 : 0}, {&c->cNk[0], cpl ? panel * 8 : 0},
       {&c->cNk[1], cpl ? panel * 8 : 0}, {&c->cNf, cpl ? full * 8 : 0},
       {(void **)&c->full64, full * 8}, {&c->Acert, panel * 8}};
@@ -866,14 +924,15 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
   int prev_ob = -1, prev_m = -1;
   for (int i = 0; i < nphases; ++i) {
     const ipr_phase &q = phases[i];
-    if (q.prec < IPR_FP64 || q.prec > IPR_FP64_OZ) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad prec", i);
+    if (q.prec < IPR_FP64 || q.prec > IPR_FP64_CRT) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad prec", i);
     PhaseC P;
     P.prec = q.prec;
     P.cont64 = is_f64(q.prec);
     const int mmax = P.cont64 ? 52 : 23;
-    P.adaptive = q.prec == IPR_FP64_OZ && q.mant_bits == IPR_MANT_ADAPTIVE;
+    P.adaptive = is_emu(q.prec) && q.mant_bits == IPR_MANT_ADAPTIVE;
     if (q.mant_bits < -1 && !P.adaptive)
-      return fail(c, IPR_E_INVALID_ARG, "phase %d: mant_bits %d (IPR_MANT_ADAPTIVE needs IPR_FP64_OZ)", i, q.mant_bits);
+      return fail(c, IPR_E_INVALID_ARG, "phase %d: mant_bits %d (IPR_MANT_ADAPTIVE needs IPR_FP64_OZ / IPR_FP64_CRT)", i,
+                  q.mant_bits);
     P.m = q.mant_bits < 0 ? native_m(q.prec) : q.mant_bits;
     if (P.m > mmax) return fail(c, IPR_E_INVALID_ARG, "phase %d: mant_bits %d > %d for this container", i, P.m, mmax);
     if (q.round != IPR_RNE && q.round != IPR_RTZ) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad round", i);
@@ -885,8 +944,8 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
     P.switch_tol = q.switch_tol; P.plateau_ratio = q.plateau_ratio; P.plateau_arm = q.plateau_arm;
     P.max_iters = q.max_iters;
     P.corr = q.corr_prec >= 0 ? q.corr_prec : is_scaled(q.prec) ? IPR_BF16 : q.prec;
-    if (P.corr < IPR_FP64 || P.corr > IPR_FP64_OZ) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad corr_prec", i);
-    if (P.corr == IPR_FP64_OZ) P.corr = IPR_FP64;   // an FP64 correction runs on DMMA
+    if (P.corr < IPR_FP64 || P.corr > IPR_FP64_CRT) return fail(c, IPR_E_INVALID_ARG, "phase %d: bad corr_prec", i);
+    if (is_emu(P.corr)) P.corr = IPR_FP64;   // an FP64 correction runs on DMMA
     if (P.corr == IPR_FP64 && !is_f64(P.prec))
       return fail(c, IPR_E_INVALID_ARG, "phase %d: an FP64 correction needs an FP64 phase", i);
     const int ob = operand_bits(q.prec);
@@ -926,14 +985,14 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     }
     bool need_c = false;
     for (auto &P : c->ph)
-      if (c->form == IPR_FORM_COUPLED && (is_scaled(P.prec) || P.prec == IPR_FP64_OZ))
+      if (c->form == IPR_FORM_COUPLED && (is_scaled(P.prec) || is_emu(P.prec)))
         return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: the coupled form takes FP64 / TF32 / BF16 phases");
     for (auto &P : c->ph)
       if (P.prec == IPR_FP64_OZ && c->npad > 47800)   // INT32 digit-group sums (ozaki.cu)
         return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ needs n <= 47800 (exact INT32 group sums)");
     for (auto &P : c->ph)
-      if (P.prec == IPR_FP64_OZ && (!is_sym(c) || c->world != 1))
-        return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ phases need a symmetric form and world = 1");
+      if (is_emu(P.prec) && (!is_sym(c) || c->world != 1))
+        return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ / IPR_FP64_CRT phases need a symmetric form and world = 1");
     if (is_sym(c)) {
       if (c->p < 2) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: the symmetric form needs p >= 2 (p = 1: Newton-Schulz)");
       if (c->form == IPR_FORM_SYMMETRIC_TRI && c->p != 2)
@@ -969,7 +1028,8 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     r.k = (int)c->trace.size(); r.phase = phase_now; r.prec = c->ph[phase_now].prec; r.mant_bits = c->m_of_cur;
     r.decision = d; r.rho = rho; r.rho_hat = rho / std::sqrt((double)c->n); r.delta = NAN; r.gemm_ms = ms;
     r.rho_cert = NAN; r.upd_ms = 0.0;
-    r.digits = c->ph[phase_now].prec == IPR_FP64_OZ ? c->last_chain_S : 0;
+    r.digits = is_emu(c->ph[phase_now].prec) ? c->last_chain_S : 0;
+    r.moduli = c->ph[phase_now].prec == IPR_FP64_CRT ? crt_moduli(crt_bits(c->last_chain_S, c->n), c->n) : 0;
     c->trace.push_back(r);
     *iters_done += 1;
     if (d == IPR_DEC_CONVERGED && c->form == IPR_FORM_COUPLED) {
@@ -1085,17 +1145,18 @@ static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho) {
   // in an IPR_FP64_OZ phase the certifying product runs on the same FP64-accurate Ozaki GEMM
   // (9 digits); ipr_residual(certify = 1) recomputes the whole chain on the DMMA pipe
   const void *X = c->Zr;
-  const int prec = c->ph[c->phase].prec == IPR_FP64_OZ ? IPR_FP64_OZ : IPR_FP64;
+  const int prec = is_emu(c->ph[c->phase].prec) ? c->ph[c->phase].prec : IPR_FP64;
   for (int j = 2; j <= c->p; ++j) {
     GemmArgs g = base_args(c, prec, X);
     chat_view(c, i, prec, &g.A, &g.a_kp, &g.a_pstride);
     g.mode = EPI_STORE_T | (j == c->p ? EPI_RESID : 0);
     g.tout = c->T[j & 1]; g.ldt = c->npad; g.part = c->part;
     if (prec == IPR_FP64_OZ) CKS(oz_operands(c, g, i, X));
+    if (prec == IPR_FP64_CRT) CKS(crt_operands(c, g, i, X));
     CK(run_gemm(c, g));
     X = c->T[j & 1];
   }
-  CK(launch_reduce_sum(c->part, tiles_n_total(c, IPR_FP64) * tiles_m(c, IPR_FP64), c->dscal + 2, c->st));
+  CK(launch_reduce_sum(c->part, tiles_n_total(c, prec) * tiles_m(c, prec), c->dscal + 2, c->st));
   CK(cudaMemcpyAsync(c->hscal + 2, c->dscal + 2, 8, cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   *rho = std::sqrt(c->hscal[2]);
@@ -1175,9 +1236,52 @@ ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_
   return IPR_OK;
 }
 
+static int g_test_digits = OZ_S;
+ipr_status ipr_test_set_digits(int digits) {
+  ipr_ctx *c = nullptr;
+  if (digits < 2 || digits > OZ_S) return fail(c, IPR_E_INVALID_ARG, "ipr_test_set_digits: digits in [2, 9]");
+  g_test_digits = digits;
+  return IPR_OK;
+}
+
+ipr_status ipr_test_crt_table(int N, int b, int64_t n, int *out40, double *dout64, int *n_for, int *b_for) {
+  ipr_ctx *c = nullptr;
+  if (N < 1 || N > CRT_MAX || !out40 || !dout64 || !n_for || !b_for)
+    return fail(c, IPR_E_INVALID_ARG, "ipr_test_crt_table: bad arguments");
+  const CrtTab &t = crt_table();
+  for (int l = 0; l < CRT_MAX; ++l) {
+    out40[l] = l < N ? t.m[l] : 0;
+    out40[20 + l] = l < N ? t.inv[N][l] : 0;
+    dout64[3 * l] = l < N ? t.H[N][l] : 0.0;
+    dout64[3 * l + 1] = l < N ? t.L[N][l] : 0.0;
+    dout64[3 * l + 2] = l < N ? t.R[N][l] : 0.0;
+  }
+  dout64[54] = t.MH[N]; dout64[55] = t.ML[N]; dout64[56] = t.MR[N];
+  dout64[57] = t.p2s1[N]; dout64[58] = t.p2s2[N];
+  *n_for = (b >= 2 && b <= CRT_BMAX && n >= 1) ? crt_moduli(b, n) : -1;
+  *b_for = (b >= 2 && b <= OZ_S && n >= 1) ? crt_bits(b, n) : 0;
+  return IPR_OK;
+}
+
+// CRT operands of a test / bench product: residue planes of X (rows) and of Yt's rows
+static cudaError_t crt_test_setup(GemmArgs &g, const void *X, const void *Y, int64_t np, int64_t n, int8_t **oa,
+                                  int8_t **ob, int **sig, uint8_t **v, cudaStream_t s, bool split_y) {
+  const int b = crt_bits(g_test_digits, n), nm = crt_moduli(b, n);
+  if (nm < 0) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMalloc((void **)oa, (size_t)(np * np) * nm);
+  if (e == cudaSuccess) e = cudaMalloc((void **)ob, (size_t)(np * np) * nm);
+  if (e == cudaSuccess) e = cudaMalloc((void **)sig, (size_t)np * 8);
+  if (e == cudaSuccess) e = cudaMalloc((void **)v, (size_t)(np * np) * nm);
+  if (e == cudaSuccess) e = launch_crt_split((const double *)X, np, np, np, b, nm, *oa, *sig, s);
+  if (e == cudaSuccess && split_y) e = launch_crt_split((const double *)Y, np, np, np, b, nm, *ob, *sig + np, s);
+  g.oz_a = *oa; g.oz_rsig = *sig; g.oz_b = *ob; g.oz_csig = *sig + np; g.crt_n = nm; g.crt_v = *v;
+  g.oz_S = g_test_digits;
+  return e;
+}
+
 ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_dev, double *Z_dev, void *stream) {
   ipr_ctx *c = nullptr;
-  if (n <= 0 || !X_dev || !Yt_dev || !Z_dev || prec < 0 || prec > IPR_FP64_OZ)
+  if (n <= 0 || !X_dev || !Yt_dev || !Z_dev || prec < 0 || prec > IPR_FP64_CRT)
     return fail(c, IPR_E_INVALID_ARG, "ipr_test_gemm: bad arguments");
   if (!is_f64(prec) && !tc_supported(prec))
     return fail(c, IPR_E_UNSUPPORTED, "ipr_test_gemm: tcgen05 path for this precision is not built");
@@ -1202,6 +1306,7 @@ ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_
   int8_t *oa = nullptr, *ob = nullptr;
   int *sig = nullptr;
   double *acc = nullptr;
+  uint8_t *cv = nullptr;
   if (prec == IPR_FP64_OZ) {   // Ozaki digits of X (A role, rows) and of Yt's rows (B role)
     e = cudaMalloc(&oa, (size_t)(np * np) * OZ_S);
     if (e == cudaSuccess) e = cudaMalloc(&ob, (size_t)(np * np) * OZ_S);
@@ -1209,14 +1314,17 @@ ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_
     if (e == cudaSuccess) e = cudaMalloc(&acc, (size_t)(np * np) * 8);
     if (e == cudaSuccess) e = launch_oz_split((const double *)X, np, np, np, OZ_S, oa, nullptr, sig, s);
     if (e == cudaSuccess) e = launch_oz_split((const double *)Y, np, np, np, OZ_S, nullptr, ob, sig + np, s);
-    g.oz_a = oa; g.oz_rsig = sig; g.oz_b = ob; g.oz_csig = sig + np; g.ozacc = acc; g.ldoz = np; g.oz_S = OZ_S;
+    g.oz_a = oa; g.oz_rsig = sig; g.oz_b = ob; g.oz_csig = sig + np; g.ozacc = acc; g.ldoz = np; g.oz_S = g_test_digits;
     if (e == cudaSuccess) e = launch_gemm_ozaki(g, s);
+  } else if (prec == IPR_FP64_CRT) {
+    e = crt_test_setup(g, X, Y, np, n, &oa, &ob, &sig, &cv, s, true);
+    if (e == cudaSuccess) e = launch_gemm_crt(g, s);
   } else {
     e = prec == IPR_FP64 ? launch_gemm_dmma(g, s) : launch_gemm_tc(g, s);
   }
   if (e == cudaSuccess) e = launch_unpad_f64(Z, n, np, Z_dev, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cudaFree(X); cudaFree(Y); cudaFree(Z); cudaFree(oa); cudaFree(ob); cudaFree(sig); cudaFree(acc);
+  cudaFree(X); cudaFree(Y); cudaFree(Z); cudaFree(oa); cudaFree(ob); cudaFree(sig); cudaFree(acc); cudaFree(cv);
   if (e != cudaSuccess) return fail(c, IPR_E_CUDA, "ipr_test_gemm: %s %s", cudaGetErrorString(e), tc_last_error());
   return IPR_OK;
 }
@@ -1227,7 +1335,7 @@ ipr_status ipr_bench_gemm(int prec, int64_t n, int warmup, int iters, void *stre
 
 ipr_status ipr_bench_gemm_epi(int prec, int64_t n, int warmup, int iters, int epi, void *stream, double *ms) {
   ipr_ctx *c = nullptr;
-  if (n <= 0 || prec < 0 || prec > IPR_FP64_OZ || warmup < 0 || iters <= 0 || !ms || epi < 0 || epi > 3)
+  if (n <= 0 || prec < 0 || prec > IPR_FP64_CRT || warmup < 0 || iters <= 0 || !ms || epi < 0 || epi > 3)
     return fail(c, IPR_E_INVALID_ARG, "ipr_bench_gemm: bad arguments");
   if (!is_f64(prec) && !tc_supported(prec))
     return fail(c, IPR_E_UNSUPPORTED, "ipr_bench_gemm: tcgen05 path for this precision is not built");
@@ -1261,19 +1369,28 @@ ipr_status ipr_bench_gemm_epi(int prec, int64_t n, int warmup, int iters, int ep
   int8_t *oa = nullptr, *ob = nullptr;
   int *sig = nullptr;
   double *acc = nullptr;
+  uint8_t *cv = nullptr;
+  if (prec == IPR_FP64_CRT) {
+    if (e == cudaSuccess) e = crt_test_setup(g, X, Y, np, n, &oa, &ob, &sig, &cv, s, false);
+    g.mode = mode ? EPI_STORE_T : 0;
+  }
   if (prec == IPR_FP64_OZ) {
     if (e == cudaSuccess) e = cudaMalloc(&oa, (size_t)(np * np) * OZ_S);
     if (e == cudaSuccess) e = cudaMalloc(&ob, (size_t)(np * np) * OZ_S);
     if (e == cudaSuccess) e = cudaMalloc(&sig, (size_t)np * 8);
     if (e == cudaSuccess) e = cudaMalloc(&acc, (size_t)(np * np) * 8);
     if (e == cudaSuccess) e = launch_oz_split((const double *)X, np, np, np, OZ_S, oa, nullptr, sig, s);
-    g.oz_a = oa; g.oz_rsig = sig; g.oz_b = ob; g.oz_csig = sig + np; g.ozacc = acc; g.ldoz = np; g.oz_S = OZ_S;
+    g.oz_a = oa; g.oz_rsig = sig; g.oz_b = ob; g.oz_csig = sig + np; g.ozacc = acc; g.ldoz = np; g.oz_S = g_test_digits;
     g.mode = mode ? EPI_STORE_T : 0;
   }
   auto run = [&]() {
     if (prec == IPR_FP64_OZ) {
       cudaError_t r = launch_oz_split((const double *)Y, np, np, np, OZ_S, nullptr, ob, sig + np, s);
       return r == cudaSuccess ? launch_gemm_ozaki(g, s) : r;
+    }
+    if (prec == IPR_FP64_CRT) {
+      cudaError_t r = launch_crt_split((const double *)Y, np, np, np, crt_bits(g_test_digits, n), g.crt_n, ob, sig + np, s);
+      return r == cudaSuccess ? launch_gemm_crt(g, s) : r;
     }
     return prec == IPR_FP64 ? launch_gemm_dmma(g, s) : launch_gemm_tc(g, s);
   };
@@ -1285,7 +1402,7 @@ ipr_status ipr_bench_gemm_epi(int prec, int64_t n, int warmup, int iters, int ep
   float t = 0.f;
   if (e == cudaSuccess) e = cudaEventElapsedTime(&t, e0, e1);
   if (e == cudaSuccess) *ms = (double)t / iters;
-  cudaFree(X); cudaFree(Y); cudaFree(T); cudaFree(pm); cudaFree(oa); cudaFree(ob); cudaFree(sig); cudaFree(acc);
+  cudaFree(X); cudaFree(Y); cudaFree(T); cudaFree(pm); cudaFree(oa); cudaFree(ob); cudaFree(sig); cudaFree(acc); cudaFree(cv);
   if (e0) cudaEventDestroy(e0);
   if (e1) cudaEventDestroy(e1);
   if (e != cudaSuccess) return fail(c, IPR_E_CUDA, "ipr_bench_gemm: %s %s", cudaGetErrorString(e), tc_last_error());

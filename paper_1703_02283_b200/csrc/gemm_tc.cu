@@ -380,19 +380,19 @@ __device__ __forceinline__ void st_t(void *base, int64_t idx, double w) {
   else if (TP == 1) ((__nv_bfloat16 *)base)[idx] = __float2bfloat16_rn((float)w);
   else ((float *)base)[idx] = to_tf32((float)w);
 }
-template <int TP, bool DR>
-__device__ __forceinline__ void epi_row_t(const GemmArgs &g, int64_t row, int64_t col, const double (&v)[32], EpiAcc &ea) {
+template <int TP, bool DR, int W>
+__device__ __forceinline__ void epi_row_t(const GemmArgs &g, int64_t row, int64_t col, const double (&v)[W], EpiAcc &ea) {
   const int mode = g.mode;
   if (!DR) {                                    // plain STORE_T
     if (mode & EPI_STORE_T) {
       #pragma unroll
-      for (int j = 0; j < 32; ++j) st_t<TP>(g.tout, (col + j) * g.ldt + row, v[j]);
+      for (int j = 0; j < W; ++j) st_t<TP>(g.tout, (col + j) * g.ldt + row, v[j]);
     }
     return;
   }
   const bool diag = (mode & EPI_DIAG_MINUS) != 0, st = (mode & EPI_STORE_T) != 0, rs = (mode & EPI_RESID) != 0;
   #pragma unroll
-  for (int j = 0; j < 32; ++j) {
+  for (int j = 0; j < W; ++j) {
     const int64_t c = col + j, gc = g.col0 + c;
     if (g.tri && row > gc) continue;
     const bool mirror = g.tri && row != gc;
@@ -408,31 +408,198 @@ __device__ __forceinline__ void epi_row_t(const GemmArgs &g, int64_t row, int64_
     }
   }
 }
-__device__ __forceinline__ void epi_row_f64(const GemmArgs &g, int64_t row, int64_t col, const double (&v)[32],
+template <int W = 32>   // W consecutive columns (even)
+__device__ __forceinline__ void epi_row_f64(const GemmArgs &g, int64_t row, int64_t col, const double (&v)[W],
                                             EpiAcc &ea) {
   const int mode = g.mode;
   if (mode & EPI_STORE_N) {
     double2 *dn = (double2 *)((double *)g.nout + row * g.ldn + col);
     #pragma unroll
-    for (int j = 0; j < 16; ++j) dn[j] = make_double2(v[2 * j], v[2 * j + 1]);
+    for (int j = 0; j < W / 2; ++j) dn[j] = make_double2(v[2 * j], v[2 * j + 1]);
   }
   if (mode & EPI_F64) {
     double2 *dz = (double2 *)(g.zout + row * g.ldz + col);
     #pragma unroll
-    for (int j = 0; j < 16; ++j) dz[j] = make_double2(v[2 * j], v[2 * j + 1]);
+    for (int j = 0; j < W / 2; ++j) dz[j] = make_double2(v[2 * j], v[2 * j + 1]);
   }
   if (!(mode & (EPI_STORE_T | EPI_RESID))) return;
   const bool dr = (mode & (EPI_DIAG_MINUS | EPI_RESID)) || g.tri;
   const int tp = is_f64(g.tprec) ? 0 : g.tprec == P_BF16 ? 1 : 2;
   if (dr) {
-    if (tp == 0) epi_row_t<0, true>(g, row, col, v, ea);
-    else if (tp == 1) epi_row_t<1, true>(g, row, col, v, ea);
-    else epi_row_t<2, true>(g, row, col, v, ea);
+    if (tp == 0) epi_row_t<0, true, W>(g, row, col, v, ea);
+    else if (tp == 1) epi_row_t<1, true, W>(g, row, col, v, ea);
+    else epi_row_t<2, true, W>(g, row, col, v, ea);
   } else {
-    if (tp == 0) epi_row_t<0, false>(g, row, col, v, ea);
-    else if (tp == 1) epi_row_t<1, false>(g, row, col, v, ea);
-    else epi_row_t<2, false>(g, row, col, v, ea);
+    if (tp == 0) epi_row_t<0, false, W>(g, row, col, v, ea);
+    else if (tp == 1) epi_row_t<1, false, W>(g, row, col, v, ea);
+    else epi_row_t<2, false, W>(g, row, col, v, ea);
   }
+}
+
+// ---- Ozaki scheme II (CRT, reading R-28; ozaki.cu) ----
+__constant__ CrtTab c_crt;
+cudaError_t tc_set_crt_table(const CrtTab &t) { return cudaMemcpyToSymbol(c_crt, &t, sizeof t); }
+
+// One 32-column chunk of one accumulator row of modulus product l (INT32, exact): the bytes
+// v = ((U mod m_l) inv_l) mod m_l to the crt_v scratch (k_crt_finish reconstructs).  Integer ALU
+// only: x mod m = x - m umulhi(x, ceil(2^32 / m)), exact or one m too far for x < 2^31.
+__device__ __forceinline__ void crt_chunk(const GemmArgs &g, int l, int64_t row, int64_t c0, const uint32_t (&r)[32]) {
+  const int nm = g.crt_n;
+  const int m = c_crt.m[l], off = c_crt.off[l], iv = c_crt.inv[nm][l];
+  const uint32_t mag = c_crt.mag[l];
+  uint32_t pk[8];
+  #pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    uint32_t w = 0;
+    #pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t x = (uint32_t)((int)r[4 * q + u] + off);     // |U| <= 2^14 n <= 2^30 < off
+      int a = (int)(x - __umulhi(x, mag) * (uint32_t)m);
+      a += a < 0 ? m : 0;
+      const uint32_t y = (uint32_t)(a * iv);                        // < 2^16
+      int b = (int)(y - __umulhi(y, mag) * (uint32_t)m);
+      b += b < 0 ? m : 0;
+      w |= (uint32_t)b << (8 * u);
+    }
+    pk[q] = w;
+  }
+  uint4 *dst = (uint4 *)(g.crt_v + ((int64_t)l * g.M + row) * g.ldv + c0);
+  dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+}
+
+// CRT reconstruction + the hot path's FP64 finish epilogue (reading R-28): one block per 128 x 256
+// output tile of the GEMM (tri: the upper-triangle pair tiles only), in two 128-column halves.
+// Lane = 4 consecutive columns (the warp reads 128 contiguous residue bytes per modulus and row),
+// warp = 4 rows of a 32-row slab: Pbar = sum_l v_l W_l - q M_N in sliced FP64 (H, L exact),
+// Z = 2^-(e_i + f_j) Pbar, then the epilogue of epi_row_f64: row-major stores directly, the K-major
+// (transposed) store of the slab through shared memory (row r, column c at r * 161 + c + c / 4:
+// conflict-free both ways).
+constexpr int CRT_FIN_LD = 161;
+__global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
+  extern __shared__ double sm_slab[];          // [32][CRT_FIN_LD]
+  __shared__ double red[8];
+  const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN), g.tri};
+  int tm, tn;
+  sch.get((int)(blockIdx.x >> 1), tm, tn);
+  const int tile_m = tm * 2 + (int)(blockIdx.x & 1);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nm = g.crt_n, mode = g.mode;
+  const bool diag = (mode & EPI_DIAG_MINUS) != 0, st = (mode & EPI_STORE_T) != 0, rsd = (mode & EPI_RESID) != 0;
+  const int tp = is_f64(g.tprec) ? 0 : g.tprec == P_BF16 ? 1 : 2;
+  const double p1 = c_crt.p2s1[nm], p2 = c_crt.p2s2[nm], iM = c_crt.invM[nm];
+  const double MH = c_crt.MH[nm], ML = c_crt.ML[nm], MR = c_crt.MR[nm];
+  double r2 = 0.0;
+  #pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+    const int64_t colb = (int64_t)tn * TC_BN + 128 * half, c0 = colb + 4 * lane;
+    int cs[4];
+    #pragma unroll
+    for (int u = 0; u < 4; ++u) cs[u] = g.oz_csig[c0 + u];
+    #pragma unroll 1
+    for (int slab = 0; slab < 4; ++slab) {
+      #pragma unroll 1
+      for (int i = 0; i < 4; ++i) {
+        const int rl = 4 * w + i;
+        const int64_t row = (int64_t)tile_m * TC_BM + slab * 32 + rl;
+        uint32_t bv[CRT_MAX];
+        #pragma unroll
+        for (int l = 0; l < CRT_MAX; ++l)
+          if (l < nm) bv[l] = *(const uint32_t *)(g.crt_v + ((int64_t)l * g.M + row) * g.ldv + c0);
+        double sh[4], sl[4], sr[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) { sh[u] = 0.0; sl[u] = 0.0; sr[u] = 0.0; }
+        #pragma unroll
+        for (int l = 0; l < CRT_MAX; ++l) {
+          if (l < nm) {
+            const double hh = c_crt.H[nm][l], lh = c_crt.L[nm][l], rh = c_crt.R[nm][l];
+            #pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              // byte -> FP64 without a conversion instruction: (2^52 + v) - 2^52, exact
+              const double v = __dsub_rn(__hiloint2double(0x43300000, (int)__byte_perm(bv[l], 0u, 0x4440 + u)),
+                                         4503599627370496.0);
+              sh[u] = __fma_rn(v, hh, sh[u]);     // integers < 2^53: exact
+              sl[u] = __fma_rn(v, lh, sl[u]);
+              sr[u] = __fma_rn(v, rh, sr[u]);     // exact unless R was rounded (s2 > 53): error << result ulp
+            }
+          }
+        }
+        const int rs = g.oz_rsig[row];
+        double vv[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double xa = __fma_rn(sh[u], p1, __dmul_rn(sl[u], p2));
+          const double q = rint(__dmul_rn(xa, iM));       // X / M_N is within 1/4 of an integer
+          const double dh = __fma_rn(-q, MH, sh[u]), dl = __fma_rn(-q, ML, sl[u]), dr = __fma_rn(-q, MR, sr[u]);
+          const double pb = __dadd_rn(__fma_rn(dh, p1, __dmul_rn(dl, p2)), dr);
+          const int e = rs + cs[u];
+          vv[u] = (e > -1000 && e < 1000) ? __dmul_rn(pb, pow2(-e)) : scalbn(pb, -e);
+        }
+        if (mode & EPI_STORE_N) {
+          double2 *dn = (double2 *)((double *)g.nout + row * g.ldn + c0);
+          dn[0] = make_double2(vv[0], vv[1]); dn[1] = make_double2(vv[2], vv[3]);
+        }
+        if (mode & EPI_F64) {
+          double2 *dz = (double2 *)(g.zout + row * g.ldz + c0);
+          dz[0] = make_double2(vv[0], vv[1]); dz[1] = make_double2(vv[2], vv[3]);
+        }
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t c = c0 + u, gc = g.col0 + c;
+          const bool skip = g.tri && row > gc;            // tri: the lower triangle comes from the mirror
+          const bool mirror = g.tri && row < gc;
+          const double wv = diag ? __dsub_rn((row == gc && row < g.n) ? g.diag : 0.0, vv[u]) : vv[u];
+          if (rsd && !skip && row < g.n && gc < g.n) {
+            const double d = __dsub_rn(row == gc ? 1.0 : 0.0, vv[u]);
+            r2 = __fma_rn(mirror ? 2.0 * d : d, d, r2);
+          }
+          if (st && mirror) {                              // (j, i) of a tri element: row-major in T
+            if (tp == 0) st_t<0>(g.tout, row * g.ldt + c, wv);
+            else if (tp == 1) st_t<1>(g.tout, row * g.ldt + c, wv);
+            else st_t<2>(g.tout, row * g.ldt + c, wv);
+          }
+          sm_slab[rl * CRT_FIN_LD + 5 * lane + u] = wv;   // column 4 lane + u, swizzled + lane
+        }
+      }
+      __syncthreads();
+      if (st) {                                            // K-major store: 32 consecutive rows per warp
+        const int64_t row = (int64_t)tile_m * TC_BM + slab * 32 + lane;
+        #pragma unroll 4
+        for (int j = 0; j < 16; ++j) {
+          const int cl = w * 16 + j;
+          const int64_t c = colb + cl;
+          if (g.tri && row > g.col0 + c) continue;
+          const double v = sm_slab[lane * CRT_FIN_LD + cl + (cl >> 2)];
+          if (tp == 0) st_t<0>(g.tout, c * g.ldt + row, v);
+          else if (tp == 1) st_t<1>(g.tout, c * g.ldt + row, v);
+          else st_t<2>(g.tout, c * g.ldt + row, v);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (rsd) {
+    const double sum = block_sum_det<256>(r2, red);
+    if (threadIdx.x == 0) g.part[((g.col0 + (int64_t)tn * TC_BN) / TC_BN) * g.tiles_m + tile_m] = sum;
+  }
+}
+
+cudaError_t launch_crt_finish(const GemmArgs &a, cudaStream_t s) {
+  const TileSched hs{(int)(a.M / (2 * TC_BM)), (int)(a.N / TC_BN), a.tri};
+  if (a.tri && (a.mode & EPI_RESID)) {   // the tiles below the diagonal are not visited: zero partials
+    cudaError_t z = cudaMemsetAsync(a.part, 0, (size_t)(a.N / TC_BN) * a.tiles_m * sizeof(double), s);
+    if (z != cudaSuccess) return z;
+  }
+  static bool attr = false;
+  const int smem = 32 * CRT_FIN_LD * 8;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_crt_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k_crt_finish<<<2 * hs.count(), 256, smem, s>>>(a);
+  ++g_launches;
+  return cudaGetLastError();
 }
 
 template <int KIND>
@@ -454,12 +621,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN), g.tri};
   const int ntiles = sch.count();
+  // CRT (oz_grouped == 3): moduli [crt_l0, crt_l1) of every tile, modulus-major (all CTA pairs
+  // stream the same residue planes at a time, as in one plain GEMM)
+  const int nitems = (KIND == 3 && g.oz_grouped == 3) ? (g.crt_l1 - g.crt_l0) * ntiles : ntiles;
   // Ozaki grouped launch: groups S+1 .. 2 per tile; otherwise one pass (g0 == g1)
   // oz_grouped == 2: the single group g.oz_g (one launch per group keeps each group's digit planes
   // L2-hot across all CTAs -- measured faster than all groups per tile in one launch)
   const int g0 = g.oz_grouped == 1 ? g.oz_S + 1 : g.oz_grouped == 2 ? g.oz_g : 0;
   const int g1 = g.oz_grouped == 1 ? 2 : g.oz_grouped == 2 ? g.oz_g : 0;
   const int gfirst = g.oz_S + 1;                 // the group that initialises the FP64 accumulator
+  const bool crt = KIND == 3 && g.oz_grouped == 3;
+  const int nsub = crt ? 1 : g0 - g1 + 1;
   const int esz = elt_size(g.prec);
   const int nkb = (int)(g.K * esz / TC_BKB);
   const int bke = TC_BKB / esz;                       // K elements per block
@@ -483,21 +655,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = pair; t < ntiles; t += npairs) {
+      for (int t = pair; t < nitems; t += npairs) {
+        const int lmod = crt ? g.crt_l0 + t / ntiles : 0;
         int tm, tn;
-        sch.get(t, tm, tn);
+        sch.get(crt ? t % ntiles : t, tm, tn);
         const int arow = tm * 2 * TC_BM + (int)rank * TC_BM;
         const int brow = tn * TC_BN + (int)rank * (TC_BN / 2);
-        for (int gi = g0; gi >= g1; --gi) {      // Ozaki groups (one pass otherwise)
-          const int nk = g.oz_grouped ? (int)((int64_t)(gi - 1) * g.a_kp * esz / TC_BKB) : nkb;
-          const int64_t boff = g.oz_grouped ? (int64_t)(OZ_S - gi + 1) * g.a_kp : 0;
+        for (int si = 0; si < nsub; ++si) {      // Ozaki groups / CRT moduli (one pass otherwise)
+          const int gi = g0 - si;
+          const int nk = crt ? (int)(g.a_kp * esz / TC_BKB)
+                             : g.oz_grouped ? (int)((int64_t)(gi - 1) * g.a_kp * esz / TC_BKB) : nkb;
+          const int64_t boff = (g.oz_grouped && !crt) ? (int64_t)(OZ_S - gi + 1) * g.a_kp : 0;
+          const int64_t kpl = crt ? (int64_t)lmod * g.a_kp : 0;      // CRT: residue plane lmod
+          const int brow2 = crt ? lmod * (int)g.N + brow : brow;
           for (int kb = 0; kb < nk; ++kb) {
             mbar_wait(&empty[stage], phase ^ 1);
             uint8_t *sa = smem + stage * TC_STAGE_BYTES, *sb = sa + TC_A_BYTES;
             if (leader) mbar_expect_tx(&full[stage], 2 * TC_STAGE_BYTES);
             const int64_t k0 = (int64_t)kb * bke;
-            tma_load_3d_pair(sa, &mapA, &full[stage], (int)(k0 % g.a_kp), arow, (int)(k0 / g.a_kp));
-            tma_load_2d_pair(sb, &mapB, &full[stage], (int)(boff + k0), brow);
+            tma_load_3d_pair(sa, &mapA, &full[stage], (int)((kpl + k0) % g.a_kp), arow, (int)((kpl + k0) / g.a_kp));
+            tma_load_2d_pair(sb, &mapB, &full[stage], (int)(boff + k0), brow2);
             if (++stage == TC_ST) { stage = 0; phase ^= 1; }
           }
         }
@@ -510,9 +687,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = pair; t < ntiles; t += npairs) {
-        for (int gi = g0; gi >= g1; --gi) {
-          const int nk = g.oz_grouped ? (int)((int64_t)(gi - 1) * g.a_kp * esz / TC_BKB) : nkb;
+      for (int t = pair; t < nitems; t += npairs) {
+        for (int si = 0; si < nsub; ++si) {
+          const int gi = g0 - si;
+          const int nk = crt ? (int)(g.a_kp * esz / TC_BKB)
+                             : g.oz_grouped ? (int)((int64_t)(gi - 1) * g.a_kp * esz / TC_BKB) : nkb;
           const int buf = it & 1;
           mbar_wait_cluster(&tempty[buf], ((it >> 1) & 1) ^ 1);
           tc_fence_after();
@@ -540,10 +719,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
     double scale = 1.0;
     if (g.sigA) scale = pow2(-(*g.sigA + *g.sigB));
     int it = 0;
-    for (int t = pair; t < ntiles; t += npairs)
-    for (int gi = g0; gi >= g1; --gi) {
+    for (int t = pair; t < nitems; t += npairs)
+    for (int si = 0; si < nsub; ++si) {
+      const int gi = g0 - si;
+      const int lmod = crt ? g.crt_l0 + t / ntiles : 0;
       int tm, tn;
-      sch.get(t, tm, tn);
+      sch.get(crt ? t % ntiles : t, tm, tn);
       const int buf = it & 1;
       mbar_wait(&tfull[buf], (it >> 1) & 1);
       tc_fence_after();
@@ -555,7 +736,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       for (int ch = hh * 4; ch < hh * 4 + 4; ++ch) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * TC_BN + ch * 32, r);
-        if (KIND == 3 && g.oz_grouped) {
+        if (crt) {
+          crt_chunk(g, lmod, row, colb + ch * 32, r);
+        } else if (KIND == 3 && g.oz_grouped) {
           // the 32 accumulator values of this row segment are loaded up front (independent loads in
           // flight; a load-add-store chain per element serialised on memory latency)
           const int rs = g.oz_rsig[row];
@@ -587,7 +770,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
-      if (KIND == 3 && g.oz_grouped && gi > 2) { ++it; continue; }   // partials after the finish only
+      if (KIND == 3 && g.oz_grouped && (crt || gi > 2)) { ++it; continue; }   // partials after the finish only
       // per-tile partials: deterministic (fixed shuffle tree, warps summed in order 0..3)
       if ((g.mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE)) || g.pmax) {
         double s = (g.mode & EPI_RESID) ? ea.r2 : ea.d2;
@@ -693,7 +876,9 @@ cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
     }
   }
   {
-    const cuuint64_t dims[2] = {(cuuint64_t)a.K, (cuuint64_t)a.N};
+    // CRT: the residue planes of the B operand stacked along N ([crt_n][N][a_kp])
+    const cuuint64_t dims[2] = {(cuuint64_t)(a.oz_grouped == 3 ? a.a_kp : a.K),
+                                (cuuint64_t)(a.oz_grouped == 3 ? a.N * a.crt_n : a.N)};
     const cuuint64_t strides[1] = {(cuuint64_t)(a.ldb * esz)};
     const cuuint32_t box[2] = {bke, (cuuint32_t)(TC_BN / 2)};
     const cuuint32_t es[2] = {1, 1};
@@ -709,8 +894,8 @@ cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
     return cudaErrorInvalidValue;
   }
   const TileSched hs{(int)(a.M / (2 * TC_BM)), (int)(a.N / TC_BN), a.tri};
-  const int ntiles = hs.count();
-  if (a.tri && (a.mode & EPI_RESID)) {   // the tiles below the diagonal are not visited: zero partials
+  const int ntiles = hs.count() * (a.oz_grouped == 3 ? a.crt_l1 - a.crt_l0 : 1);
+  if (a.tri && (a.mode & EPI_RESID) && a.oz_grouped != 3) {   // the tiles below the diagonal are not visited: zero partials
     cudaError_t z = cudaMemsetAsync(a.part, 0, (size_t)(a.N / TC_BN) * a.tiles_m * sizeof(double), s);
     if (z != cudaSuccess) return z;
   }

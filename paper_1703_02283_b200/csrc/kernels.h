@@ -31,6 +31,8 @@ cudaError_t launch_sym_update(const void *cold, int cont64, void *cnew, const vo
                               void *chat_corr_new, double *part, cudaStream_t s);
 cudaError_t launch_oz_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int S, int8_t *planes,
                             int8_t *bcat, int *sig, cudaStream_t s);
+cudaError_t launch_crt_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int b, int nm, int8_t *planes,
+                             int *sig, cudaStream_t s);
 cudaError_t launch_fill_operand(void *dst, int64_t count, int prec, uint32_t seed, cudaStream_t s);
 cudaError_t launch_test_quant(int mode, const void *in, void *out, int64_t len, int m, int rtz, int sigma,
                               cudaStream_t s);

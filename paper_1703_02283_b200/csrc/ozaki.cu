@@ -18,6 +18,10 @@
 // used here (measured in NumPy against 80-bit long double: Frobenius error 9e-16 vs 8.6e-15 for an
 // FP64 GEMM at n = 512; tests/test_gpu_ozaki.py asserts "no worse than 2x DMMA" on the GPU).
 // K-work: S(S+1)/2 = 45 int8 GEMMs of order n.
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
 #include "epilogue.cuh"
 #include "kernels.h"
@@ -111,6 +115,228 @@ cudaError_t launch_gemm_ozaki(const GemmArgs &g, cudaStream_t s) {
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+}  // namespace ipr
+
+namespace ipr {
+
+// =========================================================================================
+// Ozaki scheme II (reading R-28): FP64 products by the Chinese remainder theorem on INT8 moduli.
+//
+//   quantise  Xbar_ik = rint(2^e_i x_ik), e_i = b - 1 - floor(log2 max_k |x_ik|)  (|Xbar| <= 2^b,
+//             an FP64 integer for any b: x 2^e is exact, rint of a double is a double); the same per column of the right operand (exponent f_j)
+//   products  for l = 1..N: U_l = (Xbar mod m_l)(Ybar mod m_l), symmetric residues in [-128, 127],
+//             ONE kind::i8 GEMM each, exact in INT32 (|U_l| <= 2^14 n < 2^31 for n < 131072)
+//   CRT       Pbar = Xbar Ybar is the unique integer with |Pbar| < M_N / 2 and Pbar = U_l mod m_l:
+//             Pbar = sum_l v_l W_l - q M_N, v_l = (U_l inv_l) mod m_l, W_l = M_N / m_l (exact sliced
+//             FP64 arithmetic, common.cuh CrtTab); M_N > 4 n 2^(2b) >= 4 max |Pbar| fixes q = rint(X / M_N)
+//   scale     Z_ij = 2^-(e_i + f_j) Pbar_ij (exact)
+// Error: only the quantisation, |Xbar_ik - 2^e_i x_ik| <= 1/2, i.e. 2^-b relative to the row maximum.
+// =========================================================================================
+// pairwise coprime moduli <= 256, descending: 2^8, 3*5*17, 11*23, 251, 13*19, then primes and 7*31
+constexpr int kModuli[CRT_MAX] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217, 211, 199, 197, 193,
+                                  191, 181};
+namespace {
+// little multi-word unsigned integer (M_18 ~ 2^141 exceeds 128 bits)
+struct Big {
+  uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  void mul(uint32_t m) { uint64_t c = 0; for (auto &x : w) { c += (uint64_t)x * m; x = (uint32_t)c; c >>= 32; } }
+  uint32_t divmod(uint32_t m) {   // *this /= m, returns the remainder
+    uint64_t r = 0;
+    for (int i = 7; i >= 0; --i) { r = (r << 32) | w[i]; w[i] = (uint32_t)(r / m); r %= m; }
+    return (uint32_t)r;
+  }
+  int bitlen() const { for (int i = 7; i >= 0; --i) if (w[i]) return 32 * i + 32 - __builtin_clz(w[i]); return 0; }
+  uint64_t bits(int lo, int cnt) const {   // bits [lo, lo + cnt) (cnt <= 64)
+    uint64_t v = 0;
+    for (int k = 0; k < cnt; ++k) { const int b = lo + k; if (b < 256 && ((w[b >> 5] >> (b & 31)) & 1u)) v |= 1ull << k; }
+    return v;
+  }
+  long double ld(int below = 256) const {  // value of bits [0, below), as long double
+    long double v = 0.0L;
+    for (int i = 7; i >= 0; --i) {
+      uint32_t x = w[i];
+      if (32 * i >= below) x = 0;
+      else if (32 * i + 32 > below) x &= (uint32_t)((1ull << (below - 32 * i)) - 1);
+      v = v * 4294967296.0L + (long double)x;
+    }
+    return v;
+  }
+};
+int64_t modinv(int64_t a, int64_t m) {   // a^-1 mod m (gcd(a, m) = 1)
+  int64_t g = m, x = 0, x1 = 1, aa = a % m;
+  while (aa) { const int64_t q = g / aa, t = g - q * aa; g = aa; aa = t; const int64_t tx = x - q * x1; x = x1; x1 = tx; }
+  return ((x % m) + m) % m;
+}
+CrtTab make_crt_table() {
+  CrtTab t;
+  memset(&t, 0, sizeof t);
+  for (int l = 0; l < CRT_MAX; ++l) {
+    t.m[l] = kModuli[l];
+    t.invm[l] = 1.0 / (double)kModuli[l];
+    t.invmf[l] = 1.0f / (float)kModuli[l];
+    t.mag[l] = (uint32_t)((((uint64_t)1 << 32) + kModuli[l] - 1) / kModuli[l]);
+    t.off[l] = kModuli[l] * (int)(((1 << 30) + kModuli[l] - 1) / kModuli[l]);
+  }
+  for (int N = 1; N <= CRT_MAX; ++N) {
+    Big M;
+    M.w[0] = 1;
+    for (int l = 0; l < N; ++l) M.mul((uint32_t)kModuli[l]);
+    int E = 0;
+    for (int l = 0; l < N; ++l) { Big W = M; W.divmod((uint32_t)kModuli[l]); E = W.bitlen() > E ? W.bitlen() : E; }
+    // W = H 2^s1 + L 2^s2 + R: H, L < 2^40 exact; R < 2^s2 rounded to FP64 when s2 > 53 (its products
+    // then carry an absolute error ~2^(s2 - 40), far below the result's own rounding 2^(2b + log2 n - 53))
+    const int s1 = E > 40 ? E - 40 : 0, s2 = s1 > 40 ? s1 - 40 : 0;
+    auto slice = [&](const Big &W, double &h, double &lo, double &r) {
+      h = (double)W.bits(s1, 40 + 8);
+      lo = (double)W.bits(s2, s1 - s2);
+      r = (double)W.ld(s2);
+    };
+    for (int l = 0; l < N; ++l) {
+      Big W = M;
+      W.divmod((uint32_t)kModuli[l]);
+      Big Wc = W;
+      t.inv[N][l] = (int)modinv((int64_t)Wc.divmod((uint32_t)kModuli[l]), kModuli[l]);
+      slice(W, t.H[N][l], t.L[N][l], t.R[N][l]);
+    }
+    slice(M, t.MH[N], t.ML[N], t.MR[N]);
+    t.invM[N] = (double)(1.0L / M.ld());
+    t.p2s1[N] = ldexp(1.0, s1);
+    t.p2s2[N] = ldexp(1.0, s2);
+    t.log2M[N] = (double)log2l(M.ld());
+  }
+  return t;
+}
+}  // namespace
+
+const CrtTab &crt_table() {
+  static const CrtTab t = make_crt_table();
+  return t;
+}
+int crt_moduli(int b, int64_t n) {
+  const double need = 2.0 * b + std::log2((double)(n < 1 ? 1 : n)) + 2.0;
+  for (int N = 2; N <= CRT_MAX; ++N)
+    if (crt_table().log2M[N] > need) return N;
+  return -1;
+}
+int crt_bits(int S, int64_t n) {
+  int b = 7 * S - 1 < CRT_BMAX ? 7 * S - 1 : CRT_BMAX;
+  while (b > 2 && crt_moduli(b, n) < 0) --b;
+  return b;
+}
+
+// Symmetric residue byte of y = c2 2^42 + c1 2^21 + c0 - 2^62 modulo the compile-time modulus M
+// (c0, c1, c2 in [0, 2^21): the caller biased y by 2^62).  Integer ALU only, ~7 operations:
+// r = c0 + c1 K1 + c2 K2 + K3 < 2^30 (K3 = h - 2^62 mod M, h = the symmetric offset), u = r mod M
+// by an exact multiply-high (x < 2^30, magic ceil(2^39 / M) < 2^32: error < 2^-9 < 1/M), v = u - h.
+template <int M>
+__device__ __forceinline__ uint32_t crt_res8(uint32_t c0, uint32_t c1, uint32_t c2) {
+  constexpr uint32_t h = M == 256 ? 128 : (M - 1) / 2;
+  constexpr uint32_t K1 = (1u << 21) % M, K2 = (uint32_t)((1ull << 42) % M);
+  constexpr uint32_t K3 = (uint32_t)((h + M - (uint32_t)((1ull << 62) % M)) % M);
+  constexpr uint32_t MAG = (uint32_t)(((1ull << 39) + M - 1) / M);
+  const uint32_t r = c2 * K2 + (c1 * K1 + (c0 + K3));
+  const uint32_t u = r - (__umulhi(r, MAG) >> 7) * (uint32_t)M;
+  return (u - h) & 0xffu;
+}
+template <int L>
+__device__ __forceinline__ void crt_split8(const uint32_t (&c0)[8], const uint32_t (&c1)[8], const uint32_t (&c2)[8],
+                                           int nm, int8_t *dst, int64_t plane) {
+  if constexpr (L < CRT_MAX) {
+    if (L < nm) {
+      uint32_t b[8];
+      #pragma unroll
+      for (int u = 0; u < 8; ++u) b[u] = crt_res8<kModuli[L]>(c0[u], c1[u], c2[u]);
+      const uint32_t lo = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+      const uint32_t hi = __byte_perm(__byte_perm(b[4], b[5], 0x0040), __byte_perm(b[6], b[7], 0x0040), 0x5410);
+      *(uint2 *)(dst + (int64_t)L * plane) = make_uint2(lo, hi);
+      crt_split8<L + 1>(c0, c1, c2, nm, dst, plane);
+    }
+  }
+}
+
+// Residues of the rows of X (FP64, row-major, leading dimension ld): one block per row; plane l of
+// `planes` holds (Xbar mod m_l) at planes[l * rows * cols + r * cols + k]; sig[r] = e_r.
+__global__ void __launch_bounds__(256) k_crt_split(const double *__restrict__ X, int64_t ld, int64_t rows, int64_t cols,
+                                                   int b, int nm, int8_t *planes, int *sig) {
+  __shared__ double red[8];
+  const int64_t r = blockIdx.x;
+  const double *x = X + r * ld;
+  double mx = 0.0;
+  for (int64_t k = threadIdx.x; k < cols; k += blockDim.x) mx = fmax(mx, fabs(x[k]));
+  #pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
+    red[0] = fmax(mx, red[0]);
+  }
+  __syncthreads();
+  mx = red[0];
+  // scaled row maximum in [2^(b-1), 2^b): |Xbar| <= 2^b <= 2^62
+  const int e = (mx > 0.0) ? b - 1 - ilogb(mx) : 0;
+  if (threadIdx.x == 0) sig[r] = e;
+  const double sc = pow2(e);
+  const int64_t plane = rows * cols;
+  for (int64_t k0 = (int64_t)threadIdx.x * 8; k0 < cols; k0 += (int64_t)blockDim.x * 8) {
+    uint32_t c0[8], c1[8], c2[8];
+    const double2 *xp = (const double2 *)(x + k0);
+    #pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double2 t = xp[u >> 1];
+      // Xbar + 2^62 in [0, 2^63): three 21-bit fields
+      const uint64_t y = (uint64_t)__double2ll_rn(__dmul_rn((u & 1) ? t.y : t.x, sc)) + (1ull << 62);
+      c0[u] = (uint32_t)y & 0x1fffffu; c1[u] = (uint32_t)(y >> 21) & 0x1fffffu; c2[u] = (uint32_t)(y >> 42);
+    }
+    crt_split8<0>(c0, c1, c2, nm, planes + r * cols + k0, plane);
+  }
+}
+
+cudaError_t launch_crt_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int b, int nm, int8_t *planes,
+                             int *sig, cudaStream_t s) {
+  if (b < 2 || b > CRT_BMAX || nm < 2 || nm > CRT_MAX || cols % 8) return cudaErrorInvalidValue;
+  k_crt_split<<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, b, nm, planes, sig);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// Z = X Y for a P_FP64_CRT GemmArgs: g.oz_a / g.oz_rsig the residue planes and exponents of X (A
+// role, rows), g.oz_b / g.oz_csig those of the rows of the K-major B operand, g.crt_n moduli,
+// g.crt_v the crt_n x npad x npad byte scratch.  One persistent kind::i8 launch over every modulus,
+// modulus-major (the CTA pairs stream one residue plane pair at a time, L2 reuse as in a plain GEMM;
+// a tile-major order measured 50 GB of DRAM reads per n = 8192 product), each tile's epilogue
+// storing v_l bytes; then k_crt_finish reconstructs and applies the hot path's epilogue g.mode
+// (fused into the last modulus' epilogue it thrashed L1 on the residue loads: 3.4 ms).
+cudaError_t launch_gemm_crt(const GemmArgs &g, cudaStream_t s) {
+  static bool uploaded = false;
+  if (!uploaded) {
+    cudaError_t e = tc_set_crt_table(crt_table());
+    if (e != cudaSuccess) return e;
+    uploaded = true;
+  }
+  if (!g.oz_a || !g.oz_b || !g.oz_rsig || !g.oz_csig || !g.crt_v || g.M != g.K || g.N != g.K || g.crt_n < 2 ||
+      g.crt_n > CRT_MAX)
+    return cudaErrorInvalidValue;
+  const int64_t np = g.K;
+  GemmArgs q = g;
+  q.prec = P_INT8;
+  if (!is_f64(q.tprec) && q.tprec != P_BF16 && q.tprec != P_TF32) q.tprec = P_FP64;
+  q.A = g.oz_a; q.a_kp = np; q.a_pstride = np * np;
+  q.K = (int64_t)g.crt_n * np;                   // map extents: all residue planes
+  q.B = g.oz_b; q.ldb = np;
+  q.oz_grouped = 3;
+  q.sigA = nullptr; q.sigB = nullptr; q.pmax = nullptr;
+  q.ldv = np;
+  static int per = 0;                            // moduli per launch (bounds the drift of the CTA pairs)
+  if (!per) { const char *v = getenv("IPR_CRT_PER"); per = v ? atoi(v) : 2; per = per < 1 ? 1 : per; }
+  for (int l0 = 0; l0 < g.crt_n; l0 += per) {    // residue bytes of every modulus
+    q.crt_l0 = l0; q.crt_l1 = l0 + per < g.crt_n ? l0 + per : g.crt_n;
+    cudaError_t e = launch_gemm_tc(q, s);
+    if (e != cudaSuccess) return e;
+  }
+  return launch_crt_finish(q, s);                // reconstruction + the hot path's epilogue
 }
 
 }  // namespace ipr

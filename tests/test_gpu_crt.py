@@ -1,0 +1,138 @@
+"""GPU parity of IPR_FP64_CRT (reading R-28): FP64 GEMMs on the INT8 tensor cores by the
+Ozaki scheme II -- rows / columns quantised to b-bit integers, the integer product exact modulo
+N pairwise coprime moduli (one kind::i8 GEMM each), Chinese-remainder reconstruction in exact
+sliced FP64 arithmetic.
+
+Kernel level: bit-exact on integer operands that the quantisation keeps (b = 20); at b = 62 the
+error against an extended-precision reference is within the bound of the method (quantisation
+2^-b relative to the row / column maximum, plus the final rounding), and comparable to the FP64
+DMMA product.  Trajectory level: the symmetric forms' FP64 phase on IPR_FP64_CRT within the Level-2
+FP64 tolerance of the oracle (which computes that phase in FP64: oracle.FP64_OZ, the same storage
+rule)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.gpu_util import rel_fro, run_gpu_trajectory
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+ipr = pytest.importorskip("paper_1703_02283_b200")
+
+
+def _gemm(prec, X, Y, digits=9):
+    n = X.shape[0]
+    Z = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    ipr.ipr_test_set_digits(digits)
+    try:
+        ipr.ipr_test_gemm(prec, n, torch.from_numpy(np.ascontiguousarray(X)).cuda(),
+                          torch.from_numpy(np.ascontiguousarray(Y.T)).cuda(), Z)
+    finally:
+        ipr.ipr_test_set_digits(9)
+    return Z.cpu().numpy()
+
+
+@pytest.mark.parametrize("n", [1, 200, 513, 1024])
+def test_crt_integers_exact(n):
+    # digits 3 -> b = 20 bits: |x| <= 2^10 is kept exactly, |Pbar| < 2^53 (exact reconstruction)
+    rng = np.random.default_rng(n)
+    X = rng.integers(-1024, 1025, (n, n)).astype(np.float64)
+    Y = rng.integers(-1024, 1025, (n, n)).astype(np.float64)
+    np.testing.assert_array_equal(_gemm(ipr.IPR_FP64_CRT, X, Y, digits=3), X @ Y)
+
+
+@pytest.mark.parametrize("n,kappa,digits", [(512, 2.0, 9), (1536, 2.0, 9), (1024, 1e3, 9), (777, 2.0, 5)])
+def test_crt_error_within_method_bound(n, kappa, digits):
+    A, lam, Q = synth.spd(n, kappa, 3, return_eig=True)
+    C = (Q * lam ** -0.5) @ Q.T
+    C = (C + C.T) / 2
+    b = ipr.ipr_test_crt_table(18, digits, n)["b_for"]
+    assert b == 7 * digits - 1
+    L = np.longdouble
+    exact = A.astype(L) @ C.astype(L)
+    Z = _gemm(ipr.IPR_FP64_CRT, A, C, digits)
+    err = np.abs(Z.astype(L) - exact)
+    # |xhat - x| <= 2^-b max_k |x_ik| (rows of A), the same for the columns of C; final rounding 2 u
+    ra = np.abs(A).max(axis=1)[:, None].astype(L)
+    cc = np.abs(C).max(axis=0)[None, :].astype(L)
+    bound = 2.0 ** -b * (ra * np.abs(C).sum(axis=0)[None, :] + (np.abs(A).sum(axis=1)[:, None] + n * ra * 2.0 ** -b) * cc)
+    bound = bound * (1 + 1e-12) + 2.0 ** -51 * np.abs(exact)
+    assert np.all(err <= bound), float(np.max(err / bound))
+    if digits == 9:
+        e_cr = np.linalg.norm(err.astype(np.float64))
+        e_dm = np.linalg.norm((_gemm(ipr.IPR_FP64, A, C) - exact).astype(np.float64))
+        assert e_cr <= 2.0 * e_dm, (e_cr, e_dm)
+
+
+def test_crt_matches_digits_scheme():
+    # schemes I and II compute the same FP64 product to within their (FP64-level) errors
+    n = 640
+    A = synth.spd(n, 2.0, 4)
+    C = np.linalg.inv(A)
+    C = (C + C.T) / 2
+    z1, z2 = _gemm(ipr.IPR_FP64_OZ, A, C), _gemm(ipr.IPR_FP64_CRT, A, C)
+    assert np.max(np.abs(z1 - z2)) <= 64 * n * 2.0 ** -53 * np.max(np.abs(A)) * np.max(np.abs(C))
+
+
+@pytest.mark.parametrize("form,sched", [("symmetric", "fp64crt"), ("symmetric_tri", "fp64crt"),
+                                        ("symmetric_tri", "bf16>fp64crt/cbf16")])
+def test_crt_fp64_phase_level2(form, sched):
+    n, p = 520, 2
+    A = synth.spd(n, 2.0, 12)
+    low = dict(plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
+    OPR = {"bf16": oracle.BF16, "fp64crt": oracle.FP64_OZ}
+    pg, po = [], []
+    parts = sched.split(">")
+    for i, part in enumerate(parts):
+        prec, _, corr = part.partition("/c")
+        kw = {} if i == len(parts) - 1 else low
+        pg.append(ipr.make_phase(prec, corr_prec=corr or -1, **kw))
+        po.append(oracle.phase(OPR[prec], corr_prec=OPR[corr] if corr else -1, **kw))
+    oform = oracle.FORM_SYMMETRIC if form == "symmetric" else oracle.FORM_SYMMETRIC_TRI
+    r = oracle.solve(A, p, po, 1e-12, 80, hist=80, form=oform)
+    out, tr, hist, best = run_gpu_trajectory(A, p, pg, 1e-12, 80, form=form)
+    assert out == ipr.IPR_CONVERGED and r.outcome == oracle.CONVERGED
+    assert abs(len(tr) - len(r.records)) <= 1
+    if len(parts) == 1:
+        for k, Ck in hist.items():
+            if k < len(r.records):
+                assert rel_fro(Ck, r.C_hist[k]) <= 1e-10, k
+    else:
+        sw = next(k for k, x in enumerate(r.records) if x["decision"] == oracle.SWITCH)
+        for k in range(1, sw + 1):
+            assert rel_fro(hist[k], r.C_hist[k]) <= 4 * 2.0 ** -7, k
+    assert rel_fro(best, r.C_best) <= 1e-10
+    assert tr[-1]["rho_cert"] <= 1e-12
+    nm = ipr.ipr_test_crt_table(18, 62, n)["n_for"]                            # b = 62 at n = 520
+    assert all(t["moduli"] == nm for t in tr if t["phase"] == len(parts) - 1)
+
+
+def test_crt_adaptive_level2_and_storage_rule():
+    n, p = 520, 2
+    A = synth.spd(n, 2.0, 12)
+    low = dict(plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
+    pg = [ipr.make_phase("bf16", **low), ipr.make_phase("fp64crt", mant_bits=ipr.IPR_MANT_ADAPTIVE, corr_prec="bf16")]
+    po = [oracle.phase(oracle.BF16, **low), oracle.phase(oracle.FP64_OZ, mant_bits=oracle.MANT_ADAPTIVE,
+                                                         corr_prec=oracle.BF16)]
+    r = oracle.solve(A, p, po, 1e-12, 80, hist=80, form=oracle.FORM_SYMMETRIC_TRI)
+    out, tr, hist, best = run_gpu_trajectory(A, p, pg, 1e-12, 80, form="symmetric_tri")
+    assert out == ipr.IPR_CONVERGED and r.outcome == oracle.CONVERGED
+    mg = [t["mant_bits"] for t in tr if t["phase"] == 1]
+    mo = [x["mant_bits"] for x in r.records if x["phase"] == 1]
+    assert len(set(mg)) >= 3 and mg[-1] == 52
+    agree = sum(a == b for a, b in zip(mg, mo))
+    assert agree >= min(len(mg), len(mo)) - 1, (mg, mo)
+    mods = [t["moduli"] for t in tr if t["phase"] == 1]
+    assert mods == sorted(mods) and mods[0] < mods[-1] == ipr.ipr_test_crt_table(18, 62, n)["n_for"]
+    assert rel_fro(best, r.C_best) <= 1e-10
+    assert tr[-1]["rho_cert"] <= 1e-12
+
+
+def test_crt_unsupported_outside_symmetric_forms():
+    A = torch.from_numpy(synth.spd(64, 2.0, 0)).cuda()
+    s = ipr.Solver(A, 2, [ipr.make_phase("fp64crt")], 1e-12)
+    with pytest.raises(ipr.IprError) as e:
+        s.iterate(1)
+    assert e.value.status == ipr.IPR_E_UNSUPPORTED
+    s.close()
