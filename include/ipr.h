@@ -144,6 +144,9 @@ typedef struct {
                      /* NaN otherwise                                                         */
   int    moduli;     /* IPR_FP64_CRT: CRT moduli of this record's chain (INT8 GEMMs per FP64   */
                      /* product); 0 otherwise                                                  */
+  double kern_ms;    /* IPR_FP64_CRT: device time of the chain's kind::i8 modulus GEMM launches  */
+                     /* alone (CUDA events; the residue splits and the CRT reconstruction are   */
+                     /* the rest of gemm_ms - upd_ms); 0 otherwise                              */
 } ipr_record;
 
 /* Create a context for an n x n SPD matrix A (FP64, row-major, device, leading dimension

@@ -46,6 +46,7 @@ struct CrtTab {
   int inv[CRT_MAX + 1][CRT_MAX];     // (M_N / m_l)^-1 mod m_l
   double H[CRT_MAX + 1][CRT_MAX], L[CRT_MAX + 1][CRT_MAX], R[CRT_MAX + 1][CRT_MAX];
   double MH[CRT_MAX + 1], ML[CRT_MAX + 1], MR[CRT_MAX + 1], invM[CRT_MAX + 1];
+  double Lo[CRT_MAX + 1][CRT_MAX], MLo[CRT_MAX + 1];   // (W mod 2^s1) 2^-s1, rounded (two-slice form)
   double p2s1[CRT_MAX + 1], p2s2[CRT_MAX + 1];
   double log2M[CRT_MAX + 1];
 };
@@ -266,6 +267,11 @@ cudaError_t launch_gemm_ozaki(const GemmArgs &a, cudaStream_t s);  // FP64 on IN
 cudaError_t launch_gemm_crt(const GemmArgs &a, cudaStream_t s);    // FP64 on INT8, CRT (ozaki.cu)
 cudaError_t tc_set_crt_table(const CrtTab &t);                      // upload (gemm_tc.cu)
 cudaError_t launch_crt_finish(const GemmArgs &a, cudaStream_t s);  // CRT reconstruction + epilogue
+// Optional device timing of the kind::i8 GEMM launches of CRT products (the roofline's dominant kernel,
+// without the residue splits and the reconstruction): while set on this host thread, launch_gemm_crt
+// records an event pair around its GEMM launches (up to cap pairs; *used counts them).
+struct CrtTimer { cudaEvent_t *ev; int cap; int used; };
+void crt_set_timer(CrtTimer *t);
 bool tc_supported(int prec);
 const char *tc_last_error();
 int gemm_tile_n(int prec);   // BN of the kernel used for a precision (partial layout)

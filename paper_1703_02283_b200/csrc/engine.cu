@@ -104,6 +104,7 @@ struct ipr_ctx {
   double *dscal = nullptr; double *hscal = nullptr;   // [0] rho^2 [1] delta^2 [2] max
   int *dsig = nullptr;                  // [0] sigma_A(phase) [1,2] sigma_C ping-pong [3,4] sigma_T
   double *colsum = nullptr; int *dflag = nullptr;
+  double kern_ms = 0.0;                 // CRT: device time of the last chain's kind::i8 GEMM launches
   int cur = 0;
   int best_loc = -1;                    // 0/1: cont[best_loc] holds the best; 2: `best`; -1 none
   int best_cont64 = 1;
@@ -112,6 +113,8 @@ struct ipr_ctx {
   void *arena = nullptr;                // every O(n^2) buffer: ONE pool allocation at the first ipr_iterate
   void *aux = nullptr;                  // the small device buffers (flag, scalars, sigmas, colsum)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t kev[16] = {};             // CRT: event pairs around the kind::i8 GEMM launches of a chain
+  CrtTimer ktimer{kev, 8, 0};
   bool upd_timed = false;
 };
 
@@ -452,6 +455,9 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
   const int *sigX = scaled ? c->dsig + 0 : nullptr;
   const int64_t tm = tiles_m(c, prec), tn_loc = c->kp / gemm_tile_n(prec);
   double *part = c->part;
+  c->ktimer.used = 0;
+  crt_set_timer(prec == IPR_FP64_CRT ? &c->ktimer : nullptr);
+  struct TimerOff { ~TimerOff() { crt_set_timer(nullptr); } } timer_off;
   CK(cudaEventRecord(c->ev[0], c->st));
   if (c->form == IPR_FORM_NEWTON_SCHULZ) {
     // T = Ahat Xhat (A operand: full row-major Ahat; B: X^T panel), epilogue: residual partials
@@ -586,6 +592,12 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
   CK(cudaStreamSynchronize(c->st));
   float t = 0.f, tu = 0.f;
   CK(cudaEventElapsedTime(&t, c->ev[0], c->ev[1]));
+  c->kern_ms = 0.0;
+  for (int i = 0; i < c->ktimer.used; ++i) {
+    float tk = 0.f;
+    CK(cudaEventElapsedTime(&tk, c->kev[2 * i], c->kev[2 * i + 1]));
+    c->kern_ms += tk;
+  }
   if (c->upd_timed) { CK(cudaEventElapsedTime(&tu, c->ev[2], c->ev[3])); c->upd_timed = false; }
   if (c->pending_delta >= 0) {
     c->trace[c->pending_delta].delta = std::sqrt(c->hscal[1]);
@@ -760,6 +772,7 @@ void free_ctx(ipr_ctx *c) {
   if (c->aux) cudaFreeAsync(c->aux, c->st);
   if (c->hscal) pinned_release(c->hscal);
   for (auto &e : c->ev) if (e) cudaEventDestroy(e);
+  for (auto &e : c->kev) if (e) cudaEventDestroy(e);
   c->comm.destroy();
   delete c;
 }
@@ -889,6 +902,7 @@ ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, 
     if (!c->hscal) TRY(fail(c, IPR_E_OOM, "pinned host slab exhausted (too many live contexts)"));
   }
   for (auto &e : c->ev) TRYC(cudaEventCreate(&e));
+  for (auto &e : c->kev) TRYC(cudaEventCreate(&e));
   TRYC(cudaMemsetAsync(c->dflag, 0, 16, c->st));
   TRYC(cudaMemsetAsync(c->dsig, 0, 32, c->st));
   TRYC(launch_symcheck(A_dev, lda, n, c->dflag, c->st));
@@ -1028,6 +1042,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     r.k = (int)c->trace.size(); r.phase = phase_now; r.prec = c->ph[phase_now].prec; r.mant_bits = c->m_of_cur;
     r.decision = d; r.rho = rho; r.rho_hat = rho / std::sqrt((double)c->n); r.delta = NAN; r.gemm_ms = ms;
     r.rho_cert = NAN; r.upd_ms = 0.0;
+    r.kern_ms = c->ph[phase_now].prec == IPR_FP64_CRT ? c->kern_ms : 0.0;
     r.digits = is_emu(c->ph[phase_now].prec) ? c->last_chain_S : 0;
     r.moduli = c->ph[phase_now].prec == IPR_FP64_CRT ? crt_moduli(crt_bits(c->last_chain_S, c->n), c->n) : 0;
     c->trace.push_back(r);

@@ -471,7 +471,7 @@ __device__ __forceinline__ void crt_chunk(const GemmArgs &g, int l, int64_t row,
 // CRT reconstruction + the hot path's FP64 finish epilogue (reading R-28): one block per 128 x 256
 // output tile of the GEMM (tri: the upper-triangle pair tiles only), in two 128-column halves.
 // Lane = 4 consecutive columns (the warp reads 128 contiguous residue bytes per modulus and row),
-// warp = 4 rows of a 32-row slab: Pbar = sum_l v_l W_l - q M_N in sliced FP64 (H, L exact),
+// warp = 4 rows of a 32-row slab: Pbar = sum_l v_l W_l - q M_N in two FP64 slices (H exact, Lo rounded),
 // Z = 2^-(e_i + f_j) Pbar, then the epilogue of epi_row_f64: row-major stores directly, the K-major
 // (transposed) store of the slab through shared memory (row r, column c at r * 161 + c + c / 4:
 // conflict-free both ways).
@@ -487,8 +487,8 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
   const int nm = g.crt_n, mode = g.mode;
   const bool diag = (mode & EPI_DIAG_MINUS) != 0, st = (mode & EPI_STORE_T) != 0, rsd = (mode & EPI_RESID) != 0;
   const int tp = is_f64(g.tprec) ? 0 : g.tprec == P_BF16 ? 1 : 2;
-  const double p1 = c_crt.p2s1[nm], p2 = c_crt.p2s2[nm], iM = c_crt.invM[nm];
-  const double MH = c_crt.MH[nm], ML = c_crt.ML[nm], MR = c_crt.MR[nm];
+  const double p1 = c_crt.p2s1[nm], iM = c_crt.invM[nm];
+  const double MH = c_crt.MH[nm], MLo = c_crt.MLo[nm];
   double r2 = 0.0;
   #pragma unroll 1
   for (int half = 0; half < 2; ++half) {
@@ -499,39 +499,50 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
     #pragma unroll 1
     for (int slab = 0; slab < 4; ++slab) {
       #pragma unroll 1
-      for (int i = 0; i < 4; ++i) {
-        const int rl = 4 * w + i;
-        const int64_t row = (int64_t)tile_m * TC_BM + slab * 32 + rl;
-        uint32_t bv[CRT_MAX];
+      for (int i2 = 0; i2 < 4; i2 += 2) {            // two rows at a time: 16 independent FMA chains
+        uint32_t bv[2][CRT_MAX];
         #pragma unroll
-        for (int l = 0; l < CRT_MAX; ++l)
-          if (l < nm) bv[l] = *(const uint32_t *)(g.crt_v + ((int64_t)l * g.M + row) * g.ldv + c0);
-        double sh[4], sl[4], sr[4];
+        for (int ii = 0; ii < 2; ++ii) {
+          const int64_t row = (int64_t)tile_m * TC_BM + slab * 32 + 4 * w + i2 + ii;
+          #pragma unroll
+          for (int l = 0; l < CRT_MAX; ++l)
+            if (l < nm) bv[ii][l] = *(const uint32_t *)(g.crt_v + ((int64_t)l * g.M + row) * g.ldv + c0);
+        }
+        // two slices: sh = sum v_l H_l exact (< 2^53), so = sum v_l Lo_l (Lo_l = (W_l mod 2^s1) 2^-s1,
+        // rounded: absolute error ~2^(s1 - 45) in Pbar, far below its own last bit at these sizes)
+        double sh[2][4], so[2][4];
         #pragma unroll
-        for (int u = 0; u < 4; ++u) { sh[u] = 0.0; sl[u] = 0.0; sr[u] = 0.0; }
+        for (int ii = 0; ii < 2; ++ii)
+          #pragma unroll
+          for (int u = 0; u < 4; ++u) { sh[ii][u] = 0.0; so[ii][u] = 0.0; }
         #pragma unroll
         for (int l = 0; l < CRT_MAX; ++l) {
           if (l < nm) {
-            const double hh = c_crt.H[nm][l], lh = c_crt.L[nm][l], rh = c_crt.R[nm][l];
+            const double hh = c_crt.H[nm][l], lo = c_crt.Lo[nm][l];
             #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              // byte -> FP64 without a conversion instruction: (2^52 + v) - 2^52, exact
-              const double v = __dsub_rn(__hiloint2double(0x43300000, (int)__byte_perm(bv[l], 0u, 0x4440 + u)),
-                                         4503599627370496.0);
-              sh[u] = __fma_rn(v, hh, sh[u]);     // integers < 2^53: exact
-              sl[u] = __fma_rn(v, lh, sl[u]);
-              sr[u] = __fma_rn(v, rh, sr[u]);     // exact unless R was rounded (s2 > 53): error << result ulp
-            }
+            for (int ii = 0; ii < 2; ++ii)
+              #pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                // byte -> FP64 without a conversion instruction: (2^52 + v) - 2^52, exact
+                const double v = __dsub_rn(__hiloint2double(0x43300000, (int)__byte_perm(bv[ii][l], 0u, 0x4440 + u)),
+                                           4503599627370496.0);
+                sh[ii][u] = __fma_rn(v, hh, sh[ii][u]);
+                so[ii][u] = __fma_rn(v, lo, so[ii][u]);
+              }
           }
         }
+        #pragma unroll
+        for (int ii = 0; ii < 2; ++ii) {
+        const int rl = 4 * w + i2 + ii;
+        const int64_t row = (int64_t)tile_m * TC_BM + slab * 32 + rl;
         const int rs = g.oz_rsig[row];
         double vv[4];
         #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const double xa = __fma_rn(sh[u], p1, __dmul_rn(sl[u], p2));
-          const double q = rint(__dmul_rn(xa, iM));       // X / M_N is within 1/4 of an integer
-          const double dh = __fma_rn(-q, MH, sh[u]), dl = __fma_rn(-q, ML, sl[u]), dr = __fma_rn(-q, MR, sr[u]);
-          const double pb = __dadd_rn(__fma_rn(dh, p1, __dmul_rn(dl, p2)), dr);
+          const double q = rint(__dmul_rn(__fma_rn(sh[ii][u], p1, __dmul_rn(so[ii][u], p1)), iM));  // within 1/4 of an integer
+          const double dh = __fma_rn(-q, MH, sh[ii][u]);              // exact
+          const double dlo = __fma_rn(-q, MLo, so[ii][u]);
+          const double pb = __dmul_rn(__dadd_rn(dh, dlo), p1);        // (dh + dlo) 2^s1
           const int e = rs + cs[u];
           vv[u] = (e > -1000 && e < 1000) ? __dmul_rn(pb, pow2(-e)) : scalbn(pb, -e);
         }
@@ -559,6 +570,7 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
             else st_t<2>(g.tout, row * g.ldt + c, wv);
           }
           sm_slab[rl * CRT_FIN_LD + 5 * lane + u] = wv;   // column 4 lane + u, swizzled + lane
+        }
         }
       }
       __syncthreads();

@@ -186,21 +186,24 @@ CrtTab make_crt_table() {
     int E = 0;
     for (int l = 0; l < N; ++l) { Big W = M; W.divmod((uint32_t)kModuli[l]); E = W.bitlen() > E ? W.bitlen() : E; }
     // W = H 2^s1 + L 2^s2 + R: H, L < 2^40 exact; R < 2^s2 rounded to FP64 when s2 > 53 (its products
-    // then carry an absolute error ~2^(s2 - 40), far below the result's own rounding 2^(2b + log2 n - 53))
+    // then carry an absolute error ~2^(s2 - 40), far below the result's own rounding 2^(2b + log2 n - 53)).
+    // Lo = L 2^(s2 - s1) + R 2^-s1 = (W mod 2^s1) 2^-s1 rounded to FP64: the two-slice form of the
+    // finish kernel (the rounding of sum v Lo ~2^(s1 - 45), negligible likewise)
     const int s1 = E > 40 ? E - 40 : 0, s2 = s1 > 40 ? s1 - 40 : 0;
-    auto slice = [&](const Big &W, double &h, double &lo, double &r) {
+    auto slice = [&](const Big &W, double &h, double &lo, double &r, double &low) {
       h = (double)W.bits(s1, 40 + 8);
       lo = (double)W.bits(s2, s1 - s2);
       r = (double)W.ld(s2);
+      low = (double)(W.ld(s1) / ldexpl(1.0L, s1));
     };
     for (int l = 0; l < N; ++l) {
       Big W = M;
       W.divmod((uint32_t)kModuli[l]);
       Big Wc = W;
       t.inv[N][l] = (int)modinv((int64_t)Wc.divmod((uint32_t)kModuli[l]), kModuli[l]);
-      slice(W, t.H[N][l], t.L[N][l], t.R[N][l]);
+      slice(W, t.H[N][l], t.L[N][l], t.R[N][l], t.Lo[N][l]);
     }
-    slice(M, t.MH[N], t.ML[N], t.MR[N]);
+    slice(M, t.MH[N], t.ML[N], t.MR[N], t.MLo[N]);
     t.invM[N] = (double)(1.0L / M.ld());
     t.p2s1[N] = ldexp(1.0, s1);
     t.p2s2[N] = ldexp(1.0, s2);
@@ -238,27 +241,26 @@ __device__ __forceinline__ uint32_t crt_res8(uint32_t c0, uint32_t c1, uint32_t 
   constexpr uint32_t MAG = (uint32_t)(((1ull << 39) + M - 1) / M);
   const uint32_t r = c2 * K2 + (c1 * K1 + (c0 + K3));
   const uint32_t u = r - (__umulhi(r, MAG) >> 7) * (uint32_t)M;
-  return (u - h) & 0xffu;
+  return u - h;                                   // the low byte is the residue (packed by PRMT)
 }
 template <int L>
-__device__ __forceinline__ void crt_split8(const uint32_t (&c0)[8], const uint32_t (&c1)[8], const uint32_t (&c2)[8],
+__device__ __forceinline__ void crt_split4(const uint32_t (&c0)[4], const uint32_t (&c1)[4], const uint32_t (&c2)[4],
                                            int nm, int8_t *dst, int64_t plane) {
   if constexpr (L < CRT_MAX) {
     if (L < nm) {
-      uint32_t b[8];
+      uint32_t b[4];
       #pragma unroll
-      for (int u = 0; u < 8; ++u) b[u] = crt_res8<kModuli[L]>(c0[u], c1[u], c2[u]);
-      const uint32_t lo = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
-      const uint32_t hi = __byte_perm(__byte_perm(b[4], b[5], 0x0040), __byte_perm(b[6], b[7], 0x0040), 0x5410);
-      *(uint2 *)(dst + (int64_t)L * plane) = make_uint2(lo, hi);
-      crt_split8<L + 1>(c0, c1, c2, nm, dst, plane);
+      for (int u = 0; u < 4; ++u) b[u] = crt_res8<kModuli[L]>(c0[u], c1[u], c2[u]);
+      *(uint32_t *)(dst + (int64_t)L * plane) =
+          __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+      crt_split4<L + 1>(c0, c1, c2, nm, dst, plane);
     }
   }
 }
 
 // Residues of the rows of X (FP64, row-major, leading dimension ld): one block per row; plane l of
 // `planes` holds (Xbar mod m_l) at planes[l * rows * cols + r * cols + k]; sig[r] = e_r.
-__global__ void __launch_bounds__(256) k_crt_split(const double *__restrict__ X, int64_t ld, int64_t rows, int64_t cols,
+__global__ void __launch_bounds__(256, 4) k_crt_split(const double *__restrict__ X, int64_t ld, int64_t rows, int64_t cols,
                                                    int b, int nm, int8_t *planes, int *sig) {
   __shared__ double red[8];
   const int64_t r = blockIdx.x;
@@ -280,27 +282,30 @@ __global__ void __launch_bounds__(256) k_crt_split(const double *__restrict__ X,
   if (threadIdx.x == 0) sig[r] = e;
   const double sc = pow2(e);
   const int64_t plane = rows * cols;
-  for (int64_t k0 = (int64_t)threadIdx.x * 8; k0 < cols; k0 += (int64_t)blockDim.x * 8) {
-    uint32_t c0[8], c1[8], c2[8];
+  for (int64_t k0 = (int64_t)threadIdx.x * 4; k0 < cols; k0 += (int64_t)blockDim.x * 4) {
+    uint32_t c0[4], c1[4], c2[4];
     const double2 *xp = (const double2 *)(x + k0);
     #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
       const double2 t = xp[u >> 1];
       // Xbar + 2^62 in [0, 2^63): three 21-bit fields
       const uint64_t y = (uint64_t)__double2ll_rn(__dmul_rn((u & 1) ? t.y : t.x, sc)) + (1ull << 62);
       c0[u] = (uint32_t)y & 0x1fffffu; c1[u] = (uint32_t)(y >> 21) & 0x1fffffu; c2[u] = (uint32_t)(y >> 42);
     }
-    crt_split8<0>(c0, c1, c2, nm, planes + r * cols + k0, plane);
+    crt_split4<0>(c0, c1, c2, nm, planes + r * cols + k0, plane);
   }
 }
 
 cudaError_t launch_crt_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int b, int nm, int8_t *planes,
                              int *sig, cudaStream_t s) {
-  if (b < 2 || b > CRT_BMAX || nm < 2 || nm > CRT_MAX || cols % 8) return cudaErrorInvalidValue;
+  if (b < 2 || b > CRT_BMAX || nm < 2 || nm > CRT_MAX || cols % 4) return cudaErrorInvalidValue;
   k_crt_split<<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, b, nm, planes, sig);
   ++g_launches;
   return cudaGetLastError();
 }
+
+thread_local CrtTimer *t_crt_timer = nullptr;
+void crt_set_timer(CrtTimer *t) { t_crt_timer = t; }
 
 // Z = X Y for a P_FP64_CRT GemmArgs: g.oz_a / g.oz_rsig the residue planes and exponents of X (A
 // role, rows), g.oz_b / g.oz_csig those of the rows of the K-major B operand, g.crt_n moduli,
@@ -329,6 +334,9 @@ cudaError_t launch_gemm_crt(const GemmArgs &g, cudaStream_t s) {
   q.oz_grouped = 3;
   q.sigA = nullptr; q.sigB = nullptr; q.pmax = nullptr;
   q.ldv = np;
+  CrtTimer *tm = t_crt_timer;
+  const bool timed = tm && tm->used < tm->cap;
+  if (timed) { cudaError_t e = cudaEventRecord(tm->ev[2 * tm->used], s); if (e != cudaSuccess) return e; }
   static int per = 0;                            // moduli per launch (bounds the drift of the CTA pairs)
   if (!per) { const char *v = getenv("IPR_CRT_PER"); per = v ? atoi(v) : 2; per = per < 1 ? 1 : per; }
   for (int l0 = 0; l0 < g.crt_n; l0 += per) {    // residue bytes of every modulus
@@ -336,6 +344,7 @@ cudaError_t launch_gemm_crt(const GemmArgs &g, cudaStream_t s) {
     cudaError_t e = launch_gemm_tc(q, s);
     if (e != cudaSuccess) return e;
   }
+  if (timed) { cudaError_t e = cudaEventRecord(tm->ev[2 * tm->used + 1], s); if (e != cudaSuccess) return e; ++tm->used; }
   return launch_crt_finish(q, s);                // reconstruction + the hot path's epilogue
 }
 
