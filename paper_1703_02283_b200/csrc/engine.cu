@@ -1068,14 +1068,23 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       // then certify ||I - C_k^p A||_F in FP64 (R-3); continue from C_{k+1} if it misses.
       const int ck = c->cur;
       const bool fast = c->zr_for == ck && c->best_loc == ck;
-      CKS(update_sym(c));
-      c->pending_delta = (int64_t)c->trace.size() - 1;
+      // p = 2 fast path: the certifying GEMM C (C A) needs only its residual partials (no T store),
+      // so R in T[p & 1] survives and the update runs only if the certification misses
+      const bool cert_first = fast && c->p == 2;
+      if (!cert_first) {
+        CKS(update_sym(c));
+        c->pending_delta = (int64_t)c->trace.size() - 1;
+      }
       double rc = NAN;
       if (fast) CKS(certify_from_zr(c, ck, &rc));
       else CKS(certify_best(c, &rc));
       c->trace.back().rho_cert = rc;
       if (!(rc <= c->final_tol)) {
         c->trace.back().decision = IPR_DEC_CONTINUE;
+        if (cert_first) {
+          CKS(update_sym(c));
+          c->pending_delta = (int64_t)c->trace.size() - 1;
+        }
         if (c->world > 1) CKS(make_xt(c, c->cur, c->ph[c->phase]));
         continue;
       }
@@ -1164,7 +1173,7 @@ static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho) {
   for (int j = 2; j <= c->p; ++j) {
     GemmArgs g = base_args(c, prec, X);
     chat_view(c, i, prec, &g.A, &g.a_kp, &g.a_pstride);
-    g.mode = EPI_STORE_T | (j == c->p ? EPI_RESID : 0);
+    g.mode = j == c->p ? EPI_RESID : EPI_STORE_T;     // the last product: residual partials only
     g.tout = c->T[j & 1]; g.ldt = c->npad; g.part = c->part;
     if (prec == IPR_FP64_OZ) CKS(oz_operands(c, g, i, X));
     if (prec == IPR_FP64_CRT) CKS(crt_operands(c, g, i, X));

@@ -184,6 +184,7 @@ cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s) {
     if (a.mode == EPI_STORE_T) return launch_mode<EPI_STORE_T>(a, s);
     if (a.mode == (EPI_STORE_T | EPI_STORE_N)) return launch_mode<EPI_STORE_T | EPI_STORE_N>(a, s);
     if (a.mode == (EPI_STORE_T | EPI_RESID)) return launch_mode<EPI_STORE_T | EPI_RESID>(a, s);
+    if (a.mode == EPI_RESID) return launch_mode<EPI_RESID>(a, s);
     if (a.mode == (EPI_STORE_T | EPI_DIAG_MINUS | EPI_RESID))
       return launch_mode<EPI_STORE_T | EPI_DIAG_MINUS | EPI_RESID>(a, s);
     if (a.mode == EPI_WSTORE) return launch_mode<EPI_WSTORE>(a, s);
