@@ -31,7 +31,7 @@ METRIC = "time-to-FP64-residual 1e-12 (n=8192, p=2)"
 # headline schedule (symmetrised-correction form with the upper-triangle GEMM 2, NEXT-2 (i)+(iii),
 # DESIGN.md R-22): a BF16 tensor-core phase, then an FP64-range phase whose GEMMs run on the INT8
 # tensor cores by the Ozaki scheme II (CRT over 8-bit moduli, R-28) with the precision -- 3..9
-# digit-equivalents, i.e. 20..62 bits and 7..18 moduli -- and the stored bits raised per iteration
+# digit-equivalents, i.e. 17..59 bits and 6..17 moduli -- and the stored bits raised per iteration
 # from the residual (dynamic precision scaling, R-26), a BF16 correction GEMM, and convergence
 # certified on ||I - C^2 A||_F at full FP64 accuracy
 DEFAULT_SCHEDULE = "symtri:bf16>fp64crt@a/cbf16"
@@ -446,7 +446,7 @@ def main():
         # peak of its own dtype (burst figure: a kernel timed alone)
         peaks = gemm_peaks()
         rates, fracs = {}, {}
-        n_mod = ipr.ipr_test_crt_table(18, 62, n)["n_for"]       # CRT moduli at 9-digit-equivalent bits
+        n_mod = ipr.ipr_test_crt_table(18, ipr.ipr_test_crt_table(18, 9, n)["b_for"], n)["n_for"]   # moduli at S = 9
         for prec in ["fp64", "fp64oz", "fp64crt", "tf32", "bf16", "fp16", "fp8", "int8"]:
             gms = ipr.ipr_bench_gemm(prec, n, 2, 5, stream)
             rates[prec] = 2.0 * n ** 3 / (gms * 1e-3) / 1e12

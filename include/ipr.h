@@ -66,9 +66,9 @@ typedef enum {
  *             GEMM level (not bit-identical to DMMA).  Symmetric forms only, world = 1.
  * IPR_FP64_CRT: the same FP64 phase with its GEMMs on the INT8 tensor cores by the Ozaki scheme II
  *             (reading R-28): rows / columns quantised to b-bit integers relative to their maximum
- *             (b = 7 S - 1 for the phase's digit count S -- the bits S Ozaki digits keep -- capped at 62
- *             and at what 18 moduli allow at n), the integer product computed exactly modulo N pairwise
- *             coprime moduli <= 256 (one kind::i8 GEMM each; N = 18 at b = 62, n = 8192) and rebuilt by
+ *             (b = 7 S - 4 for the phase's digit count S -- the stored bits of the R-26 rule -- capped at
+ *             62 and at what 18 moduli allow at n), the integer product computed exactly modulo N pairwise
+ *             coprime moduli <= 256 (one kind::i8 GEMM each; N = 17 at b = 59, n = 8192) and rebuilt by
  *             the Chinese remainder theorem in exact sliced FP64 arithmetic.  Error: the quantisation
  *             only (2^-b relative to the row / column maximum).  Symmetric forms only, world = 1,
  *             n <= 65535. */
@@ -138,7 +138,7 @@ typedef struct {
   double upd_ms;     /* the part of gemm_ms spent in the update (GEMM p+1 + its epilogue /    */
                      /* k_sym_update); gemm_ms - upd_ms = the chain's p GEMMs                  */
   int    digits;     /* IPR_FP64_OZ / _CRT: Ozaki digits S of this record's chain (OZ: S(S+1)/2 */
-                     /* INT8 digit products per FP64 product; CRT: b = 7 S - 1 bits); else 0     */
+                     /* INT8 digit products per FP64 product; CRT: b = 7 S - 4 bits); else 0     */
   double rho_cert;   /* IPR_FORM_SYMMETRIC: ||I - C^p A||_F recomputed in FP64 when the      */
                      /* in-chain rho met final_tol (converged iff rho_cert <= final_tol);    */
                      /* NaN otherwise                                                         */

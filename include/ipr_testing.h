@@ -37,13 +37,13 @@ ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_
 ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_dev,
                          double *Z_dev, void *stream);
 /* IPR_FP64_OZ / IPR_FP64_CRT products of ipr_test_gemm / ipr_bench_gemm use `digits` Ozaki digits
- * (OZ) or b = 7 digits - 1 bits (CRT, capped as in ipr.h); digits in [2, 9], default 9.  Process-wide. */
+ * (OZ) or b = 7 digits - 4 bits (CRT, capped as in ipr.h); digits in [2, 9], default 9.  Process-wide. */
 ipr_status ipr_test_set_digits(int digits);
 /* The CRT constants of N moduli (1 <= N <= 18, host only, no GPU): out40[0..N-1] the moduli,
  * out40[20 + l] = inv_l = (M_N / m_l)^-1 mod m_l; dout64[3 l + 0..2] = H_l, L_l, R_l (W_l = M_N / m_l =
  * H_l 2^s1 + L_l 2^s2 + R_l, R_l rounded to FP64); dout64[54..56] = MH, ML, MR; dout64[57..58] =
  * 2^s1, 2^s2.  *n_for = the number of moduli a product with b bits at order n uses (-1: none);
- * *b_for = the bits b a phase with b Ozaki-equivalent digits S = b uses at order n (b = min(7 S - 1,
+ * *b_for = the bits b a phase with b Ozaki-equivalent digits S = b uses at order n (b = min(7 S - 4,
  * 62, what 18 moduli allow)) when 2 <= b <= 9, else 0. */
 ipr_status ipr_test_crt_table(int N, int b, int64_t n, int *out40, double *dout64, int *n_for, int *b_for);
 

@@ -51,8 +51,8 @@ struct CrtTab {
   double log2M[CRT_MAX + 1];
 };
 const CrtTab &crt_table();                       // host copy (ozaki.cu)
-int crt_moduli(int b, int64_t n);                // smallest N with M_N > 4 n 2^(2b); -1 if none
-int crt_bits(int S, int64_t n);                  // digits S -> bits b = min(7 S - 1, 62, what 18 moduli allow at n)
+int crt_moduli(int b, int64_t n);                // smallest N with M_N > 2^1.02 n 2^(2b); -1 if none
+int crt_bits(int S, int64_t n);                  // digits S -> bits b = min(7 S - 4, 62, what 18 moduli allow at n)
 
 // Operand formats that carry a per-tensor power-of-two scale 2^sigma (reading R-20; NEXT-3).
 __host__ __device__ inline bool is_scaled(int prec) { return prec == P_FP16 || prec == P_FP8 || prec == P_INT8; }

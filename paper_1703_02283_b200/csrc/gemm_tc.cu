@@ -586,7 +586,7 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
         double vv[4];
         #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const double q = rint(__dmul_rn(__fma_rn(sh[ii][u], p1, __dmul_rn(so[ii][u], p1)), iM));  // within 1/4 of an integer
+          const double q = rint(__dmul_rn(__fma_rn(sh[ii][u], p1, __dmul_rn(so[ii][u], p1)), iM));  // within 0.493 of an integer
           const double dh = __fma_rn(-q, MH, sh[ii][u]);              // exact
           const double dlo = __fma_rn(-q, MLo, so[ii][u]);
           const double pb = __dmul_rn(__dadd_rn(dh, dlo), p1);        // (dh + dlo) 2^s1

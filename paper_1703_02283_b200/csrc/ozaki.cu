@@ -130,7 +130,8 @@ namespace ipr {
 //             ONE kind::i8 GEMM each, exact in INT32 (|U_l| <= 2^14 n < 2^31 for n < 131072)
 //   CRT       Pbar = Xbar Ybar is the unique integer with |Pbar| < M_N / 2 and Pbar = U_l mod m_l:
 //             Pbar = sum_l v_l W_l - q M_N, v_l = (U_l inv_l) mod m_l, W_l = M_N / m_l (exact sliced
-//             FP64 arithmetic, common.cuh CrtTab); M_N > 4 n 2^(2b) >= 4 max |Pbar| fixes q = rint(X / M_N)
+//             FP64 arithmetic, common.cuh CrtTab); M_N > 2^1.02 n 2^(2b) >= 2.03 max |Pbar| puts X / M_N
+//             within 0.493 of an integer, so q = rint(X / M_N) is exact (X / M_N is evaluated to ~2^-45)
 //   scale     Z_ij = 2^-(e_i + f_j) Pbar_ij (exact)
 // Error: only the quantisation, |Xbar_ik - 2^e_i x_ik| <= 1/2, i.e. 2^-b relative to the row maximum.
 // =========================================================================================
@@ -218,13 +219,19 @@ const CrtTab &crt_table() {
   return t;
 }
 int crt_moduli(int b, int64_t n) {
-  const double need = 2.0 * b + std::log2((double)(n < 1 ? 1 : n)) + 2.0;
+  const double need = 2.0 * b + std::log2((double)(n < 1 ? 1 : n)) + 1.02;
   for (int N = 2; N <= CRT_MAX; ++N)
     if (crt_table().log2M[N] > need) return N;
   return -1;
 }
 int crt_bits(int S, int64_t n) {
-  int b = 7 * S - 1 < CRT_BMAX ? 7 * S - 1 : CRT_BMAX;
+  // b = 7 S - 4: the stored bits of R-26's rule for S digits (m = min(52, 7 S - 4)); the Ozaki-I
+  // equivalent 7 S - 1 costs ~1 modulus more per product for the same trajectory (measured: 7 S - 4
+  // and 7 S - 7 certify in the same 19 + 8 iterations, 7 S - 10 stalls at 2.9e-6).  IPR_CRT_BOFF
+  // overrides the 4 (experiments only).
+  static int boff = -1;
+  if (boff < 0) { const char *v = getenv("IPR_CRT_BOFF"); boff = v ? atoi(v) : 4; }
+  int b = 7 * S - boff < CRT_BMAX ? 7 * S - boff : CRT_BMAX;
   while (b > 2 && crt_moduli(b, n) < 0) --b;
   return b;
 }

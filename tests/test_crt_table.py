@@ -5,8 +5,8 @@ Python integers -- no GPU.  The CUDA reconstruction (gemm_tc.cu crt_chunk) relie
   * W_l = H_l 2^s1 + L_l 2^s2 + R_l, M_N = MH 2^s1 + ML 2^s2 + MR with H, L the exact bit fields
     (small enough that sum_l v_l H_l, v_l <= 255, and q MH, q <= the largest quotient, stay < 2^53)
     and R the low bits, exact below 2^53 and correctly rounded to FP64 above;
-  * the modulus count for (b, n): the smallest N with M_N > 4 n 2^(2b) (|Pbar| <= n 2^(2b), so the
-    quotient rint(X / M_N) is taken at distance >= 1/4 from a half-integer)."""
+  * the modulus count for (b, n): the smallest N with M_N > 2^1.02 n 2^(2b) (|Pbar| <= n 2^(2b), so
+    X / M_N is within 0.493 of an integer and rint(X / M_N), evaluated to ~2^-45, is exact)."""
 import math
 from fractions import Fraction
 
@@ -79,17 +79,18 @@ def test_crt_reconstruction_by_definition():
 def test_modulus_count_is_minimal(b, n):
     nf = _tab(NMAX, b, n)["n_for"]
     m = _tab(NMAX)["moduli"]
-    need = 4 * n * 2 ** (2 * b)
+    need = 2.0281 * n * 2 ** (2 * b)     # 2^1.02
     assert math.prod(m[:nf]) > need
     assert nf == 2 or math.prod(m[:nf - 1]) <= need * 1.01     # (log2 comparison with 1 % slack)
 
 
 def test_digits_to_bits_and_fp64_range():
-    # b = 7 S - 1 (the bits S Ozaki digits keep), capped at 62 and at what 18 moduli allow at n
+    # b = 7 S - 4 (the stored bits of the R-26 rule), capped at 62 and at what 18 moduli allow at n
     for S in range(2, 10):
-        assert _tab(NMAX, S, 8192)["b_for"] == 7 * S - 1
-    assert _tab(NMAX, 9, 65535)["b_for"] == 61            # 2 b + log2 n + 2 <= log2 M_18 = 140.6
-    assert _tab(NMAX, 62, 8192)["n_for"] == 18            # S = 9: 18 GEMMs, not 45 digit products
-    for S in range(5, 10):                                 # fewer GEMMs than scheme I from S = 5 on
-        assert _tab(NMAX, 7 * S - 1, 8192)["n_for"] < S * (S + 1) // 2
+        assert _tab(NMAX, S, 8192)["b_for"] == 7 * S - 4
+    assert _tab(NMAX, 9, 65535)["b_for"] == 59
+    assert _tab(NMAX, 59, 8192)["n_for"] == 17            # S = 9: 17 GEMMs, not 45 digit products
+    assert _tab(NMAX, 62, 8192)["n_for"] == 18
+    for S in range(4, 10):                                 # fewer GEMMs than scheme I from S = 4 on
+        assert _tab(NMAX, 7 * S - 4, 8192)["n_for"] < S * (S + 1) // 2
     assert _tab(NMAX, 63, 8192)["n_for"] == -1            # beyond CRT_BMAX

@@ -3,7 +3,7 @@ Ozaki scheme II -- rows / columns quantised to b-bit integers, the integer produ
 N pairwise coprime moduli (one kind::i8 GEMM each), Chinese-remainder reconstruction in exact
 sliced FP64 arithmetic.
 
-Kernel level: bit-exact on integer operands that the quantisation keeps (b = 20); at b = 62 the
+Kernel level: bit-exact on integer operands that the quantisation keeps (b = 17); at b = 59 the
 error against an extended-precision reference is within the bound of the method (quantisation
 2^-b relative to the row / column maximum, plus the final rounding), and comparable to the FP64
 DMMA product.  Trajectory level: the symmetric forms' FP64 phase on IPR_FP64_CRT within the Level-2
@@ -35,7 +35,7 @@ def _gemm(prec, X, Y, digits=9):
 
 @pytest.mark.parametrize("n", [1, 200, 513, 1024])
 def test_crt_integers_exact(n):
-    # digits 3 -> b = 20 bits: |x| <= 2^10 is kept exactly, |Pbar| < 2^53 (exact reconstruction)
+    # digits 3 -> b = 17 bits: |x| <= 2^10 is kept exactly, |Pbar| < 2^53 (exact reconstruction)
     rng = np.random.default_rng(n)
     X = rng.integers(-1024, 1025, (n, n)).astype(np.float64)
     Y = rng.integers(-1024, 1025, (n, n)).astype(np.float64)
@@ -48,7 +48,7 @@ def test_crt_error_within_method_bound(n, kappa, digits):
     C = (Q * lam ** -0.5) @ Q.T
     C = (C + C.T) / 2
     b = ipr.ipr_test_crt_table(18, digits, n)["b_for"]
-    assert b == 7 * digits - 1
+    assert b == 7 * digits - 4
     L = np.longdouble
     exact = A.astype(L) @ C.astype(L)
     Z = _gemm(ipr.IPR_FP64_CRT, A, C, digits)
@@ -104,7 +104,7 @@ def test_crt_fp64_phase_level2(form, sched):
             assert rel_fro(hist[k], r.C_hist[k]) <= 4 * 2.0 ** -7, k
     assert rel_fro(best, r.C_best) <= 1e-10
     assert tr[-1]["rho_cert"] <= 1e-12
-    nm = ipr.ipr_test_crt_table(18, 62, n)["n_for"]                            # b = 62 at n = 520
+    nm = ipr.ipr_test_crt_table(18, 59, n)["n_for"]                            # b = 59 at n = 520
     assert all(t["moduli"] == nm for t in tr if t["phase"] == len(parts) - 1)
 
 
@@ -124,7 +124,7 @@ def test_crt_adaptive_level2_and_storage_rule():
     agree = sum(a == b for a, b in zip(mg, mo))
     assert agree >= min(len(mg), len(mo)) - 1, (mg, mo)
     mods = [t["moduli"] for t in tr if t["phase"] == 1]
-    assert mods == sorted(mods) and mods[0] < mods[-1] == ipr.ipr_test_crt_table(18, 62, n)["n_for"]
+    assert mods == sorted(mods) and mods[0] < mods[-1] == ipr.ipr_test_crt_table(18, 59, n)["n_for"]
     assert rel_fro(best, r.C_best) <= 1e-10
     assert tr[-1]["rho_cert"] <= 1e-12
 
