@@ -88,9 +88,12 @@ def schedule(name, n):
         if i == len(parts) - 1:
             out.append(ipr.make_phase(prec, mant_bits=m, corr_prec=corr))
         else:
-            # the symmetric form damps low-precision noise in the next phase, so a low phase runs
-            # to its plateau; the literal form leaves at rho_hat <= 1e-2 as well
-            sw = 0.0 if form.startswith("symmetric") else 1e-2 * math.sqrt(n)
+            # the symmetric form damps low-precision noise in the next phase: a low phase runs to its
+            # plateau, or until rho_hat <= 2 u of its operand format (u = 2^-(m+1); below that the format
+            # makes no further progress -- it saves the iteration that only confirms the plateau); the
+            # literal form leaves at rho_hat <= 1e-2 as well
+            mbits = {"bf16": 7, "int8": 7, "fp8": 3, "fp16": 10, "tf32": 10}.get(prec, 52)
+            sw = (2.0 * 2.0 ** -(mbits + 1) * math.sqrt(n)) if form.startswith("symmetric") else 1e-2 * math.sqrt(n)
             out.append(ipr.make_phase(prec, mant_bits=m, switch_tol=sw, plateau_ratio=0.7, plateau_arm=0.5,
                                       max_iters=40, corr_prec=corr))
     return form, out

@@ -33,7 +33,7 @@ __host__ __device__ inline int oz_digits(int m) {
 // moduli m_l <= 256 (one kind::i8 GEMM each, residues in [-128, 127]) and reconstructed by the CRT.
 // The table is per N (the modulus product M_N changes the CRT weights):
 //   X = sum_l v_l W_l, W_l = M_N / m_l, v_l = (u_l inv_l) mod m_l, u_l = (product mod m_l);
-//   W_l = H_l 2^s1 + L_l 2^s2 + R_l with H, L < 2^40 (those partial sums exact in FP64; R rounded
+//   W_l = H_l 2^s1 + L_l 2^s2 + R_l with H, L < 2^39 (those partial sums exact in FP64; R rounded
 //   to FP64 when s2 > 53, an absolute error far below the result's own rounding);
 //   P = X - q M_N, q = rint(X / M_N), with M_N = MH 2^s1 + ML 2^s2 + MR sliced the same way.
 constexpr int CRT_MAX = 18, CRT_BMAX = 62;
@@ -47,6 +47,7 @@ struct CrtTab {
   double H[CRT_MAX + 1][CRT_MAX], L[CRT_MAX + 1][CRT_MAX], R[CRT_MAX + 1][CRT_MAX];
   double MH[CRT_MAX + 1], ML[CRT_MAX + 1], MR[CRT_MAX + 1], invM[CRT_MAX + 1];
   double Lo[CRT_MAX + 1][CRT_MAX], MLo[CRT_MAX + 1];   // (W mod 2^s1) 2^-s1, rounded (two-slice form)
+  double CH[CRT_MAX + 1], CL[CRT_MAX + 1];             // 256 sum_l H_l (exact), 256 sum_l Lo_l (bias of 256 + v)
   double p2s1[CRT_MAX + 1], p2s2[CRT_MAX + 1];
   double log2M[CRT_MAX + 1];
 };

@@ -523,6 +523,7 @@ __device__ __forceinline__ void crt_chunk(const GemmArgs &g, int l, int64_t row,
 // (transposed) store of the slab through shared memory (row r, column c at r * 161 + c + c / 4:
 // conflict-free both ways).
 constexpr int CRT_FIN_LD = 161;
+template <int NM>   // the modulus count: the loops over moduli unroll exactly, constants come from c[] directly
 __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
   extern __shared__ double sm_slab[];          // [32][CRT_FIN_LD]
   __shared__ double red[8];
@@ -531,29 +532,36 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
   sch.get((int)(blockIdx.x >> 1), tm, tn);
   const int tile_m = tm * 2 + (int)(blockIdx.x & 1);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nm = g.crt_n, mode = g.mode;
+  constexpr int nm = NM;
+  const int mode = g.mode;
   const bool diag = (mode & EPI_DIAG_MINUS) != 0, st = (mode & EPI_STORE_T) != 0, rsd = (mode & EPI_RESID) != 0;
   const int tp = is_f64(g.tprec) ? 0 : g.tprec == P_BF16 ? 1 : 2;
   const double p1 = c_crt.p2s1[nm], iM = c_crt.invM[nm];
-  const double MH = c_crt.MH[nm], MLo = c_crt.MLo[nm];
+  const double MH = c_crt.MH[nm], MLo = c_crt.MLo[nm], CH = c_crt.CH[nm], CL = c_crt.CL[nm];
   double r2 = 0.0;
+  // block-uniform tile class: a tile that touches neither the diagonal nor the padding takes the
+  // branch-free path (tri: strictly above the diagonal, every element mirrored)
+  const int64_t r0 = (int64_t)tile_m * TC_BM, gcb = g.col0 + (int64_t)tn * TC_BN;
+  const bool clean = (r0 + TC_BM <= g.n) && (gcb + TC_BN <= g.n) && (r0 + TC_BM <= gcb || gcb + TC_BN <= r0);
+  const bool mir = g.tri != 0;                       // clean + tri => strictly upper
   #pragma unroll 1
   for (int half = 0; half < 2; ++half) {
     const int64_t colb = (int64_t)tn * TC_BN + 128 * half, c0 = colb + 4 * lane;
-    int cs[4];
+    double scol[4];
     #pragma unroll
-    for (int u = 0; u < 4; ++u) cs[u] = g.oz_csig[c0 + u];
+    for (int u = 0; u < 4; ++u) scol[u] = scalbn(1.0, -g.oz_csig[c0 + u]);   // exact powers of two
     #pragma unroll 1
     for (int slab = 0; slab < 4; ++slab) {
       #pragma unroll 1
       for (int i2 = 0; i2 < 4; i2 += 2) {            // two rows at a time: 16 independent FMA chains
-        uint32_t bv[2][CRT_MAX];
+        uint32_t bv[2][NM];
         #pragma unroll
         for (int ii = 0; ii < 2; ++ii) {
-          const int64_t row = (int64_t)tile_m * TC_BM + slab * 32 + 4 * w + i2 + ii;
+          const int64_t row = r0 + slab * 32 + 4 * w + i2 + ii;
+          const uint8_t *src = g.crt_v + row * g.ldv + c0;
+          const int64_t plane = g.M * g.ldv;
           #pragma unroll
-          for (int l = 0; l < CRT_MAX; ++l)
-            if (l < nm) bv[ii][l] = *(const uint32_t *)(g.crt_v + ((int64_t)l * g.M + row) * g.ldv + c0);
+          for (int l = 0; l < NM; ++l) bv[ii][l] = *(const uint32_t *)(src + l * plane);
         }
         // two slices: sh = sum v_l H_l exact (< 2^53), so = sum v_l Lo_l (Lo_l = (W_l mod 2^s1) 2^-s1,
         // rounded: absolute error ~2^(s1 - 45) in Pbar, far below its own last bit at these sizes)
@@ -563,75 +571,111 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
           #pragma unroll
           for (int u = 0; u < 4; ++u) { sh[ii][u] = 0.0; so[ii][u] = 0.0; }
         #pragma unroll
-        for (int l = 0; l < CRT_MAX; ++l) {
-          if (l < nm) {
-            const double hh = c_crt.H[nm][l], lo = c_crt.Lo[nm][l];
+        for (int l = 0; l < NM; ++l) {
+          const double hh = c_crt.H[nm][l], lo = c_crt.Lo[nm][l];
+          #pragma unroll
+          for (int ii = 0; ii < 2; ++ii)
             #pragma unroll
-            for (int ii = 0; ii < 2; ++ii)
-              #pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                // byte -> FP64 without a conversion instruction: (2^52 + v) - 2^52, exact
-                const double v = __dsub_rn(__hiloint2double(0x43300000, (int)__byte_perm(bv[ii][l], 0u, 0x4440 + u)),
-                                           4503599627370496.0);
-                sh[ii][u] = __fma_rn(v, hh, sh[ii][u]);
-                so[ii][u] = __fma_rn(v, lo, so[ii][u]);
-              }
-          }
+            for (int u = 0; u < 4; ++u) {
+              // 256 + v as an FP64 bit pattern (exponent 8, v in the top mantissa bits): no conversion,
+              // no FP64 add; the bias 256 sum_l H_l (exact) / 256 sum_l Lo_l is removed below
+              const uint32_t f = u == 0 ? (bv[ii][l] << 12) : u == 1 ? (bv[ii][l] << 4)
+                               : u == 2 ? (bv[ii][l] >> 4) : (bv[ii][l] >> 12);
+              const double d = __hiloint2double((int)((f & 0xff000u) | 0x40700000u), 0);
+              sh[ii][u] = __fma_rn(d, hh, sh[ii][u]);   // integers < 2^53: exact
+              so[ii][u] = __fma_rn(d, lo, so[ii][u]);
+            }
         }
         #pragma unroll
         for (int ii = 0; ii < 2; ++ii) {
-        const int rl = 4 * w + i2 + ii;
-        const int64_t row = (int64_t)tile_m * TC_BM + slab * 32 + rl;
-        const int rs = g.oz_rsig[row];
-        double vv[4];
-        #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const double q = rint(__dmul_rn(__fma_rn(sh[ii][u], p1, __dmul_rn(so[ii][u], p1)), iM));  // within 0.493 of an integer
-          const double dh = __fma_rn(-q, MH, sh[ii][u]);              // exact
-          const double dlo = __fma_rn(-q, MLo, so[ii][u]);
-          const double pb = __dmul_rn(__dadd_rn(dh, dlo), p1);        // (dh + dlo) 2^s1
-          const int e = rs + cs[u];
-          vv[u] = (e > -1000 && e < 1000) ? __dmul_rn(pb, pow2(-e)) : scalbn(pb, -e);
-        }
-        if (mode & EPI_STORE_N) {
-          double2 *dn = (double2 *)((double *)g.nout + row * g.ldn + c0);
-          dn[0] = make_double2(vv[0], vv[1]); dn[1] = make_double2(vv[2], vv[3]);
-        }
-        if (mode & EPI_F64) {
-          double2 *dz = (double2 *)(g.zout + row * g.ldz + c0);
-          dz[0] = make_double2(vv[0], vv[1]); dz[1] = make_double2(vv[2], vv[3]);
-        }
-        #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int64_t c = c0 + u, gc = g.col0 + c;
-          const bool skip = g.tri && row > gc;            // tri: the lower triangle comes from the mirror
-          const bool mirror = g.tri && row < gc;
-          const double wv = diag ? __dsub_rn((row == gc && row < g.n) ? g.diag : 0.0, vv[u]) : vv[u];
-          if (rsd && !skip && row < g.n && gc < g.n) {
-            const double d = __dsub_rn(row == gc ? 1.0 : 0.0, vv[u]);
-            r2 = __fma_rn(mirror ? 2.0 * d : d, d, r2);
+          const int rl = 4 * w + i2 + ii;
+          const int64_t row = r0 + slab * 32 + rl;
+          const double srow = scalbn(1.0, -g.oz_rsig[row]);
+          double vv[4], wv[4];
+          #pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const double shu = __dsub_rn(sh[ii][u], CH), sou = __dsub_rn(so[ii][u], CL);   // exact / ~2^-40
+            const double q = rint(__dmul_rn(__fma_rn(shu, p1, __dmul_rn(sou, p1)), iM));  // within 0.493 of an integer
+            const double dh = __fma_rn(-q, MH, shu);                    // exact
+            const double dlo = __fma_rn(-q, MLo, sou);
+            const double pb = __dmul_rn(__dadd_rn(dh, dlo), p1);        // (dh + dlo) 2^s1
+            vv[u] = __dmul_rn(__dmul_rn(pb, srow), scol[u]);            // 2^-(e_i + f_j) Pbar, exact scaling
           }
-          if (st && mirror) {                              // (j, i) of a tri element: row-major in T
-            if (tp == 0) st_t<0>(g.tout, row * g.ldt + c, wv);
-            else if (tp == 1) st_t<1>(g.tout, row * g.ldt + c, wv);
-            else st_t<2>(g.tout, row * g.ldt + c, wv);
+          if (mode & EPI_STORE_N) {
+            double2 *dn = (double2 *)((double *)g.nout + row * g.ldn + c0);
+            dn[0] = make_double2(vv[0], vv[1]); dn[1] = make_double2(vv[2], vv[3]);
           }
-          sm_slab[rl * CRT_FIN_LD + 5 * lane + u] = wv;   // column 4 lane + u, swizzled + lane
-        }
+          if (mode & EPI_F64) {
+            double2 *dz = (double2 *)(g.zout + row * g.ldz + c0);
+            dz[0] = make_double2(vv[0], vv[1]); dz[1] = make_double2(vv[2], vv[3]);
+          }
+          if (clean) {                                   // off the diagonal, inside n
+            #pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double d = __dsub_rn(0.0, vv[u]);
+              wv[u] = diag ? d : vv[u];
+              if (rsd) r2 = __fma_rn(mir ? 2.0 * d : d, d, r2);
+            }
+            if (st && mir) {                             // (j, i): row-major in T, one vector store
+              if (tp == 0) {
+                double2 *m = (double2 *)((double *)g.tout + row * g.ldt + c0);
+                m[0] = make_double2(wv[0], wv[1]); m[1] = make_double2(wv[2], wv[3]);
+              } else if (tp == 1) {
+                const __nv_bfloat162 a = __floats2bfloat162_rn((float)wv[0], (float)wv[1]);
+                const __nv_bfloat162 b = __floats2bfloat162_rn((float)wv[2], (float)wv[3]);
+                *(uint2 *)((__nv_bfloat16 *)g.tout + row * g.ldt + c0) = make_uint2(*(const uint32_t *)&a, *(const uint32_t *)&b);
+              } else {
+                *(float4 *)((float *)g.tout + row * g.ldt + c0) =
+                    make_float4(to_tf32((float)wv[0]), to_tf32((float)wv[1]), to_tf32((float)wv[2]), to_tf32((float)wv[3]));
+              }
+            }
+          } else {
+            #pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int64_t c = c0 + u, gc = g.col0 + c;
+              const bool skip = g.tri && row > gc;            // tri: the lower triangle comes from the mirror
+              const bool mirror = g.tri && row < gc;
+              wv[u] = diag ? __dsub_rn((row == gc && row < g.n) ? g.diag : 0.0, vv[u]) : vv[u];
+              if (rsd && !skip && row < g.n && gc < g.n) {
+                const double d = __dsub_rn(row == gc ? 1.0 : 0.0, vv[u]);
+                r2 = __fma_rn(mirror ? 2.0 * d : d, d, r2);
+              }
+              if (st && mirror) {                              // (j, i) of a tri element: row-major in T
+                if (tp == 0) st_t<0>(g.tout, row * g.ldt + c, wv[u]);
+                else if (tp == 1) st_t<1>(g.tout, row * g.ldt + c, wv[u]);
+                else st_t<2>(g.tout, row * g.ldt + c, wv[u]);
+              }
+            }
+          }
+          #pragma unroll
+          for (int u = 0; u < 4; ++u) sm_slab[rl * CRT_FIN_LD + 5 * lane + u] = wv[u];   // column 4 lane + u, + lane
         }
       }
       __syncthreads();
       if (st) {                                            // K-major store: 32 consecutive rows per warp
-        const int64_t row = (int64_t)tile_m * TC_BM + slab * 32 + lane;
-        #pragma unroll 4
-        for (int j = 0; j < 16; ++j) {
-          const int cl = w * 16 + j;
-          const int64_t c = colb + cl;
-          if (g.tri && row > g.col0 + c) continue;
-          const double v = sm_slab[lane * CRT_FIN_LD + cl + (cl >> 2)];
-          if (tp == 0) st_t<0>(g.tout, c * g.ldt + row, v);
-          else if (tp == 1) st_t<1>(g.tout, c * g.ldt + row, v);
-          else st_t<2>(g.tout, c * g.ldt + row, v);
+        const int64_t row = r0 + slab * 32 + lane;
+        const bool chk = g.tri && !clean;
+        if (tp == 0) {
+          #pragma unroll 4
+          for (int j = 0; j < 16; ++j) {
+            const int cl = w * 16 + j;
+            const int64_t c = colb + cl;
+            if (!(chk && row > g.col0 + c)) st_t<0>(g.tout, c * g.ldt + row, sm_slab[lane * CRT_FIN_LD + cl + (cl >> 2)]);
+          }
+        } else if (tp == 1) {
+          #pragma unroll 4
+          for (int j = 0; j < 16; ++j) {
+            const int cl = w * 16 + j;
+            const int64_t c = colb + cl;
+            if (!(chk && row > g.col0 + c)) st_t<1>(g.tout, c * g.ldt + row, sm_slab[lane * CRT_FIN_LD + cl + (cl >> 2)]);
+          }
+        } else {
+          #pragma unroll 4
+          for (int j = 0; j < 16; ++j) {
+            const int cl = w * 16 + j;
+            const int64_t c = colb + cl;
+            if (!(chk && row > g.col0 + c)) st_t<2>(g.tout, c * g.ldt + row, sm_slab[lane * CRT_FIN_LD + cl + (cl >> 2)]);
+          }
         }
       }
       __syncthreads();
@@ -649,14 +693,23 @@ cudaError_t launch_crt_finish(const GemmArgs &a, cudaStream_t s) {
     cudaError_t z = cudaMemsetAsync(a.part, 0, (size_t)(a.N / TC_BN) * a.tiles_m * sizeof(double), s);
     if (z != cudaSuccess) return z;
   }
-  static bool attr = false;
   const int smem = 32 * CRT_FIN_LD * 8;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_crt_finish, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
+  switch (a.crt_n) {
+#define CRT_FIN(N)                                                                                       \
+    case N: {                                                                                            \
+      static bool attr = false;                                                                          \
+      if (!attr) {                                                                                       \
+        cudaError_t e = cudaFuncSetAttribute(k_crt_finish<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        if (e != cudaSuccess) return e;                                                                  \
+        attr = true;                                                                                     \
+      }                                                                                                  \
+      k_crt_finish<N><<<2 * hs.count(), 256, smem, s>>>(a);                                              \
+    } break;
+    CRT_FIN(2) CRT_FIN(3) CRT_FIN(4) CRT_FIN(5) CRT_FIN(6) CRT_FIN(7) CRT_FIN(8) CRT_FIN(9) CRT_FIN(10)
+    CRT_FIN(11) CRT_FIN(12) CRT_FIN(13) CRT_FIN(14) CRT_FIN(15) CRT_FIN(16) CRT_FIN(17) CRT_FIN(18)
+#undef CRT_FIN
+    default: return cudaErrorInvalidValue;
   }
-  k_crt_finish<<<2 * hs.count(), 256, smem, s>>>(a);
   ++g_launches;
   return cudaGetLastError();
 }

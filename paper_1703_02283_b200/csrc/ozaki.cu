@@ -186,13 +186,14 @@ CrtTab make_crt_table() {
     for (int l = 0; l < N; ++l) M.mul((uint32_t)kModuli[l]);
     int E = 0;
     for (int l = 0; l < N; ++l) { Big W = M; W.divmod((uint32_t)kModuli[l]); E = W.bitlen() > E ? W.bitlen() : E; }
-    // W = H 2^s1 + L 2^s2 + R: H, L < 2^40 exact; R < 2^s2 rounded to FP64 when s2 > 53 (its products
+    // W = H 2^s1 + L 2^s2 + R: H, L < 2^39 exact; R < 2^s2 rounded to FP64 when s2 > 53 (its products
     // then carry an absolute error ~2^(s2 - 40), far below the result's own rounding 2^(2b + log2 n - 53)).
     // Lo = L 2^(s2 - s1) + R 2^-s1 = (W mod 2^s1) 2^-s1 rounded to FP64: the two-slice form of the
     // finish kernel (the rounding of sum v Lo ~2^(s1 - 45), negligible likewise)
-    const int s1 = E > 40 ? E - 40 : 0, s2 = s1 > 40 ? s1 - 40 : 0;
+    // 39-bit H: the finish kernel accumulates (256 + v_l) H_l, 18 * 511 * 2^39 < 2^53
+    const int s1 = E > 39 ? E - 39 : 0, s2 = s1 > 39 ? s1 - 39 : 0;
     auto slice = [&](const Big &W, double &h, double &lo, double &r, double &low) {
-      h = (double)W.bits(s1, 40 + 8);
+      h = (double)W.bits(s1, 39 + 9);
       lo = (double)W.bits(s2, s1 - s2);
       r = (double)W.ld(s2);
       low = (double)(W.ld(s1) / ldexpl(1.0L, s1));
@@ -205,6 +206,11 @@ CrtTab make_crt_table() {
       slice(W, t.H[N][l], t.L[N][l], t.R[N][l], t.Lo[N][l]);
     }
     slice(M, t.MH[N], t.ML[N], t.MR[N], t.MLo[N]);
+    double ch = 0.0;
+    long double cl = 0.0L;
+    for (int l = 0; l < N; ++l) { ch += 256.0 * t.H[N][l]; cl += 256.0L * (long double)t.Lo[N][l]; }
+    t.CH[N] = ch;                                 // exact: < 2^52
+    t.CL[N] = (double)cl;
     t.invM[N] = (double)(1.0L / M.ld());
     t.p2s1[N] = ldexp(1.0, s1);
     t.p2s2[N] = ldexp(1.0, s2);

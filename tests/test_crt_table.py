@@ -3,7 +3,8 @@ Python integers -- no GPU.  The CUDA reconstruction (gemm_tc.cu crt_chunk) relie
   * pairwise coprime moduli <= 256 (the CRT is then a bijection Z_M -> prod Z_{m_l});
   * inv_l W_l = 1 (mod m_l) with W_l = M_N / m_l (so sum_l ((u_l inv_l) mod m_l) W_l = u_l mod m_l);
   * W_l = H_l 2^s1 + L_l 2^s2 + R_l, M_N = MH 2^s1 + ML 2^s2 + MR with H, L the exact bit fields
-    (small enough that sum_l v_l H_l, v_l <= 255, and q MH, q <= the largest quotient, stay < 2^53)
+    (small enough that sum_l (256 + v_l) H_l, v_l <= 255, and q MH, q <= the largest quotient, stay
+    < 2^53)
     and R the low bits, exact below 2^53 and correctly rounded to FP64 above;
   * the modulus count for (b, n): the smallest N with M_N > 2^1.02 n 2^(2b) (|Pbar| <= n 2^(2b), so
     X / M_N is within 0.493 of an integer and rint(X / M_N), evaluated to ~2^-45, is exact)."""
@@ -44,19 +45,18 @@ def test_weights_inverses_and_slices_exact(N):
     M = math.prod(m)
     s1, s2 = (int(math.log2(x)) for x in t["p2s"])
     assert t["p2s"] == (2.0 ** s1, 2.0 ** s2)
-    assert s1 == 0 or s1 - s2 == 40 or s2 == 0
+    assert s1 == 0 or s1 - s2 == 39 or s2 == 0
     for l in range(N):
         W = M // m[l]
         H, L, R = t["HLR"][l]
         _check_slices(W, H, L, R, s1, s2)
-        assert H < 2 ** 40 and L < 2 ** 40
+        assert H < 2 ** 39 and L < 2 ** 39
         assert (t["inv"][l] * W) % m[l] == 1
         assert 0 <= t["inv"][l] < m[l]
     _check_slices(M, *t["M_HLR"], s1, s2)
     MH, ML = (int(x) for x in t["M_HLR"][:2])
-    # exactness budget of the FP64 sums of the exact slices: v_l <= 255
-    for k in range(2):
-        assert 255 * sum(int(t["HLR"][l][k]) for l in range(N)) < 2 ** 53
+    # exactness budget of the FP64 sums of the exact slice: the finish accumulates (256 + v_l) H_l
+    assert 511 * sum(int(t["HLR"][l][0]) for l in range(N)) < 2 ** 53
     qmax = math.ceil(Fraction(sum(255 * (M // x) for x in m), M))
     assert qmax * MH < 2 ** 53 and qmax * ML < 2 ** 53
 
