@@ -136,3 +136,24 @@ def test_crt_unsupported_outside_symmetric_forms():
         s.iterate(1)
     assert e.value.status == ipr.IPR_E_UNSUPPORTED
     s.close()
+
+
+def test_crt_product_full_size_sampled_rows():
+    # the bench's launch configuration (n = 8192, 2 moduli per launch, S = 9 -> b = 59, 17 moduli):
+    # sampled rows of Z = A A against the oracle's FP64 matvec, within the method's bound plus the
+    # reference's own FP64 rounding
+    n = 8192
+    A, _ = synth.spd_torch(n, 2.0, 5, device="cuda")
+    Z = torch.empty_like(A)
+    ipr.ipr_test_gemm(ipr.IPR_FP64_CRT, n, A, A, Z)      # A symmetric: its K-major form is A itself
+    A_np, Z_np = A.cpu().numpy(), Z.cpu().numpy()
+    b = ipr.ipr_test_crt_table(18, 9, n)["b_for"]
+    absA = np.abs(A_np)
+    rmax = absA.max(axis=1)
+    colsum = absA.sum(axis=0)
+    for i in [0, 1, 4097, 8191]:
+        ref = oracle.matvec(A_np, A_np[i])            # row i of A A (A symmetric)
+        mag = oracle.matvec(absA, absA[i])
+        bound = 2.0 ** -b * (rmax[i] * colsum + (absA[i].sum() + n * rmax[i] * 2.0 ** -b) * rmax) \
+            + 2.0 ** -51 * np.abs(ref) + n * 2.0 ** -53 * mag
+        assert np.all(np.abs(Z_np[i] - ref) <= bound), (i, float(np.max(np.abs(Z_np[i] - ref) / bound)))
