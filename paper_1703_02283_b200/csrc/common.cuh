@@ -74,6 +74,10 @@ enum EpiMode : int {
   EPI_OZACC = 512,    // Ozaki group g: ozacc[j * ldoz + i] (+)= 2^(rsig_i + csig_j - 7 g) * D_ij (INT32 D)
   EPI_COUPLED = 1024, // coupled form: w = q_m(D); Mhat = qin(w) -> tout, Nhat = qin(((p+1)delta - w)/p)
                       // -> nkout (both K-major at col * ldt + row); with EPI_RESID for rho
+  EPI_SYMUPD = 2048,  // symmetric-tri form, fused update (tcgen05, tri): D = S = W + W^T from the
+                      // K-concatenated GEMM [Chat | Rhat] [Rhat ; Chat]; C_{k+1} = q_m(C + S/(2p)) at (i,j)
+                      // and (j,i) -> cnew, + the next operands (chat_new in prec, qnext planes 0 and 2 in
+                      // the correction format tprec), delta partials
 };
 
 struct GemmArgs {
@@ -115,6 +119,11 @@ struct GemmArgs {
                         // OZ_S * npad, B offset (OZ_S - g + 1) * npad), the finish epilogue g.mode
                         // fused into group 2; g.mode holds the FINISH mode
   const int8_t *oz_a;   // A-role digit planes [S][npad][npad] (row-major per plane)
+  int64_t b_pstride;    // != 0: B is K-concatenated planes too, element (k,j) at
+                        // B + (k / a_kp) * b_pstride + j * ldb + k % a_kp (3-D tensor map)
+  void *qnext;          // EPI_SYMUPD: [3][npad][npad] correction-format buffer of the next iterate (planes
+                        // 0 and 2 receive Chat_{k+1}); ldh is its row stride
+  int hprec;            // EPI_SYMUPD: format of chat_new (the phase's operand; prec is the MMA format)
   const int8_t *oz_b;   // B-role digits, per output column j: [S * npad] = digit planes S..1 of column j
                         // (oz_grouped == 3, CRT: residue planes [crt_n][npad][npad] of both operands)
   int crt_n;            // oz_grouped == 3: number of moduli (one kind::i8 GEMM each)

@@ -14,6 +14,7 @@
 // [G][npad][kp] so one in-place ncclAllGather assembles it; every per-tile partial has a
 // global slot so rho / delta are reduced in the same fixed order for any G.
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -86,6 +87,9 @@ struct ipr_ctx {
   int *crA_sig = nullptr, *crC_sig[2] = {nullptr, nullptr}, *crB_sig = nullptr;
   int crA_b = -1, crC_b[2] = {-1, -1};
   uint8_t *crV = nullptr;
+  // symmetric-tri form, fused update (EPI_SYMUPD): per iterate buffer [Chat | Rhat | Chat] in the
+  // correction format -- the A operand [Chat | Rhat] is planes 0-1, the B operand [Rhat ; Chat] planes 1-2
+  void *qbuf[2] = {nullptr, nullptr};
   // coupled form (R-27): Mhat and Nhat K-major local panels (ping-pong), Nhat as the replicated A
   // operand (panel-major), which set is current, and whether the next chain must re-anchor M
   void *cM[2] = {nullptr, nullptr}, *cNk[2] = {nullptr, nullptr}, *cNf = nullptr;
@@ -383,6 +387,20 @@ ipr_status crt_operands(ipr_ctx *c, GemmArgs &g, int i, const void *Xt) {
   crt_args(c, g, b);
   return IPR_OK;
 }
+// fused symmetric update (EPI_SYMUPD) for this phase: tri form, one GPU, unscaled phase operands and a
+// tcgen05 correction format
+// Off by default (IPR_FUSED_SYMUPD=1 enables it): measured 1.39 ms per n = 8192 update against 1.08 ms
+// for the W GEMM + k_sym_update pair -- with K = 2n a wave's operand blocks (~136 MB) exceed L2 and the
+// epilogue's FP64 conversions and stores compete with the operand streams.
+bool fused_sym_ok(const ipr_ctx *c, const PhaseC &P) {
+  static int on = -1;
+  if (on < 0) { const char *v = getenv("IPR_FUSED_SYMUPD"); on = v && atoi(v) ? 1 : 0; }
+  return on && c->world == 1 && c->form == IPR_FORM_SYMMETRIC_TRI && !is_scaled(P.prec) &&
+         (P.corr == IPR_BF16 || P.corr == IPR_TF32) && tc_supported(P.corr);
+}
+void *qplane(ipr_ctx *c, int i, int prec, int plane) {
+  return (char *)c->qbuf[i] + (size_t)plane * (size_t)(c->npad * c->npad) * elt_size(prec);
+}
 // operand formats that share storage (FP64 and FP64-by-Ozaki both keep Chat in FP64)
 inline bool same_fmt(int a, int b) { return a == b || (is_f64(a) && is_f64(b)); }
 inline bool is_sym(const ipr_ctx *c) { return c->form == IPR_FORM_SYMMETRIC || c->form == IPR_FORM_SYMMETRIC_TRI; }
@@ -432,6 +450,11 @@ ipr_status begin_phase(ipr_ctx *c, bool first) {
     CKS(oz_split_chat(c, c->cur));
   }
   if (c->form == IPR_FORM_NEWTON_SCHULZ) CKS(make_xt(c, c->cur, P));
+  if (fused_sym_ok(c, P)) {        // [Chat | . | Chat] of the entering iterate in the correction format
+    const int64_t cnt = c->npad * c->npad;
+    CK(launch_make_operand(cont_ptr(c, c->cur, P), P.cont64, cnt, P.corr, nullptr, qplane(c, c->cur, P.corr, 0), c->st));
+    CK(launch_make_operand(cont_ptr(c, c->cur, P), P.cont64, cnt, P.corr, nullptr, qplane(c, c->cur, P.corr, 2), c->st));
+  }
   if (is_sym(c)) {
     CKS(make_corr_operand(c, c->cur, P));
     if (c->world > 1) CKS(make_xt(c, c->cur, P));
@@ -516,6 +539,7 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
         g.tri = c->form == IPR_FORM_SYMMETRIC_TRI;   // Z_2 = C A C: upper triangle + mirror
       }
       g.tout = (scaled && j < c->p) ? (void *)c->tscr : c->T[j & 1];
+      if (j == c->p && fused_sym_ok(c, P)) g.tout = qplane(c, c->cur, P.corr, 1);   // Rhat into [Chat | Rhat | Chat]
       g.ldt = c->npad;
       g.part = part;
       if (prec == IPR_FP64_OZ) {
@@ -653,6 +677,32 @@ ipr_status update_sym(ipr_ctx *c) {
   const PhaseC &P = c->ph[c->phase];
   const int nx = 1 - c->cur;
   if (c->best_loc == nx) CKS(save_best(c));
+  if (fused_sym_ok(c, P)) {
+    // S = Chat Rhat + Rhat Chat = W + W^T as ONE upper-triangle GEMM over K = 2n ([Chat | Rhat] x
+    // [Rhat ; Chat], both symmetric), the update C_{k+1} = q_m(C + S/(2p)) and the next operands fused
+    // into its epilogue (no W round trip, no k_sym_update pass)
+    const int64_t np = c->npad;
+    GemmArgs g = base_args(c, P.corr, qplane(c, c->cur, P.corr, 1));
+    g.A = qplane(c, c->cur, P.corr, 0); g.a_kp = np; g.a_pstride = np * np;
+    g.K = 2 * np; g.ldb = np; g.b_pstride = np * np;
+    g.mode = EPI_SYMUPD; g.tri = 1; g.tprec = P.corr;
+    g.cold = cont_ptr(c, c->cur, P); g.cnew = cont_ptr(c, nx, P); g.ldc = c->kp;
+    g.chat_new = (is_f64(P.prec) || is_scaled(P.prec)) ? nullptr : chat_slot(c, nx, P.prec);
+    g.hprec = P.prec;
+    g.qnext = c->qbuf[nx]; g.ldh = np;
+    g.m = P.adaptive ? c->oz_m_next : P.m; g.rtz = P.rtz; g.cont64 = P.cont64;
+    g.part = c->part;
+    CK(cudaEventRecord(c->ev[2], c->st));
+    CK(run_gemm(c, g));
+    CK(launch_reduce_sum(c->part, tiles_n_total(c, P.corr) * tiles_m(c, P.corr), c->dscal + 1, c->st));
+    CK(cudaEventRecord(c->ev[3], c->st));
+    c->upd_timed = true;
+    if (P.prec == IPR_FP64_OZ) CKS(oz_split_chat(c, nx));
+    c->crC_b[nx] = -1;
+    c->m_of_cur = P.adaptive ? c->oz_m_next : P.m;
+    c->cur = nx;
+    return IPR_OK;
+  }
   GemmArgs g = base_args(c, P.corr, c->T[c->p & 1]);
   if (same_fmt(P.corr, P.prec)) chat_view(c, c->cur, P.prec, &g.A, &g.a_kp, &g.a_pstride);
   else { g.A = c->chatc[c->cur]; g.a_kp = c->kp; g.a_pstride = c->npad * c->kp; }
@@ -785,6 +835,9 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
   bool fp16 = false, oz = false, cr = false;   // any scaled-format phase: FP32 T scratch; Ozaki I / II
   for (auto &P : c->ph) { fp16 |= is_scaled(P.prec); oz |= P.prec == IPR_FP64_OZ; cr |= P.prec == IPR_FP64_CRT; }
   const size_t crp = cr ? full * CRT_MAX : 0, crs = cr ? (size_t)c->npad * 4 : 0;
+  bool fq = false;                      // any phase with the fused symmetric update: [Chat | Rhat | Chat] x 2
+  for (auto &P : c->ph) fq |= fused_sym_ok(c, P);
+  const size_t qb = fq ? 3 * full * 4 : 0;
   struct Slot { void **p; size_t bytes; };
   const Slot slots[] = {
       {&c->chat[0], full * 8}, {&c->chat[1], full * 8}, {&c->cont[0], panel * 4}, {&c->cont[1], panel * 4},
@@ -804,6 +857,7 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       {(void **)&c->crA, crp}, {(void **)&c->crC[0], crp}, {(void **)&c->crC[1], crp}, {(void **)&c->crB, crp},
       {(void **)&c->crA_sig, crs}, {(void **)&c->crC_sig[0], crs}, {(void **)&c->crC_sig[1], crs},
       {(void **)&c->crB_sig, crs}, {(void **)&c->crV, cr ? full * CRT_MAX : 0},
+      {&c->qbuf[0], qb}, {&c->qbuf[1], qb},
       {&c->cM[0], cpl ? panel * 8 : 0}, {&c->cM[1], cpl ? panel * 8 : 0}, {&c->cNk[0], cpl ? panel * 8 : 0},
       {&c->cNk[1], cpl ? panel * 8 : 0}, {&c->cNf, cpl ? full * 8 : 0},
       {(void **)&c->full64, full * 8}, {&c->Acert, panel * 8}};

@@ -195,17 +195,27 @@ __device__ __forceinline__ double acc_to_f64(uint32_t w) {
 
 struct TileSched {      // pair tiles: tiles_m pair-rows (256 rows) x tiles_n (256 columns)
   int tiles_m, tiles_n, tri;
-  // tri (square, symmetric-tri GEMM 2): only the upper-triangle pair tiles tm <= tn, column by
-  // column, so the persistent CTA pairs share the work evenly
+  // tri (square, symmetric-tri GEMM 2 / fused update): only the upper-triangle pair tiles tm <= tn, in
+  // bands of TRI_GC pair-columns, row by row inside a band, so the CTA pairs in flight share their A
+  // row blocks (TRI_GC tiles each) and B column blocks (the band) in L2 -- a column-by-column order
+  // streamed ~8 GB per K = 2n fused-update GEMM from DRAM
+  static constexpr int TRI_GC = 8;
   __host__ __device__ int count() const { return tri ? tiles_n * (tiles_n + 1) / 2 : tiles_m * tiles_n; }
   __device__ void get(int t, int &tm, int &tn) const {
     if (tri) {
-      int c = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
-      while (c * (c + 1) / 2 > t) --c;
-      while ((c + 1) * (c + 2) / 2 <= t) ++c;
-      tn = c;
-      tm = t - c * (c + 1) / 2;
-      return;
+      for (int c0 = 0;; c0 += TRI_GC) {                // band [c0, c1): c0 * w full-width rows, then its diagonal
+        const int c1 = min(c0 + TRI_GC, tiles_n), w = c1 - c0;
+        const int nb = c0 * w + w * (w + 1) / 2;
+        if (t < nb) {
+          if (t < c0 * w) { tm = t / w; tn = c0 + t % w; return; }
+          t -= c0 * w;
+          int r = 0;
+          while (t >= w - r) { t -= w - r; ++r; }      // diagonal block: row c0 + r has w - r tiles
+          tm = c0 + r; tn = c0 + r + t;
+          return;
+        }
+        t -= nb;
+      }
     }
     const int per_group = TC_GROUP_M * tiles_n;
     const int gidx = t / per_group, first_m = gidx * TC_GROUP_M;
@@ -215,6 +225,99 @@ struct TileSched {      // pair tiles: tiles_m pair-rows (256 rows) x tiles_n (2
     tn = r / gm;
   }
 };
+
+// Store of an updated iterate value to the container (FP32 / FP64) and to an operand (BF16 / TF32).
+__device__ __forceinline__ void put_cont(void *base, int64_t idx, int cont64, double v) {
+  if (cont64) ((double *)base)[idx] = v;
+  else ((float *)base)[idx] = (float)v;
+}
+__device__ __forceinline__ void put_op(void *base, int64_t idx, int prec, double v) {
+  if (prec == P_BF16) ((__nv_bfloat16 *)base)[idx] = __float2bfloat16_rn((float)v);
+  else ((float *)base)[idx] = to_tf32((float)v);
+}
+// EPI_SYMUPD on one 32-column segment of row `row` (reading R-22 with the tri form): the accumulator
+// is S_ij = (Chat Rhat + Rhat Chat)_ij (FP32, one accumulation over K = 2n); e = S/(2p) (exact
+// reciprocal for p = 2^k), C_{k+1} = q_m(C_ij + e) -- the op order of k_sym_update with s = S -- stored
+// at (i,j) and (j,i) in the container and as the next operands, delta partials weighted 2 off the
+// diagonal; elements below the diagonal are left to their mirror (bitwise symmetric iterates).
+__device__ __forceinline__ void sym_update_chunk(const GemmArgs &g, int64_t row, int64_t col, const uint32_t (&r)[32],
+                                                 EpiAcc &ea) {
+  const bool pow2p = (g.p & (g.p - 1)) == 0;
+  const double tp2 = (double)(2 * g.p), itp = 1.0 / tp2;
+  const int64_t plane = g.M * g.ldh;
+  const bool upper = row < g.col0 + col;              // the whole segment strictly above the diagonal
+  #pragma unroll 1
+  for (int j0 = 0; j0 < 32; j0 += 8) {                // not unrolled: compact code (instruction cache)
+    double cv[8], cn[8];
+    if (g.cont64) {
+      const double2 *src = (const double2 *)((const double *)g.cold + row * g.ldc + col + j0);
+      #pragma unroll
+      for (int q = 0; q < 4; ++q) { const double2 t = src[q]; cv[2 * q] = t.x; cv[2 * q + 1] = t.y; }
+    } else {
+      const float4 *src = (const float4 *)((const float *)g.cold + row * g.ldc + col + j0);
+      #pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const float4 t = src[q];
+        cv[4 * q] = t.x; cv[4 * q + 1] = t.y; cv[4 * q + 2] = t.z; cv[4 * q + 3] = t.w;
+      }
+    }
+    #pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int64_t c = col + j0 + v, gc = g.col0 + c;
+      const double s = (double)__uint_as_float(r[j0 + v]);
+      const double e = pow2p ? __dmul_rn(s, itp) : __ddiv_rn(s, tp2);
+      const double x = __dadd_rn(cv[v], e);
+      cn[v] = g.cont64 ? q_e11(x, g.m, g.rtz) : (double)q_e8(x, g.m, g.rtz);
+      if (!upper && row > gc) continue;                // lower triangle: the mirror element's value
+      const double dd = __dsub_rn(cn[v], cv[v]);
+      ea.d2 = __fma_rn(row != gc ? 2.0 * dd : dd, dd, ea.d2);
+      if (row != gc) {                                 // mirror (j, i): coalesced across the warp's rows
+        put_cont(g.cnew, c * g.ldc + row, g.cont64, cn[v]);
+        if (g.chat_new) put_op(g.chat_new, c * g.ldc + row, g.hprec, cn[v]);
+        put_op(g.qnext, c * g.ldh + row, g.tprec, cn[v]);
+        put_op(g.qnext, 2 * plane + c * g.ldh + row, g.tprec, cn[v]);
+      }
+      if (!upper) {                                    // diagonal segment: per-element direct stores
+        put_cont(g.cnew, row * g.ldc + c, g.cont64, cn[v]);
+        if (g.chat_new) put_op(g.chat_new, row * g.ldc + c, g.hprec, cn[v]);
+        put_op(g.qnext, row * g.ldh + c, g.tprec, cn[v]);
+        put_op(g.qnext, 2 * plane + row * g.ldh + c, g.tprec, cn[v]);
+      }
+    }
+    if (upper) {                                       // direct (i, j): vector stores of the 8 values
+      if (g.cont64) {
+        double2 *d = (double2 *)((double *)g.cnew + row * g.ldc + col + j0);
+        #pragma unroll
+        for (int q = 0; q < 4; ++q) d[q] = make_double2(cn[2 * q], cn[2 * q + 1]);
+      } else {
+        float4 *d = (float4 *)((float *)g.cnew + row * g.ldc + col + j0);
+        #pragma unroll
+        for (int q = 0; q < 2; ++q)
+          d[q] = make_float4((float)cn[4 * q], (float)cn[4 * q + 1], (float)cn[4 * q + 2], (float)cn[4 * q + 3]);
+      }
+      #pragma unroll
+      for (int o = 0; o < 3; ++o) {                    // chat_new (prec), qnext planes 0 and 2 (tprec)
+        void *base = o == 0 ? g.chat_new : g.qnext;
+        if (!base) continue;
+        const int pr = o == 0 ? g.hprec : g.tprec;
+        const int64_t idx = (o == 0 ? row * g.ldc : (o == 2 ? 2 * plane : 0) + row * g.ldh) + col + j0;
+        if (pr == P_BF16) {
+          uint32_t w[4];
+          #pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const __nv_bfloat162 b2 = __floats2bfloat162_rn((float)cn[2 * q], (float)cn[2 * q + 1]);
+            w[q] = *(const uint32_t *)&b2;
+          }
+          *(uint4 *)((__nv_bfloat16 *)base + idx) = make_uint4(w[0], w[1], w[2], w[3]);
+        } else {
+          float4 *d = (float4 *)((float *)base + idx);
+          d[0] = make_float4(to_tf32((float)cn[0]), to_tf32((float)cn[1]), to_tf32((float)cn[2]), to_tf32((float)cn[3]));
+          d[1] = make_float4(to_tf32((float)cn[4]), to_tf32((float)cn[5]), to_tf32((float)cn[6]), to_tf32((float)cn[7]));
+        }
+      }
+    }
+  }
+}
 
 // One 32-column chunk of one accumulator row: the fused epilogue with vectorised row access.
 template <int KIND>
@@ -714,7 +817,10 @@ cudaError_t launch_crt_finish(const GemmArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int KIND>
+// EF = 1: the fused symmetric update (EPI_SYMUPD) is the only epilogue of this instance -- with the
+// general epilogue's code in the same kernel the instruction cache thrashed (tensor pipe 30 % busy,
+// "no instruction" the top stall)
+template <int KIND, int EF = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const GemmArgs g) {
   extern __shared__ uint8_t smem_raw[];
@@ -786,7 +892,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
             if (leader) mbar_expect_tx(&full[stage], 2 * TC_STAGE_BYTES);
             const int64_t k0 = (int64_t)kb * bke;
             tma_load_3d_pair(sa, &mapA, &full[stage], (int)((kpl + k0) % g.a_kp), arow, (int)((kpl + k0) / g.a_kp));
-            tma_load_2d_pair(sb, &mapB, &full[stage], (int)(boff + k0), brow2);
+            if (g.b_pstride) tma_load_3d_pair(sb, &mapB, &full[stage], (int)(k0 % g.a_kp), brow2, (int)(k0 / g.a_kp));
+            else tma_load_2d_pair(sb, &mapB, &full[stage], (int)(boff + k0), brow2);
             if (++stage == TC_ST) { stage = 0; phase ^= 1; }
           }
         }
@@ -848,7 +955,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       for (int ch = hh * 4; ch < hh * 4 + 4; ++ch) {
         uint32_t r[32];
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * TC_BN + ch * 32, r);
-        if (crt) {
+        if (EF == 1) {
+          sym_update_chunk(g, row, colb + ch * 32, r, ea);
+        } else if (crt) {
           crt_chunk(g, lmod, row, colb + ch * 32, r);
         } else if (KIND == 3 && g.oz_grouped) {
           // the 32 accumulator values of this row segment are loaded up front (independent loads in
@@ -884,7 +993,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
       if (KIND == 3 && g.oz_grouped && (crt || gi > 2)) { ++it; continue; }   // partials after the finish only
       // per-tile partials: deterministic (fixed shuffle tree, warps summed in order 0..3)
-      if ((g.mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE)) || g.pmax) {
+      if ((g.mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE | EPI_SYMUPD)) || g.pmax) {
         double s = (g.mode & EPI_RESID) ? ea.r2 : ea.d2;
         float mx = ea.mx;
         #pragma unroll
@@ -896,7 +1005,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
         asm volatile("bar.sync 1, 256;\n" ::: "memory");
         if (et == 0) {
           const int64_t tile = ((g.col0 + colb) / TC_BN) * g.tiles_m + tile_m;
-          if (g.mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE))
+          if (g.mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE | EPI_SYMUPD))
           {
             const double *rr = red[it & 1];
             double acc = 0.0;
@@ -987,7 +1096,18 @@ cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
       return cudaErrorInvalidValue;
     }
   }
-  {
+  if (a.b_pstride) {   // K-concatenated B planes (fused symmetric update): [K / a_kp][N][a_kp] with plane stride
+    const cuuint64_t dims[3] = {(cuuint64_t)a.a_kp, (cuuint64_t)a.N, (cuuint64_t)(a.K / a.a_kp)};
+    const cuuint64_t strides[2] = {(cuuint64_t)(a.ldb * esz), (cuuint64_t)(a.b_pstride * esz)};
+    const cuuint32_t box[3] = {bke, (cuuint32_t)(TC_BN / 2), 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (enc(&mb, dt, 3, (void *)a.B, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS) {
+      snprintf(g_tc_err, sizeof g_tc_err, "cuTensorMapEncodeTiled(B, 3-D) failed");
+      return cudaErrorInvalidValue;
+    }
+  } else {
     // CRT: the residue planes of the B operand stacked along N ([crt_n][N][a_kp])
     const cuuint64_t dims[2] = {(cuuint64_t)(a.oz_grouped == 3 ? a.a_kp : a.K),
                                 (cuuint64_t)(a.oz_grouped == 3 ? a.N * a.crt_n : a.N)};
@@ -1007,28 +1127,32 @@ cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
   }
   const TileSched hs{(int)(a.M / (2 * TC_BM)), (int)(a.N / TC_BN), a.tri};
   const int ntiles = hs.count() * (a.oz_grouped == 3 ? a.crt_l1 - a.crt_l0 : 1);
-  if (a.tri && (a.mode & EPI_RESID) && a.oz_grouped != 3) {   // the tiles below the diagonal are not visited: zero partials
+  if (a.tri && (a.mode & (EPI_RESID | EPI_SYMUPD)) && a.oz_grouped != 3) {   // the tiles below the diagonal are not visited: zero partials
     cudaError_t z = cudaMemsetAsync(a.part, 0, (size_t)(a.N / TC_BN) * a.tiles_m * sizeof(double), s);
     if (z != cudaSuccess) return z;
   }
   const int maxpairs = num_sms() / 2;
   const int grid = 2 * (ntiles < maxpairs ? ntiles : maxpairs);
   cudaError_t e = cudaSuccess;
-  switch (tc_kind(a.prec)) {
-#define TC_LAUNCH(K)                                                                                     \
-    case K: {                                                                                            \
+  const bool symupd = (a.mode & EPI_SYMUPD) != 0;
+  if (symupd && tc_kind(a.prec) > 1) return cudaErrorNotSupported;
+  switch (tc_kind(a.prec) + (symupd ? 4 : 0)) {
+#define TC_LAUNCH(C, K, EF)                                                                              \
+    case C: {                                                                                            \
       static bool attr = false;                                                                          \
       if (!attr) {                                                                                       \
-        e = cudaFuncSetAttribute(k_gemm_tc<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM);     \
+        e = cudaFuncSetAttribute(k_gemm_tc<K, EF>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM); \
         if (e != cudaSuccess) return e;                                                                  \
         attr = true;                                                                                     \
       }                                                                                                  \
-      k_gemm_tc<K><<<grid, TC_NT, TC_SMEM, s>>>(ma, mb, a);                                              \
+      k_gemm_tc<K, EF><<<grid, TC_NT, TC_SMEM, s>>>(ma, mb, a);                                          \
     } break;
-    TC_LAUNCH(0)
-    TC_LAUNCH(1)
-    TC_LAUNCH(2)
-    TC_LAUNCH(3)
+    TC_LAUNCH(0, 0, 0)
+    TC_LAUNCH(1, 1, 0)
+    TC_LAUNCH(2, 2, 0)
+    TC_LAUNCH(3, 3, 0)
+    TC_LAUNCH(4, 0, 1)
+    TC_LAUNCH(5, 1, 1)
 #undef TC_LAUNCH
   }
   ++g_launches;

@@ -164,3 +164,33 @@ def test_tri_close_to_full_and_errors():
         s.iterate(1)
     assert e.value.status == ipr.IPR_E_INVALID_ARG
     s.close()
+
+
+def test_fused_symmetric_update_matches_separate():
+    # EPI_SYMUPD (off by default, IPR_FUSED_SYMUPD=1): S = W + W^T from one K-concatenated upper-triangle
+    # GEMM with the update in its epilogue -- same trajectory class as W GEMM + k_sym_update, checked in a
+    # subprocess so the process-wide switch does not leak into the other tests
+    import os, subprocess, sys, json
+    code = (
+        "import json, numpy as np, synth, torch, paper_1703_02283_b200 as ipr\n"
+        "from tests.gpu_util import run_gpu_trajectory\n"
+        "A = synth.spd(640, 2.0, 3)\n"
+        "low = dict(plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)\n"
+        "pg = [ipr.make_phase('bf16', **low), ipr.make_phase('fp64crt', mant_bits=ipr.IPR_MANT_ADAPTIVE, corr_prec='bf16')]\n"
+        "out, tr, hist, best = run_gpu_trajectory(A, 2, pg, 1e-12, 80, form='symmetric_tri')\n"
+        "np.save('/tmp/ipr_fused_best.npy', best)\n"
+        "print(json.dumps(dict(out=out, n=len(tr), cert=tr[-1]['rho_cert'], sym=bool(np.array_equal(best, best.T)))))\n")
+    env = dict(os.environ, IPR_FUSED_SYMUPD="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["out"] == ipr.IPR_CONVERGED and res["cert"] <= 1e-12 and res["sym"], res
+    fused = np.load("/tmp/ipr_fused_best.npy")
+    A = synth.spd(640, 2.0, 3)
+    low = dict(plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
+    pg = [ipr.make_phase("bf16", **low), ipr.make_phase("fp64crt", mant_bits=ipr.IPR_MANT_ADAPTIVE, corr_prec="bf16")]
+    out, tr, hist, best = run_gpu_trajectory(A, 2, pg, 1e-12, 80, form="symmetric_tri")
+    assert out == ipr.IPR_CONVERGED
+    assert rel_fro(fused, best) <= 1e-10
+    assert abs(res["n"] - len(tr)) <= 1
