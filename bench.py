@@ -35,7 +35,7 @@ METRIC = "time-to-FP64-residual 1e-12 (n=8192, p=2)"
 # from the residual (dynamic precision scaling, R-26), a BF16 correction GEMM, and convergence
 # certified on ||I - C^2 A||_F at full FP64 accuracy
 DEFAULT_SCHEDULE = "symtri:bf16>fp64crt@a/cbf16"
-EXTRA_SCHEDULES = ["fp64", "symtri:bf16>fp64oz@a/cbf16", "sym:fp64crt", "symtri:bf16>fp64oz@23/cbf16>fp64oz/cbf16", "symtri:bf16>fp64oz/cbf16", "sym:fp64oz", "symtri:fp8>bf16>fp64oz@23/cbf16>fp64oz/cbf16",
+EXTRA_SCHEDULES = ["fp64", "symtri:bf16>fp64oz@a/cbf16", "symtri:fp8>bf16>fp64crt@a/cbf16", "symtri:int8>bf16>fp64crt@a/cbf16", "sym:fp64crt", "symtri:bf16>fp64oz@23/cbf16>fp64oz/cbf16", "symtri:bf16>fp64oz/cbf16", "sym:fp64oz", "symtri:fp8>bf16>fp64oz@23/cbf16>fp64oz/cbf16",
                    "bf16>fp64", "tf32>fp64", "fp16>fp64", "sym:fp64", "sym:fp64/cbf16", "symtri:fp64/cbf16",
                    "symtri:bf16>fp64/cbf16", "symtri:bf16>tf32>fp64/cbf16", "symtri:fp8>bf16>fp64/cbf16",
                    "symtri:int8>bf16>fp64/cbf16", "symtri:fp16>fp64/cbf16",

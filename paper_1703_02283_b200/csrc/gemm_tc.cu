@@ -361,7 +361,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
   //     diagonal stores every element twice -- K-major (coalesced across the warp's rows) and
   //     mirrored row-major with 16-byte vector stores (the generic path's per-element mirror stores
   //     were uncoalesced: 1.11 ms vs 0.76 ms for the full GEMM 1).  Same FP64 arithmetic and order.
-  if (KIND <= 1 && g.tri && scale == 1.0 && (mode & EPI_STORE_T) &&
+  if (g.tri && (mode & EPI_STORE_T) &&
       (mode & ~(EPI_STORE_T | EPI_DIAG_MINUS | EPI_RESID)) == 0 && (g.tprec == P_BF16 || g.tprec == P_TF32) &&
       row < g.col0 + col) {
     const bool dm = (mode & EPI_DIAG_MINUS) != 0, rsd = (mode & EPI_RESID) != 0;
@@ -370,7 +370,8 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
       uint32_t pk[16];
       #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const double v = (double)__uint_as_float(r[j]);
+        const double a = acc_to_f64<KIND>(r[j]);
+        const double v = scale == 1.0 ? a : __dmul_rn(a, scale);   // scaled formats: exact 2^-(sigma)
         const double w = dm ? __dsub_rn(0.0, v) : v;          // row < gc: off the diagonal
         const __nv_bfloat16 b = __float2bfloat16_rn((float)w);
         t[(col + j) * g.ldt + row] = b;
@@ -389,7 +390,8 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
       float f[32];
       #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const double v = (double)__uint_as_float(r[j]);
+        const double a = acc_to_f64<KIND>(r[j]);
+        const double v = scale == 1.0 ? a : __dmul_rn(a, scale);
         const double w = dm ? __dsub_rn(0.0, v) : v;
         f[j] = to_tf32((float)w);
         t[(col + j) * g.ldt + row] = f[j];

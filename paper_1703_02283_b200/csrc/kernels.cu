@@ -130,27 +130,131 @@ __global__ void k_c0(const double *A, int64_t lda, int64_t n, int64_t col0, int6
   else ((float *)cont)[o] = q_e8(v, m, rtz);
 }
 
-// container (FP32 or FP64) local panel -> operand (phase prec), same [npad][kp] layout
-__global__ void k_make_operand(const void *cont, int cont64, int64_t count, int prec, const int *sig, void *op) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= count) return;
-  const double c = cont64 ? ((const double *)cont)[t] : (double)((const float *)cont)[t];
-  store_operand(op, t, prec, c, sig ? sig[0] : 0);
+// container (FP32 or FP64) local panel -> operand (phase prec), same [npad][kp] layout.  8 elements per
+// thread (vector loads; the per-element operand rounding is unchanged), scalar tail.
+// FP8 E4M3 from FP32 values (the container / scratch values are FP32): x 2^sg is exact in FP32 for
+// the scaled range, and the hardware RNE conversion (satfinite, subnormals kept) is the same single
+// rounding as to_e4m3 from FP64 (reading R-24)
+__device__ __forceinline__ void store8_fp8_f32(void *op, int64_t t0, const float (&f)[8], int sg) {
+  const float sc = __int_as_float((127 + sg) << 23);
+  uint32_t w[2];
+  #pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(make_float2(f[4 * q] * sc, f[4 * q + 1] * sc), __NV_SATFINITE, __NV_E4M3);
+    const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(make_float2(f[4 * q + 2] * sc, f[4 * q + 3] * sc), __NV_SATFINITE, __NV_E4M3);
+    w[q] = (uint32_t)lo | ((uint32_t)hi << 16);
+  }
+  *(uint2 *)((uint8_t *)op + t0) = make_uint2(w[0], w[1]);
+}
+template <int PREC>
+__device__ __forceinline__ void store8(void *op, int64_t t0, const double (&v)[8], int sg) {
+  if (PREC == P_FP8 || PREC == P_INT8) {
+    uint32_t w[2] = {0u, 0u};
+    #pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const double x = __dmul_rn(v[u], pow2(sg));
+      const uint32_t b = PREC == P_FP8 ? (uint32_t)to_e4m3(x) : (uint32_t)(uint8_t)to_int8(x);
+      w[u >> 2] |= b << (8 * (u & 3));
+    }
+    *(uint2 *)((uint8_t *)op + t0) = make_uint2(w[0], w[1]);
+  } else if (PREC == P_BF16 || PREC == P_FP16) {
+    uint32_t w[4];
+    #pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (PREC == P_BF16) {
+        const __nv_bfloat162 b2 = __floats2bfloat162_rn((float)v[2 * q], (float)v[2 * q + 1]);
+        w[q] = *(const uint32_t *)&b2;
+      } else {
+        const __half2 h2 = __floats2half2_rn((float)__dmul_rn(v[2 * q], pow2(sg)), (float)__dmul_rn(v[2 * q + 1], pow2(sg)));
+        w[q] = *(const uint32_t *)&h2;
+      }
+    }
+    *(uint4 *)((uint16_t *)op + t0) = make_uint4(w[0], w[1], w[2], w[3]);
+  } else {
+    #pragma unroll
+    for (int u = 0; u < 8; ++u) store_operand(op, t0 + u, PREC, v[u], sg);
+  }
+}
+template <int PREC>
+__global__ void k_make_operand8(const void *cont, int cont64, int64_t count, const int *sig, void *op) {
+  const int64_t t0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (t0 >= count) return;
+  const int sg = sig ? sig[0] : 0;
+  if (t0 + 8 > count) {
+    for (int64_t t = t0; t < count; ++t) {
+      const double c = cont64 ? ((const double *)cont)[t] : (double)((const float *)cont)[t];
+      store_operand(op, t, PREC, c, sg);
+    }
+    return;
+  }
+  double v[8];
+  if (cont64) {
+    #pragma unroll
+    for (int q = 0; q < 4; ++q) { const double2 d = ((const double2 *)((const double *)cont + t0))[q]; v[2 * q] = d.x; v[2 * q + 1] = d.y; }
+  } else {
+    float f8[8];
+    #pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const float4 f = ((const float4 *)((const float *)cont + t0))[q];
+      f8[4 * q] = f.x; f8[4 * q + 1] = f.y; f8[4 * q + 2] = f.z; f8[4 * q + 3] = f.w;
+    }
+    if (PREC == P_FP8 && sg > -100 && sg < 100) { store8_fp8_f32(op, t0, f8, sg); return; }
+    #pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = f8[u];
+  }
+  store8<PREC>(op, t0, v, sg);
 }
 
 // T scratch (FP32, [kp][npad]) -> scaled operand (FP16 / FP8 / INT8) with the exponent sig[0]
-__global__ void k_scale_op(const float *src, int64_t count, const int *sig, int prec, void *dst) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= count) return;
-  store_operand(dst, t, prec, (double)src[t], sig[0]);
+template <int PREC>
+__global__ void k_scale_op8(const float *src, int64_t count, const int *sig, void *dst) {
+  const int64_t t0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (t0 >= count) return;
+  const int sg = sig[0];
+  if (t0 + 8 > count) {
+    for (int64_t t = t0; t < count; ++t) store_operand(dst, t, PREC, (double)src[t], sg);
+    return;
+  }
+  float f8[8];
+  #pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const float4 f = ((const float4 *)(src + t0))[q];
+    f8[4 * q] = f.x; f8[4 * q + 1] = f.y; f8[4 * q + 2] = f.z; f8[4 * q + 3] = f.w;
+  }
+  if (PREC == P_FP8 && sg > -100 && sg < 100) { store8_fp8_f32(dst, t0, f8, sg); return; }
+  double v[8];
+  #pragma unroll
+  for (int u = 0; u < 8; ++u) v[u] = f8[u];
+  store8<PREC>(dst, t0, v, sg);
 }
 
 __global__ void k_maxabs_cont(const void *cont, int cont64, int64_t count, float *pmax) {
   __shared__ float red[32];
   float mx = 0.f;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (int64_t)gridDim.x * blockDim.x) {
-    const double c = cont64 ? ((const double *)cont)[t] : (double)((const float *)cont)[t];
-    mx = fmaxf(mx, fabsf((float)c));
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (cont64) {
+    const int64_t n2 = count / 2;
+    for (int64_t q = t; q < n2; q += stride) {
+      const double2 d = ((const double2 *)cont)[q];
+      mx = fmaxf(mx, fmaxf(fabsf((float)d.x), fabsf((float)d.y)));
+    }
+    for (int64_t u = 2 * n2 + t; u < count; u += stride) mx = fmaxf(mx, fabsf((float)((const double *)cont)[u]));
+  } else {
+    const int64_t n4 = count / 4;
+    int64_t q = t;
+    for (; q + 3 * stride < n4; q += 4 * stride) {     // 4 independent 16-byte loads in flight
+      float4 f[4];
+      #pragma unroll
+      for (int u = 0; u < 4; ++u) f[u] = ((const float4 *)cont)[q + u * stride];
+      #pragma unroll
+      for (int u = 0; u < 4; ++u) mx = fmaxf(mx, fmaxf(fmaxf(fabsf(f[u].x), fabsf(f[u].y)), fmaxf(fabsf(f[u].z), fabsf(f[u].w))));
+    }
+    for (; q < n4; q += stride) {
+      const float4 f = ((const float4 *)cont)[q];
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(f.x), fabsf(f.y)), fmaxf(fabsf(f.z), fabsf(f.w))));
+    }
+    for (int64_t u = 4 * n4 + t; u < count; u += stride) mx = fmaxf(mx, fabsf(((const float *)cont)[u]));
   }
   const float b = block_max<256>(mx, red);
   if (threadIdx.x == 0) pmax[blockIdx.x] = b;
@@ -386,11 +490,25 @@ cudaError_t launch_c0(const double *A, int64_t lda, int64_t n, int64_t npad, int
 }
 cudaError_t launch_make_operand(const void *cont, int cont64, int64_t count, int prec, const int *sig, void *op,
                                 cudaStream_t s) {
-  k_make_operand<<<nblk(count, 256), 256, 0, s>>>(cont, cont64, count, prec, sig, op);
+  const unsigned g = nblk((count + 7) / 8, 256);
+  switch (prec) {
+    case P_BF16: k_make_operand8<P_BF16><<<g, 256, 0, s>>>(cont, cont64, count, sig, op); break;
+    case P_FP16: k_make_operand8<P_FP16><<<g, 256, 0, s>>>(cont, cont64, count, sig, op); break;
+    case P_FP8: k_make_operand8<P_FP8><<<g, 256, 0, s>>>(cont, cont64, count, sig, op); break;
+    case P_INT8: k_make_operand8<P_INT8><<<g, 256, 0, s>>>(cont, cont64, count, sig, op); break;
+    case P_TF32: k_make_operand8<P_TF32><<<g, 256, 0, s>>>(cont, cont64, count, sig, op); break;
+    default: k_make_operand8<P_FP64><<<g, 256, 0, s>>>(cont, cont64, count, sig, op); break;
+  }
   LAUNCH_CHECK();
 }
 cudaError_t launch_scale_op(const float *src, int64_t count, const int *sig, int prec, void *dst, cudaStream_t s) {
-  k_scale_op<<<nblk(count, 256), 256, 0, s>>>(src, count, sig, prec, dst);
+  const unsigned g = nblk((count + 7) / 8, 256);
+  switch (prec) {
+    case P_FP16: k_scale_op8<P_FP16><<<g, 256, 0, s>>>(src, count, sig, dst); break;
+    case P_FP8: k_scale_op8<P_FP8><<<g, 256, 0, s>>>(src, count, sig, dst); break;
+    case P_INT8: k_scale_op8<P_INT8><<<g, 256, 0, s>>>(src, count, sig, dst); break;
+    default: return cudaErrorInvalidValue;
+  }
   LAUNCH_CHECK();
 }
 cudaError_t launch_maxabs_cont(const void *cont, int cont64, int64_t count, float *pmax, int nparts, cudaStream_t s) {
