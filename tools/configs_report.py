@@ -39,7 +39,7 @@ def run(A, p, phases, label, max_iters=400, form="literal", tol=1e-12):
     rmin, kmin = min(fin) if fin else (float("nan"), -1)
     per = {}
     for t in tr:
-        native = {"fp64": 52, "fp64oz": 52, "bf16": 7, "tf32": 10, "fp16": 10, "fp8": 3, "int8": 7}[t["prec"]]
+        native = {"fp64": 52, "fp64oz": 52, "fp64crt": 52, "bf16": 7, "tf32": 10, "fp16": 10, "fp8": 3, "int8": 7}[t["prec"]]
         d = per.setdefault(t["prec"] + ("" if t["mant_bits"] == native else f"/m{t['mant_bits']}"),
                            {"iters": 0, "ms": 0.0, "gemms": 0})
         d["iters"] += 1
@@ -125,7 +125,9 @@ def main():
             A, _ = synth.spd_torch(n, kappa, seed) if n >= 4096 else (torch.from_numpy(synth.spd(n, kappa, seed)).cuda(), None)
             lab = f"{name} n={n} p={p} kappa={kappa:g} ({tag})"
             runs = [(f"{sym}:fp64/cbf16", 1e-12)]
-            runs.append((f"{sym}:bf16>fp64oz@a/cbf16" if (n <= 8192 and p == 2) else f"{sym}:bf16>fp64/cbf16", 1e-12))
+            # FP64 phase on INT8 tensor cores (CRT, R-28) where its residue planes fit (n <= 8192: ~6 GB;
+            # n = 32768 would need ~190 GB), else DMMA
+            runs.append((f"{sym}:bf16>fp64crt@a/cbf16" if n <= 8192 else f"{sym}:bf16>fp64/cbf16", 1e-12))
             if tag == "stated":
                 runs.append(("cpl:fp64", 1e-6))
             for sched, tol in runs:
