@@ -21,6 +21,7 @@ RUNS = [  # (label, p, schedule, final_tol)
     ("p2 symtri:fp64/cbf16", 2, "symtri:fp64/cbf16", 1e-12),
     ("p2 symtri:bf16>fp64/cbf16", 2, "symtri:bf16>fp64/cbf16", 1e-12),
     ("p2 symtri:bf16>fp64oz@a/cbf16", 2, "symtri:bf16>fp64oz@a/cbf16", 1e-12),
+    ("p2 symtri:bf16>fp64crt@a/cbf16", 2, "symtri:bf16>fp64crt@a/cbf16", 1e-12),
     ("p2 cpl:fp64 (to 1e-6)", 2, "cpl:fp64", 1e-6),
 ]
 
