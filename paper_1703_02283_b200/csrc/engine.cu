@@ -83,9 +83,10 @@ struct ipr_ctx {
   // [npad] of Ahat, of Chat (per iterate buffer; symmetric, so one set serves both roles) and of the
   // current B operand, their exponents, the bits b each set was split with (-1: stale), and the
   // byte scratch of the modulus products
-  int8_t *crA = nullptr, *crC[2] = {nullptr, nullptr}, *crB = nullptr;
-  int *crA_sig = nullptr, *crC_sig[2] = {nullptr, nullptr}, *crB_sig = nullptr;
-  int crA_b = -1, crC_b[2] = {-1, -1};
+  // ONE Chat set (keyed by iterate buffer and bits; re-split lazily -- at n = 32768 a set is 19 GB)
+  int8_t *crA = nullptr, *crC = nullptr, *crB = nullptr;
+  int *crA_sig = nullptr, *crC_sig = nullptr, *crB_sig = nullptr;
+  int crA_b = -1, crC_for = -1, crC_b = -1;
   uint8_t *crV = nullptr;
   // symmetric-tri form, fused update (EPI_SYMUPD): per iterate buffer [Chat | Rhat | Chat] in the
   // correction format -- the A operand [Chat | Rhat] is planes 0-1, the B operand [Rhat ; Chat] planes 1-2
@@ -365,10 +366,10 @@ ipr_status crt_ensure_a(ipr_ctx *c, int b) {
   return IPR_OK;
 }
 ipr_status crt_ensure_c(ipr_ctx *c, int i, int b) {
-  if (c->crC_b[i] == b) return IPR_OK;
-  CK(launch_crt_split((const double *)c->chat[i], c->npad, c->npad, c->npad, b, crt_moduli(b, c->n), c->crC[i],
-                      c->crC_sig[i], c->st));
-  c->crC_b[i] = b;
+  if (c->crC_for == i && c->crC_b == b) return IPR_OK;
+  CK(launch_crt_split((const double *)c->chat[i], c->npad, c->npad, c->npad, b, crt_moduli(b, c->n), c->crC,
+                      c->crC_sig, c->st));
+  c->crC_for = i; c->crC_b = b;
   return IPR_OK;
 }
 void crt_args(ipr_ctx *c, GemmArgs &g, int b) {
@@ -381,8 +382,8 @@ ipr_status crt_operands(ipr_ctx *c, GemmArgs &g, int i, const void *Xt) {
   if (i < 0) CKS(crt_ensure_a(c, b));
   else CKS(crt_ensure_c(c, i, b));
   CK(launch_crt_split((const double *)Xt, c->npad, c->npad, c->npad, b, crt_moduli(b, c->n), c->crB, c->crB_sig, c->st));
-  g.oz_a = i < 0 ? c->crA : c->crC[i];
-  g.oz_rsig = i < 0 ? c->crA_sig : c->crC_sig[i];
+  g.oz_a = i < 0 ? c->crA : c->crC;
+  g.oz_rsig = i < 0 ? c->crA_sig : c->crC_sig;
   g.oz_b = c->crB; g.oz_csig = c->crB_sig;
   crt_args(c, g, b);
   return IPR_OK;
@@ -444,7 +445,7 @@ ipr_status begin_phase(ipr_ctx *c, bool first) {
   }
   CKS(make_operand(c, c->cur, P));
   c->c_anchor = true;                // coupled form: re-anchor M = X^p A in this phase
-  c->crA_b = -1; c->crC_b[0] = -1; c->crC_b[1] = -1;   // CRT residues: split lazily per chain
+  c->crA_b = -1; c->crC_for = -1; c->crC_b = -1;     // CRT residues: split lazily per chain
   if (P.prec == IPR_FP64_OZ) {   // digits of Ahat (A role) and of Chat (both roles; G = 1, symmetric)
     CK(launch_oz_split((const double *)c->Aop, c->npad, c->npad, c->npad, OZ_S, c->ozA, nullptr, c->ozA_sig, c->st));
     CKS(oz_split_chat(c, c->cur));
@@ -554,7 +555,7 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
           const int b = crt_bits_now(c);
           CKS(crt_ensure_a(c, b));
           CKS(crt_ensure_c(c, c->cur, b));
-          g.oz_a = c->crA; g.oz_rsig = c->crA_sig; g.oz_b = c->crC[c->cur]; g.oz_csig = c->crC_sig[c->cur];
+          g.oz_a = c->crA; g.oz_rsig = c->crA_sig; g.oz_b = c->crC; g.oz_csig = c->crC_sig;
           crt_args(c, g, b);
         } else {
           CKS(crt_operands(c, g, c->cur, c->T[(j - 1) & 1]));
@@ -698,7 +699,7 @@ ipr_status update_sym(ipr_ctx *c) {
     CK(cudaEventRecord(c->ev[3], c->st));
     c->upd_timed = true;
     if (P.prec == IPR_FP64_OZ) CKS(oz_split_chat(c, nx));
-    c->crC_b[nx] = -1;
+    if (c->crC_for == nx) c->crC_for = -1;
     c->m_of_cur = P.adaptive ? c->oz_m_next : P.m;
     c->cur = nx;
     return IPR_OK;
@@ -727,7 +728,7 @@ ipr_status update_sym(ipr_ctx *c) {
   if (is_scaled(P.prec)) CKS(make_operand(c, nx, P));   // sigma from max|C_{k+1}|, then all-gather
   else CKS(gather_chat(c, nx, P.prec));
   if (P.prec == IPR_FP64_OZ) CKS(oz_split_chat(c, nx));
-  c->crC_b[nx] = -1;
+  if (c->crC_for == nx) c->crC_for = -1;
   c->m_of_cur = P.adaptive ? c->oz_m_next : P.m;
   if (!same_fmt(P.corr, P.prec)) CKS(gather_bytes(c, c->chatc[nx], (size_t)(c->npad * c->kp) * elt_size(P.corr), "Chat corr"));
   if (c->world > 1) CKS(make_xt(c, nx, P));
@@ -838,6 +839,8 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
   bool fq = false;                      // any phase with the fused symmetric update: [Chat | Rhat | Chat] x 2
   for (auto &P : c->ph) fq |= fused_sym_ok(c, P);
   const size_t qb = fq ? 3 * full * 4 : 0;
+  size_t cesz = 2;                      // correction-format copies of Chat: BF16 2 B, TF32 4 B
+  for (auto &P : c->ph) if (!same_fmt(P.corr, P.prec) && elt_size(P.corr) > (int)cesz) cesz = elt_size(P.corr);
   struct Slot { void **p; size_t bytes; };
   const Slot slots[] = {
       {&c->chat[0], full * 8}, {&c->chat[1], full * 8}, {&c->cont[0], panel * 4}, {&c->cont[1], panel * 4},
@@ -845,7 +848,7 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       {(void **)&c->part, (size_t)c->npart * 8}, {(void **)&c->pmax, (size_t)c->npart * 4},
       {(void **)&c->tscr, fp16 ? panel * 4 : 0},
       {&c->Afull, (c->world > 1 && c->form != IPR_FORM_LITERAL) ? full * 8 : 0},
-      {&c->chatc[0], need_corr ? full * 4 : 0}, {&c->chatc[1], need_corr ? full * 4 : 0},
+      {&c->chatc[0], need_corr ? full * cesz : 0}, {&c->chatc[1], need_corr ? full * cesz : 0},
       {&c->wbuf, is_sym(c) ? full * c->wbytes : 0},
       {&c->Zr, (is_sym(c) && c->world == 1) ? panel * 8 : 0},
       {(void **)&c->ozA, oz ? full * OZ_S : 0}, {(void **)&c->ozC[0], oz ? full * OZ_S : 0},
@@ -854,13 +857,15 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       {(void **)&c->ozA_sig, oz ? (size_t)c->npad * 4 : 0}, {(void **)&c->ozC_sig[0], oz ? (size_t)c->npad * 4 : 0},
       {(void **)&c->ozC_sig[1], oz ? (size_t)c->npad * 4 : 0}, {(void **)&c->ozB_sig, oz ? (size_t)c->npad * 4 : 0},
       {(void **)&c->ozacc, oz ? full * 8 : 0},
-      {(void **)&c->crA, crp}, {(void **)&c->crC[0], crp}, {(void **)&c->crC[1], crp}, {(void **)&c->crB, crp},
-      {(void **)&c->crA_sig, crs}, {(void **)&c->crC_sig[0], crs}, {(void **)&c->crC_sig[1], crs},
+      {(void **)&c->crA, crp}, {(void **)&c->crC, crp}, {(void **)&c->crB, crp},
+      {(void **)&c->crA_sig, crs}, {(void **)&c->crC_sig, crs},
       {(void **)&c->crB_sig, crs}, {(void **)&c->crV, cr ? full * CRT_MAX : 0},
       {&c->qbuf[0], qb}, {&c->qbuf[1], qb},
       {&c->cM[0], cpl ? panel * 8 : 0}, {&c->cM[1], cpl ? panel * 8 : 0}, {&c->cNk[0], cpl ? panel * 8 : 0},
       {&c->cNk[1], cpl ? panel * 8 : 0}, {&c->cNf, cpl ? full * 8 : 0},
-      {(void **)&c->full64, full * 8}, {&c->Acert, panel * 8}};
+      // CRT arenas: the certify / copy-out scratch lives in the B-residue and v-byte scratch (dead
+      // outside a CRT product; every product re-splits its B operand)
+      {(void **)&c->full64, cr ? 0 : full * 8}, {&c->Acert, cr ? 0 : panel * 8}};
   size_t total = 0;
   for (const Slot &q : slots) total += (q.bytes + 255) / 256 * 256;
   // stream-ordered allocation from a library-owned pool that retains its memory, so back-to-back
@@ -879,6 +884,7 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
     *q.p = q.bytes ? base + off : nullptr;
     off += (q.bytes + 255) / 256 * 256;
   }
+  if (cr) { c->full64 = (double *)c->crB; c->Acert = c->crV; }   // 8 B x npad^2 <= 18 B x npad^2
   CK(cudaMemsetAsync(c->chat[0], 0, full * 8, c->st));
   CK(cudaMemsetAsync(c->chat[1], 0, full * 8, c->st));
   return IPR_OK;

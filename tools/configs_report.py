@@ -125,9 +125,9 @@ def main():
             A, _ = synth.spd_torch(n, kappa, seed) if n >= 4096 else (torch.from_numpy(synth.spd(n, kappa, seed)).cuda(), None)
             lab = f"{name} n={n} p={p} kappa={kappa:g} ({tag})"
             runs = [(f"{sym}:fp64/cbf16", 1e-12)]
-            # FP64 phase on INT8 tensor cores (CRT, R-28) where its residue planes fit (n <= 8192: ~6 GB;
-            # n = 32768 would need ~190 GB), else DMMA
-            runs.append((f"{sym}:bf16>fp64crt@a/cbf16" if n <= 8192 else f"{sym}:bf16>fp64/cbf16", 1e-12))
+            # FP64 phase on INT8 tensor cores (CRT, R-28): ~154 GB of arena at n = 32768 (one Chat residue
+            # set, scratch aliases), fits a B200
+            runs.append((f"{sym}:bf16>fp64crt@a/cbf16", 1e-12))
             if tag == "stated":
                 runs.append(("cpl:fp64", 1e-6))
             for sched, tol in runs:
