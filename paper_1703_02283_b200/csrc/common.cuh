@@ -270,6 +270,13 @@ __device__ __forceinline__ float block_max(float v, float *red) {
 
 // Host-side launch declarations (implemented in kernels.cu / gemm_dmma.cu / gemm_tc.cu).
 namespace ipr {
+// Per-device "done once" flag for device state that a process sets up lazily (function attributes,
+// __constant__ tables): one bit per device ordinal, so a second GPU in the process gets its own setup.
+struct DeviceOnce {
+  unsigned long long bits = 0ull;
+  bool done() const { int d = 0; cudaGetDevice(&d); return d < 64 && ((bits >> d) & 1ull); }
+  void set() { int d = 0; cudaGetDevice(&d); if (d < 64) bits |= 1ull << d; }
+};
 extern int64_t g_launches;
 cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s);
 cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s);  // BF16 / FP16 / TF32 / FP8 / INT8

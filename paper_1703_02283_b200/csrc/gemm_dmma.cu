@@ -165,11 +165,11 @@ __global__ void __launch_bounds__(DM_NT, 2) k_gemm_dmma(const GemmArgs g) {
 
 template <int MODE>
 static cudaError_t launch_mode(const GemmArgs &a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static DeviceOnce attr;
+  if (!attr.done()) {
     cudaError_t e = cudaFuncSetAttribute(k_gemm_dmma<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, DM_SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.set();
   }
   dim3 grid((unsigned)((a.N / DM_BN) * (a.M / DM_BM)));
   k_gemm_dmma<MODE><<<grid, DM_NT, DM_SMEM, s>>>(a);

@@ -802,11 +802,11 @@ cudaError_t launch_crt_finish(const GemmArgs &a, cudaStream_t s) {
   switch (a.crt_n) {
 #define CRT_FIN(N)                                                                                       \
     case N: {                                                                                            \
-      static bool attr = false;                                                                          \
-      if (!attr) {                                                                                       \
+      static DeviceOnce attr;                                                                            \
+      if (!attr.done()) {                                                                                \
         cudaError_t e = cudaFuncSetAttribute(k_crt_finish<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
         if (e != cudaSuccess) return e;                                                                  \
-        attr = true;                                                                                     \
+        attr.set();                                                                                      \
       }                                                                                                  \
       k_crt_finish<N><<<2 * hs.count(), 256, smem, s>>>(a);                                              \
     } break;
@@ -1057,14 +1057,13 @@ static EncodeTiledFn encode_fn() {
 char g_tc_err[256] = "";
 const char *tc_last_error() { return g_tc_err; }
 
-static int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  }
-  return n;
+static int num_sms() {            // per device ordinal (cached)
+  static int cache[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
+  return cache[dev];
 }
 
 cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
@@ -1141,11 +1140,11 @@ cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
   switch (tc_kind(a.prec) + (symupd ? 4 : 0)) {
 #define TC_LAUNCH(C, K, EF)                                                                              \
     case C: {                                                                                            \
-      static bool attr = false;                                                                          \
-      if (!attr) {                                                                                       \
+      static DeviceOnce attr;                                                                            \
+      if (!attr.done()) {                                                                                \
         e = cudaFuncSetAttribute(k_gemm_tc<K, EF>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM); \
         if (e != cudaSuccess) return e;                                                                  \
-        attr = true;                                                                                     \
+        attr.set();                                                                                      \
       }                                                                                                  \
       k_gemm_tc<K, EF><<<grid, TC_NT, TC_SMEM, s>>>(ma, mb, a);                                          \
     } break;

@@ -328,11 +328,11 @@ void crt_set_timer(CrtTimer *t) { t_crt_timer = t; }
 // storing v_l bytes; then k_crt_finish reconstructs and applies the hot path's epilogue g.mode
 // (fused into the last modulus' epilogue it thrashed L1 on the residue loads: 3.4 ms).
 cudaError_t launch_gemm_crt(const GemmArgs &g, cudaStream_t s) {
-  static bool uploaded = false;
-  if (!uploaded) {
+  static DeviceOnce uploaded;                   // the __constant__ table is per device
+  if (!uploaded.done()) {
     cudaError_t e = tc_set_crt_table(crt_table());
     if (e != cudaSuccess) return e;
-    uploaded = true;
+    uploaded.set();
   }
   if (!g.oz_a || !g.oz_b || !g.oz_rsig || !g.oz_csig || !g.crt_v || g.M != g.K || g.N != g.K || g.crt_n < 2 ||
       g.crt_n > CRT_MAX)
