@@ -242,44 +242,60 @@ int crt_bits(int S, int64_t n) {
   return b;
 }
 
-// Symmetric residue byte of y = c2 2^42 + c1 2^21 + c0 - 2^62 modulo the compile-time modulus M
-// (c0, c1, c2 in [0, 2^21): the caller biased y by 2^62).  Integer ALU only, ~7 operations:
-// r = c0 + c1 K1 + c2 K2 + K3 < 2^30 (K3 = h - 2^62 mod M, h = the symmetric offset), u = r mod M
-// by an exact multiply-high (x < 2^30, magic ceil(2^39 / M) < 2^32: error < 2^-9 < 1/M), v = u - h.
+// Symmetric residue byte of y = yb - 2^62 modulo the compile-time modulus M, yb = y + 2^62 in [0, 2^63)
+// given as its two 32-bit halves (eight unsigned bytes b_t): yb mod M = (sum_t b_t (2^(8t) mod M)) mod M,
+// the byte sum as two __dp4a (< 8 * 255 * 255 + M < 2^20) with h - 2^62 mod M folded into the first
+// accumulator, then one exact multiply-high reduction (x < 2^20, magic ceil(2^32 / M): error < 2^-12
+// < 1/M) and the shift by the symmetric offset h.  ~5 integer operations per residue.
 template <int M>
-__device__ __forceinline__ uint32_t crt_res8(uint32_t c0, uint32_t c1, uint32_t c2) {
+__device__ __forceinline__ uint32_t crt_res8(uint32_t lo, uint32_t hi) {
   constexpr uint32_t h = M == 256 ? 128 : (M - 1) / 2;
-  constexpr uint32_t K1 = (1u << 21) % M, K2 = (uint32_t)((1ull << 42) % M);
+  constexpr uint32_t w0 = 1u % M, w1 = (1u << 8) % M, w2 = (1u << 16) % M, w3 = (1u << 24) % M;
+  constexpr uint32_t w4 = (uint32_t)((1ull << 32) % M), w5 = (uint32_t)((1ull << 40) % M);
+  constexpr uint32_t w6 = (uint32_t)((1ull << 48) % M), w7 = (uint32_t)((1ull << 56) % M);
+  constexpr uint32_t KL = w0 | (w1 << 8) | (w2 << 16) | (w3 << 24), KH = w4 | (w5 << 8) | (w6 << 16) | (w7 << 24);
   constexpr uint32_t K3 = (uint32_t)((h + M - (uint32_t)((1ull << 62) % M)) % M);
-  constexpr uint32_t MAG = (uint32_t)(((1ull << 39) + M - 1) / M);
-  const uint32_t r = c2 * K2 + (c1 * K1 + (c0 + K3));
-  const uint32_t u = r - (__umulhi(r, MAG) >> 7) * (uint32_t)M;
+  constexpr uint32_t MAG = (uint32_t)(((1ull << 32) + M - 1) / M);
+  const uint32_t r = __dp4a(hi, KH, __dp4a(lo, KL, K3));
+  const uint32_t u = r - __umulhi(r, MAG) * (uint32_t)M;
   return u - h;                                   // the low byte is the residue (packed by PRMT)
 }
 template <int L>
-__device__ __forceinline__ void crt_split4(const uint32_t (&c0)[4], const uint32_t (&c1)[4], const uint32_t (&c2)[4],
-                                           int nm, int8_t *dst, int64_t plane) {
+__device__ __forceinline__ void crt_split4(const uint32_t (&lo)[4], const uint32_t (&hi)[4], int nm, int8_t *dst,
+                                           int64_t plane) {
   if constexpr (L < CRT_MAX) {
     if (L < nm) {
       uint32_t b[4];
       #pragma unroll
-      for (int u = 0; u < 4; ++u) b[u] = crt_res8<kModuli[L]>(c0[u], c1[u], c2[u]);
+      for (int u = 0; u < 4; ++u) b[u] = crt_res8<kModuli[L]>(lo[u], hi[u]);
       *(uint32_t *)(dst + (int64_t)L * plane) =
           __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
-      crt_split4<L + 1>(c0, c1, c2, nm, dst, plane);
+      crt_split4<L + 1>(lo, hi, nm, dst, plane);
     }
   }
 }
 
 // Residues of the rows of X (FP64, row-major, leading dimension ld): one block per row; plane l of
 // `planes` holds (Xbar mod m_l) at planes[l * rows * cols + r * cols + k]; sig[r] = e_r.
-__global__ void __launch_bounds__(256, 4) k_crt_split(const double *__restrict__ X, int64_t ld, int64_t rows, int64_t cols,
-                                                   int b, int nm, int8_t *planes, int *sig) {
+// SMEM: the row is staged in shared memory (cols * 8 B <= 64 KB), so the maximum pass and the residue
+// pass read it from DRAM once (with two global passes the residue writes evicted it between them).
+template <bool SMEM>
+__global__ void __launch_bounds__(256, 3) k_crt_split(const double *__restrict__ X, int64_t ld, int64_t rows,
+                                                      int64_t cols, int b, int nm, int8_t *planes, int *sig) {
+  extern __shared__ double srow[];
   __shared__ double red[8];
   const int64_t r = blockIdx.x;
   const double *x = X + r * ld;
   double mx = 0.0;
-  for (int64_t k = threadIdx.x; k < cols; k += blockDim.x) mx = fmax(mx, fabs(x[k]));
+  if (SMEM) {
+    for (int64_t k = (int64_t)threadIdx.x * 2; k < cols; k += (int64_t)blockDim.x * 2) {
+      const double2 t = *(const double2 *)(x + k);
+      *(double2 *)(srow + k) = t;
+      mx = fmax(mx, fmax(fabs(t.x), fabs(t.y)));
+    }
+  } else {
+    for (int64_t k = threadIdx.x; k < cols; k += blockDim.x) mx = fmax(mx, fabs(x[k]));
+  }
   #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
@@ -295,24 +311,36 @@ __global__ void __launch_bounds__(256, 4) k_crt_split(const double *__restrict__
   if (threadIdx.x == 0) sig[r] = e;
   const double sc = pow2(e);
   const int64_t plane = rows * cols;
+  const double *src = SMEM ? (const double *)srow : x;
+  #pragma unroll 2
   for (int64_t k0 = (int64_t)threadIdx.x * 4; k0 < cols; k0 += (int64_t)blockDim.x * 4) {
-    uint32_t c0[4], c1[4], c2[4];
-    const double2 *xp = (const double2 *)(x + k0);
+    uint32_t lo[4], hi[4];
+    const double2 *xp = (const double2 *)(src + k0);
     #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const double2 t = xp[u >> 1];
-      // Xbar + 2^62 in [0, 2^63): three 21-bit fields
+      // Xbar + 2^62 in [0, 2^63): eight unsigned bytes
       const uint64_t y = (uint64_t)__double2ll_rn(__dmul_rn((u & 1) ? t.y : t.x, sc)) + (1ull << 62);
-      c0[u] = (uint32_t)y & 0x1fffffu; c1[u] = (uint32_t)(y >> 21) & 0x1fffffu; c2[u] = (uint32_t)(y >> 42);
+      lo[u] = (uint32_t)y; hi[u] = (uint32_t)(y >> 32);
     }
-    crt_split4<0>(c0, c1, c2, nm, planes + r * cols + k0, plane);
+    crt_split4<0>(lo, hi, nm, planes + r * cols + k0, plane);
   }
 }
 
 cudaError_t launch_crt_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int b, int nm, int8_t *planes,
                              int *sig, cudaStream_t s) {
   if (b < 2 || b > CRT_BMAX || nm < 2 || nm > CRT_MAX || cols % 4) return cudaErrorInvalidValue;
-  k_crt_split<<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, b, nm, planes, sig);
+  if (cols * 8 <= 65536 && ld % 2 == 0) {
+    static DeviceOnce attr;
+    if (!attr.done()) {
+      cudaError_t e = cudaFuncSetAttribute(k_crt_split<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      if (e != cudaSuccess) return e;
+      attr.set();
+    }
+    k_crt_split<true><<<(unsigned)rows, 256, (size_t)cols * 8, s>>>(X, ld, rows, cols, b, nm, planes, sig);
+  } else {
+    k_crt_split<false><<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, b, nm, planes, sig);
+  }
   ++g_launches;
   return cudaGetLastError();
 }
