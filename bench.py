@@ -236,10 +236,10 @@ def main():
             A_np = np.ascontiguousarray((G + G.T) * 0.5 + np.eye(n) * 0.75)
         # the oracle's FP64 work for the arm's schedule: the symmetric forms evaluate p GEMMs per chain
         # plus the W GEMM per update (the oracle computes the full C A C even for `symtri`) and p
-        # certification GEMMs; 27 iterations = the GPU run of the default schedule (19 + 8,
-        # profiles/r01e_bench_line.json).  The literal form: 20 chains / 19 updates.
+        # certification GEMMs; 28 iterations = the GPU run of the default schedule (17 + 3 + 8,
+        # profiles/r01i_bench_line.json).  The literal form: 20 chains / 19 updates.
         form_ref, _ = parse_schedule(args.schedule)
-        n_gemms = 27 * (p + 1) + p if form_ref.startswith("symmetric") else 20 * p + 19
+        n_gemms = 28 * (p + 1) + p if form_ref.startswith("symmetric") else 20 * p + 19
         vals = []
         for i in range(args.warmup + args.steps):
             cb = cpu_baseline(A_np, p, n_gemms, budget_s=4.0)
