@@ -157,3 +157,43 @@ def test_crt_product_full_size_sampled_rows():
         bound = 2.0 ** -b * (rmax[i] * colsum + (absA[i].sum() + n * rmax[i] * 2.0 ** -b) * rmax) \
             + 2.0 ** -51 * np.abs(ref) + n * 2.0 ** -53 * mag
         assert np.all(np.abs(Z_np[i] - ref) <= bound), (i, float(np.max(np.abs(Z_np[i] - ref) / bound)))
+
+
+@pytest.mark.parametrize("form,p,sched", [
+    ("symmetric_tri", 2, "bf16>fp64crt@23/cbf16>fp64crt/cbf16"),   # staged precision: 23 stored bits, then 52
+    ("symmetric_tri", 2, "tf32>fp64crt/ctf32"),                     # TF32 correction GEMM
+    ("symmetric", 3, "bf16>fp64crt/cbf16"),                          # p = 3 (full symmetric form)
+    ("symmetric_tri", 2, "fp8>bf16>fp64crt@a/cbf16"),               # the bench's headline schedule
+])
+def test_crt_schedules_level2(form, p, sched):
+    n = 520
+    A = synth.spd(n, 2.0, 12)
+    low = dict(plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
+    OPR = {"bf16": oracle.BF16, "tf32": oracle.TF32, "fp8": oracle.FP8, "fp64crt": oracle.FP64_OZ}
+    pg, po = [], []
+    parts = sched.split(">")
+    for i, part in enumerate(parts):
+        part, _, m = part.partition("@")
+        if "/c" in m:
+            m, _, corr = m.partition("/c")
+            part = part + "/c" + corr
+        prec, _, corr = part.partition("/c")
+        mb = (-2 if m == "a" else int(m)) if m else -1
+        kw = {} if i == len(parts) - 1 else low
+        pg.append(ipr.make_phase(prec, mant_bits=mb, corr_prec=corr or -1, **kw))
+        po.append(oracle.phase(OPR[prec], mant_bits=mb, corr_prec=OPR[corr] if corr else -1, **kw))
+    oform = oracle.FORM_SYMMETRIC if form == "symmetric" else oracle.FORM_SYMMETRIC_TRI
+    r = oracle.solve(A, p, po, 1e-12, 120, hist=120, form=oform)
+    out, tr, hist, best = run_gpu_trajectory(A, p, pg, 1e-12, 120, form=form)
+    assert out == ipr.IPR_CONVERGED and r.outcome == oracle.CONVERGED
+    assert abs(len(tr) - len(r.records)) <= 2
+    assert rel_fro(best, r.C_best) <= 1e-10
+    assert tr[-1]["rho_cert"] <= 1e-12
+    assert any(t["moduli"] > 0 for t in tr)
+    C = best
+    # defining property: C^p A = I on probe vectors
+    for v in synth.probe_vectors(n, 3, 2):
+        x = A @ v
+        for _ in range(p):
+            x = C @ x
+        assert np.linalg.norm(x - v) / np.linalg.norm(v) < 1e-11
