@@ -35,7 +35,10 @@ constexpr int TC_A_BYTES = TC_BM * TC_BKB;          // 16 KB
 constexpr int TC_B_BYTES = (TC_BN / 2) * TC_BKB;    // 16 KB (this CTA's half of N)
 constexpr int TC_STAGE_BYTES = TC_A_BYTES + TC_B_BYTES;
 constexpr int TC_SMEM = TC_ST * TC_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int TC_GROUP_M = 8;         // pair-rows per scheduling group
+#ifndef IPR_TC_GROUP_M
+#define IPR_TC_GROUP_M 8
+#endif
+constexpr int TC_GROUP_M = IPR_TC_GROUP_M;   // pair-rows per scheduling group
 
 bool tc_supported(int prec) {
   return prec == P_BF16 || prec == P_FP16 || prec == P_TF32 || prec == P_FP8 || prec == P_INT8;
