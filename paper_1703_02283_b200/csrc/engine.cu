@@ -909,7 +909,9 @@ extern "C" {
 static ipr_status certify_best(ipr_ctx *c, double *rho);
 static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho);
 
-const char *ipr_version(void) { return "ipr 0.2.0 (sm_100a: tcgen05 BF16/FP16/TF32/FP8/INT8, DMMA FP64)"; }
+const char *ipr_version(void) {
+  return "ipr 0.3.0 (sm_100a: tcgen05 BF16/FP16/TF32/FP8/INT8, DMMA FP64, FP64 on INT8 tensor cores: Ozaki I / II-CRT)";
+}
 
 const char *ipr_last_error(const ipr_ctx *c) { return c ? c->err.c_str() : t_err.c_str(); }
 
