@@ -104,24 +104,31 @@ __device__ __forceinline__ double store_q(double x, int cont64, int m, int rtz) 
 __global__ void k_maxabs_qA(const double *A, int64_t lda, int64_t n, int cont64, int m, int rtz, float *pmax) {
   __shared__ float red[32];
   float mx = 0.f;
-  const int64_t total = n * n;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / n, j = t % n;
-    mx = fmaxf(mx, fabsf((float)store_q(A[i * lda + j], cont64, m, rtz)));
+  // rows over blocks, columns over threads (no 64-bit index division per element)
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const double *a = A + i * lda;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) mx = fmaxf(mx, fabsf((float)store_q(a[j], cont64, m, rtz)));
   }
   const float b = block_max<256>(mx, red);
   if (threadIdx.x == 0) pmax[blockIdx.x] = b;
 }
 
+template <int PREC>
 __global__ void k_stage_a(const double *A, int64_t lda, int64_t n, int64_t npad, int64_t col0, int64_t kp,
-                          int prec, int cont64, int m, int rtz, const int *sig, void *Aop) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+                          int cont64, int m, int rtz, const int *sig, void *Aop) {
+  // 4 consecutive k per thread (the operand format is a template parameter: no per-element switch)
+  const int64_t k0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   const int64_t jj = blockIdx.y;
-  if (k >= npad) return;
+  if (k0 >= npad) return;
   const int64_t j = col0 + jj;
-  double v = 0.0;
-  if (j < n && k < n) v = store_q(A[j * lda + k], cont64, m, rtz);
-  store_operand(Aop, jj * npad + k, prec, v, sig ? sig[0] : 0);
+  const int sg = sig ? sig[0] : 0;
+  #pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int64_t k = k0 + u;
+    double v = 0.0;
+    if (j < n && k < n) v = store_q(A[j * lda + k], cont64, m, rtz);
+    if (k < npad) store_operand(Aop, jj * npad + k, PREC, v, sg);
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -489,8 +496,13 @@ cudaError_t launch_maxabs_qA(const double *A, int64_t lda, int64_t n, int cont64
 }
 cudaError_t launch_stage_a(const double *A, int64_t lda, int64_t n, int64_t npad, int64_t col0, int64_t kp, int prec,
                            int cont64, int m, int rtz, const int *sig, void *Aop, cudaStream_t s) {
-  dim3 g(nblk(npad, 256), (unsigned)kp);
-  k_stage_a<<<g, 256, 0, s>>>(A, lda, n, npad, col0, kp, prec, cont64, m, rtz, sig, Aop);
+  dim3 g(nblk((npad + 3) / 4, 256), (unsigned)kp);
+  switch (prec) {
+#define STA(P) case P: k_stage_a<P><<<g, 256, 0, s>>>(A, lda, n, npad, col0, kp, cont64, m, rtz, sig, Aop); break;
+    STA(P_FP64) STA(P_TF32) STA(P_BF16) STA(P_FP16) STA(P_FP8) STA(P_INT8) STA(P_FP64_OZ) STA(P_FP64_CRT)
+#undef STA
+    default: return cudaErrorInvalidValue;
+  }
   LAUNCH_CHECK();
 }
 cudaError_t launch_c0(const double *A, int64_t lda, int64_t n, int64_t npad, int64_t col0, int64_t kp, double sv,
