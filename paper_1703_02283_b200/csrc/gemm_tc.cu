@@ -656,8 +656,14 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
   for (int half = 0; half < 2; ++half) {
     const int64_t colb = (int64_t)tn * TC_BN + 128 * half, c0 = colb + 4 * lane;
     double scol[4];
+    int csg[4];
+    bool cok = true;                              // |f_j| < 500: two scalings never leave the normal range
     #pragma unroll
-    for (int u = 0; u < 4; ++u) scol[u] = scalbn(1.0, -g.oz_csig[c0 + u]);   // exact powers of two
+    for (int u = 0; u < 4; ++u) {
+      csg[u] = g.oz_csig[c0 + u];
+      cok = cok && csg[u] > -500 && csg[u] < 500;
+      scol[u] = cok ? pow2(-csg[u]) : 1.0;
+    }
     #pragma unroll 1
     for (int slab = 0; slab < 4; ++slab) {
       #pragma unroll 1
@@ -698,7 +704,9 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
         for (int ii = 0; ii < 2; ++ii) {
           const int rl = 4 * w + i2 + ii;
           const int64_t row = r0 + slab * 32 + rl;
-          const double srow = scalbn(1.0, -g.oz_rsig[row]);
+          const int rsg = g.oz_rsig[row];
+          const bool fast = __all_sync(0xffffffffu, cok && rsg > -500 && rsg < 500);   // warp-uniform
+          const double srow = fast ? pow2(-rsg) : 1.0;
           double vv[4], wv[4];
           #pragma unroll
           for (int u = 0; u < 4; ++u) {
@@ -706,8 +714,15 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
             const double q = rint(__dmul_rn(__fma_rn(shu, p1, __dmul_rn(sou, p1)), iM));  // within 0.493 of an integer
             const double dh = __fma_rn(-q, MH, shu);                    // exact
             const double dlo = __fma_rn(-q, MLo, sou);
-            const double pb = __dmul_rn(__dadd_rn(dh, dlo), p1);        // (dh + dlo) 2^s1
-            vv[u] = __dmul_rn(__dmul_rn(pb, srow), scol[u]);            // 2^-(e_i + f_j) Pbar, exact scaling
+            vv[u] = __dmul_rn(__dadd_rn(dh, dlo), p1);                  // Pbar = (dh + dlo) 2^s1
+          }
+          // 2^-(e_i + f_j) Pbar: two exact scalings; one scalbn where the exponents are extreme
+          if (fast) {
+            #pragma unroll
+            for (int u = 0; u < 4; ++u) vv[u] = __dmul_rn(__dmul_rn(vv[u], srow), scol[u]);
+          } else {
+            #pragma unroll
+            for (int u = 0; u < 4; ++u) vv[u] = scalbn(vv[u], -(rsg + csg[u]));
           }
           if (mode & EPI_STORE_N) {
             double2 *dn = (double2 *)((double *)g.nout + row * g.ldn + c0);

@@ -309,7 +309,8 @@ __global__ void __launch_bounds__(256, 3) k_crt_split(const double *__restrict__
   // scaled row maximum in [2^(b-1), 2^b): |Xbar| <= 2^b <= 2^62
   const int e = (mx > 0.0) ? b - 1 - ilogb(mx) : 0;
   if (threadIdx.x == 0) sig[r] = e;
-  const double sc = pow2(e);
+  // 2^e in two exact factors: |e| can exceed the FP64 exponent range for tiny / huge rows
+  const double sc1 = pow2(e / 2), sc2 = pow2(e - e / 2);
   const int64_t plane = rows * cols;
   const double *src = SMEM ? (const double *)srow : x;
   #pragma unroll 2
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(256, 3) k_crt_split(const double *__restrict__
     for (int u = 0; u < 4; ++u) {
       const double2 t = xp[u >> 1];
       // Xbar + 2^62 in [0, 2^63): eight unsigned bytes
-      const uint64_t y = (uint64_t)__double2ll_rn(__dmul_rn((u & 1) ? t.y : t.x, sc)) + (1ull << 62);
+      const uint64_t y = (uint64_t)__double2ll_rn(__dmul_rn(__dmul_rn((u & 1) ? t.y : t.x, sc1), sc2)) + (1ull << 62);
       lo[u] = (uint32_t)y; hi[u] = (uint32_t)(y >> 32);
     }
     crt_split4<0>(lo, hi, nm, planes + r * cols + k0, plane);

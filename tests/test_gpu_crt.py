@@ -197,3 +197,19 @@ def test_crt_schedules_level2(form, p, sched):
         for _ in range(p):
             x = C @ x
         assert np.linalg.norm(x - v) / np.linalg.norm(v) < 1e-11
+
+
+def test_crt_extreme_row_scales():
+    # rows / columns scaled by 2^+-900: the split's exponent e_i leaves the pow2 range (|e| > 1022) and
+    # the finish must unscale by 2^-(e_i + f_j) without under/overflow -- exact on integers times powers
+    # of two (the scaled product is representable)
+    n = 256
+    rng = np.random.default_rng(3)
+    X = rng.integers(-64, 65, (n, n)).astype(np.float64)
+    Y = rng.integers(-64, 65, (n, n)).astype(np.float64)
+    rs = np.where(np.arange(n) % 3 == 0, 2.0 ** -900, np.where(np.arange(n) % 3 == 1, 2.0 ** 900, 1.0))
+    cs = np.where(np.arange(n) % 2 == 0, 2.0 ** -60, 2.0 ** 60)
+    Xs, Ys = X * rs[:, None], Y * cs[None, :]
+    Z = _gemm(ipr.IPR_FP64_CRT, Xs, Ys, digits=3)
+    ref = (X @ Y) * rs[:, None] * cs[None, :]
+    np.testing.assert_array_equal(Z, ref)
