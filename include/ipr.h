@@ -14,7 +14,7 @@
  * PAPER.md:256-261, Sec. 4.3.1), ending with FP64 refinement.
  *
  * Readings of passages the paper leaves open (product order, update form, rounding,
- * controller rules, ...) are numbered R-1 ... R-21 in DESIGN.md and cited below.
+ * controller rules, forms, emulated FP64 ...) are numbered R-1 ... R-28 in DESIGN.md and cited below.
  *
  * General conventions
  *  - Every function returns ipr_status (IPR_OK == 0).  No function aborts the process and
