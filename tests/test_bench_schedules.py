@@ -1,0 +1,46 @@
+"""Host-side pins of bench.py's schedule handling (no GPU): the default schedule string parses into
+the documented phases, low phases of the symmetric forms leave at rho_hat <= 2u of their format
+(switch_tol = 2u sqrt(n), u = 2^-(m+1)), the literal form at rho_hat <= 1e-2, and the N > 1 fallback
+replaces the single-GPU INT8-emulated FP64 phases by the DMMA FP64 phase."""
+import math
+
+import pytest
+
+bench = pytest.importorskip("bench")
+ipr = pytest.importorskip("paper_1703_02283_b200")
+
+
+def test_default_schedule_phases():
+    form, ph = bench.schedule(bench.DEFAULT_SCHEDULE, 8192)
+    assert form == "symmetric_tri"
+    assert [ipr.PREC_NAMES[p.prec] for p in ph] == ["fp8", "bf16", "fp64crt"]
+    assert ph[-1].mant_bits == ipr.IPR_MANT_ADAPTIVE and ph[-1].corr_prec == ipr.IPR_BF16
+    for p, m in zip(ph[:-1], (3, 7)):
+        assert p.switch_tol == pytest.approx(2.0 * 2.0 ** -(m + 1) * math.sqrt(8192))
+        assert p.plateau_ratio == 0.7 and p.plateau_arm == 0.5 and p.max_iters == 40
+    assert ph[-1].switch_tol == 0.0 and ph[-1].max_iters == 0
+
+
+def test_literal_low_phase_switch():
+    form, ph = bench.schedule("bf16>fp64", 1024)
+    assert form == "literal"
+    assert ph[0].switch_tol == pytest.approx(1e-2 * math.sqrt(1024))
+
+
+def test_parse_schedule_fields():
+    form, parts = bench.parse_schedule("sym:bf16>fp64oz@23/cbf16>fp64crt@a/ctf32")
+    assert form == "symmetric"
+    assert parts == [("bf16", -1, -1), ("fp64oz", "bf16", 23), ("fp64crt", "tf32", -2)]
+
+
+def test_multi_gpu_fallback_replaces_emulated_phases():
+    form, ph = bench.schedule(bench.DEFAULT_SCHEDULE, 8192)
+    for p in ph:       # the transformation bench.main applies for world > 1
+        if p.prec in (ipr.IPR_FP64_OZ, ipr.IPR_FP64_CRT):
+            p.prec = ipr.IPR_FP64
+            if p.mant_bits == ipr.IPR_MANT_ADAPTIVE:
+                p.mant_bits = -1
+    assert [ipr.PREC_NAMES[p.prec] for p in ph] == ["fp8", "bf16", "fp64"]
+    assert ph[-1].mant_bits == -1
+    src = open(bench.__file__).read()
+    assert "ph.prec in (ipr.IPR_FP64_OZ, ipr.IPR_FP64_CRT)" in src    # the same rule lives in main()
