@@ -124,14 +124,17 @@ namespace ipr {
 // =========================================================================================
 // Ozaki scheme II (reading R-28): FP64 products by the Chinese remainder theorem on INT8 moduli.
 //
-//   quantise  Xbar_ik = rint(2^e_i x_ik), e_i = b - 1 - floor(log2 max_k |x_ik|)  (|Xbar| <= 2^b,
-//             an FP64 integer for any b: x 2^e is exact, rint of a double is a double); the same per column of the right operand (exponent f_j)
+//   quantise  Xbar_ik = rint(2^e_i x_ik), e_i = b - 1 - floor(log2 max_k |x_ik|)  (|Xbar| <= 2^b, an
+//             FP64 integer for any b: x 2^e is exact, rint of a double is a double; b <= 62, so it is
+//             also an int64); the same per column of the right operand (exponent f_j)
 //   products  for l = 1..N: U_l = (Xbar mod m_l)(Ybar mod m_l), symmetric residues in [-128, 127],
 //             ONE kind::i8 GEMM each, exact in INT32 (|U_l| <= 2^14 n < 2^31 for n < 131072)
 //   CRT       Pbar = Xbar Ybar is the unique integer with |Pbar| < M_N / 2 and Pbar = U_l mod m_l:
 //             Pbar = sum_l v_l W_l - q M_N, v_l = (U_l inv_l) mod m_l, W_l = M_N / m_l (exact sliced
-//             FP64 arithmetic, common.cuh CrtTab); M_N > 2^1.02 n 2^(2b) >= 2.03 max |Pbar| puts X / M_N
-//             within 0.493 of an integer, so q = rint(X / M_N) is exact (X / M_N is evaluated to ~2^-45)
+//             FP64 arithmetic in k_crt_finish: an exact 39-bit slice and a rounded low slice, common.cuh
+//             CrtTab); M_N > 2^1.02 n 2^(2b) >= 2.03 max |Pbar| puts X / M_N within 0.493 of an integer,
+//             so q = rint(X / M_N) is exact (X / M_N is evaluated to ~2^-45)
+//   bits      b = 7 S - 4 for the phase's Ozaki-equivalent digits S (crt_bits); N = crt_moduli(b, n)
 //   scale     Z_ij = 2^-(e_i + f_j) Pbar_ij (exact)
 // Error: only the quantisation, |Xbar_ik - 2^e_i x_ik| <= 1/2, i.e. 2^-b relative to the row maximum.
 // =========================================================================================
