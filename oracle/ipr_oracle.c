@@ -285,6 +285,7 @@ typedef struct {
   int64_t n;
   double *Chat, *X, *T;
   int sigC, sigX;
+  int sigR;                   /* symmetric form: sigma of Rhat when the correction format is scaled */
 } chain_ws;
 
 static double chain(int64_t n, int p, const double *A, const double *C, const orc_phase *ph,
@@ -387,7 +388,9 @@ static double update_ns(int64_t n, const double *X, const orc_phase *ph, chain_w
  * where qc is the operand format of the correction GEMM (corr_prec; = prec by default).
  * C_{k+1} is exactly symmetric whenever C_k is (W_ij + W_ji is commutative in IEEE).
  * Scaled formats (FP16/FP8/INT8) scale Chat, Ahat and qin(Z_j) by powers of two (reading R-20)
- * and unscale every product exactly; the correction format must be BF16, TF32 or FP64.
+ * and unscale every product exactly; the correction format is BF16, TF32 or FP64, or the phase's
+ * own scaled format (an FP8 phase with an FP8 correction, R-29): then Rhat = 2^sigR R and
+ * qc(C) = Chat carry their own sigmas and W is unscaled by 2^-(sigC + sigR), exactly.
  * ------------------------------------------------------------------------------ */
 static int is_scaled(int prec) { return prec == ORC_FP16 || prec == ORC_FP8 || prec == ORC_INT8; }
 /* default correction format: the phase's own, BF16 for the scaled formats */
@@ -420,15 +423,17 @@ static double chain_sym(int64_t n, int p, int tri, const double *A, const double
       s2 += d * d;
       w->T[r * n + c] = d;
     }
-  qin_matrix(corr_of(ph), nn, w->T, w->X);                  /* w->X = Rhat            */
+  w->sigR = qin_matrix(corr_of(ph), nn, w->T, w->X);        /* w->X = Rhat (2^sigR R)  */
   return sqrt(s2);
 }
 
 static double update_sym(int64_t n, int p, const double *C, const orc_phase *ph, chain_ws *w,
                          double *C_next) {
   const int64_t nn = n * n;
-  qin_matrix(corr_of(ph), nn, C, w->Chat);                  /* qc(C)                  */
+  const int sigCc = qin_matrix(corr_of(ph), nn, C, w->Chat); /* qc(C)                 */
   orc_gemm(n, w->Chat, w->X, w->T);                         /* W = qc(C) Rhat         */
+  if (sigCc + w->sigR != 0)   /* a scaled (FP8) correction: unscale exactly, as the chain does */
+    for (int64_t i = 0; i < nn; ++i) w->T[i] = ldexp(w->T[i], -(sigCc + w->sigR));
   const double tp = (double)(2 * p);
   double s2 = 0.0;
   for (int64_t i = 0; i < n; ++i)
@@ -557,7 +562,7 @@ double orc_step_ns(int64_t n, const double *A, const double *X, const orc_phase 
 
 double orc_step_sym(int64_t n, int p, const double *A, const double *C, const orc_phase *ph,
                     double *C_next, double *delta) {
-  if (p < 2 || is_scaled(corr_of(ph))) return NAN;
+  if (p < 2 || (is_scaled(corr_of(ph)) && corr_of(ph) != ph->prec)) return NAN;
   chain_ws w;
   if (!ws_alloc(&w, n)) { ws_free(&w); return NAN; }
   const double rho = chain_sym(n, p, 0, A, C, ph, &w);
@@ -588,7 +593,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
   if (sym) {
     if (p < 2 || (form == ORC_FORM_SYMMETRIC_TRI && p != 2)) return -1;
     for (int i = 0; i < nphases; ++i)
-      if (is_scaled(corr_of(&phases[i]))) return -1;
+      if (is_scaled(corr_of(&phases[i])) && corr_of(&phases[i]) != phases[i].prec) return -1;
   }
   if (form < ORC_FORM_LITERAL || form > ORC_FORM_COUPLED) return -1;
   if (!orc_is_symmetric(n, A)) return -2;

@@ -535,11 +535,18 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
           g.mode |= EPI_STORE_N; g.nout = c->Zr; g.ldn = c->npad; c->zr_for = c->cur;
         }
       }
+      // R-29: a scaled correction (= prec) takes R = I - Z_p through the FP32 scratch + per-tile max
+      const bool rscr = j == c->p && is_scaled(P.corr);
       if (j == c->p) {
         g.mode |= EPI_DIAG_MINUS | EPI_RESID; g.diag = 1.0; g.tprec = P.corr;
         g.tri = c->form == IPR_FORM_SYMMETRIC_TRI;   // Z_2 = C A C: upper triangle + mirror
+        if (rscr) {
+          g.mode = (g.mode & ~EPI_STORE_T) | EPI_TSCRATCH; g.pmax = c->pmax;
+          // tri: tiles below the diagonal are not visited -- their partial maxima must not be stale
+          if (g.tri) CK(cudaMemsetAsync(c->pmax, 0, sizeof(float) * tiles_n_total(c, prec) * tm, c->st));
+        }
       }
-      g.tout = (scaled && j < c->p) ? (void *)c->tscr : c->T[j & 1];
+      g.tout = ((scaled && j < c->p) || rscr) ? (void *)c->tscr : c->T[j & 1];
       if (j == c->p && fused_sym_ok(c, P)) g.tout = qplane(c, c->cur, P.corr, 1);   // Rhat into [Chat | Rhat | Chat]
       g.ldt = c->npad;
       g.part = part;
@@ -562,6 +569,11 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
         }
       }
       CK(run_gemm(c, g));
+      if (rscr) {   // sigma_R -> dsig[3 + (p & 1)] (not the slot GEMM p read), Rhat -> T[p & 1]
+        CKS(gather_pmax(c, c->pmax, tn_loc * tm));
+        CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 3 + (j & 1), prec, c->st));
+        CK(launch_scale_op(c->tscr, c->kp * c->npad, c->dsig + 3 + (j & 1), prec, c->T[j & 1], c->st));
+      }
       if (scaled && j < c->p) {
         CKS(gather_pmax(c, c->pmax, tn_loc * tm));
         CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 3 + (j & 1), prec, c->st));
@@ -707,6 +719,7 @@ ipr_status update_sym(ipr_ctx *c) {
   GemmArgs g = base_args(c, P.corr, c->T[c->p & 1]);
   if (same_fmt(P.corr, P.prec)) chat_view(c, c->cur, P.prec, &g.A, &g.a_kp, &g.a_pstride);
   else { g.A = c->chatc[c->cur]; g.a_kp = c->kp; g.a_pstride = c->npad * c->kp; }
+  if (is_scaled(P.corr)) { g.sigA = c->dsig + 1 + c->cur; g.sigB = c->dsig + 3 + (c->p & 1); }   // R-29
   // W holds the exact accumulator values: FP64 for an FP64 (DMMA) correction, else FP32
   const int wb = P.corr == IPR_FP64 ? 8 : 4;
   g.mode = EPI_WSTORE;
@@ -1077,8 +1090,9 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
         return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: the symmetric-tri form is single-GPU (mirror writes cross panels)");
       c->wbytes = 4;
       for (auto &P : c->ph) {
-        if (is_scaled(P.corr))
-          return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: the symmetric form's correction must be BF16, TF32 or FP64");
+        if (is_scaled(P.corr) && P.corr != P.prec)
+          return fail(c, IPR_E_UNSUPPORTED,
+                      "ipr_iterate: the symmetric form's correction must be BF16, TF32, FP64 or the phase's own scaled format");
         if (P.corr != IPR_FP64 && !tc_supported(P.corr))
           return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: tcgen05 path for the correction precision is not built");
         need_c |= !same_fmt(P.corr, P.prec);

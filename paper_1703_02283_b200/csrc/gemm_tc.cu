@@ -364,11 +364,14 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
   //     diagonal stores every element twice -- K-major (coalesced across the warp's rows) and
   //     mirrored row-major with 16-byte vector stores (the generic path's per-element mirror stores
   //     were uncoalesced: 1.11 ms vs 0.76 ms for the full GEMM 1).  Same FP64 arithmetic and order.
-  if (g.tri && (mode & EPI_STORE_T) &&
-      (mode & ~(EPI_STORE_T | EPI_DIAG_MINUS | EPI_RESID)) == 0 && (g.tprec == P_BF16 || g.tprec == P_TF32) &&
-      row < g.col0 + col) {
+  //     Also R-29's FP32 scratch of a scaled R (TSCRATCH instead of STORE_T, + the tile maximum).
+  if (g.tri && row < g.col0 + col &&
+      (((mode & EPI_STORE_T) && (mode & ~(EPI_STORE_T | EPI_DIAG_MINUS | EPI_RESID)) == 0 &&
+        (g.tprec == P_BF16 || g.tprec == P_TF32)) ||
+       ((mode & EPI_TSCRATCH) && (mode & ~(EPI_TSCRATCH | EPI_DIAG_MINUS | EPI_RESID)) == 0))) {
+    const bool ts = (mode & EPI_TSCRATCH) != 0;
     const bool dm = (mode & EPI_DIAG_MINUS) != 0, rsd = (mode & EPI_RESID) != 0;
-    if (g.tprec == P_BF16) {
+    if (!ts && g.tprec == P_BF16) {
       __nv_bfloat16 *t = (__nv_bfloat16 *)g.tout;
       uint32_t pk[16];
       #pragma unroll
@@ -396,7 +399,8 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
         const double a = acc_to_f64<KIND>(r[j]);
         const double v = scale == 1.0 ? a : __dmul_rn(a, scale);
         const double w = dm ? __dsub_rn(0.0, v) : v;
-        f[j] = to_tf32((float)w);
+        f[j] = ts ? (float)w : to_tf32((float)w);
+        if (ts) ea.mx = fmaxf(ea.mx, fabsf(f[j]));
         t[(col + j) * g.ldt + row] = f[j];
         if (rsd && row < g.n && g.col0 + col + j < g.n) {
           const double d = __dsub_rn(0.0, v);
@@ -442,6 +446,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
       }
       if (mode & EPI_TSCRATCH) {
         ((float *)g.tout)[c * g.ldt + row] = (float)w;
+        if (mirror) ((float *)g.tout)[row * g.ldt + c] = (float)w;
         ea.mx = fmaxf(ea.mx, fabsf((float)w));
       }
       if (mode & EPI_RESID) {

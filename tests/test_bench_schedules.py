@@ -15,6 +15,7 @@ def test_default_schedule_phases():
     assert form == "symmetric_tri"
     assert [ipr.PREC_NAMES[p.prec] for p in ph] == ["fp8", "bf16", "fp64crt"]
     assert ph[-1].mant_bits == ipr.IPR_MANT_ADAPTIVE and ph[-1].corr_prec == ipr.IPR_BF16
+    assert ph[0].corr_prec == ipr.IPR_FP8 and ph[1].corr_prec == -1     # R-29: FP8 correction in the FP8 phase
     for p, m in zip(ph[:-1], (3, 7)):
         assert p.switch_tol == pytest.approx(2.0 * 2.0 ** -(m + 1) * math.sqrt(8192))
         assert p.plateau_ratio == 0.7 and p.plateau_arm == 0.5 and p.max_iters == 40
@@ -40,7 +41,11 @@ def test_multi_gpu_fallback_replaces_emulated_phases():
             p.prec = ipr.IPR_FP64
             if p.mant_bits == ipr.IPR_MANT_ADAPTIVE:
                 p.mant_bits = -1
+        if p.corr_prec == ipr.IPR_FP8:
+            p.corr_prec = ipr.IPR_BF16
     assert [ipr.PREC_NAMES[p.prec] for p in ph] == ["fp8", "bf16", "fp64"]
+    assert ph[0].corr_prec == ipr.IPR_BF16
     assert ph[-1].mant_bits == -1
     src = open(bench.__file__).read()
     assert "ph.prec in (ipr.IPR_FP64_OZ, ipr.IPR_FP64_CRT)" in src    # the same rule lives in main()
+    assert "if ph.corr_prec == ipr.IPR_FP8:" in src

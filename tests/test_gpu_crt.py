@@ -163,7 +163,8 @@ def test_crt_product_full_size_sampled_rows():
     ("symmetric_tri", 2, "bf16>fp64crt@23/cbf16>fp64crt/cbf16"),   # staged precision: 23 stored bits, then 52
     ("symmetric_tri", 2, "tf32>fp64crt/ctf32"),                     # TF32 correction GEMM
     ("symmetric", 3, "bf16>fp64crt/cbf16"),                          # p = 3 (full symmetric form)
-    ("symmetric_tri", 2, "fp8>bf16>fp64crt@a/cbf16"),               # the bench's headline schedule
+    ("symmetric_tri", 2, "fp8>bf16>fp64crt@a/cbf16"),               # BF16 correction in the FP8 phase
+    ("symmetric_tri", 2, "fp8/cfp8>bf16>fp64crt@a/cbf16"),          # the bench's headline schedule (R-29)
 ])
 def test_crt_schedules_level2(form, p, sched):
     n = 520

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 ipr = pytest.importorskip("paper_1703_02283_b200")
 
-OPR = {"fp64": oracle.FP64, "tf32": oracle.TF32, "bf16": oracle.BF16, "fp16": oracle.FP16}
+OPR = {"fp64": oracle.FP64, "tf32": oracle.TF32, "bf16": oracle.BF16, "fp16": oracle.FP16, "fp8": oracle.FP8}
 LOW = dict(switch_tol=0.0, plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
 
 
@@ -49,7 +49,10 @@ def run_sym(A, p, name, tol, iters, form="symmetric"):
                                          (2, "tf32>fp64/cbf16", "symmetric"), (3, "bf16>fp64/ctf32", "symmetric"),
                                          (2, "bf16/ctf32>fp64", "symmetric"), (2, "fp64", "symmetric_tri"),
                                          (2, "bf16>fp64/cbf16", "symmetric_tri"), (2, "tf32>fp64", "symmetric_tri"),
-                                         (2, "fp16>fp64/cbf16", "symmetric_tri"), (3, "fp16/ctf32>fp64", "symmetric")])
+                                         (2, "fp16>fp64/cbf16", "symmetric_tri"), (3, "fp16/ctf32>fp64", "symmetric"),
+                                         # R-29: scaled correction (FP32 scratch of R + sigma_R)
+                                         (2, "fp8/cfp8>fp64", "symmetric_tri"), (2, "fp8/cfp8>fp64", "symmetric"),
+                                         (3, "fp16/cfp16>fp64", "symmetric")])
 def test_diagonal_bit_exact(p, name, form):
     A = synth.diag_spd(200, 1e3, 9)
     r, (out, tr, hist, best) = run_sym(A, p, name, 1e-13, 120, form)
@@ -82,7 +85,8 @@ def test_fp64_twin_trajectory(n, p, form):
 @pytest.mark.parametrize("name,m,form", [("bf16>fp64/cbf16", 7, "symmetric"), ("tf32>fp64/cbf16", 10, "symmetric"),
                                          ("bf16>fp64", 7, "symmetric"), ("bf16>tf32>fp64/cbf16", 7, "symmetric"),
                                          ("bf16>fp64/cbf16", 7, "symmetric_tri"), ("fp16>fp64/cbf16", 10, "symmetric_tri"),
-                                         ("bf16>tf32>fp64/cbf16", 7, "symmetric_tri")])
+                                         ("bf16>tf32>fp64/cbf16", 7, "symmetric_tri"),
+                                         ("fp8/cfp8>bf16>fp64/cbf16", 4, "symmetric_tri")])   # R-29
 def test_mixed_level2(name, m, form):
     # Level 2: low-phase iterates within 4 * 2^-m of the oracle, the same switch
     # iteration (R-6: +-1 only at a tie), final C within 1e-10, certified rho <= 1e-12; and the

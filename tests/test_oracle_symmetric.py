@@ -157,8 +157,8 @@ def test_stable_at_kappa_10_where_literal_diverges():
 def test_rejects_p1_and_scaled_correction():
     with pytest.raises(ValueError):
         oracle.solve(np.eye(4), 1, [oracle.phase()], form=SYM)
-    with pytest.raises(ValueError):   # the correction format must be BF16 / TF32 / FP64
-        oracle.solve(np.eye(4), 2, [oracle.phase(oracle.FP16, corr_prec=oracle.FP16), oracle.phase()], form=SYM)
+    with pytest.raises(ValueError):   # BF16 / TF32 / FP64, or the phase's own scaled format (R-29)
+        oracle.solve(np.eye(4), 2, [oracle.phase(oracle.FP16, corr_prec=oracle.FP8), oracle.phase()], form=SYM)
     assert np.isnan(oracle.step_sym(np.eye(2), np.eye(2), 1, oracle.phase())[0])
     # scaled phases default to a BF16 correction and converge (FP16 -> FP64)
     A = synth.spd(64, 2.0, 0)
@@ -208,3 +208,41 @@ def test_adaptive_digits_rule_pins():
                      form=SYM)
     ms = [x["mant_bits"] for x in r.records if x["phase"] == 1]
     assert r.outcome == oracle.CONVERGED and ms == sorted(ms) and ms[0] < 52 and ms[-1] == 52
+
+
+@pytest.mark.parametrize("prec", [oracle.FP8, oracle.FP16, oracle.INT8])
+def test_scaled_correction_step_is_exact_newton_step(prec):
+    # R-29 pin: with A = s D_a, C = D_c / sqrt(s) diagonal and every intermediate (a c, c^2 a,
+    # R = 1 - c^2 a, c R) exact in E4M3 / FP16 / INT8 after power-of-two scaling, one symmetric
+    # step with a scaled correction (corr = prec) must equal the exact Newton step of Eq. (1)
+    # c' = c + c (1 - c^p a) / p for p = 2.  s = 2^20 makes sigma_C, sigma_A,
+    # sigma_Z and sigma_R all non-zero and different: dropping or mixing up any unscale fails.
+    s = 2.0 ** 20
+    a = np.array([1.0, 1.0, 4.0, 1.0]) * s
+    c = np.array([0.75, 1.0, 0.25, 0.5]) / np.sqrt(s)     # R = 0.4375, 0, 0.75, 0.75
+    if prec == oracle.INT8:                               # INT8: 7-bit fixed point relative to the max
+        c = np.array([0.75, 1.0, 0.5, 0.5]) / np.sqrt(s)  # R = 0.4375, 0, 0.75, 0.75 (a = 1, 1, 1, 1)
+        a = np.full(4, s)
+    A, C = np.diag(a), np.diag(c)
+    ph = oracle.phase(prec, mant_bits=23, corr_prec=prec)
+    rho, C1, _ = oracle.step_sym(A, C, 2, ph)
+    R = 1.0 - c * c * a
+    np.testing.assert_array_equal(C1, np.diag(c + c * R / 2.0))
+    assert rho == pytest.approx(np.sqrt(np.sum(R * R)), rel=1e-15)
+
+
+def test_fp8_correction_schedule_converges():
+    # R-29: FP8 phase with an FP8 correction, then BF16, then FP64 (the bench's low phases):
+    # converges to the same root; the FP8 phase's rate is slower than with a BF16 correction
+    # by at most a few iterations (|mu| + 2^-4 per step)
+    A = synth.spd(96, 2.0, 5)
+    low = dict(plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
+    ref = np.real(scipy.linalg.fractional_matrix_power(A, -0.5))
+    counts = {}
+    for corr in (oracle.FP8, oracle.BF16):
+        r = oracle.solve(A, 2, [oracle.phase(oracle.FP8, corr_prec=corr, **low), oracle.phase(oracle.BF16, **low),
+                                oracle.phase()], 1e-12, 150, form=oracle.FORM_SYMMETRIC_TRI)
+        assert r.outcome == oracle.CONVERGED
+        assert np.linalg.norm(r.C_best - ref) / np.linalg.norm(ref) < 1e-12
+        counts[corr] = sum(1 for x in r.records if x["phase"] == 0)
+    assert counts[oracle.FP8] <= counts[oracle.BF16] + 4, counts
