@@ -22,6 +22,8 @@ extern "C" {
  *   mode 4: FP32 in  -> FP16 out (uint16 bit patterns) of 2^sigma * x, RNE (R-20 scaling)
  *   mode 5: FP64 in  -> FP8 E4M3 out (uint8 bit patterns) of 2^sigma * x, one RNE rounding (NEXT-3)
  *   mode 6: FP64 in  -> INT8 out of sat_127(rint(2^sigma * x)) (fixed point, NEXT-3)
+ *   mode 7: as mode 0, through the symmetric update's branch-free normal-range path + its fallback
+ *   mode 8: as mode 1, likewise
  * m: stored mantissa bits (modes 0/1), round: ipr_round (modes 0/1).  len >= 0. */
 ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_t len, int m,
                              int round, int sigma, void *stream);

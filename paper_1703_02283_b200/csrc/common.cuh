@@ -144,7 +144,9 @@ __device__ __forceinline__ uint64_t round_mag64(uint64_t mag, int s, int rtz) {
   const uint64_t mask = ~((1ull << s) - 1ull);
   if (rtz) return mag & mask;
   const uint64_t half = (1ull << (s - 1)) - 1ull;
-  const uint64_t lsb = (mag >> s) & 1ull;
+  // parity of q = mag / 2^s (the oracle's integer multiple of the ulp); at s = 52 (m = 0) q is the
+  // implicit bit: 1 (odd) for normals, 0 for subnormals -- not the exponent's low bit
+  const uint64_t lsb = s >= 52 ? (uint64_t)((mag >> 52) != 0ull) : (mag >> s) & 1ull;
   return (mag + half + lsb) & mask;
 }
 
@@ -159,27 +161,60 @@ __device__ __forceinline__ double q_e11(double x, int m, int rtz) {
   return bits2d(r | sign);
 }
 
-// FP64 value -> m stored bits in an e8 (FP32) container, single rounding from FP64.
-__device__ __forceinline__ float q_e8(double x, int m, int rtz) {
+// FP64 value -> m stored bits in an e8 (FP32) container, single rounding from FP64.  q_e8d returns
+// the result as the (exactly equal) double: callers that continue in FP64 skip two F2F conversions
+// (XU pipe: the symmetric update was XU-bound).
+__device__ __forceinline__ double q_e8d(double x, int m, int rtz) {
   const uint64_t b = d2bits(x);
   const uint64_t sign = b & 0x8000000000000000ull, mag = b ^ sign;
-  if (mag >= 0x7ff0000000000000ull) return (float)x;     // Inf / NaN
+  if (mag >= 0x7ff0000000000000ull) return (double)(float)x;   // Inf / NaN (as the FP32 conversion)
   const uint64_t E128 = (uint64_t)(1023 + 128) << 52;    // 2^128: beyond e8
   const uint64_t E126 = (uint64_t)(1023 - 126) << 52;    // 2^-126: e8 normal minimum
   // max finite of e8 with m bits: (2 - 2^-m) 2^127
   const double maxf = bits2d(((uint64_t)(1023 + 127) << 52) | (((1ull << m) - 1ull) << (52 - m)));
-  if (mag >= E128) return rtz ? (float)copysign(maxf, x) : (float)copysign(__longlong_as_double(0x7ff0000000000000ll), x);
+  if (mag >= E128) return rtz ? copysign(maxf, x) : copysign(__longlong_as_double(0x7ff0000000000000ll), x);
   if (mag >= E126) {
     const uint64_t r = round_mag64(mag, 52 - m, rtz);
-    if (r >= E128) return (float)copysign(__longlong_as_double(0x7ff0000000000000ll), x);
-    return (float)bits2d(r | sign);                      // exact: <= m+1 significant bits
+    if (r >= E128) return copysign(__longlong_as_double(0x7ff0000000000000ll), x);
+    return bits2d(r | sign);                             // exact in FP32: <= m+1 significant bits
   }
   // e8 subnormal range: multiples of 2^(-126-m)
   const double up = bits2d((uint64_t)(1023 + 126 + m) << 52);
   const double dn = bits2d((uint64_t)(1023 - 126 - m) << 52);
   const double y = __dmul_rn(x, up);
   const double q = rtz ? trunc(y) : rint(y);
-  return (float)__dmul_rn(q, dn);
+  return __dmul_rn(q, dn);                               // a multiple of 2^-149 below 2^-126: exact in FP32
+}
+__device__ __forceinline__ float q_e8(double x, int m, int rtz) { return (float)q_e8d(x, m, rtz); }
+
+// Branch-free q_e8d / q_e11 for the common case (hot loops of the symmetric update): the caller
+// hoists the rounding constants (QRound) and keeps q only if `ok` (the value and its rounding stay
+// in the normal range of the container), else calls q_e8d / q_e11.  Same bits as those whenever ok.
+struct QRound {
+  uint64_t mask, half;
+  int sh, rtz;
+  __device__ __forceinline__ QRound(int m, int rtz_) : sh(52 - m), rtz(rtz_) {
+    mask = sh > 0 ? ~((1ull << sh) - 1ull) : ~0ull;
+    half = sh > 0 && !rtz_ ? (1ull << (sh - 1)) - 1ull : 0ull;
+  }
+  __device__ __forceinline__ uint64_t round(uint64_t mag) const {
+    const uint64_t lsb = (sh > 0 && !rtz) ? (sh >= 52 ? (uint64_t)((mag >> 52) != 0ull) : (mag >> sh) & 1ull) : 0ull;
+    return (mag + half + lsb) & mask;
+  }
+};
+__device__ __forceinline__ double q_e8d_fast(double x, const QRound &q, bool &ok) {
+  const uint64_t b = d2bits(x);
+  const uint64_t sign = b & 0x8000000000000000ull, mag = b ^ sign;
+  const uint64_t E128 = (uint64_t)(1023 + 128) << 52, E126 = (uint64_t)(1023 - 126) << 52;
+  const uint64_t r = q.round(mag);
+  ok = ok && (mag - E126 < E128 - E126) && r < E128;   // normal e8 input and result (0 goes slow)
+  return bits2d(r | sign);
+}
+__device__ __forceinline__ double q_e11_fast(double x, const QRound &q, bool &ok) {
+  const uint64_t b = d2bits(x);
+  const uint64_t sign = b & 0x8000000000000000ull, mag = b ^ sign;
+  ok = ok && mag < 0x7ff0000000000000ull;              // finite (q_e11 handles subnormals alike)
+  return bits2d(q.round(mag) | sign);
 }
 
 // FP32 -> TF32 grid (e8m10), round-to-nearest-even, Inf/NaN kept (operand conversion).

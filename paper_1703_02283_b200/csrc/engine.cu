@@ -1326,7 +1326,7 @@ ipr_status ipr_plan(int64_t n, int world, int rank, int prec, int64_t *out8) {
 ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_t len, int m, int round, int sigma,
                              void *stream) {
   ipr_ctx *c = nullptr;
-  if (mode < 0 || mode > 6 || len < 0 || (len > 0 && (!in_dev || !out_dev)))
+  if (mode < 0 || mode > 8 || len < 0 || (len > 0 && (!in_dev || !out_dev)))
     return fail(c, IPR_E_INVALID_ARG, "ipr_test_quantize: bad arguments");
   if ((mode == 0 && (m < 0 || m > 23)) || (mode == 1 && (m < 0 || m > 52)))
     return fail(c, IPR_E_INVALID_ARG, "ipr_test_quantize: bad m");

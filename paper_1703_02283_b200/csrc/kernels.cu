@@ -369,7 +369,7 @@ __global__ void k_transpose(const T *src, int64_t rows, int64_t cols, T *dst) {
 // GLOBAL tile index (col tile * npad/64 + row tile): the same reduction order for any G.
 // ---------------------------------------------------------------------------------------
 template <typename CT, typename WT>
-__global__ void __launch_bounds__(256) k_sym_update(const CT *__restrict__ cold, CT *__restrict__ cnew,
+__global__ void __launch_bounds__(256, 4) k_sym_update(const CT *__restrict__ cold, CT *__restrict__ cnew,
                                                     const WT *__restrict__ W, int64_t npad, int64_t kp, int64_t col0,
                                                     int p, int m, int rtz, int prec, void *chat_new, int corr,
                                                     void *chat_corr_new, double *part) {
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(256) k_sym_update(const CT *__restrict__ cold,
   {
     const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
     const int64_t gi = ib + tx;
-    const WT *src = W + (gi / kp) * slot + gi % kp;
+    const WT *src = kp == npad ? W + gi : W + (gi / kp) * slot + gi % kp;   // G = 1: no 64-bit division
     #pragma unroll
     for (int r = ty; r < 64; r += 4) t[r][tx] = src[(col0 + jb + r) * kp];
   }
@@ -391,6 +391,7 @@ __global__ void __launch_bounds__(256) k_sym_update(const CT *__restrict__ cold,
   const int c4 = (threadIdx.x & 15) * 4, ry = threadIdx.x >> 4;   // 16 x 16 threads
   const bool pow2p = (p & (p - 1)) == 0;
   const double tp = (double)(2 * p), itp = 1.0 / tp;
+  const QRound qr(m, rtz);
   const WT *wl = W + (col0 / kp) * slot;                  // this rank's slot
   double d2 = 0.0;
   #pragma unroll
@@ -412,12 +413,21 @@ __global__ void __launch_bounds__(256) k_sym_update(const CT *__restrict__ cold,
       const double2 a = *(const double2 *)((const double *)cold + ci), b = *(const double2 *)((const double *)cold + ci + 2);
       cv[0] = a.x; cv[1] = a.y; cv[2] = b.x; cv[3] = b.y;
     }
+    double xv[4];
+    bool ok = true;
     #pragma unroll
     for (int v = 0; v < 4; ++v) {
       const double sw = __dadd_rn(wv[v], (double)t[c4 + v][r]);
       const double e = pow2p ? __dmul_rn(sw, itp) : __ddiv_rn(sw, tp);   // d/(2p); exact recip. for 2^k
-      const double x = __dadd_rn(cv[v], e);
-      cn[v] = sizeof(CT) == 8 ? q_e11(x, m, rtz) : (double)q_e8(x, m, rtz);
+      xv[v] = __dadd_rn(cv[v], e);
+      cn[v] = sizeof(CT) == 8 ? q_e11_fast(xv[v], qr, ok) : q_e8d_fast(xv[v], qr, ok);
+    }
+    if (!ok) {                                    // zero / subnormal / overflow: the general quantiser
+      #pragma unroll
+      for (int v = 0; v < 4; ++v) cn[v] = sizeof(CT) == 8 ? q_e11(xv[v], m, rtz) : q_e8d(xv[v], m, rtz);
+    }
+    #pragma unroll
+    for (int v = 0; v < 4; ++v) {
       const double dd = __dsub_rn(cn[v], cv[v]);
       d2 = __fma_rn(dd, dd, d2);
     }
@@ -470,6 +480,22 @@ __global__ void k_test_quant(int mode, const void *in, void *out, int64_t len, i
     case 4: { __half h = __float2half_rn((float)__dmul_rn((double)((const float *)in)[t], pow2(sigma))); ((uint16_t *)out)[t] = *(uint16_t *)&h; } break;
     case 5: ((uint8_t *)out)[t] = to_e4m3(__dmul_rn(((const double *)in)[t], pow2(sigma))); break;   // FP8 E4M3
     case 6: ((int8_t *)out)[t] = to_int8(__dmul_rn(((const double *)in)[t], pow2(sigma))); break;    // INT8
+    case 7: {   // mode 0 through the symmetric update's branch-free path (QRound) + its fallback
+      const double x = ((const double *)in)[t];
+      const QRound q(m, rtz);
+      bool ok = true;
+      double r = q_e8d_fast(x, q, ok);
+      if (!ok) r = q_e8d(x, m, rtz);
+      ((float *)out)[t] = (float)r;
+    } break;
+    case 8: {   // mode 1 likewise
+      const double x = ((const double *)in)[t];
+      const QRound q(m, rtz);
+      bool ok = true;
+      double r = q_e11_fast(x, q, ok);
+      if (!ok) r = q_e11(x, m, rtz);
+      ((double *)out)[t] = r;
+    } break;
   }
 }
 

@@ -20,6 +20,9 @@ def _wide(count):
     x = np.exp2(e) * RNG.choice([-1.0, 1.0], size=count)
     x[:1000] = RNG.standard_normal(1000)
     x[1000:1010] = [0.0, -0.0, np.inf, -np.inf, np.nan, 1.0, -1.0, 2.0 ** -149, 2.0 ** -126, 3.4e38]
+    ties = [s * (1.0 + k * 2.0 ** -(m + 1)) * 2.0 ** e for m in range(24) for k in (1, 3)
+            for e, s in ((0, 1.0), (127, -1.0), (-126, 1.0))]     # RNE ties at every m, at the range ends
+    x[1010:1010 + len(ties)] = ties
     return x
 
 
@@ -29,22 +32,24 @@ def _eq_bits(a, b):
     return np.array_equal(a.view(np.uint64)[~both_nan], b.view(np.uint64)[~both_nan])
 
 
+@pytest.mark.parametrize("mode", [0, 7])    # 7: the update's branch-free path (QRound) + fallback
 @pytest.mark.parametrize("m", [0, 2, 7, 10, 16, 23])
 @pytest.mark.parametrize("rtz", [0, 1])
-def test_quant_e8_container(m, rtz):
+def test_quant_e8_container(m, rtz, mode):
     x = _wide(1 << 20)
     y = torch.empty(x.size, dtype=torch.float32, device="cuda")
-    ipr.ipr_test_quantize(0, torch_cuda(x), y, m=m, round=rtz)
+    ipr.ipr_test_quantize(mode, torch_cuda(x), y, m=m, round=rtz)
     assert _eq_bits(y.cpu().numpy().astype(np.float64), oracle.qm(x, 8, m, bool(rtz)))
 
 
+@pytest.mark.parametrize("mode", [1, 8])    # 8: the update's branch-free path (QRound) + fallback
 @pytest.mark.parametrize("m", [0, 7, 10, 23, 40, 52])
 @pytest.mark.parametrize("rtz", [0, 1])
-def test_quant_e11_container(m, rtz):
+def test_quant_e11_container(m, rtz, mode):
     x = np.concatenate([_wide(1 << 19), RNG.standard_normal(1 << 18) * 1e-310,
                         np.exp2(RNG.uniform(1000, 1024, 1 << 16))])
     y = torch.empty(x.size, dtype=torch.float64, device="cuda")
-    ipr.ipr_test_quantize(1, torch_cuda(x), y, m=m, round=rtz)
+    ipr.ipr_test_quantize(mode, torch_cuda(x), y, m=m, round=rtz)
     assert _eq_bits(y.cpu().numpy(), oracle.qm(x, 11, m, bool(rtz)))
 
 
