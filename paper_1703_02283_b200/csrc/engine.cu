@@ -292,13 +292,14 @@ ipr_status stage_a(ipr_ctx *c, const PhaseC &P, void *dst, int *sig_dst) {
 }
 
 // container cont(i) -> operand Chat(i) (+ FP16 sigma), then all-gather (a8 / a9)
-ipr_status make_operand(ipr_ctx *c, int i, const PhaseC &P) {
+// premax: the per-rank max |C| is already in pmax[rank] (k_sym_update's amax), one partial per rank
+ipr_status make_operand(ipr_ctx *c, int i, const PhaseC &P, bool premax = false) {
   const int64_t cnt = c->npad * c->kp;
   if (!is_f64(P.prec)) {
     const int *sig = nullptr;
     if (is_scaled(P.prec)) {
-      const int nparts = 256;
-      CK(launch_maxabs_cont(c->cont[i], P.cont64, cnt, c->pmax + c->rank * nparts, nparts, c->st));
+      const int nparts = premax ? 1 : 256;
+      if (!premax) CK(launch_maxabs_cont(c->cont[i], P.cont64, cnt, c->pmax + c->rank * nparts, nparts, c->st));
       CKS(gather_pmax(c, c->pmax, nparts));
       CK(launch_reduce_max(c->pmax, (int64_t)nparts * c->world, nullptr, c->dsig + 1 + i, P.prec, c->st));
       sig = c->dsig + 1 + i;
@@ -729,16 +730,19 @@ ipr_status update_sym(ipr_ctx *c) {
   CK(cudaEventRecord(c->ev[2], c->st));
   CK(run_gemm(c, g));
   CKS(gather_bytes(c, c->wbuf, (size_t)(c->npad * c->kp) * wb, "W"));
+  // scaled phases: the update also takes max |C_{k+1}| (this rank's slot of pmax) for the next sigma
+  unsigned *amax = is_scaled(P.prec) ? (unsigned *)(c->pmax + c->rank) : nullptr;
+  if (amax) CK(cudaMemsetAsync(amax, 0, sizeof(unsigned), c->st));
   CK(launch_sym_update(cont_ptr(c, c->cur, P), P.cont64, cont_ptr(c, nx, P), c->wbuf, wb == 8, c->npad,
                        c->kp, c->col0, c->p, P.adaptive ? c->oz_m_next : P.m, P.rtz, P.prec,
                        (is_f64(P.prec) || is_scaled(P.prec)) ? nullptr : chat_slot(c, nx, P.prec), P.corr,
-                       same_fmt(P.corr, P.prec) ? nullptr : chatc_slot(c, nx, P.corr), c->part, c->st));
+                       same_fmt(P.corr, P.prec) ? nullptr : chatc_slot(c, nx, P.corr), c->part, amax, c->st));
   CK(cudaEventRecord(c->ev[3], c->st));
   c->upd_timed = true;
   const int64_t t64 = c->npad / 64;
   CKS(gather_partials(c, c->part, (c->kp / 64) * t64));
   CK(launch_reduce_sum(c->part, t64 * t64, c->dscal + 1, c->st));
-  if (is_scaled(P.prec)) CKS(make_operand(c, nx, P));   // sigma from max|C_{k+1}|, then all-gather
+  if (is_scaled(P.prec)) CKS(make_operand(c, nx, P, true));   // sigma from the update's max|C_{k+1}|
   else CKS(gather_chat(c, nx, P.prec));
   if (P.prec == IPR_FP64_OZ) CKS(oz_split_chat(c, nx));
   if (c->crC_for == nx) c->crC_for = -1;

@@ -372,9 +372,10 @@ template <typename CT, typename WT>
 __global__ void __launch_bounds__(256, 4) k_sym_update(const CT *__restrict__ cold, CT *__restrict__ cnew,
                                                     const WT *__restrict__ W, int64_t npad, int64_t kp, int64_t col0,
                                                     int p, int m, int rtz, int prec, void *chat_new, int corr,
-                                                    void *chat_corr_new, double *part) {
+                                                    void *chat_corr_new, double *part, unsigned *amax) {
   __shared__ WT t[64][65];
   __shared__ double red[8];
+  __shared__ float redf[8];
   const int64_t jb = (int64_t)blockIdx.x * 64;             // local column tile
   const int64_t ib = (int64_t)blockIdx.y * 64;             // row tile
   const int64_t slot = npad * kp;
@@ -394,6 +395,7 @@ __global__ void __launch_bounds__(256, 4) k_sym_update(const CT *__restrict__ co
   const QRound qr(m, rtz);
   const WT *wl = W + (col0 / kp) * slot;                  // this rank's slot
   double d2 = 0.0;
+  float mx = 0.f;                                         // max |C_{k+1}| (amax: scaled next operand)
   #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int r = ry + 16 * u;
@@ -430,6 +432,7 @@ __global__ void __launch_bounds__(256, 4) k_sym_update(const CT *__restrict__ co
     for (int v = 0; v < 4; ++v) {
       const double dd = __dsub_rn(cn[v], cv[v]);
       d2 = __fma_rn(dd, dd, d2);
+      mx = fmaxf(mx, fabsf((float)cn[v]));                // as k_maxabs_cont: fmaxf drops NaN
     }
     if (sizeof(CT) == 4) {
       *(float4 *)((float *)cnew + ci) = make_float4((float)cn[0], (float)cn[1], (float)cn[2], (float)cn[3]);
@@ -455,6 +458,10 @@ __global__ void __launch_bounds__(256, 4) k_sym_update(const CT *__restrict__ co
   }
   const double b = block_sum_det<256>(d2, red);
   if (threadIdx.x == 0) part[((col0 + jb) / 64) * (npad / 64) + blockIdx.y] = b;
+  if (amax) {   // non-negative, never NaN: the uint order of the bits is the float order
+    const float bm = block_max<256>(mx, redf);
+    if (threadIdx.x == 0) atomicMax(amax, __float_as_uint(bm));
+  }
 }
 
 // measurement hook: operand filled with pseudo-random values on the format's grid (|v| < 1;
@@ -607,11 +614,11 @@ cudaError_t launch_transpose(const void *src, int64_t rows, int64_t cols, int es
 
 cudaError_t launch_sym_update(const void *cold, int cont64, void *cnew, const void *W, int w64, int64_t npad,
                               int64_t kp, int64_t col0, int p, int m, int rtz, int prec, void *chat_new, int corr,
-                              void *chat_corr_new, double *part, cudaStream_t s) {
+                              void *chat_corr_new, double *part, unsigned *amax, cudaStream_t s) {
   if (kp % 64 || npad % 64) return cudaErrorInvalidValue;
   dim3 g((unsigned)(kp / 64), (unsigned)(npad / 64)), b(256);
 #define SYMU(CT, WT) k_sym_update<CT, WT><<<g, b, 0, s>>>((const CT *)cold, (CT *)cnew, (const WT *)W, npad, kp, col0, \
-                                                          p, m, rtz, prec, chat_new, corr, chat_corr_new, part)
+                                                          p, m, rtz, prec, chat_new, corr, chat_corr_new, part, amax)
   if (cont64 && w64) SYMU(double, double);
   else if (cont64) SYMU(double, float);
   else if (w64) SYMU(float, double);
