@@ -393,23 +393,51 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
       for (int q = 0; q < 4; ++q) m[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
     } else {
       float *t = (float *)g.tout;
-      float f[32];
-      #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const double a = acc_to_f64<KIND>(r[j]);
-        const double v = scale == 1.0 ? a : __dmul_rn(a, scale);
-        const double w = dm ? __dsub_rn(0.0, v) : v;
-        f[j] = ts ? (float)w : to_tf32((float)w);
-        if (ts) ea.mx = fmaxf(ea.mx, fabsf(f[j]));
-        t[(col + j) * g.ldt + row] = f[j];
-        if (rsd && row < g.n && g.col0 + col + j < g.n) {
-          const double d = __dsub_rn(0.0, v);
-          ea.r2 = __fma_rn(2.0 * d, d, ea.r2);
-        }
-      }
       float4 *m = (float4 *)(t + row * g.ldt + col);
+      if (ts) {
+        // R-29 scratch: the stored float is one FP32 multiply by the power-of-two scale (the same
+        // float as (float)(acc * scale) in FP64, as in (b)); FP64 only for the residual, from the
+        // exact product -- the same values and order as below, fewer dependent FP64 operations
+        const float sf = (float)scale;
+        #pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float f[4];
+          #pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = 4 * q + u;
+            const float a = KIND == 3 ? (float)(int32_t)r[j] : __uint_as_float(r[j]);
+            const float fv = __fmul_rn(a, sf);
+            f[u] = dm ? __fsub_rn(0.0f, fv) : fv;      // 0 - v as in FP64: +0 for v = 0
+            ea.mx = fmaxf(ea.mx, fabsf(f[u]));
+            t[(col + j) * g.ldt + row] = f[u];
+            if (rsd && row < g.n && g.col0 + col + j < g.n) {
+              const double v = scale == 1.0 ? acc_to_f64<KIND>(r[j]) : __dmul_rn(acc_to_f64<KIND>(r[j]), scale);
+              ea.r2 = __fma_rn(-2.0 * v, -v, ea.r2);   // d = 0 - v: 2 d d with the same rounding
+            }
+          }
+          m[q] = make_float4(f[0], f[1], f[2], f[3]);
+        }
+        return;
+      }
       #pragma unroll
-      for (int q = 0; q < 8; ++q) m[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+      for (int q = 0; q < 8; ++q) {        // 4 at a time: the mirror float4 leaves as soon as it is complete
+        float f[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int j = 4 * q + u;
+          const double a = acc_to_f64<KIND>(r[j]);
+          const double v = scale == 1.0 ? a : __dmul_rn(a, scale);
+          const double w = dm ? __dsub_rn(0.0, v) : v;
+          f[u] = ts ? (float)w : to_tf32((float)w);
+          if (ts) ea.mx = fmaxf(ea.mx, fabsf(f[u]));
+          t[(col + j) * g.ldt + row] = f[u];
+          if (rsd && row < g.n && g.col0 + col + j < g.n) {
+            const double d = __dsub_rn(0.0, v);
+            ea.r2 = __fma_rn(2.0 * d, d, ea.r2);
+          }
+        }
+        m[q] = make_float4(f[0], f[1], f[2], f[3]);
+      }
     }
     return;
   }
