@@ -26,6 +26,7 @@ cudaError_t launch_copy_out(const double *src, int64_t npad, int64_t kp, int64_t
 cudaError_t launch_pad_copy(const void *src, int64_t n, int64_t npad, int esz, void *dst, cudaStream_t s);
 cudaError_t launch_unpad_f64(const double *src, int64_t n, int64_t npad, double *dst, cudaStream_t s);
 cudaError_t launch_transpose(const void *src, int64_t rows, int64_t cols, int esz, void *dst, cudaStream_t s);
+// amax (nullable): atomicMax of the bits of max |C_{k+1}| (as float) -- the caller zeroes it first
 cudaError_t launch_sym_update(const void *cold, int cont64, void *cnew, const void *W, int w64, int64_t npad,
                               int64_t kp, int64_t col0, int p, int m, int rtz, int prec, void *chat_new, int corr,
                               void *chat_corr_new, double *part, unsigned *amax, cudaStream_t s);
