@@ -20,7 +20,7 @@ def main():
     sched = a.schedule or bench.DEFAULT_SCHEDULE
     st = torch.cuda.current_stream()
     for n, kappa, seed in [(4096, 2.0, 0), (4096, 2.0, 1), (4096, 5.0, 2), (8192, 2.0, 6), (8192, 2.0, 7),
-                           (8192, 5.0, 8), (6144, 2.0, 9), (2560, 2.0, 10)]:
+                           (8192, 5.0, 8), (6144, 2.0, 9), (2560, 2.0, 10), (4096, 10.0, 11), (4096, 20.0, 12)]:
         A, _ = synth.spd_torch(n, kappa, seed, device="cuda")
         form, ph = bench.schedule(sched, n)
         ph[-1].max_iters = 60
