@@ -455,6 +455,49 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
     }
     return;
   }
+  // (d) the (c) modes with an FP32 / TF32 R on a segment that is not strictly above the diagonal
+  //     (the diagonal tiles of the tri GEMM): the generic path's arithmetic and order, but the mirror
+  //     row segment leaves as float4 stores where all four elements are strictly upper -- the
+  //     generic path's scalar mirror stores (32 rows per warp store) made a diagonal tile cost ~2
+  //     mainloops, and the CTA pairs that drew one set the tri kernel's makespan
+  if (g.tri && row >= g.col0 + col &&
+      (((mode & EPI_STORE_T) && (mode & ~(EPI_STORE_T | EPI_DIAG_MINUS | EPI_RESID)) == 0 && g.tprec == P_TF32) ||
+       ((mode & EPI_TSCRATCH) && (mode & ~(EPI_TSCRATCH | EPI_DIAG_MINUS | EPI_RESID)) == 0))) {
+    const int64_t gc0 = g.col0 + col;
+    if (row > gc0 + 31) return;                      // the whole segment comes from the mirror
+    const bool ts = (mode & EPI_TSCRATCH) != 0, dm = (mode & EPI_DIAG_MINUS) != 0, rsd = (mode & EPI_RESID) != 0;
+    float *t = (float *)g.tout;
+    float f[32];
+    #pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int64_t gc = gc0 + j;
+      f[j] = 0.f;
+      if (row > gc) continue;                        // lower triangle: from the mirror
+      const double a = acc_to_f64<KIND>(r[j]);
+      const double v = scale == 1.0 ? a : __dmul_rn(a, scale);
+      const double w = dm ? __dsub_rn((row == gc && row < g.n) ? g.diag : 0.0, v) : v;
+      f[j] = ts ? (float)w : to_tf32((float)w);
+      t[(col + j) * g.ldt + row] = f[j];             // K-major: coalesced across the warp's rows
+      if (ts) ea.mx = fmaxf(ea.mx, fabsf(f[j]));
+      if (rsd && row < g.n && gc < g.n) {
+        const double d = __dsub_rn(row == gc ? 1.0 : 0.0, v);
+        ea.r2 = __fma_rn(row != gc ? 2.0 * d : d, d, ea.r2);
+      }
+    }
+    float *mr = t + row * g.ldt + col;               // mirror (row, c), c > row
+    #pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t c4 = gc0 + 4 * q;
+      if (c4 > row) {
+        *(float4 *)(mr + 4 * q) = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+      } else if (c4 + 3 > row) {
+        #pragma unroll
+        for (int u = 1; u < 4; ++u)
+          if (c4 + u > row) mr[4 * q + u] = f[4 * q + u];
+      }
+    }
+    return;
+  }
   if (mode & (EPI_STORE_T | EPI_TSCRATCH | EPI_RESID | EPI_F64)) {
     #pragma unroll
     for (int j = 0; j < 32; ++j) {
