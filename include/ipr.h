@@ -118,8 +118,11 @@ typedef struct {
   int       max_iters;     /* per-phase cap on chains; 0 = unlimited                          */
   int       corr_prec;     /* IPR_FORM_SYMMETRIC only: ipr_prec of the correction GEMM        */
                            /* W = qc(C) qc(I - C^{p-1}AC); -1 = prec (BF16 for the scaled     */
-                           /* FP16/FP8/INT8 phases).  Must be BF16, TF32 or FP64; FP64     */
-                           /* only in FP64 phases.  A BF16/TF32 correction in an FP64 phase   */
+                           /* FP16/FP8/INT8 phases).  Must be BF16, TF32 or FP64 (FP64     */
+                           /* only in FP64 phases), or the phase's own scaled format (FP16 /  */
+                           /* FP8 / INT8 = prec: R-29, R and C scaled by powers of two, W     */
+                           /* unscaled exactly; else IPR_E_UNSUPPORTED at ipr_iterate).       */
+                           /* A BF16/TF32 correction in an FP64 phase                         */
                            /* is mixed-precision refinement: R is small, so W needs only      */
                            /* relative accuracy (R-22).  Ignored by other forms.    */
 } ipr_phase;
