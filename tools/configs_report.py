@@ -128,6 +128,8 @@ def main():
             # FP64 phase on INT8 tensor cores (CRT, R-28): ~154 GB of arena at n = 32768 (one Chat residue
             # set, scratch aliases), fits a B200
             runs.append((f"{sym}:bf16>fp64crt@a/cbf16", 1e-12))
+            if tag == "twin" and n < 32768:   # bench.py's default: FP8 phase with FP8 correction (R-29) first
+                runs.append((f"{sym}:fp8/cfp8>bf16>fp64crt@a/cbf16", 1e-12))
             if tag == "stated":
                 runs.append(("cpl:fp64", 1e-6))
             for sched, tol in runs:
