@@ -14,7 +14,7 @@
  * PAPER.md:256-261, Sec. 4.3.1), ending with FP64 refinement.
  *
  * Readings of passages the paper leaves open (product order, update form, rounding,
- * controller rules, forms, emulated FP64 ...) are numbered R-1 ... R-28 in DESIGN.md and cited below.
+ * controller rules, forms, emulated FP64, certificates ...) are numbered R-1 ... R-30 in DESIGN.md and cited below.
  *
  * General conventions
  *  - Every function returns ipr_status (IPR_OK == 0).  No function aborts the process and
@@ -187,9 +187,11 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
  * C_k stays exactly symmetric; at the fixed point the error multiplier is
  * mu_ij = 1 - (x_i g_ij + x_j g_ji)/(2p) (|mu| <= 0.03 at kappa = 2, < 1 up to kappa ~ 34 for
  * p = 2), so low-precision noise is damped in the FP64 phase instead of persisting.
- * The trace's rho is rho_s; when it meets final_tol in the last phase the engine computes
- * C_{k+1}, then certifies ||I - C_k^p A||_F with FP64 DMMA GEMMs: converged if that is <=
- * final_tol (record.rho_cert), else the iteration continues from C_{k+1}.
+ * The trace's rho is rho_s; when it meets final_tol in the last phase the engine certifies
+ * ||I - C_k^p A||_F (record.rho_cert, see ipr_set_cert; by default the literal chain C (C A) on the
+ * FP64 DMMA pipe -- exactly the computation of ipr_residual(certify = 1)): converged iff that is <=
+ * final_tol, and the certified C_k is the answer ipr_finalize returns; else the iteration continues
+ * from C_{k+1}.
  *
  * IPR_FORM_SYMMETRIC_TRI (p = 2, world = 1): as IPR_FORM_SYMMETRIC, but
  * Z_2 = C A C -- symmetric in exact arithmetic -- is computed on the upper triangle only (tiles
@@ -207,13 +209,29 @@ typedef enum { IPR_FORM_LITERAL = 0, IPR_FORM_NEWTON_SCHULZ = 1, IPR_FORM_SYMMET
                IPR_FORM_SYMMETRIC_TRI = 3, IPR_FORM_COUPLED = 4 } ipr_form;
 ipr_status ipr_set_form(ipr_ctx *c, int form);
 
+/* Convergence certificate of the symmetric and coupled forms, whose in-chain residual is not the
+ * north-star residual ||I - C^p A||_F (reading R-3; R-30).  Call before the first ipr_iterate.
+ *  IPR_CERT_FP64 (default): ||I - C_k^p A||_F of the candidate C_k by the literal chain T_1 = C A,
+ *    T_j = C T_{j-1} on the FP64 DMMA pipe (p GEMMs, deterministic), the same function that
+ *    ipr_residual(certify = 1) runs on the returned iterate -- so for a converged solve the two agree
+ *    bit for bit, and "converged" means that FP64 residual is <= final_tol.
+ *  IPR_CERT_PHASE: the same residual from the FP64-range phase's own product (IPR_FP64_CRT / _OZ: the
+ *    INT8-emulated GEMM, reusing Z_1 = A C of the chain: p - 1 products instead of p DMMA GEMMs).  An
+ *    ESTIMATE: it is more accurate than the DMMA evaluation (exact integer sums, 2^-b quantisation) but
+ *    a different rounding, so ipr_residual(certify = 1) may exceed final_tol for a solve it accepted
+ *    (measured: 9.72e-13 accepted, DMMA 1.004e-12, n = 4096, kappa = 5).  Diagnostics only.
+ * Errors: IPR_E_INVALID_ARG (unknown mode), IPR_E_STATE (after the first ipr_iterate). */
+typedef enum { IPR_CERT_FP64 = 0, IPR_CERT_PHASE = 1 } ipr_cert;
+ipr_status ipr_set_cert(ipr_ctx *c, int mode);
+
 /* Run at most max_iters (> 0) chains.  *iters_done = chains evaluated by this call,
  * *outcome = IPR_RUNNING if the budget ran out, else the terminal outcome.  Resumable. */
 ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *outcome);
 
 /* certify == 0: the in-chain residual of the latest evaluated iterate (reading R-4).
- * certify == 1: ||I - C_best^p A||_F recomputed with FP64 DMMA GEMMs from the best iterate
- * (the one ipr_finalize returns), reading R-3. */
+ * certify == 1: ||I - C_best^p A||_F recomputed with FP64 DMMA GEMMs (the literal chain, the last
+ * GEMM keeping only its residual partials) from the best iterate (the one ipr_finalize returns),
+ * reading R-3 -- the IPR_CERT_FP64 certificate, bit for bit. */
 ipr_status ipr_residual(ipr_ctx *c, int certify, double *rho);
 
 /* Copy up to cap trace records; *count = total records so far (may exceed cap). */

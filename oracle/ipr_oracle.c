@@ -661,6 +661,8 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
         r.delta = coupled_step(n, p, C, ph, &w, Mh, Nh, Cn, &rho_next);
         double *t = C; C = Cn; Cn = t;
         m_of_C = phase_m(ph);
+      } else {
+        memcpy(C_best, C, (size_t)nn * sizeof(double));   /* the certified iterate is the answer (R-30) */
       }
     } else if (d == ORC_CONVERGED && sym) {
       /* rho_s = ||I - C^{p-1} A C||_F is not the north-star residual: certify
@@ -674,6 +676,8 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
         r.decision = d;
         double *t = C; C = Cn; Cn = t;
         m_of_C = phase_m(&ph_k);
+      } else {
+        memcpy(C_best, C, (size_t)nn * sizeof(double));   /* the certified iterate is the answer (R-30) */
       }
     } else if (d == ORC_CONTINUE && coupled) {
       r.delta = coupled_step(n, p, C, ph, &w, Mh, Nh, Cn, &rho_next);

@@ -34,8 +34,10 @@ EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_
             "ipr_get_iterate", "ipr_get_norms", "ipr_finalize", "ipr_last_error",
             "ipr_nccl_unique_id", "ipr_version", "ipr_test_quantize", "ipr_test_gemm",
             "ipr_launch_count", "ipr_plan", "ipr_set_form", "ipr_bench_gemm", "ipr_bench_gemm_epi",
-            "ipr_test_set_digits", "ipr_test_crt_table"]
+            "ipr_test_set_digits", "ipr_test_crt_table", "ipr_set_cert"]
 IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ, IPR_FORM_SYMMETRIC, IPR_FORM_SYMMETRIC_TRI, IPR_FORM_COUPLED = 0, 1, 2, 3, 4
+IPR_CERT_FP64, IPR_CERT_PHASE = 0, 1
+CERT_BY_NAME = {"fp64": IPR_CERT_FP64, "dmma": IPR_CERT_FP64, "phase": IPR_CERT_PHASE}
 FORM_BY_NAME = {"literal": IPR_FORM_LITERAL, "newton_schulz": IPR_FORM_NEWTON_SCHULZ, "ns": IPR_FORM_NEWTON_SCHULZ,
                 "symmetric": IPR_FORM_SYMMETRIC, "sym": IPR_FORM_SYMMETRIC,
                 "symmetric_tri": IPR_FORM_SYMMETRIC_TRI, "symtri": IPR_FORM_SYMMETRIC_TRI,
@@ -85,6 +87,7 @@ def _load():
     L.ipr_launch_count.restype = C.c_int64
     L.ipr_plan.argtypes = [i64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)]
     L.ipr_set_form.argtypes = [vp, C.c_int]
+    L.ipr_set_cert.argtypes = [vp, C.c_int]
     L.ipr_bench_gemm.argtypes = [C.c_int, i64, C.c_int, C.c_int, vp, dp]
     L.ipr_bench_gemm_epi.argtypes = [C.c_int, i64, C.c_int, C.c_int, C.c_int, vp, dp]
     L.ipr_test_set_digits.argtypes = [C.c_int]
@@ -109,6 +112,25 @@ def _ptr(x) -> int:
     if isinstance(x, int):
         return x
     return x.data_ptr()
+
+
+def _check_matrix(x, n: int, what: str, ref=None):
+    """A boundary matrix must be an FP64 CUDA tensor, n x n, unit column stride (ipr.h: FP64,
+    row-major, device, leading dimension >= n) -- anything else would make the library read or
+    write the wrong bytes.  Raw integer pointers are passed through unchecked."""
+    if x is None or isinstance(x, int):
+        return
+    import torch
+    if x.dtype != torch.float64:
+        raise ValueError(f"{what}: dtype must be torch.float64 (got {x.dtype})")
+    if not x.is_cuda:
+        raise ValueError(f"{what}: must be a CUDA tensor (got device {x.device})")
+    if ref is not None and not isinstance(ref, int) and x.device != ref.device:
+        raise ValueError(f"{what}: on {x.device}, A is on {ref.device}")
+    if x.dim() != 2 or x.shape[0] < n or x.shape[1] < n:
+        raise ValueError(f"{what}: shape must be ({n}, {n}) (got {tuple(x.shape)})")
+    if x.stride(1) != 1 or x.stride(0) < n:
+        raise ValueError(f"{what}: needs stride(1) == 1 and stride(0) >= n (got {x.stride()})")
 
 
 def _stream(s) -> int:
@@ -143,6 +165,7 @@ def ipr_nccl_unique_id() -> bytes:
 
 def ipr_init(n: int, A, lda: int | None = None, stream=None, world: int = 1, rank: int = 0,
              nccl_unique_id: bytes | None = None, grid_rows: int = 1, grid_cols: int | None = None):
+    _check_matrix(A, n, "ipr_init: A")
     ctx = C.c_void_p()
     uid = C.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id is not None else None
     _check(_lib.ipr_init(C.byref(ctx), n, _ptr(A), lda if lda is not None else n, _stream(stream),
@@ -166,6 +189,11 @@ def ipr_set_schedule(ctx, p: int, phases, final_tol: float):
 def ipr_set_form(ctx, form):
     f = FORM_BY_NAME[form] if isinstance(form, str) else int(form)
     _check(_lib.ipr_set_form(ctx, f), ctx)
+
+
+def ipr_set_cert(ctx, mode):
+    m = CERT_BY_NAME[mode] if isinstance(mode, str) else int(mode)
+    _check(_lib.ipr_set_cert(ctx, m), ctx)
 
 
 def ipr_iterate(ctx, max_iters: int):
@@ -192,6 +220,8 @@ def ipr_get_trace(ctx):
 
 
 def ipr_get_iterate(ctx, which: int, C_out, ldc: int | None = None):
+    if C_out is not None and not isinstance(C_out, int):
+        _check_matrix(C_out, C_out.shape[0], "ipr_get_iterate: C_out")
     _check(_lib.ipr_get_iterate(ctx, which, _ptr(C_out), ldc if ldc is not None else C_out.shape[1]), ctx)
 
 
@@ -202,6 +232,12 @@ def ipr_get_norms(ctx):
 
 
 def ipr_finalize(ctx, C_out=None, ldc: int | None = None):
+    if C_out is not None and not isinstance(C_out, int):
+        try:
+            _check_matrix(C_out, C_out.shape[0], "ipr_finalize: C_out")
+        except ValueError:
+            _lib.ipr_finalize(ctx, None, 0)   # still free the context
+            raise
     st = _lib.ipr_finalize(ctx, _ptr(C_out), ldc if ldc is not None else (C_out.shape[1] if C_out is not None else 0))
     _check(st)
 
@@ -264,7 +300,8 @@ class Solver:
     """Owns one ipr_ctx.  A: FP64 CUDA tensor (n x n, symmetric), kept alive by the Solver."""
 
     def __init__(self, A, p: int, phases, final_tol: float = 1e-12, stream=None, world: int = 1,
-                 rank: int = 0, nccl_unique_id: bytes | None = None, form="literal"):
+                 rank: int = 0, nccl_unique_id: bytes | None = None, form="literal", cert="fp64"):
+        _check_matrix(A, A.shape[0], "Solver: A")
         self.A = A
         self.n = A.shape[0]
         self.ctx = ipr_init(self.n, A, A.stride(0), stream, world, rank, nccl_unique_id)
@@ -272,6 +309,7 @@ class Solver:
             ipr_set_schedule(self.ctx, p, [ph if isinstance(ph, ipr_phase) else make_phase(**ph)
                                            for ph in phases], final_tol)
             ipr_set_form(self.ctx, form)
+            ipr_set_cert(self.ctx, cert)
         except Exception:
             ipr_finalize(self.ctx)
             self.ctx = None
@@ -298,6 +336,7 @@ class Solver:
         import torch
         if out is None:
             out = torch.empty((self.n, self.n), dtype=torch.float64, device=self.A.device)
+        _check_matrix(out, self.n, "iterate_copy: out", self.A)
         ipr_get_iterate(self.ctx, which, out, out.stride(0))
         return out
 
@@ -305,6 +344,7 @@ class Solver:
         import torch
         if out is None:
             out = torch.empty((self.n, self.n), dtype=torch.float64, device=self.A.device)
+        _check_matrix(out, self.n, "finalize: out", self.A)
         ctx, self.ctx = self.ctx, None
         ipr_finalize(ctx, out, out.stride(0))
         return out
@@ -322,9 +362,9 @@ class Solver:
 
 
 def solve(A, p: int, phases, final_tol: float = 1e-12, max_iters: int = 1000, stream=None,
-          form="literal"):
+          form="literal", cert="fp64"):
     """Run a full solve; returns (C_best, outcome name, trace)."""
-    s = Solver(A, p, phases, final_tol, stream, form=form)
+    s = Solver(A, p, phases, final_tol, stream, form=form, cert=cert)
     s.iterate(max_iters)
     tr = s.trace()
     out = OUTCOME_NAMES[s.outcome]

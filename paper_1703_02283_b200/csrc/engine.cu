@@ -121,6 +121,7 @@ struct ipr_ctx {
   cudaEvent_t kev[16] = {};             // CRT: event pairs around the kind::i8 GEMM launches of a chain
   CrtTimer ktimer{kev, 8, 0};
   bool upd_timed = false;
+  int cert = IPR_CERT_FP64;             // convergence certificate of the symmetric / coupled forms (ipr_set_cert)
 };
 
 namespace {
@@ -528,11 +529,11 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
       g.mode = (scaled && j < c->p) ? EPI_TSCRATCH : EPI_STORE_T;
       if (scaled && j < c->p) { g.pmax = c->pmax; }
       if (j == 1) {
-        // FP64 last phase (G = 1): also keep Z_1 = A C row-major -- the B operand of C (C A), so
-        // certifying ||I - C^p A||_F costs p - 1 GEMMs instead of p
+        // IPR_CERT_PHASE, FP64 last phase (G = 1): also keep Z_1 = A C row-major -- the B operand of
+        // C (C A), so the phase-product estimate of ||I - C^p A||_F costs p - 1 GEMMs instead of p
         c->zr_for = -1;
         const bool full = P.adaptive ? c->oz_S_cur == OZ_S : P.m == 52;
-        if (c->Zr && is_f64(prec) && full && c->phase == (int)c->ph.size() - 1) {
+        if (c->Zr && c->cert == IPR_CERT_PHASE && is_f64(prec) && full && c->phase == (int)c->ph.size() - 1) {
           g.mode |= EPI_STORE_N; g.nout = c->Zr; g.ldn = c->npad; c->zr_for = c->cur;
         }
       }
@@ -924,6 +925,7 @@ ipr_status gather_f64(ipr_ctx *c, const double *local) {
 extern "C" {
 
 static ipr_status certify_best(ipr_ctx *c, double *rho);
+static ipr_status certify_iter(ipr_ctx *c, int i, double *rho);
 static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho);
 
 const char *ipr_version(void) {
@@ -1066,6 +1068,14 @@ ipr_status ipr_set_form(ipr_ctx *c, int form) {
   return IPR_OK;
 }
 
+ipr_status ipr_set_cert(ipr_ctx *c, int mode) {
+  if (!c) return fail(c, IPR_E_INVALID_ARG, "ipr_set_cert: null context");
+  if (c->started) return fail(c, IPR_E_STATE, "ipr_set_cert: iteration already started");
+  if (mode != IPR_CERT_FP64 && mode != IPR_CERT_PHASE) return fail(c, IPR_E_INVALID_ARG, "ipr_set_cert: unknown mode %d", mode);
+  c->cert = mode;
+  return IPR_OK;
+}
+
 ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *outcome) {
   if (!c || !iters_done || !outcome) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: null pointer");
   if (!c->scheduled) return fail(c, IPR_E_STATE, "ipr_iterate: call ipr_set_schedule first");
@@ -1128,10 +1138,11 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     c->trace.push_back(r);
     *iters_done += 1;
     if (d == IPR_DEC_CONVERGED && c->form == IPR_FORM_COUPLED) {
-      // rho = ||I - M_k||_F tracks ||I - X_k^p A||_F only up to drift: certify the best iterate
-      // in FP64 (R-3, R-27); if it misses, take the step and continue
+      // rho = ||I - M_k||_F tracks ||I - X_k^p A||_F only up to drift: certify X_k itself with the
+      // FP64 literal chain on DMMA (R-3, R-27; the computation ipr_residual(certify = 1) runs); if it
+      // misses, take the step and continue.  A certified X_k is the answer (best := X_k).
       double rc = NAN;
-      CKS(certify_best(c, &rc));
+      CKS(certify_iter(c, c->cur, &rc));
       c->trace.back().rho_cert = rc;
       if (!(rc <= c->final_tol)) {
         c->trace.back().decision = IPR_DEC_CONTINUE;
@@ -1139,25 +1150,30 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
         c->pending_delta = (int64_t)c->trace.size() - 1;
         continue;
       }
+      c->best_loc = c->cur; c->best_cont64 = is_f64(c->ph[c->phase].prec);
       c->done = true;
       c->outcome = d;
       break;
     }
     if (d == IPR_DEC_CONVERGED && is_sym(c)) {
-      // rho_s = ||I - C^{p-1}AC||_F met final_tol: compute C_{k+1} (the T buffers are consumed),
-      // then certify ||I - C_k^p A||_F in FP64 (R-3); continue from C_{k+1} if it misses.
+      // rho_s = ||I - C^{p-1}AC||_F met final_tol: certify ||I - C_k^p A||_F (R-3, R-30).
+      //  IPR_CERT_FP64 (default): the literal chain C (C A) on the FP64 DMMA pipe -- the same function
+      //    ipr_residual(certify = 1) runs, so a converged solve's re-check equals its certificate bit
+      //    for bit.  p = 2: the certification stores only T_1 (T[1]); R (T[p & 1] = T[0]) survives, so
+      //    the update runs only if the certification misses.
+      //  IPR_CERT_PHASE: the phase's own product from the Z_1 = A C its chain kept (an FP64-range
+      //    estimate: the CRT / Ozaki quantisation error is not bounded here -- see ipr.h).
+      // A certified C_k is the answer (best := C_k); on a miss the iteration continues from C_{k+1}.
       const int ck = c->cur;
-      const bool fast = c->zr_for == ck && c->best_loc == ck;
-      // p = 2 fast path: the certifying GEMM C (C A) needs only its residual partials (no T store),
-      // so R in T[p & 1] survives and the update runs only if the certification misses
-      const bool cert_first = fast && c->p == 2;
+      const bool phase_cert = c->cert == IPR_CERT_PHASE && c->zr_for == ck && c->best_loc == ck;
+      const bool cert_first = c->p == 2;
       if (!cert_first) {
         CKS(update_sym(c));
         c->pending_delta = (int64_t)c->trace.size() - 1;
       }
       double rc = NAN;
-      if (fast) CKS(certify_from_zr(c, ck, &rc));
-      else CKS(certify_best(c, &rc));
+      if (phase_cert) CKS(certify_from_zr(c, ck, &rc));
+      else CKS(certify_iter(c, ck, &rc));
       c->trace.back().rho_cert = rc;
       if (!(rc <= c->final_tol)) {
         c->trace.back().decision = IPR_DEC_CONTINUE;
@@ -1168,6 +1184,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
         if (c->world > 1) CKS(make_xt(c, c->cur, c->ph[c->phase]));
         continue;
       }
+      c->best_loc = ck; c->best_cont64 = is_f64(c->ph[c->phase].prec);
       c->done = true;
       c->outcome = d;
       break;
@@ -1267,16 +1284,17 @@ static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho) {
   return IPR_OK;
 }
 
-static ipr_status certify_best(ipr_ctx *c, double *rho) {
-  // reading R-3: ||I - C_best^p A||_F with FP64 DMMA GEMMs
-  CKS(copy_iterate(c, 1, nullptr, 0));              // full64 = best (FP64, panel-major)
+// ||I - C^p A||_F of the FP64 iterate in full64 (panel-major, every rank) with the literal chain on the
+// FP64 DMMA pipe: T_1 = C A, T_j = C T_{j-1}; the last GEMM keeps only its residual partials, so T[p & 1]
+// is not written for p = 2 (reading R-3).  Deterministic: the same iterate gives the same bits.
+static ipr_status certify_full64(ipr_ctx *c, double *rho) {
   PhaseC P64{IPR_FP64, 52, 0, 1, 0, 0, 0, 0};
   CKS(stage_a(c, P64, c->Acert, c->dsig + 0));
   const void *X = c->Acert;
   for (int j = 1; j <= c->p; ++j) {
     GemmArgs g = base_args(c, IPR_FP64, X);
     g.A = c->full64; g.a_kp = c->kp; g.a_pstride = c->npad * c->kp;
-    g.mode = EPI_STORE_T | (j == c->p ? EPI_RESID : 0);
+    g.mode = j == c->p ? EPI_RESID : EPI_STORE_T;
     g.tout = c->T[j & 1]; g.ldt = c->npad; g.part = c->part;
     CK(run_gemm(c, g));
     X = c->T[j & 1];
@@ -1288,6 +1306,20 @@ static ipr_status certify_best(ipr_ctx *c, double *rho) {
   CK(cudaStreamSynchronize(c->st));
   *rho = std::sqrt(c->hscal[2]);
   return IPR_OK;
+}
+
+// the iterate in buffer i (the candidate C_k), FP64, gathered into full64
+static ipr_status certify_iter(ipr_ctx *c, int i, double *rho) {
+  const PhaseC &P = c->ph[c->phase];
+  double *slot = c->full64 + (size_t)c->rank * c->npad * c->kp;
+  CK(launch_cont_to_f64(cont_ptr(c, i, P), P.cont64, c->npad * c->kp, slot, c->st));
+  CKS(gather_f64(c, slot));
+  return certify_full64(c, rho);
+}
+
+static ipr_status certify_best(ipr_ctx *c, double *rho) {
+  CKS(copy_iterate(c, 1, nullptr, 0));              // full64 = best (FP64, panel-major)
+  return certify_full64(c, rho);
 }
 
 ipr_status ipr_residual(ipr_ctx *c, int certify, double *rho) {
