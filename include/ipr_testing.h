@@ -69,6 +69,22 @@ ipr_status ipr_bench_gemm_epi(int prec, int64_t n, int warmup, int iters, int ep
  * every world size, so per-tile partials reduce in the same order for any G. */
 ipr_status ipr_plan(int64_t n, int world, int rank, int prec, int64_t *out8);
 
+/* Read an intermediate of the last iteration of a symmetric-form context (test hook for the
+ * full-size step parity of tests/test_gpu_fullsize.py: each stage of one step is checked on sampled
+ * elements the oracle computes one by one from the previous stage's values).  After ipr_iterate has
+ * evaluated C_k and computed C_{k+1} (outcome IPR_RUNNING), `what` selects:
+ *   IPR_PEEK_AHAT   (0) Ahat of the phase, K-major [npad][npad] (element (k, j) at k + j npad)
+ *   IPR_PEEK_CHAT   (1) Chat of C_k (the chain's operand), row-major [npad][npad]
+ *   IPR_PEEK_Z1     (2) qin(Z_1) of C_k (the B operand of GEMM 2), K-major
+ *   IPR_PEEK_RHAT   (3) Rhat = qc(I - Z_p) of C_k (the B operand of the W GEMM), K-major
+ *   IPR_PEEK_W      (4) W = qc(C_k) Rhat as stored (FP32 / FP64), row-major
+ *   IPR_PEEK_CHATC  (5) qc(C_k) (the correction GEMM's A operand; = Chat if the formats agree), row-major
+ * The values are converted to FP64 and unscaled by the operand's 2^-sigma (exact); dst: npad^2 doubles
+ * on the device, npad = *npad_out (zero padding beyond n).  G = 1, symmetric forms, non-Ozaki phases;
+ * else IPR_E_UNSUPPORTED. */
+enum { IPR_PEEK_AHAT = 0, IPR_PEEK_CHAT = 1, IPR_PEEK_Z1 = 2, IPR_PEEK_RHAT = 3, IPR_PEEK_W = 4, IPR_PEEK_CHATC = 5 };
+ipr_status ipr_test_peek(ipr_ctx *c, int what, double *dst_dev, int64_t *npad_out);
+
 /* Number of this process's kernel launches since load (all libipr kernels). */
 int64_t ipr_launch_count(void);
 

@@ -18,8 +18,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ipr_oracle.c")
 _LIB = os.path.join(_HERE, "libipr_oracle.so")
 
-FP64, TF32, BF16, FP16, FP8, INT8, FP64_OZ = 0, 1, 2, 3, 4, 5, 6
-MANT_ADAPTIVE = -2   # FP64_OZ phases: digits / stored bits chosen per iteration (reading R-26)
+FP64, TF32, BF16, FP16, FP8, INT8, FP64_OZ, FP64_CRT = 0, 1, 2, 3, 4, 5, 6, 7
+MANT_ADAPTIVE = -2   # FP64_OZ / FP64_CRT phases: digits / stored bits chosen per iteration (reading R-26)
 RNE, RTZ = 0, 1
 CONTINUE, CONVERGED, ITER_LIMIT, DIVERGED, NONFINITE, SWITCH = 0, 1, 2, 3, 4, 5
 OUTCOME_NAMES = {0: "running", 1: "converged", 2: "iter_limit", 3: "diverged", 4: "nonfinite",
@@ -94,6 +94,11 @@ def lib():
         L.orc_sigma.argtypes = [C.c_int, C.c_double]
         L.orc_oz_digits.argtypes = [C.c_double, C.c_int64]
         L.orc_oz_adaptive_m.argtypes = [C.c_int]
+        L.orc_digits_for_m.argtypes = [C.c_int]
+        L.orc_crt_bits.argtypes = [C.c_int, C.c_int64]
+        L.orc_gemm_crt.argtypes = [C.c_int64, C.c_int, _dp, _dp, _dp]
+        L.orc_gemm_crt_pairs.argtypes = [C.c_int64, C.c_int, _dp, _dp, C.c_int64, C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_int64), _dp]
         L.orc_q_int8.restype = C.c_double
         L.orc_q_int8.argtypes = [C.c_double]
         L.orc_ctrl_init.argtypes = [C.POINTER(Ctrl), C.c_int64, C.c_int, C.c_double]
@@ -157,6 +162,36 @@ def oz_digits(rho_hat_target: float, n: int) -> int:
 
 def oz_adaptive_m(S: int) -> int:
     return lib().orc_oz_adaptive_m(S)
+
+
+def digits_for_m(m: int) -> int:
+    """Digits S of a fixed-m FP64_OZ / FP64_CRT phase (reading R-23)."""
+    return lib().orc_digits_for_m(m)
+
+
+def crt_bits(S: int, n: int) -> int:
+    """Bits b of an FP64_CRT product with S Ozaki-equivalent digits at order n (reading R-28)."""
+    return lib().orc_crt_bits(S, n)
+
+
+def gemm_crt(X, Y, b: int) -> np.ndarray:
+    """Z = X (x)_b Y: rows of X / columns of Y quantised to b-bit integers relative to their maximum,
+    the integer product exact, one rounding (reading R-28; the definition the GPU's CRT GEMM emulates)."""
+    X, Y = _f64(X), _f64(Y)
+    Z = np.empty_like(X)
+    lib().orc_gemm_crt(X.shape[0], int(b), _p(X), _p(Y), _p(Z))
+    return Z
+
+
+def gemm_crt_pairs(X, Y, b: int, I, J) -> np.ndarray:
+    """Elements (I[q], J[q]) of gemm_crt(X, Y, b), exponents from the full rows / columns."""
+    X, Y = _f64(X), _f64(Y)
+    I = np.ascontiguousarray(I, dtype=np.int64)
+    J = np.ascontiguousarray(J, dtype=np.int64)
+    Z = np.empty(I.shape[0])
+    lib().orc_gemm_crt_pairs(X.shape[0], int(b), _p(X), _p(Y), I.shape[0],
+                             I.ctypes.data_as(C.POINTER(C.c_int64)), J.ctypes.data_as(C.POINTER(C.c_int64)), _p(Z))
+    return Z
 
 
 def q_int8(x: float) -> float:

@@ -61,7 +61,8 @@ void orc_prec_format(int prec, int *E, int *M) {
 }
 /* Reading R-8: container of a phase = its accumulate format: e8 (FP32) for the
  * BF16/FP16/TF32 phases, e11 (FP64) for FP64 phases. */
-int orc_container_E(int prec) { return (prec == ORC_FP64 || prec == ORC_FP64_OZ) ? 11 : 8; }
+static int is_f64p(int prec) { return prec == ORC_FP64 || prec == ORC_FP64_OZ || prec == ORC_FP64_CRT; }
+int orc_container_E(int prec) { return is_f64p(prec) ? 11 : 8; }
 int orc_native_m(int prec) { int E, M; orc_prec_format(prec, &E, &M); return M; }
 
 static int phase_m(const orc_phase *ph) {
@@ -87,7 +88,134 @@ int orc_oz_digits(double rho_hat_target, int64_t n) {
 }
 int orc_oz_adaptive_m(int S) { return 7 * S - 4 < 52 ? 7 * S - 4 : 52; }
 static int is_adaptive(const orc_phase *ph) {
-  return ph->prec == ORC_FP64_OZ && ph->mant_bits == ORC_MANT_ADAPTIVE;
+  return (ph->prec == ORC_FP64_OZ || ph->prec == ORC_FP64_CRT) && ph->mant_bits == ORC_MANT_ADAPTIVE;
+}
+int orc_digits_for_m(int m) {
+  int S = (m + 12 + 6) / 7;               /* ceil((m + 12) / 7) for m >= 0 */
+  return S < 2 ? 2 : S > 9 ? 9 : S;
+}
+
+/* ---------------------------------------------------------------------------------
+ * FP64-range products by the Chinese remainder theorem (Ozaki scheme II; reading R-28 --
+ * not in the paper; its "custom number of mantissa bits", PAPER.md:191-194 [Sec. 4.2], applied to
+ * the operands of an integer product).  What the GPU emulation computes is, by definition, the EXACT
+ * product of the b-bit integer quantisations of the operands' rows (left) and columns (right),
+ * rescaled and rounded once; the moduli, residues and CRT reconstruction are only the GPU's way of
+ * forming that integer product, so none of them appears here except the moduli's product, which caps b.
+ * ------------------------------------------------------------------------------ */
+static const int crt_moduli_def[18] = {256, 255, 253, 251, 247, 241, 239, 233, 229, 227, 223, 217,
+                                       211, 199, 197, 193, 191, 181};   /* DESIGN.md R-28 */
+int orc_crt_bits(int S, int64_t n) {
+  double log2M = 0.0;
+  for (int l = 0; l < 18; ++l) log2M += log2((double)crt_moduli_def[l]);
+  int b = 7 * S - 4 < 62 ? 7 * S - 4 : 62;
+  while (b > 2 && !(2.0 * b + log2((double)(n < 1 ? 1 : n)) + 1.02 < log2M)) --b;
+  return b;
+}
+
+/* exponent that puts max|x| into [2^(b-1), 2^b): b - 1 - floor(log2 max|x|) */
+static int crt_exp(double mx, int b) {
+  if (!(mx > 0.0)) return 0;
+  int ex;
+  frexp(mx, &ex);                          /* mx = f 2^ex, f in [0.5, 1): floor(log2 mx) = ex - 1 */
+  return b - 1 - (ex - 1);
+}
+
+/* unsigned 192-bit magnitude, little-endian 64-bit words */
+typedef struct { uint64_t w[3]; } u192;
+static void u192_add(u192 *a, unsigned __int128 v) {
+  unsigned __int128 s = (unsigned __int128)a->w[0] + (uint64_t)v;
+  a->w[0] = (uint64_t)s;
+  s = (unsigned __int128)a->w[1] + (uint64_t)(v >> 64) + (uint64_t)(s >> 64);
+  a->w[1] = (uint64_t)s;
+  a->w[2] += (uint64_t)(s >> 64);
+}
+static int u192_cmp(const u192 *a, const u192 *b) {
+  for (int i = 2; i >= 0; --i) if (a->w[i] != b->w[i]) return a->w[i] > b->w[i] ? 1 : -1;
+  return 0;
+}
+static u192 u192_sub(const u192 *a, const u192 *b) {   /* a - b, a >= b */
+  u192 r;
+  uint64_t br = 0;
+  for (int i = 0; i < 3; ++i) {
+    const uint64_t t = a->w[i] - b->w[i] - br;
+    br = (a->w[i] < b->w[i] || (a->w[i] == b->w[i] && br)) ? 1 : 0;
+    r.w[i] = t;
+  }
+  return r;
+}
+static int u192_bit(const u192 *a, int k) { return (int)((a->w[k >> 6] >> (k & 63)) & 1u); }
+/* RN(a 2^scale): round the integer a to 53 significant bits (ties to even), then scale by 2^scale
+ * (exact for the normal results these products have) */
+static double u192_to_double(const u192 *a, int scale) {
+  int top = -1;
+  for (int k = 191; k >= 0; --k) if (u192_bit(a, k)) { top = k; break; }
+  if (top < 0) return 0.0;
+  if (top < 53) return ldexp((double)a->w[0], scale);   /* exact: fewer than 54 bits */
+  const int sh = top - 52;                              /* keep bits [sh, top] */
+  uint64_t mant = 0;
+  for (int k = top; k >= sh; --k) mant = (mant << 1) | (uint64_t)u192_bit(a, k);
+  const int guard = u192_bit(a, sh - 1);
+  int sticky = 0;
+  for (int k = sh - 2; k >= 0 && !sticky; --k) sticky = u192_bit(a, k);
+  if (guard && (sticky || (mant & 1u))) mant += 1;      /* may carry to 2^53: still exact in FP64 */
+  return ldexp((double)mant, sh + scale);
+}
+
+/* the exact element (Xbar_i. Ybar_.j) 2^-(e+f), rounded once */
+static double crt_elem(int64_t n, const int64_t *xr, int64_t xs, const int64_t *yc, int64_t ys, int e, int f) {
+  u192 pos = {{0, 0, 0}}, neg = {{0, 0, 0}};
+  for (int64_t k = 0; k < n; ++k) {
+    const __int128 pr = (__int128)xr[k * xs] * (__int128)yc[k * ys];   /* |pr| <= 2^124 */
+    if (pr >= 0) u192_add(&pos, (unsigned __int128)pr);
+    else u192_add(&neg, (unsigned __int128)(-pr));
+  }
+  if (u192_cmp(&pos, &neg) >= 0) { const u192 d = u192_sub(&pos, &neg); return u192_to_double(&d, -(e + f)); }
+  const u192 d = u192_sub(&neg, &pos);
+  return -u192_to_double(&d, -(e + f));
+}
+
+void orc_gemm_crt_pairs(int64_t n, int b, const double *X, const double *Y, int64_t npairs, const int64_t *I,
+                        const int64_t *J, double *Z) {
+  #pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t q = 0; q < npairs; ++q) {
+    int64_t *xr = (int64_t *)malloc((size_t)n * sizeof(int64_t)), *yc = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    const int64_t i = I[q], j = J[q];
+    double mx = 0.0, my = 0.0;
+    for (int64_t k = 0; k < n; ++k) {
+      if (fabs(X[i * n + k]) > mx) mx = fabs(X[i * n + k]);
+      if (fabs(Y[k * n + j]) > my) my = fabs(Y[k * n + j]);
+    }
+    const int e = crt_exp(mx, b), f = crt_exp(my, b);
+    for (int64_t k = 0; k < n; ++k) {
+      xr[k] = (int64_t)nearbyint(ldexp(X[i * n + k], e));
+      yc[k] = (int64_t)nearbyint(ldexp(Y[k * n + j], f));
+    }
+    Z[q] = crt_elem(n, xr, 1, yc, 1, e, f);
+    free(xr); free(yc);
+  }
+}
+
+void orc_gemm_crt(int64_t n, int b, const double *X, const double *Y, double *Z) {
+  int64_t *Xb = (int64_t *)malloc((size_t)(n * n) * sizeof(int64_t));
+  int64_t *Yb = (int64_t *)malloc((size_t)(n * n) * sizeof(int64_t));
+  int *e = (int *)malloc((size_t)n * sizeof(int)), *f = (int *)malloc((size_t)n * sizeof(int));
+  for (int64_t i = 0; i < n; ++i) {                      /* rows of X */
+    double mx = 0.0;
+    for (int64_t k = 0; k < n; ++k) if (fabs(X[i * n + k]) > mx) mx = fabs(X[i * n + k]);
+    e[i] = crt_exp(mx, b);
+    for (int64_t k = 0; k < n; ++k) Xb[i * n + k] = (int64_t)nearbyint(ldexp(X[i * n + k], e[i]));
+  }
+  for (int64_t j = 0; j < n; ++j) {                      /* columns of Y */
+    double mx = 0.0;
+    for (int64_t k = 0; k < n; ++k) if (fabs(Y[k * n + j]) > mx) mx = fabs(Y[k * n + j]);
+    f[j] = crt_exp(mx, b);
+    for (int64_t k = 0; k < n; ++k) Yb[k * n + j] = (int64_t)nearbyint(ldexp(Y[k * n + j], f[j]));
+  }
+  #pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) Z[i * n + j] = crt_elem(n, Xb + i * n, 1, Yb + j, n, e[i], f[j]);
+  free(Xb); free(Yb); free(e); free(f);
 }
 static double clampq(double q) { return q < 1e-3 ? 1e-3 : q > 1.0 ? 1.0 : q; }
 /* stored value of a phase: q_m in the container (approximate storage) */
@@ -133,7 +261,7 @@ static double maxabs_of(int64_t len, const double *x) {
 static int qin_matrix(int prec, int64_t len, const double *x, double *y) {
   int E, M;
   orc_prec_format(prec, &E, &M);
-  if (prec == ORC_FP64 || prec == ORC_FP64_OZ) { if (y != x) memcpy(y, x, (size_t)len * sizeof(double)); return 0; }
+  if (is_f64p(prec)) { if (y != x) memcpy(y, x, (size_t)len * sizeof(double)); return 0; }
   const int sigma = orc_sigma(prec, maxabs_of(len, x));
   if (prec == ORC_INT8) {
     for (int64_t i = 0; i < len; ++i) y[i] = orc_q_int8(ldexp(x[i], sigma));
@@ -286,7 +414,14 @@ typedef struct {
   double *Chat, *X, *T;
   int sigC, sigX;
   int sigR;                   /* symmetric form: sigma of Rhat when the correction format is scaled */
+  int crt_b;                  /* FP64_CRT phase: bits b of this chain's products (0: exact FP64 GEMMs) */
 } chain_ws;
+
+/* a chain product of the symmetric forms: the FP64 GEMM, or the CRT product of an FP64_CRT phase */
+static void chain_gemm(const chain_ws *w, int64_t n, const double *X, const double *Y, double *Z) {
+  if (w->crt_b > 0) orc_gemm_crt(n, w->crt_b, X, Y, Z);
+  else orc_gemm(n, X, Y, Z);
+}
 
 static double chain(int64_t n, int p, const double *A, const double *C, const orc_phase *ph,
                     chain_ws *w) {
@@ -405,10 +540,10 @@ static double chain_sym(int64_t n, int p, int tri, const double *A, const double
   for (int64_t i = 0; i < nn; ++i) w->T[i] = store_q(ph, A[i]);
   const int sigA = qin_matrix(ph->prec, nn, w->T, w->X);    /* w->X = Ahat            */
   w->sigC = qin_matrix(ph->prec, nn, C, w->Chat);           /* w->Chat = Chat         */
-  orc_gemm(n, w->X, w->Chat, w->T);                         /* Z_1 = Ahat Chat        */
+  chain_gemm(w, n, w->X, w->Chat, w->T);                    /* Z_1 = Ahat Chat        */
   int sigX = sigA;                                           /* scaled formats: unscale */
   for (int j = 1; j <= p; ++j) {
-    if (j > 1) orc_gemm(n, w->Chat, w->X, w->T);            /* Z_j = Chat qin(Z_{j-1}) */
+    if (j > 1) chain_gemm(w, n, w->Chat, w->X, w->T);       /* Z_j = Chat qin(Z_{j-1}) */
     if (sigX + w->sigC != 0)
       for (int64_t i = 0; i < nn; ++i) w->T[i] = ldexp(w->T[i], -(sigX + w->sigC));
     if (j < p) sigX = qin_matrix(ph->prec, nn, w->T, w->X); /* qin(Z_j)               */
@@ -518,6 +653,7 @@ static int ws_alloc(chain_ws *w, int64_t n) {
   const size_t b = (size_t)(n * n) * sizeof(double);
   w->n = n;
   w->Chat = (double *)malloc(b); w->X = (double *)malloc(b); w->T = (double *)malloc(b);
+  w->crt_b = 0;
   return w->Chat && w->X && w->T;
 }
 static void ws_free(chain_ws *w) { free(w->Chat); free(w->X); free(w->T); }
@@ -565,6 +701,8 @@ double orc_step_sym(int64_t n, int p, const double *A, const double *C, const or
   if (p < 2 || (is_scaled(corr_of(ph)) && corr_of(ph) != ph->prec)) return NAN;
   chain_ws w;
   if (!ws_alloc(&w, n)) { ws_free(&w); return NAN; }
+  if (ph->prec == ORC_FP64_CRT)   /* a single step: the digits of the phase's fixed m (9 if adaptive) */
+    w.crt_b = orc_crt_bits(is_adaptive(ph) ? 9 : orc_digits_for_m(phase_m(ph)), n);
   const double rho = chain_sym(n, p, 0, A, C, ph, &w);
   if (C_next) { const double d = update_sym(n, p, C, ph, &w, C_next); if (delta) *delta = d; }
   ws_free(&w);
@@ -596,6 +734,8 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
       if (is_scaled(corr_of(&phases[i])) && corr_of(&phases[i]) != phases[i].prec) return -1;
   }
   if (form < ORC_FORM_LITERAL || form > ORC_FORM_COUPLED) return -1;
+  for (int i = 0; i < nphases; ++i)   /* FP64_CRT products are defined for the symmetric forms only */
+    if (phases[i].prec == ORC_FP64_CRT && !sym) return -1;
   if (!orc_is_symmetric(n, A)) return -2;
   const int64_t nn = n * n;
   double nrm[3];
@@ -627,11 +767,14 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
   for (int k = 0; k < max_total; ++k) {
     const orc_phase *ph = &phases[ctl.phase];
     orc_phase ph_k = *ph;             /* the phase with this iteration's storage bits */
+    int S_k = orc_digits_for_m(phase_m(ph));
     if (is_adaptive(ph)) {
       const double q = (isfinite(ph_r1) && isfinite(ph_r2) && ph_r2 > 0.0) ? clampq(ph_r1 / ph_r2) : 0.03;
-      const int S = k == 0 ? 9 : orc_oz_digits(last_rho_hat * q * q, n);
-      ph_k.mant_bits = orc_oz_adaptive_m(S);
+      S_k = k == 0 ? 9 : orc_oz_digits(last_rho_hat * q * q, n);
+      ph_k.mant_bits = orc_oz_adaptive_m(S_k);
     }
+    /* FP64_CRT: this chain's products at b = orc_crt_bits(S_k) (R-26 digits, R-28 bits) */
+    w.crt_b = ph->prec == ORC_FP64_CRT ? orc_crt_bits(S_k, n) : 0;
     if (C_hist && k < hist_cap) memcpy(C_hist + (int64_t)k * nn, C, (size_t)nn * sizeof(double));
     double rho;
     if (coupled) {

@@ -30,7 +30,13 @@ extern "C" {
 /* ORC_FP64_OZ (= 6): an FP64 phase whose GPU GEMMs are emulated on INT8 tensor cores (Ozaki scheme,
  * reading R-23).  The oracle computes it exactly like ORC_FP64: the emulation is an FP64-accurate
  * GEMM, so the two sides differ by FP64-level rounding only (Level 2 tolerance, not bit-exact). */
-enum { ORC_FP64 = 0, ORC_TF32 = 1, ORC_BF16 = 2, ORC_FP16 = 3, ORC_FP8 = 4, ORC_INT8 = 5, ORC_FP64_OZ = 6 };
+/* ORC_FP64_CRT (= 7): an FP64 phase whose GPU GEMMs run on INT8 tensor cores by the Chinese remainder
+ * theorem (Ozaki scheme II, reading R-28).  Unlike FP64_OZ its products are NOT FP64-accurate by design:
+ * each row of the left operand / column of the right one is quantised to b-bit integers relative to its
+ * maximum.  The oracle computes that definition exactly (orc_gemm_crt: exact integer product, one
+ * rounding), so the GPU's CRT phases have a true reference. */
+enum { ORC_FP64 = 0, ORC_TF32 = 1, ORC_BF16 = 2, ORC_FP16 = 3, ORC_FP8 = 4, ORC_INT8 = 5, ORC_FP64_OZ = 6,
+       ORC_FP64_CRT = 7 };
 enum { ORC_RNE = 0, ORC_RTZ = 1 };
 enum { ORC_CONTINUE = 0, ORC_CONVERGED = 1, ORC_ITER_LIMIT = 2, ORC_DIVERGED = 3,
        ORC_NONFINITE = 4, ORC_SWITCH = 5 };
@@ -159,6 +165,22 @@ int orc_sigma(int prec, double maxabs);
 enum { ORC_MANT_ADAPTIVE = -2 };
 int orc_oz_digits(double rho_hat_target, int64_t n);
 int orc_oz_adaptive_m(int S);
+/* Digits S of a fixed-m FP64_OZ / FP64_CRT phase: S = clamp(ceil((m + 12) / 7), 2, 9) (reading R-23). */
+int orc_digits_for_m(int m);
+/* Bits b of an FP64_CRT product with S Ozaki-equivalent digits at order n (reading R-28):
+ * b = min(7 S - 4, 62), lowered while 2 b + log2 n + 1.02 >= log2 of the product of the 18 moduli
+ * (the exact integer product must stay below M / 2^1.02 for its reconstruction to be unique). */
+int orc_crt_bits(int S, int64_t n);
+/* Z = X (x)_b Y (n x n row-major): the CRT product's definition (reading R-28).
+ *   Xbar_ik = rint(2^{e_i} x_ik), e_i = b - 1 - floor(log2 max_k |x_ik|)  (0 for a zero row)
+ *   Ybar_kj = rint(2^{f_j} y_kj), f_j = b - 1 - floor(log2 max_k |y_kj|)  (0 for a zero column)
+ *   Z_ij    = RN( 2^{-(e_i + f_j)} sum_k Xbar_ik Ybar_kj )   -- the integer sum exact, ONE rounding.
+ * rint = round half to even.  1 <= b <= 62. */
+void orc_gemm_crt(int64_t n, int b, const double *X, const double *Y, double *Z);
+/* Selected elements of the same product: Z[q] = (X (x)_b Y)[I[q]][J[q]], q < npairs (the exponents from
+ * the FULL row I[q] of X and column J[q] of Y) -- sampled outputs of full-size products. */
+void orc_gemm_crt_pairs(int64_t n, int b, const double *X, const double *Y, int64_t npairs, const int64_t *I,
+                        const int64_t *J, double *Z);
 double orc_q_int8(double x);
 
 #ifdef __cplusplus

@@ -34,7 +34,7 @@ EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_
             "ipr_get_iterate", "ipr_get_norms", "ipr_finalize", "ipr_last_error",
             "ipr_nccl_unique_id", "ipr_version", "ipr_test_quantize", "ipr_test_gemm",
             "ipr_launch_count", "ipr_plan", "ipr_set_form", "ipr_bench_gemm", "ipr_bench_gemm_epi",
-            "ipr_test_set_digits", "ipr_test_crt_table", "ipr_set_cert"]
+            "ipr_test_set_digits", "ipr_test_crt_table", "ipr_set_cert", "ipr_test_peek"]
 IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ, IPR_FORM_SYMMETRIC, IPR_FORM_SYMMETRIC_TRI, IPR_FORM_COUPLED = 0, 1, 2, 3, 4
 IPR_CERT_FP64, IPR_CERT_PHASE = 0, 1
 CERT_BY_NAME = {"fp64": IPR_CERT_FP64, "dmma": IPR_CERT_FP64, "phase": IPR_CERT_PHASE}
@@ -88,6 +88,7 @@ def _load():
     L.ipr_plan.argtypes = [i64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int64)]
     L.ipr_set_form.argtypes = [vp, C.c_int]
     L.ipr_set_cert.argtypes = [vp, C.c_int]
+    L.ipr_test_peek.argtypes = [vp, C.c_int, vp, C.POINTER(C.c_int64)]
     L.ipr_bench_gemm.argtypes = [C.c_int, i64, C.c_int, C.c_int, vp, dp]
     L.ipr_bench_gemm_epi.argtypes = [C.c_int, i64, C.c_int, C.c_int, C.c_int, vp, dp]
     L.ipr_test_set_digits.argtypes = [C.c_int]
@@ -281,6 +282,21 @@ def ipr_bench_gemm_epi(prec, n: int, warmup: int = 2, iters: int = 5, epi: int =
     ms = C.c_double(0)
     _check(_lib.ipr_bench_gemm_epi(pr, n, warmup, iters, epi, _stream(stream), C.byref(ms)))
     return ms.value
+
+
+IPR_PEEK_AHAT, IPR_PEEK_CHAT, IPR_PEEK_Z1, IPR_PEEK_RHAT, IPR_PEEK_W, IPR_PEEK_CHATC = 0, 1, 2, 3, 4, 5
+
+
+def ipr_test_peek(ctx, what: int, npad: int):
+    """An intermediate of the last step as an (npad, npad) FP64 CUDA tensor (raw buffer order; see
+    ipr_testing.h for which are K-major)."""
+    import torch
+    out = torch.empty((npad, npad), dtype=torch.float64, device="cuda")
+    got = C.c_int64(0)
+    _check(_lib.ipr_test_peek(ctx, what, _ptr(out), C.byref(got)), ctx)
+    if got.value != npad:
+        raise IprError(IPR_E_INVALID_ARG, f"ipr_test_peek: npad is {got.value}, not {npad}")
+    return out
 
 
 def ipr_launch_count() -> int:

@@ -1348,6 +1348,38 @@ ipr_status ipr_finalize(ipr_ctx *c, double *C_dev_out, int64_t ldc) {
 // ---- test hooks (include/ipr_testing.h) ----
 int64_t ipr_launch_count(void) { return g_launches; }
 
+ipr_status ipr_test_peek(ipr_ctx *c, int what, double *dst, int64_t *npad_out) {
+  if (!c || !dst || !npad_out || what < IPR_PEEK_AHAT || what > IPR_PEEK_CHATC)
+    return fail(c, IPR_E_INVALID_ARG, "ipr_test_peek: bad arguments");
+  if (!c->started || c->trace.empty()) return fail(c, IPR_E_STATE, "ipr_test_peek: no iteration yet");
+  const PhaseC &P = c->ph[c->phase];
+  if (!is_sym(c) || c->world != 1 || P.prec == IPR_FP64_OZ || fused_sym_ok(c, P))
+    return fail(c, IPR_E_UNSUPPORTED, "ipr_test_peek: symmetric forms, G = 1, non-Ozaki-I phases");
+  const int prev = 1 - c->cur;              // C_k: the update wrote C_{k+1} into buffer cur
+  const int64_t cnt = c->npad * c->npad;
+  const void *src = nullptr;
+  int prec = P.prec;
+  const int *sig = nullptr;
+  const bool sc = is_scaled(P.prec), scc = is_scaled(P.corr);
+  switch (what) {
+    case IPR_PEEK_AHAT: src = c->Aop; sig = sc ? c->dsig + 0 : nullptr; break;
+    case IPR_PEEK_CHAT: src = c->chat[prev]; sig = sc ? c->dsig + 1 + prev : nullptr; break;
+    case IPR_PEEK_Z1: src = c->T[1]; sig = sc ? c->dsig + 4 : nullptr; break;
+    case IPR_PEEK_RHAT: src = c->T[c->p & 1]; prec = P.corr; sig = scc ? c->dsig + 3 + (c->p & 1) : nullptr; break;
+    case IPR_PEEK_W: src = c->wbuf; prec = c->wbytes == 8 && P.corr == IPR_FP64 ? IPR_FP64 : -1; break;
+    case IPR_PEEK_CHATC:
+      if (same_fmt(P.corr, P.prec)) { src = c->chat[prev]; sig = sc ? c->dsig + 1 + prev : nullptr; }
+      else { src = c->chatc[prev]; prec = P.corr; }
+      break;
+  }
+  if (is_f64(prec)) prec = IPR_FP64;
+  if (c->p != 2 && what == IPR_PEEK_Z1) return fail(c, IPR_E_UNSUPPORTED, "ipr_test_peek: Z1 for p = 2 only");
+  CK(launch_peek(src, prec, sig, cnt, dst, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  *npad_out = c->npad;
+  return IPR_OK;
+}
+
 ipr_status ipr_plan(int64_t n, int world, int rank, int prec, int64_t *out8) {
   ipr_ctx *c = nullptr;
   if (n <= 0 || world < 1 || rank < 0 || rank >= world || prec < 0 || prec > IPR_INT8 || !out8)

@@ -571,6 +571,28 @@ cudaError_t launch_maxabs_cont(const void *cont, int cont64, int64_t count, floa
   k_maxabs_cont<<<nparts, 256, 0, s>>>(cont, cont64, count, pmax);
   LAUNCH_CHECK();
 }
+// test hook (ipr_test_peek): an operand-format buffer as FP64 values, unscaled by 2^-sigma (exact)
+__global__ void k_peek(const void *src, int prec, const int *sig, int64_t count, double *dst) {
+  const double us = sig ? pow2(-*sig) : 1.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    double v;
+    switch (prec) {
+      case P_BF16: v = (double)__bfloat162float(((const __nv_bfloat16 *)src)[i]); break;
+      case P_FP16: v = (double)__half2float(((const __half *)src)[i]); break;
+      case P_FP8: { __nv_fp8_e4m3 q; q.__x = ((const __nv_fp8_storage_t *)src)[i]; v = (double)(float)q; break; }
+      case P_INT8: v = (double)((const int8_t *)src)[i]; break;
+      case P_TF32: v = (double)((const float *)src)[i]; break;
+      case -1: v = (double)((const float *)src)[i]; break;   // an FP32 scratch / container
+      default: v = ((const double *)src)[i]; break;
+    }
+    dst[i] = v * us;
+  }
+}
+cudaError_t launch_peek(const void *src, int prec, const int *sig, int64_t count, double *dst, cudaStream_t s) {
+  k_peek<<<nblk(count, 256), 256, 0, s>>>(src, prec, sig, count, dst);
+  LAUNCH_CHECK();
+}
+
 cudaError_t launch_cont_to_f64(const void *cont, int cont64, int64_t count, double *dst, cudaStream_t s) {
   k_cont_to_f64<<<nblk(count, 256), 256, 0, s>>>(cont, cont64, count, dst);
   LAUNCH_CHECK();

@@ -6,9 +6,10 @@ sliced FP64 arithmetic.
 Kernel level: bit-exact on integer operands that the quantisation keeps (b = 17); at b = 59 the
 error against an extended-precision reference is within the bound of the method (quantisation
 2^-b relative to the row / column maximum, plus the final rounding), and comparable to the FP64
-DMMA product.  Trajectory level: the symmetric forms' FP64 phase on IPR_FP64_CRT within the Level-2
-FP64 tolerance of the oracle (which computes that phase in FP64: oracle.FP64_OZ, the same storage
-rule)."""
+DMMA product, and element-wise against the oracle's definition of the CRT product (oracle.gemm_crt:
+the b-bit quantisations' exact integer product, one rounding).  Trajectory level: the symmetric forms'
+FP64-range phase on IPR_FP64_CRT against the oracle's FP64_CRT phase (the same quantised products at
+the same per-chain bits, R-26 / R-28), at the Level-2 FP64 tolerance."""
 import numpy as np
 import pytest
 
@@ -65,6 +66,28 @@ def test_crt_error_within_method_bound(n, kappa, digits):
         assert e_cr <= 2.0 * e_dm, (e_cr, e_dm)
 
 
+@pytest.mark.parametrize("n,digits", [(1, 9), (37, 3), (256, 5), (300, 9), (513, 7), (1024, 9)])
+def test_crt_gemm_matches_oracle_definition(n, digits):
+    # R-28's definition computed exactly by the oracle (integer product exact, one rounding) vs the
+    # GPU's modular products + sliced FP64 reconstruction, element by element, on operands with rows /
+    # columns spanning 2^+-40 (so e_i, f_j differ per row / column) and both signs
+    rng = np.random.default_rng(1000 + n)
+    X = rng.standard_normal((n, n)) * 2.0 ** rng.integers(-40, 41, n)[:, None]
+    Y = rng.standard_normal((n, n)) * 2.0 ** rng.integers(-40, 41, n)[None, :]
+    if n > 2:
+        X[1] = 0.0                     # a zero row: e = 0, Z row exactly 0
+        Y[:, 2] = 0.0
+    b = ipr.ipr_test_crt_table(18, digits, n)["b_for"]
+    assert b == oracle.crt_bits(digits, n)
+    Zg = _gemm(ipr.IPR_FP64_CRT, X, Y, digits)
+    Zo = oracle.gemm_crt(X, Y, b)
+    ulp = np.spacing(np.abs(Zo))
+    d = np.abs(Zg - Zo)
+    assert np.all(d <= 2 * ulp), float(np.max(d / ulp))
+    exact_frac = float(np.mean(Zg == Zo))
+    assert exact_frac >= 0.9, exact_frac
+
+
 def test_crt_matches_digits_scheme():
     # schemes I and II compute the same FP64 product to within their (FP64-level) errors
     n = 640
@@ -81,7 +104,7 @@ def test_crt_fp64_phase_level2(form, sched):
     n, p = 520, 2
     A = synth.spd(n, 2.0, 12)
     low = dict(plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
-    OPR = {"bf16": oracle.BF16, "fp64crt": oracle.FP64_OZ}
+    OPR = {"bf16": oracle.BF16, "fp64crt": oracle.FP64_CRT}
     pg, po = [], []
     parts = sched.split(">")
     for i, part in enumerate(parts):
@@ -113,7 +136,7 @@ def test_crt_adaptive_level2_and_storage_rule():
     A = synth.spd(n, 2.0, 12)
     low = dict(plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
     pg = [ipr.make_phase("bf16", **low), ipr.make_phase("fp64crt", mant_bits=ipr.IPR_MANT_ADAPTIVE, corr_prec="bf16")]
-    po = [oracle.phase(oracle.BF16, **low), oracle.phase(oracle.FP64_OZ, mant_bits=oracle.MANT_ADAPTIVE,
+    po = [oracle.phase(oracle.BF16, **low), oracle.phase(oracle.FP64_CRT, mant_bits=oracle.MANT_ADAPTIVE,
                                                          corr_prec=oracle.BF16)]
     r = oracle.solve(A, p, po, 1e-12, 80, hist=80, form=oracle.FORM_SYMMETRIC_TRI)
     out, tr, hist, best = run_gpu_trajectory(A, p, pg, 1e-12, 80, form="symmetric_tri")
@@ -170,7 +193,7 @@ def test_crt_schedules_level2(form, p, sched):
     n = 520
     A = synth.spd(n, 2.0, 12)
     low = dict(plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
-    OPR = {"bf16": oracle.BF16, "tf32": oracle.TF32, "fp8": oracle.FP8, "fp64crt": oracle.FP64_OZ}
+    OPR = {"bf16": oracle.BF16, "tf32": oracle.TF32, "fp8": oracle.FP8, "fp64crt": oracle.FP64_CRT}
     pg, po = [], []
     parts = sched.split(">")
     for i, part in enumerate(parts):

@@ -194,14 +194,12 @@ def test_tri_variant_mirrors_upper_triangle():
 
 
 def test_adaptive_digits_rule_pins():
-    # R-26 storage rule written out: S = clamp(ceil((log2(30 sqrt n) - log2 t) / 7), 3, 9),
-    # m = min(52, 7 S - 4); the first chain uses S = 9; precision rises inside the phase and the
-    # solve still reaches the certified FP64 residual.
-    import math
-    for t, n in [(1e-4, 8192), (1e-16, 8192), (3e-3, 512), (1.0, 64)]:
-        S = min(9, max(3, math.ceil((math.log2(30 * math.sqrt(n)) - math.log2(t)) / 7)))
-        assert oracle.oz_digits(t, n) == S
-    assert [oracle.oz_adaptive_m(S) for S in (3, 5, 8, 9)] == [17, 31, 52, 52]
+    # R-26: the rule's accuracy property is pinned in tests/test_oracle_crt.py
+    # (test_adaptive_digit_rule_property: the product error at the chosen digits stays below t / 2);
+    # here its range and the in-phase behaviour: S saturates at 3 and 9, precision rises inside the
+    # phase and the solve still reaches the certified FP64 residual.
+    assert oracle.oz_digits(1.0, 64) == 3 and oracle.oz_digits(1e-30, 8192) == 9
+    assert oracle.oz_digits(float("nan"), 64) == 9 and oracle.oz_digits(0.0, 64) == 9
     A = synth.spd(96, 2.0, 4)
     low = oracle.phase(oracle.BF16, plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
     r = oracle.solve(A, 2, [low, oracle.phase(oracle.FP64_OZ, mant_bits=oracle.MANT_ADAPTIVE)], 1e-12, 80,
