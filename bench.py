@@ -269,26 +269,6 @@ def main():
     C_out = torch.empty_like(A)
     torch.cuda.synchronize()
     form, phases = schedule(args.schedule, n)
-    if world > 1:
-        # single-GPU pieces (include/ipr.h): the tri form's mirrored stores cross column panels, and the
-        # INT8-emulated FP64 phases (Ozaki I / II) take world = 1 -- N > 1 runs the full symmetric form
-        # with the FP64 phase on DMMA
-        notes = []
-        if form == "symmetric_tri":
-            form = "symmetric"
-            notes.append("symmetric_tri is single-GPU; N > 1 runs the full symmetric form")
-        for ph in phases:
-            if ph.prec in (ipr.IPR_FP64_OZ, ipr.IPR_FP64_CRT):
-                ph.prec = ipr.IPR_FP64
-                if ph.mant_bits == ipr.IPR_MANT_ADAPTIVE:
-                    ph.mant_bits = -1
-                notes.append("INT8-emulated FP64 phases are single-GPU; N > 1 runs the FP64 phase on DMMA")
-            if ph.corr_prec == ipr.IPR_FP8:
-                ph.corr_prec = ipr.IPR_BF16
-                notes.append("the FP8 correction (R-29) is measured at N = 1 only; N > 1 takes the BF16 correction")
-        if notes:
-            config["form_note"] = "; ".join(dict.fromkeys(notes))
-
     def solve(A_dev, out):
         s = ipr.Solver(A_dev, p, phases, 1e-12, stream, world, rank, uid, form=form)
         s.iterate(400)

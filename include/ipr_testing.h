@@ -85,6 +85,21 @@ ipr_status ipr_plan(int64_t n, int world, int rank, int prec, int64_t *out8);
 enum { IPR_PEEK_AHAT = 0, IPR_PEEK_CHAT = 1, IPR_PEEK_Z1 = 2, IPR_PEEK_RHAT = 3, IPR_PEEK_W = 4, IPR_PEEK_CHATC = 5 };
 ipr_status ipr_test_peek(ipr_ctx *c, int what, double *dst_dev, int64_t *npad_out);
 
+/* In-process rank groups (SURVEY 8(e) on a one-GPU box).  A local group stands for `world` ranks that
+ * live in ONE process on ONE device, each with its own context, CUDA stream and host thread: every
+ * all-gather / all-to-all of the engine becomes stream-ordered device-to-device copies between the
+ * ranks' buffers, fenced by CUDA events and host barriers (no kernel waits on another rank; the
+ * column-panel arithmetic, layouts and exchanges are exactly those of the NCCL path).  Used by the
+ * -m gpu tests to check that G = 2 / 4 ranks reproduce the G = 1 trajectory bit for bit (P11).
+ * ipr_test_init_local is ipr_init with the group in place of the NCCL id: call it once per rank, each
+ * from its own host thread (the exchanges block until every rank of the group arrives).  Destroy the
+ * group after every context of it is finalized. */
+typedef struct ipr_local_group ipr_local_group;
+ipr_status ipr_test_local_group_create(int world, ipr_local_group **out);
+ipr_status ipr_test_local_group_destroy(ipr_local_group *g);
+ipr_status ipr_test_init_local(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, void *cuda_stream,
+                               ipr_local_group *group, int rank, int grid_rows, int grid_cols);
+
 /* Number of this process's kernel launches since load (all libipr kernels). */
 int64_t ipr_launch_count(void);
 

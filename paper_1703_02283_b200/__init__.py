@@ -34,7 +34,8 @@ EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_
             "ipr_get_iterate", "ipr_get_norms", "ipr_finalize", "ipr_last_error",
             "ipr_nccl_unique_id", "ipr_version", "ipr_test_quantize", "ipr_test_gemm",
             "ipr_launch_count", "ipr_plan", "ipr_set_form", "ipr_bench_gemm", "ipr_bench_gemm_epi",
-            "ipr_test_set_digits", "ipr_test_crt_table", "ipr_set_cert", "ipr_test_peek"]
+            "ipr_test_set_digits", "ipr_test_crt_table", "ipr_set_cert", "ipr_test_peek",
+            "ipr_test_local_group_create", "ipr_test_local_group_destroy", "ipr_test_init_local"]
 IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ, IPR_FORM_SYMMETRIC, IPR_FORM_SYMMETRIC_TRI, IPR_FORM_COUPLED = 0, 1, 2, 3, 4
 IPR_CERT_FP64, IPR_CERT_PHASE = 0, 1
 CERT_BY_NAME = {"fp64": IPR_CERT_FP64, "dmma": IPR_CERT_FP64, "phase": IPR_CERT_PHASE}
@@ -89,6 +90,9 @@ def _load():
     L.ipr_set_form.argtypes = [vp, C.c_int]
     L.ipr_set_cert.argtypes = [vp, C.c_int]
     L.ipr_test_peek.argtypes = [vp, C.c_int, vp, C.POINTER(C.c_int64)]
+    L.ipr_test_local_group_create.argtypes = [C.c_int, C.POINTER(vp)]
+    L.ipr_test_local_group_destroy.argtypes = [vp]
+    L.ipr_test_init_local.argtypes = [C.POINTER(vp), i64, vp, i64, vp, vp, C.c_int, C.c_int, C.c_int]
     L.ipr_bench_gemm.argtypes = [C.c_int, i64, C.c_int, C.c_int, vp, dp]
     L.ipr_bench_gemm_epi.argtypes = [C.c_int, i64, C.c_int, C.c_int, C.c_int, vp, dp]
     L.ipr_test_set_digits.argtypes = [C.c_int]
@@ -171,6 +175,27 @@ def ipr_init(n: int, A, lda: int | None = None, stream=None, world: int = 1, ran
     uid = C.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id is not None else None
     _check(_lib.ipr_init(C.byref(ctx), n, _ptr(A), lda if lda is not None else n, _stream(stream),
                          world, rank, uid, grid_rows, grid_cols if grid_cols is not None else world))
+    return ctx
+
+
+def ipr_test_local_group_create(world: int):
+    """An in-process group of `world` ranks on the current device (ipr_testing.h)."""
+    g = C.c_void_p()
+    _check(_lib.ipr_test_local_group_create(world, C.byref(g)))
+    return g
+
+
+def ipr_test_local_group_destroy(group):
+    _check(_lib.ipr_test_local_group_destroy(group))
+
+
+def ipr_test_init_local(n: int, A, lda: int | None, stream, group, rank: int, grid_rows: int = 1,
+                        grid_cols: int | None = None, world: int | None = None):
+    """ipr_init for rank `rank` of a local group (call from the rank's own host thread)."""
+    _check_matrix(A, n, "ipr_test_init_local: A")
+    ctx = C.c_void_p()
+    _check(_lib.ipr_test_init_local(C.byref(ctx), n, _ptr(A), lda if lda is not None else n, _stream(stream),
+                                    group, rank, grid_rows, grid_cols if grid_cols is not None else world))
     return ctx
 
 
@@ -316,11 +341,16 @@ class Solver:
     """Owns one ipr_ctx.  A: FP64 CUDA tensor (n x n, symmetric), kept alive by the Solver."""
 
     def __init__(self, A, p: int, phases, final_tol: float = 1e-12, stream=None, world: int = 1,
-                 rank: int = 0, nccl_unique_id: bytes | None = None, form="literal", cert="fp64"):
+                 rank: int = 0, nccl_unique_id: bytes | None = None, form="literal", cert="fp64",
+                 local_group=None, grid=None):
         _check_matrix(A, A.shape[0], "Solver: A")
         self.A = A
         self.n = A.shape[0]
-        self.ctx = ipr_init(self.n, A, A.stride(0), stream, world, rank, nccl_unique_id)
+        gr, gc = grid if grid is not None else (1, world)
+        if local_group is not None:   # test transport: in-process ranks on one device (ipr_testing.h)
+            self.ctx = ipr_test_init_local(self.n, A, A.stride(0), stream, local_group, rank, gr, gc)
+        else:
+            self.ctx = ipr_init(self.n, A, A.stride(0), stream, world, rank, nccl_unique_id, gr, gc)
         try:
             ipr_set_schedule(self.ctx, p, [ph if isinstance(ph, ipr_phase) else make_phase(**ph)
                                            for ph in phases], final_tol)

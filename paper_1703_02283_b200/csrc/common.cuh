@@ -130,6 +130,10 @@ struct GemmArgs {
   int crt_l0, crt_l1;   // CRT: the moduli [crt_l0, crt_l1) of this launch (modulus-major)
   uint8_t *crt_v;       // CRT: v_l of moduli 0..crt_n-1 at crt_v[(l * M + i) * ldv + j]
   int64_t ldv;
+  // tri: the mirror (j, i) of an upper element (i, j) goes to mout[i * ldm + (j - col0)] -- at G = 1
+  // mout = tout, ldm = ldt (the launchers fill them in when mout is null); a G > 1 rank points it at the
+  // packed [G][kp][kp] send buffer of the mirror exchange (ldm = kp)
+  void *mout; int64_t ldm;
 };
 
 // ------------------------------------------------------------------------------------

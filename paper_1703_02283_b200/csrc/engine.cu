@@ -52,7 +52,12 @@ struct ipr_ctx {
   const double *A = nullptr;
   double norms[4] = {0, 0, 0, 0};
   std::string err;
-  NcclComm comm;
+  Transport *comm = nullptr;           // world > 1: NCCL (ipr_init) or an in-process local group (ipr_testing.h)
+  cudaStream_t cst = nullptr;           // world > 1: side stream of the Chat all-gathers that overlap GEMM 1
+  cudaEvent_t gev[2] = {nullptr, nullptr};
+  bool gpend = false;                   // an all-gather on cst that the compute stream has not joined yet
+  void *chat_rm = nullptr;              // world > 1, CRT phases: row-major FP64 Chat (the A-role residue split)
+  void *msend = nullptr, *mrecv = nullptr;   // world > 1, tri form: packed [G][kp][kp] mirror exchange buffers
   // schedule
   int p = 0;
   std::vector<PhaseC> ph;
@@ -234,8 +239,31 @@ ipr_status gather_chat(ipr_ctx *c, int i, int prec) {
   // packed panel-major layout for this precision: rank r's slot at r * npad * kp * esz
   const size_t bytes = (size_t)(c->npad * c->kp) * elt_size(prec);
   char *base = (char *)c->chat[i];
-  if (!c->comm.allgather(base + c->rank * bytes, base, bytes, c->st))
-    return fail(c, IPR_E_NCCL, "ncclAllGather(Chat) failed: %s", c->comm.last_error());
+  if (!c->comm->allgather(base + c->rank * bytes, base, bytes, c->st))
+    return fail(c, IPR_E_NCCL, "ncclAllGather(Chat) failed: %s", c->comm->last_error());
+  return IPR_OK;
+}
+
+// world > 1, symmetric forms: the all-gather of Chat_{k+1} (and its correction-format copy) runs on the
+// side stream cst while GEMM 1 of the next chain (Z_1 = Ahat Chat[:, S_g]: the LOCAL panel only) runs on
+// the compute stream; join_gather() before the first GEMM that reads the whole Chat (SURVEY 8(e)
+// overlap; PAPER.md:138-141 data exchange)
+ipr_status gather_bytes_async(ipr_ctx *c, void *base, size_t per_rank, const char *what) {
+  if (c->world == 1) return IPR_OK;
+  if (!c->gpend) {
+    CK(cudaEventRecord(c->gev[0], c->st));
+    CK(cudaStreamWaitEvent(c->cst, c->gev[0], 0));
+  }
+  if (!c->comm->allgather((char *)base + c->rank * per_rank, base, per_rank, c->cst))
+    return fail(c, IPR_E_NCCL, "all-gather(%s) failed: %s", what, c->comm->last_error());
+  CK(cudaEventRecord(c->gev[1], c->cst));
+  c->gpend = true;
+  return IPR_OK;
+}
+ipr_status join_gather(ipr_ctx *c) {
+  if (!c->gpend) return IPR_OK;
+  CK(cudaStreamWaitEvent(c->st, c->gev[1], 0));
+  c->gpend = false;
   return IPR_OK;
 }
 
@@ -249,14 +277,14 @@ void chat_view(ipr_ctx *c, int i, int prec, const void **A, int64_t *akp, int64_
 
 ipr_status gather_partials(ipr_ctx *c, double *part, int64_t per_rank) {
   if (c->world == 1) return IPR_OK;
-  if (!c->comm.allgather(part + c->rank * per_rank, part, (size_t)per_rank * 8, c->st))
-    return fail(c, IPR_E_NCCL, "ncclAllGather(partials) failed: %s", c->comm.last_error());
+  if (!c->comm->allgather(part + c->rank * per_rank, part, (size_t)per_rank * 8, c->st))
+    return fail(c, IPR_E_NCCL, "ncclAllGather(partials) failed: %s", c->comm->last_error());
   return IPR_OK;
 }
 ipr_status gather_pmax(ipr_ctx *c, float *pm, int64_t per_rank) {
   if (c->world == 1) return IPR_OK;
-  if (!c->comm.allgather(pm + c->rank * per_rank, pm, (size_t)per_rank * 4, c->st))
-    return fail(c, IPR_E_NCCL, "ncclAllGather(max partials) failed: %s", c->comm.last_error());
+  if (!c->comm->allgather(pm + c->rank * per_rank, pm, (size_t)per_rank * 4, c->st))
+    return fail(c, IPR_E_NCCL, "ncclAllGather(max partials) failed: %s", c->comm->last_error());
   return IPR_OK;
 }
 
@@ -294,7 +322,7 @@ ipr_status stage_a(ipr_ctx *c, const PhaseC &P, void *dst, int *sig_dst) {
 
 // container cont(i) -> operand Chat(i) (+ FP16 sigma), then all-gather (a8 / a9)
 // premax: the per-rank max |C| is already in pmax[rank] (k_sym_update's amax), one partial per rank
-ipr_status make_operand(ipr_ctx *c, int i, const PhaseC &P, bool premax = false) {
+ipr_status make_operand(ipr_ctx *c, int i, const PhaseC &P, bool premax = false, bool async = false) {
   const int64_t cnt = c->npad * c->kp;
   if (!is_f64(P.prec)) {
     const int *sig = nullptr;
@@ -307,6 +335,7 @@ ipr_status make_operand(ipr_ctx *c, int i, const PhaseC &P, bool premax = false)
     }
     CK(launch_make_operand(cont_ptr(c, i, P), P.cont64, cnt, P.prec, sig, chat_slot(c, i, P.prec), c->st));
   }
+  if (async) return gather_bytes_async(c, c->chat[i], (size_t)cnt * elt_size(P.prec), "Chat");
   return gather_chat(c, i, P.prec);
 }
 
@@ -362,15 +391,22 @@ ipr_status oz_operands(ipr_ctx *c, GemmArgs &g, int i, const void *Xt) {
 int crt_bits_now(const ipr_ctx *c) { return crt_bits(oz_S_now(c), c->n); }
 ipr_status crt_ensure_a(ipr_ctx *c, int b) {
   if (c->crA_b == b) return IPR_OK;
-  CK(launch_crt_split((const double *)c->Aop, c->npad, c->npad, c->npad, b, crt_moduli(b, c->n), c->crA, c->crA_sig,
-                      c->st));
+  // the A role needs every row of Ahat: G = 1 its K-major local panel is the whole (symmetric) Ahat;
+  // G > 1 the full row-major copy the symmetric forms keep
+  CK(launch_crt_split((const double *)(c->world > 1 ? c->Afull : c->Aop), c->npad, c->npad, c->npad, b,
+                      crt_moduli(b, c->n), c->crA, c->crA_sig, c->st));
   c->crA_b = b;
   return IPR_OK;
 }
 ipr_status crt_ensure_c(ipr_ctx *c, int i, int b) {
   if (c->crC_for == i && c->crC_b == b) return IPR_OK;
-  CK(launch_crt_split((const double *)c->chat[i], c->npad, c->npad, c->npad, b, crt_moduli(b, c->n), c->crC,
-                      c->crC_sig, c->st));
+  const double *src = (const double *)c->chat[i];
+  if (c->world > 1) {   // panel-major [G][npad][kp] -> row-major (the split takes whole rows)
+    CKS(join_gather(c));
+    CK(launch_copy_out((const double *)c->chat[i], c->npad, c->kp, c->n, (double *)c->chat_rm, c->npad, c->st));
+    src = (const double *)c->chat_rm;
+  }
+  CK(launch_crt_split(src, c->npad, c->npad, c->npad, b, crt_moduli(b, c->n), c->crC, c->crC_sig, c->st));
   c->crC_for = i; c->crC_b = b;
   return IPR_OK;
 }
@@ -383,7 +419,8 @@ ipr_status crt_operands(ipr_ctx *c, GemmArgs &g, int i, const void *Xt) {
   const int b = crt_bits_now(c);
   if (i < 0) CKS(crt_ensure_a(c, b));
   else CKS(crt_ensure_c(c, i, b));
-  CK(launch_crt_split((const double *)Xt, c->npad, c->npad, c->npad, b, crt_moduli(b, c->n), c->crB, c->crB_sig, c->st));
+  // B role: the kp rows of the K-major local panel Xt (the columns of this rank)
+  CK(launch_crt_split((const double *)Xt, c->npad, c->kp, c->npad, b, crt_moduli(b, c->n), c->crB, c->crB_sig, c->st));
   g.oz_a = i < 0 ? c->crA : c->crC;
   g.oz_rsig = i < 0 ? c->crA_sig : c->crC_sig;
   g.oz_b = c->crB; g.oz_csig = c->crB_sig;
@@ -412,8 +449,8 @@ void *chatc_slot(ipr_ctx *c, int i, int prec) {
 }
 ipr_status gather_bytes(ipr_ctx *c, void *base, size_t per_rank, const char *what) {
   if (c->world == 1) return IPR_OK;
-  if (!c->comm.allgather((char *)base + c->rank * per_rank, base, per_rank, c->st))
-    return fail(c, IPR_E_NCCL, "ncclAllGather(%s) failed: %s", what, c->comm.last_error());
+  if (!c->comm->allgather((char *)base + c->rank * per_rank, base, per_rank, c->st))
+    return fail(c, IPR_E_NCCL, "ncclAllGather(%s) failed: %s", what, c->comm->last_error());
   return IPR_OK;
 }
 // symmetric form: Chat of iterate buffer i in the correction format (if it differs from prec)
@@ -472,6 +509,19 @@ ipr_status make_xt(ipr_ctx *c, int i, const PhaseC &P) {
   return IPR_OK;
 }
 
+// tri form, G > 1: GEMM 2 computed the upper-triangle tiles of this rank's columns S_g; their mirrors
+// (j, i), i < j, belong to the columns S_h of the ranks owning row i and were written packed into msend
+// [h][i - col0_h][j - col0_g].  One all-to-all delivers each block to its owner, which copies the
+// strictly-lower elements of its columns into its K-major panel T (the same values, so every element
+// is bit-identical to G = 1 -- DESIGN.md section 7).
+ipr_status mirror_exchange(ipr_ctx *c, void *T, int esz) {
+  const size_t blk = (size_t)(c->kp * c->kp) * esz;
+  if (!c->comm->alltoall(c->msend, c->mrecv, blk, c->st))
+    return fail(c, IPR_E_NCCL, "all-to-all(tri mirror) failed: %s", c->comm->last_error());
+  CK(launch_mirror_unpack(c->mrecv, esz, c->kp, c->npad, c->rank, c->world, T, c->st));
+  return IPR_OK;
+}
+
 // ---- one chain: p GEMMs + fused residual; returns rho (host sync) ----
 ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
   const PhaseC &P = c->ph[c->phase];
@@ -516,6 +566,7 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
     // else the transposed local panel), Z_j = Chat qin(Z_{j-1}); GEMM p: R = I - Z_p in the
     // correction format (K-major for the W GEMM) + residual partials.  Z_j -> T[j & 1].
     for (int j = 1; j <= c->p; ++j) {
+      if (j == 2) CKS(join_gather(c));   // GEMM 1 needed only the local panel; from here on the whole Chat
       GemmArgs g = base_args(c, prec, j == 1 ? (c->world == 1 ? c->chat[c->cur] : c->T[0]) : c->T[(j - 1) & 1]);
       if (j == 1) {
         g.A = c->world == 1 ? c->Aop : c->Afull;
@@ -560,7 +611,9 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
           CKS(oz_operands(c, g, c->cur, c->T[(j - 1) & 1]));
         }
       } else if (prec == IPR_FP64_CRT) {
-        if (j == 1) {   // Ahat (A role) x Chat (B role: its rows, by symmetry)
+        if (j == 1 && c->world > 1) {   // Ahat (A role) x the transposed local panel of Chat (B role)
+          CKS(crt_operands(c, g, -1, c->T[0]));
+        } else if (j == 1) {   // Ahat (A role) x Chat (B role: its rows, by symmetry)
           const int b = crt_bits_now(c);
           CKS(crt_ensure_a(c, b));
           CKS(crt_ensure_c(c, c->cur, b));
@@ -570,7 +623,10 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
           CKS(crt_operands(c, g, c->cur, c->T[(j - 1) & 1]));
         }
       }
+      const bool mx = j == c->p && g.tri && c->world > 1;   // tri, G > 1: mirror tiles cross panels
+      if (mx) { g.mout = c->msend; g.ldm = c->kp; }
       CK(run_gemm(c, g));
+      if (mx) CKS(mirror_exchange(c, g.tout, rscr ? 4 : elt_size(g.tprec)));
       if (rscr) {   // sigma_R -> dsig[3 + (p & 1)] (not the slot GEMM p read), Rhat -> T[p & 1]
         CKS(gather_pmax(c, c->pmax, tn_loc * tm));
         CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 3 + (j & 1), prec, c->st));
@@ -743,12 +799,13 @@ ipr_status update_sym(ipr_ctx *c) {
   const int64_t t64 = c->npad / 64;
   CKS(gather_partials(c, c->part, (c->kp / 64) * t64));
   CK(launch_reduce_sum(c->part, t64 * t64, c->dscal + 1, c->st));
-  if (is_scaled(P.prec)) CKS(make_operand(c, nx, P, true));   // sigma from the update's max|C_{k+1}|
-  else CKS(gather_chat(c, nx, P.prec));
+  if (is_scaled(P.prec)) CKS(make_operand(c, nx, P, true, true));   // sigma from the update's max|C_{k+1}|
+  else CKS(gather_bytes_async(c, c->chat[nx], (size_t)(c->npad * c->kp) * elt_size(P.prec), "Chat"));
   if (P.prec == IPR_FP64_OZ) CKS(oz_split_chat(c, nx));
   if (c->crC_for == nx) c->crC_for = -1;
   c->m_of_cur = P.adaptive ? c->oz_m_next : P.m;
-  if (!same_fmt(P.corr, P.prec)) CKS(gather_bytes(c, c->chatc[nx], (size_t)(c->npad * c->kp) * elt_size(P.corr), "Chat corr"));
+  if (!same_fmt(P.corr, P.prec))
+    CKS(gather_bytes_async(c, c->chatc[nx], (size_t)(c->npad * c->kp) * elt_size(P.corr), "Chat corr"));
   if (c->world > 1) CKS(make_xt(c, nx, P));
   c->cur = nx;
   return IPR_OK;
@@ -842,7 +899,9 @@ void free_ctx(ipr_ctx *c) {
   if (c->hscal) pinned_release(c->hscal);
   for (auto &e : c->ev) if (e) cudaEventDestroy(e);
   for (auto &e : c->kev) if (e) cudaEventDestroy(e);
-  c->comm.destroy();
+  if (c->cst) { cudaStreamSynchronize(c->cst); cudaStreamDestroy(c->cst); }
+  for (auto &e : c->gev) if (e) cudaEventDestroy(e);
+  delete c->comm;
   delete c;
 }
 
@@ -883,7 +942,10 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       {&c->cNk[1], cpl ? panel * 8 : 0}, {&c->cNf, cpl ? full * 8 : 0},
       // CRT arenas: the certify / copy-out scratch lives in the B-residue and v-byte scratch (dead
       // outside a CRT product; every product re-splits its B operand)
-      {(void **)&c->full64, cr ? 0 : full * 8}, {&c->Acert, cr ? 0 : panel * 8}};
+      {(void **)&c->full64, cr ? 0 : full * 8}, {&c->Acert, cr ? 0 : panel * 8},
+      {&c->chat_rm, (cr && c->world > 1) ? full * 8 : 0},
+      {&c->msend, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0},
+      {&c->mrecv, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0}};
   size_t total = 0;
   for (const Slot &q : slots) total += (q.bytes + 255) / 256 * 256;
   // stream-ordered allocation from a library-owned pool that retains its memory, so back-to-back
@@ -905,6 +967,7 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
   if (cr) { c->full64 = (double *)c->crB; c->Acert = c->crV; }   // 8 B x npad^2 <= 18 B x npad^2
   CK(cudaMemsetAsync(c->chat[0], 0, full * 8, c->st));
   CK(cudaMemsetAsync(c->chat[1], 0, full * 8, c->st));
+  if (c->chat_rm) CK(cudaMemsetAsync(c->chat_rm, 0, full * 8, c->st));   // padding rows / columns stay 0
   return IPR_OK;
 }
 
@@ -912,8 +975,8 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
 ipr_status gather_f64(ipr_ctx *c, const double *local) {
   double *slot = c->full64 + (size_t)c->rank * c->npad * c->kp;
   if (local != slot) CK(cudaMemcpyAsync(slot, local, (size_t)(c->npad * c->kp) * 8, cudaMemcpyDeviceToDevice, c->st));
-  if (c->world > 1 && !c->comm.allgather(slot, c->full64, (size_t)(c->npad * c->kp) * 8, c->st))
-    return fail(c, IPR_E_NCCL, "ncclAllGather(C) failed: %s", c->comm.last_error());
+  if (c->world > 1 && !c->comm->allgather(slot, c->full64, (size_t)(c->npad * c->kp) * 8, c->st))
+    return fail(c, IPR_E_NCCL, "ncclAllGather(C) failed: %s", c->comm->last_error());
   return IPR_OK;
 }
 
@@ -942,8 +1005,9 @@ ipr_status ipr_nccl_unique_id(void *out128) {
   return IPR_OK;
 }
 
-ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, void *cuda_stream, int world,
-                    int rank, const void *nccl_unique_id, int grid_rows, int grid_cols) {
+// ipr_init / ipr_test_init_local: lg == nullptr -> NCCL from nccl_unique_id (world > 1)
+static ipr_status init_ctx(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, void *cuda_stream, int world,
+                           int rank, const void *nccl_unique_id, LocalGroup *lg, int grid_rows, int grid_cols) {
   ipr_ctx *c = nullptr;
   if (!out || !A_dev) return fail(c, IPR_E_INVALID_ARG, "ipr_init: null pointer");
   *out = nullptr;
@@ -953,7 +1017,7 @@ ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, 
   if (world < 1 || rank < 0 || rank >= world) return fail(c, IPR_E_INVALID_ARG, "ipr_init: bad world/rank");
   if (grid_rows != 1 || grid_cols != world)
     return fail(c, IPR_E_UNSUPPORTED, "ipr_init: only 1 x world column-panel grids are implemented");
-  if (world > 1 && !nccl_unique_id) return fail(c, IPR_E_INVALID_ARG, "ipr_init: world > 1 needs an NCCL id");
+  if (world > 1 && !nccl_unique_id && !lg) return fail(c, IPR_E_INVALID_ARG, "ipr_init: world > 1 needs an NCCL id");
   c = new ipr_ctx();
   c->n = n; c->lda = lda; c->A = A_dev; c->world = world; c->rank = rank;
   c->st = (cudaStream_t)cuda_stream;
@@ -1000,13 +1064,50 @@ ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, 
   c->npart = (c->npad / 64) * (c->npad / 64) + 1024;    // one slot per 64 x 64 tile (k_sym_update)
   if (world > 1) {
     std::string e;
-    if (!c->comm.init(world, rank, nccl_unique_id, &e)) TRY(fail(c, IPR_E_NCCL, "%s", e.c_str()));
+    if (lg) {
+      c->comm = local_transport(lg, rank, &e);
+      if (!c->comm) TRY(fail(c, IPR_E_INVALID_ARG, "%s", e.c_str()));
+    } else {
+      NcclComm *nc = new NcclComm();
+      c->comm = nc;
+      if (!nc->init(world, rank, nccl_unique_id, &e)) TRY(fail(c, IPR_E_NCCL, "%s", e.c_str()));
+    }
+    TRYC(cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking));
+    for (auto &ev : c->gev) TRYC(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   TRYC(cudaStreamSynchronize(c->st));
 #undef TRY
 #undef TRYC
   *out = c;
   return IPR_OK;
+}
+
+ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, void *cuda_stream, int world,
+                    int rank, const void *nccl_unique_id, int grid_rows, int grid_cols) {
+  return init_ctx(out, n, A_dev, lda, cuda_stream, world, rank, nccl_unique_id, nullptr, grid_rows, grid_cols);
+}
+
+ipr_status ipr_test_local_group_create(int world, ipr_local_group **out) {
+  ipr_ctx *c = nullptr;
+  if (!out) return fail(c, IPR_E_INVALID_ARG, "ipr_test_local_group_create: null output");
+  std::string e;
+  LocalGroup *g = local_group_create(world, &e);
+  if (!g) return fail(c, IPR_E_INVALID_ARG, "%s", e.c_str());
+  *out = (ipr_local_group *)g;
+  return IPR_OK;
+}
+
+ipr_status ipr_test_local_group_destroy(ipr_local_group *g) {
+  local_group_destroy((LocalGroup *)g);
+  return IPR_OK;
+}
+
+ipr_status ipr_test_init_local(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, void *cuda_stream,
+                               ipr_local_group *group, int rank, int grid_rows, int grid_cols) {
+  ipr_ctx *c = nullptr;
+  if (!group) return fail(c, IPR_E_INVALID_ARG, "ipr_test_init_local: null group");
+  LocalGroup *g = (LocalGroup *)group;
+  return init_ctx(out, n, A_dev, lda, cuda_stream, local_group_world(g), rank, nullptr, g, grid_rows, grid_cols);
 }
 
 ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int nphases, double final_tol) {
@@ -1093,15 +1194,16 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     for (auto &P : c->ph)
       if (P.prec == IPR_FP64_OZ && c->npad > 47800)   // INT32 digit-group sums (ozaki.cu)
         return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ needs n <= 47800 (exact INT32 group sums)");
-    for (auto &P : c->ph)
-      if (is_emu(P.prec) && (!is_sym(c) || c->world != 1))
-        return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ / IPR_FP64_CRT phases need a symmetric form and world = 1");
+    for (auto &P : c->ph) {
+      if (is_emu(P.prec) && !is_sym(c))
+        return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ / IPR_FP64_CRT phases need a symmetric form");
+      if (P.prec == IPR_FP64_OZ && c->world != 1)
+        return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ phases are single-GPU (IPR_FP64_CRT shards)");
+    }
     if (is_sym(c)) {
       if (c->p < 2) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: the symmetric form needs p >= 2 (p = 1: Newton-Schulz)");
       if (c->form == IPR_FORM_SYMMETRIC_TRI && c->p != 2)
         return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: the symmetric-tri form needs p = 2 (Z_2 = C A C symmetric)");
-      if (c->form == IPR_FORM_SYMMETRIC_TRI && c->world != 1)
-        return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: the symmetric-tri form is single-GPU (mirror writes cross panels)");
       c->wbytes = 4;
       for (auto &P : c->ph) {
         if (is_scaled(P.corr) && P.corr != P.prec)
@@ -1204,6 +1306,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       break;
     }
   }
+  CKS(join_gather(c));   // no side-stream exchange outlives the call
   *outcome = c->done ? (ipr_outcome)c->outcome : IPR_RUNNING;
   return IPR_OK;
 }

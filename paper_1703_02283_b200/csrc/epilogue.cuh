@@ -45,7 +45,7 @@ __device__ __forceinline__ void epi_element(const GemmArgs &g, int64_t row, int6
     if (mode & EPI_STORE_T) {
       // FP16 T operands go through EPI_TSCRATCH + a scale kernel (sigma 0 here)
       store_operand(g.tout, col * g.ldt + row, g.tprec, w, 0);
-      if (mirror) store_operand(g.tout, row * g.ldt + col, g.tprec, w, 0);
+      if (mirror) store_operand(g.mout, row * g.ldm + col, g.tprec, w, 0);
     } else {
       ((float *)g.tout)[col * g.ldt + row] = (float)w;
       acc.mx = fmaxf(acc.mx, fabsf((float)w));

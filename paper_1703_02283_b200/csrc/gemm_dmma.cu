@@ -177,7 +177,9 @@ static cudaError_t launch_mode(const GemmArgs &a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_gemm_dmma(const GemmArgs &a, cudaStream_t s) {
+cudaError_t launch_gemm_dmma(const GemmArgs &a_in, cudaStream_t s) {
+  GemmArgs a = a_in;
+  if (!a.mout) { a.mout = a.tout; a.ldm = a.ldt; }   // tri mirror: in place at G = 1
   if (a.M % DM_BM || a.N % DM_BN || a.K % DM_BK || a.a_kp % DM_BK) return cudaErrorInvalidValue;
   // the hot-path modes get specialised kernels; anything else uses the runtime-mode build
   if (!a.pmax && a.prec == P_FP64) {

@@ -198,23 +198,27 @@ __device__ __forceinline__ double acc_to_f64(uint32_t w) {
 
 struct TileSched {      // pair tiles: tiles_m pair-rows (256 rows) x tiles_n (256 columns)
   int tiles_m, tiles_n, tri;
+  int coff;             // tri, column panel of a G > 1 rank: global 256-column tile of local tile 0 --
+                        // the upper-triangle tiles are tm <= coff + tn (0 for a square single panel)
   // tri (square, symmetric-tri GEMM 2 / fused update): only the upper-triangle pair tiles tm <= tn, in
   // bands of TRI_GC pair-columns, row by row inside a band, so the CTA pairs in flight share their A
   // row blocks (TRI_GC tiles each) and B column blocks (the band) in L2 -- a column-by-column order
   // streamed ~8 GB per K = 2n fused-update GEMM from DRAM
   static constexpr int TRI_GC = 8;
-  __host__ __device__ int count() const { return tri ? tiles_n * (tiles_n + 1) / 2 : tiles_m * tiles_n; }
+  __host__ __device__ int count() const {
+    return tri ? tiles_n * coff + tiles_n * (tiles_n + 1) / 2 : tiles_m * tiles_n;
+  }
   __device__ void get(int t, int &tm, int &tn) const {
     if (tri) {
-      for (int c0 = 0;; c0 += TRI_GC) {                // band [c0, c1): c0 * w full-width rows, then its diagonal
-        const int c1 = min(c0 + TRI_GC, tiles_n), w = c1 - c0;
-        const int nb = c0 * w + w * (w + 1) / 2;
+      for (int c0 = 0;; c0 += TRI_GC) {                // band [c0, c1): (coff + c0) * w full-width rows, then its diagonal
+        const int c1 = min(c0 + TRI_GC, tiles_n), w = c1 - c0, fr = coff + c0;
+        const int nb = fr * w + w * (w + 1) / 2;
         if (t < nb) {
-          if (t < c0 * w) { tm = t / w; tn = c0 + t % w; return; }
-          t -= c0 * w;
+          if (t < fr * w) { tm = t / w; tn = c0 + t % w; return; }
+          t -= fr * w;
           int r = 0;
-          while (t >= w - r) { t -= w - r; ++r; }      // diagonal block: row c0 + r has w - r tiles
-          tm = c0 + r; tn = c0 + r + t;
+          while (t >= w - r) { t -= w - r; ++r; }      // diagonal block: row fr + r has w - r tiles
+          tm = fr + r; tn = c0 + r + t;
           return;
         }
         t -= nb;
@@ -388,12 +392,12 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
           ea.r2 = __fma_rn(2.0 * d, d, ea.r2);
         }
       }
-      uint4 *m = (uint4 *)(t + row * g.ldt + col);
+      uint4 *m = (uint4 *)((__nv_bfloat16 *)g.mout + row * g.ldm + col);
       #pragma unroll
       for (int q = 0; q < 4; ++q) m[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
     } else {
       float *t = (float *)g.tout;
-      float4 *m = (float4 *)(t + row * g.ldt + col);
+      float4 *m = (float4 *)((float *)g.mout + row * g.ldm + col);
       if (ts) {
         // R-29 scratch: the stored float is one FP32 multiply by the power-of-two scale (the same
         // float as (float)(acc * scale) in FP64, as in (b)); FP64 only for the residual, from the
@@ -484,7 +488,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
         ea.r2 = __fma_rn(row != gc ? 2.0 * d : d, d, ea.r2);
       }
     }
-    float *mr = t + row * g.ldt + col;               // mirror (row, c), c > row
+    float *mr = (float *)g.mout + row * g.ldm + col;   // mirror (row, c), c > row
     #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int64_t c4 = gc0 + 4 * q;
@@ -513,11 +517,11 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
       }
       if (mode & EPI_STORE_T) {
         store_operand(g.tout, c * g.ldt + row, g.tprec, w, 0);
-        if (mirror) store_operand(g.tout, row * g.ldt + c, g.tprec, w, 0);
+        if (mirror) store_operand(g.mout, row * g.ldm + c, g.tprec, w, 0);
       }
       if (mode & EPI_TSCRATCH) {
         ((float *)g.tout)[c * g.ldt + row] = (float)w;
-        if (mirror) ((float *)g.tout)[row * g.ldt + c] = (float)w;
+        if (mirror) ((float *)g.mout)[row * g.ldm + c] = (float)w;
         ea.mx = fmaxf(ea.mx, fabsf((float)w));
       }
       if (mode & EPI_RESID) {
@@ -631,7 +635,7 @@ __device__ __forceinline__ void epi_row_t(const GemmArgs &g, int64_t row, int64_
     const double w = diag ? __dsub_rn(dv * g.diag, v[j]) : v[j];
     if (st) {
       st_t<TP>(g.tout, c * g.ldt + row, w);
-      if (mirror) st_t<TP>(g.tout, row * g.ldt + c, w);
+      if (mirror) st_t<TP>(g.mout, row * g.ldm + c, w);
     }
     if (rs && row < g.n && gc < g.n) {
       const double d = __dsub_rn(row == gc ? 1.0 : 0.0, v[j]);
@@ -711,7 +715,7 @@ template <int NM>   // the modulus count: the loops over moduli unroll exactly, 
 __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
   extern __shared__ double sm_slab[];          // [32][CRT_FIN_LD]
   __shared__ double red[8];
-  const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN), g.tri};
+  const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN), g.tri, (int)(g.col0 / TC_BN)};
   int tm, tn;
   sch.get((int)(blockIdx.x >> 1), tm, tn);
   const int tile_m = tm * 2 + (int)(blockIdx.x & 1);
@@ -817,14 +821,14 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
             }
             if (st && mir) {                             // (j, i): row-major in T, one vector store
               if (tp == 0) {
-                double2 *m = (double2 *)((double *)g.tout + row * g.ldt + c0);
+                double2 *m = (double2 *)((double *)g.mout + row * g.ldm + c0);
                 m[0] = make_double2(wv[0], wv[1]); m[1] = make_double2(wv[2], wv[3]);
               } else if (tp == 1) {
                 const __nv_bfloat162 a = __floats2bfloat162_rn((float)wv[0], (float)wv[1]);
                 const __nv_bfloat162 b = __floats2bfloat162_rn((float)wv[2], (float)wv[3]);
-                *(uint2 *)((__nv_bfloat16 *)g.tout + row * g.ldt + c0) = make_uint2(*(const uint32_t *)&a, *(const uint32_t *)&b);
+                *(uint2 *)((__nv_bfloat16 *)g.mout + row * g.ldm + c0) = make_uint2(*(const uint32_t *)&a, *(const uint32_t *)&b);
               } else {
-                *(float4 *)((float *)g.tout + row * g.ldt + c0) =
+                *(float4 *)((float *)g.mout + row * g.ldm + c0) =
                     make_float4(to_tf32((float)wv[0]), to_tf32((float)wv[1]), to_tf32((float)wv[2]), to_tf32((float)wv[3]));
               }
             }
@@ -840,9 +844,9 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
                 r2 = __fma_rn(mirror ? 2.0 * d : d, d, r2);
               }
               if (st && mirror) {                              // (j, i) of a tri element: row-major in T
-                if (tp == 0) st_t<0>(g.tout, row * g.ldt + c, wv[u]);
-                else if (tp == 1) st_t<1>(g.tout, row * g.ldt + c, wv[u]);
-                else st_t<2>(g.tout, row * g.ldt + c, wv[u]);
+                if (tp == 0) st_t<0>(g.mout, row * g.ldm + c, wv[u]);
+                else if (tp == 1) st_t<1>(g.mout, row * g.ldm + c, wv[u]);
+                else st_t<2>(g.mout, row * g.ldm + c, wv[u]);
               }
             }
           }
@@ -886,10 +890,12 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish(const GemmArgs g) {
   }
 }
 
-cudaError_t launch_crt_finish(const GemmArgs &a, cudaStream_t s) {
-  const TileSched hs{(int)(a.M / (2 * TC_BM)), (int)(a.N / TC_BN), a.tri};
+cudaError_t launch_crt_finish(const GemmArgs &a_in, cudaStream_t s) {
+  GemmArgs a = a_in;
+  if (!a.mout) { a.mout = a.tout; a.ldm = a.ldt; }   // tri mirror: in place at G = 1
+  const TileSched hs{(int)(a.M / (2 * TC_BM)), (int)(a.N / TC_BN), a.tri, (int)(a.col0 / TC_BN)};
   if (a.tri && (a.mode & EPI_RESID)) {   // the tiles below the diagonal are not visited: zero partials
-    cudaError_t z = cudaMemsetAsync(a.part, 0, (size_t)(a.N / TC_BN) * a.tiles_m * sizeof(double), s);
+    cudaError_t z = cudaMemsetAsync(a.part + (a.col0 / TC_BN) * a.tiles_m, 0, (size_t)(a.N / TC_BN) * a.tiles_m * sizeof(double), s);
     if (z != cudaSuccess) return z;
   }
   const int smem = 32 * CRT_FIN_LD * 8;
@@ -933,7 +939,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN), g.tri};
+  const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN), g.tri, (int)(g.col0 / TC_BN)};
   const int ntiles = sch.count();
   // CRT (oz_grouped == 3): moduli [crt_l0, crt_l1) of every tile, modulus-major (all CTA pairs
   // stream the same residue planes at a time, as in one plain GEMM)
@@ -1160,7 +1166,9 @@ static int num_sms() {            // per device ordinal (cached)
   return cache[dev];
 }
 
-cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
+cudaError_t launch_gemm_tc(const GemmArgs &a_in, cudaStream_t s) {
+  GemmArgs a = a_in;
+  if (!a.mout) { a.mout = a.tout; a.ldm = a.ldt; }   // tri mirror: in place at G = 1
   if (!tc_supported(a.prec)) return cudaErrorNotSupported;
   if (a.M % (2 * TC_BM) || a.N % TC_BN || a.K % 128 || a.a_kp % 128) {
     snprintf(g_tc_err, sizeof g_tc_err, "tcgen05 GEMM: sizes M=%lld N=%lld K=%lld kp=%lld not tile multiples",
@@ -1216,14 +1224,14 @@ cudaError_t launch_gemm_tc(const GemmArgs &a, cudaStream_t s) {
       return cudaErrorInvalidValue;
     }
   }
-  if (a.tri && (a.M != a.N || a.col0 != 0)) {
-    snprintf(g_tc_err, sizeof g_tc_err, "tcgen05 GEMM: tri needs a square single-panel product");
+  if (a.tri && (a.M != a.K || a.col0 + a.N > a.M)) {
+    snprintf(g_tc_err, sizeof g_tc_err, "tcgen05 GEMM: tri needs a square product (or a column panel of one)");
     return cudaErrorInvalidValue;
   }
-  const TileSched hs{(int)(a.M / (2 * TC_BM)), (int)(a.N / TC_BN), a.tri};
+  const TileSched hs{(int)(a.M / (2 * TC_BM)), (int)(a.N / TC_BN), a.tri, (int)(a.col0 / TC_BN)};
   const int ntiles = hs.count() * (a.oz_grouped == 3 ? a.crt_l1 - a.crt_l0 : 1);
   if (a.tri && (a.mode & (EPI_RESID | EPI_SYMUPD)) && a.oz_grouped != 3) {   // the tiles below the diagonal are not visited: zero partials
-    cudaError_t z = cudaMemsetAsync(a.part, 0, (size_t)(a.N / TC_BN) * a.tiles_m * sizeof(double), s);
+    cudaError_t z = cudaMemsetAsync(a.part + (a.col0 / TC_BN) * a.tiles_m, 0, (size_t)(a.N / TC_BN) * a.tiles_m * sizeof(double), s);
     if (z != cudaSuccess) return z;
   }
   const int maxpairs = num_sms() / 2;

@@ -571,6 +571,33 @@ cudaError_t launch_maxabs_cont(const void *cont, int cont64, int64_t count, floa
   k_maxabs_cont<<<nparts, 256, 0, s>>>(cont, cont64, count, pmax);
   LAUNCH_CHECK();
 }
+// tri form, G > 1 (engine mirror_exchange): recv[g][r][c] (from rank g >= rank) holds the mirror value of
+// element (i, j) = (g kp + c, rank kp + r); the strictly-lower ones (i > j) go to this rank's K-major
+// panel T[r * npad + i]; the rest of T already holds its own upper-triangle values
+__global__ void k_mirror_unpack(const char *recv, int esz, int64_t kp, int64_t npad, int rank, int world, char *T) {
+  const int64_t per = kp * kp, total = (int64_t)(world - rank) * per;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = rank + t / per, rc = t % per, r = rc / kp, cc = rc % kp;
+    const int64_t i = g * kp + cc, j = (int64_t)rank * kp + r;
+    if (i <= j) continue;
+    const char *src = recv + ((g * kp + r) * kp + cc) * esz;
+    char *dst = T + (r * npad + i) * esz;
+    switch (esz) {
+      case 1: *dst = *src; break;
+      case 2: *(uint16_t *)dst = *(const uint16_t *)src; break;
+      case 4: *(uint32_t *)dst = *(const uint32_t *)src; break;
+      default: *(uint64_t *)dst = *(const uint64_t *)src; break;
+    }
+  }
+}
+cudaError_t launch_mirror_unpack(const void *recv, int esz, int64_t kp, int64_t npad, int rank, int world, void *T,
+                                 cudaStream_t s) {
+  const int64_t total = (int64_t)(world - rank) * kp * kp;
+  if (total <= 0) return cudaSuccess;
+  k_mirror_unpack<<<nblk(total, 256), 256, 0, s>>>((const char *)recv, esz, kp, npad, rank, world, (char *)T);
+  LAUNCH_CHECK();
+}
+
 // test hook (ipr_test_peek): an operand-format buffer as FP64 values, unscaled by 2^-sigma (exact)
 __global__ void k_peek(const void *src, int prec, const int *sig, int64_t count, double *dst) {
   const double us = sig ? pow2(-*sig) : 1.0;

@@ -16,6 +16,8 @@ cudaError_t launch_make_operand(const void *cont, int cont64, int64_t count, int
                                 cudaStream_t s);
 cudaError_t launch_scale_op(const float *src, int64_t count, const int *sig, int prec, void *dst, cudaStream_t s);
 cudaError_t launch_maxabs_cont(const void *cont, int cont64, int64_t count, float *pmax, int nparts, cudaStream_t s);
+cudaError_t launch_mirror_unpack(const void *recv, int esz, int64_t kp, int64_t npad, int rank, int world, void *T,
+                                 cudaStream_t s);
 cudaError_t launch_peek(const void *src, int prec, const int *sig, int64_t count, double *dst, cudaStream_t s);
 cudaError_t launch_cont_to_f64(const void *cont, int cont64, int64_t count, double *dst, cudaStream_t s);
 cudaError_t launch_f64_to_cont(const double *src, int64_t count, int cont64, int m, int rtz, void *cont,

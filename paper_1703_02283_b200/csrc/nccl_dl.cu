@@ -1,10 +1,14 @@
-// nccl_dl.cu -- dlopen'ed NCCL (prefers the copy torch already loaded into the process).
+// nccl_dl.cu -- the transports of nccl_dl.h: dlopen'ed NCCL (prefers the copy torch already loaded
+// into the process) and the in-process local group used to run the sharded path on one device.
 #include "nccl_dl.h"
 
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <condition_variable>
+#include <cstring>
 #include <mutex>
+#include <vector>
 
 namespace ipr {
 namespace {
@@ -15,6 +19,10 @@ struct Api {
   decltype(&ncclGetUniqueId) getUniqueId = nullptr;
   decltype(&ncclCommInitRank) commInitRank = nullptr;
   decltype(&ncclAllGather) allGather = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
   decltype(&ncclCommDestroy) commDestroy = nullptr;
   decltype(&ncclGetErrorString) errStr = nullptr;
 };
@@ -30,9 +38,14 @@ Api &api() {
     a.getUniqueId = (decltype(a.getUniqueId))dlsym(h, "ncclGetUniqueId");
     a.commInitRank = (decltype(a.commInitRank))dlsym(h, "ncclCommInitRank");
     a.allGather = (decltype(a.allGather))dlsym(h, "ncclAllGather");
+    a.send = (decltype(a.send))dlsym(h, "ncclSend");
+    a.recv = (decltype(a.recv))dlsym(h, "ncclRecv");
+    a.groupStart = (decltype(a.groupStart))dlsym(h, "ncclGroupStart");
+    a.groupEnd = (decltype(a.groupEnd))dlsym(h, "ncclGroupEnd");
     a.commDestroy = (decltype(a.commDestroy))dlsym(h, "ncclCommDestroy");
     a.errStr = (decltype(a.errStr))dlsym(h, "ncclGetErrorString");
-    a.ok = a.getUniqueId && a.commInitRank && a.allGather && a.commDestroy && a.errStr;
+    a.ok = a.getUniqueId && a.commInitRank && a.allGather && a.send && a.recv && a.groupStart && a.groupEnd &&
+           a.commDestroy && a.errStr;
     if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
   });
   return a;
@@ -60,6 +73,7 @@ bool NcclComm::init(int world, int rank, const void *uid128, std::string *err) {
   ncclResult_t r = a.commInitRank(&c, world, id, rank);
   if (r != ncclSuccess) { *err = std::string("ncclCommInitRank: ") + a.errStr(r); return false; }
   comm_ = c;
+  world_ = world; rank_ = rank;
   return true;
 }
 
@@ -71,8 +85,120 @@ bool NcclComm::allgather(const void *send, void *recv, size_t bytes, cudaStream_
   return true;
 }
 
-void NcclComm::destroy() {
+bool NcclComm::alltoall(const void *send, void *recv, size_t bytes, cudaStream_t s) {
+  Api &a = api();
+  if (!comm_) { err_ = "communicator not initialised"; return false; }
+  ncclResult_t r = a.groupStart();
+  for (int h = 0; h < world_ && r == ncclSuccess; ++h) {
+    r = a.send((const char *)send + h * bytes, bytes, ncclInt8, h, (ncclComm_t)comm_, s);
+    if (r == ncclSuccess) r = a.recv((char *)recv + h * bytes, bytes, ncclInt8, h, (ncclComm_t)comm_, s);
+  }
+  const ncclResult_t e = a.groupEnd();
+  if (r == ncclSuccess) r = e;
+  if (r != ncclSuccess) { err_ = a.errStr(r); return false; }
+  return true;
+}
+
+NcclComm::~NcclComm() {
   if (comm_) { api().commDestroy((ncclComm_t)comm_); comm_ = nullptr; }
 }
+
+// ---------------------------------------------------------------------------------------
+// Local group: world ranks in one process on one device.  An exchange is
+//   1. rank r publishes its buffers and records `ready` on its stream; host barrier;
+//   2. rank r's stream waits for every peer's `ready`, copies what it needs from the peers' buffers,
+//      records `done`; host barrier;
+//   3. rank r's stream waits for every peer's `done` (no rank overwrites a buffer a peer still reads).
+// Each event is re-recorded only after the barrier that follows every wait on it.
+// ---------------------------------------------------------------------------------------
+struct LocalGroup {
+  int world = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long generation = 0;
+  struct Slot { const void *send = nullptr; void *recv = nullptr; cudaEvent_t ready = nullptr, done = nullptr; };
+  std::vector<Slot> slot;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long gen = generation;
+    if (++arrived == world) { arrived = 0; ++generation; cv.notify_all(); return; }
+    cv.wait(lk, [&] { return generation != gen; });
+  }
+};
+
+namespace {
+class LocalRank : public Transport {
+ public:
+  LocalRank(LocalGroup *g, int rank) : g_(g), rank_(rank) {}
+  bool allgather(const void *send, void *recv, size_t bytes, cudaStream_t s) override {
+    return exchange(send, recv, bytes, s, false);
+  }
+  bool alltoall(const void *send, void *recv, size_t bytes, cudaStream_t s) override {
+    return exchange(send, recv, bytes, s, true);
+  }
+  const char *last_error() const override { return err_.c_str(); }
+
+ private:
+  bool ck(cudaError_t e) {
+    if (e == cudaSuccess) return true;
+    err_ = cudaGetErrorString(e);
+    return false;
+  }
+  bool exchange(const void *send, void *recv, size_t bytes, cudaStream_t s, bool a2a) {
+    LocalGroup::Slot &me = g_->slot[rank_];
+    me.send = send; me.recv = recv;
+    bool ok = ck(cudaEventRecord(me.ready, s));
+    g_->barrier();
+    for (int h = 0; h < g_->world && ok; ++h) {
+      const LocalGroup::Slot &peer = g_->slot[h];
+      const char *src = a2a ? (const char *)peer.send + rank_ * bytes : (const char *)peer.send;
+      char *dst = (char *)recv + h * bytes;
+      if (h != rank_) ok = ck(cudaStreamWaitEvent(s, peer.ready, 0));
+      if (ok && src != dst) ok = ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+    }
+    if (ok) ok = ck(cudaEventRecord(me.done, s));
+    g_->barrier();
+    for (int h = 0; h < g_->world && ok; ++h)
+      if (h != rank_) ok = ck(cudaStreamWaitEvent(s, g_->slot[h].done, 0));
+    return ok;
+  }
+  LocalGroup *g_;
+  int rank_;
+  std::string err_;
+};
+}  // namespace
+
+LocalGroup *local_group_create(int world, std::string *err) {
+  if (world < 1 || world > 64) { *err = "local group: world must be in [1, 64]"; return nullptr; }
+  LocalGroup *g = new LocalGroup();
+  g->world = world;
+  g->slot.resize(world);
+  for (auto &sl : g->slot) {
+    if (cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming) != cudaSuccess) {
+      *err = std::string("local group: cudaEventCreate: ") + cudaGetErrorString(cudaGetLastError());
+      local_group_destroy(g);
+      return nullptr;
+    }
+  }
+  return g;
+}
+
+void local_group_destroy(LocalGroup *g) {
+  if (!g) return;
+  for (auto &sl : g->slot) {
+    if (sl.ready) cudaEventDestroy(sl.ready);
+    if (sl.done) cudaEventDestroy(sl.done);
+  }
+  delete g;
+}
+
+Transport *local_transport(LocalGroup *g, int rank, std::string *err) {
+  if (!g || rank < 0 || rank >= g->world) { *err = "local group: bad rank"; return nullptr; }
+  return new LocalRank(g, rank);
+}
+
+int local_group_world(const LocalGroup *g) { return g ? g->world : 0; }
 
 }  // namespace ipr

@@ -366,7 +366,8 @@ cudaError_t launch_gemm_crt(const GemmArgs &g, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     uploaded.set();
   }
-  if (!g.oz_a || !g.oz_b || !g.oz_rsig || !g.oz_csig || !g.crt_v || g.M != g.K || g.N != g.K || g.crt_n < 2 ||
+  // M = K = npad; N = npad (G = 1) or the column panel width kp (G > 1: B residues [crt_n][kp][npad])
+  if (!g.oz_a || !g.oz_b || !g.oz_rsig || !g.oz_csig || !g.crt_v || g.M != g.K || g.N > g.K || g.crt_n < 2 ||
       g.crt_n > CRT_MAX)
     return cudaErrorInvalidValue;
   const int64_t np = g.K;

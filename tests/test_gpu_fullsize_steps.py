@@ -102,6 +102,11 @@ def test_headline_phase_step_full_size(mat, case):
     if crt:
         np.testing.assert_array_equal(Chat, Ck)
 
+    def crt_q(X, Y, rows, cols):
+        """the CRT product's quantisation error scale 2^-b (rmax_i colsum_j + rowsum_i cmax_j) (R-28)"""
+        aX, aY = np.abs(X), np.abs(Y)
+        return 2.0 ** -b * (aX.max(axis=1)[rows] * aY.sum(axis=0)[cols] + aX.sum(axis=1)[rows] * aY.max(axis=0)[cols])
+
     def prod_bound(X, Y, rows, cols):
         """|computed - exact| bound of (X Y)[rows, cols] for an FP32-accumulated product."""
         return n * ACC[prec] * (np.abs(X[rows]) @ np.abs(Y[:, cols]))
@@ -109,12 +114,17 @@ def test_headline_phase_step_full_size(mat, case):
     # ---- stage 1: qin(Z_1) = qin(Ahat Chat), sampled columns ----
     cols = np.unique(np.concatenate([rng.integers(0, n, 6), [0, n - 1, min(2048, n - 1)]]))
     if crt:
-        # the oracle's exact CRT product (R-28 definition) element by element: within 2 ulp (the GPU's
-        # sliced-FP64 reconstruction), mostly bit-equal
+        # the oracle's exact CRT product (R-28 definition) element by element.  The GPU's sliced-FP64
+        # reconstruction has an absolute error far below the method's own quantisation error
+        # q_ij = 2^-b (rmax_i colsum_j + rowsum_i cmax_j) (measured <= 0.06 q, tools/crt_rec_diag.py) but
+        # up to ~100 ulp of the tiny off-diagonal elements: bound 2 ulp + q / 8, and >= 99 % bit-equal
         K, J = np.meshgrid(np.arange(n), cols, indexing="ij")
         ref = oracle.gemm_crt_pairs(Ahat, Chat, b, K.ravel(), J.ravel()).reshape(n, len(cols))
+        q = crt_q(Ahat, Chat, np.arange(n)[:, None], cols[None, :])
         d = np.abs(Z1[:, cols] - ref)
-        assert np.all(d <= 2 * np.spacing(np.abs(ref))), (cid, "Z1", float(np.max(d / np.spacing(np.abs(ref)))))
+        lim = 2 * np.spacing(np.abs(ref)) + q / 8
+        assert np.all(d <= lim), (cid, "Z1", float(np.max(d / lim)))
+        assert np.mean(d == 0) >= 0.99
     else:
         ref = Ahat @ Chat[:, cols]
         bnd = prod_bound(Ahat, Chat, np.arange(n), cols)
@@ -130,7 +140,7 @@ def test_headline_phase_step_full_size(mat, case):
     lo, hi = np.minimum(I, J), np.maximum(I, J)
     if crt:   # Z_2[min, max] by the oracle's exact CRT product of Chat and the GPU's qin(Z_1)
         z2 = oracle.gemm_crt_pairs(Chat, Z1, b, lo, hi)
-        b2 = 2 * np.spacing(np.abs(z2))
+        b2 = 2 * np.spacing(np.abs(z2)) + crt_q(Chat, Z1, lo, hi) / 8
     else:     # FP64 dot of the stored operands; the GPU accumulates in FP32
         z2 = np.einsum("ij,ij->i", Chat[lo], Z1[:, hi].T)
         b2 = n * ACC[prec] * np.einsum("ij,ij->i", np.abs(Chat[lo]), np.abs(Z1[:, hi].T))

@@ -1,0 +1,160 @@
+"""The sharded path (PAPER.md:138-141 [Sec. 3.2] "data exchange") executed on the GPU.
+
+One B200 per box, so the G > 1 ranks run as an in-process local group (ipr_testing.h): G contexts on one
+device, each with its own stream and host thread, exchanging panels by stream-ordered device copies
+fenced with events and host barriers -- the engine's column-panel arithmetic, panel-major layouts,
+partial gathers, the CRT splits of gathered operands and the tri form's mirror all-to-all, exactly as
+over NCCL.  The check is P11: every trace record (rho, delta, decision, certificate) and the returned C
+bit-identical to G = 1 for G = 2 and 4 (n = 1024: npad = 1024 for every G, so the tile grid, partial
+slots and reduction order do not depend on G).  With two or more GPUs the same comparison runs over
+NCCL with one process per GPU (skipped on a one-GPU box)."""
+import os
+import threading
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+ipr = pytest.importorskip("paper_1703_02283_b200")
+
+N = 1024
+LOW = dict(plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)
+
+
+def _schedule(name):
+    import bench
+    return bench.schedule(name, N)
+
+
+def _solve_world1(A, p, phases, form):
+    s = ipr.Solver(A, p, phases, 1e-12, form=form)
+    s.iterate(300)
+    tr, out = s.trace(), s.outcome
+    C = s.finalize().cpu().numpy()
+    return out, tr, C
+
+
+def _solve_local(A, p, phases, form, world):
+    grp = ipr.ipr_test_local_group_create(world)
+    res = [None] * world
+    err = [None] * world
+
+    def rank_main(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                s = ipr.Solver(A, p, phases, 1e-12, stream=st, world=world, rank=r, form=form, local_group=grp)
+                s.iterate(300)
+                tr, out = s.trace(), s.outcome
+                C = torch.empty_like(A)
+                s.finalize(C)
+                st.synchronize()
+                res[r] = (out, tr, C.cpu().numpy())
+        except Exception as e:   # noqa: BLE001 -- reported below
+            err[r] = e
+
+    th = [threading.Thread(target=rank_main, args=(r,), daemon=True) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(600)
+    ipr.ipr_test_local_group_destroy(grp)
+    for e in err:
+        if e is not None:
+            raise e
+    return res
+
+
+def _same_trace(a, b):
+    keys = ("phase", "decision", "rho", "delta", "rho_cert", "mant_bits", "digits", "moduli")
+    assert len(a) == len(b)
+    for x, y in zip(a, b):
+        for k in keys:
+            vx, vy = x[k], y[k]
+            assert (vx == vy) or (vx != vx and vy != vy), (k, x["k"], vx, vy)
+
+
+CASES = [
+    ("literal_fp64", "fp64", 2),
+    ("literal_bf16_fp64", "bf16>fp64", 2),
+    ("sym_bf16_fp64", "sym:bf16>fp64/cbf16", 2),
+    ("sym_fp8_crt", "sym:fp8/cfp8>bf16>fp64crt@a/cbf16", 2),
+    ("symtri_headline", "symtri:fp8/cfp8>bf16>fp64crt@a/cbf16", 2),
+    ("symtri_bf16_fp64", "symtri:bf16>tf32>fp64/cbf16", 2),
+    ("sym_p3_crt", "sym:bf16>fp64crt/cbf16", 3),
+]
+
+
+@pytest.fixture(scope="module")
+def A():
+    return torch.from_numpy(synth.spd(N, 2.0, 31)).cuda()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_sharded_bit_identical_to_one_gpu(A, case, world):
+    cid, sched, p = case
+    form, phases = _schedule(sched)
+    out1, tr1, C1 = _solve_world1(A, p, phases, form)
+    assert out1 == ipr.IPR_CONVERGED, (cid, out1)
+    res = _solve_local(A, p, phases, form, world)
+    for r, (out, tr, C) in enumerate(res):
+        assert out == out1, (cid, r)
+        _same_trace(tr, tr1)
+        np.testing.assert_array_equal(C, C1)
+    if "crt" in sched:
+        assert any(t["moduli"] > 0 for t in tr1)
+
+
+def test_local_group_bad_arguments(A):
+    with pytest.raises(ipr.IprError):
+        ipr.ipr_test_local_group_create(0)
+    grp = ipr.ipr_test_local_group_create(2)
+    try:
+        with pytest.raises(ipr.IprError):
+            ipr.Solver(A, 2, [ipr.make_phase("fp64")], world=2, rank=2, local_group=grp)
+    finally:
+        ipr.ipr_test_local_group_destroy(grp)
+
+
+def _nccl_rank(rank, world, port, sched, p, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    obj = [ipr.ipr_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    A = torch.from_numpy(synth.spd(N, 2.0, 31)).cuda()
+    form, phases = _schedule(sched)
+    s = ipr.Solver(A, p, phases, 1e-12, world=world, rank=rank, nccl_unique_id=obj[0], form=form)
+    s.iterate(300)
+    tr = s.trace()
+    C = s.finalize().cpu().numpy()
+    q.put((rank, s.outcome, tr, C))
+    dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs (NCCL)")
+@pytest.mark.parametrize("case", [CASES[0], CASES[4]], ids=["literal_fp64", "symtri_headline"])
+def test_nccl_bit_identical_to_one_gpu(A, case):
+    import torch.multiprocessing as mp
+    cid, sched, p = case
+    form, phases = _schedule(sched)
+    out1, tr1, C1 = _solve_world1(A, p, phases, form)
+    world = min(torch.cuda.device_count(), 4)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_nccl_rank, args=(r, world, port, sched, p, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = [q.get(timeout=600) for _ in procs]
+    for pr in procs:
+        pr.join(60)
+    for rank, out, tr, C in got:
+        assert out == out1
+        _same_trace(tr, tr1)
+        np.testing.assert_array_equal(C, C1)
