@@ -1224,7 +1224,7 @@ cudaError_t launch_gemm_tc(const GemmArgs &a_in, cudaStream_t s) {
       return cudaErrorInvalidValue;
     }
   }
-  if (a.tri && (a.M != a.K || a.col0 + a.N > a.M)) {
+  if (a.tri && a.col0 + a.N > a.M) {   // (K is crt_n npad for the CRT moduli products)
     snprintf(g_tc_err, sizeof g_tc_err, "tcgen05 GEMM: tri needs a square product (or a column panel of one)");
     return cudaErrorInvalidValue;
   }
