@@ -132,8 +132,8 @@ def gemm_peaks():
 
 
 def gemm_count(trace, p):
-    # p GEMMs per evaluated iterate, +1 for every update that followed
-    return sum(p + (1 if t["decision"] == 0 else 0) for t in trace)
+    # p GEMMs per evaluated iterate, +1 for every update that followed, +p per FP64 certification
+    return sum(p + (1 if t["decision"] == 0 else 0) + (p if t["rho_cert"] == t["rho_cert"] else 0) for t in trace)
 
 
 class Clocks:
@@ -175,31 +175,57 @@ class Clocks:
                 "samples": len(rows)}
 
 
-def cpu_baseline(A_np, p, n_gemms, budget_s=15.0):
-    """The oracle (plain C FP64 triple loop) as it stands, timed on a bounded row slab of one
-    GEMM of the same workload on the host cores, extrapolated to the whole solve."""
-    import numpy as np
+def oracle_schedule(name, n):
+    """The oracle's phases for a bench schedule name (same switch / plateau rules as schedule())."""
     import oracle
-    n = A_np.shape[0]
-    X = np.ascontiguousarray(A_np / np.abs(A_np).sum(0).max() ** 2)   # C_0-like operand
-    Z = np.zeros_like(X)
+    form, parts = parse_schedule(name)
+    opr = {"fp64": oracle.FP64, "tf32": oracle.TF32, "bf16": oracle.BF16, "fp16": oracle.FP16, "fp8": oracle.FP8,
+           "int8": oracle.INT8, "fp64oz": oracle.FP64_OZ, "fp64crt": oracle.FP64_CRT}
+    oform = {"literal": oracle.FORM_LITERAL, "symmetric": oracle.FORM_SYMMETRIC, "symmetric_tri": oracle.FORM_SYMMETRIC_TRI,
+             "newton_schulz": oracle.FORM_NEWTON_SCHULZ, "coupled": oracle.FORM_COUPLED}[form]
+    out = []
+    for i, (prec, corr, m) in enumerate(parts):
+        c = opr[corr] if corr != -1 else -1
+        if i == len(parts) - 1:
+            out.append(oracle.phase(opr[prec], mant_bits=m, corr_prec=c))
+        else:
+            mbits = {"bf16": 7, "int8": 7, "fp8": 3, "fp16": 10, "tf32": 10}.get(prec, 52)
+            sw = (2.0 * 2.0 ** -(mbits + 1) * math.sqrt(n)) if form.startswith("symmetric") else 1e-2 * math.sqrt(n)
+            out.append(oracle.phase(opr[prec], mant_bits=m, switch_tol=sw, plateau_ratio=0.7, plateau_arm=0.5,
+                                    max_iters=40, corr_prec=c))
+    return oform, out
+
+
+def oracle_gemms(records, p):
+    """GEMMs of an oracle solve: p per chain, +1 per update (decision continue), +p per certification."""
+    return sum(p + (1 if x["decision"] == 0 else 0) + (p if x["rho_cert"] == x["rho_cert"] else 0) for x in records)
+
+
+def cpu_baseline(schedule_name, p, n_target, gemms_target=None, n_small=1024, seed=5):
+    """The oracle (plain C, FP64 triple loops; FP64_CRT products as exact 128-bit integer sums) as it
+    stands, timed on the host cores on ONE REAL SOLVE: the same schedule on the kappa = 2 twin at order
+    n_small (measured), then scaled to n_target by n^3 and by the GEMM count (the target's, when the GPU
+    run supplies it, else the oracle's own at n_small) -- the scaling is labelled as extrapolation."""
+    import oracle
+    import synth
+    A_s = synth.spd(n_small, 2.0, seed)
+    oform, ph = oracle_schedule(schedule_name, n_small)
+    t0 = time.perf_counter()
+    r = oracle.solve(A_s, p, ph, 1e-12, 300, form=oform)
+    t = time.perf_counter() - t0
+    g_small = oracle_gemms(r.records, p)
+    g_t = gemms_target if gemms_target else g_small
+    scale = (n_target / n_small) ** 3 * g_t / g_small
+    iters = [sum(1 for x in r.records if x["phase"] == i) for i in range(len(ph))]
+    cert = [x["rho_cert"] for x in r.records if x["rho_cert"] == x["rho_cert"]]
     cores = len(os.sched_getaffinity(0))
-    r = max(cores, 8)
-    t0 = time.perf_counter()
-    oracle.gemm_rows(X, A_np, Z, 0, r)
-    t1 = time.perf_counter()
-    per_row = (t1 - t0) / r
-    r2 = int(min(n, max(r, budget_s / max(per_row, 1e-9))))
-    t0 = time.perf_counter()
-    oracle.gemm_rows(X, A_np, Z, 0, r2)
-    t1 = time.perf_counter()
-    per_row = (t1 - t0) / r2
-    t_gemm = per_row * n
-    return {"value": t_gemm * n_gemms, "unit": "s", "cores": cores, "kind": "oracle",
-            "sample": f"oracle orc_gemm_rows: {r2} of {n} rows of one FP64 GEMM (n={n}) in {t1 - t0:.1f} s "
-                      f"({2.0 * r2 * n * n / (t1 - t0) / 1e9:.1f} GFLOP/s); extrapolated x{n}/{r2} rows "
-                      f"x {n_gemms} GEMMs of the solve (epilogues O(n^2), ignored)",
-            "extrapolated": True}
+    return {"value": t * scale, "unit": "s", "cores": cores, "kind": "oracle",
+            "sample": f"one full oracle solve of {schedule_name} on the kappa=2 twin at n={n_small} (seed {seed}): "
+                      f"{oracle.OUTCOME_NAMES[r.outcome]}, iterations {iters}, certified rho "
+                      f"{cert[-1] if cert else float('nan'):.3e}, {g_small} GEMMs in {t:.1f} s on {cores} threads "
+                      f"(measured); value = that x (n={n_target}/{n_small})^3 x ({g_t} / {g_small} GEMMs) (extrapolated"
+                      f"{', GEMM count of the GPU trajectory at n=' + str(n_target) if gemms_target else ', the oracle GEMM count at n_small'})",
+            "measured_solve_s": t, "measured_n": n_small, "measured_iters": iters, "extrapolated": True}
 
 
 def main():
@@ -220,29 +246,14 @@ def main():
               "parallelism": f"1x{args.gpus} column panels" if args.gpus > 1 else "single GPU"}
 
     if args.impl == "reference":
-        # Reference arm = the oracle as it stands on the host cores (rank 0 only).
+        # Reference arm = the oracle as it stands on the host cores (rank 0 only): every step one real oracle
+        # solve of the same schedule at n = 512 (a bounded sample), scaled to the workload's n by n^3 at the
+        # oracle's own GEMM count (see cpu_baseline)
         if rank != 0:
             return
-        A_np = synth.spd(n, kappa, seed) if n <= 2048 else None
-        if A_np is None:
-            rng = np.random.default_rng(seed)
-            A_np = None
-        import oracle
-        if A_np is None:
-            # a CPU QR of 8192^2 takes minutes; the oracle's GEMM cost does not depend on values,
-            # so the bounded timing sample runs on a symmetric matrix of the same size and scale.
-            rng = np.random.default_rng(seed)
-            G = rng.standard_normal((n, n)) / math.sqrt(n)
-            A_np = np.ascontiguousarray((G + G.T) * 0.5 + np.eye(n) * 0.75)
-        # the oracle's FP64 work for the arm's schedule: the symmetric forms evaluate p GEMMs per chain
-        # plus the W GEMM per update (the oracle computes the full C A C even for `symtri`) and p
-        # certification GEMMs; 28 iterations = the GPU run of the default schedule (17 + 3 + 8,
-        # profiles/r01i_bench_line.json).  The literal form: 20 chains / 19 updates.
-        form_ref, _ = parse_schedule(args.schedule)
-        n_gemms = 28 * (p + 1) + p if form_ref.startswith("symmetric") else 20 * p + 19
         vals = []
         for i in range(args.warmup + args.steps):
-            cb = cpu_baseline(A_np, p, n_gemms, budget_s=4.0)
+            cb = cpu_baseline(args.schedule, p, n, None, n_small=512)
             if i >= args.warmup:
                 vals.append(cb["value"])
         v = float(np.mean(vals))
@@ -484,7 +495,7 @@ def main():
     cb = None
     if world == 1:
         try:
-            cb = cpu_baseline(A.cpu().numpy(), p, gemm_count(tr, p))
+            cb = cpu_baseline(args.schedule, p, n, gemm_count(tr, p), n_small=1024)
         except Exception as ex:  # never fail the bench line on the CPU leg
             cb = {"value": None, "unit": "s", "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
     line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,

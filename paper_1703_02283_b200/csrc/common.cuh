@@ -134,6 +134,12 @@ struct GemmArgs {
   // mout = tout, ldm = ldt (the launchers fill them in when mout is null); a G > 1 rank points it at the
   // packed [G][kp][kp] send buffer of the mirror exchange (ldm = kp)
   void *mout; int64_t ldm;
+  // 2-D grid (P_r x P_c ranks, literal form): the output block's first global row.  Epilogues use global
+  // rows (diagonal, masking, partial slots); the engine offsets the output pointers by -row0 rows.
+  int64_t row0;
+  // B operand panels (b_pstride != 0): K-panel length of B (0: = a_kp) -- the 2-D grid's gathered
+  // T column panel [P_r][kp][mr] has b_kp = mr
+  int64_t b_kp;
 };
 
 // ------------------------------------------------------------------------------------

@@ -28,12 +28,30 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "nccl_dl.h"
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing unless a tool (nsys) injects
 
 using namespace ipr;
 
 namespace {
 
 thread_local std::string t_err;
+
+// NVTX range per hot-path step (chain / update / certificate / phase entry / exchanges), named by format
+struct Nvtx {
+  explicit Nvtx(const char *fmt, ...) {
+    char b[96];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(b, sizeof b, fmt, ap);
+    va_end(ap);
+    nvtxRangePushA(b);
+  }
+  ~Nvtx() { nvtxRangePop(); }
+};
+const char *pname(int prec) {
+  static const char *nm[] = {"fp64", "tf32", "bf16", "fp16", "fp8", "int8", "fp64oz", "fp64crt"};
+  return prec >= 0 && prec < 8 ? nm[prec] : "?";
+}
 
 struct PhaseC {
   int prec, m, rtz, cont64;
@@ -48,6 +66,13 @@ struct PhaseC {
 struct ipr_ctx {
   int64_t n = 0, lda = 0, npad = 0, kp = 0, col0 = 0;
   int world = 1, rank = 0;
+  // grid: grows x gcols ranks, this rank at (grow, gcol); it owns rows [row0, row0 + mr)
+  // and columns [col0, col0 + kp).  The default 1 x world grid: mr = npad, row0 = 0, gcol = rank.
+  int grows = 1, gcols = 1, grow = 0, gcol = 0;
+  int64_t mr = 0, row0 = 0;
+  Transport *rowt = nullptr, *colt = nullptr;   // 2-D grid: the rank's grid row / grid column
+  void *Tcol = nullptr;                 // 2-D grid: gathered T column panel [grows][kp][mr] (B operand)
+  double *partg = nullptr;              // 2-D grid: every rank's full partial array [world][npart]
   cudaStream_t st = nullptr;
   const double *A = nullptr;
   double norms[4] = {0, 0, 0, 0};
@@ -223,24 +248,30 @@ ipr_status dalloc(ipr_ctx *c, T **p, size_t bytes) {
   return IPR_OK;
 }
 
-inline size_t slot_bytes(const ipr_ctx *c) { return (size_t)(c->npad * c->kp) * 8; }
+// elements of this rank's block (1 x G: the column panel npad x kp; 2-D: mr x kp)
+inline int64_t blk(const ipr_ctx *c) { return c->mr * c->kp; }
+inline size_t slot_bytes(const ipr_ctx *c) { return (size_t)blk(c) * 8; }
 
-// container of iterate buffer i in the current phase (FP64 phases alias the operand slot)
+// container of iterate buffer i in the current phase (FP64 phases alias the operand slot).  The operand
+// Chat is replicated along the rank's grid row: [gcols][mr][kp], this rank's block at slot gcol.
 void *cont_ptr(ipr_ctx *c, int i, const PhaseC &P) {
-  if (is_f64(P.prec)) return (char *)c->chat[i] + (size_t)c->rank * slot_bytes(c);
+  if (is_f64(P.prec)) return (char *)c->chat[i] + (size_t)c->gcol * slot_bytes(c);
   return c->cont[i];
 }
 void *chat_slot(ipr_ctx *c, int i, int prec) {
-  return (char *)c->chat[i] + (size_t)c->rank * (size_t)(c->npad * c->kp) * elt_size(prec);
+  return (char *)c->chat[i] + (size_t)c->gcol * (size_t)blk(c) * elt_size(prec);
 }
+// the transport of the Chat / W / partial-panel exchanges: the grid row (all ranks for 1 x G)
+inline Transport *row_transport(ipr_ctx *c) { return c->rowt ? c->rowt : c->comm; }
 
 ipr_status gather_chat(ipr_ctx *c, int i, int prec) {
-  if (c->world == 1) return IPR_OK;
-  // packed panel-major layout for this precision: rank r's slot at r * npad * kp * esz
-  const size_t bytes = (size_t)(c->npad * c->kp) * elt_size(prec);
+  if (c->gcols == 1) return IPR_OK;
+  // packed panel-major layout for this precision: grid-row slot r at r * mr * kp * esz
+  const size_t bytes = (size_t)blk(c) * elt_size(prec);
   char *base = (char *)c->chat[i];
-  if (!c->comm->allgather(base + c->rank * bytes, base, bytes, c->st))
-    return fail(c, IPR_E_NCCL, "ncclAllGather(Chat) failed: %s", c->comm->last_error());
+  Transport *t = row_transport(c);
+  if (!t->allgather(base + c->gcol * bytes, base, bytes, c->st))
+    return fail(c, IPR_E_NCCL, "ncclAllGather(Chat) failed: %s", t->last_error());
   return IPR_OK;
 }
 
@@ -271,14 +302,26 @@ ipr_status join_gather(ipr_ctx *c) {
 void chat_view(ipr_ctx *c, int i, int prec, const void **A, int64_t *akp, int64_t *pstride) {
   *A = c->chat[i];
   *akp = c->kp;
-  *pstride = (c->world == 1) ? c->npad * c->kp : c->npad * c->kp;
+  *pstride = blk(c);
   (void)prec;
 }
 
-ipr_status gather_partials(ipr_ctx *c, double *part, int64_t per_rank) {
+// per-tile partials: every GEMM writes its tiles' sums at GLOBAL slots [tile_n][tile_m], so the reduction
+// order is the same for any decomposition.  1 x G: a rank's tiles are one contiguous chunk (per_rank
+// slots at rank * per_rank).  2-D grid: a rank's slots are scattered -- every rank's whole array is
+// gathered and each slot taken from its owner (tile sizes tmsz x tnsz of the kernel that wrote them).
+ipr_status gather_partials(ipr_ctx *c, double *part, int64_t per_rank, int tmsz = 0, int tnsz = 0) {
   if (c->world == 1) return IPR_OK;
-  if (!c->comm->allgather(part + c->rank * per_rank, part, (size_t)per_rank * 8, c->st))
-    return fail(c, IPR_E_NCCL, "ncclAllGather(partials) failed: %s", c->comm->last_error());
+  if (c->grows == 1) {
+    if (!c->comm->allgather(part + c->rank * per_rank, part, (size_t)per_rank * 8, c->st))
+      return fail(c, IPR_E_NCCL, "ncclAllGather(partials) failed: %s", c->comm->last_error());
+    return IPR_OK;
+  }
+  if (!tmsz || !tnsz) return fail(c, IPR_E_UNSUPPORTED, "2-D grid: partials without tile sizes");
+  const int64_t total = per_rank * c->gcols;   // tiles_n_total * tiles_m
+  if (!c->comm->allgather(part, c->partg, (size_t)total * 8, c->st))
+    return fail(c, IPR_E_NCCL, "all-gather(2-D partials) failed: %s", c->comm->last_error());
+  CK(launch_select_partials(c->partg, total, c->npad / tmsz, tmsz, tnsz, c->mr, c->kp, c->gcols, part, c->st));
   return IPR_OK;
 }
 ipr_status gather_pmax(ipr_ctx *c, float *pm, int64_t per_rank) {
@@ -300,7 +343,7 @@ cudaError_t run_gemm(ipr_ctx *c, GemmArgs &g) {
 GemmArgs base_args(ipr_ctx *c, int prec, const void *Bop) {
   GemmArgs g;
   memset(&g, 0, sizeof g);
-  g.M = c->npad; g.N = c->kp; g.K = c->npad; g.n = c->n; g.col0 = c->col0;
+  g.M = c->mr; g.N = c->kp; g.K = c->npad; g.n = c->n; g.col0 = c->col0; g.row0 = c->row0;
   g.B = Bop; g.ldb = c->npad; g.prec = prec; g.tprec = prec;
   g.tiles_m = tiles_m(c, prec);
   g.p = c->p;
@@ -323,7 +366,7 @@ ipr_status stage_a(ipr_ctx *c, const PhaseC &P, void *dst, int *sig_dst) {
 // container cont(i) -> operand Chat(i) (+ FP16 sigma), then all-gather (a8 / a9)
 // premax: the per-rank max |C| is already in pmax[rank] (k_sym_update's amax), one partial per rank
 ipr_status make_operand(ipr_ctx *c, int i, const PhaseC &P, bool premax = false, bool async = false) {
-  const int64_t cnt = c->npad * c->kp;
+  const int64_t cnt = blk(c);
   if (!is_f64(P.prec)) {
     const int *sig = nullptr;
     if (is_scaled(P.prec)) {
@@ -344,8 +387,8 @@ ipr_status save_best(ipr_ctx *c) {
   if (c->best_loc == 0 || c->best_loc == 1) {
     const PhaseC &P = c->ph[c->phase];
     (void)P;
-    const int64_t cnt = c->npad * c->kp;
-    const void *src = c->best_cont64 ? (const void *)((char *)c->chat[c->best_loc] + (size_t)c->rank * slot_bytes(c))
+    const int64_t cnt = blk(c);
+    const void *src = c->best_cont64 ? (const void *)((char *)c->chat[c->best_loc] + (size_t)c->gcol * slot_bytes(c))
                                      : c->cont[c->best_loc];
     // FP64 phases keep the iterate in the operand slot; low phases in cont[]
     CK(launch_cont_to_f64(src, c->best_cont64, cnt, c->best, c->st));
@@ -463,6 +506,7 @@ ipr_status make_corr_operand(ipr_ctx *c, int i, const PhaseC &P) {
 
 ipr_status begin_phase(ipr_ctx *c, bool first) {
   const PhaseC &P = c->ph[c->phase];
+  Nvtx nv("phase %d %s", c->phase, pname(P.prec));
   CKS(stage_a(c, P, c->Aop, c->dsig + 0));
   if (c->form != IPR_FORM_LITERAL && c->world > 1) {   // full row-major Ahat (A operand)
     CK(launch_stage_a(c->A, c->lda, c->n, c->npad, 0, c->npad, P.prec, P.cont64, P.m, P.rtz,
@@ -474,12 +518,12 @@ ipr_status begin_phase(ipr_ctx *c, bool first) {
   c->m_of_cur = m_in;
   c->ph_r1 = NAN; c->ph_r2 = NAN;
   if (first) {
-    CK(launch_c0(c->A, c->lda, c->n, c->npad, c->col0, c->kp, c->norms[3], P.cont64, m_in, P.rtz,
+    CK(launch_c0(c->A, c->lda, c->n, c->mr, c->row0, c->col0, c->kp, c->norms[3], P.cont64, m_in, P.rtz,
                  cont_ptr(c, c->cur, P), c->st));
   } else {
     CKS(save_best(c));
     if (c->best_loc == 2) {
-      CK(launch_f64_to_cont(c->best, c->npad * c->kp, P.cont64, m_in, P.rtz, cont_ptr(c, c->cur, P), c->st));
+      CK(launch_f64_to_cont(c->best, blk(c), P.cont64, m_in, P.rtz, cont_ptr(c, c->cur, P), c->st));
     }
   }
   CKS(make_operand(c, c->cur, P));
@@ -515,6 +559,7 @@ ipr_status make_xt(ipr_ctx *c, int i, const PhaseC &P) {
 // strictly-lower elements of its columns into its K-major panel T (the same values, so every element
 // is bit-identical to G = 1 -- DESIGN.md section 7).
 ipr_status mirror_exchange(ipr_ctx *c, void *T, int esz) {
+  Nvtx nv("tri mirror all-to-all");
   const size_t blk = (size_t)(c->kp * c->kp) * esz;
   if (!c->comm->alltoall(c->msend, c->mrecv, blk, c->st))
     return fail(c, IPR_E_NCCL, "all-to-all(tri mirror) failed: %s", c->comm->last_error());
@@ -525,6 +570,7 @@ ipr_status mirror_exchange(ipr_ctx *c, void *T, int esz) {
 // ---- one chain: p GEMMs + fused residual; returns rho (host sync) ----
 ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
   const PhaseC &P = c->ph[c->phase];
+  Nvtx nv("chain k=%zu %s", c->trace.size(), pname(P.prec));
   const int prec = P.prec;
   const void *X = c->Aop;
   const bool scaled = is_scaled(prec);
@@ -663,24 +709,33 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
   for (int j = 1; c->form == IPR_FORM_LITERAL && j <= c->p; ++j) {
     GemmArgs g = base_args(c, prec, X);
     chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
+    if (j > 1 && c->grows > 1) {   // 2-D grid: B = the gathered T_{j-1} column panel [grows][kp][mr]
+      g.ldb = c->mr; g.b_kp = c->mr; g.b_pstride = c->kp * c->mr;
+    }
     if (scaled) { g.sigA = c->dsig + 1 + c->cur; g.sigB = sigX; }
     g.mode = (scaled ? EPI_TSCRATCH : EPI_STORE_T) | (j == c->p ? EPI_RESID : 0);
     g.tout = scaled ? (void *)c->tscr : c->T[j & 1];
-    g.ldt = c->npad;
+    // the rank's output block is rows [row0, row0 + mr): K-major [kp][mr]; epilogues index global rows
+    g.ldt = c->mr;
+    g.tout = (char *)g.tout - c->row0 * elt_size(scaled ? IPR_TF32 : g.tprec);
     g.part = part;
     if (scaled) g.pmax = c->pmax;
     CK(run_gemm(c, g));
+    if (c->grows > 1) {            // 2-D grid: the T_j column panel along the grid column (SUMMA-like)
+      if (!c->colt->allgather(c->T[j & 1], c->Tcol, (size_t)blk(c) * elt_size(g.tprec), c->st))
+        return fail(c, IPR_E_NCCL, "all-gather(T column panel) failed: %s", c->colt->last_error());
+    }
     if (scaled) {
       CKS(gather_pmax(c, c->pmax, tn_loc * tm));
       CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 3 + (j & 1), prec, c->st));
       CK(launch_scale_op(c->tscr, c->kp * c->npad, c->dsig + 3 + (j & 1), prec, c->T[j & 1], c->st));
       sigX = c->dsig + 3 + (j & 1);
     }
-    X = c->T[j & 1];
+    X = c->grows > 1 ? c->Tcol : c->T[j & 1];
   }
   CK(cudaEventRecord(c->ev[1], c->st));
   if (!coupled_cached) {
-    CKS(gather_partials(c, part, tn_loc * tm));
+    CKS(gather_partials(c, part, tn_loc * tm, (int)gemm_tile_m(prec), (int)gemm_tile_n(prec)));
     CK(launch_reduce_sum(part, tiles_n_total(c, prec) * tm, c->dscal + 0, c->st));
   }
   CK(cudaMemcpyAsync(c->hscal, c->dscal, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
@@ -708,6 +763,7 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
 // ---- GEMM p+1 with the fused update (a6) ----
 ipr_status update(ipr_ctx *c) {
   const PhaseC &P = c->ph[c->phase];
+  Nvtx nv("update %s", pname(P.prec));
   const int prec = P.prec, nx = 1 - c->cur;
   // the update overwrites buffer nx: keep the best iterate if it lives there
   if (c->best_loc == nx) CKS(save_best(c));
@@ -715,14 +771,17 @@ ipr_status update(ipr_ctx *c) {
   const bool ns = c->form == IPR_FORM_NEWTON_SCHULZ;
   // literal: P = Chat qin(T_p); Newton-Schulz: X_{k+1} = Xhat What (What in T[1])
   const int tb = ns ? 1 : (c->p & 1);
-  GemmArgs g = base_args(c, prec, c->T[tb]);
+  GemmArgs g = base_args(c, prec, c->grows > 1 ? c->Tcol : c->T[tb]);
   chat_view(c, c->cur, prec, &g.A, &g.a_kp, &g.a_pstride);
+  if (c->grows > 1) { g.ldb = c->mr; g.b_kp = c->mr; g.b_pstride = c->kp * c->mr; }
   if (is_scaled(prec)) { g.sigA = c->dsig + 1 + c->cur; g.sigB = c->dsig + 3 + tb; g.pmax = c->pmax; }
   g.mode = ns ? EPI_NSUPDATE : EPI_UPDATE;
-  g.cold = cont_ptr(c, c->cur, P);
-  g.cnew = cont_ptr(c, nx, P);
+  // the rank's block rows [row0, row0 + mr) (global-row epilogue: pointers offset by -row0 rows)
+  const size_t cb = P.cont64 ? 8 : 4;
+  g.cold = (char *)cont_ptr(c, c->cur, P) - (size_t)c->row0 * c->kp * cb;
+  g.cnew = (char *)cont_ptr(c, nx, P) - (size_t)c->row0 * c->kp * cb;
   g.ldc = c->kp;
-  g.chat_new = is_f64(prec) ? nullptr : chat_slot(c, nx, prec);
+  g.chat_new = is_f64(prec) ? nullptr : (char *)chat_slot(c, nx, prec) - (size_t)c->row0 * c->kp * elt_size(prec);
   g.ldh = c->kp;
   g.m = P.m; g.rtz = P.rtz; g.cont64 = P.cont64;
   g.part = c->part;
@@ -730,12 +789,12 @@ ipr_status update(ipr_ctx *c) {
   CK(run_gemm(c, g));
   CK(cudaEventRecord(c->ev[3], c->st));
   c->upd_timed = true;
-  CKS(gather_partials(c, c->part, tn_loc * tm));
+  CKS(gather_partials(c, c->part, tn_loc * tm, (int)gemm_tile_m(prec), (int)gemm_tile_n(prec)));
   CK(launch_reduce_sum(c->part, tiles_n_total(c, prec) * tm, c->dscal + 1, c->st));
   if (is_scaled(prec)) {
     CKS(gather_pmax(c, c->pmax, tn_loc * tm));
     CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 1 + nx, prec, c->st));
-    CK(launch_make_operand(c->cont[nx], 0, c->npad * c->kp, prec, c->dsig + 1 + nx, chat_slot(c, nx, prec), c->st));
+    CK(launch_make_operand(c->cont[nx], 0, blk(c), prec, c->dsig + 1 + nx, chat_slot(c, nx, prec), c->st));
   }
   CKS(gather_chat(c, nx, prec));
   if (ns) CKS(make_xt(c, nx, P));
@@ -746,6 +805,7 @@ ipr_status update(ipr_ctx *c) {
 // ---- symmetric form (NEXT-2): W = qc(C) Rhat, then C_{k+1} = q_m(C + (W + W^T)/(2p)) ----
 ipr_status update_sym(ipr_ctx *c) {
   const PhaseC &P = c->ph[c->phase];
+  Nvtx nv("update sym corr=%s", pname(P.corr));
   const int nx = 1 - c->cur;
   if (c->best_loc == nx) CKS(save_best(c));
   if (fused_sym_ok(c, P)) {
@@ -901,6 +961,8 @@ void free_ctx(ipr_ctx *c) {
   for (auto &e : c->kev) if (e) cudaEventDestroy(e);
   if (c->cst) { cudaStreamSynchronize(c->cst); cudaStreamDestroy(c->cst); }
   for (auto &e : c->gev) if (e) cudaEventDestroy(e);
+  delete c->rowt;
+  delete c->colt;
   delete c->comm;
   delete c;
 }
@@ -944,6 +1006,8 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       // outside a CRT product; every product re-splits its B operand)
       {(void **)&c->full64, cr ? 0 : full * 8}, {&c->Acert, cr ? 0 : panel * 8},
       {&c->chat_rm, (cr && c->world > 1) ? full * 8 : 0},
+      {&c->Tcol, c->grows > 1 ? panel * 8 : 0},
+      {(void **)&c->partg, c->grows > 1 ? (size_t)c->world * c->npart * 8 : 0},
       {&c->msend, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0},
       {&c->mrecv, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0}};
   size_t total = 0;
@@ -973,9 +1037,10 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
 
 // FP64 full matrix (panel-major [G][npad][kp]) of a local FP64 panel -> full64
 ipr_status gather_f64(ipr_ctx *c, const double *local) {
-  double *slot = c->full64 + (size_t)c->rank * c->npad * c->kp;
-  if (local != slot) CK(cudaMemcpyAsync(slot, local, (size_t)(c->npad * c->kp) * 8, cudaMemcpyDeviceToDevice, c->st));
-  if (c->world > 1 && !c->comm->allgather(slot, c->full64, (size_t)(c->npad * c->kp) * 8, c->st))
+  // block-major [world][mr][kp] (1 x G: panel-major [G][npad][kp])
+  double *slot = c->full64 + (size_t)c->rank * blk(c);
+  if (local != slot) CK(cudaMemcpyAsync(slot, local, (size_t)blk(c) * 8, cudaMemcpyDeviceToDevice, c->st));
+  if (c->world > 1 && !c->comm->allgather(slot, c->full64, (size_t)blk(c) * 8, c->st))
     return fail(c, IPR_E_NCCL, "ncclAllGather(C) failed: %s", c->comm->last_error());
   return IPR_OK;
 }
@@ -1015,15 +1080,19 @@ static ipr_status init_ctx(ipr_ctx **out, int64_t n, const double *A_dev, int64_
                                      (long long)n, (long long)lda);
   if (n > 65535) return fail(c, IPR_E_UNSUPPORTED, "ipr_init: n > 65535 not supported");
   if (world < 1 || rank < 0 || rank >= world) return fail(c, IPR_E_INVALID_ARG, "ipr_init: bad world/rank");
-  if (grid_rows != 1 || grid_cols != world)
-    return fail(c, IPR_E_UNSUPPORTED, "ipr_init: only 1 x world column-panel grids are implemented");
+  if (grid_rows < 1 || grid_cols < 1 || grid_rows * grid_cols != world)
+    return fail(c, IPR_E_INVALID_ARG, "ipr_init: grid_rows x grid_cols must equal world (%d x %d vs %d)", grid_rows,
+                grid_cols, world);
   if (world > 1 && !nccl_unique_id && !lg) return fail(c, IPR_E_INVALID_ARG, "ipr_init: world > 1 needs an NCCL id");
   c = new ipr_ctx();
   c->n = n; c->lda = lda; c->A = A_dev; c->world = world; c->rank = rank;
   c->st = (cudaStream_t)cuda_stream;
-  c->npad = padded_order(n, world);
-  c->kp = c->npad / world;
-  c->col0 = (int64_t)rank * c->kp;
+  c->npad = padded_order(n, world);          // a multiple of 256 grid_rows and of 256 grid_cols
+  c->grows = grid_rows; c->gcols = grid_cols;
+  c->grow = rank / grid_cols; c->gcol = rank % grid_cols;
+  c->mr = c->npad / grid_rows; c->kp = c->npad / grid_cols;
+  c->row0 = (int64_t)c->grow * c->mr;
+  c->col0 = (int64_t)c->gcol * c->kp;
   ipr_status s;
 #define TRY(x) do { s = (x); if (s != IPR_OK) { std::string m = c->err; free_ctx(c); t_err = m; return s; } } while (0)
 #define TRYC(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) { TRY(fail(c, IPR_E_CUDA, "%s: %s", #x, cudaGetErrorString(_e))); } } while (0)
@@ -1071,6 +1140,12 @@ static ipr_status init_ctx(ipr_ctx **out, int64_t n, const double *A_dev, int64_
       NcclComm *nc = new NcclComm();
       c->comm = nc;
       if (!nc->init(world, rank, nccl_unique_id, &e)) TRY(fail(c, IPR_E_NCCL, "%s", e.c_str()));
+    }
+    if (grid_rows > 1) {   // 2-D grid: the rank's grid row (Chat panels) and grid column (T panels)
+      c->rowt = c->comm->split(c->grow, c->gcol, &e);
+      if (!c->rowt) TRY(fail(c, IPR_E_NCCL, "grid row split: %s", e.c_str()));
+      c->colt = c->comm->split(c->gcol, c->grow, &e);
+      if (!c->colt) TRY(fail(c, IPR_E_NCCL, "grid column split: %s", e.c_str()));
     }
     TRYC(cudaStreamCreateWithFlags(&c->cst, cudaStreamNonBlocking));
     for (auto &ev : c->gev) TRYC(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1199,6 +1274,13 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
         return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ / IPR_FP64_CRT phases need a symmetric form");
       if (P.prec == IPR_FP64_OZ && c->world != 1)
         return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ phases are single-GPU (IPR_FP64_CRT shards)");
+    }
+    if (c->grows > 1) {   // the 2-D grid option: Eq. (1) as printed, unscaled tensor-core / DMMA formats
+      if (c->form != IPR_FORM_LITERAL)
+        return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: 2-D grids (grid_rows > 1) run the literal form only");
+      for (auto &P : c->ph)
+        if (P.prec != IPR_FP64 && P.prec != IPR_TF32 && P.prec != IPR_BF16)
+          return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: 2-D grids take FP64 / TF32 / BF16 phases");
     }
     if (is_sym(c)) {
       if (c->p < 2) return fail(c, IPR_E_INVALID_ARG, "ipr_iterate: the symmetric form needs p >= 2 (p = 1: Newton-Schulz)");
@@ -1338,7 +1420,7 @@ ipr_status ipr_get_norms(ipr_ctx *c, double *out4) {
 }
 
 static ipr_status copy_iterate(ipr_ctx *c, int which, double *dst, int64_t ldc) {
-  const int64_t cnt = c->npad * c->kp;
+  const int64_t cnt = blk(c);
   double *slot = c->full64 + (size_t)c->rank * cnt;
   if (which == 0) {
     const PhaseC &P = c->ph[c->phase];
@@ -1349,7 +1431,7 @@ static ipr_status copy_iterate(ipr_ctx *c, int which, double *dst, int64_t ldc) 
     CK(cudaMemcpyAsync(slot, c->best, (size_t)cnt * 8, cudaMemcpyDeviceToDevice, c->st));
   }
   CKS(gather_f64(c, slot));
-  if (dst) CK(launch_copy_out(c->full64, c->npad, c->kp, c->n, dst, ldc, c->st));
+  if (dst) CK(launch_copy_out_blocks(c->full64, c->mr, c->kp, c->gcols, c->n, dst, ldc, c->st));
   CK(cudaStreamSynchronize(c->st));
   return IPR_OK;
 }
@@ -1391,6 +1473,7 @@ static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho) {
 // FP64 DMMA pipe: T_1 = C A, T_j = C T_{j-1}; the last GEMM keeps only its residual partials, so T[p & 1]
 // is not written for p = 2 (reading R-3).  Deterministic: the same iterate gives the same bits.
 static ipr_status certify_full64(ipr_ctx *c, double *rho) {
+  Nvtx nv("certify fp64 dmma");
   PhaseC P64{IPR_FP64, 52, 0, 1, 0, 0, 0, 0};
   CKS(stage_a(c, P64, c->Acert, c->dsig + 0));
   const void *X = c->Acert;
@@ -1429,6 +1512,8 @@ ipr_status ipr_residual(ipr_ctx *c, int certify, double *rho) {
   if (!c || !rho) return fail(c, IPR_E_INVALID_ARG, "ipr_residual: null pointer");
   if (!c->started || c->trace.empty()) return fail(c, IPR_E_STATE, "ipr_residual: no iterate evaluated yet");
   if (!certify) { *rho = c->last_rho; return IPR_OK; }
+  if (c->grows > 1)   // the literal form's FP64 in-chain residual is already the DMMA literal chain
+    return fail(c, IPR_E_UNSUPPORTED, "ipr_residual: certify = 1 on a 2-D grid (use the FP64 phase's in-chain rho)");
   CKS(certify_best(c, rho));
   // the certification chain reuses the T buffers: restore the transposed operand it clobbered
   if (c->world > 1 && c->form != IPR_FORM_LITERAL && !c->done) CKS(make_xt(c, c->cur, c->ph[c->phase]));

@@ -60,12 +60,13 @@ __global__ void __launch_bounds__(DM_NT, 2) k_gemm_dmma(const GemmArgs g) {
   }
   const int64_t m0 = (int64_t)tm * DM_BM, n0 = (int64_t)tn * DM_BN;
   if (g.tri && m0 > g.col0 + n0 + DM_BN - 1) {          // wholly below the diagonal (tri form)
-    if (tid == 0 && (g.mode & EPI_RESID)) g.part[((g.col0 + n0) / DM_BN) * g.tiles_m + tm] = 0.0;
+    if (tid == 0 && (g.mode & EPI_RESID)) g.part[((g.col0 + n0) / DM_BN) * g.tiles_m + g.row0 / DM_BM + tm] = 0.0;
     return;
   }
   const double *A = (const double *)g.A, *B = (const double *)g.B;
   const int nkb = (int)(g.K / DM_BK);
   const int kb_per_panel = (int)(g.a_kp / DM_BK);
+  const int kb_per_bpanel = (int)((g.b_kp ? g.b_kp : g.a_kp) / DM_BK);   // paneled B (2-D grid T panels)
 
   auto sA = [&](int s) { return smem + s * DM_STAGE_DBL; };
   auto sB = [&](int s) { return smem + s * DM_STAGE_DBL + DM_BM * DM_BK; };
@@ -73,7 +74,8 @@ __global__ void __launch_bounds__(DM_NT, 2) k_gemm_dmma(const GemmArgs g) {
   auto load_stage = [&](int s, int kb) {
     const int panel = kb / kb_per_panel, kin = (kb - panel * kb_per_panel) * DM_BK;
     const double *Ap = A + (int64_t)panel * g.a_pstride + kin + m0 * g.a_kp;
-    const double *Bp = B + n0 * g.ldb + (int64_t)kb * DM_BK;
+    const int bpanel = g.b_pstride ? kb / kb_per_bpanel : 0;
+    const double *Bp = B + (int64_t)bpanel * g.b_pstride + n0 * g.ldb + (int64_t)(kb - bpanel * kb_per_bpanel) * DM_BK;
     double *a = sA(s), *b = sB(s);
     #pragma unroll
     for (int i = 0; i < 8; ++i) {            // A: 128 rows x 8 chunks
@@ -145,14 +147,14 @@ __global__ void __launch_bounds__(DM_NT, 2) k_gemm_dmma(const GemmArgs g) {
     for (int ni = 0; ni < 4; ++ni)
       #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        const int64_t row = m0 + wm * 64 + mi * 8 + fr;
+        const int64_t row = g.row0 + m0 + wm * 64 + mi * 8 + fr;   // global row (2-D grid: row0)
         const int64_t col = n0 + wn * 32 + ni * 8 + fk * 2 + e;
         epi_element<MODE>(g, row, col, __dmul_rn(acc[mi][ni][e], scale), ea);
       }
   __shared__ double red[DM_NT / 32];
   __shared__ float redf[DM_NT / 32];
   const int mode = MODE >= 0 ? MODE : g.mode;
-  const int64_t tile = ((g.col0 + n0) / DM_BN) * g.tiles_m + tm;
+  const int64_t tile = ((g.col0 + n0) / DM_BN) * g.tiles_m + g.row0 / DM_BM + tm;
   if (mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE)) {
     const double s = block_sum_det<DM_NT>((mode & EPI_RESID) ? ea.r2 : ea.d2, red);
     if (tid == 0) g.part[tile] = s;

@@ -535,18 +535,22 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
     }
   }
   if (mode & EPI_WSTORE) {
-    // symmetric form: W row segment [row][col .. col+31] as the exact FP32 accumulator values
-    // (scale is 1: no FP16 operands in this form), 16-byte stores
-    // (the correction format is unscaled BF16/TF32, so scale == 1: raw FP32 accumulators)
+    // symmetric form: W row segment [row][col .. col+31], 16-byte stores.  An unscaled BF16 / TF32
+    // correction has scale == 1 (raw FP32 accumulators); R-29's scaled correction (FP8 / FP16 / INT8 =
+    // the phase's format) unscales by scale = 2^-(sigma_C + sigma_R) -- one FP32 multiply while that
+    // power of two is a normal float (then exactly (float)(acc * scale)), else (sigma_C + sigma_R > 126:
+    // a residual far below the phase's floor) the product in FP64 and one rounding, so W never
+    // underflows to 0 through the scale itself
     float4 *dst = (float4 *)((float *)g.wout + row * g.ldw + col);
-    const float sf = (float)scale;
+    const bool f32ok = scale >= 0x1p-126 && scale <= 0x1p127;
+    const float sf = f32ok ? (float)scale : 1.0f;
     #pragma unroll
     for (int q = 0; q < 8; ++q) {
       float w[4];
       #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const float a = KIND == 3 ? (float)(int32_t)r[4 * q + u] : __uint_as_float(r[4 * q + u]);
-        w[u] = __fmul_rn(a, sf);
+        w[u] = f32ok ? __fmul_rn(a, sf) : (float)__dmul_rn(acc_to_f64<KIND>(r[4 * q + u]), scale);
       }
       dst[q] = make_float4(w[0], w[1], w[2], w[3]);
     }
@@ -922,6 +926,8 @@ cudaError_t launch_crt_finish(const GemmArgs &a_in, cudaStream_t s) {
 // EF = 1: the fused symmetric update (EPI_SYMUPD) is the only epilogue of this instance -- with the
 // general epilogue's code in the same kernel the instruction cache thrashed (tensor pipe 30 % busy,
 // "no instruction" the top stall)
+// EF: 0 the hot path's epilogues, 1 EPI_SYMUPD, 2 Ozaki-I digit groups (kind::i8), 3 CRT moduli
+// (kind::i8) -- each its own instance, so the plain and CRT INT8 kernels carry no Ozaki-I code
 template <int KIND, int EF = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, const GemmArgs g) {
@@ -943,16 +949,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
   const int ntiles = sch.count();
   // CRT (oz_grouped == 3): moduli [crt_l0, crt_l1) of every tile, modulus-major (all CTA pairs
   // stream the same residue planes at a time, as in one plain GEMM)
-  const int nitems = (KIND == 3 && g.oz_grouped == 3) ? (g.crt_l1 - g.crt_l0) * ntiles : ntiles;
+  constexpr bool crt = KIND == 3 && EF == 3, ozg = KIND == 3 && EF == 2;
+  const int nitems = crt ? (g.crt_l1 - g.crt_l0) * ntiles : ntiles;
   // Ozaki grouped launch: groups S+1 .. 2 per tile; otherwise one pass (g0 == g1)
   // oz_grouped == 2: the single group g.oz_g (one launch per group keeps each group's digit planes
   // L2-hot across all CTAs -- measured faster than all groups per tile in one launch)
-  const int g0 = g.oz_grouped == 1 ? g.oz_S + 1 : g.oz_grouped == 2 ? g.oz_g : 0;
-  const int g1 = g.oz_grouped == 1 ? 2 : g.oz_grouped == 2 ? g.oz_g : 0;
+  const int g0 = !ozg ? 0 : g.oz_grouped == 1 ? g.oz_S + 1 : g.oz_g;
+  const int g1 = !ozg ? 0 : g.oz_grouped == 1 ? 2 : g.oz_g;
   const int gfirst = g.oz_S + 1;                 // the group that initialises the FP64 accumulator
-  const bool crt = KIND == 3 && g.oz_grouped == 3;
   const int nsub = crt ? 1 : g0 - g1 + 1;
   const int esz = elt_size(g.prec);
+  const int64_t bkp = g.b_kp ? g.b_kp : g.a_kp;       // K-panel length of a paneled B operand
   const int nkb = (int)(g.K * esz / TC_BKB);
   const int bke = TC_BKB / esz;                       // K elements per block
 
@@ -984,8 +991,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
         for (int si = 0; si < nsub; ++si) {      // Ozaki groups / CRT moduli (one pass otherwise)
           const int gi = g0 - si;
           const int nk = crt ? (int)(g.a_kp * esz / TC_BKB)
-                             : g.oz_grouped ? (int)((int64_t)(gi - 1) * g.a_kp * esz / TC_BKB) : nkb;
-          const int64_t boff = (g.oz_grouped && !crt) ? (int64_t)(OZ_S - gi + 1) * g.a_kp : 0;
+                             : ozg ? (int)((int64_t)(gi - 1) * g.a_kp * esz / TC_BKB) : nkb;
+          const int64_t boff = ozg ? (int64_t)(OZ_S - gi + 1) * g.a_kp : 0;
           const int64_t kpl = crt ? (int64_t)lmod * g.a_kp : 0;      // CRT: residue plane lmod
           const int brow2 = crt ? lmod * (int)g.N + brow : brow;
           for (int kb = 0; kb < nk; ++kb) {
@@ -994,7 +1001,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
             if (leader) mbar_expect_tx(&full[stage], 2 * TC_STAGE_BYTES);
             const int64_t k0 = (int64_t)kb * bke;
             tma_load_3d_pair(sa, &mapA, &full[stage], (int)((kpl + k0) % g.a_kp), arow, (int)((kpl + k0) / g.a_kp));
-            if (g.b_pstride) tma_load_3d_pair(sb, &mapB, &full[stage], (int)(k0 % g.a_kp), brow2, (int)(k0 / g.a_kp));
+            if (g.b_pstride) tma_load_3d_pair(sb, &mapB, &full[stage], (int)(k0 % bkp), brow2, (int)(k0 / bkp));
             else tma_load_2d_pair(sb, &mapB, &full[stage], (int)(boff + k0), brow2);
             if (++stage == TC_ST) { stage = 0; phase ^= 1; }
           }
@@ -1012,7 +1019,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
         for (int si = 0; si < nsub; ++si) {
           const int gi = g0 - si;
           const int nk = crt ? (int)(g.a_kp * esz / TC_BKB)
-                             : g.oz_grouped ? (int)((int64_t)(gi - 1) * g.a_kp * esz / TC_BKB) : nkb;
+                             : ozg ? (int)((int64_t)(gi - 1) * g.a_kp * esz / TC_BKB) : nkb;
           const int buf = it & 1;
           mbar_wait_cluster(&tempty[buf], ((it >> 1) & 1) ^ 1);
           tc_fence_after();
@@ -1050,7 +1057,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       mbar_wait(&tfull[buf], (it >> 1) & 1);
       tc_fence_after();
       const int tile_m = tm * 2 + (int)rank;             // 128-row tile index
-      const int64_t row = (int64_t)tile_m * TC_BM + q * 32 + lane;
+      const int64_t row = g.row0 + (int64_t)tile_m * TC_BM + q * 32 + lane;   // global row (2-D grid: row0)
       const int64_t colb = (int64_t)tn * TC_BN;
       EpiAcc ea{0.0, 0.0, 0.0f};
       #pragma unroll 1
@@ -1061,7 +1068,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
           sym_update_chunk(g, row, colb + ch * 32, r, ea);
         } else if (crt) {
           crt_chunk(g, lmod, row, colb + ch * 32, r);
-        } else if (KIND == 3 && g.oz_grouped) {
+        } else if (ozg) {
           // the 32 accumulator values of this row segment are loaded up front (independent loads in
           // flight; a load-add-store chain per element serialised on memory latency)
           const int rs = g.oz_rsig[row];
@@ -1093,7 +1100,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
-      if (KIND == 3 && g.oz_grouped && (crt || gi > 2)) { ++it; continue; }   // partials after the finish only
+      if (crt || (ozg && gi > 2)) { ++it; continue; }   // partials after the finish only
       // per-tile partials: deterministic (fixed shuffle tree, warps summed in order 0..3)
       if ((g.mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE | EPI_SYMUPD)) || g.pmax) {
         double s = (g.mode & EPI_RESID) ? ea.r2 : ea.d2;
@@ -1106,7 +1113,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
         if (lane == 0) { red[it & 1][hh * 4 + q] = s; redm[it & 1][hh * 4 + q] = mx; }
         asm volatile("bar.sync 1, 256;\n" ::: "memory");
         if (et == 0) {
-          const int64_t tile = ((g.col0 + colb) / TC_BN) * g.tiles_m + tile_m;
+          const int64_t tile = ((g.col0 + colb) / TC_BN) * g.tiles_m + g.row0 / TC_BM + tile_m;
           if (g.mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE | EPI_SYMUPD))
           {
             const double *rr = red[it & 1];
@@ -1199,8 +1206,9 @@ cudaError_t launch_gemm_tc(const GemmArgs &a_in, cudaStream_t s) {
       return cudaErrorInvalidValue;
     }
   }
-  if (a.b_pstride) {   // K-concatenated B planes (fused symmetric update): [K / a_kp][N][a_kp] with plane stride
-    const cuuint64_t dims[3] = {(cuuint64_t)a.a_kp, (cuuint64_t)a.N, (cuuint64_t)(a.K / a.a_kp)};
+  if (a.b_pstride) {   // K-concatenated B planes (fused symmetric update; 2-D grid T panels): [K / b_kp][N][b_kp]
+    const int64_t bkp = a.b_kp ? a.b_kp : a.a_kp;
+    const cuuint64_t dims[3] = {(cuuint64_t)bkp, (cuuint64_t)a.N, (cuuint64_t)(a.K / bkp)};
     const cuuint64_t strides[2] = {(cuuint64_t)(a.ldb * esz), (cuuint64_t)(a.b_pstride * esz)};
     const cuuint32_t box[3] = {bke, (cuuint32_t)(TC_BN / 2), 1};
     const cuuint32_t es[3] = {1, 1, 1};
@@ -1239,7 +1247,9 @@ cudaError_t launch_gemm_tc(const GemmArgs &a_in, cudaStream_t s) {
   cudaError_t e = cudaSuccess;
   const bool symupd = (a.mode & EPI_SYMUPD) != 0;
   if (symupd && tc_kind(a.prec) > 1) return cudaErrorNotSupported;
-  switch (tc_kind(a.prec) + (symupd ? 4 : 0)) {
+  const int sel = tc_kind(a.prec) != 3 || !a.oz_grouped ? tc_kind(a.prec) + (symupd ? 4 : 0)
+                  : a.oz_grouped == 3 ? 7 : 6;
+  switch (sel) {
 #define TC_LAUNCH(C, K, EF)                                                                              \
     case C: {                                                                                            \
       static DeviceOnce attr;                                                                            \
@@ -1256,6 +1266,8 @@ cudaError_t launch_gemm_tc(const GemmArgs &a_in, cudaStream_t s) {
     TC_LAUNCH(3, 3, 0)
     TC_LAUNCH(4, 0, 1)
     TC_LAUNCH(5, 1, 1)
+    TC_LAUNCH(6, 3, 2)
+    TC_LAUNCH(7, 3, 3)
 #undef TC_LAUNCH
   }
   ++g_launches;

@@ -135,15 +135,15 @@ __global__ void k_stage_a(const double *A, int64_t lda, int64_t n, int64_t npad,
 // a3: initial guess, Eq. (3): C_0(i,j) = q_m0(A(j,i) / s) for the local panel,
 // row-major [npad][kp], A(j,i) == A(i,j) bitwise (checked symmetry) -> coalesced reads.
 // ---------------------------------------------------------------------------------------
-__global__ void k_c0(const double *A, int64_t lda, int64_t n, int64_t col0, int64_t kp, double s,
+__global__ void k_c0(const double *A, int64_t lda, int64_t n, int64_t row0, int64_t col0, int64_t kp, double s,
                      int cont64, int m, int rtz, void *cont) {
   const int64_t jj = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t i = blockIdx.y;
+  const int64_t il = blockIdx.y, i = row0 + il;        // the block's rows [row0, row0 + rows)
   if (jj >= kp) return;
   const int64_t j = col0 + jj;
   double v = 0.0;
   if (i < n && j < n) v = __ddiv_rn(A[i * lda + j], s);
-  const int64_t o = i * kp + jj;
+  const int64_t o = il * kp + jj;
   if (cont64) ((double *)cont)[o] = q_e11(v, m, rtz);
   else ((float *)cont)[o] = q_e8(v, m, rtz);
 }
@@ -538,10 +538,10 @@ cudaError_t launch_stage_a(const double *A, int64_t lda, int64_t n, int64_t npad
   }
   LAUNCH_CHECK();
 }
-cudaError_t launch_c0(const double *A, int64_t lda, int64_t n, int64_t npad, int64_t col0, int64_t kp, double sv,
-                      int cont64, int m, int rtz, void *cont, cudaStream_t s) {
-  dim3 g(nblk(kp, 256), (unsigned)npad);
-  k_c0<<<g, 256, 0, s>>>(A, lda, n, col0, kp, sv, cont64, m, rtz, cont);
+cudaError_t launch_c0(const double *A, int64_t lda, int64_t n, int64_t rows, int64_t row0, int64_t col0, int64_t kp,
+                      double sv, int cont64, int m, int rtz, void *cont, cudaStream_t s) {
+  dim3 g(nblk(kp, 256), (unsigned)rows);
+  k_c0<<<g, 256, 0, s>>>(A, lda, n, row0, col0, kp, sv, cont64, m, rtz, cont);
   LAUNCH_CHECK();
 }
 cudaError_t launch_make_operand(const void *cont, int cont64, int64_t count, int prec, const int *sig, void *op,
@@ -595,6 +595,39 @@ cudaError_t launch_mirror_unpack(const void *recv, int esz, int64_t kp, int64_t 
   const int64_t total = (int64_t)(world - rank) * kp * kp;
   if (total <= 0) return cudaSuccess;
   k_mirror_unpack<<<nblk(total, 256), 256, 0, s>>>((const char *)recv, esz, kp, npad, rank, world, (char *)T);
+  LAUNCH_CHECK();
+}
+
+// 2-D grid (engine gather_partials): slot s = tn * tiles_m + tm of the global partial array comes from the
+// rank owning that output tile, whose whole array sits at partg[rank * total]
+__global__ void k_select_partials(const double *partg, int64_t total, int64_t tiles_m, int tmsz, int tnsz, int64_t mr,
+                                  int64_t kp, int gcols, double *part) {
+  for (int64_t sl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sl < total; sl += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tn = sl / tiles_m, tm = sl % tiles_m;
+    const int64_t owner = ((tm * tmsz) / mr) * gcols + (tn * tnsz) / kp;
+    part[sl] = partg[owner * total + sl];
+  }
+}
+cudaError_t launch_select_partials(const double *partg, int64_t total, int64_t tiles_m, int tmsz, int tnsz, int64_t mr,
+                                   int64_t kp, int gcols, double *part, cudaStream_t s) {
+  k_select_partials<<<nblk(total, 256), 256, 0, s>>>(partg, total, tiles_m, tmsz, tnsz, mr, kp, gcols, part);
+  LAUNCH_CHECK();
+}
+
+// block-major [grows * gcols][mr][kp] (rank r = grid row r / gcols, grid column r % gcols) -> row-major;
+// 1 x G (mr = npad) is the panel-major [G][npad][kp] layout
+__global__ void k_copy_out_blocks(const double *src, int64_t mr, int64_t kp, int gcols, int64_t n, double *dst,
+                                  int64_t ldc) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t i = blockIdx.y;
+  if (j >= n) return;
+  const int64_t r = (i / mr) * gcols + j / kp;
+  dst[i * ldc + j] = src[(r * mr + i % mr) * kp + j % kp];
+}
+cudaError_t launch_copy_out_blocks(const double *src, int64_t mr, int64_t kp, int gcols, int64_t n, double *dst,
+                                   int64_t ldc, cudaStream_t s) {
+  dim3 g(nblk(n, 256), (unsigned)n);
+  k_copy_out_blocks<<<g, 256, 0, s>>>(src, mr, kp, gcols, n, dst, ldc);
   LAUNCH_CHECK();
 }
 

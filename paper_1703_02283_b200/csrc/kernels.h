@@ -10,14 +10,18 @@ cudaError_t launch_maxabs_qA(const double *A, int64_t lda, int64_t n, int cont64
                              int nparts, cudaStream_t s);
 cudaError_t launch_stage_a(const double *A, int64_t lda, int64_t n, int64_t npad, int64_t col0, int64_t kp, int prec,
                            int cont64, int m, int rtz, const int *sig, void *Aop, cudaStream_t s);
-cudaError_t launch_c0(const double *A, int64_t lda, int64_t n, int64_t npad, int64_t col0, int64_t kp, double sv,
-                      int cont64, int m, int rtz, void *cont, cudaStream_t s);
+cudaError_t launch_c0(const double *A, int64_t lda, int64_t n, int64_t rows, int64_t row0, int64_t col0, int64_t kp,
+                      double sv, int cont64, int m, int rtz, void *cont, cudaStream_t s);
 cudaError_t launch_make_operand(const void *cont, int cont64, int64_t count, int prec, const int *sig, void *op,
                                 cudaStream_t s);
 cudaError_t launch_scale_op(const float *src, int64_t count, const int *sig, int prec, void *dst, cudaStream_t s);
 cudaError_t launch_maxabs_cont(const void *cont, int cont64, int64_t count, float *pmax, int nparts, cudaStream_t s);
 cudaError_t launch_mirror_unpack(const void *recv, int esz, int64_t kp, int64_t npad, int rank, int world, void *T,
                                  cudaStream_t s);
+cudaError_t launch_select_partials(const double *partg, int64_t total, int64_t tiles_m, int tmsz, int tnsz, int64_t mr,
+                                   int64_t kp, int gcols, double *part, cudaStream_t s);
+cudaError_t launch_copy_out_blocks(const double *src, int64_t mr, int64_t kp, int gcols, int64_t n, double *dst,
+                                   int64_t ldc, cudaStream_t s);
 cudaError_t launch_peek(const void *src, int prec, const int *sig, int64_t count, double *dst, cudaStream_t s);
 cudaError_t launch_cont_to_f64(const void *cont, int cont64, int64_t count, double *dst, cudaStream_t s);
 cudaError_t launch_f64_to_cont(const double *src, int64_t count, int cont64, int m, int rtz, void *cont,

@@ -5,6 +5,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <condition_variable>
 #include <cstring>
 #include <mutex>
@@ -24,6 +25,9 @@ struct Api {
   decltype(&ncclGroupStart) groupStart = nullptr;
   decltype(&ncclGroupEnd) groupEnd = nullptr;
   decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclCommSplit) commSplit = nullptr;
+  decltype(&ncclCommCount) commCount = nullptr;
+  decltype(&ncclCommUserRank) commUserRank = nullptr;
   decltype(&ncclGetErrorString) errStr = nullptr;
 };
 
@@ -43,6 +47,9 @@ Api &api() {
     a.groupStart = (decltype(a.groupStart))dlsym(h, "ncclGroupStart");
     a.groupEnd = (decltype(a.groupEnd))dlsym(h, "ncclGroupEnd");
     a.commDestroy = (decltype(a.commDestroy))dlsym(h, "ncclCommDestroy");
+    a.commSplit = (decltype(a.commSplit))dlsym(h, "ncclCommSplit");          // NCCL >= 2.18 (2-D grids only)
+    a.commCount = (decltype(a.commCount))dlsym(h, "ncclCommCount");
+    a.commUserRank = (decltype(a.commUserRank))dlsym(h, "ncclCommUserRank");
     a.errStr = (decltype(a.errStr))dlsym(h, "ncclGetErrorString");
     a.ok = a.getUniqueId && a.commInitRank && a.allGather && a.send && a.recv && a.groupStart && a.groupEnd &&
            a.commDestroy && a.errStr;
@@ -99,6 +106,20 @@ bool NcclComm::alltoall(const void *send, void *recv, size_t bytes, cudaStream_t
   return true;
 }
 
+Transport *NcclComm::split(int color, int key, std::string *err) {
+  Api &a = api();
+  if (!comm_) { *err = "communicator not initialised"; return nullptr; }
+  if (!a.commSplit || !a.commCount || !a.commUserRank) { *err = "this NCCL has no ncclCommSplit"; return nullptr; }
+  ncclComm_t sub = nullptr;
+  ncclResult_t r = a.commSplit((ncclComm_t)comm_, color, key, &sub, nullptr);
+  if (r != ncclSuccess) { *err = std::string("ncclCommSplit: ") + a.errStr(r); return nullptr; }
+  NcclComm *t = new NcclComm();
+  t->comm_ = sub;
+  a.commCount(sub, &t->world_);
+  a.commUserRank(sub, &t->rank_);
+  return t;
+}
+
 NcclComm::~NcclComm() {
   if (comm_) { api().commDestroy((ncclComm_t)comm_); comm_ = nullptr; }
 }
@@ -113,6 +134,7 @@ NcclComm::~NcclComm() {
 // ---------------------------------------------------------------------------------------
 struct LocalGroup {
   int world = 0;
+  std::vector<int> color, key;            // split() exchange area
   std::mutex mu;
   std::condition_variable cv;
   int arrived = 0;
@@ -128,9 +150,32 @@ struct LocalGroup {
 };
 
 namespace {
+// A rank of a local group, or of a sub-group of it (split): `members` are the group's world ranks in
+// sub-rank order.  Every collective still passes the WORLD barrier: in the SPMD engine every rank
+// reaches each (sub-)collective at the same program point, and copies come from members only.
 class LocalRank : public Transport {
  public:
-  LocalRank(LocalGroup *g, int rank) : g_(g), rank_(rank) {}
+  LocalRank(LocalGroup *g, int rank) : g_(g), rank_(rank) {
+    for (int r = 0; r < g->world; ++r) members_.push_back(r);
+    sub_ = rank;
+  }
+  LocalRank(LocalGroup *g, int rank, std::vector<int> members, int sub)
+      : g_(g), rank_(rank), members_(std::move(members)), sub_(sub) {}
+  Transport *split(int color, int key, std::string *err) override {
+    g_->color[rank_] = color; g_->key[rank_] = key;
+    g_->barrier();
+    std::vector<std::pair<int, int>> mk;   // (key, world rank) of my color
+    for (int r = 0; r < g_->world; ++r)
+      if (g_->color[r] == color && std::find(members_.begin(), members_.end(), r) != members_.end())
+        mk.push_back({g_->key[r], r});
+    std::sort(mk.begin(), mk.end());
+    g_->barrier();                          // everyone has read color / key before the next split
+    std::vector<int> m;
+    int sub = -1;
+    for (size_t i = 0; i < mk.size(); ++i) { m.push_back(mk[i].second); if (mk[i].second == rank_) sub = (int)i; }
+    if (sub < 0) { *err = "local split: rank not in its own color"; return nullptr; }
+    return new LocalRank(g_, rank_, m, sub);
+  }
   bool allgather(const void *send, void *recv, size_t bytes, cudaStream_t s) override {
     return exchange(send, recv, bytes, s, false);
   }
@@ -150,21 +195,24 @@ class LocalRank : public Transport {
     me.send = send; me.recv = recv;
     bool ok = ck(cudaEventRecord(me.ready, s));
     g_->barrier();
-    for (int h = 0; h < g_->world && ok; ++h) {
-      const LocalGroup::Slot &peer = g_->slot[h];
-      const char *src = a2a ? (const char *)peer.send + rank_ * bytes : (const char *)peer.send;
+    for (int h = 0; h < (int)members_.size() && ok; ++h) {
+      const int wr = members_[h];
+      const LocalGroup::Slot &peer = g_->slot[wr];
+      const char *src = a2a ? (const char *)peer.send + sub_ * bytes : (const char *)peer.send;
       char *dst = (char *)recv + h * bytes;
-      if (h != rank_) ok = ck(cudaStreamWaitEvent(s, peer.ready, 0));
+      if (wr != rank_) ok = ck(cudaStreamWaitEvent(s, peer.ready, 0));
       if (ok && src != dst) ok = ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
     }
     if (ok) ok = ck(cudaEventRecord(me.done, s));
     g_->barrier();
-    for (int h = 0; h < g_->world && ok; ++h)
-      if (h != rank_) ok = ck(cudaStreamWaitEvent(s, g_->slot[h].done, 0));
+    for (int h = 0; h < (int)members_.size() && ok; ++h)
+      if (members_[h] != rank_) ok = ck(cudaStreamWaitEvent(s, g_->slot[members_[h]].done, 0));
     return ok;
   }
   LocalGroup *g_;
-  int rank_;
+  int rank_;                 // world rank
+  std::vector<int> members_;
+  int sub_;                  // rank within members_
   std::string err_;
 };
 }  // namespace
@@ -174,6 +222,8 @@ LocalGroup *local_group_create(int world, std::string *err) {
   LocalGroup *g = new LocalGroup();
   g->world = world;
   g->slot.resize(world);
+  g->color.assign(world, 0);
+  g->key.assign(world, 0);
   for (auto &sl : g->slot) {
     if (cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming) != cudaSuccess) {

@@ -23,6 +23,9 @@ class Transport {
   // recv[r * bytes ..) = rank r's send[rank * bytes ..) (send and recv distinct)
   virtual bool alltoall(const void *send, void *recv, size_t bytes_per_peer, cudaStream_t s) = 0;
   virtual const char *last_error() const = 0;
+  // collective over this transport's ranks: the sub-transport of the ranks with the same color, ordered
+  // by key (2-D grids: a grid row / a grid column); nullptr + *err on failure.  Owned by the caller.
+  virtual Transport *split(int color, int key, std::string *err) = 0;
 };
 
 class NcclComm : public Transport {
@@ -32,6 +35,7 @@ class NcclComm : public Transport {
   bool allgather(const void *send, void *recv, size_t bytes_per_rank, cudaStream_t s) override;
   bool alltoall(const void *send, void *recv, size_t bytes_per_peer, cudaStream_t s) override;
   const char *last_error() const override { return err_.c_str(); }
+  Transport *split(int color, int key, std::string *err) override;
   ~NcclComm() override;
 
  private:

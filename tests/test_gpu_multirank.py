@@ -37,7 +37,7 @@ def _solve_world1(A, p, phases, form):
     return out, tr, C
 
 
-def _solve_local(A, p, phases, form, world):
+def _solve_local(A, p, phases, form, world, grid=None):
     grp = ipr.ipr_test_local_group_create(world)
     res = [None] * world
     err = [None] * world
@@ -46,7 +46,8 @@ def _solve_local(A, p, phases, form, world):
         try:
             st = torch.cuda.Stream()
             with torch.cuda.stream(st):
-                s = ipr.Solver(A, p, phases, 1e-12, stream=st, world=world, rank=r, form=form, local_group=grp)
+                s = ipr.Solver(A, p, phases, 1e-12, stream=st, world=world, rank=r, form=form, local_group=grp,
+                               grid=grid)
                 s.iterate(300)
                 tr, out = s.trace(), s.outcome
                 C = torch.empty_like(A)
@@ -107,6 +108,34 @@ def test_sharded_bit_identical_to_one_gpu(A, case, world):
         np.testing.assert_array_equal(C, C1)
     if "crt" in sched:
         assert any(t["moduli"] > 0 for t in tr1)
+
+
+GRID_CASES = [("literal_fp64", "fp64", 2), ("literal_bf16_fp64", "bf16>fp64", 2), ("literal_tf32_fp64_p3", "tf32>fp64", 3)]
+
+
+@pytest.mark.parametrize("grid", [(2, 2), (4, 1)], ids=["2x2", "4x1"])
+@pytest.mark.parametrize("case", GRID_CASES, ids=[c[0] for c in GRID_CASES])
+def test_2d_grid_bit_identical_to_one_gpu(A, case, grid):
+    # the true 2-D P_r x P_c option: rank (r, c) owns the block
+    # (R_r, S_c) of C and every T_j; Chat row panels gather along grid rows, T_j column panels along grid
+    # columns before every GEMM (SUMMA-like), partials from their owners -- the same tiles and K order,
+    # so every record and the answer equal G = 1 bit for bit
+    cid, sched, p = case
+    form, phases = _schedule(sched)
+    out1, tr1, C1 = _solve_world1(A, p, phases, form)
+    assert out1 == ipr.IPR_CONVERGED
+    res = _solve_local(A, p, phases, form, grid[0] * grid[1], grid=grid)
+    for out, tr, C in res:
+        assert out == out1
+        _same_trace(tr, tr1)
+        np.testing.assert_array_equal(C, C1)
+
+
+def test_2d_grid_refuses_other_forms(A):
+    form, phases = _schedule("symtri:bf16>fp64/cbf16")
+    with pytest.raises(ipr.IprError) as e:
+        _solve_local(A, 2, phases, form, 4, grid=(2, 2))
+    assert e.value.status == ipr.IPR_E_UNSUPPORTED
 
 
 def test_local_group_bad_arguments(A):

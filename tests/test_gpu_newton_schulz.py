@@ -67,11 +67,16 @@ def test_ns_mixed_level2_and_refinement_wins(name):
     # config C2 family (p = 1, kappa = 1e3, n = 1024): the NS ordering converges, and the mixed
     # schedule needs FEWER FP64 iterations than all-FP64 (SURVEY Table A6b) -- "refined into a
     # precise solution in very few additional iterations".
-    # kappa = 1e3 is outside the stable-twin regime: during the linear phase the small eigen-
-    # components grow ~2x per iteration and FP32-vs-FP64 accumulation flips of BF16 roundings are
-    # amplified with them (measured drift 3.2e-2 at k = 21 for BF16, 1 % above 4 * 2^-7).  Level 3
-    # of DESIGN.md §4: envelopes (switch +-2, converged, answer within 1e-8), per-iterate drift
-    # bounded by 8 * 2^-m (diagnostic), and the refinement claim.
+    # kappa = 1e3 is outside the stable-twin regime.  Level 3 of DESIGN.md section 4: Level-2 drift
+    # until the oracle's commutator onset k* (gamma_k > 2^-m), then envelopes.  Here gamma stays below
+    # 2^-m through the whole low phase (k* = 66 / 33 > the switch), so Level 2 applies throughout --
+    # with reading R-31: in the Newton-Schulz linear phase (x <- x (2 - lambda x) doubles the small
+    # eigencomponents) every iteration adds an independent O(2^-m) relative rounding difference between
+    # the GPU (FP32 accumulation) and the oracle (FP64), so the drift between the two runs accumulates
+    # like a random walk and the per-iterate bound is 4 * 2^-m * max(1, sqrt(k / 8)) (measured round 1:
+    # 3.2e-2 at k = 21 for BF16, within 4 * 2^-7 * 1.62 = 5.1e-2).  Envelopes after the switch: switch
+    # +-2, converged, answer within 1e-8 (FP64-phase drift of two valid runs, SURVEY Table A5a), and
+    # the refinement claim.
     c = synth.CONFIGS["C2"]
     A, lam, _ = synth.spd(c["n"], c["kappa"], c["seed"], return_eig=True)
     m = {"bf16": 7, "tf32": 10, "fp16": 10}[name]
@@ -86,8 +91,14 @@ def test_ns_mixed_level2_and_refinement_wins(name):
     sw_o = next(k for k, x in enumerate(r.records) if x["decision"] == oracle.SWITCH)
     sw_g = next(k for k, x in enumerate(tr) if x["decision"] == ipr.IPR_DEC_SWITCH)
     assert abs(sw_g - sw_o) <= 2
-    for k in range(1, min(sw_o, sw_g) + 1):
-        assert rel_fro(hist[k], r.C_hist[k]) <= 8 * 2.0 ** -m, k
+    gam = np.array([x["gamma"] for x in r.records])
+    kstar = int(np.argmax(gam > 2.0 ** -m)) if np.any(gam > 2.0 ** -m) else len(gam)
+    drift = []
+    for k in range(1, min(sw_o, sw_g, kstar) + 1):
+        d = rel_fro(hist[k], r.C_hist[k])
+        drift.append(d)
+        assert d <= 4 * 2.0 ** -m * max(1.0, np.sqrt(k / 8.0)), (k, d)
+    print(f"{name}: k*={kstar} switch={sw_o} max drift / 4 2^-m = {max(drift) / (4 * 2.0 ** -m):.3f}")
     assert rel_fro(best, r.C_best) <= 1e-8
     fp64_only = oracle.solve(A, 1, [oracle.phase()], tol, 200, form=oracle.FORM_NEWTON_SCHULZ)
     n_fp64_mixed = sum(1 for t in tr if t["prec"] == "fp64")
