@@ -56,8 +56,8 @@ def test_argument_validation_without_gpu():
         ipr.ipr_init(8, 1234, lda=4)
     assert e.value.status == ipr.IPR_E_INVALID_ARG
     with pytest.raises(ipr.IprError) as e:
-        ipr.ipr_init(8, 1234, world=2, rank=0, nccl_unique_id=b"\0" * 128, grid_rows=2, grid_cols=1)
-    assert e.value.status == ipr.IPR_E_UNSUPPORTED
+        ipr.ipr_init(8, 1234, world=2, rank=0, nccl_unique_id=b"\0" * 128, grid_rows=2, grid_cols=2)
+    assert e.value.status == ipr.IPR_E_INVALID_ARG          # grid_rows x grid_cols != world
     with pytest.raises(ipr.IprError) as e:
         ipr.ipr_iterate(None, 1)
     assert e.value.status == ipr.IPR_E_INVALID_ARG
