@@ -100,6 +100,14 @@ ipr_status ipr_test_local_group_destroy(ipr_local_group *g);
 ipr_status ipr_test_init_local(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda, void *cuda_stream,
                                ipr_local_group *group, int rank, int grid_rows, int grid_cols);
 
+/* Guard bands (memory-safety check in place of compute-sanitizer, which this pool does not allow):
+ * ipr_test_set_guards(1) makes every context allocated afterwards (process-wide, at its first
+ * ipr_iterate) put a 4 KB band of a fixed byte pattern behind each of its arena buffers;
+ * ipr_test_check_guards re-reads every band: *bad = index of the first altered band, -1 if all intact.
+ * corrupt_first != 0 alters band 0 first (the test's positive control). */
+ipr_status ipr_test_set_guards(int on);
+ipr_status ipr_test_check_guards(ipr_ctx *c, int corrupt_first, int *bad);
+
 /* Number of this process's kernel launches since load (all libipr kernels). */
 int64_t ipr_launch_count(void);
 

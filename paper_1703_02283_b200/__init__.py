@@ -35,7 +35,8 @@ EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_
             "ipr_nccl_unique_id", "ipr_version", "ipr_test_quantize", "ipr_test_gemm",
             "ipr_launch_count", "ipr_plan", "ipr_set_form", "ipr_bench_gemm", "ipr_bench_gemm_epi",
             "ipr_test_set_digits", "ipr_test_crt_table", "ipr_set_cert", "ipr_test_peek",
-            "ipr_test_local_group_create", "ipr_test_local_group_destroy", "ipr_test_init_local"]
+            "ipr_test_local_group_create", "ipr_test_local_group_destroy", "ipr_test_init_local",
+            "ipr_test_set_guards", "ipr_test_check_guards"]
 IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ, IPR_FORM_SYMMETRIC, IPR_FORM_SYMMETRIC_TRI, IPR_FORM_COUPLED = 0, 1, 2, 3, 4
 IPR_CERT_FP64, IPR_CERT_PHASE = 0, 1
 CERT_BY_NAME = {"fp64": IPR_CERT_FP64, "dmma": IPR_CERT_FP64, "phase": IPR_CERT_PHASE}
@@ -92,6 +93,8 @@ def _load():
     L.ipr_test_peek.argtypes = [vp, C.c_int, vp, C.POINTER(C.c_int64)]
     L.ipr_test_local_group_create.argtypes = [C.c_int, C.POINTER(vp)]
     L.ipr_test_local_group_destroy.argtypes = [vp]
+    L.ipr_test_set_guards.argtypes = [C.c_int]
+    L.ipr_test_check_guards.argtypes = [vp, C.c_int, C.POINTER(C.c_int)]
     L.ipr_test_init_local.argtypes = [C.POINTER(vp), i64, vp, i64, vp, vp, C.c_int, C.c_int, C.c_int]
     L.ipr_bench_gemm.argtypes = [C.c_int, i64, C.c_int, C.c_int, vp, dp]
     L.ipr_bench_gemm_epi.argtypes = [C.c_int, i64, C.c_int, C.c_int, C.c_int, vp, dp]
@@ -322,6 +325,17 @@ def ipr_test_peek(ctx, what: int, npad: int):
     if got.value != npad:
         raise IprError(IPR_E_INVALID_ARG, f"ipr_test_peek: npad is {got.value}, not {npad}")
     return out
+
+
+def ipr_test_set_guards(on: bool):
+    _check(_lib.ipr_test_set_guards(int(on)))
+
+
+def ipr_test_check_guards(ctx, corrupt_first: bool = False) -> int:
+    """Index of the first altered arena guard band, -1 if all are intact (ipr_testing.h)."""
+    bad = C.c_int(0)
+    _check(_lib.ipr_test_check_guards(ctx, int(corrupt_first), C.byref(bad)), ctx)
+    return bad.value
 
 
 def ipr_launch_count() -> int:

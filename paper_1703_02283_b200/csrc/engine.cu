@@ -152,6 +152,7 @@ struct ipr_ctx {
   CrtTimer ktimer{kev, 8, 0};
   bool upd_timed = false;
   int cert = IPR_CERT_FP64;             // convergence certificate of the symmetric / coupled forms (ipr_set_cert)
+  std::vector<size_t> guards;           // ipr_test_set_guards: arena offsets of the guard bands
 };
 
 namespace {
@@ -969,6 +970,12 @@ void free_ctx(ipr_ctx *c) {
 
 // All O(n^2) buffers in one arena, sized once the schedule and the form are known (first
 // ipr_iterate): one cudaMalloc / cudaFree per solve, and an OOM is reported before any work.
+// test-only guard bands behind every arena buffer (compute-sanitizer is closed on the pool):
+// ipr_test_set_guards(1) before ipr_iterate, ipr_test_check_guards after
+constexpr size_t kGuard = 4096;
+constexpr unsigned char kGuardByte = 0xA5;
+int g_guards = 0;
+
 ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
   const size_t full = (size_t)(c->npad * c->npad), panel = (size_t)(c->npad * c->kp);
   const bool cpl = c->form == IPR_FORM_COUPLED;
@@ -1010,8 +1017,9 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       {(void **)&c->partg, c->grows > 1 ? (size_t)c->world * c->npart * 8 : 0},
       {&c->msend, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0},
       {&c->mrecv, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0}};
+  const size_t gb = g_guards ? kGuard : 0;
   size_t total = 0;
-  for (const Slot &q : slots) total += (q.bytes + 255) / 256 * 256;
+  for (const Slot &q : slots) total += (q.bytes + 255) / 256 * 256 + (q.bytes ? gb : 0);
   // stream-ordered allocation from a library-owned pool that retains its memory, so back-to-back
   // solves reuse the arena without driver (un)mapping: one context = one cudaMallocFromPoolAsync
   cudaMemPool_t pool = arena_pool();
@@ -1024,9 +1032,15 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
   }
   c->arena = base;
   size_t off = 0;
+  c->guards.clear();
   for (const Slot &q : slots) {
     *q.p = q.bytes ? base + off : nullptr;
     off += (q.bytes + 255) / 256 * 256;
+    if (q.bytes && gb) {
+      c->guards.push_back(off);
+      CK(cudaMemsetAsync(base + off, kGuardByte, gb, c->st));
+      off += gb;
+    }
   }
   if (cr) { c->full64 = (double *)c->crB; c->Acert = c->crV; }   // 8 B x npad^2 <= 18 B x npad^2
   CK(cudaMemsetAsync(c->chat[0], 0, full * 8, c->st));
@@ -1535,6 +1549,26 @@ ipr_status ipr_finalize(ipr_ctx *c, double *C_dev_out, int64_t ldc) {
 
 // ---- test hooks (include/ipr_testing.h) ----
 int64_t ipr_launch_count(void) { return g_launches; }
+
+ipr_status ipr_test_set_guards(int on) {
+  g_guards = on ? 1 : 0;
+  return IPR_OK;
+}
+
+ipr_status ipr_test_check_guards(ipr_ctx *c, int corrupt_first, int *bad) {
+  if (!c || !bad) return fail(c, IPR_E_INVALID_ARG, "ipr_test_check_guards: null pointer");
+  *bad = -1;
+  if (!c->arena || c->guards.empty()) return fail(c, IPR_E_STATE, "ipr_test_check_guards: no guarded arena");
+  if (corrupt_first) CK(cudaMemsetAsync((char *)c->arena + c->guards[0] + 17, 0x5A, 1, c->st));   // the control
+  std::vector<unsigned char> h(kGuard);
+  for (size_t i = 0; i < c->guards.size() && *bad < 0; ++i) {
+    CK(cudaMemcpyAsync(h.data(), (char *)c->arena + c->guards[i], kGuard, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    for (size_t k = 0; k < kGuard; ++k)
+      if (h[k] != kGuardByte) { *bad = (int)i; break; }
+  }
+  return IPR_OK;
+}
 
 ipr_status ipr_test_peek(ipr_ctx *c, int what, double *dst, int64_t *npad_out) {
   if (!c || !dst || !npad_out || what < IPR_PEEK_AHAT || what > IPR_PEEK_CHATC)
