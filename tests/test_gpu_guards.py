@@ -15,7 +15,7 @@ ipr = pytest.importorskip("paper_1703_02283_b200")
 SCHEDULES = [
     ("symtri:fp8/cfp8>bf16>fp64crt@a/cbf16", 2), ("sym:fp8/cfp8>bf16>fp64crt@a/cbf16", 2),
     ("symtri:bf16>fp64oz@a/cbf16", 2), ("symtri:int8/cint8>bf16>fp64/cbf16", 2), ("sym:fp16>fp64/cbf16", 3),
-    ("bf16>fp64", 2), ("tf32>fp64", 3), ("ns:tf32>fp64", 1), ("cpl:bf16>fp64", 2), ("fp64", 2),
+    ("bf16>fp64", 2), ("tf32>fp64", 3), ("ns:tf32>fp64", 1), ("cpl:fp64", 2), ("fp64", 2),
 ]
 
 
