@@ -370,11 +370,17 @@ def main():
         ops = mods_tot * fl_chain
         achieved = ops / (kern_ms * 1e-3) / 1e12 if kern_ms > 0 else None
         chain_ach = ops / (tot_ms * 1e-3) / 1e12 if tot_ms > 0 else None
-        pk, pk_src = sustained_int8_peak() or peaks["int8"]
+        # peak: the BURST figure -- inside the solve the INT8 GEMMs run in short bursts between other
+        # kernels and host syncs, at clocks well above the 4 s sustained measurement's (r02: 1770 vs 1357
+        # MHz median), so the sustained figure under-states the ceiling (frac > 1); both are reported
+        pk, pk_src = peaks["int8"]
+        sus = sustained_int8_peak()
         roof = {"bound": "tensor", "kernel": "k_gemm_tc<kind::i8> (Ozaki-II FP64 products: one INT8 GEMM per CRT "
                 "modulus, 2 moduli per launch)", "achieved": achieved, "peak": pk,
                 "unit": "TOPS (int8)", "frac": achieved / pk if achieved else None, "traffic": None,
-                "peak_source": pk_src, "frac_of_burst_peak": achieved / peaks["int8"][0] if achieved else None,
+                "peak_source": pk_src,
+                "frac_of_sustained_peak": achieved / sus[0] if (achieved and sus) else None,
+                "sustained_peak": sus[0] if sus else None,
                 "algorithmic_int8_ops_per_chain_avg": mods * fl_chain, "moduli_per_chain_avg": mods,
                 "chains": n_chains, "kernel_ms_per_chain_avg": kern_ms / max(n_chains, 1),
                 "avg_chain_ms": tot_ms / max(n_chains, 1), "chain_achieved_tops": chain_ach,
