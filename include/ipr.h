@@ -70,8 +70,8 @@ typedef enum {
  *             62 and at what 18 moduli allow at n), the integer product computed exactly modulo N pairwise
  *             coprime moduli <= 256 (one kind::i8 GEMM each; N = 17 at b = 59, n = 8192) and rebuilt by
  *             the Chinese remainder theorem in exact sliced FP64 arithmetic.  Error: the quantisation
- *             only (2^-b relative to the row / column maximum).  Symmetric forms only, world = 1,
- *             n <= 65535. */
+ *             (2^-b relative to the row / column maximum; the reconstruction adds <= ~0.06 of that).
+ *             Symmetric forms only, any 1 x world grid, n <= 65535. */
 typedef enum { IPR_FP64 = 0, IPR_TF32 = 1, IPR_BF16 = 2, IPR_FP16 = 3, IPR_FP8 = 4, IPR_INT8 = 5,
                IPR_FP64_OZ = 6, IPR_FP64_CRT = 7 } ipr_prec;
 
@@ -157,10 +157,16 @@ typedef struct {
  * SYMMETRIC otherwise), computes ||A||_1, ||A||_inf and max diagonal on the GPU (Eq. 3) and
  * records a warning (ipr_last_error) if the sufficient condition of reading R-12 for Eq. (2)
  * fails; that never fails init.
- * Multi-GPU: world > 1 ranks, one process per GPU, each passing the FULL A;
- * nccl_unique_id = 128 bytes from ipr_nccl_unique_id on rank 0 broadcast by the caller.
- * grid_rows x grid_cols must be 1 x world (column panels); other grids -> IPR_E_UNSUPPORTED.
- * world == 1: nccl_unique_id may be NULL, grid 1 x 1.  cuda_stream: cudaStream_t (NULL ok). */
+ * Multi-GPU: world > 1 ranks, one process per GPU, each passing
+ * the FULL A; nccl_unique_id = 128 bytes from ipr_nccl_unique_id on rank 0 broadcast by the caller.
+ * grid_rows x grid_cols must equal world (else IPR_E_INVALID_ARG):
+ *   1 x world (default): column panels -- every form and format except IPR_FP64_OZ;
+ *   P_r x P_c, P_r > 1: 2-D blocks, rank = r * P_c + c owns rows [r n/P_r, ...) x columns [c n/P_c, ...)
+ *     (padded); the literal form with FP64 / TF32 / BF16 phases (else IPR_E_UNSUPPORTED at ipr_iterate),
+ *     needs ncclCommSplit (NCCL >= 2.18).
+ * Every decomposition reproduces world = 1 bit for bit (same tiles, same K order, partials reduced in the
+ * same global order).  world == 1: nccl_unique_id may be NULL, grid 1 x 1.  cuda_stream: cudaStream_t
+ * (NULL ok). */
 ipr_status ipr_init(ipr_ctx **out, int64_t n, const double *A_dev, int64_t lda,
                     void *cuda_stream, int world, int rank, const void *nccl_unique_id,
                     int grid_rows, int grid_cols);
@@ -193,10 +199,11 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
  * final_tol, and the certified C_k is the answer ipr_finalize returns; else the iteration continues
  * from C_{k+1}.
  *
- * IPR_FORM_SYMMETRIC_TRI (p = 2, world = 1): as IPR_FORM_SYMMETRIC, but
+ * IPR_FORM_SYMMETRIC_TRI (p = 2, 1 x world grids): as IPR_FORM_SYMMETRIC, but
  * Z_2 = C A C -- symmetric in exact arithmetic -- is computed on the upper triangle only (tiles
  * wholly below the diagonal are skipped: ~1/2 of GEMM 2) and R_ij = delta_ij - Z_2[min(i,j)][max(i,j)]
- * is exactly symmetric; rho_s sums the off-diagonal terms twice.
+ * is exactly symmetric; rho_s sums the off-diagonal terms twice.  G > 1: each rank computes the upper
+ * tiles of its own columns, the mirrors reach their owners by one all-to-all.
  *
  * IPR_FORM_COUPLED (any p; FP64 / TF32 / BF16 phases): the M-carrying form
  * of Eq. (1) (reading R-27): with M = X^p A and N = ((p+1) I - M) / p, X_{k+1} = X_k N_k
