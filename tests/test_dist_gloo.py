@@ -237,3 +237,126 @@ def test_world2_gloo_symmetric_form_matches_oracle():
         np.testing.assert_array_equal(hist2[k], hist1[k])
         np.testing.assert_array_equal(hist2[k], r.C_hist[k])     # bit-identical to the oracle
         assert np.array_equal(hist2[k], hist2[k].T)
+
+
+def emulate_2d(A, p, iters, grows, gcols, rank, row_gather=None, col_gather=None, all_gather=None, tm=128, tn=256):
+    """The 2-D P_r x P_c grid's data flow of the engine (literal form, FP64): rank
+    (r, c) owns the block (R_r, S_c) of C and of every T_j; Chat row panels gather along the grid row,
+    T_{j-1} column panels along the grid column before every GEMM, each residual partial is taken
+    from the rank owning its tile (global slot order tn * tiles_m + tm, as k_select_partials)."""
+    n = A.shape[0]
+    world = grows * gcols
+    unit = 256 * world
+    npad = (n + unit - 1) // unit * unit
+    mr, kp = npad // grows, npad // gcols
+    r, c = rank // gcols, rank % gcols
+    rows, cols = slice(r * mr, (r + 1) * mr), slice(c * kp, (c + 1) * kp)
+    tiles_m, tiles_n = npad // tm, npad // tn
+    Ap = np.zeros((npad, npad)); Ap[:n, :n] = A
+    n1, ninf, _ = oracle.norms(A)
+    ph = oracle.phase(oracle.FP64)
+    C_blk = oracle.c0(Ap, n1 * ninf, ph)[rows, cols]
+
+    def row_panel(blk):          # C[R_r, :] from the grid row's blocks, in grid-column order
+        return blk.copy() if row_gather is None else np.concatenate(row_gather(blk), axis=1)
+
+    def col_panel(blk):          # T[:, S_c] from the grid column's blocks, in grid-row order
+        return blk.copy() if col_gather is None else np.concatenate(col_gather(blk), axis=0)
+
+    def block_product(Cr, X):    # (C X)[R_r, S_c] with the oracle's per-element k order
+        Cf = np.zeros((npad, npad)); Cf[rows, :] = Cr
+        Xf = np.zeros((npad, npad)); Xf[:, cols] = X
+        Z = np.zeros((npad, npad)); oracle.gemm_cols(Cf, Xf, Z, c * kp, (c + 1) * kp)
+        return Z[rows, cols]
+
+    hist, rhos = [], []
+    for k in range(iters):
+        Cr = row_panel(C_blk)
+        X = Ap[:, cols]
+        for j in range(p):
+            T_blk = block_product(Cr, X)
+            X = col_panel(T_blk)
+        # residual partials of this rank's tiles at their GLOBAL slots
+        I = np.eye(npad)[rows, cols]
+        D = I - T_blk
+        gi = np.arange(r * mr, (r + 1) * mr)[:, None]
+        gj = np.arange(c * kp, (c + 1) * kp)[None, :]
+        D = np.where((gi < n) & (gj < n), D, 0.0)
+        part = np.zeros(tiles_m * tiles_n)
+        for a in range(kp // tn):
+            for b in range(mr // tm):
+                blk = D[b * tm:(b + 1) * tm, a * tn:(a + 1) * tn]
+                part[(c * kp // tn + a) * tiles_m + r * mr // tm + b] = np.sum(blk * blk)
+        parts = [part] if all_gather is None else all_gather(part)
+        sel = np.empty_like(part)
+        for sl in range(part.size):
+            tnn, tmm = sl // tiles_m, sl % tiles_m
+            owner = ((tmm * tm) // mr) * gcols + (tnn * tn) // kp
+            sel[sl] = parts[owner][sl]
+        rho = 0.0
+        for v in sel:
+            rho += v
+        rhos.append(np.sqrt(rho))
+        P_blk = block_product(Cr, X)
+        C_blk = oracle.qm((float(p + 1) * C_blk - P_blk) / float(p), 11, 52)
+        blocks = [C_blk] if all_gather is None else all_gather(C_blk)
+        hist.append(blocks)
+    return hist, rhos, (npad, mr, kp)
+
+
+def _worker_2d(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = synth.spd(300, 2.0, 23)
+        row_groups = [dist.new_group([0, 1]), dist.new_group([2, 3])]
+        col_groups = [dist.new_group([0, 2]), dist.new_group([1, 3])]
+
+        def gatherer(group, size):
+            def g(arr):
+                t = torch.from_numpy(np.ascontiguousarray(arr))
+                out = [torch.empty_like(t) for _ in range(size)]
+                dist.all_gather(out, t, group=group)
+                return [o.numpy() for o in out]
+            return g
+
+        hist, rhos, dims = emulate_2d(A, 2, 4, 2, 2, rank, row_gather=gatherer(row_groups[rank // 2], 2),
+                                      col_gather=gatherer(col_groups[rank % 2], 2), all_gather=gatherer(None, 4))
+        if rank == 0:
+            q.put(("ok", hist, rhos, dims))
+    except Exception as e:
+        if rank == 0:
+            q.put(("err", repr(e), None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world4_gloo_2d_grid_matches_oracle():
+    # the 2 x 2 grid option: every iterate assembled from the four blocks is bit-identical to the
+    # single-process oracle trajectory of Eq. (1), and rho reduced from owner-selected partials in slot
+    # order equals the one-rank value bit for bit
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_2d, args=(r, 4, port, q)) for r in range(4)]
+    for pr in procs:
+        pr.start()
+    status, hist, rhos, dims = q.get(timeout=600)
+    for pr in procs:
+        pr.join(timeout=300)
+    assert status == "ok", hist
+    assert all(pr.exitcode == 0 for pr in procs)
+    npad, mr, kp = dims
+    A = synth.spd(300, 2.0, 23)
+    r = oracle.solve(A, 2, [oracle.phase()], 0.0, 5, hist=5)
+    hist1, rhos1, _ = emulate_2d(A, 2, 4, 1, 1, 0, all_gather=lambda a: [a])
+    for k in range(4):
+        full = np.zeros((npad, npad))
+        for rank, blk in enumerate(hist[k]):
+            rr, cc = rank // 2, rank % 2
+            full[rr * mr:(rr + 1) * mr, cc * kp:(cc + 1) * kp] = blk
+        np.testing.assert_array_equal(full[:300, :300], r.C_hist[k + 1])
+        np.testing.assert_array_equal(full[:300, :300], hist1[k][0][:300, :300])
+    assert rhos == rhos1
+    np.testing.assert_allclose(rhos, r.rho[:4], rtol=1e-13)
