@@ -193,7 +193,7 @@ __host__ __device__ constexpr uint32_t make_idesc(int prec) {
 // accumulator word -> FP64 (exact): FP32 bits, or INT32 for kind::i8
 template <int KIND>
 __device__ __forceinline__ double acc_to_f64(uint32_t w) {
-  return KIND == 3 ? (double)(int32_t)w : (double)__uint_as_float(w);
+  return KIND == 3 ? (double)(int32_t)w : f32bits_to_f64(w);
 }
 
 struct TileSched {      // pair tiles: tiles_m pair-rows (256 rows) x tiles_n (256 columns)
@@ -375,7 +375,29 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
        ((mode & EPI_TSCRATCH) && (mode & ~(EPI_TSCRATCH | EPI_DIAG_MINUS | EPI_RESID)) == 0))) {
     const bool ts = (mode & EPI_TSCRATCH) != 0;
     const bool dm = (mode & EPI_DIAG_MINUS) != 0, rsd = (mode & EPI_RESID) != 0;
-    if (!ts && g.tprec == P_BF16) {
+    if (!ts && g.tprec == P_BF16 && KIND != 3 && scale >= 0x1p-126 && scale <= 0x1p127) {
+      // the R value 0 - v (v = acc * scale, a power of two) is an exact float: round it to BF16 from FP32
+      // (the same single rounding as from FP64; no F2F per element), FP64 only for the residual sum
+      __nv_bfloat16 *t = (__nv_bfloat16 *)g.tout;
+      const float sf = (float)scale;
+      uint32_t pk[16];
+      #pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float fv = __fmul_rn(__uint_as_float(r[j]), sf);
+        const float fw = dm ? __fsub_rn(0.0f, fv) : fv;       // row < gc: off the diagonal
+        const __nv_bfloat16 b = __float2bfloat16_rn(fw);
+        t[(col + j) * g.ldt + row] = b;
+        const uint32_t bits = (uint32_t)__bfloat16_as_ushort(b);
+        pk[j >> 1] = (j & 1) ? (pk[j >> 1] | (bits << 16)) : bits;
+        if (rsd && row < g.n && g.col0 + col + j < g.n) {
+          const double d = f32bits_to_f64(__float_as_uint(__fsub_rn(0.0f, fv)));   // 0 - v, exact
+          ea.r2 = __fma_rn(2.0 * d, d, ea.r2);
+        }
+      }
+      uint4 *m = (uint4 *)((__nv_bfloat16 *)g.mout + row * g.ldm + col);
+      #pragma unroll
+      for (int q = 0; q < 4; ++q) m[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    } else if (!ts && g.tprec == P_BF16) {
       __nv_bfloat16 *t = (__nv_bfloat16 *)g.tout;
       uint32_t pk[16];
       #pragma unroll
@@ -417,7 +439,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
             if (rsd && row < g.n && g.col0 + col + j < g.n) {
               const double v = scale == 1.0 ? acc_to_f64<KIND>(r[j]) : __dmul_rn(acc_to_f64<KIND>(r[j]), scale);
               ea.r2 = __fma_rn(-2.0 * v, -v, ea.r2);   // d = 0 - v: 2 d d with the same rounding
-            }
+            }   // (acc_to_f64: the integer-pipe conversion, f32bits_to_f64)
           }
           m[q] = make_float4(f[0], f[1], f[2], f[3]);
         }
