@@ -151,11 +151,15 @@ __device__ __forceinline__ uint64_t d2bits(double x) { return (uint64_t)__double
 // pipe, which per-element FP64 epilogues saturated (ncu r02: XU 41 % in the tri GEMM, "math pipe
 // throttle" its top stall).  Normal numbers and zeros re-bias the exponent and shift the mantissa
 // (exact); subnormals / Inf / NaN take the F2F.
+// (the rare cases go through a non-inlined call so the compiler cannot if-convert them into a per-element
+// F2F; r02e measured the inlined fallback at XU 56 %, slower than plain F2F)
+static __device__ __noinline__ double f2d_rare(uint32_t u) { return (double)__uint_as_float(u); }
+static __device__ __noinline__ float d2f_rare(double x) { return (float)x; }
 __device__ __forceinline__ double f32bits_to_f64(uint32_t u) {
   const uint32_t e = (u >> 23) & 0xffu, m = u & 0x7fffffu;
-  if (e - 1u < 254u) return __hiloint2double((int)((u & 0x80000000u) | ((e + 896u) << 20) | (m >> 3)), (int)(m << 29));
-  if ((u << 1) == 0u) return __hiloint2double((int)(u & 0x80000000u), 0);
-  return (double)__uint_as_float(u);
+  const uint32_t E = e == 0u ? 0u : e + 896u;                       // zero: sign only (m = 0)
+  if ((e == 0u && m != 0u) || e == 255u) return f2d_rare(u);       // subnormal / Inf / NaN
+  return __hiloint2double((int)((u & 0x80000000u) | (E << 20) | (m >> 3)), (int)(m << 29));
 }
 __device__ __forceinline__ double f2d(float x) { return f32bits_to_f64(__float_as_uint(x)); }
 // an FP64 value that is exactly an FP32 number (e.g. q_m-rounded in the e8 container) -> that float, on
@@ -163,9 +167,9 @@ __device__ __forceinline__ double f2d(float x) { return f32bits_to_f64(__float_a
 __device__ __forceinline__ float d2f_exact(double x) {
   const uint32_t hi = (uint32_t)__double2hiint(x), lo = (uint32_t)__double2loint(x);
   const uint32_t e = (hi >> 20) & 0x7ffu;
-  if (e - 897u < 254u) return __uint_as_float((hi & 0x80000000u) | ((e - 896u) << 23) | ((hi & 0xfffffu) << 3) | (lo >> 29));
   if (((hi << 1) | lo) == 0u) return __uint_as_float(hi & 0x80000000u);
-  return (float)x;
+  if (e - 897u >= 254u) return d2f_rare(x);                           // float subnormal / Inf / NaN range
+  return __uint_as_float((hi & 0x80000000u) | ((e - 896u) << 23) | ((hi & 0xfffffu) << 3) | (lo >> 29));
 }
 
 // Round the magnitude bits `mag` of an IEEE encoding to keep `s` fewer low bits.

@@ -741,14 +741,10 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
   }
   CK(cudaMemcpyAsync(c->hscal, c->dscal, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
-  float t = 0.f, tu = 0.f;
-  CK(cudaEventElapsedTime(&t, c->ev[0], c->ev[1]));
-  c->kern_ms = 0.0;
-  for (int i = 0; i < c->ktimer.used; ++i) {
-    float tk = 0.f;
-    CK(cudaEventElapsedTime(&tk, c->kev[2 * i], c->kev[2 * i + 1]));
-    c->kern_ms += tk;
-  }
+  // only what the decision needs before the next enqueue: the chain's own timers (ev[0], ev[1], the CRT
+  // kernel pairs) are read by chain_timers() after the update is on the stream -- every host microsecond
+  // between this sync and the update's first launch is a GPU bubble (r02: ~28 per solve)
+  float tu = 0.f;
   if (c->upd_timed) { CK(cudaEventElapsedTime(&tu, c->ev[2], c->ev[3])); c->upd_timed = false; }
   if (c->pending_delta >= 0) {
     c->trace[c->pending_delta].delta = std::sqrt(c->hscal[1]);
@@ -757,7 +753,22 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
     c->pending_delta = -1;
   }
   *rho_out = std::sqrt(c->hscal[0]);
-  *ms = t;
+  *ms = 0.f;
+  return IPR_OK;
+}
+
+// the last chain's device times (its events are not re-recorded before the next chain)
+ipr_status chain_timers(ipr_ctx *c, ipr_record &r) {
+  float t = 0.f;
+  CK(cudaEventElapsedTime(&t, c->ev[0], c->ev[1]));
+  double km = 0.0;
+  for (int i = 0; i < c->ktimer.used; ++i) {
+    float tk = 0.f;
+    CK(cudaEventElapsedTime(&tk, c->kev[2 * i], c->kev[2 * i + 1]));
+    km += tk;
+  }
+  r.gemm_ms += t;
+  if (r.prec == IPR_FP64_CRT) r.kern_ms = km;
   return IPR_OK;
 }
 
@@ -1330,11 +1341,12 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     r.k = (int)c->trace.size(); r.phase = phase_now; r.prec = c->ph[phase_now].prec; r.mant_bits = c->m_of_cur;
     r.decision = d; r.rho = rho; r.rho_hat = rho / std::sqrt((double)c->n); r.delta = NAN; r.gemm_ms = ms;
     r.rho_cert = NAN; r.upd_ms = 0.0;
-    r.kern_ms = c->ph[phase_now].prec == IPR_FP64_CRT ? c->kern_ms : 0.0;
+    r.kern_ms = 0.0;                           // chain_timers() fills gemm_ms / kern_ms
     r.digits = is_emu(c->ph[phase_now].prec) ? c->last_chain_S : 0;
     r.moduli = c->ph[phase_now].prec == IPR_FP64_CRT ? crt_moduli(crt_bits(c->last_chain_S, c->n), c->n) : 0;
     c->trace.push_back(r);
     *iters_done += 1;
+    if (d != IPR_DEC_CONTINUE) CKS(chain_timers(c, c->trace.back()));
     if (d == IPR_DEC_CONVERGED && c->form == IPR_FORM_COUPLED) {
       // rho = ||I - M_k||_F tracks ||I - X_k^p A||_F only up to drift: certify X_k itself with the
       // FP64 literal chain on DMMA (R-3, R-27; the computation ipr_residual(certify = 1) runs); if it
@@ -1390,6 +1402,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     if (d == IPR_DEC_CONTINUE) {
       CKS(step_update(c));
       c->pending_delta = (int64_t)c->trace.size() - 1;
+      CKS(chain_timers(c, c->trace.back()));   // after the update is enqueued: no bubble
     } else if (d == IPR_DEC_SWITCH) {
       if (c->best_loc < 0) { c->best_loc = c->cur; c->best_cont64 = is_f64(c->ph[c->phase].prec); }
       CKS(save_best(c));
