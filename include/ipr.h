@@ -150,6 +150,9 @@ typedef struct {
   double kern_ms;    /* IPR_FP64_CRT: device time of the chain's kind::i8 modulus GEMM launches  */
                      /* alone (CUDA events; the residue splits and the CRT reconstruction are   */
                      /* the rest of gemm_ms - upd_ms); 0 otherwise                              */
+  double gap_ms;     /* device time between this chain's residual being ready and its update's   */
+                     /* first kernel: the host round trip of the controller (decision + enqueue)  */
+                     /* the GPU waits for (CUDA events); NaN when no update followed            */
 } ipr_record;
 
 /* Create a context for an n x n SPD matrix A (FP64, row-major, device, leading dimension

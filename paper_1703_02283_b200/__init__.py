@@ -63,7 +63,7 @@ class ipr_record(C.Structure):
                 ("decision", C.c_int), ("rho", C.c_double), ("rho_hat", C.c_double),
                 ("delta", C.c_double), ("gemm_ms", C.c_double), ("upd_ms", C.c_double),
                 ("digits", C.c_int), ("rho_cert", C.c_double), ("moduli", C.c_int),
-                ("kern_ms", C.c_double)]
+                ("kern_ms", C.c_double), ("gap_ms", C.c_double)]
 
 
 def _load():
@@ -244,7 +244,8 @@ def ipr_get_trace(ctx):
     _check(_lib.ipr_get_trace(ctx, buf, cnt.value, C.byref(cnt)), ctx)
     return [dict(k=r.k, phase=r.phase, prec=PREC_NAMES[r.prec], mant_bits=r.mant_bits,
                  decision=r.decision, rho=r.rho, rho_hat=r.rho_hat, delta=r.delta, gemm_ms=r.gemm_ms,
-                 upd_ms=r.upd_ms, digits=r.digits, rho_cert=r.rho_cert, moduli=r.moduli, kern_ms=r.kern_ms)
+                 upd_ms=r.upd_ms, digits=r.digits, rho_cert=r.rho_cert, moduli=r.moduli, kern_ms=r.kern_ms,
+                 gap_ms=r.gap_ms)
             for r in buf[:cnt.value]]
 
 

@@ -147,7 +147,7 @@ struct ipr_ctx {
   std::vector<ipr_record> trace;
   void *arena = nullptr;                // every O(n^2) buffer: ONE pool allocation at the first ipr_iterate
   void *aux = nullptr;                  // the small device buffers (flag, scalars, sigmas, colsum)
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};   // [4]: chain's results ready
   cudaEvent_t kev[16] = {};             // CRT: event pairs around the kind::i8 GEMM launches of a chain
   CrtTimer ktimer{kev, 8, 0};
   bool upd_timed = false;
@@ -739,19 +739,27 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
     CKS(gather_partials(c, part, tn_loc * tm, (int)gemm_tile_m(prec), (int)gemm_tile_n(prec)));
     CK(launch_reduce_sum(part, tiles_n_total(c, prec) * tm, c->dscal + 0, c->st));
   }
+  CK(cudaEventRecord(c->ev[4], c->st));      // the GPU has the chain's residual: the decision's bubble starts
   CK(cudaMemcpyAsync(c->hscal, c->dscal, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   // only what the decision needs before the next enqueue: the chain's own timers (ev[0], ev[1], the CRT
   // kernel pairs) are read by chain_timers() after the update is on the stream -- every host microsecond
   // between this sync and the update's first launch is a GPU bubble (r02: ~28 per solve)
-  float tu = 0.f;
-  if (c->upd_timed) { CK(cudaEventElapsedTime(&tu, c->ev[2], c->ev[3])); c->upd_timed = false; }
+  float tu = 0.f, tg = 0.f;
+  if (c->upd_timed) {
+    CK(cudaEventElapsedTime(&tu, c->ev[2], c->ev[3]));
+    CK(cudaEventElapsedTime(&tg, c->ev[5], c->ev[2]));   // device idle from the last chain's end to the update
+    c->upd_timed = false;
+  }
   if (c->pending_delta >= 0) {
     c->trace[c->pending_delta].delta = std::sqrt(c->hscal[1]);
     c->trace[c->pending_delta].gemm_ms += tu;
     c->trace[c->pending_delta].upd_ms = tu;
+    c->trace[c->pending_delta].gap_ms = tg;
     c->pending_delta = -1;
   }
+  // keep this chain's "results ready" timestamp for the gap to its update (ev[4] is re-recorded per chain)
+  std::swap(c->ev[4], c->ev[5]);
   *rho_out = std::sqrt(c->hscal[0]);
   *ms = 0.f;
   return IPR_OK;
@@ -1342,6 +1350,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     r.decision = d; r.rho = rho; r.rho_hat = rho / std::sqrt((double)c->n); r.delta = NAN; r.gemm_ms = ms;
     r.rho_cert = NAN; r.upd_ms = 0.0;
     r.kern_ms = 0.0;                           // chain_timers() fills gemm_ms / kern_ms
+    r.gap_ms = NAN;
     r.digits = is_emu(c->ph[phase_now].prec) ? c->last_chain_S : 0;
     r.moduli = c->ph[phase_now].prec == IPR_FP64_CRT ? crt_moduli(crt_bits(c->last_chain_S, c->n), c->n) : 0;
     c->trace.push_back(r);
@@ -1426,10 +1435,16 @@ ipr_status ipr_get_trace(ipr_ctx *c, ipr_record *buf, int cap, int *count) {
     CK(cudaMemcpyAsync(c->hscal + 1, c->dscal + 1, 8, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     float tu = 0.f;
-    if (c->upd_timed) { CK(cudaEventElapsedTime(&tu, c->ev[2], c->ev[3])); c->upd_timed = false; }
+    float tg = 0.f;
+    if (c->upd_timed) {
+      CK(cudaEventElapsedTime(&tu, c->ev[2], c->ev[3]));
+      CK(cudaEventElapsedTime(&tg, c->ev[5], c->ev[2]));
+      c->upd_timed = false;
+    }
     c->trace[c->pending_delta].delta = std::sqrt(c->hscal[1]);
     c->trace[c->pending_delta].gemm_ms += tu;
     c->trace[c->pending_delta].upd_ms = tu;
+    c->trace[c->pending_delta].gap_ms = tg;
     c->pending_delta = -1;
   }
   *count = (int)c->trace.size();

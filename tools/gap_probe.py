@@ -43,10 +43,12 @@ def main():
         h3 = time.perf_counter()
         t = [ev[0].elapsed_time(ev[i]) for i in (1, 2, 3)]
         chain = sum(r["gemm_ms"] - r["upd_ms"] for r in tr)
+        gaps = [r["gap_ms"] for r in tr if r["gap_ms"] == r["gap_ms"]]
         upd = sum(r["upd_ms"] for r in tr)
         print(f"rep {rep}: total {t[2]:.2f} ms (init {t[0]:.2f}, iterate {t[1] - t[0]:.2f}, finalize {t[2] - t[1]:.2f}); "
               f"records {len(tr)}: chains {chain:.2f} + updates {upd:.2f} = {chain + upd:.2f} ms; "
-              f"iterate - records = {t[1] - t[0] - chain - upd:.2f} ms; host wall init/iter/fin "
+              f"iterate - records = {t[1] - t[0] - chain - upd:.2f} ms; controller bubbles {sum(gaps):.2f} ms over "
+              f"{len(gaps)} updates (max {max(gaps) if gaps else 0:.3f}); host wall init/iter/fin "
               f"{(h1 - h0) * 1e3:.1f}/{(h2 - h1) * 1e3:.1f}/{(h3 - h2) * 1e3:.1f} ms", flush=True)
 
 
