@@ -191,9 +191,10 @@ __host__ __device__ constexpr uint32_t make_idesc(int prec) {
   return (dfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)((2 * TC_BM) >> 4) << 24);
 }
 // accumulator word -> FP64 (exact): FP32 bits, or INT32 for kind::i8
+// (the integer-pipe f32bits_to_f64 measured slower here: 291 -> 321 / 331 us for the FP8 tri GEMM, r02e/f)
 template <int KIND>
 __device__ __forceinline__ double acc_to_f64(uint32_t w) {
-  return KIND == 3 ? (double)(int32_t)w : f32bits_to_f64(w);
+  return KIND == 3 ? (double)(int32_t)w : (double)__uint_as_float(w);
 }
 
 struct TileSched {      // pair tiles: tiles_m pair-rows (256 rows) x tiles_n (256 columns)
@@ -390,7 +391,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
         const uint32_t bits = (uint32_t)__bfloat16_as_ushort(b);
         pk[j >> 1] = (j & 1) ? (pk[j >> 1] | (bits << 16)) : bits;
         if (rsd && row < g.n && g.col0 + col + j < g.n) {
-          const double d = f32bits_to_f64(__float_as_uint(__fsub_rn(0.0f, fv)));   // 0 - v, exact
+          const double d = (double)__fsub_rn(0.0f, fv);   // 0 - v, exact
           ea.r2 = __fma_rn(2.0 * d, d, ea.r2);
         }
       }
