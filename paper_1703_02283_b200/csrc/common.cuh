@@ -147,31 +147,6 @@ struct GemmArgs {
 // ------------------------------------------------------------------------------------
 __device__ __forceinline__ double bits2d(uint64_t b) { return __longlong_as_double((long long)b); }
 __device__ __forceinline__ uint64_t d2bits(double x) { return (uint64_t)__double_as_longlong(x); }
-// FP32 bits -> the same value in FP64, on the integer pipe: the hardware F2F.F64.F32 issues on the XU
-// pipe, which per-element FP64 epilogues saturated (ncu r02: XU 41 % in the tri GEMM, "math pipe
-// throttle" its top stall).  Normal numbers and zeros re-bias the exponent and shift the mantissa
-// (exact); subnormals / Inf / NaN take the F2F.
-// (the rare cases go through a non-inlined call so the compiler cannot if-convert them into a per-element
-// F2F; r02e measured the inlined fallback at XU 56 %, slower than plain F2F)
-static __device__ __noinline__ double f2d_rare(uint32_t u) { return (double)__uint_as_float(u); }
-static __device__ __noinline__ float d2f_rare(double x) { return (float)x; }
-__device__ __forceinline__ double f32bits_to_f64(uint32_t u) {
-  const uint32_t e = (u >> 23) & 0xffu, m = u & 0x7fffffu;
-  const uint32_t E = e == 0u ? 0u : e + 896u;                       // zero: sign only (m = 0)
-  if ((e == 0u && m != 0u) || e == 255u) return f2d_rare(u);       // subnormal / Inf / NaN
-  return __hiloint2double((int)((u & 0x80000000u) | (E << 20) | (m >> 3)), (int)(m << 29));
-}
-__device__ __forceinline__ double f2d(float x) { return f32bits_to_f64(__float_as_uint(x)); }
-// an FP64 value that is exactly an FP32 number (e.g. q_m-rounded in the e8 container) -> that float, on
-// the integer pipe for normal numbers and zeros (F2F.F32.F64 is an XU instruction); else the hardware cvt
-__device__ __forceinline__ float d2f_exact(double x) {
-  const uint32_t hi = (uint32_t)__double2hiint(x), lo = (uint32_t)__double2loint(x);
-  const uint32_t e = (hi >> 20) & 0x7ffu;
-  if (((hi << 1) | lo) == 0u) return __uint_as_float(hi & 0x80000000u);
-  if (e - 897u >= 254u) return d2f_rare(x);                           // float subnormal / Inf / NaN range
-  return __uint_as_float((hi & 0x80000000u) | ((e - 896u) << 23) | ((hi & 0xfffffu) << 3) | (lo >> 29));
-}
-
 // Round the magnitude bits `mag` of an IEEE encoding to keep `s` fewer low bits.
 __device__ __forceinline__ uint64_t round_mag64(uint64_t mag, int s, int rtz) {
   if (s <= 0) return mag;

@@ -191,7 +191,8 @@ __host__ __device__ constexpr uint32_t make_idesc(int prec) {
   return (dfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)((2 * TC_BM) >> 4) << 24);
 }
 // accumulator word -> FP64 (exact): FP32 bits, or INT32 for kind::i8
-// (the integer-pipe f32bits_to_f64 measured slower here: 291 -> 321 / 331 us for the FP8 tri GEMM, r02e/f)
+// (an integer-pipe FP32 -> FP64 conversion measured slower here: 291 -> 321 / 331 us for the FP8 tri GEMM, and
+// 4.5 -> 8.5 ms per solve in k_sym_update, r02e/f/i -- the hardware F2F stays)
 template <int KIND>
 __device__ __forceinline__ double acc_to_f64(uint32_t w) {
   return KIND == 3 ? (double)(int32_t)w : (double)__uint_as_float(w);
@@ -440,7 +441,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
             if (rsd && row < g.n && g.col0 + col + j < g.n) {
               const double v = scale == 1.0 ? acc_to_f64<KIND>(r[j]) : __dmul_rn(acc_to_f64<KIND>(r[j]), scale);
               ea.r2 = __fma_rn(-2.0 * v, -v, ea.r2);   // d = 0 - v: 2 d d with the same rounding
-            }   // (acc_to_f64: the integer-pipe conversion, f32bits_to_f64)
+            }
           }
           m[q] = make_float4(f[0], f[1], f[2], f[3]);
         }
@@ -565,17 +566,25 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
     // a residual far below the phase's floor) the product in FP64 and one rounding, so W never
     // underflows to 0 through the scale itself
     float4 *dst = (float4 *)((float *)g.wout + row * g.ldw + col);
-    const bool f32ok = scale >= 0x1p-126 && scale <= 0x1p127;
-    const float sf = f32ok ? (float)scale : 1.0f;
-    #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      float w[4];
+    if (scale >= 0x1p-126 && scale <= 0x1p127) {       // warp-uniform: one loop or the other
+      const float sf = (float)scale;
       #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float a = KIND == 3 ? (float)(int32_t)r[4 * q + u] : __uint_as_float(r[4 * q + u]);
-        w[u] = f32ok ? __fmul_rn(a, sf) : (float)__dmul_rn(acc_to_f64<KIND>(r[4 * q + u]), scale);
+      for (int q = 0; q < 8; ++q) {
+        float w[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float a = KIND == 3 ? (float)(int32_t)r[4 * q + u] : __uint_as_float(r[4 * q + u]);
+          w[u] = __fmul_rn(a, sf);
+        }
+        dst[q] = make_float4(w[0], w[1], w[2], w[3]);
       }
-      dst[q] = make_float4(w[0], w[1], w[2], w[3]);
+    } else {
+      #pragma unroll 1
+      for (int q = 0; q < 8; ++q) {
+        float w[4];
+        for (int u = 0; u < 4; ++u) w[u] = (float)__dmul_rn(acc_to_f64<KIND>(r[4 * q + u]), scale);
+        dst[q] = make_float4(w[0], w[1], w[2], w[3]);
+      }
     }
   }
   if (mode & (EPI_UPDATE | EPI_NSUPDATE)) {

@@ -402,15 +402,15 @@ __global__ void __launch_bounds__(256, 4) k_sym_update(const CT *__restrict__ co
     const int64_t ci = (ib + r) * kp + jb + c4;
     double wv[4], cv[4], cn[4];
     if (sizeof(WT) == 4) {
-      const float4 a = *(const float4 *)((const float *)wl + ci);   // FP32 -> FP64 on the integer pipe
-      wv[0] = f2d(a.x); wv[1] = f2d(a.y); wv[2] = f2d(a.z); wv[3] = f2d(a.w);
+      const float4 a = *(const float4 *)((const float *)wl + ci);
+      wv[0] = a.x; wv[1] = a.y; wv[2] = a.z; wv[3] = a.w;
     } else {
       const double2 a = *(const double2 *)((const double *)wl + ci), b = *(const double2 *)((const double *)wl + ci + 2);
       wv[0] = a.x; wv[1] = a.y; wv[2] = b.x; wv[3] = b.y;
     }
     if (sizeof(CT) == 4) {
       const float4 a = *(const float4 *)((const float *)cold + ci);
-      cv[0] = f2d(a.x); cv[1] = f2d(a.y); cv[2] = f2d(a.z); cv[3] = f2d(a.w);
+      cv[0] = a.x; cv[1] = a.y; cv[2] = a.z; cv[3] = a.w;
     } else {
       const double2 a = *(const double2 *)((const double *)cold + ci), b = *(const double2 *)((const double *)cold + ci + 2);
       cv[0] = a.x; cv[1] = a.y; cv[2] = b.x; cv[3] = b.y;
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(256, 4) k_sym_update(const CT *__restrict__ co
     bool ok = true;
     #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      const double sw = __dadd_rn(wv[v], sizeof(WT) == 4 ? f2d((float)t[c4 + v][r]) : (double)t[c4 + v][r]);
+      const double sw = __dadd_rn(wv[v], (double)t[c4 + v][r]);
       const double e = pow2p ? __dmul_rn(sw, itp) : __ddiv_rn(sw, tp);   // d/(2p); exact recip. for 2^k
       xv[v] = __dadd_rn(cv[v], e);
       cn[v] = sizeof(CT) == 8 ? q_e11_fast(xv[v], qr, ok) : q_e8d_fast(xv[v], qr, ok);
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(256, 4) k_sym_update(const CT *__restrict__ co
     for (int v = 0; v < 4; ++v) {
       const double dd = __dsub_rn(cn[v], cv[v]);
       d2 = __fma_rn(dd, dd, d2);
-      cf[v] = sizeof(CT) == 4 ? d2f_exact(cn[v]) : (float)cn[v];
+      cf[v] = (float)cn[v];                               // exact for the e8 container
       mx = fmaxf(mx, fabsf(cf[v]));                       // as k_maxabs_cont: fmaxf drops NaN
     }
     if (sizeof(CT) == 4) {
