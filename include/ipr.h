@@ -14,7 +14,7 @@
  * PAPER.md:256-261, Sec. 4.3.1), ending with FP64 refinement.
  *
  * Readings of passages the paper leaves open (product order, update form, rounding,
- * controller rules, forms, emulated FP64, certificates ...) are numbered R-1 ... R-30 in DESIGN.md and cited below.
+ * controller rules, forms, emulated FP64, certificates ...) are numbered R-1 ... R-32 in DESIGN.md and cited below.
  *
  * General conventions
  *  - Every function returns ipr_status (IPR_OK == 0).  No function aborts the process and
@@ -197,8 +197,8 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
  * mu_ij = 1 - (x_i g_ij + x_j g_ji)/(2p) (|mu| <= 0.03 at kappa = 2, < 1 up to kappa ~ 34 for
  * p = 2), so low-precision noise is damped in the FP64 phase instead of persisting.
  * The trace's rho is rho_s; when it meets final_tol in the last phase the engine certifies
- * ||I - C_k^p A||_F (record.rho_cert, see ipr_set_cert; by default the literal chain C (C A) on the
- * FP64 DMMA pipe -- exactly the computation of ipr_residual(certify = 1)): converged iff that is <=
+ * ||I - C_k^p A||_F (record.rho_cert, see ipr_set_cert; by default on the FP64 DMMA pipe -- exactly
+ * the computation of ipr_residual(certify = 1)): converged iff that is <=
  * final_tol, and the certified C_k is the answer ipr_finalize returns; else the iteration continues
  * from C_{k+1}.
  *
@@ -221,8 +221,10 @@ ipr_status ipr_set_form(ipr_ctx *c, int form);
 
 /* Convergence certificate of the symmetric and coupled forms, whose in-chain residual is not the
  * north-star residual ||I - C^p A||_F (reading R-3; R-30).  Call before the first ipr_iterate.
- *  IPR_CERT_FP64 (default): ||I - C_k^p A||_F of the candidate C_k by the literal chain T_1 = C A,
- *    T_j = C T_{j-1} on the FP64 DMMA pipe (p GEMMs, deterministic), the same function that
+ *  IPR_CERT_FP64 (default): ||I - C_k^p A||_F of the candidate C_k on the FP64 DMMA pipe
+ *    (deterministic): p = 2 as ||I - Y A||_F with Y = C C computed on its upper tiles and mirrored
+ *    (C and so Y are bitwise symmetric; 1.5 GEMMs; R-32), other p by the literal chain
+ *    T_1 = C A, T_j = C T_{j-1} (p GEMMs) -- the same function that
  *    ipr_residual(certify = 1) runs on the returned iterate -- so for a converged solve the two agree
  *    bit for bit, and "converged" means that FP64 residual is <= final_tol.
  *  IPR_CERT_PHASE: the same residual from the FP64-range phase's own product (IPR_FP64_CRT / _OZ: the
@@ -239,9 +241,10 @@ ipr_status ipr_set_cert(ipr_ctx *c, int mode);
 ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *outcome);
 
 /* certify == 0: the in-chain residual of the latest evaluated iterate (reading R-4).
- * certify == 1: ||I - C_best^p A||_F recomputed with FP64 DMMA GEMMs (the literal chain, the last
- * GEMM keeping only its residual partials) from the best iterate (the one ipr_finalize returns),
- * reading R-3 -- the IPR_CERT_FP64 certificate, bit for bit. */
+ * certify == 1: ||I - C_best^p A||_F recomputed with FP64 DMMA GEMMs from the best iterate (the one
+ * ipr_finalize returns), the last GEMM keeping only its residual partials (reading R-3) -- the
+ * form's own FP64 certificate, bit for bit: the literal form's FP64 chain C (C A) (its in-chain
+ * rho), the symmetric / coupled forms' IPR_CERT_FP64 ((C C) A for p = 2, R-32). */
 ipr_status ipr_residual(ipr_ctx *c, int certify, double *rho);
 
 /* Copy up to cap trace records; *count = total records so far (may exceed cap). */

@@ -1376,7 +1376,8 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     }
     if (d == IPR_DEC_CONVERGED && is_sym(c)) {
       // rho_s = ||I - C^{p-1}AC||_F met final_tol: certify ||I - C_k^p A||_F (R-3, R-30).
-      //  IPR_CERT_FP64 (default): the literal chain C (C A) on the FP64 DMMA pipe -- the same function
+      //  IPR_CERT_FP64 (default): ||I - C^p A||_F on the FP64 DMMA pipe (p = 2: (C C) A with C C on its
+      //    upper tiles, reading R-32; else the literal chain C (C A)) -- the same function
       //    ipr_residual(certify = 1) runs, so a converged solve's re-check equals its certificate bit
       //    for bit.  p = 2: the certification stores only T_1 (T[1]); R (T[p & 1] = T[0]) survives, so
       //    the update runs only if the certification misses.
@@ -1518,14 +1519,40 @@ static ipr_status certify_full64(ipr_ctx *c, double *rho) {
   Nvtx nv("certify fp64 dmma");
   PhaseC P64{IPR_FP64, 52, 0, 1, 0, 0, 0, 0};
   CKS(stage_a(c, P64, c->Acert, c->dsig + 0));
-  const void *X = c->Acert;
-  for (int j = 1; j <= c->p; ++j) {
-    GemmArgs g = base_args(c, IPR_FP64, X);
+  if (c->p == 2 && c->form != IPR_FORM_LITERAL) {
+    // reading R-32: ||I - Y A||_F with Y = C C.  C is bitwise symmetric, so the DMMA product Y is too
+    // (each Y_ij and Y_ji is the same K-ordered sum of the same products; tests/test_gpu_certify.py):
+    // G = 1 computes only its upper tiles and mirrors them (tri), a G > 1 rank its full column panel,
+    // then all-gathers Y -- the same bits.  1.5 DMMA GEMMs instead of the chain's 2.  The literal
+    // form keeps the chain C (C A): its FP64 phase's in-chain rho is that chain and IS its certificate.
+    GemmArgs g = base_args(c, IPR_FP64, c->full64);   // G = 1: C is its own K-major form
     g.A = c->full64; g.a_kp = c->kp; g.a_pstride = c->npad * c->kp;
-    g.mode = j == c->p ? EPI_RESID : EPI_STORE_T;
-    g.tout = c->T[j & 1]; g.ldt = c->npad; g.part = c->part;
+    double *Y = (double *)c->T[1];
+    if (c->world == 1) {
+      g.tri = 1; g.mode = EPI_STORE_T; g.tout = Y; g.ldt = c->npad;   // Y row-major (= its transpose)
+    } else {
+      // B(k, j) = C[col0 + j][k]: row col0 + j of the gathered panel-major C, a paneled B view (T[0]
+      // holds R, which the update needs if the certificate misses)
+      g.B = c->full64 + (size_t)c->col0 * c->kp; g.ldb = c->kp; g.b_kp = c->kp; g.b_pstride = c->npad * c->kp;
+      g.mode = EPI_STORE_N; g.nout = Y; g.ldn = c->kp; // Y[:, S_g] as a [npad][kp] panel
+    }
     CK(run_gemm(c, g));
-    X = c->T[j & 1];
+    if (c->world > 1) CKS(gather_f64(c, Y));           // full64 := Y, panel-major
+    GemmArgs h = base_args(c, IPR_FP64, c->Acert);
+    h.A = c->world == 1 ? (const void *)Y : (const void *)c->full64;
+    h.a_kp = c->kp; h.a_pstride = c->npad * c->kp;
+    h.mode = EPI_RESID; h.part = c->part;
+    CK(run_gemm(c, h));
+  } else {
+    const void *X = c->Acert;
+    for (int j = 1; j <= c->p; ++j) {
+      GemmArgs g = base_args(c, IPR_FP64, X);
+      g.A = c->full64; g.a_kp = c->kp; g.a_pstride = c->npad * c->kp;
+      g.mode = j == c->p ? EPI_RESID : EPI_STORE_T;
+      g.tout = c->T[j & 1]; g.ldt = c->npad; g.part = c->part;
+      CK(run_gemm(c, g));
+      X = c->T[j & 1];
+    }
   }
   const int64_t tm = tiles_m(c, IPR_FP64), tn_loc = c->kp / gemm_tile_n(IPR_FP64);
   CKS(gather_partials(c, c->part, tn_loc * tm));

@@ -186,6 +186,7 @@ cudaError_t launch_gemm_dmma(const GemmArgs &a_in, cudaStream_t s) {
   // the hot-path modes get specialised kernels; anything else uses the runtime-mode build
   if (!a.pmax && a.prec == P_FP64) {
     if (a.mode == EPI_STORE_T) return launch_mode<EPI_STORE_T>(a, s);
+    if (a.mode == EPI_STORE_N) return launch_mode<EPI_STORE_N>(a, s);
     if (a.mode == (EPI_STORE_T | EPI_STORE_N)) return launch_mode<EPI_STORE_T | EPI_STORE_N>(a, s);
     if (a.mode == (EPI_STORE_T | EPI_RESID)) return launch_mode<EPI_STORE_T | EPI_RESID>(a, s);
     if (a.mode == EPI_RESID) return launch_mode<EPI_RESID>(a, s);
