@@ -328,6 +328,27 @@ __device__ __forceinline__ void sym_update_chunk(const GemmArgs &g, int64_t row,
   }
 }
 
+// Residual partials inside the tcgen05 epilogue without FP64 arithmetic.  On sm_100a the FP64 pipe
+// stalls while tcgen05.mma streams (ncu r02: the tri GEMM's DMUL / DADD / DFMA drew 47 % of the
+// epilogue's stall samples as math-pipe throttle, tensor pipe 50 % busy), so w d^2 (w = 1 or 2, exact)
+// of an FP32 d is split exactly by one FMA into p + e and added to a float-float accumulator (TwoSum;
+// hi + lo carries ~48 bits); a chunk's (hi, lo) joins the FP64 partial once per 32 elements.
+__device__ __forceinline__ void ff_add_sq(float &hi, float &lo, float d, float w) {
+  const float p = __fmul_rn(__fmul_rn(d, d), w);
+  const float e = __fmul_rn(__fmaf_rn(d, d, -__fmul_rn(d, d)), w);   // d^2 - fl(d^2), exact
+  const float sm = __fadd_rn(hi, p);
+  const float bb = __fsub_rn(sm, hi);
+  const float er = __fadd_rn(__fsub_rn(hi, __fsub_rn(sm, bb)), __fsub_rn(p, bb));
+  lo = __fadd_rn(lo, __fadd_rn(er, e));
+  hi = sm;
+}
+// the chunk's sum into the FP64 partial; false if it overflowed FP32 (the caller redoes it in FP64)
+__device__ __forceinline__ bool ff_flush(float hi, float lo, double &r2) {
+  if (!(fabsf(hi) <= 3.0e38f)) return false;
+  r2 = __dadd_rn(r2, __dadd_rn((double)hi, (double)lo));
+  return true;
+}
+
 // One 32-column chunk of one accumulator row: the fused epilogue with vectorised row access.
 template <int KIND>
 __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_t col, const uint32_t (&r)[32],
@@ -347,8 +368,13 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
     return;
   }
   if (mode & EPI_COUPLED) {           // coupled form: the generic per-element FP64 epilogue
+    // a copy for the rolled loop: dynamic indexing of r itself would put every epilogue's accumulator
+    // registers in local memory (a 128-byte stack frame and 8 STL.128 per chunk in all modes)
+    uint32_t rl[32];
+    #pragma unroll
+    for (int j = 0; j < 32; ++j) rl[j] = r[j];
     #pragma unroll 1
-    for (int j = 0; j < 32; ++j) epi_element<-1>(g, row, col + j, __dmul_rn(acc_to_f64<KIND>(r[j]), scale), ea);
+    for (int j = 0; j < 32; ++j) epi_element<-1>(g, row, col + j, __dmul_rn(acc_to_f64<KIND>(rl[j]), scale), ea);
     return;
   }
   // ---- FP32 fast paths (no FP64 arithmetic; results identical to the general path below) ----
@@ -383,6 +409,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
       __nv_bfloat16 *t = (__nv_bfloat16 *)g.tout;
       const float sf = (float)scale;
       uint32_t pk[16];
+      float rh = 0.f, rlo = 0.f;
       #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const float fv = __fmul_rn(__uint_as_float(r[j]), sf);
@@ -391,10 +418,15 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
         t[(col + j) * g.ldt + row] = b;
         const uint32_t bits = (uint32_t)__bfloat16_as_ushort(b);
         pk[j >> 1] = (j & 1) ? (pk[j >> 1] | (bits << 16)) : bits;
-        if (rsd && row < g.n && g.col0 + col + j < g.n) {
-          const double d = (double)__fsub_rn(0.0f, fv);   // 0 - v, exact
-          ea.r2 = __fma_rn(2.0 * d, d, ea.r2);
-        }
+        if (rsd && row < g.n && g.col0 + col + j < g.n) ff_add_sq(rh, rlo, fv, 2.0f);   // 2 (0 - v)^2
+      }
+      if (rsd && !ff_flush(rh, rlo, ea.r2)) {
+        #pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (row < g.n && g.col0 + col + j < g.n) {
+            const double d = __dsub_rn(0.0, __dmul_rn(acc_to_f64<KIND>(r[j]), scale));
+            ea.r2 = __fma_rn(2.0 * d, d, ea.r2);
+          }
       }
       uint4 *m = (uint4 *)((__nv_bfloat16 *)g.mout + row * g.ldm + col);
       #pragma unroll
@@ -427,6 +459,10 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
         // float as (float)(acc * scale) in FP64, as in (b)); FP64 only for the residual, from the
         // exact product -- the same values and order as below, fewer dependent FP64 operations
         const float sf = (float)scale;
+        // FP32 residual terms need v = acc * scale exact in FP32: FP32 accumulators (not INT32) and a
+        // normal-range scale (warp-uniform); otherwise the FP64 terms
+        const bool f32r = KIND != 3 && scale >= 0x1p-126 && scale <= 0x1p127;
+        float rh = 0.f, rlo = 0.f;
         #pragma unroll
         for (int q = 0; q < 8; ++q) {
           float f[4];
@@ -439,11 +475,23 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
             ea.mx = fmaxf(ea.mx, fabsf(f[u]));
             t[(col + j) * g.ldt + row] = f[u];
             if (rsd && row < g.n && g.col0 + col + j < g.n) {
-              const double v = scale == 1.0 ? acc_to_f64<KIND>(r[j]) : __dmul_rn(acc_to_f64<KIND>(r[j]), scale);
-              ea.r2 = __fma_rn(-2.0 * v, -v, ea.r2);   // d = 0 - v: 2 d d with the same rounding
+              if (f32r) {
+                ff_add_sq(rh, rlo, fv, 2.0f);          // d = 0 - v: 2 d^2
+              } else {
+                const double v = scale == 1.0 ? acc_to_f64<KIND>(r[j]) : __dmul_rn(acc_to_f64<KIND>(r[j]), scale);
+                ea.r2 = __fma_rn(-2.0 * v, -v, ea.r2);
+              }
             }
           }
           m[q] = make_float4(f[0], f[1], f[2], f[3]);
+        }
+        if (rsd && f32r && !ff_flush(rh, rlo, ea.r2)) {
+          #pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (row < g.n && g.col0 + col + j < g.n) {
+              const double v = __dmul_rn(acc_to_f64<KIND>(r[j]), scale);
+              ea.r2 = __fma_rn(-2.0 * v, -v, ea.r2);
+            }
         }
         return;
       }
@@ -496,11 +544,25 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
     const bool ts = (mode & EPI_TSCRATCH) != 0, dm = (mode & EPI_DIAG_MINUS) != 0, rsd = (mode & EPI_RESID) != 0;
     float *t = (float *)g.tout;
     float f[32];
+    // off-diagonal elements in FP32 (exact v = acc * scale: FP32 accumulators, normal-range scale;
+    // (float)(0 - v) then equals 0 - fv), the one diagonal element of the row in FP64 as before
+    const bool f32r = KIND != 3 && scale >= 0x1p-126 && scale <= 0x1p127;
+    const float sf = (float)scale;
+    float rh = 0.f, rlo = 0.f;
     #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int64_t gc = gc0 + j;
       f[j] = 0.f;
       if (row > gc) continue;                        // lower triangle: from the mirror
+      if (f32r && row != gc) {
+        const float fv = __fmul_rn(__uint_as_float(r[j]), sf);
+        const float fw = dm ? __fsub_rn(0.0f, fv) : fv;
+        f[j] = ts ? fw : to_tf32(fw);
+        t[(col + j) * g.ldt + row] = f[j];
+        if (ts) ea.mx = fmaxf(ea.mx, fabsf(f[j]));
+        if (rsd && row < g.n && gc < g.n) ff_add_sq(rh, rlo, fv, 2.0f);
+        continue;
+      }
       const double a = acc_to_f64<KIND>(r[j]);
       const double v = scale == 1.0 ? a : __dmul_rn(a, scale);
       const double w = dm ? __dsub_rn((row == gc && row < g.n) ? g.diag : 0.0, v) : v;
@@ -510,6 +572,15 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
       if (rsd && row < g.n && gc < g.n) {
         const double d = __dsub_rn(row == gc ? 1.0 : 0.0, v);
         ea.r2 = __fma_rn(row != gc ? 2.0 * d : d, d, ea.r2);
+      }
+    }
+    if (rsd && f32r && !ff_flush(rh, rlo, ea.r2)) {
+      #pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int64_t gc = gc0 + j;
+        if (row >= gc || row >= g.n || gc >= g.n) continue;
+        const double v = __dmul_rn(acc_to_f64<KIND>(r[j]), scale);
+        ea.r2 = __fma_rn(-2.0 * v, -v, ea.r2);
       }
     }
     float *mr = (float *)g.mout + row * g.ldm + col;   // mirror (row, c), c > row
@@ -579,9 +650,10 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
         dst[q] = make_float4(w[0], w[1], w[2], w[3]);
       }
     } else {
-      #pragma unroll 1
+      #pragma unroll
       for (int q = 0; q < 8; ++q) {
         float w[4];
+        #pragma unroll
         for (int u = 0; u < 4; ++u) w[u] = (float)__dmul_rn(acc_to_f64<KIND>(r[4 * q + u]), scale);
         dst[q] = make_float4(w[0], w[1], w[2], w[3]);
       }
@@ -1134,19 +1206,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
       if (lane == 0) mbar_arrive_cluster(&tempty[buf], 0);
       if (crt || (ozg && gi > 2)) { ++it; continue; }   // partials after the finish only
       // per-tile partials: deterministic (fixed shuffle tree, warps summed in order 0..3)
-      if ((g.mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE | EPI_SYMUPD)) || g.pmax) {
+      const bool need_s = (g.mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE | EPI_SYMUPD)) != 0;
+      if (need_s || g.pmax) {
         double s = (g.mode & EPI_RESID) ? ea.r2 : ea.d2;
         float mx = ea.mx;
-        #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          s += __shfl_xor_sync(0xffffffffu, s, o);
-          mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (need_s) {                                    // FP64 only when a sum partial is wanted
+          #pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         }
+        #pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if (lane == 0) { red[it & 1][hh * 4 + q] = s; redm[it & 1][hh * 4 + q] = mx; }
         asm volatile("bar.sync 1, 256;\n" ::: "memory");
         if (et == 0) {
           const int64_t tile = ((g.col0 + colb) / TC_BN) * g.tiles_m + g.row0 / TC_BM + tile_m;
-          if (g.mode & (EPI_RESID | EPI_UPDATE | EPI_NSUPDATE | EPI_SYMUPD))
+          if (need_s)
           {
             const double *rr = red[it & 1];
             double acc = 0.0;

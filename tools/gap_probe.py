@@ -14,6 +14,7 @@ def main():
     ap.add_argument("--schedule", default=None)
     ap.add_argument("--cert", default="fp64")
     ap.add_argument("--reps", type=int, default=4)
+    ap.add_argument("--trace", action="store_true", help="print the last rep's records")
     a = ap.parse_args()
     import torch
     import bench
@@ -50,6 +51,11 @@ def main():
               f"iterate - records = {t[1] - t[0] - chain - upd:.2f} ms; controller bubbles {sum(gaps):.2f} ms over "
               f"{len(gaps)} updates (max {max(gaps) if gaps else 0:.3f}); host wall init/iter/fin "
               f"{(h1 - h0) * 1e3:.1f}/{(h2 - h1) * 1e3:.1f}/{(h3 - h2) * 1e3:.1f} ms", flush=True)
+    if a.trace:
+        for r in tr:
+            print(f"k={r['k']:3d} ph={r['phase']} dec={r['decision']} rho={r['rho']:.3e} cert={r['rho_cert']:.3e} "
+                  f"m={r['mant_bits']} S={r['digits']} N={r['moduli']} chain={r['gemm_ms'] - r['upd_ms']:.3f} "
+                  f"upd={r['upd_ms']:.3f} kern={r['kern_ms']:.3f} delta={r['delta']:.3e}", flush=True)
 
 
 if __name__ == "__main__":
