@@ -132,8 +132,10 @@ def gemm_peaks():
 
 
 def gemm_count(trace, p):
-    # p GEMMs per evaluated iterate, +1 for every update that followed, +p per FP64 certification
-    return sum(p + (1 if t["decision"] == 0 else 0) + (p if t["rho_cert"] == t["rho_cert"] else 0) for t in trace)
+    # p GEMMs per evaluated chain (none for a certificate-only record, R-33), +1 for every update that
+    # followed, +p per FP64 certification
+    return sum((p if t["rho"] == t["rho"] else 0) + (1 if t["decision"] == 0 else 0) +
+               (p if t["rho_cert"] == t["rho_cert"] else 0) for t in trace)
 
 
 class Clocks:
@@ -197,8 +199,10 @@ def oracle_schedule(name, n):
 
 
 def oracle_gemms(records, p):
-    """GEMMs of an oracle solve: p per chain, +1 per update (decision continue), +p per certification."""
-    return sum(p + (1 if x["decision"] == 0 else 0) + (p if x["rho_cert"] == x["rho_cert"] else 0) for x in records)
+    """GEMMs of an oracle solve: p per chain (none for a certificate-only record, R-33), +1 per update
+    (decision continue), +p per certification."""
+    return sum((p if x["rho"] == x["rho"] else 0) + (1 if x["decision"] == 0 else 0) +
+               (p if x["rho_cert"] == x["rho_cert"] else 0) for x in records)
 
 
 def cpu_baseline(schedule_name, p, n_target, gemms_target=None, n_small=1024, seed=5):

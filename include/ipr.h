@@ -127,14 +127,16 @@ typedef struct {
                            /* relative accuracy (R-22).  Ignored by other forms.    */
 } ipr_phase;
 
-/* Trace record: one per evaluated iterate C_k (one chain of p GEMMs). */
+/* Trace record: one per evaluated iterate C_k (one chain of p GEMMs, or -- reading R-33 -- only the
+ * FP64 certificate of an iterate predicted to converge, when that certificate passed). */
 typedef struct {
   int    k;          /* record index (0-based)                                               */
   int    phase;      /* schedule index of the phase that evaluated C_k                       */
   int    prec;       /* ipr_prec of that phase                                               */
   int    mant_bits;  /* effective m of that phase                                            */
   int    decision;   /* ipr_decision taken after this residual                               */
-  double rho;        /* in-chain ||I - C_k^p A||_F (reading R-4)                             */
+  double rho;        /* in-chain ||I - C_k^p A||_F (reading R-4); NaN for a certificate-only */
+                     /* record (R-33: rho_cert holds the FP64 residual, decision CONVERGED)    */
   double rho_hat;    /* rho / sqrt(n)                                                        */
   double delta;      /* ||C_{k+1} - C_k||_F of the update that followed (NaN if none)        */
   double gemm_ms;    /* device time of this record's GEMMs (chain + update), CUDA events     */
@@ -142,8 +144,9 @@ typedef struct {
                      /* k_sym_update); gemm_ms - upd_ms = the chain's p GEMMs                  */
   int    digits;     /* IPR_FP64_OZ / _CRT: Ozaki digits S of this record's chain (OZ: S(S+1)/2 */
                      /* INT8 digit products per FP64 product; CRT: b = 7 S - 4 bits); else 0     */
-  double rho_cert;   /* IPR_FORM_SYMMETRIC: ||I - C^p A||_F recomputed in FP64 when the      */
-                     /* in-chain rho met final_tol (converged iff rho_cert <= final_tol);    */
+  double rho_cert;   /* symmetric / coupled forms: ||I - C_k^p A||_F recomputed in FP64 when  */
+                     /* the in-chain rho met final_tol, or before the chain when the last    */
+                     /* phase's rate predicted it (R-33); converged iff rho_cert <= final_tol;*/
                      /* NaN otherwise                                                         */
   int    moduli;     /* IPR_FP64_CRT: CRT moduli of this record's chain (INT8 GEMMs per FP64   */
                      /* product); 0 otherwise                                                  */
@@ -232,8 +235,13 @@ ipr_status ipr_set_form(ipr_ctx *c, int form);
  *    ESTIMATE: it is more accurate than the DMMA evaluation (exact integer sums, 2^-b quantisation) but
  *    a different rounding, so ipr_residual(certify = 1) may exceed final_tol for a solve it accepted
  *    (measured: 9.72e-13 accepted, DMMA 1.004e-12, n = 4096, kappa = 5).  Diagnostics only.
+ *  IPR_FP64 triggers the certificate of the symmetric forms in two ways (R-33): when the
+ *    in-chain rho_s of C_k meets final_tol, and -- after an update in the last phase -- when the phase's
+ *    linear rate predicts it, rho_k (rho_k / rho_{k-1}) <= final_tol / 2: then C_{k+1} is certified
+ *    BEFORE its chain, which runs only if the certificate misses (the converged record then has
+ *    rho = NaN).  IPR_CERT_FP64_CHAIN: the same certificate, triggered by the in-chain rho only.
  * Errors: IPR_E_INVALID_ARG (unknown mode), IPR_E_STATE (after the first ipr_iterate). */
-typedef enum { IPR_CERT_FP64 = 0, IPR_CERT_PHASE = 1 } ipr_cert;
+typedef enum { IPR_CERT_FP64 = 0, IPR_CERT_PHASE = 1, IPR_CERT_FP64_CHAIN = 2 } ipr_cert;
 ipr_status ipr_set_cert(ipr_ctx *c, int mode);
 
 /* Run at most max_iters (> 0) chains.  *iters_done = chains evaluated by this call,

@@ -88,6 +88,7 @@ def lib():
         L.orc_step_ns.restype = C.c_double
         L.orc_step_ns.argtypes = [C.c_int64, _dp, _dp, C.POINTER(Phase), _dp, _dp]
         L.orc_jacobi.argtypes = [C.c_int64, _dp, _dp, _dp]
+        L.orc_set_predict_cert.argtypes = [C.c_int]
         L.orc_inv_proot_eig.argtypes = [C.c_int64, _dp, _dp, C.c_int, _dp]
         L.orc_spectral.argtypes = [C.c_int64, _dp, C.c_int, C.c_double, C.c_int, _dp]
         L.orc_fp16_sigma.argtypes = [C.c_double]
@@ -291,11 +292,15 @@ FORM_LITERAL, FORM_NEWTON_SCHULZ, FORM_SYMMETRIC, FORM_SYMMETRIC_TRI, FORM_COUPL
 
 
 def solve(A, p: int, phases, final_tol: float = 1e-12, max_total: int = 200,
-          hist: int = 0, gamma_normA2: float = 0.0, form: int = FORM_LITERAL) -> SolveResult:
+          hist: int = 0, gamma_normA2: float = 0.0, form: int = FORM_LITERAL,
+          predict_cert: bool = True) -> SolveResult:
     """Full controller-driven solve (init + iterations), reading R-5 of DESIGN.md.
     form = FORM_LITERAL (Eq. 1 as printed), FORM_NEWTON_SCHULZ (p = 1, X(2I - AX)) or
-    FORM_SYMMETRIC (p >= 2, C + (W + W^T)/(2p); convergence certified on ||I - C^p A||_F)."""
+    FORM_SYMMETRIC (p >= 2, C + (W + W^T)/(2p); convergence certified on ||I - C^p A||_F).
+    predict_cert: reading R-33 (certificate-first iterates in the symmetric forms' last phase; the
+    GPU's IPR_CERT_FP64) -- False mirrors IPR_CERT_FP64_CHAIN."""
     A = _f64(A)
+    lib().orc_set_predict_cert(1 if predict_cert else 0)
     n = A.shape[0]
     arr = (Phase * len(phases))(*phases)
     recs = (Record * max_total)()

@@ -717,6 +717,13 @@ int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int np
                         cap_rec, nrec, C_best, C_hist, hist_cap, gamma_normA2, s_out);
 }
 
+/* Reading R-33: after an update in the last phase of a symmetric form, the in-phase
+ * linear rate q = rho_k / rho_{k-1} predicts rho_{k+1} ~ rho_k q; when that is <= final_tol / 2 the
+ * next iterate is certified (FP64 literal chain) before its own chain, and the chain runs only if the
+ * certificate misses.  The GPU engine's default (IPR_CERT_FP64); 0 = trigger on the chain only. */
+static int g_predict_cert = 1;
+void orc_set_predict_cert(int on) { g_predict_cert = on != 0; }
+
 int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase *phases,
                    int nphases, double final_tol, int max_total, orc_record *rec, int cap_rec,
                    int *nrec, double *C_best, double *C_hist, int hist_cap, double gamma_normA2,
@@ -764,8 +771,28 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
   /* R-26 state: last residual (any phase), the last two in-phase residuals, the stored m of C */
   double last_rho_hat = NAN, ph_r1 = NAN, ph_r2 = NAN;
   int m_of_C = is_adaptive(&phases[0]) ? 52 : phase_m(&phases[0]);
+  int cert_pending = 0;               /* R-33 */
   for (int k = 0; k < max_total; ++k) {
     const orc_phase *ph = &phases[ctl.phase];
+    double cert_pre = NAN;
+    if (cert_pending) {               /* R-33: the predicted-converged iterate, certificate first */
+      cert_pending = 0;
+      if (C_hist && k < hist_cap) memcpy(C_hist + (int64_t)k * nn, C, (size_t)nn * sizeof(double));
+      const orc_phase ph64 = {ORC_FP64, -1, ORC_RNE, 0.0, 0.0, 0.0, 0, -1};
+      cert_pre = chain(n, p, A, C, &ph64, &w);
+      if (cert_pre <= final_tol) {
+        orc_record r;
+        r.k = k; r.phase = ctl.phase; r.prec = ph->prec; r.mant_bits = m_of_C;
+        r.decision = ORC_CONVERGED; r.rho = NAN; r.rho_hat = NAN; r.delta = NAN;
+        r.gamma = (gamma_normA2 > 0) ? gamma_of(n, C, A, gamma_normA2, g1, g2) : NAN;
+        r.rho_cert = cert_pre;
+        memcpy(C_best, C, (size_t)nn * sizeof(double));   /* the certified iterate is the answer */
+        if (*nrec < cap_rec) rec[*nrec] = r;
+        *nrec += 1;
+        outcome = ORC_CONVERGED;
+        break;
+      }
+    }
     orc_phase ph_k = *ph;             /* the phase with this iteration's storage bits */
     int S_k = orc_digits_for_m(phase_m(ph));
     if (is_adaptive(ph)) {
@@ -792,7 +819,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
     r.k = k; r.phase = phase_now; r.prec = ph->prec; r.mant_bits = m_of_C;
     r.decision = d; r.rho = rho; r.rho_hat = rho / sqrt((double)n); r.delta = NAN;
     r.gamma = (gamma_normA2 > 0) ? gamma_of(n, C, A, gamma_normA2, g1, g2) : NAN;
-    r.rho_cert = NAN;
+    r.rho_cert = cert_pre;
     if (d == ORC_CONVERGED && coupled) {
       /* rho = ||I - M_k||_F tracks ||I - X_k^p A||_F only up to drift: certify on X_k itself
        * (the best iterate), continue with the step if it misses (as the GPU engine does) */
@@ -813,7 +840,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
        * iteration continues from the update computed first (as the GPU engine does). */
       r.delta = update_sym(n, p, C, &ph_k, &w, Cn);
       const orc_phase ph64 = {ORC_FP64, -1, ORC_RNE, 0.0, 0.0, 0.0, 0, -1};
-      r.rho_cert = chain(n, p, A, C, &ph64, &w);
+      r.rho_cert = isfinite(cert_pre) ? cert_pre : chain(n, p, A, C, &ph64, &w);   /* R-33: once */
       if (!(r.rho_cert <= final_tol)) {
         d = ORC_CONTINUE;
         r.decision = d;
@@ -845,6 +872,10 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
     last_rho_hat = rho / sqrt((double)n);
     if (d == ORC_SWITCH) { ph_r1 = NAN; ph_r2 = NAN; }
     else { ph_r2 = ph_r1; ph_r1 = rho; }
+    /* R-33: certify the next iterate first when the last phase's rate predicts it converged */
+    if (d == ORC_CONTINUE && sym && g_predict_cert && ctl.phase == nphases - 1 && isfinite(ph_r1) &&
+        isfinite(ph_r2) && ph_r2 > 0.0 && ph_r1 < ph_r2 && ph_r1 * (ph_r1 / ph_r2) <= 0.5 * final_tol)
+      cert_pending = 1;
     if (*nrec < cap_rec) rec[*nrec] = r;
     *nrec += 1;
     if (d != ORC_CONTINUE && d != ORC_SWITCH) { outcome = d; break; }

@@ -128,6 +128,8 @@ int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int np
  * ||I - X^p A||_F like the symmetric forms.  No scaled formats. */
 enum { ORC_FORM_LITERAL = 0, ORC_FORM_NEWTON_SCHULZ = 1, ORC_FORM_SYMMETRIC = 2,
        ORC_FORM_SYMMETRIC_TRI = 3, ORC_FORM_COUPLED = 4 };
+/* Reading R-33: certificate-first iterates in the last phase of the symmetric forms (default on). */
+void orc_set_predict_cert(int on);
 int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase *phases,
                    int nphases, double final_tol, int max_total, orc_record *rec, int cap_rec,
                    int *nrec, double *C_best, double *C_hist, int hist_cap, double gamma_normA2,

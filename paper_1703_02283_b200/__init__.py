@@ -38,8 +38,9 @@ EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_
             "ipr_test_local_group_create", "ipr_test_local_group_destroy", "ipr_test_init_local",
             "ipr_test_set_guards", "ipr_test_check_guards"]
 IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ, IPR_FORM_SYMMETRIC, IPR_FORM_SYMMETRIC_TRI, IPR_FORM_COUPLED = 0, 1, 2, 3, 4
-IPR_CERT_FP64, IPR_CERT_PHASE = 0, 1
-CERT_BY_NAME = {"fp64": IPR_CERT_FP64, "dmma": IPR_CERT_FP64, "phase": IPR_CERT_PHASE}
+IPR_CERT_FP64, IPR_CERT_PHASE, IPR_CERT_FP64_CHAIN = 0, 1, 2
+CERT_BY_NAME = {"fp64": IPR_CERT_FP64, "dmma": IPR_CERT_FP64, "phase": IPR_CERT_PHASE,
+                "fp64chain": IPR_CERT_FP64_CHAIN}
 FORM_BY_NAME = {"literal": IPR_FORM_LITERAL, "newton_schulz": IPR_FORM_NEWTON_SCHULZ, "ns": IPR_FORM_NEWTON_SCHULZ,
                 "symmetric": IPR_FORM_SYMMETRIC, "sym": IPR_FORM_SYMMETRIC,
                 "symmetric_tri": IPR_FORM_SYMMETRIC_TRI, "symtri": IPR_FORM_SYMMETRIC_TRI,

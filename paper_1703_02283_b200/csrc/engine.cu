@@ -152,6 +152,8 @@ struct ipr_ctx {
   CrtTimer ktimer{kev, 8, 0};
   bool upd_timed = false;
   int cert = IPR_CERT_FP64;             // convergence certificate of the symmetric / coupled forms (ipr_set_cert)
+  bool cert_pending = false;            // R-33: certify the next iterate before (instead of) its chain
+  double cert_prev = NAN;               // R-33: that certificate missed: its value, for the chain's record
   std::vector<size_t> guards;           // ipr_test_set_guards: arena offsets of the guard bands
 };
 
@@ -1280,9 +1282,20 @@ ipr_status ipr_set_form(ipr_ctx *c, int form) {
 ipr_status ipr_set_cert(ipr_ctx *c, int mode) {
   if (!c) return fail(c, IPR_E_INVALID_ARG, "ipr_set_cert: null context");
   if (c->started) return fail(c, IPR_E_STATE, "ipr_set_cert: iteration already started");
-  if (mode != IPR_CERT_FP64 && mode != IPR_CERT_PHASE) return fail(c, IPR_E_INVALID_ARG, "ipr_set_cert: unknown mode %d", mode);
+  if (mode != IPR_CERT_FP64 && mode != IPR_CERT_PHASE && mode != IPR_CERT_FP64_CHAIN)
+    return fail(c, IPR_E_INVALID_ARG, "ipr_set_cert: unknown mode %d", mode);
   c->cert = mode;
   return IPR_OK;
+}
+
+// Reading R-33: after an update in the last phase of a symmetric form, the in-phase linear rate
+// q = rho_k / rho_{k-1} predicts rho_{k+1} ~ rho_k q.  When that is <= final_tol / 2 the next iterate is
+// certified first (the FP64 residual the stop needs anyway); its chain -- computed only to trigger the
+// certificate -- runs only if the certificate misses.  The oracle mirrors the rule (orc_solve_form).
+static bool predict_cert(const ipr_ctx *c) {
+  if (c->cert != IPR_CERT_FP64 || !is_sym(c) || c->phase != (int)c->ph.size() - 1) return false;
+  if (!(std::isfinite(c->ph_r1) && std::isfinite(c->ph_r2) && c->ph_r2 > 0.0 && c->ph_r1 < c->ph_r2)) return false;
+  return c->ph_r1 * (c->ph_r1 / c->ph_r2) <= 0.5 * c->final_tol;
 }
 
 ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *outcome) {
@@ -1336,6 +1349,28 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     c->started = true;
   }
   for (int it = 0; it < max_iters; ++it) {
+    if (c->cert_pending) {                 // R-33: the predicted-converged iterate, certificate first
+      c->cert_pending = false;
+      double rc = NAN;
+      CKS(certify_iter(c, c->cur, &rc));
+      if (rc <= c->final_tol) {
+        ipr_record r;
+        memset(&r, 0, sizeof r);
+        r.k = (int)c->trace.size(); r.phase = c->phase; r.prec = c->ph[c->phase].prec; r.mant_bits = c->m_of_cur;
+        r.decision = IPR_DEC_CONVERGED; r.rho = NAN; r.rho_hat = NAN; r.delta = NAN; r.rho_cert = rc;
+        r.gap_ms = NAN;
+        c->trace.push_back(r);
+        *iters_done += 1;
+        c->best_loc = c->cur; c->best_cont64 = is_f64(c->ph[c->phase].prec);
+        c->done = true;
+        c->outcome = IPR_DEC_CONVERGED;
+        break;
+      }
+      c->cert_prev = rc;                   // missed: the chain runs; its record carries this certificate
+      if (c->world > 1) CKS(make_xt(c, c->cur, c->ph[c->phase]));   // the certificate reused the T buffers
+    }
+    const double cert_pre = c->cert_prev;
+    c->cert_prev = NAN;
     double rho = NAN;
     float ms = 0.f;
     CKS(chain(c, &rho, &ms));
@@ -1348,7 +1383,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     ipr_record r;
     r.k = (int)c->trace.size(); r.phase = phase_now; r.prec = c->ph[phase_now].prec; r.mant_bits = c->m_of_cur;
     r.decision = d; r.rho = rho; r.rho_hat = rho / std::sqrt((double)c->n); r.delta = NAN; r.gemm_ms = ms;
-    r.rho_cert = NAN; r.upd_ms = 0.0;
+    r.rho_cert = cert_pre; r.upd_ms = 0.0;
     r.kern_ms = 0.0;                           // chain_timers() fills gemm_ms / kern_ms
     r.gap_ms = NAN;
     r.digits = is_emu(c->ph[phase_now].prec) ? c->last_chain_S : 0;
@@ -1392,7 +1427,8 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
         c->pending_delta = (int64_t)c->trace.size() - 1;
       }
       double rc = NAN;
-      if (phase_cert) CKS(certify_from_zr(c, ck, &rc));
+      if (std::isfinite(cert_pre)) rc = cert_pre;      // certified before the chain (R-33) and missed
+      else if (phase_cert) CKS(certify_from_zr(c, ck, &rc));
       else CKS(certify_iter(c, ck, &rc));
       c->trace.back().rho_cert = rc;
       if (!(rc <= c->final_tol)) {
@@ -1402,6 +1438,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
           c->pending_delta = (int64_t)c->trace.size() - 1;
         }
         if (c->world > 1) CKS(make_xt(c, c->cur, c->ph[c->phase]));
+        c->cert_pending = predict_cert(c);
         continue;
       }
       c->best_loc = ck; c->best_cont64 = is_f64(c->ph[c->phase].prec);
@@ -1412,6 +1449,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     if (d == IPR_DEC_CONTINUE) {
       CKS(step_update(c));
       c->pending_delta = (int64_t)c->trace.size() - 1;
+      c->cert_pending = predict_cert(c);
       CKS(chain_timers(c, c->trace.back()));   // after the update is enqueued: no bubble
     } else if (d == IPR_DEC_SWITCH) {
       if (c->best_loc < 0) { c->best_loc = c->cur; c->best_cont64 = is_f64(c->ph[c->phase].prec); }

@@ -63,7 +63,7 @@ def test_diagonal_bit_exact(p, name, form):
             np.testing.assert_array_equal(Ck, r.C_hist[k], err_msg=f"iterate {k}")
     np.testing.assert_array_equal(best, r.C_best)
     for t, x in zip(tr, r.records):
-        assert t["rho"] == pytest.approx(x["rho"], rel=1e-12, abs=1e-300)
+        assert t["rho"] == pytest.approx(x["rho"], rel=1e-12, abs=1e-300, nan_ok=True)   # NaN: R-33
     assert tr[-1]["rho_cert"] <= 1e-13
 
 
@@ -132,7 +132,8 @@ def test_config_c3_family_level3_envelope():
     pg, po = schedules("bf16>fp64/cbf16")
     r = oracle.solve(A, 2, po, 1e-12, 80, form=oracle.FORM_SYMMETRIC)
     out, tr, _, _ = run_gpu_trajectory(A, 2, pg, 1e-12, 80, keep=False, form="symmetric")
-    mg, mo = min(t["rho"] for t in tr), min(x["rho"] for x in r.records)
+    mg = min(t["rho"] for t in tr if np.isfinite(t["rho"]))        # R-33 records have rho = NaN
+    mo = min(x["rho"] for x in r.records if np.isfinite(x["rho"]))
     assert mg <= 4 * mo and mo <= 4 * mg
     assert (out == ipr.IPR_CONVERGED) == (r.outcome == oracle.CONVERGED)
 

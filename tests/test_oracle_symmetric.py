@@ -244,3 +244,36 @@ def test_fp8_correction_schedule_converges():
         assert np.linalg.norm(r.C_best - ref) / np.linalg.norm(ref) < 1e-12
         counts[corr] = sum(1 for x in r.records if x["phase"] == 0)
     assert counts[oracle.FP8] <= counts[oracle.BF16] + 4, counts
+
+
+@pytest.mark.parametrize("form,p", [(SYM, 2), (SYM, 3), (oracle.FORM_SYMMETRIC_TRI, 2)])
+def test_certificate_first_rule(form, p):
+    # reading R-33: with the last phase's rate predicting rho_{k+1} = rho_k^2 / rho_{k-1} <= tol / 2 the
+    # next iterate is certified before its chain (the BF16 -> FP64 schedule: noise-driven linear rate).
+    # Pinned: (a) the same iterates and records as the chain-triggered solve, except (b) the last record
+    # is certificate-only (rho NaN) with the same certificate value of the same iterate, (c) that value
+    # is the FP64 residual ||I - C^p A||_F of the returned C (numpy's own product, within the FP64
+    # rounding of an O(1e-13) quantity) and <= tol, (d) the rule fired exactly where the rate predicted.
+    A = synth.spd(96, 2.0, 7)
+    ph = [oracle.phase(oracle.BF16, plateau_ratio=0.7, plateau_arm=0.5, max_iters=40),
+          oracle.phase(corr_prec=oracle.BF16)]
+    a = oracle.solve(A, p, ph, 1e-12, 100, hist=100, form=form, predict_cert=True)
+    b = oracle.solve(A, p, ph, 1e-12, 100, hist=100, form=form, predict_cert=False)
+    assert a.outcome == oracle.CONVERGED and b.outcome == oracle.CONVERGED
+    assert len(a.records) == len(b.records)
+    for k in range(len(a.records)):
+        np.testing.assert_array_equal(a.C_hist[k], b.C_hist[k])
+    for x, y in zip(a.records[:-1], b.records[:-1]):
+        assert x["rho"] == y["rho"] and x["decision"] == y["decision"]
+    last, lb = a.records[-1], b.records[-1]
+    assert np.isnan(last["rho"]) and np.isfinite(lb["rho"]) and last["decision"] == oracle.CONVERGED
+    assert last["rho_cert"] == lb["rho_cert"] <= 1e-12
+    np.testing.assert_array_equal(a.C_best, b.C_best)
+    E = np.eye(96) - np.linalg.matrix_power(a.C_best, p) @ A
+    assert abs(last["rho_cert"] - np.linalg.norm(E)) <= 1e-13
+    r1, r2 = a.records[-2]["rho"], a.records[-3]["rho"]
+    assert a.records[-2]["phase"] == a.records[-3]["phase"] == 1
+    assert r1 * (r1 / r2) <= 0.5e-12
+    for x, y in zip(a.records[1:-2], a.records[:-3]):   # and no earlier record predicted it
+        if x["phase"] == y["phase"] == 1 and x["decision"] == oracle.CONTINUE and x["rho"] < y["rho"]:
+            assert x["rho"] * (x["rho"] / y["rho"]) > 0.5e-12
