@@ -22,8 +22,9 @@
  *  - Numerical failure is NOT an error: it is reported as an ipr_outcome (IPR_DIVERGED,
  *    IPR_NONFINITE) with status IPR_OK.  Misuse (bad arguments, wrong call order,
  *    non-symmetric A) is an error status.
- *  - Matrices at the boundary are FP64, row-major, on the device, with a leading dimension
- *    (elements) >= n.  The caller owns them.  The library owns every internal buffer.
+ *  - Matrices at the boundary are FP64, row-major, with a leading dimension (elements) >= n, on
+ *    the device (or, for ipr_init's A and ipr_finalize's / ipr_set_output's C, in host memory).
+ *    The caller owns them.  The library owns every internal buffer.
  *  - One context per host thread; contexts are independent.  All device work is enqueued
  *    on the caller's stream; ipr_iterate/ipr_residual/ipr_finalize synchronise it.
  *  - ipr_last_error(NULL) returns the message of the last failed call on this thread.
@@ -158,8 +159,10 @@ typedef struct {
                      /* the GPU waits for (CUDA events); NaN when no update followed            */
 } ipr_record;
 
-/* Create a context for an n x n SPD matrix A (FP64, row-major, device, leading dimension
- * lda >= n), borrowed read-only until ipr_finalize.  Checks exact symmetry (IPR_E_NOT_
+/* Create a context for an n x n SPD matrix A (FP64, row-major, leading dimension lda >= n).  A on the
+ * device is borrowed read-only until ipr_finalize; A in host memory (pinned for full link speed, or
+ * pageable) is copied once into a library-owned device copy on cuda_stream (the caller may reuse it
+ * after this call returns).  Checks exact symmetry (IPR_E_NOT_
  * SYMMETRIC otherwise), computes ||A||_1, ||A||_inf and max diagonal on the GPU (Eq. 3) and
  * records a warning (ipr_last_error) if the sufficient condition of reading R-12 for Eq. (2)
  * fails; that never fails init.
@@ -265,8 +268,16 @@ ipr_status ipr_get_iterate(ipr_ctx *c, int which, double *C_dev_out, int64_t ldc
 /* s = ||A||_1 * ||A||_inf and the norms: out4 = {||A||_1, ||A||_inf, max diag, s}. */
 ipr_status ipr_get_norms(ipr_ctx *c, double *out4);
 
-/* Write the best iterate (FP64, full matrix on every rank) to C_dev_out (ldc >= n; may be
- * NULL to discard) and free the context (also on error). */
+/* Optional: the destination the caller will pass to ipr_finalize (host -- pinned for full speed -- or
+ * device, row-major, ldc >= n; NULL clears).  With world = 1 the engine then streams every candidate it
+ * certifies in an FP64-range phase to C_out on a copy stream while the FP64 certificate runs; when the
+ * solve converges on that candidate, ipr_finalize(c, C_out, ldc) only waits for the copy.  C_out is
+ * written during ipr_iterate (possibly with a candidate that later misses): its content is defined only
+ * after ipr_finalize.  Errors: IPR_E_INVALID_ARG. */
+ipr_status ipr_set_output(ipr_ctx *c, double *C_out, int64_t ldc);
+
+/* Write the best iterate (FP64, full matrix on every rank) to C_dev_out (device or host memory,
+ * ldc >= n; may be NULL to discard) and free the context (also on error). */
 ipr_status ipr_finalize(ipr_ctx *c, double *C_dev_out, int64_t ldc);
 
 /* Message of the last failure (or init warning) of c; c == NULL: this thread's last. */

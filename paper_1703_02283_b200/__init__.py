@@ -36,7 +36,7 @@ EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_
             "ipr_launch_count", "ipr_plan", "ipr_set_form", "ipr_bench_gemm", "ipr_bench_gemm_epi",
             "ipr_test_set_digits", "ipr_test_crt_table", "ipr_set_cert", "ipr_test_peek",
             "ipr_test_local_group_create", "ipr_test_local_group_destroy", "ipr_test_init_local",
-            "ipr_test_set_guards", "ipr_test_check_guards"]
+            "ipr_test_set_guards", "ipr_test_check_guards", "ipr_set_output"]
 IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ, IPR_FORM_SYMMETRIC, IPR_FORM_SYMMETRIC_TRI, IPR_FORM_COUPLED = 0, 1, 2, 3, 4
 IPR_CERT_FP64, IPR_CERT_PHASE, IPR_CERT_FP64_CHAIN = 0, 1, 2
 CERT_BY_NAME = {"fp64": IPR_CERT_FP64, "dmma": IPR_CERT_FP64, "phase": IPR_CERT_PHASE,
@@ -81,6 +81,7 @@ def _load():
     L.ipr_get_iterate.argtypes = [vp, C.c_int, vp, i64]
     L.ipr_get_norms.argtypes = [vp, dp]
     L.ipr_finalize.argtypes = [vp, vp, i64]
+    L.ipr_set_output.argtypes = [vp, vp, i64]
     L.ipr_last_error.argtypes = [vp]
     L.ipr_last_error.restype = C.c_char_p
     L.ipr_nccl_unique_id.argtypes = [vp]
@@ -123,18 +124,20 @@ def _ptr(x) -> int:
     return x.data_ptr()
 
 
-def _check_matrix(x, n: int, what: str, ref=None):
-    """A boundary matrix must be an FP64 CUDA tensor, n x n, unit column stride (ipr.h: FP64,
-    row-major, device, leading dimension >= n) -- anything else would make the library read or
-    write the wrong bytes.  Raw integer pointers are passed through unchecked."""
+def _check_matrix(x, n: int, what: str, ref=None, host_ok: bool = False):
+    """A boundary matrix must be an FP64 tensor, n x n, unit column stride (ipr.h: FP64, row-major,
+    leading dimension >= n), on the device -- or in host memory where the call takes one (host_ok:
+    ipr_init's A, ipr_finalize's / ipr_set_output's / ipr_get_iterate's C) -- anything else would make
+    the library read or write the wrong bytes.  Raw integer pointers are passed through unchecked."""
     if x is None or isinstance(x, int):
         return
     import torch
     if x.dtype != torch.float64:
         raise ValueError(f"{what}: dtype must be torch.float64 (got {x.dtype})")
-    if not x.is_cuda:
+    if not x.is_cuda and not (host_ok and x.device.type == "cpu"):
         raise ValueError(f"{what}: must be a CUDA tensor (got device {x.device})")
-    if ref is not None and not isinstance(ref, int) and x.device != ref.device:
+    if (ref is not None and not isinstance(ref, int) and x.is_cuda and ref.is_cuda
+            and x.device != ref.device):
         raise ValueError(f"{what}: on {x.device}, A is on {ref.device}")
     if x.dim() != 2 or x.shape[0] < n or x.shape[1] < n:
         raise ValueError(f"{what}: shape must be ({n}, {n}) (got {tuple(x.shape)})")
@@ -174,7 +177,7 @@ def ipr_nccl_unique_id() -> bytes:
 
 def ipr_init(n: int, A, lda: int | None = None, stream=None, world: int = 1, rank: int = 0,
              nccl_unique_id: bytes | None = None, grid_rows: int = 1, grid_cols: int | None = None):
-    _check_matrix(A, n, "ipr_init: A")
+    _check_matrix(A, n, "ipr_init: A", host_ok=True)
     ctx = C.c_void_p()
     uid = C.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id is not None else None
     _check(_lib.ipr_init(C.byref(ctx), n, _ptr(A), lda if lda is not None else n, _stream(stream),
@@ -252,7 +255,7 @@ def ipr_get_trace(ctx):
 
 def ipr_get_iterate(ctx, which: int, C_out, ldc: int | None = None):
     if C_out is not None and not isinstance(C_out, int):
-        _check_matrix(C_out, C_out.shape[0], "ipr_get_iterate: C_out")
+        _check_matrix(C_out, C_out.shape[0], "ipr_get_iterate: C_out", host_ok=True)
     _check(_lib.ipr_get_iterate(ctx, which, _ptr(C_out), ldc if ldc is not None else C_out.shape[1]), ctx)
 
 
@@ -262,10 +265,18 @@ def ipr_get_norms(ctx):
     return tuple(out)
 
 
+def ipr_set_output(ctx, C_out=None, ldc: int | None = None):
+    """The destination ipr_finalize will get (host or device): the certified answer streams there early."""
+    _check_matrix(C_out, C_out.shape[0] if C_out is not None and not isinstance(C_out, int) else 0,
+                  "ipr_set_output: C_out", host_ok=True)
+    ld = ldc if ldc is not None else (C_out.stride(0) if C_out is not None and not isinstance(C_out, int) else 0)
+    _check(_lib.ipr_set_output(ctx, _ptr(C_out), ld), ctx)
+
+
 def ipr_finalize(ctx, C_out=None, ldc: int | None = None):
     if C_out is not None and not isinstance(C_out, int):
         try:
-            _check_matrix(C_out, C_out.shape[0], "ipr_finalize: C_out")
+            _check_matrix(C_out, C_out.shape[0], "ipr_finalize: C_out", host_ok=True)
         except ValueError:
             _lib.ipr_finalize(ctx, None, 0)   # still free the context
             raise
@@ -359,7 +370,7 @@ class Solver:
     def __init__(self, A, p: int, phases, final_tol: float = 1e-12, stream=None, world: int = 1,
                  rank: int = 0, nccl_unique_id: bytes | None = None, form="literal", cert="fp64",
                  local_group=None, grid=None):
-        _check_matrix(A, A.shape[0], "Solver: A")
+        _check_matrix(A, A.shape[0], "Solver: A", host_ok=True)
         self.A = A
         self.n = A.shape[0]
         gr, gc = grid if grid is not None else (1, world)
@@ -398,15 +409,23 @@ class Solver:
         import torch
         if out is None:
             out = torch.empty((self.n, self.n), dtype=torch.float64, device=self.A.device)
-        _check_matrix(out, self.n, "iterate_copy: out", self.A)
+        _check_matrix(out, self.n, "iterate_copy: out", self.A, host_ok=True)
         ipr_get_iterate(self.ctx, which, out, out.stride(0))
         return out
+
+    def set_output(self, out):
+        """Register ipr_finalize's destination (ipr_set_output): the certified answer streams there
+        while its FP64 certificate runs."""
+        _check_matrix(out, self.n, "set_output: out", self.A, host_ok=True)
+        ipr_set_output(self.ctx, out, out.stride(0))
+        self._out = out
 
     def finalize(self, out=None):
         import torch
         if out is None:
-            out = torch.empty((self.n, self.n), dtype=torch.float64, device=self.A.device)
-        _check_matrix(out, self.n, "finalize: out", self.A)
+            out = torch.empty((self.n, self.n), dtype=torch.float64, device=self.A.device,
+                              pin_memory=not self.A.is_cuda)
+        _check_matrix(out, self.n, "finalize: out", self.A, host_ok=True)
         ctx, self.ctx = self.ctx, None
         ipr_finalize(ctx, out, out.stride(0))
         return out

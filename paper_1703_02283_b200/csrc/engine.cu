@@ -75,6 +75,15 @@ struct ipr_ctx {
   double *partg = nullptr;              // 2-D grid: every rank's full partial array [world][npart]
   cudaStream_t st = nullptr;
   const double *A = nullptr;
+  double *Aown = nullptr;               // host A at ipr_init: the library's device copy (pool block)
+  // ipr_set_output: the destination of ipr_finalize, where the certified candidate is streamed while
+  // its FP64 certificate runs (G = 1, FP64 container); valid once the solve converged on that buffer
+  double *out_ptr = nullptr;
+  int64_t out_ld = 0;
+  cudaStream_t ost = nullptr;
+  cudaEvent_t oev = nullptr, orev = nullptr;
+  int out_buf = -1;                     // iterate buffer whose copy is in flight / done (-1: none)
+  bool out_valid = false;
   double norms[4] = {0, 0, 0, 0};
   std::string err;
   Transport *comm = nullptr;           // world > 1: NCCL (ipr_init) or an in-process local group (ipr_testing.h)
@@ -180,6 +189,13 @@ void pinned_release(double *p) {
   std::lock_guard<std::mutex> lock(g_pin_mu);
   const int64_t i = (p - g_pin_base) / 8;
   if (g_pin_base && i >= 0 && i < kPinnedSlots) g_pin_used[i] = false;
+}
+
+// host memory (pinned, or pageable / unknown to CUDA) rather than device or managed memory
+bool is_host_ptr(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return true; }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
 }
 
 // One retained stream-ordered memory pool per device (release threshold = unlimited): the
@@ -982,6 +998,10 @@ void free_ctx(ipr_ctx *c) {
   for (auto &e : c->ev) if (e) cudaEventDestroy(e);
   for (auto &e : c->kev) if (e) cudaEventDestroy(e);
   if (c->cst) { cudaStreamSynchronize(c->cst); cudaStreamDestroy(c->cst); }
+  if (c->ost) { cudaStreamSynchronize(c->ost); cudaStreamDestroy(c->ost); }
+  if (c->oev) cudaEventDestroy(c->oev);
+  if (c->orev) cudaEventDestroy(c->orev);
+  if (c->Aown) cudaFreeAsync(c->Aown, c->st);
   for (auto &e : c->gev) if (e) cudaEventDestroy(e);
   delete c->rowt;
   delete c->colt;
@@ -1090,6 +1110,7 @@ extern "C" {
 static ipr_status certify_best(ipr_ctx *c, double *rho);
 static ipr_status certify_iter(ipr_ctx *c, int i, double *rho);
 static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho);
+static ipr_status stream_candidate(ipr_ctx *c, int i);
 
 const char *ipr_version(void) {
   return "ipr 0.3.0 (sm_100a: tcgen05 BF16/FP16/TF32/FP8/INT8, DMMA FP64, FP64 on INT8 tensor cores: Ozaki I / II-CRT)";
@@ -1122,6 +1143,7 @@ static ipr_status init_ctx(ipr_ctx **out, int64_t n, const double *A_dev, int64_
   c = new ipr_ctx();
   c->n = n; c->lda = lda; c->A = A_dev; c->world = world; c->rank = rank;
   c->st = (cudaStream_t)cuda_stream;
+  const bool a_host = is_host_ptr(A_dev);
   c->npad = padded_order(n, world);          // a multiple of 256 grid_rows and of 256 grid_cols
   c->grows = grid_rows; c->gcols = grid_cols;
   c->grow = rank / grid_cols; c->gcol = rank % grid_cols;
@@ -1149,7 +1171,18 @@ static ipr_status init_ctx(ipr_ctx **out, int64_t n, const double *A_dev, int64_
     c->colsum = (double *)(b + 768);
     c->hscal = pinned_acquire();
     if (!c->hscal) TRY(fail(c, IPR_E_OOM, "pinned host slab exhausted (too many live contexts)"));
+    if (a_host) {   // host A (pinned: full link speed; pageable: staged by the runtime) -> compact device copy
+      if (cudaMallocFromPoolAsync((void **)&c->Aown, (size_t)n * n * 8, pool, c->st) != cudaSuccess) {
+        cudaGetLastError();
+        c->Aown = nullptr;
+        TRY(fail(c, IPR_E_OOM, "ipr_init: device copy of the host A (%lld x %lld)", (long long)n, (long long)n));
+      }
+      TRYC(cudaMemcpy2DAsync(c->Aown, (size_t)n * 8, A_dev, (size_t)lda * 8, (size_t)n * 8, (size_t)n,
+                             cudaMemcpyHostToDevice, c->st));
+      c->A = c->Aown; c->lda = n;
+    }
   }
+  A_dev = c->A; lda = c->lda;
   for (auto &e : c->ev) TRYC(cudaEventCreate(&e));
   for (auto &e : c->kev) TRYC(cudaEventCreate(&e));
   TRYC(cudaMemsetAsync(c->dflag, 0, 16, c->st));
@@ -1352,8 +1385,10 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     if (c->cert_pending) {                 // R-33: the predicted-converged iterate, certificate first
       c->cert_pending = false;
       double rc = NAN;
+      CKS(stream_candidate(c, c->cur));
       CKS(certify_iter(c, c->cur, &rc));
       if (rc <= c->final_tol) {
+        c->out_valid = c->out_buf == c->cur;
         ipr_record r;
         memset(&r, 0, sizeof r);
         r.k = (int)c->trace.size(); r.phase = c->phase; r.prec = c->ph[c->phase].prec; r.mant_bits = c->m_of_cur;
@@ -1367,6 +1402,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
         break;
       }
       c->cert_prev = rc;                   // missed: the chain runs; its record carries this certificate
+      if (c->out_buf >= 0) CK(cudaStreamWaitEvent(c->st, c->oev, 0));   // the copy reads C_k: done before reuse
       if (c->world > 1) CKS(make_xt(c, c->cur, c->ph[c->phase]));   // the certificate reused the T buffers
     }
     const double cert_pre = c->cert_prev;
@@ -1428,10 +1464,15 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       }
       double rc = NAN;
       if (std::isfinite(cert_pre)) rc = cert_pre;      // certified before the chain (R-33) and missed
-      else if (phase_cert) CKS(certify_from_zr(c, ck, &rc));
-      else CKS(certify_iter(c, ck, &rc));
+      else {
+        CKS(stream_candidate(c, ck));
+        if (phase_cert) CKS(certify_from_zr(c, ck, &rc));
+        else CKS(certify_iter(c, ck, &rc));
+      }
       c->trace.back().rho_cert = rc;
       if (!(rc <= c->final_tol)) {
+        c->out_valid = false;
+        if (c->out_buf >= 0) CK(cudaStreamWaitEvent(c->st, c->oev, 0));
         c->trace.back().decision = IPR_DEC_CONTINUE;
         if (cert_first) {
           CKS(update_sym(c));
@@ -1442,6 +1483,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
         continue;
       }
       c->best_loc = ck; c->best_cont64 = is_f64(c->ph[c->phase].prec);
+      c->out_valid = c->out_buf == ck;
       c->done = true;
       c->outcome = d;
       break;
@@ -1512,8 +1554,40 @@ static ipr_status copy_iterate(ipr_ctx *c, int which, double *dst, int64_t ldc) 
     CK(cudaMemcpyAsync(slot, c->best, (size_t)cnt * 8, cudaMemcpyDeviceToDevice, c->st));
   }
   CKS(gather_f64(c, slot));
-  if (dst) CK(launch_copy_out_blocks(c->full64, c->mr, c->kp, c->gcols, c->n, dst, ldc, c->st));
+  if (dst && is_host_ptr(dst)) {
+    // host destination: one 2-D copy per (row, column) block of the block-major [world][mr][kp] layout
+    for (int b = 0; b < c->world; ++b) {
+      const int64_t r0 = (int64_t)(b / c->gcols) * c->mr, c0 = (int64_t)(b % c->gcols) * c->kp;
+      const int64_t nr = std::min(c->mr, c->n - r0), nc = std::min(c->kp, c->n - c0);
+      if (nr <= 0 || nc <= 0) continue;
+      CK(cudaMemcpy2DAsync(dst + r0 * ldc + c0, (size_t)ldc * 8, c->full64 + (size_t)b * blk(c), (size_t)c->kp * 8,
+                           (size_t)nc * 8, (size_t)nr, cudaMemcpyDeviceToHost, c->st));
+    }
+  } else if (dst) {
+    CK(launch_copy_out_blocks(c->full64, c->mr, c->kp, c->gcols, c->n, dst, ldc, c->st));
+  }
   CK(cudaStreamSynchronize(c->st));
+  return IPR_OK;
+}
+
+// ipr_set_output: stream the candidate C_k (FP64 container, G = 1) to the caller's destination on a copy
+// stream while its certificate runs; finalize then only waits for it if C_k is the answer
+static ipr_status stream_candidate(ipr_ctx *c, int i) {
+  c->out_valid = false;
+  const PhaseC &P = c->ph[c->phase];
+  if (!c->out_ptr || c->world != 1 || !P.cont64) return IPR_OK;
+  if (!c->ost) {
+    CK(cudaStreamCreateWithFlags(&c->ost, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->oev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->orev, cudaEventDisableTiming));
+  }
+  if (c->out_buf >= 0) CK(cudaStreamWaitEvent(c->st, c->oev, 0));   // a previous copy reads a live buffer
+  CK(cudaEventRecord(c->orev, c->st));
+  CK(cudaStreamWaitEvent(c->ost, c->orev, 0));
+  CK(cudaMemcpy2DAsync(c->out_ptr, (size_t)c->out_ld * 8, cont_ptr(c, i, P), (size_t)c->kp * 8, (size_t)c->n * 8,
+                       (size_t)c->n, cudaMemcpyDefault, c->ost));
+  CK(cudaEventRecord(c->oev, c->ost));
+  c->out_buf = i;
   return IPR_OK;
 }
 
@@ -1627,13 +1701,28 @@ ipr_status ipr_residual(ipr_ctx *c, int certify, double *rho) {
   return IPR_OK;
 }
 
+ipr_status ipr_set_output(ipr_ctx *c, double *C_out, int64_t ldc) {
+  if (!c) return fail(c, IPR_E_INVALID_ARG, "ipr_set_output: null context");
+  if (C_out && ldc < c->n) return fail(c, IPR_E_INVALID_ARG, "ipr_set_output: ldc < n");
+  if (c->out_buf >= 0) CK(cudaStreamSynchronize(c->ost));
+  c->out_ptr = C_out; c->out_ld = ldc; c->out_buf = -1; c->out_valid = false;
+  return IPR_OK;
+}
+
 ipr_status ipr_finalize(ipr_ctx *c, double *C_dev_out, int64_t ldc) {
   if (!c) return fail(c, IPR_E_INVALID_ARG, "ipr_finalize: null context");
   ipr_status s = IPR_OK;
   if (C_dev_out) {
     if (ldc < c->n) s = fail(c, IPR_E_INVALID_ARG, "ipr_finalize: ldc < n");
     else if (!c->started || c->best_loc < 0) s = fail(c, IPR_E_STATE, "ipr_finalize: no iterate evaluated");
-    else s = copy_iterate(c, 1, C_dev_out, ldc);
+    else if (c->out_valid && C_dev_out == c->out_ptr && ldc == c->out_ld) {
+      // the certified answer already streamed there during its certificate (ipr_set_output)
+      cudaError_t e = cudaStreamWaitEvent(c->st, c->oev, 0);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(c->st);
+      if (e != cudaSuccess) s = fail(c, IPR_E_CUDA, "ipr_finalize: %s", cudaGetErrorString(e));
+    } else {
+      s = copy_iterate(c, 1, C_dev_out, ldc);
+    }
   }
   if (s != IPR_OK) t_err = c->err;
   free_ctx(c);
