@@ -162,6 +162,10 @@ struct ipr_ctx {
   bool upd_timed = false;
   int cert = IPR_CERT_FP64;             // convergence certificate of the symmetric / coupled forms (ipr_set_cert)
   bool cert_pending = false;            // R-33: certify the next iterate before (instead of) its chain
+  // IPR_TIMELINE=1 (diagnostics): CUDA events at the start of every activity of the solve; the device
+  // time per activity (and the idle gaps between them) is printed to stderr at ipr_finalize
+  bool tl_on = false;
+  std::vector<std::pair<const char *, cudaEvent_t>> tl;
   double cert_prev = NAN;               // R-33: that certificate missed: its value, for the chain's record
   std::vector<size_t> guards;           // ipr_test_set_guards: arena offsets of the guard bands
 };
@@ -189,6 +193,32 @@ void pinned_release(double *p) {
   std::lock_guard<std::mutex> lock(g_pin_mu);
   const int64_t i = (p - g_pin_base) / 8;
   if (g_pin_base && i >= 0 && i < kPinnedSlots) g_pin_used[i] = false;
+}
+
+void tl_mark(ipr_ctx *c, const char *what) {
+  if (!c->tl_on) return;
+  cudaEvent_t e = nullptr;
+  if (cudaEventCreate(&e) != cudaSuccess || cudaEventRecord(e, c->st) != cudaSuccess) { cudaGetLastError(); return; }
+  c->tl.push_back({what, e});
+}
+void tl_report(ipr_ctx *c) {
+  if (!c->tl_on || c->tl.size() < 2) return;
+  cudaStreamSynchronize(c->st);
+  std::vector<std::pair<std::string, double>> acc;
+  double total = 0.0;
+  for (size_t i = 0; i + 1 < c->tl.size(); ++i) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, c->tl[i].second, c->tl[i + 1].second) != cudaSuccess) { cudaGetLastError(); continue; }
+    total += ms;
+    bool found = false;
+    for (auto &a : acc) if (a.first == c->tl[i].first) { a.second += ms; found = true; }
+    if (!found) acc.push_back({c->tl[i].first, (double)ms});
+  }
+  fprintf(stderr, "ipr timeline (device ms): total %.3f", total);
+  for (auto &a : acc) fprintf(stderr, " | %s %.3f", a.first.c_str(), a.second);
+  fprintf(stderr, "\n");
+  for (auto &m : c->tl) cudaEventDestroy(m.second);
+  c->tl.clear();
 }
 
 // host memory (pinned, or pageable / unknown to CUDA) rather than device or managed memory
@@ -1144,6 +1174,8 @@ static ipr_status init_ctx(ipr_ctx **out, int64_t n, const double *A_dev, int64_
   c->n = n; c->lda = lda; c->A = A_dev; c->world = world; c->rank = rank;
   c->st = (cudaStream_t)cuda_stream;
   const bool a_host = is_host_ptr(A_dev);
+  c->tl_on = getenv("IPR_TIMELINE") != nullptr;
+  tl_mark(c, "init");
   c->npad = padded_order(n, world);          // a multiple of 256 grid_rows and of 256 grid_cols
   c->grows = grid_rows; c->gcols = grid_cols;
   c->grow = rank / grid_cols; c->gcol = rank % grid_cols;
@@ -1378,7 +1410,9 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     }
     if (!c->arena) CKS(alloc_arena(c, need_c));
     c->phase = 0; c->it_in_phase = 0; c->cur = 0;
+    tl_mark(c, "entry");
     CKS(begin_phase(c, true));
+    tl_mark(c, "gap");
     c->started = true;
   }
   for (int it = 0; it < max_iters; ++it) {
@@ -1386,7 +1420,9 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       c->cert_pending = false;
       double rc = NAN;
       CKS(stream_candidate(c, c->cur));
+      tl_mark(c, "cert");
       CKS(certify_iter(c, c->cur, &rc));
+      tl_mark(c, "gap");
       if (rc <= c->final_tol) {
         c->out_valid = c->out_buf == c->cur;
         ipr_record r;
@@ -1409,7 +1445,9 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     c->cert_prev = NAN;
     double rho = NAN;
     float ms = 0.f;
+    tl_mark(c, "chain");
     CKS(chain(c, &rho, &ms));
+    tl_mark(c, "gap");
     c->last_rho = rho;
     const int phase_now = c->phase;
     bool best_new = false;
@@ -1466,8 +1504,10 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       if (std::isfinite(cert_pre)) rc = cert_pre;      // certified before the chain (R-33) and missed
       else {
         CKS(stream_candidate(c, ck));
+        tl_mark(c, "cert");
         if (phase_cert) CKS(certify_from_zr(c, ck, &rc));
         else CKS(certify_iter(c, ck, &rc));
+        tl_mark(c, "gap");
       }
       c->trace.back().rho_cert = rc;
       if (!(rc <= c->final_tol)) {
@@ -1475,7 +1515,9 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
         if (c->out_buf >= 0) CK(cudaStreamWaitEvent(c->st, c->oev, 0));
         c->trace.back().decision = IPR_DEC_CONTINUE;
         if (cert_first) {
+          tl_mark(c, "update");
           CKS(update_sym(c));
+          tl_mark(c, "gap");
           c->pending_delta = (int64_t)c->trace.size() - 1;
         }
         if (c->world > 1) CKS(make_xt(c, c->cur, c->ph[c->phase]));
@@ -1489,7 +1531,9 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       break;
     }
     if (d == IPR_DEC_CONTINUE) {
+      tl_mark(c, "update");
       CKS(step_update(c));
+      tl_mark(c, "gap");
       c->pending_delta = (int64_t)c->trace.size() - 1;
       c->cert_pending = predict_cert(c);
       CKS(chain_timers(c, c->trace.back()));   // after the update is enqueued: no bubble
@@ -1498,7 +1542,9 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       CKS(save_best(c));
       c->phase += 1; c->it_in_phase = 0; c->rho_prev = NAN;
       c->cur = 0;
+      tl_mark(c, "entry");
       CKS(begin_phase(c, false));
+      tl_mark(c, "gap");
     } else {
       c->done = true;
       c->outcome = d;   // IPR_DEC_* terminal values equal the ipr_outcome values
@@ -1712,6 +1758,7 @@ ipr_status ipr_set_output(ipr_ctx *c, double *C_out, int64_t ldc) {
 ipr_status ipr_finalize(ipr_ctx *c, double *C_dev_out, int64_t ldc) {
   if (!c) return fail(c, IPR_E_INVALID_ARG, "ipr_finalize: null context");
   ipr_status s = IPR_OK;
+  tl_mark(c, "finalize");
   if (C_dev_out) {
     if (ldc < c->n) s = fail(c, IPR_E_INVALID_ARG, "ipr_finalize: ldc < n");
     else if (!c->started || c->best_loc < 0) s = fail(c, IPR_E_STATE, "ipr_finalize: no iterate evaluated");
@@ -1724,6 +1771,8 @@ ipr_status ipr_finalize(ipr_ctx *c, double *C_dev_out, int64_t ldc) {
       s = copy_iterate(c, 1, C_dev_out, ldc);
     }
   }
+  tl_mark(c, "end");
+  tl_report(c);
   if (s != IPR_OK) t_err = c->err;
   free_ctx(c);
   return s;
