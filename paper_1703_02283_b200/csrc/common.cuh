@@ -140,6 +140,9 @@ struct GemmArgs {
   // B operand panels (b_pstride != 0): K-panel length of B (0: = a_kp) -- the 2-D grid's gathered
   // T column panel [P_r][kp][mr] has b_kp = mr
   int64_t b_kp;
+  // diagnostics only (IPR_DIAG_EPI, read by launch_gemm_tc; results are wrong when set): bit 0 skips the
+  // tri epilogue's residual terms, bit 1 its K-major stores, bit 2 its mirror stores
+  int diag_epi;
 };
 
 // ------------------------------------------------------------------------------------

@@ -473,8 +473,8 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
             const float fv = __fmul_rn(a, sf);
             f[u] = dm ? __fsub_rn(0.0f, fv) : fv;      // 0 - v as in FP64: +0 for v = 0
             ea.mx = fmaxf(ea.mx, fabsf(f[u]));
-            t[(col + j) * g.ldt + row] = f[u];
-            if (rsd && row < g.n && g.col0 + col + j < g.n) {
+            if (!(g.diag_epi & 2)) t[(col + j) * g.ldt + row] = f[u];
+            if (rsd && !(g.diag_epi & 1) && row < g.n && g.col0 + col + j < g.n) {
               if (f32r) {
                 ff_add_sq(rh, rlo, fv, 2.0f);          // d = 0 - v: 2 d^2
               } else {
@@ -483,7 +483,7 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
               }
             }
           }
-          m[q] = make_float4(f[0], f[1], f[2], f[3]);
+          if (!(g.diag_epi & 4)) m[q] = make_float4(f[0], f[1], f[2], f[3]);
         }
         if (rsd && f32r && !ff_flush(rh, rlo, ea.r2)) {
           #pragma unroll
@@ -1347,6 +1347,11 @@ cudaError_t launch_gemm_tc(const GemmArgs &a_in, cudaStream_t s) {
   if (a.tri && (a.mode & (EPI_RESID | EPI_SYMUPD)) && a.oz_grouped != 3) {   // the tiles below the diagonal are not visited: zero partials
     cudaError_t z = cudaMemsetAsync(a.part + (a.col0 / TC_BN) * a.tiles_m, 0, (size_t)(a.N / TC_BN) * a.tiles_m * sizeof(double), s);
     if (z != cudaSuccess) return z;
+  }
+  {
+    static int diag = -1;
+    if (diag < 0) { const char *v = getenv("IPR_DIAG_EPI"); diag = v ? atoi(v) : 0; }
+    a.diag_epi = diag;
   }
   const int maxpairs = num_sms() / 2;
   const int grid = 2 * (ntiles < maxpairs ? ntiles : maxpairs);

@@ -38,6 +38,7 @@ def main():
         print(json.dumps({"n": n, "kappa": kappa, "seed": seed, "schedule": sched, "outcome": oc,
                           "iters_per_phase": [sum(1 for t in tr if t["phase"] == i) for i in range(len(ph))],
                           "rho_cert": cert[-1] if cert else None, "dmma_recheck": chk,
+                          "certificates": len(cert), "cert_first": bool(tr and tr[-1]["rho"] != tr[-1]["rho"]),
                           "time_s": e0.elapsed_time(e1) / 1e3}), flush=True)
         del A
         torch.cuda.empty_cache()
