@@ -143,6 +143,11 @@ struct GemmArgs {
   // diagnostics only (IPR_DIAG_EPI, read by launch_gemm_tc; results are wrong when set): bit 0 skips the
   // tri epilogue's residual terms, bit 1 its K-major stores, bit 2 its mirror stores
   int diag_epi;
+  // CRT modulus launches after the first of a product (ozaki.cu): launched with programmatic stream
+  // serialization, so a launch's CTAs start on the SMs its predecessor's tail frees (the launches are
+  // independent: other residue planes, other v-byte planes); each waits for its predecessor before it
+  // exits, so the finish kernel, launched normally, sees every modulus complete
+  int pdl;
 };
 
 // ------------------------------------------------------------------------------------

@@ -1048,6 +1048,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
+  if (KIND == 3 && EF == 3) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");   // next modulus launch
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN), g.tri, (int)(g.col0 / TC_BN)};
   const int ntiles = sch.count();
@@ -1246,6 +1247,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
   }
+  if (KIND == 3 && EF == 3 && g.pdl) asm volatile("griddepcontrol.wait;\n" ::: "memory");   // predecessor done
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1369,7 +1371,18 @@ cudaError_t launch_gemm_tc(const GemmArgs &a_in, cudaStream_t s) {
         if (e != cudaSuccess) return e;                                                                  \
         attr.set();                                                                                      \
       }                                                                                                  \
-      k_gemm_tc<K, EF><<<grid, TC_NT, TC_SMEM, s>>>(ma, mb, a);                                          \
+      if (a.pdl) {                                                                                       \
+        cudaLaunchConfig_t cfg = {};                                                                     \
+        cudaLaunchAttribute at[1];                                                                       \
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                   \
+        at[0].val.programmaticStreamSerializationAllowed = 1;                                            \
+        cfg.gridDim = dim3((unsigned)grid); cfg.blockDim = dim3(TC_NT); cfg.dynamicSmemBytes = TC_SMEM;  \
+        cfg.stream = s; cfg.attrs = at; cfg.numAttrs = 1;                                                \
+        e = cudaLaunchKernelEx(&cfg, k_gemm_tc<K, EF>, ma, mb, a);                                       \
+        if (e != cudaSuccess) return e;                                                                  \
+      } else {                                                                                           \
+        k_gemm_tc<K, EF><<<grid, TC_NT, TC_SMEM, s>>>(ma, mb, a);                                        \
+      }                                                                                                  \
     } break;
     TC_LAUNCH(0, 0, 0)
     TC_LAUNCH(1, 1, 0)

@@ -385,8 +385,11 @@ cudaError_t launch_gemm_crt(const GemmArgs &g, cudaStream_t s) {
   if (timed) { cudaError_t e = cudaEventRecord(tm->ev[2 * tm->used], s); if (e != cudaSuccess) return e; }
   static int per = 0;                            // moduli per launch (bounds the drift of the CTA pairs)
   if (!per) { const char *v = getenv("IPR_CRT_PER"); per = v ? atoi(v) : 2; per = per < 1 ? 1 : per; }
+  static int pdl = -1;                           // IPR_CRT_PDL=0: plain stream order (A/B measurements)
+  if (pdl < 0) { const char *v = getenv("IPR_CRT_PDL"); pdl = v ? atoi(v) != 0 : 1; }
   for (int l0 = 0; l0 < g.crt_n; l0 += per) {    // residue bytes of every modulus
     q.crt_l0 = l0; q.crt_l1 = l0 + per < g.crt_n ? l0 + per : g.crt_n;
+    q.pdl = pdl && l0 > 0;                       // overlap a launch's ramp with its predecessor's tail
     cudaError_t e = launch_gemm_tc(q, s);
     if (e != cudaSuccess) return e;
   }
