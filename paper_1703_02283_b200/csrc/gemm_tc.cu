@@ -185,8 +185,9 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t saddr) {
 // Instruction descriptor: K-major A and B, M = 256 (pair), N = 256.  D format (bits 4-5): F32 = 1,
 // S32 = 2 (kind::i8).  A/B formats (bits 7-9 / 10-12): kind::f16 F16 = 0, BF16 = 1; kind::tf32
 // TF32 = 2; kind::f8f6f4 E4M3 = 0; kind::i8 signed = 1.
-__host__ __device__ constexpr uint32_t make_idesc(int prec) {
-  const uint32_t fmt = prec == P_BF16 ? 1u : prec == P_FP16 ? 0u : prec == P_TF32 ? 2u : prec == P_FP8 ? 0u : 1u;
+__host__ __device__ constexpr uint32_t make_idesc(int prec, bool u8 = false) {   // u8: kind::i8 unsigned operands
+  const uint32_t fmt = prec == P_BF16 ? 1u : prec == P_FP16 ? 0u : prec == P_TF32 ? 2u : prec == P_FP8 ? 0u
+                       : u8 ? 0u : 1u;
   const uint32_t dfmt = prec == P_INT8 ? 2u : 1u;
   return (dfmt << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)(TC_BN >> 3) << 17) | ((uint32_t)((2 * TC_BM) >> 4) << 24);
 }
@@ -788,7 +789,8 @@ cudaError_t tc_set_crt_table(const CrtTab &t) { return cudaMemcpyToSymbol(c_crt,
 // only: x mod m = x - m umulhi(x, ceil(2^32 / m)), exact or one m too far for x < 2^31.
 __device__ __forceinline__ void crt_chunk(const GemmArgs &g, int l, int64_t row, int64_t c0, const uint32_t (&r)[32]) {
   const int nm = g.crt_n;
-  const int m = c_crt.m[l], off = c_crt.off[l], iv = c_crt.inv[nm][l];
+  // unsigned residues (crt_unsigned(K)): U = sum of byte products < 2^31, no offset needed
+  const int m = c_crt.m[l], off = crt_unsigned(g.a_kp) ? 0 : c_crt.off[l], iv = c_crt.inv[nm][l];
   const uint32_t mag = c_crt.mag[l];
   uint32_t pk[8];
   #pragma unroll
@@ -1116,7 +1118,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
   } else if (warp == 1) {
     // ===== MMA issuer (leader CTA, single thread) =====
     if (leader && lane == 0) {
-      const uint32_t idesc = make_idesc(g.prec);
+      const uint32_t idesc = make_idesc(g.prec, crt && crt_unsigned(g.a_kp));   // CRT: residues in [0, m) below
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;

@@ -250,30 +250,33 @@ int crt_bits(int S, int64_t n) {
 // the byte sum as two __dp4a (< 8 * 255 * 255 + M < 2^20) with h - 2^62 mod M folded into the first
 // accumulator, then one exact multiply-high reduction (x < 2^20, magic ceil(2^32 / M): error < 2^-12
 // < 1/M) and the shift by the symmetric offset h.  ~5 integer operations per residue.
-template <int M>
+// UNS: the residue in [0, M) itself (u8 x u8 modulus GEMMs, crt_unsigned): no symmetric shift, and for
+// M = 256 the low byte of the sum directly.
+template <int M, bool UNS = false>
 __device__ __forceinline__ uint32_t crt_res8(uint32_t lo, uint32_t hi) {
-  constexpr uint32_t h = M == 256 ? 128 : (M - 1) / 2;
+  constexpr uint32_t h = UNS ? 0u : M == 256 ? 128 : (M - 1) / 2;
   constexpr uint32_t w0 = 1u % M, w1 = (1u << 8) % M, w2 = (1u << 16) % M, w3 = (1u << 24) % M;
   constexpr uint32_t w4 = (uint32_t)((1ull << 32) % M), w5 = (uint32_t)((1ull << 40) % M);
   constexpr uint32_t w6 = (uint32_t)((1ull << 48) % M), w7 = (uint32_t)((1ull << 56) % M);
   constexpr uint32_t KL = w0 | (w1 << 8) | (w2 << 16) | (w3 << 24), KH = w4 | (w5 << 8) | (w6 << 16) | (w7 << 24);
   constexpr uint32_t K3 = (uint32_t)((h + M - (uint32_t)((1ull << 62) % M)) % M);
   constexpr uint32_t MAG = (uint32_t)(((1ull << 32) + M - 1) / M);
+  if (UNS && M == 256) return lo;                 // y mod 256: the low byte (2^62 = 0 mod 256)
   const uint32_t r = __dp4a(hi, KH, __dp4a(lo, KL, K3));
   const uint32_t u = r - __umulhi(r, MAG) * (uint32_t)M;
-  return u - h;                                   // the low byte is the residue (packed by PRMT)
+  return UNS ? u : u - h;                         // the low byte is the residue (packed by PRMT)
 }
-template <int L>
+template <int L, bool UNS>
 __device__ __forceinline__ void crt_split4(const uint32_t (&lo)[4], const uint32_t (&hi)[4], int nm, int8_t *dst,
                                            int64_t plane) {
   if constexpr (L < CRT_MAX) {
     if (L < nm) {
       uint32_t b[4];
       #pragma unroll
-      for (int u = 0; u < 4; ++u) b[u] = crt_res8<kModuli[L]>(lo[u], hi[u]);
+      for (int u = 0; u < 4; ++u) b[u] = crt_res8<kModuli[L], UNS>(lo[u], hi[u]);
       *(uint32_t *)(dst + (int64_t)L * plane) =
           __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
-      crt_split4<L + 1>(lo, hi, nm, dst, plane);
+      crt_split4<L + 1, UNS>(lo, hi, nm, dst, plane);
     }
   }
 }
@@ -282,7 +285,7 @@ __device__ __forceinline__ void crt_split4(const uint32_t (&lo)[4], const uint32
 // `planes` holds (Xbar mod m_l) at planes[l * rows * cols + r * cols + k]; sig[r] = e_r.
 // SMEM: the row is staged in shared memory (cols * 8 B <= 64 KB), so the maximum pass and the residue
 // pass read it from DRAM once (with two global passes the residue writes evicted it between them).
-template <bool SMEM>
+template <bool SMEM, bool UNS>
 __global__ void __launch_bounds__(256, 3) k_crt_split(const double *__restrict__ X, int64_t ld, int64_t rows,
                                                       int64_t cols, int b, int nm, int8_t *planes, int *sig) {
   extern __shared__ double srow[];
@@ -327,23 +330,27 @@ __global__ void __launch_bounds__(256, 3) k_crt_split(const double *__restrict__
       const uint64_t y = (uint64_t)__double2ll_rn(__dmul_rn(__dmul_rn((u & 1) ? t.y : t.x, sc1), sc2)) + (1ull << 62);
       lo[u] = (uint32_t)y; hi[u] = (uint32_t)(y >> 32);
     }
-    crt_split4<0>(lo, hi, nm, planes + r * cols + k0, plane);
+    crt_split4<0, UNS>(lo, hi, nm, planes + r * cols + k0, plane);
   }
 }
 
 cudaError_t launch_crt_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int b, int nm, int8_t *planes,
                              int *sig, cudaStream_t s) {
   if (b < 2 || b > CRT_BMAX || nm < 2 || nm > CRT_MAX || cols % 4) return cudaErrorInvalidValue;
+  const bool uns = crt_unsigned(cols);           // cols = the GEMM's K (row length of the residue planes)
   if (cols * 8 <= 65536 && ld % 2 == 0) {
     static DeviceOnce attr;
     if (!attr.done()) {
-      cudaError_t e = cudaFuncSetAttribute(k_crt_split<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      cudaError_t e = cudaFuncSetAttribute(k_crt_split<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_crt_split<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
       if (e != cudaSuccess) return e;
       attr.set();
     }
-    k_crt_split<true><<<(unsigned)rows, 256, (size_t)cols * 8, s>>>(X, ld, rows, cols, b, nm, planes, sig);
+    if (uns) k_crt_split<true, true><<<(unsigned)rows, 256, (size_t)cols * 8, s>>>(X, ld, rows, cols, b, nm, planes, sig);
+    else k_crt_split<true, false><<<(unsigned)rows, 256, (size_t)cols * 8, s>>>(X, ld, rows, cols, b, nm, planes, sig);
   } else {
-    k_crt_split<false><<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, b, nm, planes, sig);
+    k_crt_split<false, false><<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, b, nm, planes, sig);
   }
   ++g_launches;
   return cudaGetLastError();
