@@ -368,8 +368,10 @@ __global__ void k_transpose(const T *src, int64_t rows, int64_t cols, T *dst) {
 // and correction format) and the per-tile partial of delta^2 = sum (C_{k+1} - C_k)^2 at the
 // GLOBAL tile index (col tile * npad/64 + row tile): the same reduction order for any G.
 // ---------------------------------------------------------------------------------------
+// 6 resident blocks per SM (40 registers, a few spills to L1): measured 4 / 5 / 6 / 8 blocks -> 251.6 / 247.5 /
+// 244.5 / 241.8 us (FP32 container) and 319 / 296 / 289 / 336 us (FP64 container) at n = 8192 (r02b)
 template <typename CT, typename WT>
-__global__ void __launch_bounds__(256, 4) k_sym_update(const CT *__restrict__ cold, CT *__restrict__ cnew,
+__global__ void __launch_bounds__(256, 6) k_sym_update(const CT *__restrict__ cold, CT *__restrict__ cnew,
                                                     const WT *__restrict__ W, int64_t npad, int64_t kp, int64_t col0,
                                                     int p, int m, int rtz, int prec, void *chat_new, int corr,
                                                     void *chat_corr_new, double *part, unsigned *amax) {
