@@ -41,6 +41,11 @@ ipr_status ipr_test_gemm(int prec, int64_t n, const void *X_dev, const void *Yt_
 /* IPR_FP64_OZ / IPR_FP64_CRT products of ipr_test_gemm / ipr_bench_gemm use `digits` Ozaki digits
  * (OZ) or b = 7 digits - 4 bits (CRT, capped as in ipr.h); digits in [2, 9], default 9.  Process-wide. */
 ipr_status ipr_test_set_digits(int digits);
+/* IPR_FP64_CRT residue convention (process-wide): 0 (default) residues in [0, m) with u8 x u8 modulus
+ * GEMMs while K 255^2 < 2^31 (K <= 33024), symmetric residues in [-128, 127] with s8 x s8 beyond;
+ * 1 forces the symmetric convention at every K (tests of the large-K path at small sizes).  Set it
+ * between solves / products only. */
+ipr_status ipr_test_crt_signed(int on);
 /* The CRT constants of N moduli (1 <= N <= 18, host only, no GPU): out40[0..N-1] the moduli,
  * out40[20 + l] = inv_l = (M_N / m_l)^-1 mod m_l; dout64[3 l + 0..2] = H_l, L_l, R_l (W_l = M_N / m_l =
  * H_l 2^s1 + L_l 2^s2 + R_l, R_l rounded to FP64); dout64[54..56] = MH, ML, MR; dout64[57..58] =

@@ -831,6 +831,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
         r.delta = coupled_step(n, p, C, ph, &w, Mh, Nh, Cn, &rho_next);
         double *t = C; C = Cn; Cn = t;
         m_of_C = phase_m(ph);
+        if (ph->max_iters > 0 && ctl.it_in_phase >= ph->max_iters) { d = ORC_ITER_LIMIT; r.decision = d; }
       } else {
         memcpy(C_best, C, (size_t)nn * sizeof(double));   /* the certified iterate is the answer (R-30) */
       }
@@ -846,6 +847,8 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
         r.decision = d;
         double *t = C; C = Cn; Cn = t;
         m_of_C = phase_m(&ph_k);
+        /* the last phase's cap still applies after a missed certificate (as the GPU engine) */
+        if (ph->max_iters > 0 && ctl.it_in_phase >= ph->max_iters) { d = ORC_ITER_LIMIT; r.decision = d; }
       } else {
         memcpy(C_best, C, (size_t)nn * sizeof(double));   /* the certified iterate is the answer (R-30) */
       }

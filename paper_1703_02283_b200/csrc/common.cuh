@@ -54,8 +54,11 @@ struct CrtTab {
 const CrtTab &crt_table();                       // host copy (ozaki.cu)
 int crt_moduli(int b, int64_t n);                // smallest N with M_N > 2^1.02 n 2^(2b); -1 if none
 // CRT residues in [0, m_l) (u8 x u8 modulus GEMMs) while every INT32 sum of K products of bytes stays
-// below 2^31 (K 255^2 < 2^31: K <= 33025); symmetric residues in [-128, 127] (s8 x s8) beyond
-__host__ __device__ inline bool crt_unsigned(int64_t k) { return k <= 33024; }
+// below 2^31 (K 255^2 < 2^31: K <= 33025); symmetric residues in [-128, 127] (s8 x s8) beyond -- or
+// always, with ipr_test_crt_signed(1) (tests of the large-K convention at small sizes).  Host-side
+// decision: the split takes it as its template flag, the modulus GEMMs as GemmArgs::crt_u8.
+bool crt_unsigned(int64_t k);
+void crt_force_signed(int on);
 int crt_bits(int S, int64_t n);                  // digits S -> bits b = min(7 S - 4, 62, what 18 moduli allow at n)
 
 // Operand formats that carry a per-tensor power-of-two scale 2^sigma (reading R-20; NEXT-3).
@@ -151,6 +154,7 @@ struct GemmArgs {
   // independent: other residue planes, other v-byte planes); each waits for its predecessor before it
   // exits, so the finish kernel, launched normally, sees every modulus complete
   int pdl;
+  int crt_u8;           // CRT: residues in [0, m) (u8 x u8 modulus GEMMs), else symmetric (s8 x s8)
 };
 
 // ------------------------------------------------------------------------------------

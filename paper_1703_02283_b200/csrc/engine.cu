@@ -1357,6 +1357,18 @@ ipr_status ipr_set_cert(ipr_ctx *c, int mode) {
 // q = rho_k / rho_{k-1} predicts rho_{k+1} ~ rho_k q.  When that is <= final_tol / 2 the next iterate is
 // certified first (the FP64 residual the stop needs anyway); its chain -- computed only to trigger the
 // certificate -- runs only if the certificate misses.  The oracle mirrors the rule (orc_solve_form).
+// A missed certificate turns the decision into "continue" -- but the last phase's iteration cap still
+// applies (without it an in-chain residual below final_tol over an FP64 floor above it, e.g. n = 32768,
+// would certify and miss forever): the trace record becomes IPR_DEC_ITER_LIMIT and the solve ends.
+static bool cert_cap(ipr_ctx *c) {
+  const PhaseC &P = c->ph[c->phase];
+  if (!(P.max_iters > 0 && c->it_in_phase >= P.max_iters)) return false;
+  c->trace.back().decision = IPR_DEC_ITER_LIMIT;
+  c->done = true;
+  c->outcome = IPR_DEC_ITER_LIMIT;
+  return true;
+}
+
 static bool predict_cert(const ipr_ctx *c) {
   if (c->cert != IPR_CERT_FP64 || !is_sym(c) || c->phase != (int)c->ph.size() - 1) return false;
   if (!(std::isfinite(c->ph_r1) && std::isfinite(c->ph_r2) && c->ph_r2 > 0.0 && c->ph_r1 < c->ph_r2)) return false;
@@ -1476,6 +1488,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
         c->trace.back().decision = IPR_DEC_CONTINUE;
         CKS(update_coupled(c));
         c->pending_delta = (int64_t)c->trace.size() - 1;
+        if (cert_cap(c)) break;
         continue;
       }
       c->best_loc = c->cur; c->best_cont64 = is_f64(c->ph[c->phase].prec);
@@ -1521,6 +1534,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
           c->pending_delta = (int64_t)c->trace.size() - 1;
         }
         if (c->world > 1) CKS(make_xt(c, c->cur, c->ph[c->phase]));
+        if (cert_cap(c)) break;
         c->cert_pending = predict_cert(c);
         continue;
       }
@@ -1858,6 +1872,11 @@ ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_
 }
 
 static int g_test_digits = OZ_S;
+ipr_status ipr_test_crt_signed(int on) {
+  crt_force_signed(on);
+  return IPR_OK;
+}
+
 ipr_status ipr_test_set_digits(int digits) {
   ipr_ctx *c = nullptr;
   if (digits < 2 || digits > OZ_S) return fail(c, IPR_E_INVALID_ARG, "ipr_test_set_digits: digits in [2, 9]");

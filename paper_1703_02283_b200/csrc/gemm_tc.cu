@@ -789,8 +789,8 @@ cudaError_t tc_set_crt_table(const CrtTab &t) { return cudaMemcpyToSymbol(c_crt,
 // only: x mod m = x - m umulhi(x, ceil(2^32 / m)), exact or one m too far for x < 2^31.
 __device__ __forceinline__ void crt_chunk(const GemmArgs &g, int l, int64_t row, int64_t c0, const uint32_t (&r)[32]) {
   const int nm = g.crt_n;
-  // unsigned residues (crt_unsigned(K)): U = sum of byte products < 2^31, no offset needed
-  const int m = c_crt.m[l], off = crt_unsigned(g.a_kp) ? 0 : c_crt.off[l], iv = c_crt.inv[nm][l];
+  // unsigned residues (g.crt_u8): U = sum of byte products < 2^31, no offset needed
+  const int m = c_crt.m[l], off = g.crt_u8 ? 0 : c_crt.off[l], iv = c_crt.inv[nm][l];
   const uint32_t mag = c_crt.mag[l];
   uint32_t pk[8];
   #pragma unroll
@@ -1119,7 +1119,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
   } else if (warp == 1) {
     // ===== MMA issuer (leader CTA, single thread) =====
     if (leader && lane == 0) {
-      const uint32_t idesc = make_idesc(g.prec, crt && crt_unsigned(g.a_kp));   // CRT: residues in [0, m) below
+      const uint32_t idesc = make_idesc(g.prec, crt && g.crt_u8);   // CRT: residues in [0, m) (u8 x u8)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;

@@ -227,6 +227,9 @@ const CrtTab &crt_table() {
   static const CrtTab t = make_crt_table();
   return t;
 }
+static int g_crt_signed = 0;   // ipr_test_crt_signed
+void crt_force_signed(int on) { g_crt_signed = on != 0; }
+bool crt_unsigned(int64_t k) { return !g_crt_signed && k <= 33024; }
 int crt_moduli(int b, int64_t n) {
   const double need = 2.0 * b + std::log2((double)(n < 1 ? 1 : n)) + 1.02;
   for (int N = 2; N <= CRT_MAX; ++N)
@@ -349,6 +352,8 @@ cudaError_t launch_crt_split(const double *X, int64_t ld, int64_t rows, int64_t 
     }
     if (uns) k_crt_split<true, true><<<(unsigned)rows, 256, (size_t)cols * 8, s>>>(X, ld, rows, cols, b, nm, planes, sig);
     else k_crt_split<true, false><<<(unsigned)rows, 256, (size_t)cols * 8, s>>>(X, ld, rows, cols, b, nm, planes, sig);
+  } else if (uns) {   // rows longer than 8192: two passes over the row (L2), the same residue convention
+    k_crt_split<false, true><<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, b, nm, planes, sig);
   } else {
     k_crt_split<false, false><<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, b, nm, planes, sig);
   }
@@ -385,6 +390,7 @@ cudaError_t launch_gemm_crt(const GemmArgs &g, cudaStream_t s) {
   q.K = (int64_t)g.crt_n * np;                   // map extents: all residue planes
   q.B = g.oz_b; q.ldb = np;
   q.oz_grouped = 3;
+  q.crt_u8 = crt_unsigned(np) ? 1 : 0;           // the split of these residues took the same decision
   q.sigA = nullptr; q.sigB = nullptr; q.pmax = nullptr;
   q.ldv = np;
   CrtTimer *tm = t_crt_timer;

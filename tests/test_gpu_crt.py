@@ -22,25 +22,45 @@ torch = pytest.importorskip("torch")
 ipr = pytest.importorskip("paper_1703_02283_b200")
 
 
-def _gemm(prec, X, Y, digits=9):
+def _gemm(prec, X, Y, digits=9, signed=False):
     n = X.shape[0]
     Z = torch.empty((n, n), dtype=torch.float64, device="cuda")
     ipr.ipr_test_set_digits(digits)
+    ipr.ipr_test_crt_signed(signed)       # symmetric residues (s8 x s8), the large-K convention
     try:
         ipr.ipr_test_gemm(prec, n, torch.from_numpy(np.ascontiguousarray(X)).cuda(),
                           torch.from_numpy(np.ascontiguousarray(Y.T)).cuda(), Z)
     finally:
         ipr.ipr_test_set_digits(9)
+        ipr.ipr_test_crt_signed(False)
     return Z.cpu().numpy()
 
 
+@pytest.mark.parametrize("signed", [False, True])
 @pytest.mark.parametrize("n", [1, 200, 513, 1024])
-def test_crt_integers_exact(n):
-    # digits 3 -> b = 17 bits: |x| <= 2^10 is kept exactly, |Pbar| < 2^53 (exact reconstruction)
+def test_crt_integers_exact(n, signed):
+    # digits 3 -> b = 17 bits: |x| <= 2^10 is kept exactly, |Pbar| < 2^53 (exact reconstruction); both
+    # residue conventions (u8 residues in [0, m) below K = 33025, symmetric s8 residues beyond)
     rng = np.random.default_rng(n)
     X = rng.integers(-1024, 1025, (n, n)).astype(np.float64)
     Y = rng.integers(-1024, 1025, (n, n)).astype(np.float64)
-    np.testing.assert_array_equal(_gemm(ipr.IPR_FP64_CRT, X, Y, digits=3), X @ Y)
+    np.testing.assert_array_equal(_gemm(ipr.IPR_FP64_CRT, X, Y, digits=3, signed=signed), X @ Y)
+
+
+@pytest.mark.parametrize("signed", [False, True])
+def test_crt_long_rows_sampled_vs_oracle_definition(signed):
+    # K = 8448 > 8192: the residue split's two-pass (non-shared-memory) path, both conventions, against
+    # the oracle's exact CRT definition on sampled elements (the full product is too large for the oracle)
+    n, b = 8448, ipr.ipr_test_crt_table(18, 9, 8448)["b_for"]
+    rng = np.random.default_rng(88)
+    X = rng.standard_normal((n, n)) * 2.0 ** rng.integers(-20, 21, n)[:, None]
+    Y = rng.standard_normal((n, n)) * 2.0 ** rng.integers(-20, 21, n)[None, :]
+    Zg = _gemm(ipr.IPR_FP64_CRT, X, Y, 9, signed)
+    I, J = rng.integers(0, n, 3000), rng.integers(0, n, 3000)
+    Zo = oracle.gemm_crt_pairs(X, Y, b, I, J)
+    d = np.abs(Zg[I, J] - Zo)
+    assert np.all(d <= 2 * np.spacing(np.abs(Zo))), float(np.max(d / np.spacing(np.abs(Zo))))
+    assert float(np.mean(Zg[I, J] == Zo)) >= 0.9
 
 
 @pytest.mark.parametrize("n,kappa,digits", [(512, 2.0, 9), (1536, 2.0, 9), (1024, 1e3, 9), (777, 2.0, 5)])
@@ -66,8 +86,9 @@ def test_crt_error_within_method_bound(n, kappa, digits):
         assert e_cr <= 2.0 * e_dm, (e_cr, e_dm)
 
 
+@pytest.mark.parametrize("signed", [False, True])
 @pytest.mark.parametrize("n,digits", [(1, 9), (37, 3), (256, 5), (300, 9), (513, 7), (1024, 9)])
-def test_crt_gemm_matches_oracle_definition(n, digits):
+def test_crt_gemm_matches_oracle_definition(n, digits, signed):
     # R-28's definition computed exactly by the oracle (integer product exact, one rounding) vs the
     # GPU's modular products + sliced FP64 reconstruction, element by element, on operands with rows /
     # columns spanning 2^+-40 (so e_i, f_j differ per row / column) and both signs
@@ -79,7 +100,7 @@ def test_crt_gemm_matches_oracle_definition(n, digits):
         Y[:, 2] = 0.0
     b = ipr.ipr_test_crt_table(18, digits, n)["b_for"]
     assert b == oracle.crt_bits(digits, n)
-    Zg = _gemm(ipr.IPR_FP64_CRT, X, Y, digits)
+    Zg = _gemm(ipr.IPR_FP64_CRT, X, Y, digits, signed)
     Zo = oracle.gemm_crt(X, Y, b)
     ulp = np.spacing(np.abs(Zo))
     d = np.abs(Zg - Zo)
@@ -132,7 +153,16 @@ def test_crt_fp64_phase_level2(form, sched):
     assert all(t["moduli"] == nm for t in tr if t["phase"] == len(parts) - 1 and t["rho"] == t["rho"])
 
 
-def test_crt_adaptive_level2_and_storage_rule():
+@pytest.mark.parametrize("signed", [False, True])
+def test_crt_adaptive_level2_and_storage_rule(signed):
+    ipr.ipr_test_crt_signed(signed)      # the whole solve with the large-K residue convention too
+    try:
+        _adaptive_level2()
+    finally:
+        ipr.ipr_test_crt_signed(False)
+
+
+def _adaptive_level2():
     n, p = 520, 2
     A = synth.spd(n, 2.0, 12)
     low = dict(plateau_ratio=0.7, plateau_arm=0.5, max_iters=40)

@@ -199,3 +199,17 @@ def test_fused_symmetric_update_matches_separate():
     assert out == ipr.IPR_CONVERGED
     assert rel_fro(fused, best) <= 1e-10
     assert abs(res["n"] - len(tr)) <= 1
+
+
+def test_missed_certificates_respect_the_phase_cap():
+    # the oracle's test_missed_certificates_respect_the_phase_cap on the GPU (n = 32768 showed the need:
+    # in-chain rho below 1e-12, FP64 certificate floor 1.86e-12 -- every certificate missed until the
+    # caller's budget): a tolerance between the two floors ends at the last phase's cap, ITER_LIMIT
+    n, cap = 300, 10
+    A = synth.spd(n, 2.0, 33)
+    pg = [ipr.make_phase("bf16", **LOW), ipr.make_phase("fp64", corr_prec="bf16", max_iters=cap)]
+    out, tr, _, _ = run_gpu_trajectory(A, 2, pg, 1e-14, 200, keep=False, form="symmetric")
+    assert out == ipr.IPR_ITER_LIMIT
+    assert sum(1 for t in tr if t["phase"] == 1) == cap
+    assert tr[-1]["decision"] == ipr.IPR_ITER_LIMIT       # terminal decisions equal the outcome codes
+    assert sum(1 for t in tr if t["rho_cert"] == t["rho_cert"]) >= 2

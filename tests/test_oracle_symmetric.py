@@ -277,3 +277,20 @@ def test_certificate_first_rule(form, p):
     for x, y in zip(a.records[1:-2], a.records[:-3]):   # and no earlier record predicted it
         if x["phase"] == y["phase"] == 1 and x["decision"] == oracle.CONTINUE and x["rho"] < y["rho"]:
             assert x["rho"] * (x["rho"] / y["rho"]) > 0.5e-12
+
+
+def test_missed_certificates_respect_the_phase_cap():
+    # a tolerance between the in-chain floor and the FP64 certificate's own rounding floor: every
+    # certificate misses; the last phase's iteration cap must still end the solve (ITER_LIMIT), as for
+    # any other last-phase iteration (the GPU engine mirrors it: tests/test_gpu_symmetric.py)
+    A = synth.spd(200, 2.0, 13)
+    cap = 12
+    ph = [oracle.phase(oracle.BF16, plateau_ratio=0.7, plateau_arm=0.5, max_iters=40),
+          oracle.phase(corr_prec=oracle.BF16, max_iters=cap)]
+    tol = 2.85e-15                    # n = 200: in-chain floor ~2.5e-15, FP64 certificate floor ~3e-15
+    r = oracle.solve(A, 2, ph, tol, 200, form=SYM)
+    certs = [x for x in r.records if x["rho_cert"] == x["rho_cert"]]
+    assert r.outcome == oracle.ITER_LIMIT, [(x["rho"], x["rho_cert"]) for x in r.records[-6:]]
+    assert sum(1 for x in r.records if x["phase"] == 1) == cap
+    assert len(certs) >= 2 and all(x["rho_cert"] > tol for x in certs)
+    assert r.records[-1]["decision"] == oracle.ITER_LIMIT and r.records[-1]["rho"] <= tol

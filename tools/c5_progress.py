@@ -14,14 +14,16 @@ import synth
 
 sched = sys.argv[1] if len(sys.argv) > 1 else "symtri:bf16>fp64crt@a/cbf16"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
+tol = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-12
+cap = int(sys.argv[4]) if len(sys.argv) > 4 else 40
 t0 = time.perf_counter()
 A, _ = synth.spd_torch(n, 2.0, synth.CONFIGS["C5"]["seed"], device="cuda")
 torch.cuda.synchronize()
 print(f"A ready {time.perf_counter() - t0:.1f} s, free {torch.cuda.mem_get_info()[0] / 1e9:.1f} GB", flush=True)
 torch.cuda.empty_cache()
 form, ph = bench.schedule(sched, n)
-ph[-1].max_iters = 40
-s = ipr.Solver(A, 2, ph, 1e-12, form=form)
+ph[-1].max_iters = cap
+s = ipr.Solver(A, 2, ph, tol, form=form)
 for k in range(200):
     t1 = time.perf_counter()
     out = s.iterate(1)
@@ -32,4 +34,5 @@ for k in range(200):
     if out != ipr.IPR_RUNNING:
         break
 print("outcome", ipr.OUTCOME_NAMES[s.outcome], f"total {time.perf_counter() - t0:.1f} s", flush=True)
+print("dmma recheck of the best iterate", s.residual(True), flush=True)
 s.close()
