@@ -421,6 +421,7 @@ def main():
     if args.e2e_steps > 0:
         A_host = A.cpu().pin_memory()
         C_host = torch.empty_like(A_host).pin_memory()
+        solve(A_host, C_host, early_out=True)   # untimed warm-up of this path (copy stream, pool block of A)
         barrier()
         f0 = torch.cuda.Event(enable_timing=True)
         f1 = torch.cuda.Event(enable_timing=True)
