@@ -213,15 +213,19 @@ struct TileSched {      // pair tiles: tiles_m pair-rows (256 rows) x tiles_n (2
   }
   __device__ void get(int t, int &tm, int &tn) const {
     if (tri) {
+      // the tiles ON the diagonal first (their epilogue takes the slower mixed path): the last wave --
+      // whose epilogue nothing overlaps -- then holds only strictly-upper tiles
+      if (t < tiles_n) { tm = coff + t; tn = t; return; }
+      t -= tiles_n;
       for (int c0 = 0;; c0 += TRI_GC) {                // band [c0, c1): (coff + c0) * w full-width rows, then its diagonal
         const int c1 = min(c0 + TRI_GC, tiles_n), w = c1 - c0, fr = coff + c0;
-        const int nb = fr * w + w * (w + 1) / 2;
+        const int nb = fr * w + w * (w - 1) / 2;       // (the diagonal tiles went first)
         if (t < nb) {
           if (t < fr * w) { tm = t / w; tn = c0 + t % w; return; }
           t -= fr * w;
           int r = 0;
-          while (t >= w - r) { t -= w - r; ++r; }      // diagonal block: row fr + r has w - r tiles
-          tm = fr + r; tn = c0 + r + t;
+          while (t >= w - r - 1) { t -= w - r - 1; ++r; }   // diagonal block: row fr + r has w - r - 1 tiles right of it
+          tm = fr + r; tn = c0 + r + 1 + t;
           return;
         }
         t -= nb;
