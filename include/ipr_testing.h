@@ -46,6 +46,11 @@ ipr_status ipr_test_set_digits(int digits);
  * 1 forces the symmetric convention at every K (tests of the large-K path at small sizes).  Set it
  * between solves / products only. */
 ipr_status ipr_test_crt_signed(int on);
+/* The NCCL transport's plumbing on one GPU (NCCL refuses two ranks on one device, so the multi-process
+ * path cannot run here): dlopen and symbol binding, a 1-rank communicator from ipr_nccl_unique_id's
+ * source, an in-place all-gather, the grouped send / recv all-to-all and ncclCommSplit, results checked
+ * byte by byte.  IPR_E_NCCL (message in ipr_last_error) on any failure. */
+ipr_status ipr_test_nccl_selftest(void);
 /* The CRT constants of N moduli (1 <= N <= 18, host only, no GPU): out40[0..N-1] the moduli,
  * out40[20 + l] = inv_l = (M_N / m_l)^-1 mod m_l; dout64[3 l + 0..2] = H_l, L_l, R_l (W_l = M_N / m_l =
  * H_l 2^s1 + L_l 2^s2 + R_l, R_l rounded to FP64); dout64[54..56] = MH, ML, MR; dout64[57..58] =

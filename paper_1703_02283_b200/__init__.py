@@ -36,7 +36,7 @@ EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_
             "ipr_launch_count", "ipr_plan", "ipr_set_form", "ipr_bench_gemm", "ipr_bench_gemm_epi",
             "ipr_test_set_digits", "ipr_test_crt_table", "ipr_set_cert", "ipr_test_peek",
             "ipr_test_local_group_create", "ipr_test_local_group_destroy", "ipr_test_init_local",
-            "ipr_test_set_guards", "ipr_test_check_guards", "ipr_set_output", "ipr_test_crt_signed"]
+            "ipr_test_set_guards", "ipr_test_check_guards", "ipr_set_output", "ipr_test_crt_signed", "ipr_test_nccl_selftest"]
 IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ, IPR_FORM_SYMMETRIC, IPR_FORM_SYMMETRIC_TRI, IPR_FORM_COUPLED = 0, 1, 2, 3, 4
 IPR_CERT_FP64, IPR_CERT_PHASE, IPR_CERT_FP64_CHAIN = 0, 1, 2
 CERT_BY_NAME = {"fp64": IPR_CERT_FP64, "dmma": IPR_CERT_FP64, "phase": IPR_CERT_PHASE,
@@ -291,6 +291,11 @@ def ipr_test_quantize(mode: int, x_in, x_out, m: int = 0, round: int = IPR_RNE, 
 
 def ipr_test_gemm(prec: int, n: int, X, Yt, Z, stream=None):
     _check(_lib.ipr_test_gemm(prec, n, _ptr(X), _ptr(Yt), _ptr(Z), _stream(stream)))
+
+
+def ipr_test_nccl_selftest():
+    """NCCL transport plumbing on one GPU (ipr_testing.h); raises IprError on failure."""
+    _check(_lib.ipr_test_nccl_selftest())
 
 
 def ipr_test_crt_signed(on: bool):

@@ -1872,6 +1872,44 @@ ipr_status ipr_test_quantize(int mode, const void *in_dev, void *out_dev, int64_
 }
 
 static int g_test_digits = OZ_S;
+ipr_status ipr_test_nccl_selftest(void) {
+  // the NCCL transport's plumbing on one GPU (NCCL refuses two ranks on one device): dlopen + symbol
+  // binding, a 1-rank communicator, in-place all-gather, grouped send / recv all-to-all, split
+  ipr_ctx *c = nullptr;
+  std::string e;
+  unsigned char uid[128];
+  if (!NcclComm::unique_id(uid, &e)) return fail(c, IPR_E_NCCL, "nccl selftest: unique id: %s", e.c_str());
+  NcclComm comm;
+  if (!comm.init(1, 0, uid, &e)) return fail(c, IPR_E_NCCL, "nccl selftest: %s", e.c_str());
+  const size_t nb = 1 << 16;
+  std::vector<unsigned char> h(3 * nb), back(3 * nb);
+  for (size_t i = 0; i < nb; ++i) h[i] = (unsigned char)(i * 131 + 7);
+  unsigned char *d = nullptr;
+  cudaStream_t st = nullptr;
+  if (cudaMalloc((void **)&d, 3 * nb) != cudaSuccess || cudaStreamCreate(&st) != cudaSuccess)
+    return fail(c, IPR_E_CUDA, "nccl selftest: %s", cudaGetErrorString(cudaGetLastError()));
+  ipr_status s = IPR_OK;
+  cudaMemset(d, 0, 3 * nb);
+  cudaMemcpy(d, h.data(), nb, cudaMemcpyHostToDevice);
+  Transport *sub = nullptr;
+  if (!comm.allgather(d, d, nb, st)) s = fail(c, IPR_E_NCCL, "nccl selftest: all-gather: %s", comm.last_error());
+  else if (!comm.alltoall(d, d + nb, nb, st)) s = fail(c, IPR_E_NCCL, "nccl selftest: all-to-all: %s", comm.last_error());
+  else if (!(sub = comm.split(0, 0, &e))) s = fail(c, IPR_E_NCCL, "nccl selftest: split: %s", e.c_str());
+  else if (!sub->allgather(d + nb, d + 2 * nb, nb, st))
+    s = fail(c, IPR_E_NCCL, "nccl selftest: split all-gather: %s", sub->last_error());
+  if (s == IPR_OK && cudaStreamSynchronize(st) == cudaSuccess &&
+      cudaMemcpy(back.data(), d, 3 * nb, cudaMemcpyDeviceToHost) == cudaSuccess) {
+    for (size_t i = 0; i < 3 * nb && s == IPR_OK; ++i)
+      if (back[i] != h[i % nb]) s = fail(c, IPR_E_NCCL, "nccl selftest: byte %zu is %d, expected %d", i, back[i], h[i % nb]);
+  } else if (s == IPR_OK) {
+    s = fail(c, IPR_E_CUDA, "nccl selftest: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  delete sub;
+  cudaStreamDestroy(st);
+  cudaFree(d);
+  return s;
+}
+
 ipr_status ipr_test_crt_signed(int on) {
   crt_force_signed(on);
   return IPR_OK;

@@ -187,3 +187,9 @@ def test_nccl_bit_identical_to_one_gpu(A, case):
         assert out == out1
         _same_trace(tr, tr1)
         np.testing.assert_array_equal(C, C1)
+
+
+def test_nccl_transport_plumbing_one_gpu():
+    # the production transport's calls (dlopen'ed NCCL: init, in-place all-gather, grouped send / recv
+    # all-to-all, split) on a 1-rank communicator -- the multi-process test above needs >= 2 GPUs
+    ipr.ipr_test_nccl_selftest()
