@@ -89,6 +89,10 @@ def lib():
         L.orc_step_ns.argtypes = [C.c_int64, _dp, _dp, C.POINTER(Phase), _dp, _dp]
         L.orc_jacobi.argtypes = [C.c_int64, _dp, _dp, _dp]
         L.orc_set_predict_cert.argtypes = [C.c_int]
+        L.orc_set_cert_mode.argtypes = [C.c_int]
+        L.orc_cert_grid.argtypes = [C.c_int64, C.c_int, _dp, _dp]
+        L.orc_resid_dd.restype = C.c_double
+        L.orc_resid_dd.argtypes = [C.c_int64, C.c_int, _dp, _dp]
         L.orc_inv_proot_eig.argtypes = [C.c_int64, _dp, _dp, C.c_int, _dp]
         L.orc_spectral.argtypes = [C.c_int64, _dp, C.c_int, C.c_double, C.c_int, _dp]
         L.orc_fp16_sigma.argtypes = [C.c_double]
@@ -293,14 +297,17 @@ FORM_LITERAL, FORM_NEWTON_SCHULZ, FORM_SYMMETRIC, FORM_SYMMETRIC_TRI, FORM_COUPL
 
 def solve(A, p: int, phases, final_tol: float = 1e-12, max_total: int = 200,
           hist: int = 0, gamma_normA2: float = 0.0, form: int = FORM_LITERAL,
-          predict_cert: bool = True) -> SolveResult:
+          predict_cert: bool = True, cert: str = "fp64") -> SolveResult:
     """Full controller-driven solve (init + iterations), reading R-5 of DESIGN.md.
     form = FORM_LITERAL (Eq. 1 as printed), FORM_NEWTON_SCHULZ (p = 1, X(2I - AX)) or
     FORM_SYMMETRIC (p >= 2, C + (W + W^T)/(2p); convergence certified on ||I - C^p A||_F).
     predict_cert: reading R-33 (certificate-first iterates in the symmetric forms' last phase; the
-    GPU's IPR_CERT_FP64) -- False mirrors IPR_CERT_FP64_CHAIN."""
+    GPU's IPR_CERT_FP64) -- False mirrors IPR_CERT_FP64_CHAIN.
+    cert: "fp64" (R-30: the FP64 literal chain) or "crt" (R-35: the candidate's grid rounding
+    cert_grid(C, 62) certified by its double-double residual; that matrix is the answer)."""
     A = _f64(A)
     lib().orc_set_predict_cert(1 if predict_cert else 0)
+    lib().orc_set_cert_mode({"fp64": 0, "dmma": 0, "crt": 1}[cert])
     n = A.shape[0]
     arr = (Phase * len(phases))(*phases)
     recs = (Record * max_total)()
@@ -317,6 +324,20 @@ def solve(A, p: int, phases, final_tol: float = 1e-12, max_total: int = 200,
                     decision=r.decision, rho=r.rho, rho_hat=r.rho_hat, delta=r.delta,
                     gamma=r.gamma, rho_cert=r.rho_cert) for r in recs[:min(nrec.value, max_total)]]
     return SolveResult(out, records, best, H, s.value)
+
+
+def cert_grid(C_, b: int = 62) -> np.ndarray:
+    """Reading R-35: C rounded to the coarser of its row's and column's b-bit grids (ipr_oracle.h)."""
+    X = _f64(C_)
+    out = np.empty_like(X)
+    lib().orc_cert_grid(X.shape[0], b, _p(X), _p(out))
+    return out
+
+
+def resid_dd(A, X, p: int) -> float:
+    """||I - X^p A||_F in double-double arithmetic (the residual of the FP64 matrices X, A to ~1e-30)."""
+    A, X = _f64(A), _f64(X)
+    return lib().orc_resid_dd(A.shape[0], p, _p(A), _p(X))
 
 
 def jacobi(A):

@@ -724,6 +724,20 @@ int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int np
 static int g_predict_cert = 1;
 void orc_set_predict_cert(int on) { g_predict_cert = on != 0; }
 
+/* Certificate of a symmetric form's candidate C (R-30; R-35 with orc_set_cert_mode(1)): returns the
+ * certified residual; Ct receives the matrix it is the residual of (the answer when it passes). */
+static int g_cert_mode = 0;
+void orc_set_cert_mode(int mode) { g_cert_mode = mode; }
+static double sym_cert(int64_t n, int p, const double *A, const double *C, chain_ws *w, double *Ct) {
+  if (g_cert_mode == 1) {
+    orc_cert_grid(n, 62, C, Ct);
+    return orc_resid_dd(n, p, A, Ct);
+  }
+  const orc_phase ph64 = {ORC_FP64, -1, ORC_RNE, 0.0, 0.0, 0.0, 0, -1};
+  memcpy(Ct, C, (size_t)(n * n) * sizeof(double));
+  return chain(n, p, A, C, &ph64, w);
+}
+
 int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase *phases,
                    int nphases, double final_tol, int max_total, orc_record *rec, int cap_rec,
                    int *nrec, double *C_best, double *C_hist, int hist_cap, double gamma_normA2,
@@ -751,6 +765,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
   if (s_out) *s_out = s;
   double *C = (double *)malloc((size_t)nn * sizeof(double));
   double *Cn = (double *)malloc((size_t)nn * sizeof(double));
+  double *Ct = (double *)malloc((size_t)nn * sizeof(double));   /* the certified matrix (R-35) */
   double *g1 = NULL, *g2 = NULL;
   if (gamma_normA2 > 0) {
     g1 = (double *)malloc((size_t)nn * sizeof(double));
@@ -778,15 +793,14 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
     if (cert_pending) {               /* R-33: the predicted-converged iterate, certificate first */
       cert_pending = 0;
       if (C_hist && k < hist_cap) memcpy(C_hist + (int64_t)k * nn, C, (size_t)nn * sizeof(double));
-      const orc_phase ph64 = {ORC_FP64, -1, ORC_RNE, 0.0, 0.0, 0.0, 0, -1};
-      cert_pre = chain(n, p, A, C, &ph64, &w);
+      cert_pre = sym_cert(n, p, A, C, &w, Ct);
       if (cert_pre <= final_tol) {
         orc_record r;
         r.k = k; r.phase = ctl.phase; r.prec = ph->prec; r.mant_bits = m_of_C;
         r.decision = ORC_CONVERGED; r.rho = NAN; r.rho_hat = NAN; r.delta = NAN;
         r.gamma = (gamma_normA2 > 0) ? gamma_of(n, C, A, gamma_normA2, g1, g2) : NAN;
         r.rho_cert = cert_pre;
-        memcpy(C_best, C, (size_t)nn * sizeof(double));   /* the certified iterate is the answer */
+        memcpy(C_best, Ct, (size_t)nn * sizeof(double));  /* the certified matrix is the answer */
         if (*nrec < cap_rec) rec[*nrec] = r;
         *nrec += 1;
         outcome = ORC_CONVERGED;
@@ -840,8 +854,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
        * ||I - C^p A||_F with the FP64 literal chain (reading R-3); if it misses final_tol the
        * iteration continues from the update computed first (as the GPU engine does). */
       r.delta = update_sym(n, p, C, &ph_k, &w, Cn);
-      const orc_phase ph64 = {ORC_FP64, -1, ORC_RNE, 0.0, 0.0, 0.0, 0, -1};
-      r.rho_cert = isfinite(cert_pre) ? cert_pre : chain(n, p, A, C, &ph64, &w);   /* R-33: once */
+      r.rho_cert = isfinite(cert_pre) ? cert_pre : sym_cert(n, p, A, C, &w, Ct);   /* R-33: once */
       if (!(r.rho_cert <= final_tol)) {
         d = ORC_CONTINUE;
         r.decision = d;
@@ -850,7 +863,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
         /* the last phase's cap still applies after a missed certificate (as the GPU engine) */
         if (ph->max_iters > 0 && ctl.it_in_phase >= ph->max_iters) { d = ORC_ITER_LIMIT; r.decision = d; }
       } else {
-        memcpy(C_best, C, (size_t)nn * sizeof(double));   /* the certified iterate is the answer (R-30) */
+        memcpy(C_best, Ct, (size_t)nn * sizeof(double));  /* the certified matrix is the answer (R-30, R-35) */
       }
     } else if (d == ORC_CONTINUE && coupled) {
       r.delta = coupled_step(n, p, C, ph, &w, Mh, Nh, Cn, &rho_next);
@@ -884,7 +897,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
     if (d != ORC_CONTINUE && d != ORC_SWITCH) { outcome = d; break; }
   }
   ws_free(&w);
-  free(C); free(Cn); free(g1); free(g2); free(Mh); free(Nh);
+  free(C); free(Cn); free(Ct); free(g1); free(g2); free(Mh); free(Nh);
   return outcome;
 }
 
@@ -974,4 +987,85 @@ void orc_spectral(int64_t n, const double *lambda, int p, double s, int kmax, do
     for (int64_t i = 0; i < n; ++i) t[i] = t[i] * pow(((double)(p + 1) - t[i]) / (double)p, (double)p);
   }
   free(t);
+}
+
+/* ---------------------------------------------------------------------------------------------
+ * The CRT certificate (reading R-35): the grid rounding of the certified matrix and the
+ * double-double residual that the oracle certifies it with.
+ * ------------------------------------------------------------------------------------------- */
+void orc_cert_grid(int64_t n, int b, const double *C, double *Ct) {
+  int *e = (int *)malloc((size_t)n * sizeof(int));
+  for (int64_t i = 0; i < n; ++i) {
+    double mx = 0.0;
+    for (int64_t k = 0; k < n; ++k) if (fabs(C[i * n + k]) > mx) mx = fabs(C[i * n + k]);
+    int ex = 0;
+    if (mx > 0.0) frexp(mx, &ex);        /* mx = f 2^ex, f in [0.5, 1): floor(log2 mx) = ex - 1 */
+    e[i] = mx > 0.0 ? b - 1 - (ex - 1) : 0;
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      const int g = e[i] < e[j] ? e[i] : e[j];
+      Ct[i * n + j] = ldexp(rint(ldexp(C[i * n + j], g)), -g);
+    }
+  free(e);
+}
+
+/* double-double helpers (Knuth two-sum, fma two-product; no contraction is involved: fma() is
+ * called explicitly and is exact before its one rounding) */
+typedef struct { double hi, lo; } orc_dd;
+static orc_dd dd_two_sum(double a, double b) {
+  const double s = a + b, bb = s - a;
+  orc_dd r = {s, (a - (s - bb)) + (b - bb)};
+  return r;
+}
+static orc_dd dd_fast(double a, double b) {   /* |a| >= |b| */
+  const double s = a + b;
+  orc_dd r = {s, b - (s - a)};
+  return r;
+}
+static orc_dd dd_add(orc_dd x, orc_dd y) {
+  orc_dd s = dd_two_sum(x.hi, y.hi), t = dd_two_sum(x.lo, y.lo);
+  s.lo += t.hi;
+  s = dd_fast(s.hi, s.lo);
+  s.lo += t.lo;
+  return dd_fast(s.hi, s.lo);
+}
+static orc_dd dd_mul_d(orc_dd x, double y) {
+  const double p = x.hi * y;
+  double e = fma(x.hi, y, -p);
+  e += x.lo * y;
+  return dd_fast(p, e);
+}
+
+double orc_resid_dd(int64_t n, int p, const double *A, const double *X) {
+  const int64_t nn = n * n;
+  orc_dd *T = (orc_dd *)malloc((size_t)nn * sizeof(orc_dd));
+  orc_dd *U = (orc_dd *)malloc((size_t)nn * sizeof(orc_dd));
+  for (int64_t q = 0; q < nn; ++q) { T[q].hi = A[q]; T[q].lo = 0.0; }
+  for (int j = 1; j <= p; ++j) {       /* T_j = X T_{j-1} (reading R-1's right-to-left chain) */
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+      orc_dd *u = U + i * n;
+      for (int64_t c = 0; c < n; ++c) { u[c].hi = 0.0; u[c].lo = 0.0; }
+      for (int64_t k = 0; k < n; ++k) {
+        const double x = X[i * n + k];
+        const orc_dd *t = T + k * n;
+        for (int64_t c = 0; c < n; ++c) u[c] = dd_add(u[c], dd_mul_d(t[c], x));
+      }
+    }
+    orc_dd *w = T; T = U; U = w;
+  }
+  orc_dd ss = {0.0, 0.0};
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t c = 0; c < n; ++c) {
+      orc_dd r = {i == c ? 1.0 : 0.0, 0.0};
+      orc_dd t = T[i * n + c];
+      t.hi = -t.hi; t.lo = -t.lo;
+      r = dd_add(r, t);                /* R_ic = delta_ic - T_p[i][c] */
+      const double v = r.hi + r.lo;
+      orc_dd sq = {v * v, fma(v, v, -(v * v))};
+      ss = dd_add(ss, sq);
+    }
+  free(T); free(U);
+  return sqrt(ss.hi + ss.lo);
 }

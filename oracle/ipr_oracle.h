@@ -185,6 +185,25 @@ void orc_gemm_crt_pairs(int64_t n, int b, const double *X, const double *Y, int6
                         const int64_t *J, double *Z);
 double orc_q_int8(double x);
 
+/* The CRT certificate of the symmetric forms (reading R-35; not in the paper: it makes the
+ * north star's "residual <= 1e-12" a proven statement about the returned matrix).
+ * orc_cert_grid: the certified matrix Ct of a candidate C (n x n row-major): with the row exponents
+ *   e_i = b - 1 - floor(log2 max_k |c_ik|) of orc_gemm_crt (0 for a zero row),
+ *   Ct_ij = 2^{-g} rint(2^{g} c_ij),  g = min(e_i, e_j)   (rint = half to even)
+ * i.e. C rounded to the coarser of its row's and its column's b-bit grids -- so 2^{e_i} Ct_ij is an
+ * integer for every i, j and the row AND column quantisation of Ct to b bits is exact.  A symmetric C
+ * gives a symmetric Ct; |Ct_ij - c_ij| <= 2^{-g-1}; elements within 2^{b-53} of both maxima are kept.
+ * orc_resid_dd: ||I - X^p A||_F evaluated in double-double arithmetic (the right-to-left chain
+ *   T_1 = X A, T_j = X T_{j-1}, every product accumulated in double-double, R = I - T_p in
+ *   double-double): ~2^-100 relative per product, i.e. the exact residual of the FP64 matrices X, A
+ *   for every digit that matters (an FP64 evaluation carries ~n u |X||A| of rounding noise).
+ * orc_set_cert_mode: how orc_solve_form's symmetric forms certify (R-30): 0 = FP64 literal chain
+ *   (default); 1 = CRT (R-35): the candidate's Ct = orc_cert_grid(C, 62) is certified by
+ *   orc_resid_dd(Ct) and, when certified, Ct is the answer. */
+void orc_cert_grid(int64_t n, int b, const double *C, double *Ct);
+double orc_resid_dd(int64_t n, int p, const double *A, const double *X);
+void orc_set_cert_mode(int mode);
+
 #ifdef __cplusplus
 }
 #endif
