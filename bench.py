@@ -55,6 +55,10 @@ def parse():
     ap.add_argument("--schedule", default=DEFAULT_SCHEDULE,
                     help="[sym:|ns:]phase>phase..., phase = prec[/c<corr prec>], e.g. fp64, bf16>fp64, "
                          "sym:bf16>fp64/cbf16 (sym: = IPR_FORM_SYMMETRIC, NEXT-2)")
+    ap.add_argument("--cert", choices=["auto", "crt", "fp64"], default="auto",
+                    help="convergence certificate: crt = IPR_CERT_CRT (a proven bound on the exact residual, "
+                         "R-35; one GPU, symmetric p = 2 with an fp64crt phase), fp64 = IPR_CERT_FP64 (DMMA "
+                         "evaluation, R-30); auto = crt where it applies")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     return ap.parse_args()
@@ -284,8 +288,14 @@ def main():
     C_out = torch.empty_like(A)
     torch.cuda.synchronize()
     form, phases = schedule(args.schedule, n)
+    cert = args.cert
+    if cert == "auto":
+        crt_ok = world == 1 and form.startswith("symmetric") and p == 2 and \
+            any(ipr.PREC_NAMES[q.prec] == "fp64crt" for q in phases)
+        cert = "crt" if crt_ok else "fp64"
+    config["certificate"] = cert
     def solve(A_dev, out, early_out=False):
-        s = ipr.Solver(A_dev, p, phases, 1e-12, stream, world, rank, uid, form=form)
+        s = ipr.Solver(A_dev, p, phases, 1e-12, stream, world, rank, uid, form=form, cert=cert)
         if early_out:
             s.set_output(out)     # the certified answer streams to `out` while its certificate runs
         s.iterate(400)
@@ -320,17 +330,19 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     tr, outcome = traces[-1]
-    # independent check outside the timed region: one more solve, then ||I - C^p A||_F of the
-    # returned iterate recomputed by ipr_residual(certify=1) -- the literal chain on the FP64 DMMA pipe.
-    # The in-solve certificate (IPR_CERT_FP64, R-30) is that same computation, so the two agree bit for
-    # bit; "converged" requires both the outcome and this re-check <= 1e-12.
-    sv = ipr.Solver(A, p, phases, 1e-12, stream, world, rank, uid, form=form)
+    # independent check outside the timed region: one more solve, then its certificate recomputed from
+    # the returned matrix by ipr_residual(certify=1) (the same function as the in-solve certificate, so
+    # the two agree bit for bit), and the FP64 DMMA evaluation ipr_residual(certify=2) beside it.
+    # "converged" requires the outcome and the re-computed certificate <= 1e-12.
+    sv = ipr.Solver(A, p, phases, 1e-12, stream, world, rank, uid, form=form, cert=cert)
     sv.iterate(400)
-    rho_dmma = sv.residual(True)
+    rho_recheck = sv.residual(1)
+    cert_terms = ipr.ipr_test_cert_info(sv.ctx) if cert == "crt" else None
+    rho_dmma = sv.residual(2)
     sv.close()
-    cert = [t["rho_cert"] for t in tr if t["rho_cert"] == t["rho_cert"]]
-    final_rho = cert[-1] if cert else tr[-1]["rho"]
-    ok = outcome == ipr.IPR_CONVERGED and rho_dmma <= 1e-12
+    certs = [t["rho_cert"] for t in tr if t["rho_cert"] == t["rho_cert"]]
+    final_rho = certs[-1] if certs else tr[-1]["rho"]
+    ok = outcome == ipr.IPR_CONVERGED and rho_recheck <= 1e-12
 
     # roofline of the dominant kernel (the FP64 DMMA GEMM): algorithmic flops per launch =
     # 2 n^3 (local panel: 2 n^2 n/G); duration from the library's CUDA events on the launch stream
@@ -465,6 +477,25 @@ def main():
                            "final_rho": c2[-1] if c2 else t2[-1]["rho"],
                            "gemm_tflops_low": (lg * 2.0 * n ** 3 / (lms * 1e-3) / 1e12) if lms > 0 else None}
         extras["schedules"] = sched
+        # the same schedule certified by the FP64 DMMA evaluation (IPR_CERT_FP64, R-30) instead
+        if cert == "crt":
+            f2, ph = schedule(args.schedule, n)
+            torch.cuda.synchronize()
+            g0 = torch.cuda.Event(enable_timing=True)
+            g1 = torch.cuda.Event(enable_timing=True)
+            g0.record(stream)
+            s = ipr.Solver(A, p, ph, 1e-12, stream, form=f2, cert="fp64")
+            s.iterate(400)
+            g1.record(stream)
+            t2 = s.trace()
+            torch.cuda.synchronize()
+            c2 = [t["rho_cert"] for t in t2 if t["rho_cert"] == t["rho_cert"]]
+            extras["cert_fp64_dmma"] = {
+                "time_s": g0.elapsed_time(g1) / 1e3, "outcome": ipr.OUTCOME_NAMES[s.outcome],
+                "iters_per_phase": [sum(1 for t in t2 if t["phase"] == i) for i in range(len(ph))],
+                "rho_cert": c2[-1] if c2 else None,
+                "note": "IPR_CERT_FP64: the same schedule certified by the FP64 DMMA evaluation (1.5 DMMA GEMMs)"}
+            s.close()
         # the cost of the honest certificate: the default schedule with the phase-product estimate
         # (IPR_CERT_PHASE: the CRT product, p - 1 products instead of p DMMA GEMMs) -- diagnostics only,
         # its acceptance is not an FP64 certificate (ipr.h ipr_set_cert)
@@ -513,9 +544,16 @@ def main():
     line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
-            "converged": ok, "iterations": len(tr), "final_rho": final_rho, "final_rho_dmma_recheck": rho_dmma,
-            "certificate": "IPR_CERT_FP64: ||I - C^2 A||_F of the returned C by the literal chain on the FP64 DMMA "
+            "converged": ok, "iterations": len(tr), "final_rho": final_rho, "final_rho_recheck": rho_recheck,
+            "final_rho_dmma_recheck": rho_dmma,
+            "certificate": ("IPR_CERT_CRT (R-35): a proven upper bound on the EXACT ||I - C^2 A||_F of the returned C "
+                            "(the candidate on its 62-bit row/column grid), from exact integer products on the INT8 "
+                            "tensor cores plus the a-posteriori quantisation / reconstruction bounds, inside the timed "
+                            "solve (= ipr_residual(certify=1), bit for bit); final_rho_dmma_recheck is an FP64 DMMA "
+                            "evaluation of the same C (~n u rounding noise)") if cert == "crt" else
+                           "IPR_CERT_FP64: ||I - C^2 A||_F of the returned C by the literal chain on the FP64 DMMA "
                            "pipe inside the timed solve (= ipr_residual(certify=1), bit for bit)",
+            "certificate_terms": cert_terms,
             "iters_per_phase": [sum(1 for t in tr if t["phase"] == i) for i in range(len(phases))],
             "roofline": roof, "cpu_baseline": cb, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary()}

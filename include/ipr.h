@@ -243,8 +243,19 @@ ipr_status ipr_set_form(ipr_ctx *c, int form);
  *    linear rate predicts it, rho_k (rho_k / rho_{k-1}) <= final_tol / 2: then C_{k+1} is certified
  *    BEFORE its chain, which runs only if the certificate misses (the converged record then has
  *    rho = NaN).  IPR_CERT_FP64_CHAIN: the same certificate, triggered by the in-chain rho only.
+ *  IPR_CERT_CRT (reading R-35; symmetric forms, p = 2, one GPU, an IPR_FP64_CRT phase, FP64 last phase):
+ *    a PROVEN upper bound on ||I - Ct^2 A||_F, where Ct is the candidate C_k rounded to the coarser of its
+ *    row's and its column's 62-bit grids (|Ct - C_k| <= 2^-62 of the row / column maximum; the rounding
+ *    makes Ct's integer quantisation exact), from exact integer products on the INT8 tensor cores
+ *    (Y = Ct Ct on its upper tiles, then Y A; 1.5 x 18 modulus GEMMs) plus the quantisation and
+ *    reconstruction errors bounded a posteriori (||A||_2 <= ||A||_1, ||Y||_2 <= ||Y||_inf).  Converged
+ *    means that bound is <= final_tol, and Ct is the answer (it replaces C_k; ipr_set_output streams Ct).
+ *    Triggered like IPR_CERT_FP64 (R-33).  An FP64 DMMA evaluation carries ~n u |C|^2 |A| of rounding
+ *    noise (4-6e-13 at n = 8192); this bound is a statement about the exact residual.  Candidates whose
+ *    exponents leave (-400, 400) or that are not bitwise symmetric fall back to IPR_CERT_FP64's DMMA
+ *    evaluation of Ct.  Unsupported configurations fail at the first ipr_iterate (IPR_E_UNSUPPORTED).
  * Errors: IPR_E_INVALID_ARG (unknown mode), IPR_E_STATE (after the first ipr_iterate). */
-typedef enum { IPR_CERT_FP64 = 0, IPR_CERT_PHASE = 1, IPR_CERT_FP64_CHAIN = 2 } ipr_cert;
+typedef enum { IPR_CERT_FP64 = 0, IPR_CERT_PHASE = 1, IPR_CERT_FP64_CHAIN = 2, IPR_CERT_CRT = 3 } ipr_cert;
 ipr_status ipr_set_cert(ipr_ctx *c, int mode);
 
 /* Run at most max_iters (> 0) chains.  *iters_done = chains evaluated by this call,
@@ -252,10 +263,12 @@ ipr_status ipr_set_cert(ipr_ctx *c, int mode);
 ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *outcome);
 
 /* certify == 0: the in-chain residual of the latest evaluated iterate (reading R-4).
- * certify == 1: ||I - C_best^p A||_F recomputed with FP64 DMMA GEMMs from the best iterate (the one
+ * certify == 1: ||I - C_best^p A||_F recomputed (IPR_CERT_FP64: with FP64 DMMA GEMMs) from the best iterate (the one
  * ipr_finalize returns), the last GEMM keeping only its residual partials (reading R-3) -- the
  * form's own FP64 certificate, bit for bit: the literal form's FP64 chain C (C A) (its in-chain
- * rho), the symmetric / coupled forms' IPR_CERT_FP64 ((C C) A for p = 2, R-32). */
+ * rho), the symmetric / coupled forms' IPR_CERT_FP64 ((C C) A for p = 2, R-32) -- or, with IPR_CERT_CRT,
+ * that certificate's bound for Ct = the grid rounding of C_best (= C_best for a CRT-certified answer).
+ * certify == 2: the FP64 DMMA evaluation of C_best whatever the certificate mode. */
 ipr_status ipr_residual(ipr_ctx *c, int certify, double *rho);
 
 /* Copy up to cap trace records; *count = total records so far (may exceed cap). */

@@ -121,6 +121,12 @@ ipr_status ipr_test_check_guards(ipr_ctx *c, int corrupt_first, int *bad);
 /* Number of this process's kernel launches since load (all libipr kernels). */
 int64_t ipr_launch_count(void);
 
+/* The terms of the last IPR_CERT_CRT certificate of c (reading R-35; NaN before one ran):
+ * out[0] the certified bound (record.rho_cert), [1] ||I - P||_F as evaluated from the exact product,
+ * [2] beta (the bound's error terms), [3] ||Ytilde - Yh||_F, [4] ||Atilde - A||_F, [5] the ||A||_2 bound,
+ * [6] the ||Y||_2 bound, [7] eY, [8] eP (reconstruction bounds), [9] moduli.  out has 10 slots. */
+ipr_status ipr_test_cert_info(ipr_ctx *c, double *out10);
+
 #ifdef __cplusplus
 }
 #endif

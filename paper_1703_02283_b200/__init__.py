@@ -36,11 +36,12 @@ EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_
             "ipr_launch_count", "ipr_plan", "ipr_set_form", "ipr_bench_gemm", "ipr_bench_gemm_epi",
             "ipr_test_set_digits", "ipr_test_crt_table", "ipr_set_cert", "ipr_test_peek",
             "ipr_test_local_group_create", "ipr_test_local_group_destroy", "ipr_test_init_local",
-            "ipr_test_set_guards", "ipr_test_check_guards", "ipr_set_output", "ipr_test_crt_signed", "ipr_test_nccl_selftest"]
+            "ipr_test_set_guards", "ipr_test_check_guards", "ipr_set_output", "ipr_test_crt_signed", "ipr_test_nccl_selftest",
+            "ipr_test_cert_info"]
 IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ, IPR_FORM_SYMMETRIC, IPR_FORM_SYMMETRIC_TRI, IPR_FORM_COUPLED = 0, 1, 2, 3, 4
-IPR_CERT_FP64, IPR_CERT_PHASE, IPR_CERT_FP64_CHAIN = 0, 1, 2
+IPR_CERT_FP64, IPR_CERT_PHASE, IPR_CERT_FP64_CHAIN, IPR_CERT_CRT = 0, 1, 2, 3
 CERT_BY_NAME = {"fp64": IPR_CERT_FP64, "dmma": IPR_CERT_FP64, "phase": IPR_CERT_PHASE,
-                "fp64chain": IPR_CERT_FP64_CHAIN}
+                "fp64chain": IPR_CERT_FP64_CHAIN, "crt": IPR_CERT_CRT}
 FORM_BY_NAME = {"literal": IPR_FORM_LITERAL, "newton_schulz": IPR_FORM_NEWTON_SCHULZ, "ns": IPR_FORM_NEWTON_SCHULZ,
                 "symmetric": IPR_FORM_SYMMETRIC, "sym": IPR_FORM_SYMMETRIC,
                 "symmetric_tri": IPR_FORM_SYMMETRIC_TRI, "symtri": IPR_FORM_SYMMETRIC_TRI,
@@ -93,6 +94,7 @@ def _load():
     L.ipr_set_form.argtypes = [vp, C.c_int]
     L.ipr_set_cert.argtypes = [vp, C.c_int]
     L.ipr_test_peek.argtypes = [vp, C.c_int, vp, C.POINTER(C.c_int64)]
+    L.ipr_test_cert_info.argtypes = [vp, C.POINTER(C.c_double)]
     L.ipr_test_local_group_create.argtypes = [C.c_int, C.POINTER(vp)]
     L.ipr_test_local_group_destroy.argtypes = [vp]
     L.ipr_test_set_guards.argtypes = [C.c_int]
@@ -236,7 +238,9 @@ def ipr_iterate(ctx, max_iters: int):
     return done.value, out.value
 
 
-def ipr_residual(ctx, certify: bool = False) -> float:
+def ipr_residual(ctx, certify: int = 0) -> float:
+    """certify: 0 the in-chain residual, 1 the context's certificate of the best iterate, 2 its FP64 DMMA
+    evaluation (ipr.h)."""
     r = C.c_double(0)
     _check(_lib.ipr_residual(ctx, int(certify), C.byref(r)), ctx)
     return r.value
@@ -339,6 +343,16 @@ def ipr_bench_gemm_epi(prec, n: int, warmup: int = 2, iters: int = 5, epi: int =
 IPR_PEEK_AHAT, IPR_PEEK_CHAT, IPR_PEEK_Z1, IPR_PEEK_RHAT, IPR_PEEK_W, IPR_PEEK_CHATC = 0, 1, 2, 3, 4, 5
 
 
+CERT_INFO_KEYS = ("bound", "est", "beta", "dY", "dA", "A2", "Y2", "eY", "eP", "moduli")
+
+
+def ipr_test_cert_info(ctx) -> dict:
+    """The terms of the last IPR_CERT_CRT certificate (reading R-35; ipr_testing.h)."""
+    out = (C.c_double * 10)()
+    _check(_lib.ipr_test_cert_info(ctx, out), ctx)
+    return dict(zip(CERT_INFO_KEYS, list(out)))
+
+
 def ipr_test_peek(ctx, what: int, npad: int):
     """An intermediate of the last step as an (npad, npad) FP64 CUDA tensor (raw buffer order; see
     ipr_testing.h for which are K-major)."""
@@ -410,7 +424,7 @@ class Solver:
     def trace(self):
         return ipr_get_trace(self.ctx)
 
-    def residual(self, certify: bool = False) -> float:
+    def residual(self, certify: int = 0) -> float:
         return ipr_residual(self.ctx, certify)
 
     def norms(self):

@@ -50,6 +50,13 @@ struct CrtTab {
   double CH[CRT_MAX + 1], CL[CRT_MAX + 1];             // 256 sum_l H_l (exact), 256 sum_l Lo_l (bias of 256 + v)
   double p2s1[CRT_MAX + 1], p2s2[CRT_MAX + 1];
   double log2M[CRT_MAX + 1];
+  // exact four-slice form (the CRT certificate, reading R-35): W_l = H 2^s1 + L 2^s2 + X3 2^s3 + X4,
+  // every slice an integer < 2^39 (M: MH < 2^48), s2 = max(s1 - 39, 0), s3 = max(s2 - 39, 0); the
+  // biases 256 sum_l slice_l are exact; every sum of (256 + v_l) slice_l is an integer < 2^53
+  double X3[CRT_MAX + 1][CRT_MAX], X4[CRT_MAX + 1][CRT_MAX];
+  double MX3[CRT_MAX + 1], MX4[CRT_MAX + 1];
+  double CB2[CRT_MAX + 1], CB3[CRT_MAX + 1], CB4[CRT_MAX + 1];
+  double p2s3[CRT_MAX + 1];
 };
 const CrtTab &crt_table();                       // host copy (ozaki.cu)
 int crt_moduli(int b, int64_t n);                // smallest N with M_N > 2^1.02 n 2^(2b); -1 if none
@@ -155,6 +162,7 @@ struct GemmArgs {
   // exits, so the finish kernel, launched normally, sees every modulus complete
   int pdl;
   int crt_u8;           // CRT: residues in [0, m) (u8 x u8 modulus GEMMs), else symmetric (s8 x s8)
+  int crt_dd;           // CRT: reconstruct exactly as a double-double (the certificate, launch_crt_finish_dd)
 };
 
 // ------------------------------------------------------------------------------------
@@ -343,6 +351,7 @@ cudaError_t launch_gemm_ozaki(const GemmArgs &a, cudaStream_t s);  // FP64 on IN
 cudaError_t launch_gemm_crt(const GemmArgs &a, cudaStream_t s);    // FP64 on INT8, CRT (ozaki.cu)
 cudaError_t tc_set_crt_table(const CrtTab &t);                      // upload (gemm_tc.cu)
 cudaError_t launch_crt_finish(const GemmArgs &a, cudaStream_t s);  // CRT reconstruction + epilogue
+cudaError_t launch_crt_finish_dd(const GemmArgs &a, cudaStream_t s);  // exact CRT reconstruction (R-35)
 // Optional device timing of the kind::i8 GEMM launches of CRT products (the roofline's dominant kernel,
 // without the residue splits and the reconstruction): while set on this host thread, launch_gemm_crt
 // records an event pair around its GEMM launches (up to cap pairs; *used counts them).

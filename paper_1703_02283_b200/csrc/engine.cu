@@ -167,6 +167,11 @@ struct ipr_ctx {
   bool tl_on = false;
   std::vector<std::pair<const char *, cudaEvent_t>> tl;
   double cert_prev = NAN;               // R-33: that certificate missed: its value, for the chain's record
+  // IPR_CERT_CRT (reading R-35): per-row quantities of the certificate's splits [8][npad], the pinned
+  // host copy of its reductions, and the last certificate's components (ipr_test_cert_info)
+  double *certv = nullptr;
+  double *hcert = nullptr;
+  double cert_info[10] = {NAN, NAN, NAN, NAN, NAN, NAN, NAN, NAN, NAN, NAN};
   std::vector<size_t> guards;           // ipr_test_set_guards: arena offsets of the guard bands
 };
 
@@ -535,6 +540,8 @@ void *qplane(ipr_ctx *c, int i, int prec, int plane) {
 }
 // operand formats that share storage (FP64 and FP64-by-Ozaki both keep Chat in FP64)
 inline bool same_fmt(int a, int b) { return a == b || (is_f64(a) && is_f64(b)); }
+// IPR_CERT_CRT (reading R-35): the certificate quantises its operands to 62 bits (18 moduli up to n = 86000)
+constexpr int kCertBits = 62;
 inline bool is_sym(const ipr_ctx *c) { return c->form == IPR_FORM_SYMMETRIC || c->form == IPR_FORM_SYMMETRIC_TRI; }
 void *chatc_slot(ipr_ctx *c, int i, int prec) {
   return (char *)c->chatc[i] + (size_t)c->rank * (size_t)(c->npad * c->kp) * elt_size(prec);
@@ -1025,6 +1032,7 @@ void free_ctx(ipr_ctx *c) {
   if (c->arena) cudaFreeAsync(c->arena, c->st);   // back to the library's retained pool
   if (c->aux) cudaFreeAsync(c->aux, c->st);
   if (c->hscal) pinned_release(c->hscal);
+  if (c->hcert) pinned_release(c->hcert);
   for (auto &e : c->ev) if (e) cudaEventDestroy(e);
   for (auto &e : c->kev) if (e) cudaEventDestroy(e);
   if (c->cst) { cudaStreamSynchronize(c->cst); cudaStreamDestroy(c->cst); }
@@ -1085,6 +1093,7 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       {(void **)&c->full64, cr ? 0 : full * 8}, {&c->Acert, cr ? 0 : panel * 8},
       {&c->chat_rm, (cr && c->world > 1) ? full * 8 : 0},
       {&c->Tcol, c->grows > 1 ? panel * 8 : 0},
+      {(void **)&c->certv, (cr && is_sym(c) && c->world == 1) ? (size_t)c->npad * 8 * 8 : 0},
       {(void **)&c->partg, c->grows > 1 ? (size_t)c->world * c->npart * 8 : 0},
       {&c->msend, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0},
       {&c->mrecv, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0}};
@@ -1347,7 +1356,7 @@ ipr_status ipr_set_form(ipr_ctx *c, int form) {
 ipr_status ipr_set_cert(ipr_ctx *c, int mode) {
   if (!c) return fail(c, IPR_E_INVALID_ARG, "ipr_set_cert: null context");
   if (c->started) return fail(c, IPR_E_STATE, "ipr_set_cert: iteration already started");
-  if (mode != IPR_CERT_FP64 && mode != IPR_CERT_PHASE && mode != IPR_CERT_FP64_CHAIN)
+  if (mode != IPR_CERT_FP64 && mode != IPR_CERT_PHASE && mode != IPR_CERT_FP64_CHAIN && mode != IPR_CERT_CRT)
     return fail(c, IPR_E_INVALID_ARG, "ipr_set_cert: unknown mode %d", mode);
   c->cert = mode;
   return IPR_OK;
@@ -1370,7 +1379,8 @@ static bool cert_cap(ipr_ctx *c) {
 }
 
 static bool predict_cert(const ipr_ctx *c) {
-  if (c->cert != IPR_CERT_FP64 || !is_sym(c) || c->phase != (int)c->ph.size() - 1) return false;
+  if ((c->cert != IPR_CERT_FP64 && c->cert != IPR_CERT_CRT) || !is_sym(c) || c->phase != (int)c->ph.size() - 1)
+    return false;
   if (!(std::isfinite(c->ph_r1) && std::isfinite(c->ph_r2) && c->ph_r2 > 0.0 && c->ph_r1 < c->ph_r2)) return false;
   return c->ph_r1 * (c->ph_r1 / c->ph_r2) <= 0.5 * c->final_tol;
 }
@@ -1397,6 +1407,15 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
         return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ / IPR_FP64_CRT phases need a symmetric form");
       if (P.prec == IPR_FP64_OZ && c->world != 1)
         return fail(c, IPR_E_UNSUPPORTED, "ipr_iterate: IPR_FP64_OZ phases are single-GPU (IPR_FP64_CRT shards)");
+    }
+    if (c->cert == IPR_CERT_CRT) {   // reading R-35: where the CRT certificate is built
+      bool crt = false;
+      for (auto &P : c->ph) crt |= P.prec == IPR_FP64_CRT;
+      const int nm = crt_moduli(kCertBits, c->n);
+      if (!is_sym(c) || c->p != 2 || c->world != 1 || c->grows != 1 || !crt || !c->ph.back().cont64 || nm < 16)
+        return fail(c, IPR_E_UNSUPPORTED,
+                    "ipr_iterate: IPR_CERT_CRT needs a symmetric form with p = 2 on one GPU, an IPR_FP64_CRT phase and "
+                    "an FP64 last phase, and n <= 65535");
     }
     if (c->grows > 1) {   // the 2-D grid option: Eq. (1) as printed, unscaled tensor-core / DMMA formats
       if (c->form != IPR_FORM_LITERAL)
@@ -1634,6 +1653,7 @@ static ipr_status copy_iterate(ipr_ctx *c, int which, double *dst, int64_t ldc) 
 // stream while its certificate runs; finalize then only waits for it if C_k is the answer
 static ipr_status stream_candidate(ipr_ctx *c, int i) {
   c->out_valid = false;
+  if (c->cert == IPR_CERT_CRT) return IPR_OK;   // certify_crt streams the certified matrix Ct itself
   const PhaseC &P = c->ph[c->phase];
   if (!c->out_ptr || c->world != 1 || !P.cont64) return IPR_OK;
   if (!c->ost) {
@@ -1735,17 +1755,117 @@ static ipr_status certify_full64(ipr_ctx *c, double *rho) {
   return IPR_OK;
 }
 
+// Reading R-35 (IPR_CERT_CRT; symmetric forms, p = 2, one GPU): a PROVEN upper bound on ||I - Ct^2 A||_F
+// for the certified matrix Ct -- the candidate C in full64 rounded to the coarser of its row's and its
+// column's b-bit grids (b = 62; |Ct - C| <= 2^-62 relative to the row / column maximum) -- from exact
+// integer products on the INT8 tensor cores (Ozaki scheme II, R-28) instead of FP64 DMMA GEMMs:
+//   1. e_i from C's rows; Ct in place (full64); the residues of 2^e_i Ct_ij -- EXACT, so the one residue
+//      set is both operands of Y = Ct Ct (Ct is symmetric; checked bitwise)
+//   2. A staged in FP64 (T[1]) and split at b bits: Atilde, ||Atilde - A||_F
+//   3. Y = Ct Ct on the upper tiles (mirrored), reconstructed exactly as hi (T[1]) + lo (Zr)
+//   4. Y split from hi + lo: Ytilde, ||Ytilde - Yh||_F, the row sums of |hi| + |lo|
+//   5. P = Ytilde Atilde exact; the partials of (delta_ij - hi) - lo
+// Since I - Ct^2 A = (I - P) + (Ytilde - Y) Atilde + Y (Atilde - A) (Y = Ct^2 exact),
+//   ||I - Ct^2 A||_F <= ||I - P||_F + (dY + eY)(||A||_2 + dA) + ||Y||_2 dA,
+// with ||A||_2 <= ||A||_1 and ||Y||_2 <= ||Y||_inf (both symmetric), dY / dA the measured quantisation
+// errors, eY / eP the reconstruction bounds (n 2^(s1-48) max 2^-(e_i+f_j)), every FP64 sum inflated by
+// 1 + 1e-10 (>= n u for n <= 9e5).  *rho = that bound; c->cert_info keeps its terms.
+// i >= 0: the candidate came from iterate buffer i -- with ipr_set_output the certified Ct streams to the
+// caller during the products, and a passing Ct replaces C_i in its (FP64) container: Ct is the answer.
+static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
+  Nvtx nv("certify crt");
+  cudaStream_t st = c->st;
+  const int b = kCertBits, nm = crt_moduli(b, c->n);
+  const int64_t np = c->npad;
+  double *Ct = c->full64;
+  double *err2Y = c->certv, *asumY = c->certv + np, *scY = c->certv + 2 * np, *err2A = c->certv + 3 * np;
+  double *asumA = c->certv + 4 * np, *scA = c->certv + 5 * np, *scC = c->certv + 6 * np;
+  if (!c->hcert && !(c->hcert = pinned_acquire())) return fail(c, IPR_E_OOM, "pinned host slab exhausted");
+  // 1. the certified matrix and its residues
+  CK(launch_cert_rowexp(Ct, np, np, np, b, c->crC_sig, scC, st));
+  CK(launch_cert_round_split(Ct, np, np, np, nm, c->crC_sig, c->crC, st));
+  c->crC_for = -1;
+  CK(cudaMemsetAsync(c->dflag + 2, 0, 4, st));
+  CK(launch_symcheck(Ct, np, c->n, c->dflag + 2, st));
+  if (i >= 0 && c->out_ptr) {                      // ipr_set_output: stream Ct while the products run
+    if (!c->ost) {
+      CK(cudaStreamCreateWithFlags(&c->ost, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->oev, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->orev, cudaEventDisableTiming));
+    }
+    if (c->out_buf >= 0) CK(cudaStreamWaitEvent(st, c->oev, 0));
+    CK(cudaEventRecord(c->orev, st));
+    CK(cudaStreamWaitEvent(c->ost, c->orev, 0));
+    CK(cudaMemcpy2DAsync(c->out_ptr, (size_t)c->out_ld * 8, Ct, (size_t)np * 8, (size_t)c->n * 8, (size_t)c->n,
+                         cudaMemcpyDefault, c->ost));
+    CK(cudaEventRecord(c->oev, c->ost));
+    c->out_buf = i;
+  }
+  // 2. A (FP64, m = 52) and its residues
+  PhaseC P64{IPR_FP64, 52, 0, 1, 0, 0, 0, 0};
+  CKS(stage_a(c, P64, c->T[1], c->dsig + 0));
+  CK(launch_cert_split((const double *)c->T[1], nullptr, np, np, np, b, nm, c->crA, c->crA_sig, scA, err2A, asumA, st));
+  c->crA_b = -1;
+  // 3. Y = Ct Ct, upper tiles, exact, hi + lo
+  GemmArgs g = base_args(c, IPR_FP64_CRT, nullptr);
+  g.oz_a = c->crC; g.oz_rsig = c->crC_sig; g.oz_b = c->crC; g.oz_csig = c->crC_sig;
+  g.crt_n = nm; g.crt_v = c->crV; g.crt_dd = 1; g.tri = 1;
+  g.mode = EPI_STORE_N; g.nout = c->T[1]; g.ldn = np; g.zout = (double *)c->Zr; g.ldz = np;
+  CK(launch_gemm_crt(g, st));
+  // 4. residues of Y from hi + lo
+  CK(launch_cert_split((const double *)c->T[1], (const double *)c->Zr, np, np, np, b, nm, c->crC, c->crC_sig, scY,
+                       err2Y, asumY, st));
+  c->zr_for = -1;
+  // 5. P = Ytilde Atilde: residual partials
+  GemmArgs h = base_args(c, IPR_FP64_CRT, nullptr);
+  h.oz_a = c->crC; h.oz_rsig = c->crC_sig; h.oz_b = c->crA; h.oz_csig = c->crA_sig;
+  h.crt_n = nm; h.crt_v = c->crV; h.crt_dd = 1; h.mode = EPI_RESID; h.part = c->part;
+  CK(launch_gemm_crt(h, st));
+  CK(launch_reduce_sum(c->part, tiles_n_total(c, IPR_FP64_CRT) * tiles_m(c, IPR_FP64_CRT), c->dscal + 16, st));
+  const double *vv[6] = {err2Y, err2A, asumY, scY, scA, scC};
+  const int ops[6] = {0, 0, 1, 1, 1, 1};
+  CK(launch_cert_stats(vv, ops, 6, np, c->dscal + 17, st));
+  CK(cudaMemcpyAsync(c->hcert, c->dscal + 16, 7 * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(c->hcert + 7, c->dflag + 2, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const double SR = c->hcert[0], SY = c->hcert[1], SA = c->hcert[2], Yinf = c->hcert[3];
+  const double scYm = c->hcert[4], scAm = c->hcert[5], scCm = c->hcert[6];
+  int asym = 0;
+  memcpy(&asym, c->hcert + 7, 4);
+  const double infl = 1.0 + 1e-10, nd = (double)c->n, rec = ldexp(crt_table().p2s1[nm], -48);
+  const double eY = nd * rec * scCm * scCm, eP = nd * rec * scYm * scAm;
+  const double dY = std::sqrt(SY) * infl, dA = std::sqrt(SA) * infl;
+  const double A2 = c->norms[0] * infl, Y2 = Yinf * infl + eY;
+  const double est = std::sqrt(SR);
+  const double beta = (dY + eY) * (A2 + dA) + Y2 * dA + eP;
+  double bound = (est * infl + beta) * infl;
+  if (asym || !std::isfinite(bound)) bound = NAN;   // exponents out of range / an asymmetric candidate
+  const double info[10] = {bound, est, beta, dY, dA, A2, Y2, eY, eP, (double)nm};
+  memcpy(c->cert_info, info, sizeof info);
+  if (std::isnan(bound)) {                         // outside what the bound covers: the FP64 DMMA certificate
+    CKS(certify_full64(c, rho));
+    c->cert_info[0] = *rho;
+    return IPR_OK;
+  }
+  *rho = bound;
+  if (i >= 0 && bound <= c->final_tol)             // the certified Ct is the answer
+    CK(cudaMemcpyAsync(cont_ptr(c, i, c->ph[c->phase]), Ct, (size_t)np * np * 8, cudaMemcpyDeviceToDevice, st));
+  return IPR_OK;
+}
+
 // the iterate in buffer i (the candidate C_k), FP64, gathered into full64
 static ipr_status certify_iter(ipr_ctx *c, int i, double *rho) {
   const PhaseC &P = c->ph[c->phase];
   double *slot = c->full64 + (size_t)c->rank * c->npad * c->kp;
   CK(launch_cont_to_f64(cont_ptr(c, i, P), P.cont64, c->npad * c->kp, slot, c->st));
   CKS(gather_f64(c, slot));
+  if (c->cert == IPR_CERT_CRT) return certify_crt(c, i, rho);
   return certify_full64(c, rho);
 }
 
 static ipr_status certify_best(ipr_ctx *c, double *rho) {
   CKS(copy_iterate(c, 1, nullptr, 0));              // full64 = best (FP64, panel-major)
+  if (c->cert == IPR_CERT_CRT) return certify_crt(c, -1, rho);
   return certify_full64(c, rho);
 }
 
@@ -1755,7 +1875,12 @@ ipr_status ipr_residual(ipr_ctx *c, int certify, double *rho) {
   if (!certify) { *rho = c->last_rho; return IPR_OK; }
   if (c->grows > 1)   // the literal form's FP64 in-chain residual is already the DMMA literal chain
     return fail(c, IPR_E_UNSUPPORTED, "ipr_residual: certify = 1 on a 2-D grid (use the FP64 phase's in-chain rho)");
-  CKS(certify_best(c, rho));
+  if (certify == 2) {                              // the FP64 DMMA evaluation whatever the mode (R-30)
+    CKS(copy_iterate(c, 1, nullptr, 0));
+    CKS(certify_full64(c, rho));
+  } else {
+    CKS(certify_best(c, rho));
+  }
   // the certification chain reuses the T buffers: restore the transposed operand it clobbered
   if (c->world > 1 && c->form != IPR_FORM_LITERAL && !c->done) CKS(make_xt(c, c->cur, c->ph[c->phase]));
   return IPR_OK;
@@ -1794,6 +1919,12 @@ ipr_status ipr_finalize(ipr_ctx *c, double *C_dev_out, int64_t ldc) {
 
 // ---- test hooks (include/ipr_testing.h) ----
 int64_t ipr_launch_count(void) { return g_launches; }
+
+ipr_status ipr_test_cert_info(ipr_ctx *c, double *out10) {
+  if (!c || !out10) return fail(c, IPR_E_INVALID_ARG, "ipr_test_cert_info: null pointer");
+  memcpy(out10, c->cert_info, sizeof c->cert_info);
+  return IPR_OK;
+}
 
 ipr_status ipr_test_set_guards(int on) {
   g_guards = on ? 1 : 0;

@@ -1034,6 +1034,167 @@ cudaError_t launch_crt_finish(const GemmArgs &a_in, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// CRT reconstruction for the certificate (reading R-35): the EXACT integer Pbar of every element,
+// returned as a double-double.  W_l = H 2^s1 + L 2^s2 + X3 2^s3 + X4 with integer slices < 2^39, so each
+// slice sum S_k = sum_l (256 + v_l) slice_l is an exact FP64 integer (< 2^53); q = rint(X / M) is
+// exact (X / M within 0.493 of an integer, evaluated to ~2^-40), D_k = S_k - bias_k - q M_k exact, and
+// Pbar = D_1 2^s1 + D_2 2^s2 + D_3 2^s3 + D_4 by an error-free two-sum cascade: hi + lo = Pbar within
+// 6 u^2 sum_k |D_k 2^sk| <= 2^(s1 - 48) (engine.cu certify_crt bounds it), scaled by 2^-(e_i + f_j)
+// exactly.  MODE 0: hi -> nout, lo -> zout (tri: the upper elements and their mirrors, K-major through
+// two shared-memory slabs as in k_crt_finish); MODE 1: per-tile partials of R_ij^2, R_ij = (delta_ij -
+// hi) - lo over i, j < n (tri weight 2 off the diagonal).  Exponents are in (-400, 400) (the
+// certificate's splits flag anything else), so every scaling is exact.
+__device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
+  s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+template <int NM, int MODE>
+__global__ void __launch_bounds__(256, 2) k_crt_finish_dd(const GemmArgs g) {
+  extern __shared__ double sm_dd[];            // MODE 0: [2][32][CRT_FIN_LD]
+  __shared__ double red[8];
+  const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN), g.tri, (int)(g.col0 / TC_BN)};
+  int tm, tn;
+  sch.get((int)(blockIdx.x >> 1), tm, tn);
+  const int tile_m = tm * 2 + (int)(blockIdx.x & 1);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int nm = NM;
+  const double p1 = c_crt.p2s1[nm], p2 = c_crt.p2s2[nm], p3 = c_crt.p2s3[nm], iM = c_crt.invM[nm];
+  const double MH = c_crt.MH[nm], ML = c_crt.ML[nm], M3 = c_crt.MX3[nm], M4 = c_crt.MX4[nm];
+  const double B1 = c_crt.CH[nm], B2 = c_crt.CB2[nm], B3 = c_crt.CB3[nm], B4 = c_crt.CB4[nm];
+  double r2 = 0.0;
+  const int64_t r0 = (int64_t)tile_m * TC_BM;
+  double *slh = sm_dd, *sll = sm_dd + 32 * CRT_FIN_LD;
+  #pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+    const int64_t colb = (int64_t)tn * TC_BN + 128 * half, c0 = colb + 4 * lane;
+    double scol[4];
+    #pragma unroll
+    for (int u = 0; u < 4; ++u) scol[u] = pow2(-g.oz_csig[c0 + u]);
+    #pragma unroll 1
+    for (int slab = 0; slab < 4; ++slab) {
+      #pragma unroll 1
+      for (int i2 = 0; i2 < 4; ++i2) {
+        const int rl = 4 * w + i2;
+        const int64_t row = r0 + slab * 32 + rl;
+        uint32_t bv[NM];
+        {
+          const uint8_t *src = g.crt_v + row * g.ldv + c0;
+          const int64_t plane = g.M * g.ldv;
+          #pragma unroll
+          for (int l = 0; l < NM; ++l) bv[l] = *(const uint32_t *)(src + l * plane);
+        }
+        double s1[4], s2[4], s3[4], s4[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) { s1[u] = 0.0; s2[u] = 0.0; s3[u] = 0.0; s4[u] = 0.0; }
+        #pragma unroll
+        for (int l = 0; l < NM; ++l) {
+          const double h1 = c_crt.H[nm][l], h2 = c_crt.L[nm][l], h3 = c_crt.X3[nm][l], h4 = c_crt.X4[nm][l];
+          #pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t f = u == 0 ? (bv[l] << 12) : u == 1 ? (bv[l] << 4) : u == 2 ? (bv[l] >> 4) : (bv[l] >> 12);
+            const double d = __hiloint2double((int)((f & 0xff000u) | 0x40700000u), 0);   // 256 + v_l
+            s1[u] = __fma_rn(d, h1, s1[u]);            // integers < 2^53: exact
+            s2[u] = __fma_rn(d, h2, s2[u]);
+            s3[u] = __fma_rn(d, h3, s3[u]);
+            s4[u] = __fma_rn(d, h4, s4[u]);
+          }
+        }
+        const double srow = pow2(-g.oz_rsig[row]);
+        double vh[4], vl[4];
+        #pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double t1 = __dsub_rn(s1[u], B1), t2 = __dsub_rn(s2[u], B2);   // exact
+          const double t3 = __dsub_rn(s3[u], B3), t4 = __dsub_rn(s4[u], B4);
+          const double q = rint(__dmul_rn(__fma_rn(t1, p1, __dmul_rn(t2, p2)), iM));
+          const double a = __dmul_rn(__fma_rn(-q, MH, t1), p1);          // D_1 2^s1 (exact)
+          const double b = __dmul_rn(__fma_rn(-q, ML, t2), p2);
+          const double c = __dmul_rn(__fma_rn(-q, M3, t3), p3);
+          const double d = __fma_rn(-q, M4, t4);
+          double sA, e1, sB, e2, sC, e3, hi, lo;
+          two_sum(a, b, sA, e1);
+          two_sum(sA, c, sB, e2);
+          two_sum(sB, d, sC, e3);
+          two_sum(sC, __dadd_rn(__dadd_rn(e1, e2), e3), hi, lo);
+          const double sc = __dmul_rn(srow, scol[u]);                      // 2^-(e_i + f_j): exact
+          vh[u] = __dmul_rn(hi, sc);
+          vl[u] = __dmul_rn(lo, sc);
+        }
+        if (MODE == 0) {
+          #pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int64_t gc = g.col0 + c0 + u;
+            if (!g.tri || row <= gc) {
+              ((double *)g.nout)[row * g.ldn + c0 + u] = vh[u];
+              g.zout[row * g.ldz + c0 + u] = vl[u];
+            }
+            slh[rl * CRT_FIN_LD + 5 * lane + u] = vh[u];
+            sll[rl * CRT_FIN_LD + 5 * lane + u] = vl[u];
+          }
+        } else {
+          #pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int64_t gc = g.col0 + c0 + u;
+            if (row < g.n && gc < g.n && (!g.tri || row <= gc)) {
+              const double rr = __dsub_rn(__dsub_rn(row == gc ? 1.0 : 0.0, vh[u]), vl[u]);
+              r2 = __fma_rn((g.tri && row < gc) ? 2.0 * rr : rr, rr, r2);
+            }
+          }
+        }
+      }
+      if (MODE == 0) {
+        __syncthreads();
+        if (g.tri) {                                     // mirrors: (row, c) -> [c][row], 32 rows per warp
+          const int64_t row = r0 + slab * 32 + lane;
+          #pragma unroll 4
+          for (int j = 0; j < 16; ++j) {
+            const int cl = w * 16 + j;
+            const int64_t c = colb + cl;
+            if (row < g.col0 + c) {
+              ((double *)g.nout)[c * g.ldn + row] = slh[lane * CRT_FIN_LD + cl + (cl >> 2)];
+              g.zout[c * g.ldz + row] = sll[lane * CRT_FIN_LD + cl + (cl >> 2)];
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+  }
+  if (MODE == 1) {
+    const double sum = block_sum_det<256>(r2, red);
+    if (threadIdx.x == 0) g.part[((g.col0 + (int64_t)tn * TC_BN) / TC_BN) * g.tiles_m + tile_m] = sum;
+  }
+}
+
+cudaError_t launch_crt_finish_dd(const GemmArgs &a, cudaStream_t s) {
+  const TileSched hs{(int)(a.M / (2 * TC_BM)), (int)(a.N / TC_BN), a.tri, (int)(a.col0 / TC_BN)};
+  const int mode = (a.mode & EPI_RESID) ? 1 : 0;
+  if (mode == 0 && (!a.nout || !a.zout)) return cudaErrorInvalidValue;
+  if (mode == 1 && a.tri) {   // the tiles below the diagonal are not visited: zero partials
+    cudaError_t z = cudaMemsetAsync(a.part + (a.col0 / TC_BN) * a.tiles_m, 0, (size_t)(a.N / TC_BN) * a.tiles_m * sizeof(double), s);
+    if (z != cudaSuccess) return z;
+  }
+  const int smem = mode == 0 ? 2 * 32 * CRT_FIN_LD * 8 : 0;
+#define CRT_FIN_DD(N)                                                                                     \
+  case N: {                                                                                               \
+    static DeviceOnce attr;                                                                               \
+    if (!attr.done()) {                                                                                   \
+      cudaError_t e = cudaFuncSetAttribute(k_crt_finish_dd<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 32 * CRT_FIN_LD * 8); \
+      if (e != cudaSuccess) return e;                                                                     \
+      attr.set();                                                                                         \
+    }                                                                                                     \
+    if (mode == 0) k_crt_finish_dd<N, 0><<<2 * hs.count(), 256, smem, s>>>(a);                            \
+    else k_crt_finish_dd<N, 1><<<2 * hs.count(), 256, 0, s>>>(a);                                         \
+  } break;
+  switch (a.crt_n) {
+    CRT_FIN_DD(16) CRT_FIN_DD(17) CRT_FIN_DD(18)
+    default: return cudaErrorInvalidValue;
+  }
+#undef CRT_FIN_DD
+  ++g_launches;
+  return cudaGetLastError();
+}
+
 // EF = 1: the fused symmetric update (EPI_SYMUPD) is the only epilogue of this instance -- with the
 // general epilogue's code in the same kernel the instruction cache thrashed (tensor pipe 30 % busy,
 // "no instruction" the top stall)

@@ -41,6 +41,14 @@ cudaError_t launch_oz_split(const double *X, int64_t ld, int64_t rows, int64_t c
                             int8_t *bcat, int *sig, cudaStream_t s);
 cudaError_t launch_crt_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int b, int nm, int8_t *planes,
                              int *sig, cudaStream_t s);
+// the CRT certificate (reading R-35, ozaki.cu)
+cudaError_t launch_cert_rowexp(const double *X, int64_t ld, int64_t rows, int64_t cols, int b, int *sig, double *scale,
+                               cudaStream_t s);
+cudaError_t launch_cert_round_split(double *X, int64_t ld, int64_t rows, int64_t cols, int nm, const int *sig,
+                                    int8_t *planes, cudaStream_t s);
+cudaError_t launch_cert_split(const double *Xh, const double *Xl, int64_t ld, int64_t rows, int64_t cols, int b, int nm,
+                              int8_t *planes, int *sig, double *scale, double *err2, double *asum, cudaStream_t s);
+cudaError_t launch_cert_stats(const double *const *v, const int *op, int nv, int64_t len, double *out, cudaStream_t s);
 cudaError_t launch_fill_operand(void *dst, int64_t count, int prec, uint32_t seed, cudaStream_t s);
 cudaError_t launch_test_quant(int mode, const void *in, void *out, int64_t len, int m, int rtz, int sigma,
                               cudaStream_t s);

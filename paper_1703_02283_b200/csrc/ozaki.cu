@@ -201,14 +201,23 @@ CrtTab make_crt_table() {
       r = (double)W.ld(s2);
       low = (double)(W.ld(s1) / ldexpl(1.0L, s1));
     };
+    const int s3 = s2 > 39 ? s2 - 39 : 0;
+    double b2 = 0.0, b3 = 0.0, b4 = 0.0;
     for (int l = 0; l < N; ++l) {
       Big W = M;
       W.divmod((uint32_t)kModuli[l]);
       Big Wc = W;
       t.inv[N][l] = (int)modinv((int64_t)Wc.divmod((uint32_t)kModuli[l]), kModuli[l]);
       slice(W, t.H[N][l], t.L[N][l], t.R[N][l], t.Lo[N][l]);
+      t.X3[N][l] = (double)W.bits(s3, s2 - s3);
+      t.X4[N][l] = (double)W.bits(0, s3);
+      b2 += 256.0 * t.L[N][l]; b3 += 256.0 * t.X3[N][l]; b4 += 256.0 * t.X4[N][l];   // exact: < 2^52
     }
     slice(M, t.MH[N], t.ML[N], t.MR[N], t.MLo[N]);
+    t.MX3[N] = (double)M.bits(s3, s2 - s3);
+    t.MX4[N] = (double)M.bits(0, s3);
+    t.CB2[N] = b2; t.CB3[N] = b3; t.CB4[N] = b4;
+    t.p2s3[N] = ldexp(1.0, s3);
     double ch = 0.0;
     long double cl = 0.0L;
     for (int l = 0; l < N; ++l) { ch += 256.0 * t.H[N][l]; cl += 256.0L * (long double)t.Lo[N][l]; }
@@ -407,7 +416,235 @@ cudaError_t launch_gemm_crt(const GemmArgs &g, cudaStream_t s) {
     if (e != cudaSuccess) return e;
   }
   if (timed) { cudaError_t e = cudaEventRecord(tm->ev[2 * tm->used + 1], s); if (e != cudaSuccess) return e; ++tm->used; }
-  return launch_crt_finish(q, s);                // reconstruction + the hot path's epilogue
+  return g.crt_dd ? launch_crt_finish_dd(q, s)  // the certificate's exact reconstruction (R-35)
+                  : launch_crt_finish(q, s);     // reconstruction + the hot path's epilogue
+}
+
+}  // namespace ipr
+
+namespace ipr {
+
+// =========================================================================================
+// The CRT certificate (reading R-35): ||I - Ct^2 A||_F of the certified matrix Ct (the candidate C
+// rounded to the coarser of its row's and its column's b-bit grids) from EXACT integer products,
+// with every remaining error bounded a posteriori (engine.cu certify_crt):
+//   k_cert_rowexp       e_r of the candidate's rows (the split's exponent rule), the row scale 2^-e_r
+//   k_cert_round_split  Ct_rk = 2^-g rint(2^g c_rk), g = min(e_r, e_k), in place, and the residues of
+//                       2^e_r Ct_rk (an integer: the quantisation of Ct is exact in rows AND columns)
+//   k_cert_split        the residues of an operand given as a double-double (hi, lo) -- or a plain
+//                       FP64 matrix -- with its quantisation error sum_k d_rk^2 and sum_k |x_rk| per row
+// Residues of y + 2^63 (|y| <= 2^62 + 2^10 here: the double-double rows may exceed 2^b by a few ulps).
+// =========================================================================================
+template <int M, bool UNS>
+__device__ __forceinline__ uint32_t cert_res8(uint32_t lo, uint32_t hi) {
+  constexpr uint32_t h = UNS ? 0u : M == 256 ? 128 : (M - 1) / 2;
+  constexpr uint32_t w0 = 1u % M, w1 = (1u << 8) % M, w2 = (1u << 16) % M, w3 = (1u << 24) % M;
+  constexpr uint32_t w4 = (uint32_t)((1ull << 32) % M), w5 = (uint32_t)((1ull << 40) % M);
+  constexpr uint32_t w6 = (uint32_t)((1ull << 48) % M), w7 = (uint32_t)((1ull << 56) % M);
+  constexpr uint32_t KL = w0 | (w1 << 8) | (w2 << 16) | (w3 << 24), KH = w4 | (w5 << 8) | (w6 << 16) | (w7 << 24);
+  constexpr uint32_t K3 = (uint32_t)((h + M - (uint32_t)((1ull << 63) % M)) % M);
+  constexpr uint32_t MAG = (uint32_t)(((1ull << 32) + M - 1) / M);
+  if (UNS && M == 256) return lo;                 // y mod 256: the low byte (2^63 = 0 mod 256)
+  const uint32_t r = __dp4a(hi, KH, __dp4a(lo, KL, K3));
+  const uint32_t u = r - __umulhi(r, MAG) * (uint32_t)M;
+  return UNS ? u : u - h;
+}
+template <int L, bool UNS>
+__device__ __forceinline__ void cert_split4(const uint32_t (&lo)[4], const uint32_t (&hi)[4], int nm, int8_t *dst,
+                                            int64_t plane) {
+  if constexpr (L < CRT_MAX) {
+    if (L < nm) {
+      uint32_t b[4];
+      #pragma unroll
+      for (int u = 0; u < 4; ++u) b[u] = cert_res8<kModuli[L], UNS>(lo[u], hi[u]);
+      *(uint32_t *)(dst + (int64_t)L * plane) =
+          __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+      cert_split4<L + 1, UNS>(lo, hi, nm, dst, plane);
+    }
+  }
+}
+// 2^e x exactly for |e| <= 2000 (two power-of-two factors)
+__device__ __forceinline__ double scale2(double x, int e) { return __dmul_rn(__dmul_rn(x, pow2(e / 2)), pow2(e - e / 2)); }
+__device__ __forceinline__ double row_absmax(const double *x, int64_t cols, double *red) {
+  double mx = 0.0;
+  for (int64_t k = threadIdx.x; k < cols; k += blockDim.x) mx = fmax(mx, fabs(x[k]));
+  #pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) mx = fmax(mx, red[w]);
+    red[0] = fmax(mx, red[0]);
+  }
+  __syncthreads();
+  return red[0];
+}
+// exponent rule of the split (k_crt_split): scaled row maximum in [2^(b-1), 2^b); 0 for a zero row.
+// Rows outside |e| <= 400 (maxima beyond 2^+-340) are flagged: the certificate then falls back.
+__device__ __forceinline__ int cert_exp(double mx, int b, bool *ok) {
+  if (!(mx > 0.0)) { *ok = mx == 0.0; return 0; }
+  const int e = b - 1 - ilogb(mx);
+  *ok = e >= -400 && e <= 400;
+  return e;
+}
+
+__global__ void __launch_bounds__(256) k_cert_rowexp(const double *__restrict__ X, int64_t ld, int64_t cols, int b,
+                                                     int *sig, double *scale) {
+  __shared__ double red[8];
+  const int64_t r = blockIdx.x;
+  const double mx = row_absmax(X + r * ld, cols, red);
+  bool ok;
+  const int e = cert_exp(mx, b, &ok);
+  if (threadIdx.x == 0) { sig[r] = e; scale[r] = !ok ? NAN : mx > 0.0 ? scale2(1.0, -e) : 0.0; }
+}
+
+template <bool UNS>
+__global__ void __launch_bounds__(256, 3) k_cert_round_split(double *__restrict__ X, int64_t ld, int64_t rows,
+                                                             int64_t cols, int nm, const int *__restrict__ sig,
+                                                             int8_t *planes) {
+  const int64_t r = blockIdx.x;
+  double *x = X + r * ld;
+  const int er = sig[r];
+  const int64_t plane = rows * cols;
+  for (int64_t k0 = (int64_t)threadIdx.x * 4; k0 < cols; k0 += (int64_t)blockDim.x * 4) {
+    uint32_t lo[4], hi[4];
+    double v[4];
+    const double2 a = *(const double2 *)(x + k0), c = *(const double2 *)(x + k0 + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = c.x; v[3] = c.y;
+    const int4 ek = *(const int4 *)(sig + k0);
+    const int es[4] = {ek.x, ek.y, ek.z, ek.w};
+    #pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int g = min(er, es[u]);
+      v[u] = scale2(rint(scale2(v[u], g)), -g);                    // Ct_rk on the grid 2^-g (exact)
+      const uint64_t y = (uint64_t)__double2ll_rn(scale2(v[u], er)) + (1ull << 63);   // 2^e_r Ct_rk: an integer
+      lo[u] = (uint32_t)y; hi[u] = (uint32_t)(y >> 32);
+    }
+    *(double2 *)(x + k0) = make_double2(v[0], v[1]);
+    *(double2 *)(x + k0 + 2) = make_double2(v[2], v[3]);
+    cert_split4<0, UNS>(lo, hi, nm, planes + r * cols + k0, plane);
+  }
+}
+
+template <bool UNS, bool LO>
+__global__ void __launch_bounds__(256, 3) k_cert_split(const double *__restrict__ Xh, const double *__restrict__ Xl,
+                                                       int64_t ld, int64_t rows, int64_t cols, int b, int nm,
+                                                       int8_t *planes, int *sig, double *scale, double *err2,
+                                                       double *asum) {
+  __shared__ double red[8];
+  const int64_t r = blockIdx.x;
+  const double *xh = Xh + r * ld;
+  const double *xl = LO ? Xl + r * ld : nullptr;
+  const double mx = row_absmax(xh, cols, red);
+  bool ok;
+  const int e = cert_exp(mx, b, &ok);
+  const int64_t plane = rows * cols;
+  double es = 0.0, as = 0.0;
+  for (int64_t k0 = (int64_t)threadIdx.x * 4; k0 < cols; k0 += (int64_t)blockDim.x * 4) {
+    uint32_t lo[4], hi[4];
+    double vh[4], vl[4] = {0.0, 0.0, 0.0, 0.0};
+    {
+      const double2 a = *(const double2 *)(xh + k0), c = *(const double2 *)(xh + k0 + 2);
+      vh[0] = a.x; vh[1] = a.y; vh[2] = c.x; vh[3] = c.y;
+    }
+    if (LO) {
+      const double2 a = *(const double2 *)(xl + k0), c = *(const double2 *)(xl + k0 + 2);
+      vl[0] = a.x; vl[1] = a.y; vl[2] = c.x; vl[3] = c.y;
+    }
+    #pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      as += fabs(vh[u]) + fabs(vl[u]);
+      const double hs = scale2(vh[u], e), ls = scale2(vl[u], e);
+      long long y;
+      double d;
+      if (fabs(hs) >= 4503599627370496.0) {                      // hs an integer: y = hs + rint(ls)
+        const double fl = rint(ls);
+        y = __double2ll_rn(hs) + __double2ll_rn(fl);
+        d = __dsub_rn(ls, fl);
+      } else {                                                     // |ls| <= ulp(hs) / 2 <= 1/4
+        const double fh = rint(hs);
+        y = __double2ll_rn(fh);
+        d = __dadd_rn(__dsub_rn(hs, fh), ls);                      // hs - fh exact
+      }
+      es = __fma_rn(d, d, es);
+      const uint64_t yy = (uint64_t)y + (1ull << 63);
+      lo[u] = (uint32_t)yy; hi[u] = (uint32_t)(yy >> 32);
+    }
+    cert_split4<0, UNS>(lo, hi, nm, planes + r * cols + k0, plane);
+  }
+  es = block_sum_det<256>(es, red);
+  __syncthreads();
+  as = block_sum_det<256>(as, red);
+  if (threadIdx.x == 0) {
+    sig[r] = e;
+    scale[r] = !ok ? NAN : mx > 0.0 ? scale2(1.0, -e) : 0.0;
+    err2[r] = !ok ? NAN : scale2(es, -2 * e);                    // sum_k (2^-e d_rk)^2
+    asum[r] = as;
+  }
+}
+
+cudaError_t launch_cert_rowexp(const double *X, int64_t ld, int64_t rows, int64_t cols, int b, int *sig, double *scale,
+                               cudaStream_t s) {
+  k_cert_rowexp<<<(unsigned)rows, 256, 0, s>>>(X, ld, cols, b, sig, scale);
+  ++g_launches;
+  return cudaGetLastError();
+}
+cudaError_t launch_cert_round_split(double *X, int64_t ld, int64_t rows, int64_t cols, int nm, const int *sig,
+                                    int8_t *planes, cudaStream_t s) {
+  if (nm < 2 || nm > CRT_MAX || cols % 4 || ld % 2) return cudaErrorInvalidValue;
+  if (crt_unsigned(cols)) k_cert_round_split<true><<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, nm, sig, planes);
+  else k_cert_round_split<false><<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, nm, sig, planes);
+  ++g_launches;
+  return cudaGetLastError();
+}
+cudaError_t launch_cert_split(const double *Xh, const double *Xl, int64_t ld, int64_t rows, int64_t cols, int b, int nm,
+                              int8_t *planes, int *sig, double *scale, double *err2, double *asum, cudaStream_t s) {
+  if (b < 2 || b > CRT_BMAX || nm < 2 || nm > CRT_MAX || cols % 4 || ld % 2) return cudaErrorInvalidValue;
+  const bool uns = crt_unsigned(cols);
+#define CERT_SPLIT(U, L) k_cert_split<U, L><<<(unsigned)rows, 256, 0, s>>>(Xh, Xl, ld, rows, cols, b, nm, planes, sig, scale, err2, asum)
+  if (uns) { if (Xl) CERT_SPLIT(true, true); else CERT_SPLIT(true, false); }
+  else { if (Xl) CERT_SPLIT(false, true); else CERT_SPLIT(false, false); }
+#undef CERT_SPLIT
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+// Deterministic reductions of the per-row certificate quantities: out[q] = sum (op 0) or max (op 1) of
+// v[q][0 .. len) (NaN propagates through both), one block, fixed order.
+struct CertStatArgs { const double *v[8]; int op[8]; };
+__global__ void __launch_bounds__(256) k_cert_stats(const CertStatArgs a, int nv, int64_t len, double *out) {
+  __shared__ double red[8];
+  for (int q = 0; q < nv; ++q) {
+    const double *x = a.v[q];
+    const bool mx = a.op[q] != 0;
+    double t = 0.0;
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+      const double y = x[i];
+      t = mx ? ((y > t || y != y) ? y : t) : t + y;
+    }
+    if (!mx) {
+      t = block_sum_det<256>(t, red);
+    } else {
+      #pragma unroll
+      for (int o = 16; o > 0; o >>= 1) { const double y = __shfl_xor_sync(0xffffffffu, t, o); t = (y > t || y != y) ? y : t; }
+      __syncthreads();
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+      __syncthreads();
+      if (threadIdx.x == 0) for (int w = 0; w < 8; ++w) t = (red[w] > t || red[w] != red[w]) ? red[w] : t;
+    }
+    if (threadIdx.x == 0) out[q] = t;
+    __syncthreads();
+  }
+}
+cudaError_t launch_cert_stats(const double *const *v, const int *op, int nv, int64_t len, double *out, cudaStream_t s) {
+  if (nv < 1 || nv > 8) return cudaErrorInvalidValue;
+  CertStatArgs a;
+  memset(&a, 0, sizeof a);
+  for (int q = 0; q < nv; ++q) { a.v[q] = v[q]; a.op[q] = op[q]; }
+  k_cert_stats<<<1, 256, 0, s>>>(a, nv, len, out);
+  ++g_launches;
+  return cudaGetLastError();
 }
 
 }  // namespace ipr

@@ -1,6 +1,6 @@
 """One solve of a BASELINE workload through the C-ABI (harness tool for ncu captures).
 
-  python tools/one_solve.py [--workload H_twin] [--schedule symtri:bf16>fp64/cbf16]"""
+  python tools/one_solve.py [--workload H_twin] [--schedule symtri:bf16>fp64/cbf16] [--cert crt|fp64]"""
 import argparse
 import os
 import sys
@@ -13,6 +13,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="H_twin")
     ap.add_argument("--schedule", default=None)
+    ap.add_argument("--cert", default="crt")
     a = ap.parse_args()
     import torch
     import bench
@@ -22,7 +23,7 @@ def main():
     n, p = cfg["n"], cfg["p"]
     A, _ = synth.spd_torch(n, cfg["kappa"], cfg["seed"], device="cuda")
     form, ph = bench.schedule(a.schedule or bench.DEFAULT_SCHEDULE, n)
-    s = ipr.Solver(A, p, ph, 1e-12, torch.cuda.current_stream(), form=form)
+    s = ipr.Solver(A, p, ph, 1e-12, torch.cuda.current_stream(), form=form, cert=a.cert)
     s.iterate(400)
     tr = s.trace()
     out = s.finalize()
