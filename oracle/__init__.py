@@ -93,6 +93,7 @@ def lib():
         L.orc_cert_grid.argtypes = [C.c_int64, C.c_int, _dp, _dp]
         L.orc_resid_dd.restype = C.c_double
         L.orc_resid_dd.argtypes = [C.c_int64, C.c_int, _dp, _dp]
+        L.orc_resid_rows_dd.argtypes = [C.c_int64, C.c_int, _dp, _dp, C.c_int64, C.POINTER(C.c_int64), _dp]
         L.orc_inv_proot_eig.argtypes = [C.c_int64, _dp, _dp, C.c_int, _dp]
         L.orc_spectral.argtypes = [C.c_int64, _dp, C.c_int, C.c_double, C.c_int, _dp]
         L.orc_fp16_sigma.argtypes = [C.c_double]
@@ -338,6 +339,15 @@ def resid_dd(A, X, p: int) -> float:
     """||I - X^p A||_F in double-double arithmetic (the residual of the FP64 matrices X, A to ~1e-30)."""
     A, X = _f64(A), _f64(X)
     return lib().orc_resid_dd(A.shape[0], p, _p(A), _p(X))
+
+
+def resid_rows_dd(A, X, p: int, rows) -> np.ndarray:
+    """Squared 2-norms of the given rows of I - X^p A, in double-double arithmetic (sampled rows)."""
+    A, X = _f64(A), _f64(X)
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.empty(len(r))
+    lib().orc_resid_rows_dd(A.shape[0], p, _p(A), _p(X), len(r), r.ctypes.data_as(C.POINTER(C.c_int64)), _p(out))
+    return out
 
 
 def jacobi(A):

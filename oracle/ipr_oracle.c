@@ -1069,3 +1069,35 @@ double orc_resid_dd(int64_t n, int p, const double *A, const double *X) {
   free(T); free(U);
   return sqrt(ss.hi + ss.lo);
 }
+
+void orc_resid_rows_dd(int64_t n, int p, const double *A, const double *X, int64_t nrows, const int64_t *rows,
+                       double *out) {
+  orc_dd *v = (orc_dd *)malloc((size_t)n * sizeof(orc_dd));
+  orc_dd *u = (orc_dd *)malloc((size_t)n * sizeof(orc_dd));
+  for (int64_t q = 0; q < nrows; ++q) {
+    const int64_t i = rows[q];
+    for (int64_t c = 0; c < n; ++c) { v[c].hi = X[i * n + c]; v[c].lo = 0.0; }   /* x_i^T */
+    for (int j = 1; j <= p; ++j) {     /* v <- v X (p - 1 times), then v <- v A */
+      const double *M = j < p ? X : A;
+      #pragma omp parallel for schedule(static)
+      for (int64_t c = 0; c < n; ++c) {
+        orc_dd acc = {0.0, 0.0};
+        for (int64_t k = 0; k < n; ++k) acc = dd_add(acc, dd_mul_d(v[k], M[k * n + c]));
+        u[c] = acc;
+      }
+      orc_dd *w = v; v = u; u = w;
+    }
+    orc_dd ss = {0.0, 0.0};
+    for (int64_t c = 0; c < n; ++c) {
+      orc_dd r = {c == i ? 1.0 : 0.0, 0.0};
+      orc_dd t = v[c];
+      t.hi = -t.hi; t.lo = -t.lo;
+      r = dd_add(r, t);
+      const double e = r.hi + r.lo;
+      orc_dd sq = {e * e, fma(e, e, -(e * e))};
+      ss = dd_add(ss, sq);
+    }
+    out[q] = ss.hi + ss.lo;
+  }
+  free(v); free(u);
+}

@@ -203,6 +203,11 @@ double orc_q_int8(double x);
 void orc_cert_grid(int64_t n, int b, const double *C, double *Ct);
 double orc_resid_dd(int64_t n, int p, const double *A, const double *X);
 void orc_set_cert_mode(int mode);
+/* Rows of the same residual: out[q] = sum_j (I - X^p A)[rows[q]][j]^2 in double-double arithmetic
+ * (row i of X^p A = ((x_i^T X) ... X) A, every vector-matrix product accumulated in double-double) --
+ * sampled rows of full-size residuals. */
+void orc_resid_rows_dd(int64_t n, int p, const double *A, const double *X, int64_t nrows, const int64_t *rows,
+                       double *out);
 
 #ifdef __cplusplus
 }

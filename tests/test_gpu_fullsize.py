@@ -188,3 +188,32 @@ def test_default_schedule_certifies_in_fp64(n, kappa, seed):
     assert certs[-1] <= 1e-12 and all(c > 1e-12 for c in certs[:-1])
     assert s.residual(True) == certs[-1]
     s.close()
+
+
+def test_headline_crt_certificate_full_size(twin):
+    # bench.py's default schedule certified by IPR_CERT_CRT (R-35) at n = 8192: a proven bound on the exact
+    # residual of the returned matrix.  At this size the oracle checks it on sampled rows: the exact
+    # (double-double) residual rows of the returned C never exceed the bound, and -- the residual of this
+    # random twin being spread over all rows -- they extrapolate to the bound's evaluated part within 2x;
+    # the answer is its own 62-bit grid rounding; the FP64 DMMA evaluation of the same C lies within its
+    # rounding noise (~5e-13 here) of it; the bound's error terms are small beside the residual.
+    import math
+    import bench
+    A, A_np = twin
+    n = A.shape[0]
+    form, ph = bench.schedule(bench.DEFAULT_SCHEDULE, n)
+    s = ipr.Solver(A, 2, ph, 1e-12, form=form, cert="crt")
+    assert s.iterate(200) == ipr.IPR_CONVERGED
+    tr = s.trace()
+    info = ipr.ipr_test_cert_info(s.ctx)
+    assert tr[-1]["rho_cert"] == info["bound"] <= 1e-12
+    assert info["beta"] <= 0.2 * info["est"] and info["moduli"] == 18
+    assert s.residual(1) == info["bound"]
+    dmma = s.residual(2)
+    C = s.finalize().cpu().numpy()
+    np.testing.assert_array_equal(C, oracle.cert_grid(C, 62))
+    rows = [0, 1, 2047, 4097, 8191]
+    r2 = oracle.resid_rows_dd(A_np, C, 2, rows)
+    assert math.sqrt(r2.sum()) <= info["bound"]
+    assert 0.5 * info["est"] <= math.sqrt(r2.sum() * n / len(rows)) <= 2.0 * info["est"]
+    assert abs(dmma - info["est"]) <= 1e-12

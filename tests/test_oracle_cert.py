@@ -137,3 +137,19 @@ def test_solve_with_crt_certificate_mirrors_the_fp64_certificate_trajectory(form
     cb = b.records[-1]["rho_cert"]
     assert cb == oracle.resid_dd(A, b.C_best, 2) <= 1e-12
     assert abs(cb - a.records[-1]["rho_cert"]) < 64 * 2.0 ** -53 * n
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_resid_rows_dd_exact_rows(p):
+    # every row against exact rational arithmetic; their sum is the squared full residual
+    A, X = _near_root(5, p, 30 + p)
+    n = 5
+    Af = [[Fraction(float(v)) for v in r] for r in A]
+    Xf = [[Fraction(float(v)) for v in r] for r in X]
+    T = Af
+    for _ in range(p):
+        T = [[sum(Xf[i][k] * T[k][j] for k in range(n)) for j in range(n)] for i in range(n)]
+    want = [float(sum(((1 if i == j else 0) - T[i][j]) ** 2 for j in range(n))) for i in range(n)]
+    got = oracle.resid_rows_dd(A, X, p, range(n))
+    np.testing.assert_allclose(got, want, rtol=1e-12)
+    assert math.sqrt(got.sum()) == pytest.approx(oracle.resid_dd(A, X, p), rel=1e-13)
