@@ -84,3 +84,14 @@ def test_guards_intact_sharded(sched, grid):
     ipr.ipr_test_local_group_destroy(grp)
     assert all(e is None for e in err), err
     assert bad == [-1] * world
+
+
+@pytest.mark.parametrize("n", [300, 520, 1000])
+@pytest.mark.parametrize("sched", ["symtri:fp8/cfp8>bf16>fp64crt@a/cbf16", "sym:bf16>fp64crt@a/cbf16"])
+def test_guards_intact_crt_certificate(n, sched):
+    # IPR_CERT_CRT (R-35): the grid-rounding split, the double-double finish with its mirrored hi / lo
+    # stores, the double-double split and the certificate's statistics stay inside their buffers
+    A = torch.from_numpy(synth.spd(n, 2.0, 60 + n)).cuda()
+    bad, out = _solve_checked(A, 2, sched, cert="crt")
+    assert bad == -1, (sched, n, bad)
+    assert out == ipr.IPR_CONVERGED

@@ -1,5 +1,5 @@
 """C5's kappa = 2 twin (n = 32768) one iteration at a time, printing each record as it lands (diagnose a
-slow or stuck large solve).  python tools/c5_progress.py [schedule] [n]"""
+slow or stuck large solve).  python tools/c5_progress.py [schedule] [n] [tol] [cap] [cert]"""
 import json
 import os
 import sys
@@ -16,6 +16,7 @@ sched = sys.argv[1] if len(sys.argv) > 1 else "symtri:bf16>fp64crt@a/cbf16"
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 32768
 tol = float(sys.argv[3]) if len(sys.argv) > 3 else 1e-12
 cap = int(sys.argv[4]) if len(sys.argv) > 4 else 40
+cert = sys.argv[5] if len(sys.argv) > 5 else "crt"
 t0 = time.perf_counter()
 A, _ = synth.spd_torch(n, 2.0, synth.CONFIGS["C5"]["seed"], device="cuda")
 torch.cuda.synchronize()
@@ -23,7 +24,7 @@ print(f"A ready {time.perf_counter() - t0:.1f} s, free {torch.cuda.mem_get_info(
 torch.cuda.empty_cache()
 form, ph = bench.schedule(sched, n)
 ph[-1].max_iters = cap
-s = ipr.Solver(A, 2, ph, tol, form=form)
+s = ipr.Solver(A, 2, ph, tol, form=form, cert=cert)
 for k in range(200):
     t1 = time.perf_counter()
     out = s.iterate(1)
@@ -34,5 +35,8 @@ for k in range(200):
     if out != ipr.IPR_RUNNING:
         break
 print("outcome", ipr.OUTCOME_NAMES[s.outcome], f"total {time.perf_counter() - t0:.1f} s", flush=True)
-print("dmma recheck of the best iterate", s.residual(True), flush=True)
+if cert == "crt":
+    print("certificate terms", json.dumps(ipr.ipr_test_cert_info(s.ctx)), flush=True)
+print("certificate recheck of the best iterate", s.residual(1), flush=True)
+print("dmma evaluation of the best iterate", s.residual(2), flush=True)
 s.close()
