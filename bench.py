@@ -57,7 +57,7 @@ def parse():
                          "sym:bf16>fp64/cbf16 (sym: = IPR_FORM_SYMMETRIC, NEXT-2)")
     ap.add_argument("--cert", choices=["auto", "crt", "fp64"], default="auto",
                     help="convergence certificate: crt = IPR_CERT_CRT (a proven bound on the exact residual, "
-                         "R-35; one GPU, symmetric p = 2 with an fp64crt phase), fp64 = IPR_CERT_FP64 (DMMA "
+                         "R-35; symmetric p = 2 with an fp64crt phase, any 1 x G), fp64 = IPR_CERT_FP64 (DMMA "
                          "evaluation, R-30); auto = crt where it applies")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -290,7 +290,7 @@ def main():
     form, phases = schedule(args.schedule, n)
     cert = args.cert
     if cert == "auto":
-        crt_ok = world == 1 and form.startswith("symmetric") and p == 2 and \
+        crt_ok = form.startswith("symmetric") and p == 2 and \
             any(ipr.PREC_NAMES[q.prec] == "fp64crt" for q in phases)
         cert = "crt" if crt_ok else "fp64"
     config["certificate"] = cert

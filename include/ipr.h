@@ -243,7 +243,7 @@ ipr_status ipr_set_form(ipr_ctx *c, int form);
  *    linear rate predicts it, rho_k (rho_k / rho_{k-1}) <= final_tol / 2: then C_{k+1} is certified
  *    BEFORE its chain, which runs only if the certificate misses (the converged record then has
  *    rho = NaN).  IPR_CERT_FP64_CHAIN: the same certificate, triggered by the in-chain rho only.
- *  IPR_CERT_CRT (reading R-35; symmetric forms, p = 2, one GPU, an IPR_FP64_CRT phase, FP64 last phase):
+ *  IPR_CERT_CRT (reading R-35; symmetric forms, p = 2, 1 x G grids, an IPR_FP64_CRT phase, FP64 last phase):
  *    a PROVEN upper bound on ||I - Ct^2 A||_F, where Ct is the candidate C_k rounded to the coarser of its
  *    row's and its column's 62-bit grids (|Ct - C_k| <= 2^-62 of the row / column maximum; the rounding
  *    makes Ct's integer quantisation exact), from exact integer products on the INT8 tensor cores
@@ -253,7 +253,10 @@ ipr_status ipr_set_form(ipr_ctx *c, int form);
  *    Triggered like IPR_CERT_FP64 (R-33).  An FP64 DMMA evaluation carries ~n u |C|^2 |A| of rounding
  *    noise (4-6e-13 at n = 8192); this bound is a statement about the exact residual.  Candidates whose
  *    exponents leave (-400, 400) or that are not bitwise symmetric fall back to IPR_CERT_FP64's DMMA
- *    evaluation of Ct.  Unsupported configurations fail at the first ipr_iterate (IPR_E_UNSUPPORTED).
+ *    evaluation of Ct.  G > 1: every rank rounds and splits the gathered candidate, computes its column
+ *    panel of Y (stored K-major: the rows S_g of the symmetric Y) and of Y A, and all-gathers Y's residue
+ *    planes and row statistics -- the bound is bit-identical to G = 1.  Unsupported configurations fail at
+ *    the first ipr_iterate (IPR_E_UNSUPPORTED).
  * Errors: IPR_E_INVALID_ARG (unknown mode), IPR_E_STATE (after the first ipr_iterate). */
 typedef enum { IPR_CERT_FP64 = 0, IPR_CERT_PHASE = 1, IPR_CERT_FP64_CHAIN = 2, IPR_CERT_CRT = 3 } ipr_cert;
 ipr_status ipr_set_cert(ipr_ctx *c, int mode);

@@ -1093,7 +1093,7 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       {(void **)&c->full64, cr ? 0 : full * 8}, {&c->Acert, cr ? 0 : panel * 8},
       {&c->chat_rm, (cr && c->world > 1) ? full * 8 : 0},
       {&c->Tcol, c->grows > 1 ? panel * 8 : 0},
-      {(void **)&c->certv, (cr && is_sym(c) && c->world == 1) ? (size_t)c->npad * 8 * 8 : 0},
+      {(void **)&c->certv, (cr && is_sym(c)) ? (size_t)c->npad * 8 * 8 : 0},
       {(void **)&c->partg, c->grows > 1 ? (size_t)c->world * c->npart * 8 : 0},
       {&c->msend, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0},
       {&c->mrecv, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0}};
@@ -1412,10 +1412,10 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       bool crt = false;
       for (auto &P : c->ph) crt |= P.prec == IPR_FP64_CRT;
       const int nm = crt_moduli(kCertBits, c->n);
-      if (!is_sym(c) || c->p != 2 || c->world != 1 || c->grows != 1 || !crt || !c->ph.back().cont64 || nm < 16)
+      if (!is_sym(c) || c->p != 2 || c->grows != 1 || !crt || !c->ph.back().cont64 || nm < 16)
         return fail(c, IPR_E_UNSUPPORTED,
-                    "ipr_iterate: IPR_CERT_CRT needs a symmetric form with p = 2 on one GPU, an IPR_FP64_CRT phase and "
-                    "an FP64 last phase, and n <= 65535");
+                    "ipr_iterate: IPR_CERT_CRT needs a symmetric form with p = 2 on a 1 x G grid, an IPR_FP64_CRT "
+                    "phase and an FP64 last phase, and n <= 65535");
     }
     if (c->grows > 1) {   // the 2-D grid option: Eq. (1) as printed, unscaled tensor-core / DMMA formats
       if (c->form != IPR_FORM_LITERAL)
@@ -1776,18 +1776,22 @@ static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
   Nvtx nv("certify crt");
   cudaStream_t st = c->st;
   const int b = kCertBits, nm = crt_moduli(b, c->n);
-  const int64_t np = c->npad;
-  double *Ct = c->full64;
+  const int64_t np = c->npad, kp = c->kp, col0 = c->col0;
+  const bool sh = c->world > 1;                    // 1 x G column panels: rank g owns the columns S_g
   double *err2Y = c->certv, *asumY = c->certv + np, *scY = c->certv + 2 * np, *err2A = c->certv + 3 * np;
   double *asumA = c->certv + 4 * np, *scA = c->certv + 5 * np, *scC = c->certv + 6 * np;
   if (!c->hcert && !(c->hcert = pinned_acquire())) return fail(c, IPR_E_OOM, "pinned host slab exhausted");
+  // G > 1: the gathered C (panel-major in full64) row-major in chat_rm; every rank rounds and splits all
+  // of it (the A role of Y = Ct Ct needs every row), the B role takes the rows S_g of the same residues
+  double *Ct = sh ? (double *)c->chat_rm : c->full64;
+  if (sh) CK(launch_copy_out(c->full64, np, kp, c->n, Ct, np, st));
   // 1. the certified matrix and its residues
   CK(launch_cert_rowexp(Ct, np, np, np, b, c->crC_sig, scC, st));
   CK(launch_cert_round_split(Ct, np, np, np, nm, c->crC_sig, c->crC, st));
   c->crC_for = -1;
   CK(cudaMemsetAsync(c->dflag + 2, 0, 4, st));
   CK(launch_symcheck(Ct, np, c->n, c->dflag + 2, st));
-  if (i >= 0 && c->out_ptr) {                      // ipr_set_output: stream Ct while the products run
+  if (i >= 0 && c->out_ptr && !sh) {               // ipr_set_output: stream Ct while the products run
     if (!c->ost) {
       CK(cudaStreamCreateWithFlags(&c->ost, cudaStreamNonBlocking));
       CK(cudaEventCreateWithFlags(&c->oev, cudaEventDisableTiming));
@@ -1801,27 +1805,52 @@ static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
     CK(cudaEventRecord(c->oev, c->ost));
     c->out_buf = i;
   }
-  // 2. A (FP64, m = 52) and its residues
+  const int8_t *ctB = c->crC;                      // B role of Ct: its rows S_g (G > 1: compact copy in crB)
+  double *ylo = (double *)c->Zr;
+  if (sh) {
+    CK(cudaMemcpy2DAsync(c->crB, (size_t)(kp * np), c->crC + col0 * np, (size_t)(np * np), (size_t)(kp * np), (size_t)nm,
+                         cudaMemcpyDeviceToDevice, st));
+    ctB = c->crB;
+    ylo = (double *)(c->crB + ((size_t)nm * kp * np + 255) / 256 * 256);   // 18/G + 8/G <= 18 bytes per n^2
+  }
+  // 2. A (FP64, m = 52; its local K-major panel = the rows S_g) and its residues
   PhaseC P64{IPR_FP64, 52, 0, 1, 0, 0, 0, 0};
   CKS(stage_a(c, P64, c->T[1], c->dsig + 0));
-  CK(launch_cert_split((const double *)c->T[1], nullptr, np, np, np, b, nm, c->crA, c->crA_sig, scA, err2A, asumA, st));
+  CK(launch_cert_split((const double *)c->T[1], nullptr, np, kp, np, b, nm, c->crA, 0, c->crA_sig, scA + col0,
+                       err2A + col0, asumA + col0, st));
   c->crA_b = -1;
-  // 3. Y = Ct Ct, upper tiles, exact, hi + lo
+  // 3. Y = Ct Ct exact, hi + lo: G = 1 its upper tiles mirrored (row-major); G > 1 the column panel
+  //    Y[:, S_g] stored K-major, i.e. the rows S_g of the symmetric Y
   GemmArgs g = base_args(c, IPR_FP64_CRT, nullptr);
-  g.oz_a = c->crC; g.oz_rsig = c->crC_sig; g.oz_b = c->crC; g.oz_csig = c->crC_sig;
-  g.crt_n = nm; g.crt_v = c->crV; g.crt_dd = 1; g.tri = 1;
-  g.mode = EPI_STORE_N; g.nout = c->T[1]; g.ldn = np; g.zout = (double *)c->Zr; g.ldz = np;
+  g.oz_a = c->crC; g.oz_rsig = c->crC_sig; g.oz_b = ctB; g.oz_csig = c->crC_sig + col0;
+  g.crt_n = nm; g.crt_v = c->crV; g.crt_dd = 1;
+  g.nout = c->T[1]; g.ldn = np; g.zout = ylo; g.ldz = np;
+  if (sh) g.mode = EPI_STORE_T;
+  else { g.tri = 1; g.mode = EPI_STORE_N; }
   CK(launch_gemm_crt(g, st));
-  // 4. residues of Y from hi + lo
-  CK(launch_cert_split((const double *)c->T[1], (const double *)c->Zr, np, np, np, b, nm, c->crC, c->crC_sig, scY,
-                       err2Y, asumY, st));
+  // 4. residues of Y's rows (G > 1: the rows S_g into their global slots, then all-gathered)
+  CK(launch_cert_split((const double *)c->T[1], ylo, np, kp, np, b, nm, c->crC + col0 * np, np * np, c->crC_sig + col0,
+                       scY + col0, err2Y + col0, asumY + col0, st));
   c->zr_for = -1;
-  // 5. P = Ytilde Atilde: residual partials
+  if (sh) {
+    for (int l = 0; l < nm; ++l) {
+      int8_t *pl = c->crC + (size_t)l * np * np;
+      if (!c->comm->allgather(pl + col0 * np, pl, (size_t)(kp * np), st))
+        return fail(c, IPR_E_NCCL, "all-gather(Y residues) failed: %s", c->comm->last_error());
+    }
+    bool ok = c->comm->allgather(c->crC_sig + col0, c->crC_sig, (size_t)kp * 4, st);
+    for (double *v : {scY, err2Y, asumY, scA, err2A})
+      ok = ok && c->comm->allgather(v + col0, v, (size_t)kp * 8, st);
+    if (!ok) return fail(c, IPR_E_NCCL, "all-gather(certificate rows) failed: %s", c->comm->last_error());
+  }
+  // 5. P = Ytilde Atilde (the local columns): residual partials in their global slots
   GemmArgs h = base_args(c, IPR_FP64_CRT, nullptr);
   h.oz_a = c->crC; h.oz_rsig = c->crC_sig; h.oz_b = c->crA; h.oz_csig = c->crA_sig;
   h.crt_n = nm; h.crt_v = c->crV; h.crt_dd = 1; h.mode = EPI_RESID; h.part = c->part;
   CK(launch_gemm_crt(h, st));
-  CK(launch_reduce_sum(c->part, tiles_n_total(c, IPR_FP64_CRT) * tiles_m(c, IPR_FP64_CRT), c->dscal + 16, st));
+  const int64_t tm = tiles_m(c, IPR_FP64_CRT);
+  CKS(gather_partials(c, c->part, kp / gemm_tile_n(IPR_FP64_CRT) * tm));
+  CK(launch_reduce_sum(c->part, tiles_n_total(c, IPR_FP64_CRT) * tm, c->dscal + 16, st));
   const double *vv[6] = {err2Y, err2A, asumY, scY, scA, scC};
   const int ops[6] = {0, 0, 1, 1, 1, 1};
   CK(launch_cert_stats(vv, ops, 6, np, c->dscal + 17, st));
@@ -1843,13 +1872,20 @@ static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
   const double info[10] = {bound, est, beta, dY, dA, A2, Y2, eY, eP, (double)nm};
   memcpy(c->cert_info, info, sizeof info);
   if (std::isnan(bound)) {                         // outside what the bound covers: the FP64 DMMA certificate
+    if (sh) {                                      // full64 must hold Ct panel-major again (the gathered C)
+      CK(cudaMemcpy2DAsync(c->full64 + (size_t)c->rank * np * kp, (size_t)kp * 8, Ct + col0, (size_t)np * 8,
+                           (size_t)kp * 8, (size_t)np, cudaMemcpyDeviceToDevice, st));
+      CKS(gather_f64(c, c->full64 + (size_t)c->rank * np * kp));
+    }
     CKS(certify_full64(c, rho));
     c->cert_info[0] = *rho;
     return IPR_OK;
   }
   *rho = bound;
-  if (i >= 0 && bound <= c->final_tol)             // the certified Ct is the answer
-    CK(cudaMemcpyAsync(cont_ptr(c, i, c->ph[c->phase]), Ct, (size_t)np * np * 8, cudaMemcpyDeviceToDevice, st));
+  if (i >= 0 && bound <= c->final_tol) {           // the certified Ct is the answer (its local columns)
+    CK(cudaMemcpy2DAsync(cont_ptr(c, i, c->ph[c->phase]), (size_t)kp * 8, Ct + col0, (size_t)np * 8, (size_t)kp * 8,
+                         (size_t)np, cudaMemcpyDeviceToDevice, st));
+  }
   return IPR_OK;
 }
 

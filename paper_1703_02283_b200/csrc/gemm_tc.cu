@@ -1041,7 +1041,8 @@ cudaError_t launch_crt_finish(const GemmArgs &a_in, cudaStream_t s) {
 // Pbar = D_1 2^s1 + D_2 2^s2 + D_3 2^s3 + D_4 by an error-free two-sum cascade: hi + lo = Pbar within
 // 6 u^2 sum_k |D_k 2^sk| <= 2^(s1 - 48) (engine.cu certify_crt bounds it), scaled by 2^-(e_i + f_j)
 // exactly.  MODE 0: hi -> nout, lo -> zout (tri: the upper elements and their mirrors, K-major through
-// two shared-memory slabs as in k_crt_finish); MODE 1: per-tile partials of R_ij^2, R_ij = (delta_ij -
+// two shared-memory slabs as in k_crt_finish); MODE 2: the same, K-major only ([local col][row]: the
+// rows of a symmetric product's column panel, G > 1); MODE 1: per-tile partials of R_ij^2, R_ij = (delta_ij -
 // hi) - lo over i, j < n (tri weight 2 off the diagonal).  Exponents are in (-400, 400) (the
 // certificate's splits flag anything else), so every scaling is exact.
 __device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
@@ -1120,11 +1121,11 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish_dd(const GemmArgs g) {
           vh[u] = __dmul_rn(hi, sc);
           vl[u] = __dmul_rn(lo, sc);
         }
-        if (MODE == 0) {
+        if (MODE != 1) {
           #pragma unroll
           for (int u = 0; u < 4; ++u) {
             const int64_t gc = g.col0 + c0 + u;
-            if (!g.tri || row <= gc) {
+            if (MODE == 0 && (!g.tri || row <= gc)) {
               ((double *)g.nout)[row * g.ldn + c0 + u] = vh[u];
               g.zout[row * g.ldz + c0 + u] = vl[u];
             }
@@ -1142,15 +1143,15 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish_dd(const GemmArgs g) {
           }
         }
       }
-      if (MODE == 0) {
+      if (MODE != 1) {
         __syncthreads();
-        if (g.tri) {                                     // mirrors: (row, c) -> [c][row], 32 rows per warp
-          const int64_t row = r0 + slab * 32 + lane;
+        if (MODE == 2 || g.tri) {                        // (row, c) -> [c][row], 32 rows per warp: the tri
+          const int64_t row = r0 + slab * 32 + lane;     // mirrors (MODE 0), or the whole tile K-major (MODE 2)
           #pragma unroll 4
           for (int j = 0; j < 16; ++j) {
             const int cl = w * 16 + j;
             const int64_t c = colb + cl;
-            if (row < g.col0 + c) {
+            if (MODE == 2 || row < g.col0 + c) {
               ((double *)g.nout)[c * g.ldn + row] = slh[lane * CRT_FIN_LD + cl + (cl >> 2)];
               g.zout[c * g.ldz + row] = sll[lane * CRT_FIN_LD + cl + (cl >> 2)];
             }
@@ -1168,22 +1169,25 @@ __global__ void __launch_bounds__(256, 2) k_crt_finish_dd(const GemmArgs g) {
 
 cudaError_t launch_crt_finish_dd(const GemmArgs &a, cudaStream_t s) {
   const TileSched hs{(int)(a.M / (2 * TC_BM)), (int)(a.N / TC_BN), a.tri, (int)(a.col0 / TC_BN)};
-  const int mode = (a.mode & EPI_RESID) ? 1 : 0;
-  if (mode == 0 && (!a.nout || !a.zout)) return cudaErrorInvalidValue;
+  const int mode = (a.mode & EPI_RESID) ? 1 : (a.mode & EPI_STORE_T) ? 2 : 0;
+  if (mode != 1 && (!a.nout || !a.zout)) return cudaErrorInvalidValue;
   if (mode == 1 && a.tri) {   // the tiles below the diagonal are not visited: zero partials
     cudaError_t z = cudaMemsetAsync(a.part + (a.col0 / TC_BN) * a.tiles_m, 0, (size_t)(a.N / TC_BN) * a.tiles_m * sizeof(double), s);
     if (z != cudaSuccess) return z;
   }
-  const int smem = mode == 0 ? 2 * 32 * CRT_FIN_LD * 8 : 0;
+  const int smem = mode != 1 ? 2 * 32 * CRT_FIN_LD * 8 : 0;
 #define CRT_FIN_DD(N)                                                                                     \
   case N: {                                                                                               \
     static DeviceOnce attr;                                                                               \
     if (!attr.done()) {                                                                                   \
       cudaError_t e = cudaFuncSetAttribute(k_crt_finish_dd<N, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 32 * CRT_FIN_LD * 8); \
+      if (e == cudaSuccess)                                                                               \
+        e = cudaFuncSetAttribute(k_crt_finish_dd<N, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 32 * CRT_FIN_LD * 8); \
       if (e != cudaSuccess) return e;                                                                     \
       attr.set();                                                                                         \
     }                                                                                                     \
     if (mode == 0) k_crt_finish_dd<N, 0><<<2 * hs.count(), 256, smem, s>>>(a);                            \
+    else if (mode == 2) k_crt_finish_dd<N, 2><<<2 * hs.count(), 256, smem, s>>>(a);                       \
     else k_crt_finish_dd<N, 1><<<2 * hs.count(), 256, 0, s>>>(a);                                         \
   } break;
   switch (a.crt_n) {

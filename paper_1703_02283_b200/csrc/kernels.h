@@ -46,8 +46,10 @@ cudaError_t launch_cert_rowexp(const double *X, int64_t ld, int64_t rows, int64_
                                cudaStream_t s);
 cudaError_t launch_cert_round_split(double *X, int64_t ld, int64_t rows, int64_t cols, int nm, const int *sig,
                                     int8_t *planes, cudaStream_t s);
+// pstride: the residue plane stride (0: rows * cols); row r of X writes planes + l * pstride + r * cols
 cudaError_t launch_cert_split(const double *Xh, const double *Xl, int64_t ld, int64_t rows, int64_t cols, int b, int nm,
-                              int8_t *planes, int *sig, double *scale, double *err2, double *asum, cudaStream_t s);
+                              int8_t *planes, int64_t pstride, int *sig, double *scale, double *err2, double *asum,
+                              cudaStream_t s);
 cudaError_t launch_cert_stats(const double *const *v, const int *op, int nv, int64_t len, double *out, cudaStream_t s);
 cudaError_t launch_fill_operand(void *dst, int64_t count, int prec, uint32_t seed, cudaStream_t s);
 cudaError_t launch_test_quant(int mode, const void *in, void *out, int64_t len, int m, int rtz, int sigma,

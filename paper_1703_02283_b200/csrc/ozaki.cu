@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(256, 3) k_cert_round_split(double *__restrict_
 
 template <bool UNS, bool LO>
 __global__ void __launch_bounds__(256, 3) k_cert_split(const double *__restrict__ Xh, const double *__restrict__ Xl,
-                                                       int64_t ld, int64_t rows, int64_t cols, int b, int nm,
+                                                       int64_t ld, int64_t plane, int64_t cols, int b, int nm,
                                                        int8_t *planes, int *sig, double *scale, double *err2,
                                                        double *asum) {
   __shared__ double red[8];
@@ -539,7 +539,6 @@ __global__ void __launch_bounds__(256, 3) k_cert_split(const double *__restrict_
   const double mx = row_absmax(xh, cols, red);
   bool ok;
   const int e = cert_exp(mx, b, &ok);
-  const int64_t plane = rows * cols;
   double es = 0.0, as = 0.0;
   for (int64_t k0 = (int64_t)threadIdx.x * 4; k0 < cols; k0 += (int64_t)blockDim.x * 4) {
     uint32_t lo[4], hi[4];
@@ -599,10 +598,12 @@ cudaError_t launch_cert_round_split(double *X, int64_t ld, int64_t rows, int64_t
   return cudaGetLastError();
 }
 cudaError_t launch_cert_split(const double *Xh, const double *Xl, int64_t ld, int64_t rows, int64_t cols, int b, int nm,
-                              int8_t *planes, int *sig, double *scale, double *err2, double *asum, cudaStream_t s) {
+                              int8_t *planes, int64_t pstride, int *sig, double *scale, double *err2, double *asum,
+                              cudaStream_t s) {
   if (b < 2 || b > CRT_BMAX || nm < 2 || nm > CRT_MAX || cols % 4 || ld % 2) return cudaErrorInvalidValue;
   const bool uns = crt_unsigned(cols);
-#define CERT_SPLIT(U, L) k_cert_split<U, L><<<(unsigned)rows, 256, 0, s>>>(Xh, Xl, ld, rows, cols, b, nm, planes, sig, scale, err2, asum)
+  const int64_t plane = pstride ? pstride : rows * cols;
+#define CERT_SPLIT(U, L) k_cert_split<U, L><<<(unsigned)rows, 256, 0, s>>>(Xh, Xl, ld, plane, cols, b, nm, planes, sig, scale, err2, asum)
   if (uns) { if (Xl) CERT_SPLIT(true, true); else CERT_SPLIT(true, false); }
   else { if (Xl) CERT_SPLIT(false, true); else CERT_SPLIT(false, false); }
 #undef CERT_SPLIT

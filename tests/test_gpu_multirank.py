@@ -29,15 +29,15 @@ def _schedule(name):
     return bench.schedule(name, N)
 
 
-def _solve_world1(A, p, phases, form):
-    s = ipr.Solver(A, p, phases, 1e-12, form=form)
+def _solve_world1(A, p, phases, form, cert="fp64"):
+    s = ipr.Solver(A, p, phases, 1e-12, form=form, cert=cert)
     s.iterate(300)
     tr, out = s.trace(), s.outcome
     C = s.finalize().cpu().numpy()
     return out, tr, C
 
 
-def _solve_local(A, p, phases, form, world, grid=None):
+def _solve_local(A, p, phases, form, world, grid=None, cert="fp64"):
     grp = ipr.ipr_test_local_group_create(world)
     res = [None] * world
     err = [None] * world
@@ -47,7 +47,7 @@ def _solve_local(A, p, phases, form, world, grid=None):
             st = torch.cuda.Stream()
             with torch.cuda.stream(st):
                 s = ipr.Solver(A, p, phases, 1e-12, stream=st, world=world, rank=r, form=form, local_group=grp,
-                               grid=grid)
+                               grid=grid, cert=cert)
                 s.iterate(300)
                 tr, out = s.trace(), s.outcome
                 C = torch.empty_like(A)
@@ -110,6 +110,25 @@ def test_sharded_bit_identical_to_one_gpu(A, case, world):
         assert any(t["moduli"] > 0 for t in tr1)
 
 
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("case", [CASES[3], CASES[4]], ids=["sym_fp8_crt", "symtri_headline"])
+def test_sharded_crt_certificate_bit_identical_to_one_gpu(A, case, world):
+    # IPR_CERT_CRT (R-35) at G > 1: every rank rounds / splits the gathered candidate, computes the
+    # column panel Y[:, S_g] exactly (stored K-major: the rows S_g of the symmetric Y), splits those rows,
+    # all-gathers the residue planes and the row statistics, and P[:, S_g] with partials in their global
+    # slots -- the certified bound, every record and the answer bit-identical to G = 1
+    cid, sched, p = case
+    form, phases = _schedule(sched)
+    out1, tr1, C1 = _solve_world1(A, p, phases, form, cert="crt")
+    assert out1 == ipr.IPR_CONVERGED, (cid, out1)
+    res = _solve_local(A, p, phases, form, world, cert="crt")
+    for r, (out, tr, C) in enumerate(res):
+        assert out == out1, (cid, r)
+        _same_trace(tr, tr1)
+        np.testing.assert_array_equal(C, C1)
+    assert tr1[-1]["rho_cert"] <= 1e-12
+
+
 GRID_CASES = [("literal_fp64", "fp64", 2), ("literal_bf16_fp64", "bf16>fp64", 2), ("literal_tf32_fp64_p3", "tf32>fp64", 3)]
 
 
@@ -149,7 +168,7 @@ def test_local_group_bad_arguments(A):
         ipr.ipr_test_local_group_destroy(grp)
 
 
-def _nccl_rank(rank, world, port, sched, p, q):
+def _nccl_rank(rank, world, port, sched, p, q, cert="fp64"):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
@@ -158,7 +177,7 @@ def _nccl_rank(rank, world, port, sched, p, q):
     dist.broadcast_object_list(obj, src=0)
     A = torch.from_numpy(synth.spd(N, 2.0, 31)).cuda()
     form, phases = _schedule(sched)
-    s = ipr.Solver(A, p, phases, 1e-12, world=world, rank=rank, nccl_unique_id=obj[0], form=form)
+    s = ipr.Solver(A, p, phases, 1e-12, world=world, rank=rank, nccl_unique_id=obj[0], form=form, cert=cert)
     s.iterate(300)
     tr = s.trace()
     C = s.finalize().cpu().numpy()
@@ -167,17 +186,18 @@ def _nccl_rank(rank, world, port, sched, p, q):
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs (NCCL)")
-@pytest.mark.parametrize("case", [CASES[0], CASES[4]], ids=["literal_fp64", "symtri_headline"])
-def test_nccl_bit_identical_to_one_gpu(A, case):
+@pytest.mark.parametrize("case,cert", [(CASES[0], "fp64"), (CASES[4], "fp64"), (CASES[4], "crt")],
+                         ids=["literal_fp64", "symtri_headline", "symtri_headline_crt_cert"])
+def test_nccl_bit_identical_to_one_gpu(A, case, cert):
     import torch.multiprocessing as mp
     cid, sched, p = case
     form, phases = _schedule(sched)
-    out1, tr1, C1 = _solve_world1(A, p, phases, form)
+    out1, tr1, C1 = _solve_world1(A, p, phases, form, cert=cert)
     world = min(torch.cuda.device_count(), 4)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = 29500 + os.getpid() % 1000
-    procs = [ctx.Process(target=_nccl_rank, args=(r, world, port, sched, p, q)) for r in range(world)]
+    procs = [ctx.Process(target=_nccl_rank, args=(r, world, port, sched, p, q, cert)) for r in range(world)]
     for pr in procs:
         pr.start()
     got = [q.get(timeout=600) for _ in procs]
