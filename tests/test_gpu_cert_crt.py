@@ -126,3 +126,32 @@ def test_crt_certificate_unsupported_configurations():
             s.iterate(1)
         assert e.value.status == ipr.IPR_E_UNSUPPORTED
         s.close()
+
+
+def test_crt_certificate_out_of_range_falls_back_to_the_dmma_evaluation():
+    # A scaled by 2^500: C ~ 2^-500, whose row exponents leave the (-400, 400) range the certificate's exact
+    # scalings cover -- the certificate of such a candidate is R-30's FP64 DMMA evaluation of Ct instead,
+    # i.e. ipr_residual(certify=1) == ipr_residual(certify=2).  (Eq. (3)'s C_0 is not scale-invariant for
+    # p = 2 -- C_0^2 A scales as 2^-sc -- so such a solve does not converge in a test's budget: the
+    # certificate is exercised on its early iterates.)
+    n = 256
+    A = torch.from_numpy(np.ldexp(synth.spd(n, 2.0, 9), 500)).cuda()
+    s = ipr.Solver(A, 2, [ipr.make_phase("fp64crt", mant_bits=ipr.IPR_MANT_ADAPTIVE)], 1e-12,
+                   form="symmetric_tri", cert="crt")
+    assert s.iterate(2) == ipr.IPR_RUNNING
+    r1 = s.residual(1)
+    info = ipr.ipr_test_cert_info(s.ctx)
+    assert info["bound"] == r1 and info["beta"] != info["beta"]        # the DMMA value, no bound terms
+    assert r1 == s.residual(2)
+    s.close()
+
+
+@pytest.mark.parametrize("n", [1, 17, 128])
+def test_crt_certificate_tiny_sizes(n):
+    A_np = synth.spd(n, 2.0, 70 + n) if n > 1 else np.array([[0.7]])
+    s, out = _solve(A_np)
+    assert out == ipr.IPR_CONVERGED
+    info = ipr.ipr_test_cert_info(s.ctx)
+    C = s.finalize().cpu().numpy()
+    exact = _check_bound(A_np, info, C, info["bound"])
+    assert exact <= 1e-12
