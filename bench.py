@@ -209,7 +209,16 @@ def oracle_gemms(records, p):
                (p if x["rho_cert"] == x["rho_cert"] else 0) for x in records)
 
 
-def cpu_baseline(schedule_name, p, n_target, gemms_target=None, n_small=1024, seed=5):
+def auto_cert(schedule_name, p, choice="auto"):
+    """The certificate a run uses: IPR_CERT_CRT (R-35) where it applies -- a symmetric form, p = 2, an
+    fp64crt phase -- else IPR_CERT_FP64 (R-30); an explicit choice wins."""
+    if choice != "auto":
+        return choice
+    form, parts = parse_schedule(schedule_name)
+    return "crt" if form.startswith("symmetric") and p == 2 and any(x[0] == "fp64crt" for x in parts) else "fp64"
+
+
+def cpu_baseline(schedule_name, p, n_target, gemms_target=None, n_small=1024, seed=5, cert="fp64"):
     """The oracle (plain C, FP64 triple loops; FP64_CRT products as exact 128-bit integer sums) as it
     stands, timed on the host cores on ONE REAL SOLVE: the same schedule on the kappa = 2 twin at order
     n_small (measured), then scaled to n_target by n^3 and by the GEMM count (the target's, when the GPU
@@ -219,18 +228,18 @@ def cpu_baseline(schedule_name, p, n_target, gemms_target=None, n_small=1024, se
     A_s = synth.spd(n_small, 2.0, seed)
     oform, ph = oracle_schedule(schedule_name, n_small)
     t0 = time.perf_counter()
-    r = oracle.solve(A_s, p, ph, 1e-12, 300, form=oform)
+    r = oracle.solve(A_s, p, ph, 1e-12, 300, form=oform, cert=cert)
     t = time.perf_counter() - t0
     g_small = oracle_gemms(r.records, p)
     g_t = gemms_target if gemms_target else g_small
     scale = (n_target / n_small) ** 3 * g_t / g_small
     iters = [sum(1 for x in r.records if x["phase"] == i) for i in range(len(ph))]
-    cert = [x["rho_cert"] for x in r.records if x["rho_cert"] == x["rho_cert"]]
+    certs = [x["rho_cert"] for x in r.records if x["rho_cert"] == x["rho_cert"]]
     cores = len(os.sched_getaffinity(0))
     return {"value": t * scale, "unit": "s", "cores": cores, "kind": "oracle",
-            "sample": f"one full oracle solve of {schedule_name} on the kappa=2 twin at n={n_small} (seed {seed}): "
+            "sample": f"one full oracle solve of {schedule_name} (certificate {cert}) on the kappa=2 twin at n={n_small} (seed {seed}): "
                       f"{oracle.OUTCOME_NAMES[r.outcome]}, iterations {iters}, certified rho "
-                      f"{cert[-1] if cert else float('nan'):.3e}, {g_small} GEMMs in {t:.1f} s on {cores} threads "
+                      f"{certs[-1] if certs else float('nan'):.3e}, {g_small} GEMMs in {t:.1f} s on {cores} threads "
                       f"(measured); value = that x (n={n_target}/{n_small})^3 x ({g_t} / {g_small} GEMMs) (extrapolated"
                       f"{', GEMM count of the GPU trajectory at n=' + str(n_target) if gemms_target else ', the oracle GEMM count at n_small'})",
             "measured_solve_s": t, "measured_n": n_small, "measured_iters": iters, "extrapolated": True}
@@ -253,6 +262,9 @@ def main():
               "l2": "inputs larger than L2 (A = %.0f MB FP64 > 126 MB); no flush" % (n * n * 8 / 1e6),
               "parallelism": f"1x{args.gpus} column panels" if args.gpus > 1 else "single GPU"}
 
+    cert = auto_cert(args.schedule, p, args.cert)
+    config["certificate"] = cert
+
     if args.impl == "reference":
         # Reference arm = the oracle as it stands on the host cores (rank 0 only): every step one real oracle
         # solve of the same schedule at n = 512 (a bounded sample), scaled to the workload's n by n^3 at the
@@ -261,7 +273,7 @@ def main():
             return
         vals = []
         for i in range(args.warmup + args.steps):
-            cb = cpu_baseline(args.schedule, p, n, None, n_small=512)
+            cb = cpu_baseline(args.schedule, p, n, None, n_small=512, cert=cert)
             if i >= args.warmup:
                 vals.append(cb["value"])
         v = float(np.mean(vals))
@@ -288,12 +300,6 @@ def main():
     C_out = torch.empty_like(A)
     torch.cuda.synchronize()
     form, phases = schedule(args.schedule, n)
-    cert = args.cert
-    if cert == "auto":
-        crt_ok = form.startswith("symmetric") and p == 2 and \
-            any(ipr.PREC_NAMES[q.prec] == "fp64crt" for q in phases)
-        cert = "crt" if crt_ok else "fp64"
-    config["certificate"] = cert
     def solve(A_dev, out, early_out=False):
         s = ipr.Solver(A_dev, p, phases, 1e-12, stream, world, rank, uid, form=form, cert=cert)
         if early_out:
@@ -538,7 +544,7 @@ def main():
     cb = None
     if world == 1:
         try:
-            cb = cpu_baseline(args.schedule, p, n, gemm_count(tr, p), n_small=1024)
+            cb = cpu_baseline(args.schedule, p, n, gemm_count(tr, p), n_small=1024, cert=cert)
         except Exception as ex:  # never fail the bench line on the CPU leg
             cb = {"value": None, "unit": "s", "cores": None, "kind": "oracle", "sample": f"failed: {ex}"}
     line = {"metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
