@@ -1051,7 +1051,7 @@ __device__ __forceinline__ void two_sum(double a, double b, double &s, double &e
   e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
 }
 template <int NM, int MODE>
-__global__ void __launch_bounds__(256, 2) k_crt_finish_dd(const GemmArgs g) {
+__global__ void __launch_bounds__(256, MODE == 1 ? 3 : 2) k_crt_finish_dd(const GemmArgs g) {
   extern __shared__ double sm_dd[];            // MODE 0: [2][32][CRT_FIN_LD]
   __shared__ double red[8];
   const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN), g.tri, (int)(g.col0 / TC_BN)};
