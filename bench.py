@@ -209,13 +209,14 @@ def oracle_gemms(records, p):
                (p if x["rho_cert"] == x["rho_cert"] else 0) for x in records)
 
 
-def auto_cert(schedule_name, p, choice="auto"):
-    """The certificate a run uses: IPR_CERT_CRT (R-35) where it applies -- a symmetric form, p = 2, an
-    fp64crt phase -- else IPR_CERT_FP64 (R-30); an explicit choice wins."""
+def auto_cert(schedule_name, p, choice="auto", world=1):
+    """The certificate a run uses: IPR_CERT_CRT (R-35) where it applies -- a symmetric form with an fp64crt
+    phase, p = 2 (any 1 x G) or p = 3 (one GPU) -- else IPR_CERT_FP64 (R-30); an explicit choice wins."""
     if choice != "auto":
         return choice
     form, parts = parse_schedule(schedule_name)
-    return "crt" if form.startswith("symmetric") and p == 2 and any(x[0] == "fp64crt" for x in parts) else "fp64"
+    crt = any(x[0] == "fp64crt" for x in parts) and form.startswith("symmetric")
+    return "crt" if crt and (p == 2 or (p == 3 and world == 1)) else "fp64"
 
 
 def cpu_baseline(schedule_name, p, n_target, gemms_target=None, n_small=1024, seed=5, cert="fp64"):
@@ -262,7 +263,7 @@ def main():
               "l2": "inputs larger than L2 (A = %.0f MB FP64 > 126 MB); no flush" % (n * n * 8 / 1e6),
               "parallelism": f"1x{args.gpus} column panels" if args.gpus > 1 else "single GPU"}
 
-    cert = auto_cert(args.schedule, p, args.cert)
+    cert = auto_cert(args.schedule, p, args.cert, int(os.environ.get("WORLD_SIZE", "1")))
     config["certificate"] = cert
 
     if args.impl == "reference":

@@ -1093,7 +1093,7 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       {(void **)&c->full64, cr ? 0 : full * 8}, {&c->Acert, cr ? 0 : panel * 8},
       {&c->chat_rm, (cr && c->world > 1) ? full * 8 : 0},
       {&c->Tcol, c->grows > 1 ? panel * 8 : 0},
-      {(void **)&c->certv, (cr && is_sym(c)) ? (size_t)c->npad * 8 * 8 : 0},
+      {(void **)&c->certv, (cr && is_sym(c)) ? (size_t)c->npad * 12 * 8 : 0},
       {(void **)&c->partg, c->grows > 1 ? (size_t)c->world * c->npart * 8 : 0},
       {&c->msend, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0},
       {&c->mrecv, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0}};
@@ -1412,10 +1412,11 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
       bool crt = false;
       for (auto &P : c->ph) crt |= P.prec == IPR_FP64_CRT;
       const int nm = crt_moduli(kCertBits, c->n);
-      if (!is_sym(c) || c->p != 2 || c->grows != 1 || !crt || !c->ph.back().cont64 || nm < 16)
+      if (!is_sym(c) || !(c->p == 2 || (c->p == 3 && c->world == 1)) || c->grows != 1 || !crt ||
+          !c->ph.back().cont64 || nm < 16)
         return fail(c, IPR_E_UNSUPPORTED,
-                    "ipr_iterate: IPR_CERT_CRT needs a symmetric form with p = 2 on a 1 x G grid, an IPR_FP64_CRT "
-                    "phase and an FP64 last phase, and n <= 65535");
+                    "ipr_iterate: IPR_CERT_CRT needs a symmetric form with p = 2 on a 1 x G grid or p = 3 on one GPU, "
+                    "an IPR_FP64_CRT phase and an FP64 last phase, and n <= 65535");
     }
     if (c->grows > 1) {   // the 2-D grid option: Eq. (1) as printed, unscaled tensor-core / DMMA formats
       if (c->form != IPR_FORM_LITERAL)
@@ -1778,8 +1779,11 @@ static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
   const int b = kCertBits, nm = crt_moduli(b, c->n);
   const int64_t np = c->npad, kp = c->kp, col0 = c->col0;
   const bool sh = c->world > 1;                    // 1 x G column panels: rank g owns the columns S_g
+  const bool p3 = c->p == 3;                       // p = 3 (G = 1): T = Ct Ytilde between Y and the residual
   double *err2Y = c->certv, *asumY = c->certv + np, *scY = c->certv + 2 * np, *err2A = c->certv + 3 * np;
   double *asumA = c->certv + 4 * np, *scA = c->certv + 5 * np, *scC = c->certv + 6 * np;
+  double *err2T = c->certv + 7 * np, *asumT = c->certv + 8 * np, *scT = c->certv + 9 * np;
+  double *asumC = c->certv + 10 * np;
   if (!c->hcert && !(c->hcert = pinned_acquire())) return fail(c, IPR_E_OOM, "pinned host slab exhausted");
   // G > 1: the gathered C (panel-major in full64) row-major in chat_rm; every rank rounds and splits all
   // of it (the A role of Y = Ct Ct needs every row), the B role takes the rows S_g of the same residues
@@ -1787,7 +1791,7 @@ static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
   if (sh) CK(launch_copy_out(c->full64, np, kp, c->n, Ct, np, st));
   // 1. the certified matrix and its residues
   CK(launch_cert_rowexp(Ct, np, np, np, b, c->crC_sig, scC, st));
-  CK(launch_cert_round_split(Ct, np, np, np, nm, c->crC_sig, c->crC, st));
+  CK(launch_cert_round_split(Ct, np, np, np, nm, c->crC_sig, c->crC, p3 ? asumC : nullptr, st));
   c->crC_for = -1;
   CK(cudaMemsetAsync(c->dflag + 2, 0, 4, st));
   CK(launch_symcheck(Ct, np, c->n, c->dflag + 2, st));
@@ -1813,11 +1817,13 @@ static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
     ctB = c->crB;
     ylo = (double *)(c->crB + ((size_t)nm * kp * np + 255) / 256 * 256);   // 18/G + 8/G <= 18 bytes per n^2
   }
-  // 2. A (FP64, m = 52; its local K-major panel = the rows S_g) and its residues
   PhaseC P64{IPR_FP64, 52, 0, 1, 0, 0, 0, 0};
-  CKS(stage_a(c, P64, c->T[1], c->dsig + 0));
-  CK(launch_cert_split((const double *)c->T[1], nullptr, np, kp, np, b, nm, c->crA, 0, c->crA_sig, scA + col0,
-                       err2A + col0, asumA + col0, st));
+  // 2. (p = 2) A (FP64, m = 52; its local K-major panel = the rows S_g) and its residues
+  if (!p3) {
+    CKS(stage_a(c, P64, c->T[1], c->dsig + 0));
+    CK(launch_cert_split((const double *)c->T[1], nullptr, np, kp, np, b, nm, c->crA, 0, c->crA_sig, scA + col0,
+                         err2A + col0, asumA + col0, st));
+  }
   c->crA_b = -1;
   // 3. Y = Ct Ct exact, hi + lo: G = 1 its upper tiles mirrored (row-major); G > 1 the column panel
   //    Y[:, S_g] stored K-major, i.e. the rows S_g of the symmetric Y
@@ -1828,22 +1834,38 @@ static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
   if (sh) g.mode = EPI_STORE_T;
   else { g.tri = 1; g.mode = EPI_STORE_N; }
   CK(launch_gemm_crt(g, st));
-  // 4. residues of Y's rows (G > 1: the rows S_g into their global slots, then all-gathered)
-  CK(launch_cert_split((const double *)c->T[1], ylo, np, kp, np, b, nm, c->crC + col0 * np, np * np, c->crC_sig + col0,
-                       scY + col0, err2Y + col0, asumY + col0, st));
   c->zr_for = -1;
-  if (sh) {
-    for (int l = 0; l < nm; ++l) {
-      int8_t *pl = c->crC + (size_t)l * np * np;
-      if (!c->comm->allgather(pl + col0 * np, pl, (size_t)(kp * np), st))
-        return fail(c, IPR_E_NCCL, "all-gather(Y residues) failed: %s", c->comm->last_error());
+  if (p3) {
+    // p = 3: Y's rows -> crA (Y is exactly symmetric, so its row quantisation read as columns is the B
+    // role of T = Ct Ytilde); T exact (full) -> hi + lo; T's rows -> crC; then A -> crA
+    int *ysig = c->crA_sig;
+    CK(launch_cert_split((const double *)c->T[1], ylo, np, np, np, b, nm, c->crA, 0, ysig, scY, err2Y, asumY, st));
+    GemmArgs t = base_args(c, IPR_FP64_CRT, nullptr);
+    t.oz_a = c->crC; t.oz_rsig = c->crC_sig; t.oz_b = c->crA; t.oz_csig = ysig;
+    t.crt_n = nm; t.crt_v = c->crV; t.crt_dd = 1;
+    t.nout = c->T[1]; t.ldn = np; t.zout = ylo; t.ldz = np; t.mode = EPI_STORE_N;
+    CK(launch_gemm_crt(t, st));
+    CK(launch_cert_split((const double *)c->T[1], ylo, np, np, np, b, nm, c->crC, 0, c->crC_sig, scT, err2T, asumT, st));
+    CKS(stage_a(c, P64, c->T[1], c->dsig + 0));
+    CK(launch_cert_split((const double *)c->T[1], nullptr, np, np, np, b, nm, c->crA, 0, c->crA_sig, scA, err2A, asumA,
+                         st));
+  } else {
+    // 4. residues of Y's rows (G > 1: the rows S_g into their global slots, then all-gathered)
+    CK(launch_cert_split((const double *)c->T[1], ylo, np, kp, np, b, nm, c->crC + col0 * np, np * np, c->crC_sig + col0,
+                         scY + col0, err2Y + col0, asumY + col0, st));
+    if (sh) {
+      for (int l = 0; l < nm; ++l) {
+        int8_t *pl = c->crC + (size_t)l * np * np;
+        if (!c->comm->allgather(pl + col0 * np, pl, (size_t)(kp * np), st))
+          return fail(c, IPR_E_NCCL, "all-gather(Y residues) failed: %s", c->comm->last_error());
+      }
+      bool ok = c->comm->allgather(c->crC_sig + col0, c->crC_sig, (size_t)kp * 4, st);
+      for (double *v : {scY, err2Y, asumY, scA, err2A})
+        ok = ok && c->comm->allgather(v + col0, v, (size_t)kp * 8, st);
+      if (!ok) return fail(c, IPR_E_NCCL, "all-gather(certificate rows) failed: %s", c->comm->last_error());
     }
-    bool ok = c->comm->allgather(c->crC_sig + col0, c->crC_sig, (size_t)kp * 4, st);
-    for (double *v : {scY, err2Y, asumY, scA, err2A})
-      ok = ok && c->comm->allgather(v + col0, v, (size_t)kp * 8, st);
-    if (!ok) return fail(c, IPR_E_NCCL, "all-gather(certificate rows) failed: %s", c->comm->last_error());
   }
-  // 5. P = Ytilde Atilde (the local columns): residual partials in their global slots
+  // 5. P = Ltilde Atilde (L = Y for p = 2, T for p = 3; the local columns): residual partials in their global slots
   GemmArgs h = base_args(c, IPR_FP64_CRT, nullptr);
   h.oz_a = c->crC; h.oz_rsig = c->crC_sig; h.oz_b = c->crA; h.oz_csig = c->crA_sig;
   h.crt_n = nm; h.crt_v = c->crV; h.crt_dd = 1; h.mode = EPI_RESID; h.part = c->part;
@@ -1854,19 +1876,41 @@ static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
   const double *vv[6] = {err2Y, err2A, asumY, scY, scA, scC};
   const int ops[6] = {0, 0, 1, 1, 1, 1};
   CK(launch_cert_stats(vv, ops, 6, np, c->dscal + 17, st));
+  if (p3) {
+    const double *vt[4] = {err2T, asumT, scT, asumC};
+    const int ot[4] = {0, 1, 1, 1};
+    CK(launch_cert_stats(vt, ot, 4, np, c->dscal + 24, st));
+  }
   CK(cudaMemcpyAsync(c->hcert, c->dscal + 16, 7 * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(c->hcert + 7, c->dflag + 2, 4, cudaMemcpyDeviceToHost, st));
+  double ht[4] = {0, 0, 0, 0};
+  if (p3) CK(cudaMemcpyAsync(ht, c->dscal + 24, 4 * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   const double SR = c->hcert[0], SY = c->hcert[1], SA = c->hcert[2], Yinf = c->hcert[3];
   const double scYm = c->hcert[4], scAm = c->hcert[5], scCm = c->hcert[6];
   int asym = 0;
   memcpy(&asym, c->hcert + 7, 4);
   const double infl = 1.0 + 1e-10, nd = (double)c->n, rec = ldexp(crt_table().p2s1[nm], -48);
-  const double eY = nd * rec * scCm * scCm, eP = nd * rec * scYm * scAm;
+  const double eY = nd * rec * scCm * scCm;        // ||Yh - Ct Ct||_F (reconstruction, >= its inf-norm too)
   const double dY = std::sqrt(SY) * infl, dA = std::sqrt(SA) * infl;
-  const double A2 = c->norms[0] * infl, Y2 = Yinf * infl + eY;
+  const double A2 = c->norms[0] * infl;
   const double est = std::sqrt(SR);
-  const double beta = (dY + eY) * (A2 + dA) + Y2 * dA + eP;
+  double beta, Y2, eP;
+  if (!p3) {
+    // I - Ct^2 A = (I - P) + (Ytilde - Ct^2) Atilde + Ct^2 (Atilde - A)
+    eP = nd * rec * scYm * scAm;
+    Y2 = Yinf * infl + eY;                         // ||Ct^2||_2 <= ||Ct^2||_inf (symmetric)
+    beta = (dY + eY) * (A2 + dA) + Y2 * dA + eP;
+  } else {
+    // I - Ct^3 A = (I - P) + (Ttilde - Ct^3) Atilde + Ct^3 (Atilde - A), with Ttilde - Ct^3 =
+    // (Ttilde - Th) + (Th - Ct Ytilde) + Ct (Ytilde - Ct^2): E3 = dT + eT + ||Ct||_2 (dY + eY)
+    const double dT = std::sqrt(ht[0]) * infl, Tinf = ht[1], scTm = ht[2], C2 = ht[3] * infl;
+    const double eT = nd * rec * scCm * scYm;
+    eP = nd * rec * scTm * scAm;
+    const double E3 = dT + eT + C2 * (dY + eY);
+    Y2 = Tinf * infl + std::sqrt(nd) * E3;         // ||Ct^3||_2 <= ||Ct^3||_inf <= ||Th||_inf + sqrt(n) ||T - Ct^3||_F
+    beta = E3 * (A2 + dA) + Y2 * dA + eP;
+  }
   double bound = (est * infl + beta) * infl;
   if (asym || !std::isfinite(bound)) bound = NAN;   // exponents out of range / an asymmetric candidate
   const double info[10] = {bound, est, beta, dY, dA, A2, Y2, eY, eP, (double)nm};

@@ -502,7 +502,9 @@ __global__ void __launch_bounds__(256) k_cert_rowexp(const double *__restrict__ 
 template <bool UNS>
 __global__ void __launch_bounds__(256, 3) k_cert_round_split(double *__restrict__ X, int64_t ld, int64_t rows,
                                                              int64_t cols, int nm, const int *__restrict__ sig,
-                                                             int8_t *planes) {
+                                                             int8_t *planes, double *asum) {
+  __shared__ double red[8];
+  double as = 0.0;
   const int64_t r = blockIdx.x;
   double *x = X + r * ld;
   const int er = sig[r];
@@ -518,12 +520,17 @@ __global__ void __launch_bounds__(256, 3) k_cert_round_split(double *__restrict_
     for (int u = 0; u < 4; ++u) {
       const int g = min(er, es[u]);
       v[u] = scale2(rint(scale2(v[u], g)), -g);                    // Ct_rk on the grid 2^-g (exact)
+      as += fabs(v[u]);
       const uint64_t y = (uint64_t)__double2ll_rn(scale2(v[u], er)) + (1ull << 63);   // 2^e_r Ct_rk: an integer
       lo[u] = (uint32_t)y; hi[u] = (uint32_t)(y >> 32);
     }
     *(double2 *)(x + k0) = make_double2(v[0], v[1]);
     *(double2 *)(x + k0 + 2) = make_double2(v[2], v[3]);
     cert_split4<0, UNS>(lo, hi, nm, planes + r * cols + k0, plane);
+  }
+  if (asum) {                                                        // sum_k |Ct_rk| (||Ct||_inf, p >= 3)
+    as = block_sum_det<256>(as, red);
+    if (threadIdx.x == 0) asum[r] = as;
   }
 }
 
@@ -590,10 +597,10 @@ cudaError_t launch_cert_rowexp(const double *X, int64_t ld, int64_t rows, int64_
   return cudaGetLastError();
 }
 cudaError_t launch_cert_round_split(double *X, int64_t ld, int64_t rows, int64_t cols, int nm, const int *sig,
-                                    int8_t *planes, cudaStream_t s) {
+                                    int8_t *planes, double *asum, cudaStream_t s) {
   if (nm < 2 || nm > CRT_MAX || cols % 4 || ld % 2) return cudaErrorInvalidValue;
-  if (crt_unsigned(cols)) k_cert_round_split<true><<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, nm, sig, planes);
-  else k_cert_round_split<false><<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, nm, sig, planes);
+  if (crt_unsigned(cols)) k_cert_round_split<true><<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, nm, sig, planes, asum);
+  else k_cert_round_split<false><<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, nm, sig, planes, asum);
   ++g_launches;
   return cudaGetLastError();
 }

@@ -155,3 +155,30 @@ def test_crt_certificate_tiny_sizes(n):
     C = s.finalize().cpu().numpy()
     exact = _check_bound(A_np, info, C, info["bound"])
     assert exact <= 1e-12
+
+
+@pytest.mark.parametrize("n", [256, 520])
+def test_crt_certificate_p3(n):
+    # p = 3 (one GPU): Y = Ct Ct exact, T = Ct Ytilde exact (Y symmetric, so its row quantisation is the
+    # column operand), P = Ttilde Atilde; the bound carries ||Ct||_inf (dY + eY) through T
+    A_np = synth.spd(n, 2.0, 80 + n)
+    A = torch.from_numpy(A_np).cuda()
+    s = ipr.Solver(A, 3, _gpu_phases(), 1e-12, form="symmetric", cert="crt")
+    assert s.iterate(200) == ipr.IPR_CONVERGED
+    tr = s.trace()
+    info = ipr.ipr_test_cert_info(s.ctx)
+    assert tr[-1]["rho_cert"] == info["bound"] <= 1e-12
+    assert s.residual(1) == info["bound"]
+    C = s.finalize().cpu().numpy()
+    np.testing.assert_array_equal(C, oracle.cert_grid(C, 62))
+    exact = oracle.resid_dd(A_np, C, 3)
+    assert exact <= info["bound"] and abs(info["est"] - exact) <= info["beta"] + 1e-9 * exact
+    # unconverged iterates too (the trajectory's early records)
+    s2 = ipr.Solver(A, 3, _gpu_phases(), 1e-12, form="symmetric", cert="crt")
+    s2.iterate(6)
+    b2 = s2.residual(1)
+    i2 = ipr.ipr_test_cert_info(s2.ctx)
+    C2 = s2.iterate_copy(1).cpu().numpy()
+    s2.close()
+    e2 = oracle.resid_dd(A_np, oracle.cert_grid(C2, 62), 3)
+    assert e2 <= b2 and abs(i2["est"] - e2) <= i2["beta"] + 1e-9 * e2 and e2 > 1e-12

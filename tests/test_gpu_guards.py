@@ -87,11 +87,12 @@ def test_guards_intact_sharded(sched, grid):
 
 
 @pytest.mark.parametrize("n", [300, 520, 1000])
-@pytest.mark.parametrize("sched", ["symtri:fp8/cfp8>bf16>fp64crt@a/cbf16", "sym:bf16>fp64crt@a/cbf16"])
-def test_guards_intact_crt_certificate(n, sched):
+@pytest.mark.parametrize("sched,p", [("symtri:fp8/cfp8>bf16>fp64crt@a/cbf16", 2), ("sym:bf16>fp64crt@a/cbf16", 2),
+                                     ("sym:bf16>fp64crt@a/cbf16", 3)])
+def test_guards_intact_crt_certificate(n, sched, p):
     # IPR_CERT_CRT (R-35): the grid-rounding split, the double-double finish with its mirrored hi / lo
     # stores, the double-double split and the certificate's statistics stay inside their buffers
     A = torch.from_numpy(synth.spd(n, 2.0, 60 + n)).cuda()
-    bad, out = _solve_checked(A, 2, sched, cert="crt")
+    bad, out = _solve_checked(A, p, sched, cert="crt")
     assert bad == -1, (sched, n, bad)
     assert out == ipr.IPR_CONVERGED

@@ -22,15 +22,18 @@ def low_then_fp64(low, n, m=-1, fp64_cap=0, switch_rho_hat=1e-2):
             ipr.make_phase("fp64", max_iters=fp64_cap)]
 
 
-def run(A, p, phases, label, max_iters=400, form="literal", tol=1e-12):
+def run(A, p, phases, label, max_iters=400, form="literal", tol=1e-12, cert="fp64"):
     n = A.shape[0]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    s = ipr.Solver(A, p, phases, tol, form=form)
+    s = ipr.Solver(A, p, phases, tol, form=form, cert=cert)
     s.iterate(max_iters)
     tr = s.trace()
     out = ipr.OUTCOME_NAMES[s.outcome]
-    certified = s.residual(True) if tr else float("nan")
+    certs = [t["rho_cert"] for t in tr if t["rho_cert"] == t["rho_cert"]]
+    t_solve = time.perf_counter() - t0
+    certified = s.residual(1) if tr else float("nan")
+    dmma = s.residual(2) if tr and cert == "crt" else certified
     s.close()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
@@ -49,7 +52,8 @@ def run(A, p, phases, label, max_iters=400, form="literal", tol=1e-12):
         d["tflops"] = d["gemms"] * 2.0 * n ** 3 / (d["ms"] * 1e-3) / 1e12 if d["ms"] > 0 else None
     rec = {"label": label, "n": n, "p": p, "outcome": out, "iterations": len(tr), "min_rho": rmin,
            "argmin": kmin, "final_rho": rho[-1] if rho else None, "certified_rho_best": certified,
-           "time_s": dt, "phases": per}
+           "certificate": cert, "rho_cert": certs[-1] if certs else None, "dmma_eval_best": dmma,
+           "solve_s": t_solve, "time_s": dt, "phases": per}
     print(json.dumps(rec), flush=True)
     return rec
 
@@ -58,6 +62,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default="")
     ap.add_argument("--out", default="")
+    ap.add_argument("--cert", default="auto", help="auto (IPR_CERT_CRT where it applies) | crt | fp64")
     a = ap.parse_args()
     only = set(a.only.split(",")) if a.only else None
     recs = []
@@ -135,7 +140,8 @@ def main():
             for sched, tol in runs:
                 form, ph = bench.schedule(sched, n)
                 ph[-1].max_iters = 40 if n >= 32768 else 120
-                recs.append(run(A, p, ph, lab + " " + sched, form=form, tol=tol))
+                cert = bench.auto_cert(sched, p, a.cert) if not (p == 3 and form == "symmetric_tri") else "fp64"
+                recs.append(run(A, p, ph, lab + " " + sched + f" [cert {cert}]", form=form, tol=tol, cert=cert))
             del A
             torch.cuda.empty_cache()
     if a.out:
