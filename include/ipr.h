@@ -243,11 +243,12 @@ ipr_status ipr_set_form(ipr_ctx *c, int form);
  *    linear rate predicts it, rho_k (rho_k / rho_{k-1}) <= final_tol / 2: then C_{k+1} is certified
  *    BEFORE its chain, which runs only if the certificate misses (the converged record then has
  *    rho = NaN).  IPR_CERT_FP64_CHAIN: the same certificate, triggered by the in-chain rho only.
- *  IPR_CERT_CRT (reading R-35; symmetric forms, p = 2, 1 x G grids, an IPR_FP64_CRT phase, FP64 last phase):
+ *  IPR_CERT_CRT (reading R-35; symmetric forms, p = 2 on 1 x G grids or p = 3 on one GPU, an IPR_FP64_CRT
+ *    phase, FP64 last phase):
  *    a PROVEN upper bound on ||I - Ct^2 A||_F, where Ct is the candidate C_k rounded to the coarser of its
  *    row's and its column's 62-bit grids (|Ct - C_k| <= 2^-62 of the row / column maximum; the rounding
  *    makes Ct's integer quantisation exact), from exact integer products on the INT8 tensor cores
- *    (Y = Ct Ct on its upper tiles, then Y A; 1.5 x 18 modulus GEMMs) plus the quantisation and
+ *    (Y = Ct Ct on its upper tiles, then Y A; 1.5 x 18 modulus GEMMs; p = 3: Y, T = Ct Y, T A) plus the quantisation and
  *    reconstruction errors bounded a posteriori (||A||_2 <= ||A||_1, ||Y||_2 <= ||Y||_inf).  Converged
  *    means that bound is <= final_tol, and Ct is the answer (it replaces C_k; ipr_set_output streams Ct).
  *    Triggered like IPR_CERT_FP64 (R-33).  An FP64 DMMA evaluation carries ~n u |C|^2 |A| of rounding
