@@ -39,6 +39,11 @@ constexpr int TC_SMEM = TC_ST * TC_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers
 #define IPR_TC_GROUP_M 8
 #endif
 constexpr int TC_GROUP_M = IPR_TC_GROUP_M;   // pair-rows per scheduling group
+// CRT modulus GEMMs: 16 pair-rows per group -- each B (residue) column block is streamed n / (16 x 256)
+// times instead of n / (8 x 256) per modulus (DRAM traffic; the launches are tensor-bound either way)
+#ifndef IPR_CRT_GROUP_M
+#define IPR_CRT_GROUP_M 16
+#endif
 
 bool tc_supported(int prec) {
   return prec == P_BF16 || prec == P_FP16 || prec == P_TF32 || prec == P_FP8 || prec == P_INT8;
@@ -203,6 +208,7 @@ struct TileSched {      // pair tiles: tiles_m pair-rows (256 rows) x tiles_n (2
   int tiles_m, tiles_n, tri;
   int coff;             // tri, column panel of a G > 1 rank: global 256-column tile of local tile 0 --
                         // the upper-triangle tiles are tm <= coff + tn (0 for a square single panel)
+  int gm = TC_GROUP_M;  // pair-rows per L2 raster group (non-tri)
   // tri (square, symmetric-tri GEMM 2 / fused update): only the upper-triangle pair tiles tm <= tn, in
   // bands of TRI_GC pair-columns, row by row inside a band, so the CTA pairs in flight share their A
   // row blocks (TRI_GC tiles each) and B column blocks (the band) in L2 -- a column-by-column order
@@ -231,12 +237,12 @@ struct TileSched {      // pair tiles: tiles_m pair-rows (256 rows) x tiles_n (2
         t -= nb;
       }
     }
-    const int per_group = TC_GROUP_M * tiles_n;
-    const int gidx = t / per_group, first_m = gidx * TC_GROUP_M;
-    const int gm = min(tiles_m - first_m, TC_GROUP_M);
+    const int per_group = this->gm * tiles_n;
+    const int gidx = t / per_group, first_m = gidx * this->gm;
+    const int gmm = min(tiles_m - first_m, this->gm);
     const int r = t - gidx * per_group;
-    tm = first_m + r % gm;
-    tn = r / gm;
+    tm = first_m + r % gmm;
+    tn = r / gmm;
   }
 };
 
@@ -1222,11 +1228,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_NT, 1)
   const bool leader = rank == 0;
   if (KIND == 3 && EF == 3) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");   // next modulus launch
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN), g.tri, (int)(g.col0 / TC_BN)};
+  constexpr bool crt = KIND == 3 && EF == 3, ozg = KIND == 3 && EF == 2;
+  TileSched sch{(int)(g.M / (2 * TC_BM)), (int)(g.N / TC_BN), g.tri, (int)(g.col0 / TC_BN)};
+  if (crt) sch.gm = IPR_CRT_GROUP_M;
   const int ntiles = sch.count();
   // CRT (oz_grouped == 3): moduli [crt_l0, crt_l1) of every tile, modulus-major (all CTA pairs
   // stream the same residue planes at a time, as in one plain GEMM)
-  constexpr bool crt = KIND == 3 && EF == 3, ozg = KIND == 3 && EF == 2;
   const int nitems = crt ? (g.crt_l1 - g.crt_l0) * ntiles : ntiles;
   // Ozaki grouped launch: groups S+1 .. 2 per tile; otherwise one pass (g0 == g1)
   // oz_grouped == 2: the single group g.oz_g (one launch per group keeps each group's digit planes
