@@ -23,6 +23,7 @@ RUNS = [  # (label, p, schedule, final_tol)
     ("p2 symtri:bf16>fp64oz@a/cbf16", 2, "symtri:bf16>fp64oz@a/cbf16", 1e-12),
     ("p2 symtri:bf16>fp64crt@a/cbf16", 2, "symtri:bf16>fp64crt@a/cbf16", 1e-12),
     ("p2 cpl:fp64 (to 1e-6)", 2, "cpl:fp64", 1e-6),
+    ("p2 symtri:fp8/cfp8>bf16>fp64crt@a/cbf16 [crt cert]", 2, "symtri:fp8/cfp8>bf16>fp64crt@a/cbf16", 1e-12),
 ]
 
 
@@ -30,6 +31,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sizes", default="768,1536,3072,6144")
     ap.add_argument("--out", default=None)
+    ap.add_argument("--runs", default="", help="comma-separated substrings of the run labels to keep")
     a = ap.parse_args()
     import torch
     import bench
@@ -45,16 +47,19 @@ def main():
             ev = torch.linalg.eigvalsh(A)
             kap = float(ev[-1] / ev[0])
             for label, p, sched, tol in RUNS:
+                if a.runs and not any(k in label for k in a.runs.split(",")):
+                    continue
+                cert_mode = "crt" if "[crt cert]" in label else "fp64"
                 form, ph = bench.schedule(sched, n)
                 st = torch.cuda.current_stream()
                 for rep in range(2):
                     torch.cuda.synchronize()
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(st)
-                    s = ipr.Solver(A, p, ph, tol, st, form=form)
+                    s = ipr.Solver(A, p, ph, tol, st, form=form, cert=cert_mode)
                     s.iterate(300)
                     tr = s.trace()
-                    cert = s.residual(True)
+                    cert = s.residual(1)
                     oc = ipr.OUTCOME_NAMES[s.outcome]
                     s.close()
                     e1.record(st)
