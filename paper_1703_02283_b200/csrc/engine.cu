@@ -1818,11 +1818,21 @@ static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
     ylo = (double *)(c->crB + ((size_t)nm * kp * np + 255) / 256 * 256);   // 18/G + 8/G <= 18 bytes per n^2
   }
   PhaseC P64{IPR_FP64, 52, 0, 1, 0, 0, 0, 0};
-  // 2. (p = 2) A (FP64, m = 52; its local K-major panel = the rows S_g) and its residues
+  // A in FP64 (m = 52; its local K-major panel = the rows S_g): an FP64-range phase with m = 52 staged exactly
+  // that as its operand (Aop), else stage it now
+  const PhaseC &Pc = c->ph[c->phase];
+  const bool aop_exact = is_f64(Pc.prec) && Pc.m == 52 && !Pc.rtz;
+  auto a_f64 = [&](ipr_ctx *cc) -> const double * {
+    if (aop_exact) return (const double *)cc->Aop;
+    if (stage_a(cc, P64, cc->T[1], cc->dsig + 0) != IPR_OK) return nullptr;
+    return (const double *)cc->T[1];
+  };
+  // 2. (p = 2) A's residues
   if (!p3) {
-    CKS(stage_a(c, P64, c->T[1], c->dsig + 0));
-    CK(launch_cert_split((const double *)c->T[1], nullptr, np, kp, np, b, nm, c->crA, 0, c->crA_sig, scA + col0,
-                         err2A + col0, asumA + col0, st));
+    const double *Af = a_f64(c);
+    if (!Af) return IPR_E_CUDA;
+    CK(launch_cert_split(Af, nullptr, np, kp, np, b, nm, c->crA, 0, c->crA_sig, scA + col0, err2A + col0,
+                         asumA + col0, st));
   }
   c->crA_b = -1;
   // 3. Y = Ct Ct exact, hi + lo: G = 1 its upper tiles mirrored (row-major); G > 1 the column panel
@@ -1846,9 +1856,9 @@ static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
     t.nout = c->T[1]; t.ldn = np; t.zout = ylo; t.ldz = np; t.mode = EPI_STORE_N;
     CK(launch_gemm_crt(t, st));
     CK(launch_cert_split((const double *)c->T[1], ylo, np, np, np, b, nm, c->crC, 0, c->crC_sig, scT, err2T, asumT, st));
-    CKS(stage_a(c, P64, c->T[1], c->dsig + 0));
-    CK(launch_cert_split((const double *)c->T[1], nullptr, np, np, np, b, nm, c->crA, 0, c->crA_sig, scA, err2A, asumA,
-                         st));
+    const double *Af = a_f64(c);
+    if (!Af) return IPR_E_CUDA;
+    CK(launch_cert_split(Af, nullptr, np, np, np, b, nm, c->crA, 0, c->crA_sig, scA, err2A, asumA, st));
   } else {
     // 4. residues of Y's rows (G > 1: the rows S_g into their global slots, then all-gathered)
     CK(launch_cert_split((const double *)c->T[1], ylo, np, kp, np, b, nm, c->crC + col0 * np, np * np, c->crC_sig + col0,
