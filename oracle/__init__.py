@@ -85,6 +85,8 @@ def lib():
                                      C.POINTER(C.c_int), _dp, _dp, C.c_int, C.c_double, _dp]
         L.orc_step_sym.restype = C.c_double
         L.orc_step_sym.argtypes = [C.c_int64, C.c_int, _dp, _dp, C.POINTER(Phase), _dp, _dp]
+        L.orc_step_sym_form.restype = C.c_double
+        L.orc_step_sym_form.argtypes = [C.c_int64, C.c_int, C.c_int, _dp, _dp, C.POINTER(Phase), _dp, _dp]
         L.orc_step_ns.restype = C.c_double
         L.orc_step_ns.argtypes = [C.c_int64, _dp, _dp, C.POINTER(Phase), _dp, _dp]
         L.orc_jacobi.argtypes = [C.c_int64, _dp, _dp, _dp]
@@ -282,14 +284,15 @@ def step_ns(A, Xk, ph: Phase, want_next: bool = True):
     return rho, nxt, d.value
 
 
-def step_sym(A, Ck, p: int, ph: Phase, want_next: bool = True):
+def step_sym(A, Ck, p: int, ph: Phase, want_next: bool = True, tri: bool = False):
     """One symmetrised-correction step (NEXT-2, p >= 2): C + (W + W^T)/(2p), W = qc(C) qc(I - Z_p),
-    Z_p = C^{p-1} A C.  Returns (rho_s(C_k) = ||I - Z_p||_F, C_{k+1}, delta)."""
+    Z_p = C^{p-1} A C.  tri: the symmetric-tri form (p = 2; R-36 below the FP64 range).
+    Returns (rho_s(C_k) = ||I - Z_p||_F, C_{k+1}, delta)."""
     A, Ck = _f64(A), _f64(Ck)
     nxt = np.empty_like(Ck) if want_next else None
     d = C.c_double(np.nan)
-    rho = lib().orc_step_sym(A.shape[0], p, _p(A), _p(Ck), C.byref(ph),
-                             _p(nxt) if want_next else None, C.byref(d))
+    rho = lib().orc_step_sym_form(A.shape[0], p, 1 if tri else 0, _p(A), _p(Ck), C.byref(ph),
+                                  _p(nxt) if want_next else None, C.byref(d))
     return rho, nxt, d.value
 
 

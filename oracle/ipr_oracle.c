@@ -562,8 +562,17 @@ static double chain_sym(int64_t n, int p, int tri, const double *A, const double
   return sqrt(s2);
 }
 
-static double update_sym(int64_t n, int p, const double *C, const orc_phase *ph, chain_ws *w,
+/* Reading R-36: the symmetric-tri form in a reduced-precision phase (not FP64 / FP64_OZ / FP64_CRT) takes
+ * the correction from W's upper triangle only, S_ij = 2 W_{min(i,j), max(i,j)} instead of W_ij + W_ji
+ * (they differ by the commutator [C, R], at the phase's own rounding level there); FP64-range phases keep
+ * W + W^T, whose symmetrisation sets the linear rate of R-22. */
+static int tri_w_phase(int tri, const orc_phase *ph) {
+  return tri && ph->prec != ORC_FP64 && ph->prec != ORC_FP64_OZ && ph->prec != ORC_FP64_CRT;
+}
+
+static double update_sym(int64_t n, int p, int tri, const double *C, const orc_phase *ph, chain_ws *w,
                          double *C_next) {
+  const int triw = tri_w_phase(tri, ph);
   const int64_t nn = n * n;
   const int sigCc = qin_matrix(corr_of(ph), nn, C, w->Chat); /* qc(C)                 */
   orc_gemm(n, w->Chat, w->X, w->T);                         /* W = qc(C) Rhat         */
@@ -573,7 +582,8 @@ static double update_sym(int64_t n, int p, const double *C, const orc_phase *ph,
   double s2 = 0.0;
   for (int64_t i = 0; i < n; ++i)
     for (int64_t j = 0; j < n; ++j) {
-      const double sw = w->T[i * n + j] + w->T[j * n + i];
+      const double sw = triw ? 2.0 * w->T[(i < j ? i : j) * n + (i < j ? j : i)]
+                             : w->T[i * n + j] + w->T[j * n + i];
       const double e = sw / tp;
       const double c1 = store_q(ph, C[i * n + j] + e);
       const double dd = c1 - C[i * n + j];
@@ -698,13 +708,18 @@ double orc_step_ns(int64_t n, const double *A, const double *X, const orc_phase 
 
 double orc_step_sym(int64_t n, int p, const double *A, const double *C, const orc_phase *ph,
                     double *C_next, double *delta) {
-  if (p < 2 || (is_scaled(corr_of(ph)) && corr_of(ph) != ph->prec)) return NAN;
+  return orc_step_sym_form(n, p, 0, A, C, ph, C_next, delta);
+}
+
+double orc_step_sym_form(int64_t n, int p, int tri, const double *A, const double *C, const orc_phase *ph,
+                         double *C_next, double *delta) {
+  if (p < 2 || (is_scaled(corr_of(ph)) && corr_of(ph) != ph->prec) || (tri && p != 2)) return NAN;
   chain_ws w;
   if (!ws_alloc(&w, n)) { ws_free(&w); return NAN; }
   if (ph->prec == ORC_FP64_CRT)   /* a single step: the digits of the phase's fixed m (9 if adaptive) */
     w.crt_b = orc_crt_bits(is_adaptive(ph) ? 9 : orc_digits_for_m(phase_m(ph)), n);
-  const double rho = chain_sym(n, p, 0, A, C, ph, &w);
-  if (C_next) { const double d = update_sym(n, p, C, ph, &w, C_next); if (delta) *delta = d; }
+  const double rho = chain_sym(n, p, tri, A, C, ph, &w);
+  if (C_next) { const double d = update_sym(n, p, tri, C, ph, &w, C_next); if (delta) *delta = d; }
   ws_free(&w);
   return rho;
 }
@@ -853,7 +868,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
       /* rho_s = ||I - C^{p-1} A C||_F is not the north-star residual: certify
        * ||I - C^p A||_F with the FP64 literal chain (reading R-3); if it misses final_tol the
        * iteration continues from the update computed first (as the GPU engine does). */
-      r.delta = update_sym(n, p, C, &ph_k, &w, Cn);
+      r.delta = update_sym(n, p, form == ORC_FORM_SYMMETRIC_TRI, C, &ph_k, &w, Cn);
       r.rho_cert = isfinite(cert_pre) ? cert_pre : sym_cert(n, p, A, C, &w, Ct);   /* R-33: once */
       if (!(r.rho_cert <= final_tol)) {
         d = ORC_CONTINUE;
@@ -871,7 +886,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
       m_of_C = phase_m(ph);
     } else if (d == ORC_CONTINUE) {
       r.delta = form == ORC_FORM_NEWTON_SCHULZ ? update_ns(n, C, ph, &w, Cn)
-                : sym                           ? update_sym(n, p, C, &ph_k, &w, Cn)
+                : sym                           ? update_sym(n, p, form == ORC_FORM_SYMMETRIC_TRI, C, &ph_k, &w, Cn)
                                                 : update(n, p, C, ph, &w, Cn);
       double *t = C; C = Cn; Cn = t;
       m_of_C = phase_m(&ph_k);

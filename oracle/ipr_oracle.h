@@ -143,6 +143,11 @@ double orc_step_ns(int64_t n, const double *A, const double *X, const orc_phase 
  * Returns NaN for p < 2 or an FP16 phase. */
 double orc_step_sym(int64_t n, int p, const double *A, const double *C, const orc_phase *ph,
                     double *C_next, double *delta);
+/* The same step for a form: tri = 0 ORC_FORM_SYMMETRIC, 1 ORC_FORM_SYMMETRIC_TRI (p = 2; Z_2 from its upper
+ * triangle and -- reading R-36, in phases below the FP64 range -- the correction from W's upper triangle:
+ * C_{k+1} = q_m(C + 2 W_{min(i,j),max(i,j)} / (2p))). */
+double orc_step_sym_form(int64_t n, int p, int tri, const double *A, const double *C, const orc_phase *ph,
+                         double *C_next, double *delta);
 
 /* Cyclic Jacobi eigen-decomposition of a symmetric matrix (n small).
  * lambda ascending, V columns = eigenvectors (row-major n x n).  Returns sweeps used. */

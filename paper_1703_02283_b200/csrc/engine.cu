@@ -878,6 +878,16 @@ ipr_status update(ipr_ctx *c) {
 }
 
 // ---- symmetric form (NEXT-2): W = qc(C) Rhat, then C_{k+1} = q_m(C + (W + W^T)/(2p)) ----
+// Reading R-36: the symmetric-tri form in a phase below the FP64 range (FP8 / INT8 / FP16 / BF16 / TF32) takes
+// the correction from W's upper triangle only, S_ij = 2 W_{min(i,j), max(i,j)} instead of W_ij + W_ji (they
+// differ by the commutator [C, R], at the phase's own rounding level there): the W GEMM runs on its upper
+// tiles.  FP64-range phases keep W + W^T (its symmetrisation sets R-22's linear rate).  IPR_TRI_W=0: off.
+int wtri_phase(const ipr_ctx *c, const PhaseC &P) {
+  static int on = -1;
+  if (on < 0) { const char *v = getenv("IPR_TRI_W"); on = v ? atoi(v) != 0 : 1; }
+  return on && c->form == IPR_FORM_SYMMETRIC_TRI && !is_f64(P.prec) ? 1 : 0;
+}
+
 ipr_status update_sym(ipr_ctx *c) {
   const PhaseC &P = c->ph[c->phase];
   Nvtx nv("update sym corr=%s", pname(P.corr));
@@ -915,6 +925,9 @@ ipr_status update_sym(ipr_ctx *c) {
   if (is_scaled(P.corr)) { g.sigA = c->dsig + 1 + c->cur; g.sigB = c->dsig + 3 + (c->p & 1); }   // R-29
   // W holds the exact accumulator values: FP64 for an FP64 (DMMA) correction, else FP32
   const int wb = P.corr == IPR_FP64 ? 8 : 4;
+  // reading R-36: the tri form below the FP64 range computes only W's upper tiles (S = 2 W_{min, max})
+  const int wtri = wtri_phase(c, P);
+  g.tri = wtri;
   g.mode = EPI_WSTORE;
   g.w64 = wb == 8;
   g.wout = (char *)c->wbuf + (size_t)c->rank * (size_t)(c->npad * c->kp) * wb;
@@ -928,7 +941,7 @@ ipr_status update_sym(ipr_ctx *c) {
   CK(launch_sym_update(cont_ptr(c, c->cur, P), P.cont64, cont_ptr(c, nx, P), c->wbuf, wb == 8, c->npad,
                        c->kp, c->col0, c->p, P.adaptive ? c->oz_m_next : P.m, P.rtz, P.prec,
                        (is_f64(P.prec) || is_scaled(P.prec)) ? nullptr : chat_slot(c, nx, P.prec), P.corr,
-                       same_fmt(P.corr, P.prec) ? nullptr : chatc_slot(c, nx, P.corr), c->part, amax, c->st));
+                       same_fmt(P.corr, P.prec) ? nullptr : chatc_slot(c, nx, P.corr), c->part, amax, wtri, c->st));
   CK(cudaEventRecord(c->ev[3], c->st));
   c->upd_timed = true;
   const int64_t t64 = c->npad / 64;

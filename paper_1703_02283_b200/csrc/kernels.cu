@@ -374,7 +374,7 @@ template <typename CT, typename WT>
 __global__ void __launch_bounds__(256, 6) k_sym_update(const CT *__restrict__ cold, CT *__restrict__ cnew,
                                                     const WT *__restrict__ W, int64_t npad, int64_t kp, int64_t col0,
                                                     int p, int m, int rtz, int prec, void *chat_new, int corr,
-                                                    void *chat_corr_new, double *part, unsigned *amax) {
+                                                    void *chat_corr_new, double *part, unsigned *amax, int wtri) {
   __shared__ WT t[64][65];
   __shared__ double red[8];
   __shared__ float redf[8];
@@ -421,7 +421,10 @@ __global__ void __launch_bounds__(256, 6) k_sym_update(const CT *__restrict__ co
     bool ok = true;
     #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      const double sw = __dadd_rn(wv[v], (double)t[c4 + v][r]);
+      // wtri (reading R-36, the tri form below the FP64 range): W holds its upper triangle only, S_ij =
+      // 2 W_{min(i,j), max(i,j)} (doubling is exact); else S = W + W^T
+      const double sw = !wtri ? __dadd_rn(wv[v], (double)t[c4 + v][r])
+                              : 2.0 * ((ib + r <= col0 + jb + c4 + v) ? wv[v] : (double)t[c4 + v][r]);
       const double e = pow2p ? __dmul_rn(sw, itp) : __ddiv_rn(sw, tp);   // d/(2p); exact recip. for 2^k
       xv[v] = __dadd_rn(cv[v], e);
       cn[v] = sizeof(CT) == 8 ? q_e11_fast(xv[v], qr, ok) : q_e8d_fast(xv[v], qr, ok);
@@ -701,11 +704,11 @@ cudaError_t launch_transpose(const void *src, int64_t rows, int64_t cols, int es
 
 cudaError_t launch_sym_update(const void *cold, int cont64, void *cnew, const void *W, int w64, int64_t npad,
                               int64_t kp, int64_t col0, int p, int m, int rtz, int prec, void *chat_new, int corr,
-                              void *chat_corr_new, double *part, unsigned *amax, cudaStream_t s) {
+                              void *chat_corr_new, double *part, unsigned *amax, int wtri, cudaStream_t s) {
   if (kp % 64 || npad % 64) return cudaErrorInvalidValue;
   dim3 g((unsigned)(kp / 64), (unsigned)(npad / 64)), b(256);
 #define SYMU(CT, WT) k_sym_update<CT, WT><<<g, b, 0, s>>>((const CT *)cold, (CT *)cnew, (const WT *)W, npad, kp, col0, \
-                                                          p, m, rtz, prec, chat_new, corr, chat_corr_new, part, amax)
+                                                          p, m, rtz, prec, chat_new, corr, chat_corr_new, part, amax, wtri)
   if (cont64 && w64) SYMU(double, double);
   else if (cont64) SYMU(double, float);
   else if (w64) SYMU(float, double);

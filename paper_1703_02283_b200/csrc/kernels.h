@@ -36,7 +36,7 @@ cudaError_t launch_transpose(const void *src, int64_t rows, int64_t cols, int es
 // amax (nullable): atomicMax of the bits of max |C_{k+1}| (as float) -- the caller zeroes it first
 cudaError_t launch_sym_update(const void *cold, int cont64, void *cnew, const void *W, int w64, int64_t npad,
                               int64_t kp, int64_t col0, int p, int m, int rtz, int prec, void *chat_new, int corr,
-                              void *chat_corr_new, double *part, unsigned *amax, cudaStream_t s);
+                              void *chat_corr_new, double *part, unsigned *amax, int wtri, cudaStream_t s);
 cudaError_t launch_oz_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int S, int8_t *planes,
                             int8_t *bcat, int *sig, cudaStream_t s);
 cudaError_t launch_crt_split(const double *X, int64_t ld, int64_t rows, int64_t cols, int b, int nm, int8_t *planes,

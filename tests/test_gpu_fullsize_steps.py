@@ -11,7 +11,8 @@ from the previous stage's values (ipr_test_peek exposes each stage's stored oper
                              Rhat_ij = qc(delta_ij - Chat[min(i,j), :] . qin(Z_1)[:, max(i,j)]) -- the
                              mirror of the upper triangle (R-22 tri reading), and Rhat exactly symmetric
   W = qc(C) Rhat             sampled (i, j): qc(C)[i, :] . Rhat[:, j]
-  C_{k+1} = q_m(C_k + (W + W^T) / 4)   EVERY element, bit for bit (the FP64 epilogue is deterministic)
+  C_{k+1} = q_m(C_k + (W + W^T) / 4)   EVERY element, bit for bit (the FP64 epilogue is deterministic);
+                             below the FP64 range the tri form's S_ij = 2 W_{min(i,j), max(i,j)} (R-36)
 
 Bounds: FP32 accumulation n 2^-24 sum |terms| (tensor cores: FP8 / BF16), the CRT quantisation
 2^-b (row max . column abs-sum + row abs-sum . column max) (R-28), the operand rounding u of the
@@ -155,7 +156,12 @@ def test_headline_phase_step_full_size(mat, case):
     assert np.all(lim[dg] < 0.2 * np.abs(r_ref[dg]))
 
     # ---- stage 3: W = qc(C_k) Rhat (FP32 accumulate; FP8 correction: scaled operands, exact unscale) ----
+    # (reading R-36: every CASE is the symmetric-tri form; below the FP64 range only W's upper triangle is
+    # computed, so the sampled pairs are taken as (min, max) there)
+    triw = prec not in ("fp64", "fp64crt", "fp64oz")
     I3, J3 = I[:400], J[:400]
+    if triw:
+        I3, J3 = np.minimum(I3, J3), np.maximum(I3, J3)
     w_ref = np.einsum("ij,ij->i", Chc[I3], Rhat[:, J3].T)
     acc_c = 2.0 ** -53 if corr == "fp64" else 2.0 ** -24
     b3 = n * acc_c * np.einsum("ij,ij->i", np.abs(Chc[I3]), np.abs(Rhat[:, J3].T)) + 2.0 ** -24 * np.abs(w_ref)
@@ -166,6 +172,10 @@ def test_headline_phase_step_full_size(mat, case):
     m = {"fp8": 3, "bf16": 7}.get(prec, None)
     if m is None:
         m = int(ph[phase_idx].mant_bits) if ph[phase_idx].mant_bits >= 0 else 52
-    e = (W + W.T) / 4.0
+    if triw:                                  # S_ij = 2 W_{min(i,j), max(i,j)} (R-36)
+        Wu = np.triu(W)
+        e = 2.0 * (Wu + np.triu(W, 1).T) / 4.0
+    else:
+        e = (W + W.T) / 4.0
     C1_ref = oracle.qm(Ck + e, E, m)
     np.testing.assert_array_equal(Ck1, C1_ref)
