@@ -534,6 +534,15 @@ static int corr_of(const orc_phase *ph) {
   return is_scaled(ph->prec) ? ORC_BF16 : ph->prec;
 }
 
+/* Reading R-36: the symmetric-tri form in a reduced-precision phase (not FP64 / FP64_OZ / FP64_CRT) takes
+ * Z_1 = A C and W = C R from their upper triangles: Z_1 := the mirror of its upper triangle, and the
+ * correction S_ij = 2 W_{min(i,j), max(i,j)} instead of W_ij + W_ji -- each differs from the full product by a
+ * commutator ([A, C], [C, R]) that sits at the phase's own rounding level there; FP64-range phases keep the
+ * full products (the symmetrisation of W + W^T sets the linear rate of R-22). */
+static int tri_w_phase(int tri, const orc_phase *ph) {
+  return tri && ph->prec != ORC_FP64 && ph->prec != ORC_FP64_OZ && ph->prec != ORC_FP64_CRT;
+}
+
 static double chain_sym(int64_t n, int p, int tri, const double *A, const double *C,
                         const orc_phase *ph, chain_ws *w) {
   const int64_t nn = n * n;
@@ -546,6 +555,9 @@ static double chain_sym(int64_t n, int p, int tri, const double *A, const double
     if (j > 1) chain_gemm(w, n, w->Chat, w->X, w->T);       /* Z_j = Chat qin(Z_{j-1}) */
     if (sigX + w->sigC != 0)
       for (int64_t i = 0; i < nn; ++i) w->T[i] = ldexp(w->T[i], -(sigX + w->sigC));
+    if (j == 1 && tri_w_phase(tri, ph))                     /* R-36: Z_1 from its upper triangle */
+      for (int64_t r = 0; r < n; ++r)
+        for (int64_t c = 0; c < r; ++c) w->T[r * n + c] = w->T[c * n + r];
     if (j < p) sigX = qin_matrix(ph->prec, nn, w->T, w->X); /* qin(Z_j)               */
   }
   if (tri)                     /* ORC_FORM_SYMMETRIC_TRI: Z_2 = C A C from its upper triangle */
@@ -562,13 +574,6 @@ static double chain_sym(int64_t n, int p, int tri, const double *A, const double
   return sqrt(s2);
 }
 
-/* Reading R-36: the symmetric-tri form in a reduced-precision phase (not FP64 / FP64_OZ / FP64_CRT) takes
- * the correction from W's upper triangle only, S_ij = 2 W_{min(i,j), max(i,j)} instead of W_ij + W_ji
- * (they differ by the commutator [C, R], at the phase's own rounding level there); FP64-range phases keep
- * W + W^T, whose symmetrisation sets the linear rate of R-22. */
-static int tri_w_phase(int tri, const orc_phase *ph) {
-  return tri && ph->prec != ORC_FP64 && ph->prec != ORC_FP64_OZ && ph->prec != ORC_FP64_CRT;
-}
 
 static double update_sym(int64_t n, int p, int tri, const double *C, const orc_phase *ph, chain_ws *w,
                          double *C_next) {

@@ -543,6 +543,16 @@ inline bool same_fmt(int a, int b) { return a == b || (is_f64(a) && is_f64(b)); 
 // IPR_CERT_CRT (reading R-35): the certificate quantises its operands to 62 bits (18 moduli up to n = 86000)
 constexpr int kCertBits = 62;
 inline bool is_sym(const ipr_ctx *c) { return c->form == IPR_FORM_SYMMETRIC || c->form == IPR_FORM_SYMMETRIC_TRI; }
+// Reading R-36: the symmetric-tri form in a phase below the FP64 range (FP8 / INT8 / FP16 / BF16 / TF32) takes
+// Z_1 = A C and W = C R from their upper triangles -- GEMM 1 and the W GEMM run on their upper tiles, Z_1 is
+// mirrored, and S_ij = 2 W_{min(i,j), max(i,j)} replaces W_ij + W_ji: each differs from the full product by a
+// commutator ([A, C], [C, R]) at the phase's own rounding level there.  FP64-range phases keep the full
+// products (the symmetrisation of W + W^T sets R-22's linear rate).  IPR_TRI_W=0: off (A/B only).
+int wtri_phase(const ipr_ctx *c, const PhaseC &P) {
+  static int on = -1;
+  if (on < 0) { const char *v = getenv("IPR_TRI_W"); on = v ? atoi(v) != 0 : 1; }
+  return on && c->form == IPR_FORM_SYMMETRIC_TRI && !is_f64(P.prec) ? 1 : 0;
+}
 void *chatc_slot(ipr_ctx *c, int i, int prec) {
   return (char *)c->chatc[i] + (size_t)c->rank * (size_t)(c->npad * c->kp) * elt_size(prec);
 }
@@ -690,6 +700,13 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
           g.mode |= EPI_STORE_N; g.nout = c->Zr; g.ldn = c->npad; c->zr_for = c->cur;
         }
       }
+      // R-36: below the FP64 range the tri form computes Z_1 on its upper tiles and mirrors them
+      const bool z1tri = j == 1 && c->p == 2 && wtri_phase(c, P);
+      if (z1tri) {
+        g.tri = 1;
+        // tiles below the diagonal are not visited -- their partial maxima must not be stale
+        if (g.mode & EPI_TSCRATCH) CK(cudaMemsetAsync(c->pmax, 0, sizeof(float) * tiles_n_total(c, prec) * tm, c->st));
+      }
       // R-29: a scaled correction (= prec) takes R = I - Z_p through the FP32 scratch + per-tile max
       const bool rscr = j == c->p && is_scaled(P.corr);
       if (j == c->p) {
@@ -725,10 +742,10 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
           CKS(crt_operands(c, g, c->cur, c->T[(j - 1) & 1]));
         }
       }
-      const bool mx = j == c->p && g.tri && c->world > 1;   // tri, G > 1: mirror tiles cross panels
+      const bool mx = (j == c->p || z1tri) && g.tri && c->world > 1;   // tri, G > 1: mirror tiles cross panels
       if (mx) { g.mout = c->msend; g.ldm = c->kp; }
       CK(run_gemm(c, g));
-      if (mx) CKS(mirror_exchange(c, g.tout, rscr ? 4 : elt_size(g.tprec)));
+      if (mx) CKS(mirror_exchange(c, g.tout, (rscr || (scaled && j < c->p)) ? 4 : elt_size(g.tprec)));
       if (rscr) {   // sigma_R -> dsig[3 + (p & 1)] (not the slot GEMM p read), Rhat -> T[p & 1]
         CKS(gather_pmax(c, c->pmax, tn_loc * tm));
         CK(launch_reduce_max(c->pmax, tiles_n_total(c, prec) * tm, nullptr, c->dsig + 3 + (j & 1), prec, c->st));
@@ -878,16 +895,6 @@ ipr_status update(ipr_ctx *c) {
 }
 
 // ---- symmetric form (NEXT-2): W = qc(C) Rhat, then C_{k+1} = q_m(C + (W + W^T)/(2p)) ----
-// Reading R-36: the symmetric-tri form in a phase below the FP64 range (FP8 / INT8 / FP16 / BF16 / TF32) takes
-// the correction from W's upper triangle only, S_ij = 2 W_{min(i,j), max(i,j)} instead of W_ij + W_ji (they
-// differ by the commutator [C, R], at the phase's own rounding level there): the W GEMM runs on its upper
-// tiles.  FP64-range phases keep W + W^T (its symmetrisation sets R-22's linear rate).  IPR_TRI_W=0: off.
-int wtri_phase(const ipr_ctx *c, const PhaseC &P) {
-  static int on = -1;
-  if (on < 0) { const char *v = getenv("IPR_TRI_W"); on = v ? atoi(v) != 0 : 1; }
-  return on && c->form == IPR_FORM_SYMMETRIC_TRI && !is_f64(P.prec) ? 1 : 0;
-}
-
 ipr_status update_sym(ipr_ctx *c) {
   const PhaseC &P = c->ph[c->phase];
   Nvtx nv("update sym corr=%s", pname(P.corr));

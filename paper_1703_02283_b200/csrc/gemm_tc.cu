@@ -529,8 +529,10 @@ __device__ __forceinline__ void epi_chunk(const GemmArgs &g, int64_t row, int64_
     return;
   }
   // (b) FP32 scratch of a scaled format: the scale is an exact power of two, so one FP32
-  //     multiply gives the same float as (float)(acc * scale) in FP64 (one rounding for INT32)
-  if (mode == EPI_TSCRATCH) {
+  //     multiply gives the same float as (float)(acc * scale) in FP64 (one rounding for INT32).
+  //     Not for tri (R-36's GEMM 1): its segments on / below the diagonal take (d), whose lower elements
+  //     come from the mirror -- stored here too, they raced with the mirror stores of the upper ones
+  if (mode == EPI_TSCRATCH && !g.tri) {
     const float sf = (float)scale;
     float *t = (float *)g.tout + col * g.ldt + row;
     #pragma unroll

@@ -7,6 +7,7 @@ the Newton correction) is checked stage by stage on sampled elements the oracle 
 from the previous stage's values (ipr_test_peek exposes each stage's stored operand):
 
   Z_1 = Ahat Chat            sampled columns:  Ahat Chat[:, j] (oracle matvec), then the operand rounding
+                             (below the FP64 range: the mirror of its upper triangle, R-36)
   Z_2 = Chat qin(Z_1) (tri)  sampled (i, j) over every band, both triangles:
                              Rhat_ij = qc(delta_ij - Chat[min(i,j), :] . qin(Z_1)[:, max(i,j)]) -- the
                              mirror of the upper triangle (R-22 tri reading), and Rhat exactly symmetric
@@ -129,6 +130,12 @@ def test_headline_phase_step_full_size(mat, case):
     else:
         ref = Ahat @ Chat[:, cols]
         bnd = prod_bound(Ahat, Chat, np.arange(n), cols)
+        # R-36: below the FP64 range Z_1 is the mirror of its upper triangle -- rows below the diagonal of
+        # column j hold (Ahat Chat)[j, i]; Z_1 exactly symmetric
+        assert np.array_equal(Z1, Z1.T)
+        lower = np.arange(n)[:, None] > cols[None, :]
+        ref = np.where(lower, (Ahat[cols] @ Chat).T, ref)
+        bnd = np.where(lower, prod_bound(Ahat, Chat, cols, np.arange(n)).T, bnd)
         u_op = U[prec]
         sub = 2.0 ** -16 * np.abs(Z1).max() if prec == "fp8" else 0.0   # E4M3 subnormal quantum (scaled max 2^6)
         err = np.abs(Z1[:, cols] - ref)

@@ -213,3 +213,23 @@ def test_missed_certificates_respect_the_phase_cap():
     assert sum(1 for t in tr if t["phase"] == 1) == cap
     assert tr[-1]["decision"] == ipr.IPR_ITER_LIMIT       # terminal decisions equal the outcome codes
     assert sum(1 for t in tr if t["rho_cert"] == t["rho_cert"]) >= 2
+
+
+@pytest.mark.parametrize("sched", ["symtri:fp8/cfp8>bf16>fp64crt@a/cbf16", "symtri:bf16>fp64/cbf16"])
+def test_run_to_run_deterministic_scaled_tri_phases(sched):
+    # R-36's GEMM 1 on the upper tiles writes the lower elements of its diagonal tiles only through the
+    # mirror stores (an FP32-scratch path that also stored them raced with those mirrors -- found by
+    # tools/z1_det_probe.py): n = 2048 (8 diagonal pair tiles), every record and the answer bit-identical
+    import bench
+    A = torch.from_numpy(synth.spd(2048, 2.0, 9)).cuda()
+    form, ph = bench.schedule(sched, 2048)
+    res = []
+    for _ in range(2):
+        s = ipr.Solver(A, 2, ph, 1e-12, form=form, cert="crt" if "crt" in sched else "fp64")
+        s.iterate(200)
+        res.append((s.trace(), s.finalize().cpu().numpy()))
+    (t1, b1), (t2, b2) = res
+    assert t1[-1]["decision"] == ipr.IPR_DEC_CONVERGED
+    for key in ("rho", "delta", "decision", "rho_cert"):
+        assert np.array_equal([a[key] for a in t1], [a[key] for a in t2], equal_nan=True), key
+    np.testing.assert_array_equal(b1, b2)

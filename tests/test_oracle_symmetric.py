@@ -297,22 +297,28 @@ def test_missed_certificates_respect_the_phase_cap():
 
 
 def test_tri_form_low_phase_correction_from_upper_triangle():
-    # reading R-36: the symmetric-tri form below the FP64 range takes S_ij = 2 W_{min(i,j), max(i,j)}; pinned
-    # on a non-commuting 2 x 2 whose every intermediate is exact in BF16 (hand values):
-    #   Z_1 = A C = [[9/8, 5/8], [7/8, 5/4]], Z_2 = C Z_1 = [[43/64, 15/32], [15/32, 35/64]], R = I - Z_2,
-    #   W = C R = [[27/256, -91/512], [-69/512, 57/512]]  (W_01 != W_10: C and R do not commute)
+    # reading R-36: below the FP64 range the symmetric-tri form takes Z_1 = A C and W = C R from their upper
+    # triangles -- Z_1 := mirror(upper(A C)), S_ij = 2 W_{min(i,j), max(i,j)}.  Pinned on a non-commuting
+    # 2 x 2 whose every intermediate is exact in BF16 (hand values):
+    #   A C = [[9/8, 5/8], [7/8, 5/4]] -> Z_1 = [[9/8, 5/8], [5/8, 5/4]], Z_2 = mirror(upper(C Z_1)) =
+    #   [[41/64, 15/32], [15/32, 35/64]], R = I - Z_2, W = C R = [[31/256, -91/512], [-67/512, 57/512]]
+    # and, for the full symmetric form / an FP64 phase (no mirroring of Z_1, S = W + W^T):
+    #   Z_2 = [[43/64, 15/32], [15/32, 35/64]], W = [[27/256, -91/512], [-69/512, 57/512]]
     A = np.array([[2.0, 1.0], [1.0, 3.0]])
     Ck = np.array([[0.5, 0.125], [0.125, 0.375]])
-    W = np.array([[27 / 256, -91 / 512], [-69 / 512, 57 / 512]])
+    W = np.array([[31 / 256, -91 / 512], [-67 / 512, 57 / 512]])
+    Z2 = np.array([[41 / 64, 15 / 32], [15 / 32, 35 / 64]])
     up = np.array([[2 * W[0, 0], 2 * W[0, 1]], [2 * W[0, 1], 2 * W[1, 1]]])
-    std = W + W.T
     ph = oracle.phase(oracle.BF16)
     rho, C1, _ = oracle.step_sym(A, Ck, 2, ph, tri=True)
     np.testing.assert_array_equal(C1, oracle.qm(Ck + up / 4, 8, 7))
-    assert rho == pytest.approx(np.linalg.norm(np.eye(2) - np.array([[43 / 64, 15 / 32], [15 / 32, 35 / 64]])), rel=1e-15)
-    assert not np.array_equal(oracle.qm(Ck + std / 4, 8, 7), C1)
-    # the full symmetric form, and the tri form in an FP64 phase, keep W + W^T
-    _, C1s, _ = oracle.step_sym(A, Ck, 2, ph, tri=False)
-    np.testing.assert_array_equal(C1s, oracle.qm(Ck + std / 4, 8, 7))
-    _, C1f, _ = oracle.step_sym(A, Ck, 2, oracle.phase(), tri=True)
-    np.testing.assert_array_equal(C1f, Ck + std / 4)
+    assert rho == pytest.approx(np.linalg.norm(np.eye(2) - Z2), rel=1e-15)
+    assert not np.array_equal(oracle.qm(Ck + (W + W.T) / 4, 8, 7), C1)
+    Wf = np.array([[27 / 256, -91 / 512], [-69 / 512, 57 / 512]])
+    Z2f = np.array([[43 / 64, 15 / 32], [15 / 32, 35 / 64]])
+    rs, C1s, _ = oracle.step_sym(A, Ck, 2, ph, tri=False)
+    np.testing.assert_array_equal(C1s, oracle.qm(Ck + (Wf + Wf.T) / 4, 8, 7))
+    assert rs == pytest.approx(np.linalg.norm(np.eye(2) - Z2f), rel=1e-15)
+    rf, C1f, _ = oracle.step_sym(A, Ck, 2, oracle.phase(), tri=True)
+    np.testing.assert_array_equal(C1f, Ck + (Wf + Wf.T) / 4)
+    assert rf == pytest.approx(np.linalg.norm(np.eye(2) - Z2f), rel=1e-15)
