@@ -381,8 +381,10 @@ __global__ void __launch_bounds__(256, 6) k_sym_update(const CT *__restrict__ co
   const int64_t jb = (int64_t)blockIdx.x * 64;             // local column tile
   const int64_t ib = (int64_t)blockIdx.y * 64;             // row tile
   const int64_t slot = npad * kp;
+  // wtri (R-36): a tile wholly above the diagonal needs only W itself, one wholly below only the mirror
+  const bool t_up = wtri && ib + 63 <= col0 + jb, t_low = wtri && ib > col0 + jb + 63;
   // mirrored tile: t[r][c] = W(col0 + jb + r, ib + c)
-  {
+  if (!t_up) {
     const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
     const int64_t gi = ib + tx;
     const WT *src = kp == npad ? W + gi : W + (gi / kp) * slot + gi % kp;   // G = 1: no 64-bit division
@@ -402,8 +404,10 @@ __global__ void __launch_bounds__(256, 6) k_sym_update(const CT *__restrict__ co
   for (int u = 0; u < 4; ++u) {
     const int r = ry + 16 * u;
     const int64_t ci = (ib + r) * kp + jb + c4;
-    double wv[4], cv[4], cn[4];
-    if (sizeof(WT) == 4) {
+    double wv[4] = {0.0, 0.0, 0.0, 0.0}, cv[4], cn[4];
+    if (t_low) {
+      // R-36, a tile wholly below the diagonal: W's lower triangle is not computed, only the mirror is read
+    } else if (sizeof(WT) == 4) {
       const float4 a = *(const float4 *)((const float *)wl + ci);
       wv[0] = a.x; wv[1] = a.y; wv[2] = a.z; wv[3] = a.w;
     } else {

@@ -229,7 +229,7 @@ def test_run_to_run_deterministic_scaled_tri_phases(sched):
         s.iterate(200)
         res.append((s.trace(), s.finalize().cpu().numpy()))
     (t1, b1), (t2, b2) = res
-    assert t1[-1]["decision"] == ipr.IPR_DEC_CONVERGED
+    assert t1[-1]["decision"] == 1   # IPR_DEC_CONVERGED
     for key in ("rho", "delta", "decision", "rho_cert"):
         assert np.array_equal([a[key] for a in t1], [a[key] for a in t2], equal_nan=True), key
     np.testing.assert_array_equal(b1, b2)
