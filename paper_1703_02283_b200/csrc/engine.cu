@@ -1793,7 +1793,7 @@ static ipr_status certify_full64(ipr_ctx *c, double *rho) {
 // 1 + 1e-10 (>= n u for n <= 9e5).  *rho = that bound; c->cert_info keeps its terms.
 // i >= 0: the candidate came from iterate buffer i -- with ipr_set_output the certified Ct streams to the
 // caller during the products, and a passing Ct replaces C_i in its (FP64) container: Ct is the answer.
-static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
+static ipr_status certify_crt(ipr_ctx *c, int i, double *rho, const double *cand = nullptr) {
   Nvtx nv("certify crt");
   cudaStream_t st = c->st;
   const int b = kCertBits, nm = crt_moduli(b, c->n);
@@ -1809,9 +1809,11 @@ static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
   // of it (the A role of Y = Ct Ct needs every row), the B role takes the rows S_g of the same residues
   double *Ct = sh ? (double *)c->chat_rm : c->full64;
   if (sh) CK(launch_copy_out(c->full64, np, kp, c->n, Ct, np, st));
+  // cand (G = 1, FP64 container): the candidate is read in place from its container; Ct goes to full64
+  const double *Cin = cand ? cand : Ct;
   // 1. the certified matrix and its residues
-  CK(launch_cert_rowexp(Ct, np, np, np, b, c->crC_sig, scC, st));
-  CK(launch_cert_round_split(Ct, np, np, np, nm, c->crC_sig, c->crC, p3 ? asumC : nullptr, st));
+  CK(launch_cert_rowexp(Cin, np, np, np, b, c->crC_sig, scC, st));
+  CK(launch_cert_round_split(Cin, Ct, np, np, np, nm, c->crC_sig, c->crC, p3 ? asumC : nullptr, st));
   c->crC_for = -1;
   CK(cudaMemsetAsync(c->dflag + 2, 0, 4, st));
   CK(launch_symcheck(Ct, np, c->n, c->dflag + 2, st));
@@ -1966,6 +1968,8 @@ static ipr_status certify_crt(ipr_ctx *c, int i, double *rho) {
 // the iterate in buffer i (the candidate C_k), FP64, gathered into full64
 static ipr_status certify_iter(ipr_ctx *c, int i, double *rho) {
   const PhaseC &P = c->ph[c->phase];
+  if (c->cert == IPR_CERT_CRT && c->world == 1 && P.cont64)   // the FP64 container is already row-major FP64
+    return certify_crt(c, i, rho, (const double *)cont_ptr(c, i, P));
   double *slot = c->full64 + (size_t)c->rank * c->npad * c->kp;
   CK(launch_cont_to_f64(cont_ptr(c, i, P), P.cont64, c->npad * c->kp, slot, c->st));
   CKS(gather_f64(c, slot));

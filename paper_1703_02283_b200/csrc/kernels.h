@@ -44,8 +44,9 @@ cudaError_t launch_crt_split(const double *X, int64_t ld, int64_t rows, int64_t 
 // the CRT certificate (reading R-35, ozaki.cu)
 cudaError_t launch_cert_rowexp(const double *X, int64_t ld, int64_t rows, int64_t cols, int b, int *sig, double *scale,
                                cudaStream_t s);
-cudaError_t launch_cert_round_split(double *X, int64_t ld, int64_t rows, int64_t cols, int nm, const int *sig,
-                                    int8_t *planes, double *asum, cudaStream_t s);   // asum: row abs sums (nullable)
+// Xin: the candidate (row-major, ld), X: where Ct goes (may equal Xin); asum: row abs sums of Ct (nullable)
+cudaError_t launch_cert_round_split(const double *Xin, double *X, int64_t ld, int64_t rows, int64_t cols, int nm,
+                                    const int *sig, int8_t *planes, double *asum, cudaStream_t s);
 // pstride: the residue plane stride (0: rows * cols); row r of X writes planes + l * pstride + r * cols
 cudaError_t launch_cert_split(const double *Xh, const double *Xl, int64_t ld, int64_t rows, int64_t cols, int b, int nm,
                               int8_t *planes, int64_t pstride, int *sig, double *scale, double *err2, double *asum,

@@ -500,19 +500,20 @@ __global__ void __launch_bounds__(256) k_cert_rowexp(const double *__restrict__ 
 }
 
 template <bool UNS>
-__global__ void __launch_bounds__(256, 3) k_cert_round_split(double *__restrict__ X, int64_t ld, int64_t rows,
+__global__ void __launch_bounds__(256, 3) k_cert_round_split(const double *Xin, double *X, int64_t ld, int64_t rows,
                                                              int64_t cols, int nm, const int *__restrict__ sig,
                                                              int8_t *planes, double *asum) {
   __shared__ double red[8];
   double as = 0.0;
   const int64_t r = blockIdx.x;
+  const double *xi = Xin + r * ld;                 // the candidate (may be X itself: in place)
   double *x = X + r * ld;
   const int er = sig[r];
   const int64_t plane = rows * cols;
   for (int64_t k0 = (int64_t)threadIdx.x * 4; k0 < cols; k0 += (int64_t)blockDim.x * 4) {
     uint32_t lo[4], hi[4];
     double v[4];
-    const double2 a = *(const double2 *)(x + k0), c = *(const double2 *)(x + k0 + 2);
+    const double2 a = *(const double2 *)(xi + k0), c = *(const double2 *)(xi + k0 + 2);
     v[0] = a.x; v[1] = a.y; v[2] = c.x; v[3] = c.y;
     const int4 ek = *(const int4 *)(sig + k0);
     const int es[4] = {ek.x, ek.y, ek.z, ek.w};
@@ -596,11 +597,11 @@ cudaError_t launch_cert_rowexp(const double *X, int64_t ld, int64_t rows, int64_
   ++g_launches;
   return cudaGetLastError();
 }
-cudaError_t launch_cert_round_split(double *X, int64_t ld, int64_t rows, int64_t cols, int nm, const int *sig,
-                                    int8_t *planes, double *asum, cudaStream_t s) {
+cudaError_t launch_cert_round_split(const double *Xin, double *X, int64_t ld, int64_t rows, int64_t cols, int nm,
+                                    const int *sig, int8_t *planes, double *asum, cudaStream_t s) {
   if (nm < 2 || nm > CRT_MAX || cols % 4 || ld % 2) return cudaErrorInvalidValue;
-  if (crt_unsigned(cols)) k_cert_round_split<true><<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, nm, sig, planes, asum);
-  else k_cert_round_split<false><<<(unsigned)rows, 256, 0, s>>>(X, ld, rows, cols, nm, sig, planes, asum);
+  if (crt_unsigned(cols)) k_cert_round_split<true><<<(unsigned)rows, 256, 0, s>>>(Xin, X, ld, rows, cols, nm, sig, planes, asum);
+  else k_cert_round_split<false><<<(unsigned)rows, 256, 0, s>>>(Xin, X, ld, rows, cols, nm, sig, planes, asum);
   ++g_launches;
   return cudaGetLastError();
 }
