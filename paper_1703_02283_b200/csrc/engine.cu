@@ -1172,7 +1172,7 @@ static ipr_status certify_from_zr(ipr_ctx *c, int i, double *rho);
 static ipr_status stream_candidate(ipr_ctx *c, int i);
 
 const char *ipr_version(void) {
-  return "ipr 0.3.0 (sm_100a: tcgen05 BF16/FP16/TF32/FP8/INT8, DMMA FP64, FP64 on INT8 tensor cores: Ozaki I / II-CRT)";
+  return "ipr 0.4.0 (sm_100a: tcgen05 BF16/FP16/TF32/FP8/INT8, DMMA FP64, FP64 on INT8 tensor cores: Ozaki I / II-CRT; CRT certificate)";
 }
 
 const char *ipr_last_error(const ipr_ctx *c) { return c ? c->err.c_str() : t_err.c_str(); }
