@@ -202,7 +202,7 @@ def ipr_test_local_group_destroy(group):
 def ipr_test_init_local(n: int, A, lda: int | None, stream, group, rank: int, grid_rows: int = 1,
                         grid_cols: int | None = None, world: int | None = None):
     """ipr_init for rank `rank` of a local group (call from the rank's own host thread)."""
-    _check_matrix(A, n, "ipr_test_init_local: A")
+    _check_matrix(A, n, "ipr_test_init_local: A", host_ok=True)
     ctx = C.c_void_p()
     _check(_lib.ipr_test_init_local(C.byref(ctx), n, _ptr(A), lda if lda is not None else n, _stream(stream),
                                     group, rank, grid_rows, grid_cols if grid_cols is not None else world))

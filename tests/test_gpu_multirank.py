@@ -213,3 +213,45 @@ def test_nccl_transport_plumbing_one_gpu():
     # the production transport's calls (dlopen'ed NCCL: init, in-place all-gather, grouped send / recv
     # all-to-all, split) on a 1-rank communicator -- the multi-process test above needs >= 2 GPUs
     ipr.ipr_test_nccl_selftest()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_host_buffers_crt_certificate(A, world):
+    # bench.py's e2e path at N > 1: every rank passes the HOST A (pinned) to ipr_init and a host C to
+    # ipr_set_output / ipr_finalize, with the CRT certificate -- the answer bit-identical to the device
+    # path at G = 1
+    form, phases = _schedule("symtri:fp8/cfp8>bf16>fp64crt@a/cbf16")
+    out1, tr1, C1 = _solve_world1(A, 2, phases, form, cert="crt")
+    A_host = A.cpu().pin_memory()
+    grp = ipr.ipr_test_local_group_create(world)
+    res, err = [None] * world, [None] * world
+
+    def rank_main(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                s = ipr.Solver(A_host, 2, phases, 1e-12, stream=st, world=world, rank=r, form=form,
+                               local_group=grp, cert="crt")
+                C = torch.empty_like(A_host).pin_memory()
+                s.set_output(C)
+                s.iterate(300)
+                tr, out = s.trace(), s.outcome
+                s.finalize(C)
+                st.synchronize()
+                res[r] = (out, tr, C.numpy().copy())
+        except Exception as e:   # noqa: BLE001
+            err[r] = e
+
+    th = [threading.Thread(target=rank_main, args=(r,), daemon=True) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(600)
+    ipr.ipr_test_local_group_destroy(grp)
+    for e in err:
+        if e is not None:
+            raise e
+    for out, tr, C in res:
+        assert out == out1 == ipr.IPR_CONVERGED
+        _same_trace(tr, tr1)
+        np.testing.assert_array_equal(C, C1)
