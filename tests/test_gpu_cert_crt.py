@@ -182,3 +182,19 @@ def test_crt_certificate_p3(n):
     s2.close()
     e2 = oracle.resid_dd(A_np, oracle.cert_grid(C2, 62), 3)
     assert e2 <= b2 and abs(i2["est"] - e2) <= i2["beta"] + 1e-9 * e2 and e2 > 1e-12
+
+
+def test_crt_certificate_after_a_dmma_last_phase():
+    # the certificate needs a CRT phase somewhere in the schedule (its buffers) and an FP64 last phase:
+    # BF16 > CRT(23 bits) > FP64 on the DMMA pipe, certified by the CRT bound
+    import bench
+    n = 520
+    A_np = synth.spd(n, 2.0, 17)
+    form, ph = bench.schedule("symtri:bf16>fp64crt@23/cbf16>fp64/cbf16", n)
+    s = ipr.Solver(torch.from_numpy(A_np).cuda(), 2, ph, 1e-12, form=form, cert="crt")
+    assert s.iterate(300) == ipr.IPR_CONVERGED
+    tr = s.trace()
+    info = ipr.ipr_test_cert_info(s.ctx)
+    assert tr[-1]["rho_cert"] == info["bound"] <= 1e-12 and tr[-1]["phase"] == 2
+    C = s.finalize().cpu().numpy()
+    _check_bound(A_np, info, C, info["bound"])
