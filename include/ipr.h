@@ -213,10 +213,10 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
  * wholly below the diagonal are skipped: ~1/2 of GEMM 2) and R_ij = delta_ij - Z_2[min(i,j)][max(i,j)]
  * is exactly symmetric; rho_s sums the off-diagonal terms twice.  G > 1: each rank computes the upper
  * tiles of its own columns, the mirrors reach their owners by one all-to-all.  In phases below the FP64
- * range (FP8 / INT8 / FP16 / BF16 / TF32; reading R-36) Z_1 = A C and W are computed on their
- * upper tiles too: Z_1 := the mirror of its upper triangle and the correction S_ij = 2 W_{min(i,j),max(i,j)}
- * (they differ from the full products by commutators at those phases' own rounding level); FP64-range
- * phases keep the full Z_1 and W + W^T.
+ * range (FP8 / INT8 / FP16 / BF16 / TF32; reading R-36) both symmetric forms compute every chain
+ * product and W on their upper tiles: each Z_j := the mirror of its upper triangle and the correction
+ * S_ij = 2 W_{min(i,j),max(i,j)} (they differ from the full products by commutators at those phases' own
+ * rounding level); FP64-range phases keep the full products and W + W^T.
  *
  * IPR_FORM_COUPLED (any p; FP64 / TF32 / BF16 phases): the M-carrying form
  * of Eq. (1) (reading R-27): with M = X^p A and N = ((p+1) I - M) / p, X_{k+1} = X_k N_k

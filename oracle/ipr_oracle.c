@@ -534,13 +534,15 @@ static int corr_of(const orc_phase *ph) {
   return is_scaled(ph->prec) ? ORC_BF16 : ph->prec;
 }
 
-/* Reading R-36: the symmetric-tri form in a reduced-precision phase (not FP64 / FP64_OZ / FP64_CRT) takes
- * Z_1 = A C and W = C R from their upper triangles: Z_1 := the mirror of its upper triangle, and the
- * correction S_ij = 2 W_{min(i,j), max(i,j)} instead of W_ij + W_ji -- each differs from the full product by a
- * commutator ([A, C], [C, R]) that sits at the phase's own rounding level there; FP64-range phases keep the
- * full products (the symmetrisation of W + W^T sets the linear rate of R-22). */
+/* Reading R-36: the symmetric forms in a reduced-precision phase (not FP64 / FP64_OZ / FP64_CRT) take every
+ * product from its upper triangle: each Z_j := the mirror of its upper triangle (j = 1..p) and the correction
+ * S_ij = 2 W_{min(i,j), max(i,j)} instead of W_ij + W_ji -- each differs from the full product by a commutator
+ * ([A, C], [C, Z_j], [C, R]) that sits at the phase's own rounding level there (C_k is a polynomial in A up to
+ * that noise); FP64-range phases keep the full products (the symmetrisation of W + W^T sets R-22's linear
+ * rate), except the tri form's Z_2 = C A C (symmetric in exact arithmetic, ORC_FORM_SYMMETRIC_TRI). */
 static int tri_w_phase(int tri, const orc_phase *ph) {
-  return tri && ph->prec != ORC_FP64 && ph->prec != ORC_FP64_OZ && ph->prec != ORC_FP64_CRT;
+  (void)tri;
+  return ph->prec != ORC_FP64 && ph->prec != ORC_FP64_OZ && ph->prec != ORC_FP64_CRT;
 }
 
 static double chain_sym(int64_t n, int p, int tri, const double *A, const double *C,
@@ -555,12 +557,12 @@ static double chain_sym(int64_t n, int p, int tri, const double *A, const double
     if (j > 1) chain_gemm(w, n, w->Chat, w->X, w->T);       /* Z_j = Chat qin(Z_{j-1}) */
     if (sigX + w->sigC != 0)
       for (int64_t i = 0; i < nn; ++i) w->T[i] = ldexp(w->T[i], -(sigX + w->sigC));
-    if (j == 1 && tri_w_phase(tri, ph))                     /* R-36: Z_1 from its upper triangle */
+    if (j < p && tri_w_phase(tri, ph))                      /* R-36: Z_j from its upper triangle */
       for (int64_t r = 0; r < n; ++r)
         for (int64_t c = 0; c < r; ++c) w->T[r * n + c] = w->T[c * n + r];
     if (j < p) sigX = qin_matrix(ph->prec, nn, w->T, w->X); /* qin(Z_j)               */
   }
-  if (tri)                     /* ORC_FORM_SYMMETRIC_TRI: Z_2 = C A C from its upper triangle */
+  if (tri || tri_w_phase(tri, ph))   /* ORC_FORM_SYMMETRIC_TRI: Z_2 = C A C from its upper triangle; R-36: Z_p */
     for (int64_t r = 0; r < n; ++r)
       for (int64_t c = 0; c < r; ++c) w->T[r * n + c] = w->T[c * n + r];
   double s2 = 0.0;

@@ -543,15 +543,16 @@ inline bool same_fmt(int a, int b) { return a == b || (is_f64(a) && is_f64(b)); 
 // IPR_CERT_CRT (reading R-35): the certificate quantises its operands to 62 bits (18 moduli up to n = 86000)
 constexpr int kCertBits = 62;
 inline bool is_sym(const ipr_ctx *c) { return c->form == IPR_FORM_SYMMETRIC || c->form == IPR_FORM_SYMMETRIC_TRI; }
-// Reading R-36: the symmetric-tri form in a phase below the FP64 range (FP8 / INT8 / FP16 / BF16 / TF32) takes
-// Z_1 = A C and W = C R from their upper triangles -- GEMM 1 and the W GEMM run on their upper tiles, Z_1 is
-// mirrored, and S_ij = 2 W_{min(i,j), max(i,j)} replaces W_ij + W_ji: each differs from the full product by a
-// commutator ([A, C], [C, R]) at the phase's own rounding level there.  FP64-range phases keep the full
-// products (the symmetrisation of W + W^T sets R-22's linear rate).  IPR_TRI_W=0: off (A/B only).
+// Reading R-36: the symmetric forms in a phase below the FP64 range (FP8 / INT8 / FP16 / BF16 / TF32) take
+// every product from its upper triangle -- each chain GEMM Z_j and the W GEMM run on their upper tiles, the
+// Z_j are mirrored, and S_ij = 2 W_{min(i,j), max(i,j)} replaces W_ij + W_ji: each differs from the full
+// product by a commutator ([A, C], [C, Z_j], [C, R]) at the phase's own rounding level there.  FP64-range
+// phases keep the full products (the symmetrisation of W + W^T sets R-22's linear rate), except the tri
+// form's Z_2.  IPR_TRI_W=0: off (A/B only).
 int wtri_phase(const ipr_ctx *c, const PhaseC &P) {
   static int on = -1;
   if (on < 0) { const char *v = getenv("IPR_TRI_W"); on = v ? atoi(v) != 0 : 1; }
-  return on && c->form == IPR_FORM_SYMMETRIC_TRI && !is_f64(P.prec) ? 1 : 0;
+  return on && is_sym(c) && !is_f64(P.prec) ? 1 : 0;
 }
 void *chatc_slot(ipr_ctx *c, int i, int prec) {
   return (char *)c->chatc[i] + (size_t)c->rank * (size_t)(c->npad * c->kp) * elt_size(prec);
@@ -700,8 +701,8 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
           g.mode |= EPI_STORE_N; g.nout = c->Zr; g.ldn = c->npad; c->zr_for = c->cur;
         }
       }
-      // R-36: below the FP64 range the tri form computes Z_1 on its upper tiles and mirrors them
-      const bool z1tri = j == 1 && c->p == 2 && wtri_phase(c, P);
+      // R-36: below the FP64 range the symmetric forms compute every Z_j on its upper tiles and mirror them
+      const bool z1tri = j < c->p && wtri_phase(c, P);
       if (z1tri) {
         g.tri = 1;
         // tiles below the diagonal are not visited -- their partial maxima must not be stale
@@ -711,7 +712,7 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
       const bool rscr = j == c->p && is_scaled(P.corr);
       if (j == c->p) {
         g.mode |= EPI_DIAG_MINUS | EPI_RESID; g.diag = 1.0; g.tprec = P.corr;
-        g.tri = c->form == IPR_FORM_SYMMETRIC_TRI;   // Z_2 = C A C: upper triangle + mirror
+        g.tri = c->form == IPR_FORM_SYMMETRIC_TRI || wtri_phase(c, P);   // Z_2 = C A C / R-36: upper + mirror
         if (rscr) {
           g.mode = (g.mode & ~EPI_STORE_T) | EPI_TSCRATCH; g.pmax = c->pmax;
           // tri: tiles below the diagonal are not visited -- their partial maxima must not be stale
@@ -1115,8 +1116,8 @@ ipr_status alloc_arena(ipr_ctx *c, bool need_corr) {
       {&c->Tcol, c->grows > 1 ? panel * 8 : 0},
       {(void **)&c->certv, (cr && is_sym(c)) ? (size_t)c->npad * 12 * 8 : 0},
       {(void **)&c->partg, c->grows > 1 ? (size_t)c->world * c->npart * 8 : 0},
-      {&c->msend, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0},
-      {&c->mrecv, (c->world > 1 && c->form == IPR_FORM_SYMMETRIC_TRI) ? panel * 8 : 0}};
+      {&c->msend, (c->world > 1 && is_sym(c)) ? panel * 8 : 0},     // tri mirror exchange (R-36: every sym form)
+      {&c->mrecv, (c->world > 1 && is_sym(c)) ? panel * 8 : 0}};
   const size_t gb = g_guards ? kGuard : 0;
   size_t total = 0;
   for (const Slot &q : slots) total += (q.bytes + 255) / 256 * 256 + (q.bytes ? gb : 0);

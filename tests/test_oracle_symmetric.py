@@ -297,12 +297,13 @@ def test_missed_certificates_respect_the_phase_cap():
 
 
 def test_tri_form_low_phase_correction_from_upper_triangle():
-    # reading R-36: below the FP64 range the symmetric-tri form takes Z_1 = A C and W = C R from their upper
+    # reading R-36: below the FP64 range the symmetric forms take Z_1 = A C and W = C R from their upper
     # triangles -- Z_1 := mirror(upper(A C)), S_ij = 2 W_{min(i,j), max(i,j)}.  Pinned on a non-commuting
     # 2 x 2 whose every intermediate is exact in BF16 (hand values):
     #   A C = [[9/8, 5/8], [7/8, 5/4]] -> Z_1 = [[9/8, 5/8], [5/8, 5/4]], Z_2 = mirror(upper(C Z_1)) =
     #   [[41/64, 15/32], [15/32, 35/64]], R = I - Z_2, W = C R = [[31/256, -91/512], [-67/512, 57/512]]
-    # and, for the full symmetric form / an FP64 phase (no mirroring of Z_1, S = W + W^T):
+    # (the full symmetric form too, below the FP64 range: the same mirrored products), and for an FP64 phase
+    # (no mirroring of Z_1, S = W + W^T):
     #   Z_2 = [[43/64, 15/32], [15/32, 35/64]], W = [[27/256, -91/512], [-69/512, 57/512]]
     A = np.array([[2.0, 1.0], [1.0, 3.0]])
     Ck = np.array([[0.5, 0.125], [0.125, 0.375]])
@@ -317,8 +318,22 @@ def test_tri_form_low_phase_correction_from_upper_triangle():
     Wf = np.array([[27 / 256, -91 / 512], [-69 / 512, 57 / 512]])
     Z2f = np.array([[43 / 64, 15 / 32], [15 / 32, 35 / 64]])
     rs, C1s, _ = oracle.step_sym(A, Ck, 2, ph, tri=False)
-    np.testing.assert_array_equal(C1s, oracle.qm(Ck + (Wf + Wf.T) / 4, 8, 7))
-    assert rs == pytest.approx(np.linalg.norm(np.eye(2) - Z2f), rel=1e-15)
+    np.testing.assert_array_equal(C1s, C1)
+    assert rs == rho
     rf, C1f, _ = oracle.step_sym(A, Ck, 2, oracle.phase(), tri=True)
     np.testing.assert_array_equal(C1f, Ck + (Wf + Wf.T) / 4)
     assert rf == pytest.approx(np.linalg.norm(np.eye(2) - Z2f), rel=1e-15)
+
+
+def test_symmetric_form_p3_low_phase_products_from_upper_triangles():
+    # R-36 for p = 3 (the full symmetric form): below the FP64 range every Z_j and W come from their upper
+    # triangles; on an A that commutes with C (both diagonal in the same basis, here diagonal) the mirrored
+    # and the full products agree exactly, so one BF16 step equals the exact Newton step of Eq. (1) on
+    # exactly representable values (hand values: c' = c + c (1 - c^3 a) / 3 with c^3 a in {1/8, 1, 27/64})
+    a = np.array([1.0, 1.0, 1.0])
+    c = np.array([0.5, 1.0, 0.75])
+    A, Ck = np.diag(a), np.diag(c)
+    rho, C1, _ = oracle.step_sym(A, Ck, 3, oracle.phase(oracle.BF16, mant_bits=23, corr_prec=oracle.TF32))
+    r = 1 - c ** 3 * a
+    np.testing.assert_array_equal(C1, np.diag(oracle.qm(c + c * r / 3, 8, 23)))
+    assert rho == pytest.approx(np.sqrt(np.sum(r ** 2)), rel=1e-15)
