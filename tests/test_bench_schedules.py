@@ -42,3 +42,15 @@ def test_multi_gpu_runs_the_same_schedule():
     assert [ipr.PREC_NAMES[p.prec] for p in ph] == ["fp8", "bf16", "fp64crt"]
     src = open(bench.__file__).read()
     assert "form_note" not in src and "p.prec = ipr.IPR_FP64" not in src
+
+def test_auto_certificate_choice():
+    # IPR_CERT_CRT (R-35) where it applies: a symmetric form with an fp64crt phase, p = 2 at any G or p = 3
+    # on one GPU; the DMMA evaluation (R-30) otherwise; an explicit choice wins
+    import bench
+    assert bench.auto_cert(bench.DEFAULT_SCHEDULE, 2) == "crt"
+    assert bench.auto_cert(bench.DEFAULT_SCHEDULE, 2, world=8) == "crt"
+    assert bench.auto_cert("sym:bf16>fp64crt@a/cbf16", 3) == "crt"
+    assert bench.auto_cert("sym:bf16>fp64crt@a/cbf16", 3, world=2) == "fp64"
+    assert bench.auto_cert("symtri:bf16>fp64/cbf16", 2) == "fp64"        # no CRT phase: no CRT buffers
+    assert bench.auto_cert("bf16>fp64", 2) == "fp64"                      # the literal form
+    assert bench.auto_cert(bench.DEFAULT_SCHEDULE, 2, "fp64") == "fp64"
