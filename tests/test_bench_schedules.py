@@ -1,7 +1,7 @@
 """Host-side pins of bench.py's schedule handling (no GPU): the default schedule string parses into
 the documented phases, low phases of the symmetric forms leave at rho_hat <= 2u of their format
-(switch_tol = 2u sqrt(n), u = 2^-(m+1)), the literal form at rho_hat <= 1e-2, and the N > 1 fallback
-replaces the single-GPU INT8-emulated FP64 phases by the DMMA FP64 phase."""
+(switch_tol = 2u sqrt(n), u = 2^-(m+1)), the literal form at rho_hat <= 1e-2, N > 1 runs the same schedule
+(no fallback since round 2), and the certificate each run uses."""
 import math
 
 import pytest
