@@ -16,6 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="H_twin")
     ap.add_argument("--json", default=None)
+    ap.add_argument("--cert", default="auto", help="certificate: auto (bench's choice), crt, fp64")
     ap.add_argument("schedules", nargs="+")
     a = ap.parse_args()
     import torch
@@ -36,7 +37,7 @@ def main():
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
             h0 = time.perf_counter()
-            s = ipr.Solver(A, p, ph, 1e-12, st, form=form)
+            s = ipr.Solver(A, p, ph, 1e-12, st, form=form, cert=bench.auto_cert(name, p, a.cert))
             torch.cuda.synchronize()
             h1 = time.perf_counter()
             s.iterate(400)
