@@ -70,7 +70,7 @@ def parse_schedule(name):
     form = "literal"
     if ":" in name:
         f, name = name.split(":", 1)
-        form = {"sym": "symmetric", "symtri": "symmetric_tri", "ns": "newton_schulz", "lit": "literal",
+        form = {"sym": "symmetric", "symtri": "symmetric_tri", "symtriz": "symmetric_triz", "ns": "newton_schulz", "lit": "literal",
                 "cpl": "coupled"}[f]
     parts = []
     for ph in name.replace("-", ">").split(">"):
@@ -188,7 +188,7 @@ def oracle_schedule(name, n):
     opr = {"fp64": oracle.FP64, "tf32": oracle.TF32, "bf16": oracle.BF16, "fp16": oracle.FP16, "fp8": oracle.FP8,
            "int8": oracle.INT8, "fp64oz": oracle.FP64_OZ, "fp64crt": oracle.FP64_CRT}
     oform = {"literal": oracle.FORM_LITERAL, "symmetric": oracle.FORM_SYMMETRIC, "symmetric_tri": oracle.FORM_SYMMETRIC_TRI,
-             "newton_schulz": oracle.FORM_NEWTON_SCHULZ, "coupled": oracle.FORM_COUPLED}[form]
+             "symmetric_triz": oracle.FORM_SYMMETRIC_TRIZ, "newton_schulz": oracle.FORM_NEWTON_SCHULZ, "coupled": oracle.FORM_COUPLED}[form]
     out = []
     for i, (prec, corr, m) in enumerate(parts):
         c = opr[corr] if corr != -1 else -1
@@ -358,7 +358,8 @@ def main():
     # correction GEMM + k_sym_update in the symmetric form).  Algorithmic flops of a chain:
     # p * 2 n^3 / G, except the tri form, whose GEMM 2 (C A C) needs only the upper triangle:
     # 2 n^3 + n^2 (n + 1) (its extra work on the diagonal tiles is overhead, not credit).
-    fl_chain = (2.0 * n ** 3 + n * n * (n + 1.0)) if form == "symmetric_tri" else p * fl_gemm
+    fl_chain = (2.0 * n ** 3 + n * n * (n + 1.0)) if form in ("symmetric_tri", "symmetric_triz") else p * fl_gemm
+    fl_ztri = 2.0 * n * n * (n + 1.0)   # R-37: a chain whose Z_1 runs on its upper tiles too (record.ztri)
     last = ipr.PREC_NAMES[phases[-1].prec]
     recs = [t for trc, _ in traces for t in trc if t["phase"] == len(phases) - 1]   # the last phase only
     tot_ms = sum(t["gemm_ms"] - t["upd_ms"] for t in recs)
@@ -392,7 +393,7 @@ def main():
         mods_tot = sum(t["moduli"] for t in recs)
         mods = mods_tot / max(n_chains, 1)
         kern_ms = sum(t["kern_ms"] for t in recs)
-        ops = mods_tot * fl_chain
+        ops = sum(t["moduli"] * (fl_ztri if t.get("ztri") else fl_chain) for t in recs)
         achieved = ops / (kern_ms * 1e-3) / 1e12 if kern_ms > 0 else None
         chain_ach = ops / (tot_ms * 1e-3) / 1e12 if tot_ms > 0 else None
         # peak: the BURST figure -- inside the solve the INT8 GEMMs run in short bursts between other
@@ -406,11 +407,11 @@ def main():
                 "peak_source": pk_src,
                 "frac_of_sustained_peak": achieved / sus[0] if (achieved and sus) else None,
                 "sustained_peak": sus[0] if sus else None,
-                "algorithmic_int8_ops_per_chain_avg": mods * fl_chain, "moduli_per_chain_avg": mods,
-                "chains": n_chains, "kernel_ms_per_chain_avg": kern_ms / max(n_chains, 1),
+                "algorithmic_int8_ops_per_chain_avg": ops / max(n_chains, 1), "moduli_per_chain_avg": mods,
+                "chains": n_chains, "ztri_chains": sum(1 for t in recs if t.get("ztri")), "kernel_ms_per_chain_avg": kern_ms / max(n_chains, 1),
                 "avg_chain_ms": tot_ms / max(n_chains, 1), "chain_achieved_tops": chain_ach,
                 "chain_frac": chain_ach / pk if chain_ach else None,
-                "fp64_equivalent_tflops_chain": chain_ach / mods if chain_ach else None,
+                "fp64_equivalent_tflops_chain": chain_ach / mods if chain_ach else None,   # per the chains' own op counts
                 "gemm_share_of_step": step_gemm_share,
                 "kernel_share_of_step": kern_ms / (ms * args.steps) if ms > 0 else None,
                 "all_gemm_share_of_step": all_ms / (ms * args.steps) if ms > 0 else None}

@@ -151,6 +151,9 @@ typedef struct {
                      /* NaN otherwise                                                         */
   int    moduli;     /* IPR_FP64_CRT: CRT moduli of this record's chain (INT8 GEMMs per FP64   */
                      /* product); 0 otherwise                                                  */
+  int    ztri;       /* IPR_FORM_SYMMETRIC_TRIZ: 1 if this record's chain took Z_1 from its upper  */
+                     /* tiles (reading R-37: 2 n^2 (n + 1) instead of 2 n^3 + n^2 (n + 1) ops per    */
+                     /* modulus); 0 otherwise (fills the padding after moduli: the layout is unchanged) */
   double kern_ms;    /* IPR_FP64_CRT: device time of the chain's kind::i8 modulus GEMM launches  */
                      /* alone (CUDA events; the residue splits and the CRT reconstruction are   */
                      /* the rest of gemm_ms - upd_ms); 0 otherwise                              */
@@ -218,6 +221,13 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
  * S_ij = 2 W_{min(i,j),max(i,j)} (they differ from the full products by commutators at those phases' own
  * rounding level); FP64-range phases keep the full products and W + W^T.
  *
+ * IPR_FORM_SYMMETRIC_TRIZ (reading R-37; p = 2): IPR_FORM_SYMMETRIC_TRI, and in an IPR_FP64_CRT phase
+ * Z_1 = Ahat Chat is taken from its upper tiles too (mirrored; 2/3 of the chain's modulus GEMM work) from the
+ * third chain of the phase on, while every in-phase ratio rho_k / rho_{k-1} so far was <= 0.1.  One slower step
+ * switches the rule off for the rest of the phase (the full Z_1 of IPR_FORM_SYMMETRIC_TRI): on slowly
+ * contracting inputs (kappa >~ 5 in the BASELINE family) the two forms run the same trajectory.  The
+ * certificate (ipr_set_cert) does not depend on how the iterate was produced.
+ *
  * IPR_FORM_COUPLED (any p; FP64 / TF32 / BF16 phases): the M-carrying form
  * of Eq. (1) (reading R-27): with M = X^p A and N = ((p+1) I - M) / p, X_{k+1} = X_k N_k
  * and M_{k+1} = N_k^p M_k -- p + 1 GEMMs per iteration (X Nhat; Nhat Mhat; Nhat qin(T)...).  The last
@@ -226,7 +236,7 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
  * Bounded after convergence for any kappa (it does not remove noise earlier phases left in X);
  * convergence is certified on ||I - X^p A||_F like the symmetric forms. */
 typedef enum { IPR_FORM_LITERAL = 0, IPR_FORM_NEWTON_SCHULZ = 1, IPR_FORM_SYMMETRIC = 2,
-               IPR_FORM_SYMMETRIC_TRI = 3, IPR_FORM_COUPLED = 4 } ipr_form;
+               IPR_FORM_SYMMETRIC_TRI = 3, IPR_FORM_COUPLED = 4, IPR_FORM_SYMMETRIC_TRIZ = 5 } ipr_form;
 ipr_status ipr_set_form(ipr_ctx *c, int form);
 
 /* Convergence certificate of the symmetric and coupled forms, whose in-chain residual is not the

@@ -286,17 +286,19 @@ def step_ns(A, Xk, ph: Phase, want_next: bool = True):
 
 def step_sym(A, Ck, p: int, ph: Phase, want_next: bool = True, tri: bool = False):
     """One symmetrised-correction step (NEXT-2, p >= 2): C + (W + W^T)/(2p), W = qc(C) qc(I - Z_p),
-    Z_p = C^{p-1} A C.  tri: the symmetric-tri form (p = 2; R-36 below the FP64 range).
+    Z_p = C^{p-1} A C.  tri: the symmetric-tri form (p = 2; R-36 below the FP64 range); tri = 2: a chain
+    of FORM_SYMMETRIC_TRIZ whose Z_1 is taken from its upper triangle too (R-37).
     Returns (rho_s(C_k) = ||I - Z_p||_F, C_{k+1}, delta)."""
     A, Ck = _f64(A), _f64(Ck)
     nxt = np.empty_like(Ck) if want_next else None
     d = C.c_double(np.nan)
-    rho = lib().orc_step_sym_form(A.shape[0], p, 1 if tri else 0, _p(A), _p(Ck), C.byref(ph),
+    rho = lib().orc_step_sym_form(A.shape[0], p, int(tri), _p(A), _p(Ck), C.byref(ph),
                                   _p(nxt) if want_next else None, C.byref(d))
     return rho, nxt, d.value
 
 
 FORM_LITERAL, FORM_NEWTON_SCHULZ, FORM_SYMMETRIC, FORM_SYMMETRIC_TRI, FORM_COUPLED = 0, 1, 2, 3, 4
+FORM_SYMMETRIC_TRIZ = 5   # reading R-37: the tri form + Z_1 from its upper triangle in fast FP64_CRT phases
 
 
 def solve(A, p: int, phases, final_tol: float = 1e-12, max_total: int = 200,

@@ -540,6 +540,12 @@ static int corr_of(const orc_phase *ph) {
  * ([A, C], [C, Z_j], [C, R]) that sits at the phase's own rounding level there (C_k is a polynomial in A up to
  * that noise); FP64-range phases keep the full products (the symmetrisation of W + W^T sets R-22's linear
  * rate), except the tri form's Z_2 = C A C (symmetric in exact arithmetic, ORC_FORM_SYMMETRIC_TRI). */
+/* Reading R-37 (ORC_FORM_SYMMETRIC_TRIZ, p = 2): in an FP64_CRT phase the chain's Z_1 = Ahat Chat is ALSO taken from
+ * its upper triangle (tri == 2 below) while the phase contracts fast: from the third chain of the phase on, as long
+ * as every in-phase ratio rho_k / rho_{k-1} so far was <= ORC_ZTRI_RATIO (sticky: one slower step and the phase keeps
+ * the full Z_1 for good -- the mirror feeds the commutator [A, C] back into R, which only pays while the symmetric
+ * update removes it much faster than that).  W + W^T stays full. */
+#define ORC_ZTRI_RATIO 0.1
 static int tri_w_phase(int tri, const orc_phase *ph) {
   (void)tri;
   return ph->prec != ORC_FP64 && ph->prec != ORC_FP64_OZ && ph->prec != ORC_FP64_CRT;
@@ -557,7 +563,7 @@ static double chain_sym(int64_t n, int p, int tri, const double *A, const double
     if (j > 1) chain_gemm(w, n, w->Chat, w->X, w->T);       /* Z_j = Chat qin(Z_{j-1}) */
     if (sigX + w->sigC != 0)
       for (int64_t i = 0; i < nn; ++i) w->T[i] = ldexp(w->T[i], -(sigX + w->sigC));
-    if (j < p && tri_w_phase(tri, ph))                      /* R-36: Z_j from its upper triangle */
+    if (j < p && (tri_w_phase(tri, ph) || tri == 2))        /* R-36 / R-37: Z_j from its upper triangle */
       for (int64_t r = 0; r < n; ++r)
         for (int64_t c = 0; c < r; ++c) w->T[r * n + c] = w->T[c * n + r];
     if (j < p) sigX = qin_matrix(ph->prec, nn, w->T, w->X); /* qin(Z_j)               */
@@ -770,6 +776,8 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
   if (form == ORC_FORM_COUPLED)
     for (int i = 0; i < nphases; ++i)
       if (is_scaled(phases[i].prec)) return -1;
+  const int triz = form == ORC_FORM_SYMMETRIC_TRIZ;
+  if (triz) form = ORC_FORM_SYMMETRIC_TRI;   /* R-37: the tri form + the Z_1 rule below */
   const int sym = form == ORC_FORM_SYMMETRIC || form == ORC_FORM_SYMMETRIC_TRI;
   if (sym) {
     if (p < 2 || (form == ORC_FORM_SYMMETRIC_TRI && p != 2)) return -1;
@@ -807,6 +815,7 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
   int outcome = ORC_CONTINUE;
   /* R-26 state: last residual (any phase), the last two in-phase residuals, the stored m of C */
   double last_rho_hat = NAN, ph_r1 = NAN, ph_r2 = NAN;
+  int z_ok = 1;                       /* R-37: no in-phase ratio above ORC_ZTRI_RATIO so far */
   int m_of_C = is_adaptive(&phases[0]) ? 52 : phase_m(&phases[0]);
   int cert_pending = 0;               /* R-33 */
   for (int k = 0; k < max_total; ++k) {
@@ -845,7 +854,9 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
       anchor = 0;
     } else {
       rho = form == ORC_FORM_NEWTON_SCHULZ ? chain_ns(n, A, C, ph, &w)
-            : sym ? chain_sym(n, p, form == ORC_FORM_SYMMETRIC_TRI, A, C, ph, &w)
+            : sym ? chain_sym(n, p, form == ORC_FORM_SYMMETRIC_TRI
+                                        ? (triz && ph->prec == ORC_FP64_CRT && z_ok && isfinite(ph_r1) && isfinite(ph_r2) ? 2 : 1)
+                                        : 0, A, C, ph, &w)
                   : chain(n, p, A, C, ph, &w);
     }
     const int phase_now = ctl.phase;
@@ -908,8 +919,11 @@ int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase 
     }
     /* R-26 bookkeeping */
     last_rho_hat = rho / sqrt((double)n);
-    if (d == ORC_SWITCH) { ph_r1 = NAN; ph_r2 = NAN; }
-    else { ph_r2 = ph_r1; ph_r1 = rho; }
+    if (d == ORC_SWITCH) { ph_r1 = NAN; ph_r2 = NAN; z_ok = 1; }
+    else {
+      ph_r2 = ph_r1; ph_r1 = rho;
+      if (isfinite(ph_r2) && !(ph_r1 <= ORC_ZTRI_RATIO * ph_r2)) z_ok = 0;
+    }
     /* R-33: certify the next iterate first when the last phase's rate predicts it converged */
     if (d == ORC_CONTINUE && sym && g_predict_cert && ctl.phase == nphases - 1 && isfinite(ph_r1) &&
         isfinite(ph_r2) && ph_r2 > 0.0 && ph_r1 < ph_r2 && ph_r1 * (ph_r1 / ph_r2) <= 0.5 * final_tol)

@@ -126,8 +126,11 @@ int orc_solve(int64_t n, int p, const double *A, const orc_phase *phases, int np
 /* ORC_FORM_COUPLED (NEXT-2 (ii)): X_{k+1} = X_k N_k, M_{k+1} = N_k^p M_k, N = ((p+1)I - M)/p, M
  * re-anchored as X^p A at every phase start; rho = ||I - M_k||_F; convergence certified on
  * ||I - X^p A||_F like the symmetric forms.  No scaled formats. */
+/* ORC_FORM_SYMMETRIC_TRIZ (reading R-37, p = 2): ORC_FORM_SYMMETRIC_TRI, and in an FP64_CRT phase Z_1 = Ahat Chat
+ * is taken from its upper triangle too from the third chain of the phase on, while every in-phase ratio
+ * rho_k / rho_{k-1} so far was <= 0.1 (sticky off).  orc_step_sym_form: tri = 2 is that chain. */
 enum { ORC_FORM_LITERAL = 0, ORC_FORM_NEWTON_SCHULZ = 1, ORC_FORM_SYMMETRIC = 2,
-       ORC_FORM_SYMMETRIC_TRI = 3, ORC_FORM_COUPLED = 4 };
+       ORC_FORM_SYMMETRIC_TRI = 3, ORC_FORM_COUPLED = 4, ORC_FORM_SYMMETRIC_TRIZ = 5 };
 /* Reading R-33: certificate-first iterates in the last phase of the symmetric forms (default on). */
 void orc_set_predict_cert(int on);
 int orc_solve_form(int64_t n, int p, int form, const double *A, const orc_phase *phases,

@@ -39,12 +39,14 @@ EXPORTED = ["ipr_init", "ipr_set_schedule", "ipr_iterate", "ipr_residual", "ipr_
             "ipr_test_set_guards", "ipr_test_check_guards", "ipr_set_output", "ipr_test_crt_signed", "ipr_test_nccl_selftest",
             "ipr_test_cert_info"]
 IPR_FORM_LITERAL, IPR_FORM_NEWTON_SCHULZ, IPR_FORM_SYMMETRIC, IPR_FORM_SYMMETRIC_TRI, IPR_FORM_COUPLED = 0, 1, 2, 3, 4
+IPR_FORM_SYMMETRIC_TRIZ = 5   # reading R-37
 IPR_CERT_FP64, IPR_CERT_PHASE, IPR_CERT_FP64_CHAIN, IPR_CERT_CRT = 0, 1, 2, 3
 CERT_BY_NAME = {"fp64": IPR_CERT_FP64, "dmma": IPR_CERT_FP64, "phase": IPR_CERT_PHASE,
                 "fp64chain": IPR_CERT_FP64_CHAIN, "crt": IPR_CERT_CRT}
 FORM_BY_NAME = {"literal": IPR_FORM_LITERAL, "newton_schulz": IPR_FORM_NEWTON_SCHULZ, "ns": IPR_FORM_NEWTON_SCHULZ,
                 "symmetric": IPR_FORM_SYMMETRIC, "sym": IPR_FORM_SYMMETRIC,
                 "symmetric_tri": IPR_FORM_SYMMETRIC_TRI, "symtri": IPR_FORM_SYMMETRIC_TRI,
+                "symmetric_triz": IPR_FORM_SYMMETRIC_TRIZ, "symtriz": IPR_FORM_SYMMETRIC_TRIZ,
                 "coupled": IPR_FORM_COUPLED}
 
 
@@ -65,7 +67,7 @@ class ipr_record(C.Structure):
                 ("decision", C.c_int), ("rho", C.c_double), ("rho_hat", C.c_double),
                 ("delta", C.c_double), ("gemm_ms", C.c_double), ("upd_ms", C.c_double),
                 ("digits", C.c_int), ("rho_cert", C.c_double), ("moduli", C.c_int),
-                ("kern_ms", C.c_double), ("gap_ms", C.c_double)]
+                ("ztri", C.c_int), ("kern_ms", C.c_double), ("gap_ms", C.c_double)]
 
 
 def _load():
@@ -253,7 +255,7 @@ def ipr_get_trace(ctx):
     _check(_lib.ipr_get_trace(ctx, buf, cnt.value, C.byref(cnt)), ctx)
     return [dict(k=r.k, phase=r.phase, prec=PREC_NAMES[r.prec], mant_bits=r.mant_bits,
                  decision=r.decision, rho=r.rho, rho_hat=r.rho_hat, delta=r.delta, gemm_ms=r.gemm_ms,
-                 upd_ms=r.upd_ms, digits=r.digits, rho_cert=r.rho_cert, moduli=r.moduli, kern_ms=r.kern_ms,
+                 upd_ms=r.upd_ms, digits=r.digits, rho_cert=r.rho_cert, moduli=r.moduli, ztri=r.ztri, kern_ms=r.kern_ms,
                  gap_ms=r.gap_ms)
             for r in buf[:cnt.value]]
 

@@ -139,7 +139,10 @@ struct ipr_ctx {
   // dynamic precision inside an FP64_OZ phase (R-26): digits of this chain, stored bits of the
   // next iterate and of the current one, the last two in-phase residuals
   int oz_S_cur = OZ_S, oz_m_next = 52, m_of_cur = 52, last_chain_S = 0;
+  int last_chain_ztri = 0;              // R-37: the last chain took Z_1 from its upper tiles (record.ztri)
   double ph_r1 = NAN, ph_r2 = NAN;
+  bool triz = false;                    // IPR_FORM_SYMMETRIC_TRIZ (reading R-37): form = SYMMETRIC_TRI + the Z_1 rule
+  bool z_ok = true;                     // R-37: no in-phase ratio rho_k / rho_{k-1} above kZtriRatio so far
   int form = IPR_FORM_LITERAL;          // iteration form (ipr_set_form)
   float *tscr = nullptr;                // FP16 phase T scratch (FP32)
   double *full64 = nullptr;             // FP64 npad x npad scratch (copy-out / certify)
@@ -549,6 +552,14 @@ inline bool is_sym(const ipr_ctx *c) { return c->form == IPR_FORM_SYMMETRIC || c
 // product by a commutator ([A, C], [C, Z_j], [C, R]) at the phase's own rounding level there.  FP64-range
 // phases keep the full products (the symmetrisation of W + W^T sets R-22's linear rate), except the tri
 // form's Z_2.  IPR_TRI_W=0: off (A/B only).
+// Reading R-37 (IPR_FORM_SYMMETRIC_TRIZ, p = 2): in an IPR_FP64_CRT phase Z_1 = Ahat Chat is taken from its upper
+// tiles as well (2/3 of the chain's modulus GEMM work) from the third chain of the phase on, while every in-phase
+// ratio rho_k / rho_{k-1} so far was <= kZtriRatio -- sticky: one slower step and the phase keeps the full Z_1
+// (the mirror feeds the commutator [A, C] back into R; that only pays while the update removes it much faster).
+constexpr double kZtriRatio = 0.1;
+inline bool ztri_chain(const ipr_ctx *c, const PhaseC &P) {
+  return c->triz && P.prec == IPR_FP64_CRT && c->z_ok && std::isfinite(c->ph_r1) && std::isfinite(c->ph_r2);
+}
 int wtri_phase(const ipr_ctx *c, const PhaseC &P) {
   static int on = -1;
   if (on < 0) { const char *v = getenv("IPR_TRI_W"); on = v ? atoi(v) != 0 : 1; }
@@ -583,7 +594,7 @@ ipr_status begin_phase(ipr_ctx *c, bool first) {
   int m_in = P.m;
   if (P.adaptive && !first) m_in = oz_adaptive_m(oz_digits_for(c->last_rho / std::sqrt((double)c->n) * 0.03 * 0.03, c->n));
   c->m_of_cur = m_in;
-  c->ph_r1 = NAN; c->ph_r2 = NAN;
+  c->ph_r1 = NAN; c->ph_r2 = NAN; c->z_ok = true;
   if (first) {
     CK(launch_c0(c->A, c->lda, c->n, c->mr, c->row0, c->col0, c->kp, c->norms[3], P.cont64, m_in, P.rtz,
                  cont_ptr(c, c->cur, P), c->st));
@@ -674,6 +685,7 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
     c->oz_m_next = oz_adaptive_m(c->oz_S_cur);
   }
   c->last_chain_S = is_emu(prec) ? oz_S_now(c) : 0;
+  c->last_chain_ztri = ztri_chain(c, P) ? 1 : 0;
   if (is_sym(c)) {
     // Z_1 = Ahat Chat (A operand: Ahat row-major; B: Chat itself for G = 1 -- exactly symmetric --
     // else the transposed local panel), Z_j = Chat qin(Z_{j-1}); GEMM p: R = I - Z_p in the
@@ -697,12 +709,14 @@ ipr_status chain(ipr_ctx *c, double *rho_out, float *ms) {
         // C (C A), so the phase-product estimate of ||I - C^p A||_F costs p - 1 GEMMs instead of p
         c->zr_for = -1;
         const bool full = P.adaptive ? c->oz_S_cur == OZ_S : P.m == 52;
-        if (c->Zr && c->cert == IPR_CERT_PHASE && is_f64(prec) && full && c->phase == (int)c->ph.size() - 1) {
+        // (not for a chain whose Z_1 comes from its upper tiles only, R-37: the estimate then takes its own Z_1)
+        if (c->Zr && c->cert == IPR_CERT_PHASE && is_f64(prec) && full && c->phase == (int)c->ph.size() - 1 &&
+            !ztri_chain(c, P)) {
           g.mode |= EPI_STORE_N; g.nout = c->Zr; g.ldn = c->npad; c->zr_for = c->cur;
         }
       }
       // R-36: below the FP64 range the symmetric forms compute every Z_j on its upper tiles and mirror them
-      const bool z1tri = j < c->p && wtri_phase(c, P);
+      const bool z1tri = j < c->p && (wtri_phase(c, P) || ztri_chain(c, P));
       if (z1tri) {
         g.tri = 1;
         // tiles below the diagonal are not visited -- their partial maxima must not be stale
@@ -1368,9 +1382,10 @@ ipr_status ipr_set_schedule(ipr_ctx *c, int p, const ipr_phase *phases, int npha
 ipr_status ipr_set_form(ipr_ctx *c, int form) {
   if (!c) return fail(c, IPR_E_INVALID_ARG, "ipr_set_form: null context");
   if (c->started) return fail(c, IPR_E_STATE, "ipr_set_form: iteration already started");
-  if (form < IPR_FORM_LITERAL || form > IPR_FORM_COUPLED)
+  if (form < IPR_FORM_LITERAL || form > IPR_FORM_SYMMETRIC_TRIZ)
     return fail(c, IPR_E_INVALID_ARG, "ipr_set_form: unknown form %d", form);
-  c->form = form;
+  c->triz = form == IPR_FORM_SYMMETRIC_TRIZ;   // R-37: the tri form + the Z_1 rule of ztri_chain()
+  c->form = c->triz ? (int)IPR_FORM_SYMMETRIC_TRI : form;
   return IPR_OK;
 }
 
@@ -1506,6 +1521,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     bool best_new = false;
     const int d = decide(c, rho, &best_new);
     c->ph_r2 = c->ph_r1; c->ph_r1 = rho;   // R-26 in-phase history (reset by begin_phase)
+    if (std::isfinite(c->ph_r2) && !(c->ph_r1 <= kZtriRatio * c->ph_r2)) c->z_ok = false;   // R-37: sticky
     if (best_new) { c->best_loc = c->cur; c->best_cont64 = is_f64(c->ph[c->phase].prec); }
     ipr_record r;
     r.k = (int)c->trace.size(); r.phase = phase_now; r.prec = c->ph[phase_now].prec; r.mant_bits = c->m_of_cur;
@@ -1515,6 +1531,7 @@ ipr_status ipr_iterate(ipr_ctx *c, int max_iters, int *iters_done, ipr_outcome *
     r.gap_ms = NAN;
     r.digits = is_emu(c->ph[phase_now].prec) ? c->last_chain_S : 0;
     r.moduli = c->ph[phase_now].prec == IPR_FP64_CRT ? crt_moduli(crt_bits(c->last_chain_S, c->n), c->n) : 0;
+    r.ztri = c->last_chain_ztri;
     c->trace.push_back(r);
     *iters_done += 1;
     if (d != IPR_DEC_CONTINUE) CKS(chain_timers(c, c->trace.back()));

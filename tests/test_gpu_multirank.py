@@ -86,6 +86,7 @@ CASES = [
     ("symtri_headline", "symtri:fp8/cfp8>bf16>fp64crt@a/cbf16", 2),
     ("symtri_bf16_fp64", "symtri:bf16>tf32>fp64/cbf16", 2),
     ("sym_p3_crt", "sym:bf16>fp64crt/cbf16", 3),
+    ("symtriz_headline", "symtriz:fp8/cfp8>bf16>fp64crt@a/cbf16", 2),   # R-37: Z_1 mirrored across panels too
 ]
 
 
@@ -111,7 +112,7 @@ def test_sharded_bit_identical_to_one_gpu(A, case, world):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("case", [CASES[3], CASES[4]], ids=["sym_fp8_crt", "symtri_headline"])
+@pytest.mark.parametrize("case", [CASES[3], CASES[4], CASES[7]], ids=["sym_fp8_crt", "symtri_headline", "symtriz_headline"])
 def test_sharded_crt_certificate_bit_identical_to_one_gpu(A, case, world):
     # IPR_CERT_CRT (R-35) at G > 1: every rank rounds / splits the gathered candidate, computes the
     # column panel Y[:, S_g] exactly (stored K-major: the rows S_g of the symmetric Y), splits those rows,

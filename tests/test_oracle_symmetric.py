@@ -337,3 +337,71 @@ def test_symmetric_form_p3_low_phase_products_from_upper_triangles():
     r = 1 - c ** 3 * a
     np.testing.assert_array_equal(C1, np.diag(oracle.qm(c + c * r / 3, 8, 23)))
     assert rho == pytest.approx(np.sqrt(np.sum(r ** 2)), rel=1e-15)
+
+
+def test_triz_chain_takes_z1_from_its_upper_triangle_in_an_fp64_crt_phase():
+    # reading R-37 (FORM_SYMMETRIC_TRIZ): a chain of an FP64_CRT phase that the rule selects (tri = 2)
+    # mirrors Z_1 = A C as well; W + W^T stays full.  The non-commuting 2 x 2 of the R-36 pin (every
+    # intermediate a short dyadic, so the CRT products are exact), hand values:
+    #   Z_1 = mirror(upper([[9/8, 5/8], [7/8, 5/4]])) = [[9/8, 5/8], [5/8, 5/4]],
+    #   Z_2 = mirror(upper(C Z_1)) = [[41/64, 15/32], [15/32, 35/64]], W = C (I - Z_2) =
+    #   [[31/256, -91/512], [-67/512, 57/512]], C' = C + (W + W^T) / 4
+    # against the tri form's own FP64-range chain (tri = 1, Z_1 in full): Z_2 = [[43/64, ...]], W = Wf.
+    A = np.array([[2.0, 1.0], [1.0, 3.0]])
+    Ck = np.array([[0.5, 0.125], [0.125, 0.375]])
+    W = np.array([[31 / 256, -91 / 512], [-67 / 512, 57 / 512]])
+    Z2 = np.array([[41 / 64, 15 / 32], [15 / 32, 35 / 64]])
+    ph = oracle.phase(oracle.FP64_CRT)
+    rho, C1, _ = oracle.step_sym(A, Ck, 2, ph, tri=2)
+    np.testing.assert_array_equal(C1, Ck + (W + W.T) / 4)
+    assert rho == pytest.approx(np.linalg.norm(np.eye(2) - Z2), rel=1e-15)
+    Wf = np.array([[27 / 256, -91 / 512], [-69 / 512, 57 / 512]])
+    rf, C1f, _ = oracle.step_sym(A, Ck, 2, ph, tri=1)
+    np.testing.assert_array_equal(C1f, Ck + (Wf + Wf.T) / 4)
+    assert rf != rho
+
+
+def _crt_schedule(n):
+    sw = 2.0 * 2.0 ** -8 * np.sqrt(n)
+    return [oracle.phase(oracle.BF16, switch_tol=sw, plateau_ratio=0.7, plateau_arm=0.5, max_iters=40),
+            oracle.phase(oracle.FP64_CRT, mant_bits=oracle.MANT_ADAPTIVE, corr_prec=oracle.BF16)]
+
+
+def test_triz_rule_selects_chains_by_the_in_phase_contraction():
+    # R-37's rule, replayed from the solve's own iterates: chain k of the FP64_CRT phase takes Z_1 from its upper
+    # triangle iff two in-phase residuals exist and every in-phase ratio so far was <= 0.1.  Each recorded
+    # residual must equal the one-step oracle's for the chain kind the rule gives -- and differ from the other kind
+    n = 96
+    A = synth.spd(n, 2.0, 3)
+    ph = _crt_schedule(n)
+    r = oracle.solve(A, 2, ph, 1e-12, 80, hist=80, form=oracle.FORM_SYMMETRIC_TRIZ, cert="crt")
+    assert r.outcome == oracle.CONVERGED and r.records[-1]["rho_cert"] <= 1e-12
+    rhos, ok, ntri = [], True, 0
+    for rec in r.records:
+        if rec["phase"] != 1 or not np.isfinite(rec["rho"]):
+            continue
+        tri2 = ok and len(rhos) >= 2
+        # the replay runs the chain at S = 9 digits, the solve at R-26's adaptive digits: they agree to the
+        # chain's own error level (~2e-4 relative at the lowest S), the two chain kinds differ by ~2e-2
+        one = oracle.phase(oracle.FP64_CRT, mant_bits=oracle.MANT_ADAPTIVE, corr_prec=oracle.BF16)
+        got = {t: oracle.step_sym(A, r.C_hist[rec["k"]], 2, one, want_next=False, tri=t)[0] for t in (1, 2)}
+        want, other = got[2 if tri2 else 1], got[1 if tri2 else 2]
+        assert abs(rec["rho"] - want) < 0.2 * abs(rec["rho"] - other), (rec["k"], tri2, rec["rho"], want, other)
+        ntri += tri2
+        rhos.append(rec["rho"])
+        if len(rhos) >= 2 and not rhos[-1] <= 0.1 * rhos[-2]:
+            ok = False
+    assert ntri >= 3 and len(rhos) - ntri == 2
+
+
+def test_triz_equals_tri_where_the_phase_contracts_slowly():
+    # kappa = 5: the FP64_CRT phase's first in-phase ratio is above 0.1, the rule switches itself off for good
+    # and the trajectory is the tri form's, record for record
+    n = 96
+    A = synth.spd(n, 5.0, 2)
+    ph = _crt_schedule(n)
+    a = oracle.solve(A, 2, ph, 1e-12, 120, form=oracle.FORM_SYMMETRIC_TRI, cert="crt")
+    b = oracle.solve(A, 2, ph, 1e-12, 120, form=oracle.FORM_SYMMETRIC_TRIZ, cert="crt")
+    assert a.outcome == b.outcome == oracle.CONVERGED
+    assert [x["rho"] for x in a.records if np.isfinite(x["rho"])] == [x["rho"] for x in b.records if np.isfinite(x["rho"])]
+    np.testing.assert_array_equal(a.C_best, b.C_best)
