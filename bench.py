@@ -35,8 +35,8 @@ METRIC = "time-to-FP64-residual 1e-12 (n=8192, p=2)"
 # 3..9 digit-equivalents, i.e. 17..59 bits and 6..17 moduli -- and the stored bits raised per iteration
 # from the residual (R-26); BF16 correction GEMMs; convergence certified on ||I - C^2 A||_F at full FP64
 # accuracy.  (FP8 > BF16 > CRT measured 154.4-155.1 ms vs 157.0-159.0 ms for BF16 > CRT, alternating runs.)
-DEFAULT_SCHEDULE = "symtri:fp8/cfp8>bf16>fp64crt@a/cbf16"
-EXTRA_SCHEDULES = ["fp64", "symtri:fp8>bf16>fp64crt@a/cbf16", "symtri:bf16>fp64crt@a/cbf16", "symtri:bf16>fp64oz@a/cbf16", "symtri:int8>bf16>fp64crt@a/cbf16", "sym:fp64crt", "symtri:bf16>fp64oz@23/cbf16>fp64oz/cbf16", "symtri:bf16>fp64oz/cbf16", "sym:fp64oz", "symtri:fp8>bf16>fp64oz@23/cbf16>fp64oz/cbf16",
+DEFAULT_SCHEDULE = "symtriz:fp8/cfp8>bf16>fp64crt@a/cbf16"   # symtriz: reading R-37 (r02l); symtri: the r02i headline
+EXTRA_SCHEDULES = ["fp64", "symtri:fp8/cfp8>bf16>fp64crt@a/cbf16", "symtri:fp8>bf16>fp64crt@a/cbf16", "symtri:bf16>fp64crt@a/cbf16", "symtri:bf16>fp64oz@a/cbf16", "symtri:int8>bf16>fp64crt@a/cbf16", "sym:fp64crt", "symtri:bf16>fp64oz@23/cbf16>fp64oz/cbf16", "symtri:bf16>fp64oz/cbf16", "sym:fp64oz", "symtri:fp8>bf16>fp64oz@23/cbf16>fp64oz/cbf16",
                    "bf16>fp64", "tf32>fp64", "fp16>fp64", "sym:fp64", "sym:fp64/cbf16", "symtri:fp64/cbf16",
                    "symtri:bf16>fp64/cbf16", "symtri:bf16>tf32>fp64/cbf16", "symtri:fp8>bf16>fp64/cbf16",
                    "symtri:int8>bf16>fp64/cbf16", "symtri:fp16>fp64/cbf16",
@@ -504,6 +504,28 @@ def main():
                 "rho_cert": c2[-1] if c2 else None,
                 "note": "IPR_CERT_FP64: the same schedule certified by the FP64 DMMA evaluation (1.5 DMMA GEMMs)"}
             s.close()
+        # reading R-37 A/B: the tri form without the Z_1 rule (the r02i headline), same phases, same certificate
+        if args.schedule.startswith("symtriz:"):
+            f2, ph = schedule("symtri:" + args.schedule.split(":", 1)[1], n)
+            ts = []
+            for _ in range(3):
+                torch.cuda.synchronize()
+                g0 = torch.cuda.Event(enable_timing=True)
+                g1 = torch.cuda.Event(enable_timing=True)
+                g0.record(stream)
+                s = ipr.Solver(A, p, ph, 1e-12, stream, form=f2, cert=cert)
+                s.iterate(400)
+                t2 = s.trace()
+                s.finalize(C_out)
+                g1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(g0.elapsed_time(g1) / 1e3)
+            c2 = [t["rho_cert"] for t in t2 if t["rho_cert"] == t["rho_cert"]]
+            extras["form_symtri"] = {
+                "time_s": sorted(ts)[1], "outcome": ipr.OUTCOME_NAMES[s.outcome],
+                "iters_per_phase": [sum(1 for t in t2 if t["phase"] == i) for i in range(len(ph))],
+                "rho_cert": c2[-1] if c2 else None,
+                "note": "IPR_FORM_SYMMETRIC_TRI (full Z_1 in the FP64_CRT phase), same phases and certificate; median of 3"}
         # the cost of the honest certificate: the default schedule with the phase-product estimate
         # (IPR_CERT_PHASE: the CRT product, p - 1 products instead of p DMMA GEMMs) -- diagnostics only,
         # its acceptance is not an FP64 certificate (ipr.h ipr_set_cert)

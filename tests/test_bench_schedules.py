@@ -12,7 +12,7 @@ ipr = pytest.importorskip("paper_1703_02283_b200")
 
 def test_default_schedule_phases():
     form, ph = bench.schedule(bench.DEFAULT_SCHEDULE, 8192)
-    assert form == "symmetric_tri"
+    assert form == "symmetric_triz" and ipr.FORM_BY_NAME[form] == ipr.IPR_FORM_SYMMETRIC_TRIZ   # reading R-37
     assert [ipr.PREC_NAMES[p.prec] for p in ph] == ["fp8", "bf16", "fp64crt"]
     assert ph[-1].mant_bits == ipr.IPR_MANT_ADAPTIVE and ph[-1].corr_prec == ipr.IPR_BF16
     assert ph[0].corr_prec == ipr.IPR_FP8 and ph[1].corr_prec == -1     # R-29: FP8 correction in the FP8 phase
@@ -38,7 +38,7 @@ def test_multi_gpu_runs_the_same_schedule():
     # since round 2 the CRT phase, the tri form and the FP8 correction shard: bench.py
     # times the SAME schedule at every N -- no N > 1 substitution rule left in main()
     form, ph = bench.schedule(bench.DEFAULT_SCHEDULE, 8192)
-    assert form == "symmetric_tri"
+    assert form == "symmetric_triz"
     assert [ipr.PREC_NAMES[p.prec] for p in ph] == ["fp8", "bf16", "fp64crt"]
     src = open(bench.__file__).read()
     assert "form_note" not in src and "p.prec = ipr.IPR_FP64" not in src
