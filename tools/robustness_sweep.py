@@ -42,7 +42,7 @@ def main():
                           "iters_per_phase": [sum(1 for t in tr if t["phase"] == i) for i in range(len(ph))],
                           "rho_cert": cert[-1] if cert else None, "recheck": chk, "dmma_eval": dmma,
                           "est": terms["est"] if terms else None, "beta": terms["beta"] if terms else None,
-                          "certificates": len(cert), "cert_first": bool(tr and tr[-1]["rho"] != tr[-1]["rho"]),
+                          "certificates": len(cert), "ztri_chains": sum(t["ztri"] for t in tr), "cert_first": bool(tr and tr[-1]["rho"] != tr[-1]["rho"]),
                           "time_s": e0.elapsed_time(e1) / 1e3}), flush=True)
         del A
         torch.cuda.empty_cache()
